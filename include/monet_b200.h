@@ -1,0 +1,127 @@
+/* monet_b200.h — C ABI of the B200 MONeT execution engine (libmonet_b200.so).
+ *
+ * The reference has exactly one boundary on this path: the executor contract
+ * `simulate(schedule, g, catalog) -> Trace` (pkg/src/remsched/schedule.py:320)
+ * whose per-step `record()` (schedule.py:338-342) stands for "run this
+ * operator variant".  Every entry point below is one such operator variant,
+ * the arena planner the ledger's alloc/free events drive, or the profiler
+ * that fills the catalog (`Catalog`, costmodel.py:30-73; workspace bytes and
+ * costs per variant, costmodel.py:85-181).  The Python executor
+ * (paper_2010_14501_b200/engine.py) binds these with ctypes; INTEGRATION.md
+ * shows the binding a remsched maintainer would add.
+ *
+ * Conventions: plain pointers to device memory (fp32 NHWC activations, KRSC
+ * conv weights), sizes in elements unless named *_bytes, `stream` is a
+ * cudaStream_t passed as void*.  Return 0 on success, a negative
+ * -cudaError_t on failure; no C++ exception crosses this boundary.  Kernels
+ * never allocate: workspace and scratch come from the caller (the budgeted
+ * arena), sized by the *_ws_bytes / *_scratch_bytes queries.
+ * `accumulate` selects dx = f(dy) (0, first consumer allocates the gradient,
+ * schedule.py:445-449) or dx += f(dy) (1, later consumers).
+ */
+#ifndef MONET_B200_H
+#define MONET_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Convolution geometry, NHWC input [n,h,w,c], KRSC weight [k,r,s,c],
+ * NHWC output [n,p,q,k].  c and k must be multiples of 4. */
+typedef struct {
+  int n, h, w, c, k, r, s, p, q, stride_h, stride_w, pad_h, pad_w;
+} monet_conv_desc;
+
+/* conv variants (catalog ForwardVariant / BackwardVariant names):
+ *   MONET_CONV_IMPLICIT  "implicit"  tcgen05 3xTF32 implicit GEMM, im2col in registers
+ *   MONET_CONV_SPLITK    "splitk"    as implicit, plus split-K over the reduction with
+ *                                    fp32 partials in workspace (honest ws/speed trade)
+ *   MONET_CONV_TF32      "tf32"      single-pass TF32 (faster, ~1e-3 relative error) */
+enum { MONET_CONV_IMPLICIT = 0, MONET_CONV_SPLITK = 1, MONET_CONV_TF32 = 2 };
+enum { MONET_PASS_FWD = 0, MONET_PASS_DGRAD = 1, MONET_PASS_WGRAD = 2, MONET_PASS_BWD = 3 };
+
+/* --- library --------------------------------------------------------------- */
+const char* monet_version(void);
+int monet_device_check(void); /* 0 if the current device is sm_100 */
+
+/* --- convolution (K1-K3; replaces conv entries of Catalog, costmodel.py:30-44) */
+size_t monet_conv_ws_bytes(int variant, int pass, const monet_conv_desc* d);
+int monet_conv_fwd(int variant, const monet_conv_desc* d, const float* x, const float* w, float* y, void* ws,
+                   size_t ws_bytes, void* stream);
+int monet_conv_dgrad(int variant, const monet_conv_desc* d, const float* dy, const float* w, float* dx,
+                     int accumulate, void* ws, size_t ws_bytes, void* stream);
+int monet_conv_wgrad(int variant, const monet_conv_desc* d, const float* x, const float* dy, float* dw,
+                     int accumulate, void* ws, size_t ws_bytes, void* stream);
+
+/* --- dense layer (fc) -------------------------------------------------------- */
+size_t monet_linear_ws_bytes(int variant, int pass, int n, int in_f, int out_f);
+int monet_linear_fwd(int variant, const float* x, const float* w, const float* b, float* y, int n, int in_f,
+                     int out_f, void* ws, size_t ws_bytes, void* stream);
+int monet_linear_bwd(int variant, const float* x, const float* w, const float* dy, float* dx, int dx_accumulate,
+                     float* dw, float* db, int n, int in_f, int out_f, void* ws, size_t ws_bytes, void* stream);
+
+/* --- ReLU with packed sign bitmask (K4/K5) -------------------------------------
+ * mask: ceil(n/32) uint32 words, bit b of word w <-> element 32w+b; nullable. */
+int monet_relu_fwd(const float* x, float* y, uint32_t* mask, int64_t n, void* stream);
+int monet_relu_bwd_mask(const uint32_t* mask, const float* dy, float* dx, int64_t n, int accumulate, void* stream);
+int monet_relu_bwd_out(const float* y, const float* dy, float* dx, int64_t n, int accumulate, void* stream);
+int monet_relu_bwd_in(const float* x, const float* dy, float* dx, int64_t n, int accumulate, void* stream);
+
+/* --- BatchNorm, training mode, [rows = n*h*w, c] (K6-K8) ----------------------
+ * scratch: monet_bn_scratch_bytes(rows, c) bytes of caller memory. */
+size_t monet_bn_scratch_bytes(int64_t rows, int c);
+int monet_bn_fwd_train(const float* x, float* y, const float* gamma, const float* beta, float* saved_mean,
+                       float* saved_invstd, float* running_mean, float* running_var, int64_t rows, int c, float eps,
+                       float momentum, int update_running, void* scratch, void* stream);
+/* recompute: reuses saved statistics, never touches running stats */
+int monet_bn_fwd_replay(const float* x, float* y, const float* gamma, const float* beta, const float* saved_mean,
+                        const float* saved_invstd, int64_t rows, int c, void* stream);
+int monet_bn_bwd_in(const float* x, const float* dy, float* dx, int accumulate, const float* gamma,
+                    const float* saved_mean, const float* saved_invstd, float* dgamma, float* dbeta, int64_t rows,
+                    int c, void* scratch, void* stream);
+/* output-activated: xhat = (y - beta) / gamma, |gamma| clamped to >= 1e-12 */
+int monet_bn_bwd_out(const float* y, const float* dy, float* dx, int accumulate, const float* gamma,
+                     const float* beta, const float* saved_invstd, float* dgamma, float* dbeta, int64_t rows, int c,
+                     void* scratch, void* stream);
+
+/* --- residual add / gradient pass-through (K12) --------------------------- */
+int monet_add_fwd(const float* a, const float* b, float* y, int64_t n, void* stream);
+int monet_grad_pass(const float* dy, float* dx, int64_t n, float scale, int accumulate, void* stream);
+
+/* --- pooling (K11, K13) ----------------------------------------------------- */
+int monet_maxpool_fwd(const monet_conv_desc* d, const float* x, float* y, uint8_t* idx8, void* stream);
+int monet_maxpool_bwd(const monet_conv_desc* d, const uint8_t* idx8, const float* x, const float* dy, float* dx,
+                      int accumulate, void* stream);
+int monet_avgpool_fwd(const float* x, float* y, int n, int hw, int c, void* stream);
+int monet_avgpool_bwd(const float* dy, float* dx, int n, int hw, int c, int accumulate, void* stream);
+
+/* --- loss and optimizer (K13) ----------------------------------------------- */
+size_t monet_xent_scratch_bytes(int n);
+int monet_xent_fwd(const float* logits, const int32_t* labels, float* loss, int n, int classes, void* scratch,
+                   void* stream);
+int monet_xent_bwd(const float* logits, const int32_t* labels, const float* dloss, float* dlogits, int n,
+                   int classes, int accumulate, void* stream);
+int monet_sgd_step(float* w, const float* g, float* momentum_buf, int64_t n, float lr, float momentum,
+                   float weight_decay, float grad_scale, int first_step, void* stream);
+
+/* --- generic tcgen05 GEMM (test / profiler access) ---------------------------
+ * C[m,n] (=|+=) sum_k A[m,k] B[n,k]; a_mn/b_mn select MN-major operands. */
+int monet_gemm(int variant, const float* a, int a_mn, int64_t lda, const float* b, int b_mn, int64_t ldb, float* c,
+               int64_t ldc, int m, int n, int k, int accumulate, void* ws, size_t ws_bytes, void* stream);
+size_t monet_gemm_ws_bytes(int variant, int m, int n, int k);
+
+/* --- budget-capped arena: static offset planning (R2) -------------------------
+ * Blocks i = 0..count-1 live over ledger events [t_alloc[i], t_free[i]).
+ * Writes offsets (aligned to `align`) so that no two simultaneously live
+ * blocks overlap and returns the arena high-water mark in *peak_bytes.
+ * Returns -12 (ENOMEM) when the plan exceeds capacity_bytes (0 = no cap). */
+int monet_arena_plan(int64_t count, const int64_t* sizes, const int64_t* t_alloc, const int64_t* t_free,
+                     int64_t align, int64_t capacity_bytes, int64_t* offsets, int64_t* peak_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MONET_B200_H */

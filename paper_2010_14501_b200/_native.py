@@ -1,0 +1,111 @@
+"""ctypes binding of libmonet_b200.so (the C ABI in include/monet_b200.h).
+
+The library is built in-tree (``build.py``).  There is no fallback: if the
+shared object is missing or the device is not sm_100, every entry point raises
+so a GPU run can never silently execute anything but the CUDA kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libmonet_b200.so"
+
+_vp, _i32, _i64, _f32, _sz = C.c_void_p, C.c_int, C.c_int64, C.c_float, C.c_size_t
+
+
+class ConvDesc(C.Structure):
+    _fields_ = [(name, C.c_int) for name in
+                ("n", "h", "w", "c", "k", "r", "s", "p", "q", "stride_h", "stride_w", "pad_h", "pad_w")]
+
+
+_PCONV = C.POINTER(ConvDesc)
+
+# name -> (restype, argtypes)
+SIGNATURES = {
+    "monet_version": (C.c_char_p, []),
+    "monet_device_check": (_i32, []),
+    "monet_conv_ws_bytes": (_sz, [_i32, _i32, _PCONV]),
+    "monet_conv_fwd": (_i32, [_i32, _PCONV, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "monet_conv_dgrad": (_i32, [_i32, _PCONV, _vp, _vp, _vp, _i32, _vp, _sz, _vp]),
+    "monet_conv_wgrad": (_i32, [_i32, _PCONV, _vp, _vp, _vp, _i32, _vp, _sz, _vp]),
+    "monet_linear_ws_bytes": (_sz, [_i32, _i32, _i32, _i32, _i32]),
+    "monet_linear_fwd": (_i32, [_i32, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _sz, _vp]),
+    "monet_linear_bwd": (_i32, [_i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _i32, _i32, _i32, _vp, _sz, _vp]),
+    "monet_relu_fwd": (_i32, [_vp, _vp, _vp, _i64, _vp]),
+    "monet_relu_bwd_mask": (_i32, [_vp, _vp, _vp, _i64, _i32, _vp]),
+    "monet_relu_bwd_out": (_i32, [_vp, _vp, _vp, _i64, _i32, _vp]),
+    "monet_relu_bwd_in": (_i32, [_vp, _vp, _vp, _i64, _i32, _vp]),
+    "monet_bn_scratch_bytes": (_sz, [_i64, _i32]),
+    "monet_bn_fwd_train": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _f32, _f32, _i32, _vp,
+                                  _vp]),
+    "monet_bn_fwd_replay": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp]),
+    "monet_bn_bwd_in": (_i32, [_vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp]),
+    "monet_bn_bwd_out": (_i32, [_vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp]),
+    "monet_add_fwd": (_i32, [_vp, _vp, _vp, _i64, _vp]),
+    "monet_grad_pass": (_i32, [_vp, _vp, _i64, _f32, _i32, _vp]),
+    "monet_maxpool_fwd": (_i32, [_PCONV, _vp, _vp, _vp, _vp]),
+    "monet_maxpool_bwd": (_i32, [_PCONV, _vp, _vp, _vp, _vp, _i32, _vp]),
+    "monet_avgpool_fwd": (_i32, [_vp, _vp, _i32, _i32, _i32, _vp]),
+    "monet_avgpool_bwd": (_i32, [_vp, _vp, _i32, _i32, _i32, _i32, _vp]),
+    "monet_xent_scratch_bytes": (_sz, [_i32]),
+    "monet_xent_fwd": (_i32, [_vp, _vp, _vp, _i32, _i32, _vp, _vp]),
+    "monet_xent_bwd": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp]),
+    "monet_sgd_step": (_i32, [_vp, _vp, _vp, _i64, _f32, _f32, _f32, _f32, _i32, _vp]),
+    "monet_gemm": (_i32, [_i32, _vp, _i32, _i64, _vp, _i32, _i64, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _sz,
+                          _vp]),
+    "monet_gemm_ws_bytes": (_sz, [_i32, _i32, _i32, _i32]),
+    "monet_arena_plan": (_i32, [_i64, _vp, _vp, _vp, _i64, _i64, _vp, _vp]),
+}
+
+CONV_VARIANTS = {"implicit": 0, "splitk": 1, "tf32": 2}
+PASS = {"fwd": 0, "dgrad": 1, "wgrad": 2, "bwd": 3}
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+class _Lib:
+    def __init__(self, path: Path):
+        if not path.exists():
+            raise NativeError(f"{path.name} is not built; run `python -m paper_2010_14501_b200.build` "
+                              f"(there is no CPU fallback)")
+        self.path = path
+        self.dll = C.CDLL(str(path))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(self.dll, name)
+            fn.restype = res
+            fn.argtypes = args
+
+    def __getattr__(self, name):
+        fn = getattr(self.dll, "monet_" + name)
+
+        def call(*args):
+            rc = fn(*args)
+            if fn.restype is _i32 and rc != 0:
+                raise NativeError(f"monet_{name} failed with code {rc}")
+            return rc
+        return call
+
+
+_LIB: _Lib | None = None
+
+
+def lib() -> _Lib:
+    global _LIB
+    if _LIB is None:
+        _LIB = _Lib(LIB_PATH)
+    return _LIB
+
+
+def conv_desc(n, h, w, c, k, r, s, stride=1, pad=0) -> ConvDesc:
+    p = (h + 2 * pad - r) // stride + 1
+    q = (w + 2 * pad - s) // stride + 1
+    return ConvDesc(n, h, w, c, k, r, s, p, q, stride, stride, pad, pad)
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a torch tensor (None -> NULL)."""
+    return None if t is None else t.data_ptr()

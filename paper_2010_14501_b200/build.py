@@ -1,0 +1,76 @@
+"""Build libmonet_b200.so in-tree with nvcc for sm_100a.
+
+    python -m paper_2010_14501_b200.build [--force]
+
+The shared library is the C-ABI of include/monet_b200.h; it is loaded with
+ctypes (``_native.py``), so no torch headers are involved and the same .so
+serves the Python executor, the tests and a foreign (cgo/JNI/ctypes) host.
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+CSRC = PKG / "csrc"
+INCLUDE = PKG.parent / "include"
+LIB = PKG / "libmonet_b200.so"
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+CU_SOURCES = ["capi.cu"]
+CPP_SOURCES = ["arena.cpp"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _sources():
+    files = [CSRC / f for f in CU_SOURCES + CPP_SOURCES]
+    files += list(CSRC.glob("*.cuh")) + [INCLUDE / "monet_b200.h"]
+    return files
+
+
+def needs_build() -> bool:
+    if not LIB.exists():
+        return True
+    t = LIB.stat().st_mtime
+    return any(f.stat().st_mtime > t for f in _sources())
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    if not force and not needs_build():
+        return LIB
+    out_dir = PKG / "build"
+    out_dir.mkdir(exist_ok=True)
+    objs = []
+    common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", str(INCLUDE)]
+    for src in CU_SOURCES:
+        obj = out_dir / (src + ".o")
+        cmd = [NVCC, *ARCH, "-lineinfo", *common, "--expt-relaxed-constexpr", "-Xptxas", "-v",
+               "-c", str(CSRC / src), "-o", str(obj)]
+        _run(cmd, verbose)
+        objs.append(obj)
+    for src in CPP_SOURCES:
+        obj = out_dir / (src + ".o")
+        _run(["g++", "-O2", "-std=c++17", "-fPIC", "-I", str(INCLUDE), "-c", str(CSRC / src),
+              "-o", str(obj)], verbose)
+        objs.append(obj)
+    tmp = LIB.with_suffix(".so.tmp")
+    _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart"], verbose)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+def _run(cmd, verbose):
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if verbose or res.returncode:
+        sys.stderr.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+    if res.returncode:
+        raise RuntimeError(f"build step failed: {cmd[0]} (exit {res.returncode})")
+    (PKG / "build" / "ptxas.log").open("a").write(res.stderr)
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(LIB)

@@ -1,0 +1,51 @@
+"""Analytic roofline costs (ns) for catalog variants before the profiler has run.
+
+The on-device profiler (profiler.py) replaces these with measured integer
+nanoseconds; the analytic numbers keep the ILP well-posed on a CPU-only host
+and are the "expected" side of the estimate-vs-measurement check
+(B200_PROFILING.md: write the expected numbers down before measuring).
+Units: integer nanoseconds, exact ints as units.py requires.
+"""
+
+from __future__ import annotations
+
+TC_FLOPS = 250e12      # sustained 3xTF32 conv throughput assumed before profiling
+HBM_BPS = 6.0e12       # sustained HBM bandwidth for local ops
+LAUNCH_NS = 4000       # per-kernel fixed cost
+
+
+def _ns(flops=0.0, nbytes=0.0, launches=1) -> int:
+    return max(1, int(max(flops / TC_FLOPS, nbytes / HBM_BPS) * 1e9 + launches * LAUNCH_NS))
+
+
+def analytic_cost(net, op, pass_, name) -> int:
+    n = op.numel
+    if op.kind == "conv":
+        x = net.op(op.deps[0])
+        flops = 2.0 * n * x.shape[3] * op.attrs["r"] * op.attrs["s"]
+        if pass_ == "fwd":
+            return _ns(flops, 4.0 * (x.numel + n))
+        passes = 1 if net.op(op.deps[0]).kind == "input" else 2
+        return _ns(passes * flops, 8.0 * (x.numel + n), launches=3)
+    if op.kind == "fc":
+        fi = net.op(op.deps[0]).shape[1]
+        flops = 2.0 * n * fi
+        return _ns(flops if pass_ == "fwd" else 2 * flops, launches=2 if pass_ == "fwd" else 4)
+    if op.kind == "relu":
+        if pass_ == "fwd":
+            return _ns(nbytes=8.125 * n)
+        return _ns(nbytes=(8.125 if name == "bwd-mask" else 12.0) * n)
+    if op.kind == "bn":
+        return _ns(nbytes=(12.0 if pass_ == "fwd" else 20.0) * n, launches=3)
+    if op.kind == "add":
+        return _ns(nbytes=(12.0 if pass_ == "fwd" else 16.0) * n, launches=1 if pass_ == "fwd" else 2)
+    if op.kind == "maxpool":
+        x = net.op(op.deps[0])
+        return _ns(nbytes=4.0 * x.numel * (2.25 if pass_ == "fwd" else 2.0) + 5.0 * n)
+    if op.kind == "avgpool":
+        return _ns(nbytes=4.0 * net.op(op.deps[0]).numel)
+    if op.kind == "input":
+        return _ns(nbytes=8.0 * n) if pass_ == "fwd" else 1
+    if op.kind == "xent":
+        return _ns(nbytes=8.0 * net.op(op.deps[0]).numel, launches=2)
+    raise ValueError(op.kind)

@@ -1,0 +1,387 @@
+// extern "C" boundary of libmonet_b200.so (declared in include/monet_b200.h).
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/monet_b200.h"
+#include "gemm_tc.cuh"
+#include "local_ops.cuh"
+
+using namespace monet;
+
+namespace {
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int last_error() {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : -static_cast<int>(e);
+}
+
+inline int ew_blocks(long long work_items) {
+  long long b = (work_items + kEwThreads - 1) / kEwThreads;
+  return (int)std::max(1LL, std::min(b, (long long)kNumSMs * 8));
+}
+
+// ----------------------------------------------------------------- GEMM setup
+int choose_splits(int variant, int M, int N, int Kd) {
+  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int kblocks = (Kd + BK - 1) / BK;
+  if (variant != MONET_CONV_SPLITK) return 1;
+  if (tiles >= kNumSMs) return 1;
+  int want = (2 * kNumSMs + tiles - 1) / tiles;
+  int cap = std::max(1, kblocks / 4);
+  return std::max(1, std::min(want, cap));
+}
+
+size_t gemm_ws(int variant, int M, int N, int Kd) {
+  int s = choose_splits(variant, M, N, Kd);
+  return s > 1 ? (size_t)s * M * N * sizeof(float) : 0;
+}
+
+bool g_attr_set = false;
+
+int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (p.M <= 0 || p.N <= 0) return 0;
+  p.split_tf32 = variant == MONET_CONV_TF32 ? 0 : 1;
+  p.m_tiles = (p.M + BM - 1) / BM;
+  p.n_tiles = (p.N + BN - 1) / BN;
+  const int kblocks = std::max(1, (p.Kd + BK - 1) / BK);
+  int splits = choose_splits(variant, p.M, p.N, p.Kd);
+  size_t need = splits > 1 ? (size_t)splits * p.M * p.N * sizeof(float) : 0;
+  if (need > ws_bytes || (need && ws == nullptr)) {
+    splits = 1;  // never write outside the caller's workspace
+    need = 0;
+  }
+  p.kb_per_split = (kblocks + splits - 1) / splits;
+  p.splits = (kblocks + p.kb_per_split - 1) / p.kb_per_split;
+  p.ws = static_cast<float*>(ws);
+  p.epi = p.splits > 1 ? EPI_PARTIAL : (accumulate ? EPI_ACCUM : EPI_STORE);
+  if (!g_attr_set) {
+    cudaFuncSetAttribute(gemm_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    g_attr_set = true;
+  }
+  const int tiles = p.m_tiles * p.n_tiles * p.splits;
+  const int grid = std::min(tiles, kNumSMs);
+  gemm_tf32_kernel<<<grid, kThreads, kSmemBytes, st>>>(p);
+  if (p.splits > 1) {
+    long long total = (long long)p.M * p.N;
+    splitk_reduce_kernel<<<ew_blocks(total), kEwThreads, 0, st>>>(p.ws, p.c, p.M, p.N, p.ldc, p.splits, accumulate);
+  }
+  return last_error();
+}
+
+Operand op_kmajor(const float* ptr, int rows, long long ld) {
+  return Operand{OP_KMAJOR, rows, ptr, ld, 1 << 30, 0};
+}
+Operand op_mnmajor(const float* ptr, int rows, long long ld) {
+  return Operand{OP_MNMAJOR, rows, ptr, ld, 1 << 30, 0};
+}
+
+ConvGeom geom(const monet_conv_desc* d) {
+  return ConvGeom{d->n, d->h, d->w, d->c, d->k, d->r, d->s, d->p, d->q, d->stride_h, d->stride_w, d->pad_h, d->pad_w};
+}
+
+bool is_pointwise(const monet_conv_desc* d) {
+  return d->r == 1 && d->s == 1 && d->stride_h == 1 && d->stride_w == 1 && d->pad_h == 0 && d->pad_w == 0;
+}
+
+GemmParams conv_params(int pass, const monet_conv_desc* d, const float* in0, const float* in1, float* out) {
+  GemmParams p{};
+  p.g = geom(d);
+  const int rsc = d->r * d->s * d->c;
+  if (pass == MONET_PASS_FWD) {  // in0 = x, in1 = w
+    p.M = d->n * d->p * d->q;
+    p.N = d->k;
+    p.Kd = rsc;
+    p.a = is_pointwise(d) ? op_kmajor(in0, p.M, d->c) : Operand{OP_IM2COL_FPROP, p.M, in0, 0, 1 << 30, 0};
+    p.b = op_kmajor(in1, d->k, rsc);
+    p.c = out;
+    p.ldc = d->k;
+  } else if (pass == MONET_PASS_DGRAD) {  // in0 = dy, in1 = w
+    p.M = d->n * d->h * d->w;
+    p.N = d->c;
+    p.Kd = d->r * d->s * d->k;
+    p.a = is_pointwise(d) ? op_kmajor(in0, p.M, d->k) : Operand{OP_IM2COL_DGRAD, p.M, in0, 0, 1 << 30, 0};
+    // B[c, (tap, kout)] = w[kout, tap, c]
+    p.b = Operand{OP_MNMAJOR, d->c, in1, (long long)rsc, d->k, (long long)d->c};
+    p.c = out;
+    p.ldc = d->c;
+  } else {  // wgrad: in0 = x, in1 = dy
+    p.M = d->k;
+    p.N = rsc;
+    p.Kd = d->n * d->p * d->q;
+    p.a = op_mnmajor(in1, d->k, d->k);  // A[kout, pix] = dy[pix, kout]
+    p.b = is_pointwise(d) ? op_mnmajor(in0, d->c, d->c) : Operand{OP_IM2COL_WGRAD, rsc, in0, 0, 1 << 30, 0};
+    p.c = out;
+    p.ldc = rsc;
+  }
+  return p;
+}
+
+int check_desc(const monet_conv_desc* d) {
+  if (!d || d->c % 4 || d->k % 4 || d->n <= 0) return -(int)cudaErrorInvalidValue;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* monet_version(void) { return "monet_b200 0.1.0 sm_100a"; }
+
+int monet_device_check(void) {
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return (major == 10 && minor == 0) ? 0 : -2;
+}
+
+// ------------------------------------------------------------------- conv
+size_t monet_conv_ws_bytes(int variant, int pass, const monet_conv_desc* d) {
+  if (check_desc(d)) return 0;
+  if (pass == MONET_PASS_BWD)
+    return std::max(monet_conv_ws_bytes(variant, MONET_PASS_DGRAD, d), monet_conv_ws_bytes(variant, MONET_PASS_WGRAD, d));
+  GemmParams p = conv_params(pass, d, nullptr, nullptr, nullptr);
+  return gemm_ws(variant, p.M, p.N, p.Kd);
+}
+
+int monet_conv_fwd(int variant, const monet_conv_desc* d, const float* x, const float* w, float* y, void* ws,
+                   size_t ws_bytes, void* stream) {
+  if (int e = check_desc(d)) return e;
+  return launch_gemm(conv_params(MONET_PASS_FWD, d, x, w, y), variant, 0, ws, ws_bytes, S(stream));
+}
+
+int monet_conv_dgrad(int variant, const monet_conv_desc* d, const float* dy, const float* w, float* dx,
+                     int accumulate, void* ws, size_t ws_bytes, void* stream) {
+  if (int e = check_desc(d)) return e;
+  return launch_gemm(conv_params(MONET_PASS_DGRAD, d, dy, w, dx), variant, accumulate, ws, ws_bytes, S(stream));
+}
+
+int monet_conv_wgrad(int variant, const monet_conv_desc* d, const float* x, const float* dy, float* dw,
+                     int accumulate, void* ws, size_t ws_bytes, void* stream) {
+  if (int e = check_desc(d)) return e;
+  return launch_gemm(conv_params(MONET_PASS_WGRAD, d, x, dy, dw), variant, accumulate, ws, ws_bytes, S(stream));
+}
+
+// ------------------------------------------------------------------- linear
+size_t monet_linear_ws_bytes(int variant, int pass, int n, int in_f, int out_f) {
+  if (pass == MONET_PASS_FWD) return gemm_ws(variant, n, out_f, in_f);
+  return std::max(gemm_ws(variant, n, in_f, out_f), gemm_ws(variant, out_f, in_f, n));
+}
+
+int monet_linear_fwd(int variant, const float* x, const float* w, const float* b, float* y, int n, int in_f,
+                     int out_f, void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t st = S(stream);
+  long long tot = (long long)n * out_f;
+  bias_fill_kernel<<<(int)((tot + 255) / 256), 256, 0, st>>>(y, b, n, out_f);
+  GemmParams p{};
+  p.M = n;
+  p.N = out_f;
+  p.Kd = in_f;
+  p.a = op_kmajor(x, n, in_f);
+  p.b = op_kmajor(w, out_f, in_f);
+  p.c = y;
+  p.ldc = out_f;
+  return launch_gemm(p, variant, 1, ws, ws_bytes, st);
+}
+
+int monet_linear_bwd(int variant, const float* x, const float* w, const float* dy, float* dx, int dx_accumulate,
+                     float* dw, float* db, int n, int in_f, int out_f, void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t st = S(stream);
+  if (dx) {
+    GemmParams p{};
+    p.M = n;
+    p.N = in_f;
+    p.Kd = out_f;
+    p.a = op_kmajor(dy, n, out_f);
+    p.b = op_mnmajor(w, in_f, in_f);  // B[i, o] = W[o, i]
+    p.c = dx;
+    p.ldc = in_f;
+    if (int e = launch_gemm(p, variant, dx_accumulate, ws, ws_bytes, st)) return e;
+  }
+  GemmParams q{};
+  q.M = out_f;
+  q.N = in_f;
+  q.Kd = n;
+  q.a = op_mnmajor(dy, out_f, out_f);  // A[o, n] = dy[n, o]
+  q.b = op_mnmajor(x, in_f, in_f);     // B[i, n] = x[n, i]
+  q.c = dw;
+  q.ldc = in_f;
+  if (int e = launch_gemm(q, variant, 0, ws, ws_bytes, st)) return e;
+  col_sum_kernel<<<(out_f + 255) / 256, 256, 0, st>>>(dy, db, n, out_f);
+  return last_error();
+}
+
+// ------------------------------------------------------------------- generic GEMM
+size_t monet_gemm_ws_bytes(int variant, int m, int n, int k) { return gemm_ws(variant, m, n, k); }
+
+int monet_gemm(int variant, const float* a, int a_mn, int64_t lda, const float* b, int b_mn, int64_t ldb, float* c,
+               int64_t ldc, int m, int n, int k, int accumulate, void* ws, size_t ws_bytes, void* stream) {
+  GemmParams p{};
+  p.M = m;
+  p.N = n;
+  p.Kd = k;
+  p.a = a_mn ? op_mnmajor(a, m, lda) : op_kmajor(a, m, lda);
+  p.b = b_mn ? op_mnmajor(b, n, ldb) : op_kmajor(b, n, ldb);
+  p.c = c;
+  p.ldc = ldc;
+  return launch_gemm(p, variant, accumulate, ws, ws_bytes, S(stream));
+}
+
+// ------------------------------------------------------------------- ReLU
+int monet_relu_fwd(const float* x, float* y, uint32_t* mask, int64_t n, void* stream) {
+  relu_fwd_kernel<<<ew_blocks((n + 7) / 8), kEwThreads, 0, S(stream)>>>(x, y, mask, n);
+  return last_error();
+}
+int monet_relu_bwd_mask(const uint32_t* mask, const float* dy, float* dx, int64_t n, int accumulate, void* stream) {
+  relu_bwd_mask_kernel<<<ew_blocks((n + 7) / 8), kEwThreads, 0, S(stream)>>>(mask, dy, dx, n, accumulate);
+  return last_error();
+}
+int monet_relu_bwd_out(const float* y, const float* dy, float* dx, int64_t n, int accumulate, void* stream) {
+  relu_bwd_sign_kernel<<<ew_blocks(n / 4 + 1), kEwThreads, 0, S(stream)>>>(y, dy, dx, n, accumulate);
+  return last_error();
+}
+int monet_relu_bwd_in(const float* x, const float* dy, float* dx, int64_t n, int accumulate, void* stream) {
+  return monet_relu_bwd_out(x, dy, dx, n, accumulate, stream);
+}
+
+// ------------------------------------------------------------------- BatchNorm
+static int bn_blocks(int64_t rows) {
+  long long b = (rows + 255) / 256;
+  return (int)std::max(1LL, std::min(b, (long long)kNumSMs * 4));
+}
+
+size_t monet_bn_scratch_bytes(int64_t rows, int c) {
+  // partials [blocks][2][c] + sum_dy[c] + sum_dyxhat[c] + inv_gamma[c]
+  return ((size_t)bn_blocks(rows) * 2 * c + 3 * (size_t)c) * sizeof(float);
+}
+
+int monet_bn_fwd_train(const float* x, float* y, const float* gamma, const float* beta, float* saved_mean,
+                       float* saved_invstd, float* running_mean, float* running_var, int64_t rows, int c, float eps,
+                       float momentum, int update_running, void* scratch, void* stream) {
+  if (c % 4) return -(int)cudaErrorInvalidValue;
+  cudaStream_t st = S(stream);
+  float* ws = static_cast<float*>(scratch);
+  int nb = bn_blocks(rows);
+  bn_reduce_kernel<<<nb, kEwThreads, 0, st>>>(0, x, nullptr, nullptr, nullptr, rows, c, ws);
+  bn_finalize_fwd_kernel<<<(c + 255) / 256, 256, 0, st>>>(ws, nb, rows, c, eps, momentum, update_running, saved_mean,
+                                                          saved_invstd, running_mean, running_var);
+  bn_apply_kernel<<<ew_blocks(rows * c / 4), kEwThreads, 0, st>>>(x, y, saved_mean, saved_invstd, gamma, beta, rows,
+                                                                  c);
+  return last_error();
+}
+
+int monet_bn_fwd_replay(const float* x, float* y, const float* gamma, const float* beta, const float* saved_mean,
+                        const float* saved_invstd, int64_t rows, int c, void* stream) {
+  if (c % 4) return -(int)cudaErrorInvalidValue;
+  bn_apply_kernel<<<ew_blocks(rows * c / 4), kEwThreads, 0, S(stream)>>>(x, y, saved_mean, saved_invstd, gamma, beta,
+                                                                         rows, c);
+  return last_error();
+}
+
+static int bn_bwd_common(const float* src, const float* dy, float* dx, int accumulate, const float* gamma,
+                         const float* p0, const float* p1, const float* invstd, float* dgamma, float* dbeta,
+                         int64_t rows, int c, int mode, float* ws, cudaStream_t st) {
+  int nb = bn_blocks(rows);
+  float* sum_dy = ws + (size_t)nb * 2 * c;
+  float* sum_dyx = sum_dy + c;
+  bn_reduce_kernel<<<nb, kEwThreads, 0, st>>>(mode, src, dy, p0, p1, rows, c, ws);
+  bn_finalize_bwd_kernel<<<(c + 255) / 256, 256, 0, st>>>(ws, nb, c, sum_dy, sum_dyx, dgamma, dbeta);
+  bn_bwd_apply_kernel<<<ew_blocks(rows * c / 4), kEwThreads, 0, st>>>(src, dy, dx, p0, p1, gamma, invstd, sum_dy,
+                                                                      sum_dyx, rows, c, accumulate);
+  return last_error();
+}
+
+int monet_bn_bwd_in(const float* x, const float* dy, float* dx, int accumulate, const float* gamma,
+                    const float* saved_mean, const float* saved_invstd, float* dgamma, float* dbeta, int64_t rows,
+                    int c, void* scratch, void* stream) {
+  if (c % 4) return -(int)cudaErrorInvalidValue;
+  return bn_bwd_common(x, dy, dx, accumulate, gamma, saved_mean, saved_invstd, saved_invstd, dgamma, dbeta, rows, c,
+                       1, static_cast<float*>(scratch), S(stream));
+}
+
+int monet_bn_bwd_out(const float* y, const float* dy, float* dx, int accumulate, const float* gamma,
+                     const float* beta, const float* saved_invstd, float* dgamma, float* dbeta, int64_t rows, int c,
+                     void* scratch, void* stream) {
+  if (c % 4) return -(int)cudaErrorInvalidValue;
+  cudaStream_t st = S(stream);
+  float* ws = static_cast<float*>(scratch);
+  float* inv_gamma = ws + (size_t)bn_blocks(rows) * 2 * c + 2 * (size_t)c;
+  bn_inv_gamma_kernel<<<(c + 255) / 256, 256, 0, st>>>(gamma, inv_gamma, c, 1e-12f);
+  return bn_bwd_common(y, dy, dx, accumulate, gamma, beta, inv_gamma, saved_invstd, dgamma, dbeta, rows, c, 2, ws, st);
+}
+
+// ------------------------------------------------------------------- add / pass
+int monet_add_fwd(const float* a, const float* b, float* y, int64_t n, void* stream) {
+  add_kernel<<<ew_blocks(n / 4 + 1), kEwThreads, 0, S(stream)>>>(a, b, y, n);
+  return last_error();
+}
+int monet_grad_pass(const float* dy, float* dx, int64_t n, float scale, int accumulate, void* stream) {
+  scale_acc_kernel<<<ew_blocks(n / 4 + 1), kEwThreads, 0, S(stream)>>>(dy, dx, n, scale, accumulate);
+  return last_error();
+}
+
+// ------------------------------------------------------------------- pooling
+int monet_maxpool_fwd(const monet_conv_desc* d, const float* x, float* y, uint8_t* idx8, void* stream) {
+  if (d->c % 4) return -(int)cudaErrorInvalidValue;
+  long long total = (long long)d->n * d->p * d->q * (d->c / 4);
+  maxpool_fwd_kernel<<<ew_blocks(total), kEwThreads, 0, S(stream)>>>(x, y, idx8, d->n, d->h, d->w, d->c, d->p, d->q,
+                                                                     d->r, d->s, d->stride_h, d->stride_w, d->pad_h,
+                                                                     d->pad_w);
+  return last_error();
+}
+int monet_maxpool_bwd(const monet_conv_desc* d, const uint8_t* idx8, const float* x, const float* dy, float* dx,
+                      int accumulate, void* stream) {
+  long long total = (long long)d->n * d->h * d->w * d->c;
+  maxpool_bwd_kernel<<<ew_blocks(total), kEwThreads, 0, S(stream)>>>(idx8, x, dy, dx, d->n, d->h, d->w, d->c, d->p,
+                                                                     d->q, d->r, d->s, d->stride_h, d->stride_w,
+                                                                     d->pad_h, d->pad_w, accumulate);
+  return last_error();
+}
+int monet_avgpool_fwd(const float* x, float* y, int n, int hw, int c, void* stream) {
+  avgpool_fwd_kernel<<<(n * c + 255) / 256, 256, 0, S(stream)>>>(x, y, n, hw, c);
+  return last_error();
+}
+__global__ void avgpool_bwd_kernel(const float* __restrict__ dy, float* dx, int n, int hw, int c, int accumulate) {
+  long long total = (long long)n * hw * c;
+  float inv = 1.0f / (float)hw;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    long long ci = i % c, ni = i / ((long long)hw * c);
+    float v = dy[ni * c + ci] * inv;
+    dx[i] = accumulate ? dx[i] + v : v;
+  }
+}
+int monet_avgpool_bwd(const float* dy, float* dx, int n, int hw, int c, int accumulate, void* stream) {
+  avgpool_bwd_kernel<<<ew_blocks((long long)n * hw * c), kEwThreads, 0, S(stream)>>>(dy, dx, n, hw, c, accumulate);
+  return last_error();
+}
+
+// ------------------------------------------------------------------- loss / SGD
+size_t monet_xent_scratch_bytes(int n) { return (size_t)n * sizeof(float); }
+
+int monet_xent_fwd(const float* logits, const int32_t* labels, float* loss, int n, int classes, void* scratch,
+                   void* stream) {
+  cudaStream_t st = S(stream);
+  float* rows = static_cast<float*>(scratch);
+  xent_fwd_kernel<<<n, 256, 0, st>>>(logits, labels, rows, n, classes);
+  mean_kernel<<<1, 32, 0, st>>>(rows, n, loss);
+  return last_error();
+}
+
+int monet_xent_bwd(const float* logits, const int32_t* labels, const float* dloss, float* dlogits, int n,
+                   int classes, int accumulate, void* stream) {
+  xent_bwd_kernel<<<n, 256, 0, S(stream)>>>(logits, labels, dloss, dlogits, n, classes, accumulate);
+  return last_error();
+}
+
+int monet_sgd_step(float* w, const float* g, float* momentum_buf, int64_t n, float lr, float momentum,
+                   float weight_decay, float grad_scale, int first_step, void* stream) {
+  sgd_kernel<<<ew_blocks(n), kEwThreads, 0, S(stream)>>>(w, g, momentum_buf, n, lr, momentum, weight_decay, grad_scale,
+                                                         first_step);
+  return last_error();
+}
+
+}  // extern "C"

@@ -1,0 +1,559 @@
+// HBM-bound memory-efficient local operators on NHWC fp32 tensors
+// (SURVEY.md §2.2 K4-K13): sign-bitmask ReLU, training BatchNorm with
+// input- and output-activated backwards, residual add / gradient
+// pass-through, maxpool with an 8-bit window index, global average pool,
+// softmax cross-entropy, SGD with momentum.
+//
+// Mask layout (fixed once): bit b of uint32 word w <-> element
+// 32*w + b of the tensor in its physical NHWC order; tail bits are zero.
+#pragma once
+#include "common.cuh"
+
+namespace monet {
+
+constexpr int kEwThreads = 256;
+
+// ------------------------------------------------------------------ ReLU
+// y = max(x, 0) (NaN -> 0, matching mask bit x > 0); optional packed mask.
+// Each thread handles 8 consecutive elements (two float4) -> one byte of mask;
+// 4 consecutive lanes assemble one 32-bit word with shuffles.
+__global__ void relu_fwd_kernel(const float* __restrict__ x, float* y, uint32_t* __restrict__ mask,
+                                long long n) {
+  const long long n8 = (n + 7) / 8;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i - threadIdx.x % 32 < n8; i += stride) {
+    // whole warp iterates together (mask assembly uses shuffles)
+    const bool active = i < n8;
+    uint32_t byte = 0;
+    if (active) {
+      const long long e0 = i * 8;
+      if (e0 + 8 <= n) {
+        float4 a = *reinterpret_cast<const float4*>(x + e0);
+        float4 b = *reinterpret_cast<const float4*>(x + e0 + 4);
+        byte = (a.x > 0.f) | ((a.y > 0.f) << 1) | ((a.z > 0.f) << 2) | ((a.w > 0.f) << 3) | ((b.x > 0.f) << 4) |
+               ((b.y > 0.f) << 5) | ((b.z > 0.f) << 6) | ((b.w > 0.f) << 7);
+        a.x = a.x > 0.f ? a.x : 0.f;
+        a.y = a.y > 0.f ? a.y : 0.f;
+        a.z = a.z > 0.f ? a.z : 0.f;
+        a.w = a.w > 0.f ? a.w : 0.f;
+        b.x = b.x > 0.f ? b.x : 0.f;
+        b.y = b.y > 0.f ? b.y : 0.f;
+        b.z = b.z > 0.f ? b.z : 0.f;
+        b.w = b.w > 0.f ? b.w : 0.f;
+        *reinterpret_cast<float4*>(y + e0) = a;
+        *reinterpret_cast<float4*>(y + e0 + 4) = b;
+      } else {
+        for (long long e = e0; e < n; ++e) {
+          float v = x[e];
+          bool pos = v > 0.f;
+          byte |= (uint32_t)pos << (e - e0);
+          y[e] = pos ? v : 0.f;
+        }
+      }
+    }
+    if (mask != nullptr) {
+      uint32_t word = byte << (8 * (threadIdx.x & 3));
+      word |= __shfl_xor_sync(0xffffffffu, word, 1);
+      word |= __shfl_xor_sync(0xffffffffu, word, 2);
+      if (active && (threadIdx.x & 3) == 0) mask[i / 4] = word;
+    }
+  }
+}
+
+// dx (=|+=) dy * bit; bit from the packed mask.
+__global__ void relu_bwd_mask_kernel(const uint32_t* __restrict__ mask, const float* __restrict__ dy, float* dx,
+                                     long long n, int accumulate) {
+  const long long n8 = (n + 7) / 8;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n8;
+       i += (long long)gridDim.x * blockDim.x) {
+    const uint32_t byte = (__ldg(mask + i / 4) >> (8 * (i & 3))) & 0xFFu;
+    const long long e0 = i * 8;
+    if (e0 + 8 <= n) {
+      float4 a = *reinterpret_cast<const float4*>(dy + e0);
+      float4 b = *reinterpret_cast<const float4*>(dy + e0 + 4);
+      a.x = (byte & 1) ? a.x : 0.f;
+      a.y = (byte & 2) ? a.y : 0.f;
+      a.z = (byte & 4) ? a.z : 0.f;
+      a.w = (byte & 8) ? a.w : 0.f;
+      b.x = (byte & 16) ? b.x : 0.f;
+      b.y = (byte & 32) ? b.y : 0.f;
+      b.z = (byte & 64) ? b.z : 0.f;
+      b.w = (byte & 128) ? b.w : 0.f;
+      if (accumulate) {
+        float4 c = *reinterpret_cast<const float4*>(dx + e0);
+        float4 d = *reinterpret_cast<const float4*>(dx + e0 + 4);
+        a.x += c.x; a.y += c.y; a.z += c.z; a.w += c.w;
+        b.x += d.x; b.y += d.y; b.z += d.z; b.w += d.w;
+      }
+      *reinterpret_cast<float4*>(dx + e0) = a;
+      *reinterpret_cast<float4*>(dx + e0 + 4) = b;
+    } else {
+      for (long long e = e0; e < n; ++e) {
+        float v = ((byte >> (e - e0)) & 1) ? dy[e] : 0.f;
+        dx[e] = accumulate ? dx[e] + v : v;
+      }
+    }
+  }
+}
+
+// dx (=|+=) dy * [s > 0] where s is the ReLU input or output (same sign test).
+__global__ void relu_bwd_sign_kernel(const float* __restrict__ s, const float* __restrict__ dy, float* dx,
+                                     long long n, int accumulate) {
+  const long long n4 = n / 4;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    float4 v = *reinterpret_cast<const float4*>(s + 4 * i);
+    float4 g = *reinterpret_cast<const float4*>(dy + 4 * i);
+    g.x = v.x > 0.f ? g.x : 0.f;
+    g.y = v.y > 0.f ? g.y : 0.f;
+    g.z = v.z > 0.f ? g.z : 0.f;
+    g.w = v.w > 0.f ? g.w : 0.f;
+    if (accumulate) {
+      float4 c = *reinterpret_cast<const float4*>(dx + 4 * i);
+      g.x += c.x; g.y += c.y; g.z += c.z; g.w += c.w;
+    }
+    *reinterpret_cast<float4*>(dx + 4 * i) = g;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+    long long e = n4 * 4 + threadIdx.x;
+    float v = s[e] > 0.f ? dy[e] : 0.f;
+    dx[e] = accumulate ? dx[e] + v : v;
+  }
+}
+
+// ------------------------------------------------------------------ elementwise
+// y = a + b  (residual join)
+__global__ void add_kernel(const float* __restrict__ a, const float* __restrict__ b, float* y, long long n) {
+  const long long n4 = n / 4;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    float4 u = *reinterpret_cast<const float4*>(a + 4 * i);
+    float4 v = *reinterpret_cast<const float4*>(b + 4 * i);
+    *reinterpret_cast<float4*>(y + 4 * i) = make_float4(u.x + v.x, u.y + v.y, u.z + v.z, u.w + v.w);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+    long long e = n4 * 4 + threadIdx.x;
+    y[e] = a[e] + b[e];
+  }
+}
+
+// dx (=|+=) scale * dy
+__global__ void scale_acc_kernel(const float* __restrict__ dy, float* dx, long long n, float scale, int accumulate) {
+  const long long n4 = n / 4;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    float4 g = *reinterpret_cast<const float4*>(dy + 4 * i);
+    g.x *= scale; g.y *= scale; g.z *= scale; g.w *= scale;
+    if (accumulate) {
+      float4 c = *reinterpret_cast<const float4*>(dx + 4 * i);
+      g.x += c.x; g.y += c.y; g.z += c.z; g.w += c.w;
+    }
+    *reinterpret_cast<float4*>(dx + 4 * i) = g;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+    long long e = n4 * 4 + threadIdx.x;
+    float v = scale * dy[e];
+    dx[e] = accumulate ? dx[e] + v : v;
+  }
+}
+
+// ------------------------------------------------------------------ BatchNorm
+// Per-channel reduction over rows of an NHWC [rows, C] matrix.  Each block
+// owns a contiguous range of rows; a thread owns channel quad q and rows
+// r0 + rpi*j.  Partial sums go to ws[block][2][C] and are combined in fp64
+// by bn_finalize (deterministic: fixed block count and order).
+struct BnLayout {
+  int tpr;  // threads per row (channel quads handled concurrently)
+  int qpt;  // quads per thread
+  int rpi;  // rows per iteration of a block
+};
+
+__host__ __device__ inline BnLayout bn_layout(int C) {
+  BnLayout L;
+  int cq = C / 4;
+  L.tpr = cq <= kEwThreads ? cq : kEwThreads;
+  L.qpt = (cq + L.tpr - 1) / L.tpr;
+  L.rpi = kEwThreads / L.tpr;
+  return L;
+}
+
+// mode 0: sum x, sum x^2           (forward statistics)
+// mode 1: sum dy, sum dy*xhat      (backward, xhat = (x-mean)*invstd)
+// mode 2: sum dy, sum dy*xhat      (backward, xhat = (y-beta)/gamma)
+__global__ void bn_reduce_kernel(int mode, const float* __restrict__ x, const float* __restrict__ dy,
+                                 const float* __restrict__ p0, const float* __restrict__ p1, long long rows, int C,
+                                 float* __restrict__ ws) {
+  const BnLayout L = bn_layout(C);
+  const int t = threadIdx.x;
+  const int rsub = t / L.tpr;
+  const int qbase = t % L.tpr;
+  const long long rows_per_block = (rows + gridDim.x - 1) / gridDim.x;
+  const long long r_begin = blockIdx.x * rows_per_block;
+  const long long r_end = min(rows, r_begin + rows_per_block);
+  __shared__ float red[2][kEwThreads * 4];
+  for (int qi = 0; qi < L.qpt; ++qi) {
+    const int q = qbase + qi * L.tpr;
+    float s1[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
+    if (rsub < L.rpi && q < C / 4) {
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+      if (mode != 0) {
+        a = *reinterpret_cast<const float4*>(p0 + 4 * q);  // mean | beta
+        b = *reinterpret_cast<const float4*>(p1 + 4 * q);  // invstd | 1/gamma
+      }
+      for (long long r = r_begin + rsub; r < r_end; r += L.rpi) {
+        const long long off = r * C + 4 * q;
+        float4 v = *reinterpret_cast<const float4*>(x + off);
+        if (mode == 0) {
+          s1[0] += v.x; s1[1] += v.y; s1[2] += v.z; s1[3] += v.w;
+          s2[0] += v.x * v.x; s2[1] += v.y * v.y; s2[2] += v.z * v.z; s2[3] += v.w * v.w;
+        } else {
+          float4 g = *reinterpret_cast<const float4*>(dy + off);
+          float h0 = (v.x - a.x) * b.x, h1 = (v.y - a.y) * b.y, h2 = (v.z - a.z) * b.z, h3 = (v.w - a.w) * b.w;
+          s1[0] += g.x; s1[1] += g.y; s1[2] += g.z; s1[3] += g.w;
+          s2[0] += g.x * h0; s2[1] += g.y * h1; s2[2] += g.z * h2; s2[3] += g.w * h3;
+        }
+      }
+    }
+    // combine the rpi row-subgroups of each channel quad in shared memory
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      red[0][t * 4 + c] = s1[c];
+      red[1][t * 4 + c] = s2[c];
+    }
+    __syncthreads();
+    if (rsub == 0 && q < C / 4) {
+      for (int c = 0; c < 4; ++c) {
+        float a1 = 0.f, a2 = 0.f;
+        for (int j = 0; j < L.rpi; ++j) {
+          a1 += red[0][(j * L.tpr + qbase) * 4 + c];
+          a2 += red[1][(j * L.tpr + qbase) * 4 + c];
+        }
+        ws[(long long)blockIdx.x * 2 * C + 4 * q + c] = a1;
+        ws[(long long)blockIdx.x * 2 * C + C + 4 * q + c] = a2;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// forward: mean/invstd from sums; running-stat update (momentum, unbiased var)
+__global__ void bn_finalize_fwd_kernel(const float* __restrict__ ws, int nblocks, long long rows, int C, float eps,
+                                       float momentum, int update_running, float* mean_out, float* invstd_out,
+                                       float* running_mean, float* running_var) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double s1 = 0.0, s2 = 0.0;
+  for (int b = 0; b < nblocks; ++b) {
+    s1 += ws[(long long)b * 2 * C + c];
+    s2 += ws[(long long)b * 2 * C + C + c];
+  }
+  double mean = s1 / (double)rows;
+  double var = s2 / (double)rows - mean * mean;
+  if (var < 0.0) var = 0.0;
+  mean_out[c] = (float)mean;
+  invstd_out[c] = (float)(1.0 / sqrt(var + (double)eps));
+  if (update_running) {
+    double unbiased = rows > 1 ? var * (double)rows / (double)(rows - 1) : var;
+    running_mean[c] = (float)((1.0 - momentum) * running_mean[c] + momentum * mean);
+    running_var[c] = (float)((1.0 - momentum) * running_var[c] + momentum * unbiased);
+  }
+}
+
+// backward: dgamma = sum dy*xhat, dbeta = sum dy (parameter grads overwrite)
+__global__ void bn_finalize_bwd_kernel(const float* __restrict__ ws, int nblocks, int C, float* sum_dy,
+                                       float* sum_dyxhat, float* dgamma, float* dbeta) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double s1 = 0.0, s2 = 0.0;
+  for (int b = 0; b < nblocks; ++b) {
+    s1 += ws[(long long)b * 2 * C + c];
+    s2 += ws[(long long)b * 2 * C + C + c];
+  }
+  sum_dy[c] = (float)s1;
+  sum_dyxhat[c] = (float)s2;
+  if (dgamma) dgamma[c] = (float)s2;
+  if (dbeta) dbeta[c] = (float)s1;
+}
+
+// y = (x - mean) * invstd * gamma + beta   (train and replay share this kernel,
+// so a recompute with saved statistics is bit-identical to the first forward)
+__global__ void bn_apply_kernel(const float* __restrict__ x, float* y, const float* __restrict__ mean,
+                                const float* __restrict__ invstd, const float* __restrict__ gamma,
+                                const float* __restrict__ beta, long long rows, int C) {
+  const int cq = C / 4;
+  const long long n4 = rows * cq;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int q = (int)(i % cq);
+    float4 v = *reinterpret_cast<const float4*>(x + 4 * i);
+    float4 m = *reinterpret_cast<const float4*>(mean + 4 * q);
+    float4 s = *reinterpret_cast<const float4*>(invstd + 4 * q);
+    float4 g = *reinterpret_cast<const float4*>(gamma + 4 * q);
+    float4 b = *reinterpret_cast<const float4*>(beta + 4 * q);
+    v.x = (v.x - m.x) * s.x * g.x + b.x;
+    v.y = (v.y - m.y) * s.y * g.y + b.y;
+    v.z = (v.z - m.z) * s.z * g.z + b.z;
+    v.w = (v.w - m.w) * s.w * g.w + b.w;
+    *reinterpret_cast<float4*>(y + 4 * i) = v;
+  }
+}
+
+// dx (=|+=) gamma*invstd*(dy - sum_dy/M - xhat*sum_dyxhat/M)
+// xhat from x (p0 = mean, p1 = invstd) or from y (p0 = beta, p1 = 1/gamma)
+__global__ void bn_bwd_apply_kernel(const float* __restrict__ s, const float* __restrict__ dy, float* dx,
+                                    const float* __restrict__ p0, const float* __restrict__ p1,
+                                    const float* __restrict__ gamma, const float* __restrict__ invstd,
+                                    const float* __restrict__ sum_dy, const float* __restrict__ sum_dyxhat,
+                                    long long rows, int C, int accumulate) {
+  const int cq = C / 4;
+  const long long n4 = rows * cq;
+  const float inv_m = 1.0f / (float)rows;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int q = (int)(i % cq);
+    float4 v = *reinterpret_cast<const float4*>(s + 4 * i);
+    float4 g = *reinterpret_cast<const float4*>(dy + 4 * i);
+    float out[4];
+    const float vv[4] = {v.x, v.y, v.z, v.w};
+    const float gg[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int ch = 4 * q + c;
+      const float xhat = (vv[c] - p0[ch]) * p1[ch];
+      const float k = gamma[ch] * invstd[ch];
+      out[c] = k * (gg[c] - sum_dy[ch] * inv_m - xhat * sum_dyxhat[ch] * inv_m);
+    }
+    if (accumulate) {
+      float4 o = *reinterpret_cast<const float4*>(dx + 4 * i);
+      out[0] += o.x; out[1] += o.y; out[2] += o.z; out[3] += o.w;
+    }
+    *reinterpret_cast<float4*>(dx + 4 * i) = make_float4(out[0], out[1], out[2], out[3]);
+  }
+}
+
+// 1/gamma with |gamma| clamped away from 0 (output-activated BN needs gamma != 0)
+__global__ void bn_inv_gamma_kernel(const float* __restrict__ gamma, float* inv, int C, float min_abs) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  float g = gamma[c];
+  float a = fabsf(g) < min_abs ? copysignf(min_abs, g == 0.f ? 1.f : g) : g;
+  inv[c] = 1.0f / a;
+}
+
+// ------------------------------------------------------------------ pooling
+// max pool, NHWC, one thread per (n, p, q, channel quad); idx8 = window index
+// r*S+s of the first maximum (NaN propagates like torch).
+__global__ void maxpool_fwd_kernel(const float* __restrict__ x, float* __restrict__ y, uint8_t* __restrict__ idx,
+                                   int N, int H, int W, int C, int P, int Q, int R, int S, int sh, int sw, int ph,
+                                   int pw) {
+  const int cq = C / 4;
+  const long long total = (long long)N * P * Q * cq;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    int q4 = (int)(i % cq);
+    long long pix = i / cq;
+    int q = (int)(pix % Q);
+    int p = (int)((pix / Q) % P);
+    int n = (int)(pix / ((long long)P * Q));
+    float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    int arg[4] = {0, 0, 0, 0};
+    for (int r = 0; r < R; ++r) {
+      int h = p * sh - ph + r;
+      if ((unsigned)h >= (unsigned)H) continue;
+      for (int s = 0; s < S; ++s) {
+        int w = q * sw - pw + s;
+        if ((unsigned)w >= (unsigned)W) continue;
+        float4 v = *reinterpret_cast<const float4*>(x + (((long long)n * H + h) * W + w) * C + 4 * q4);
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (vv[c] > best[c] || isnan(vv[c])) {  // torch: later NaNs win
+            best[c] = vv[c];
+            arg[c] = r * S + s;
+          }
+        }
+      }
+    }
+    *reinterpret_cast<float4*>(y + pix * C + 4 * q4) = make_float4(best[0], best[1], best[2], best[3]);
+    if (idx) {
+      uint32_t packed = arg[0] | (arg[1] << 8) | (arg[2] << 16) | (arg[3] << 24);
+      *reinterpret_cast<uint32_t*>(idx + pix * C + 4 * q4) = packed;
+    }
+  }
+}
+
+// gather-form backward (deterministic): dx[n,h,w,c] = sum over windows (p,q)
+// covering (h,w) whose argmax is (h,w) of dy[n,p,q,c].  The argmax comes from
+// the saved 8-bit index, or is recomputed from x (input-activated variant).
+__global__ void maxpool_bwd_kernel(const uint8_t* __restrict__ idx, const float* __restrict__ x,
+                                   const float* __restrict__ dy, float* dx, int N, int H, int W, int C, int P,
+                                   int Q, int R, int S, int sh, int sw, int ph, int pw, int accumulate) {
+  const long long total = (long long)N * H * W * C;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    int c = (int)(i % C);
+    long long pix = i / C;
+    int w = (int)(pix % W);
+    int h = (int)((pix / W) % H);
+    int n = (int)(pix / ((long long)H * W));
+    float g = 0.f;
+    // output rows p with p*sh - ph <= h <= p*sh - ph + R - 1
+    int p_lo = max(0, (h + ph - R + sh) / sh);
+    int p_hi = min(P - 1, (h + ph) / sh);
+    int q_lo = max(0, (w + pw - S + sw) / sw);
+    int q_hi = min(Q - 1, (w + pw) / sw);
+    for (int p = p_lo; p <= p_hi; ++p) {
+      int r = h - (p * sh - ph);
+      if (r < 0 || r >= R) continue;
+      for (int q = q_lo; q <= q_hi; ++q) {
+        int s = w - (q * sw - pw);
+        if (s < 0 || s >= S) continue;
+        long long o = (((long long)n * P + p) * Q + q) * C + c;
+        int a;
+        if (idx) {
+          a = idx[o];
+        } else {
+          float best = -INFINITY;
+          a = 0;
+          for (int rr = 0; rr < R; ++rr) {
+            int hh = p * sh - ph + rr;
+            if ((unsigned)hh >= (unsigned)H) continue;
+            for (int ss = 0; ss < S; ++ss) {
+              int ww = q * sw - pw + ss;
+              if ((unsigned)ww >= (unsigned)W) continue;
+              float v = x[(((long long)n * H + hh) * W + ww) * C + c];
+              if (v > best || isnan(v)) {
+                best = v;
+                a = rr * S + ss;
+              }
+            }
+          }
+        }
+        if (a == r * S + s) g += dy[o];
+      }
+    }
+    dx[i] = accumulate ? dx[i] + g : g;
+  }
+}
+
+// global average pool: y[n, c] = mean_{hw} x[n, hw, c]
+__global__ void avgpool_fwd_kernel(const float* __restrict__ x, float* __restrict__ y, int N, int HW, int C) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N * C) return;
+  int n = i / C, c = i % C;
+  const float* base = x + (long long)n * HW * C + c;
+  float s = 0.f;
+  for (int j = 0; j < HW; ++j) s += base[(long long)j * C];
+  y[i] = s / (float)HW;
+}
+
+// ------------------------------------------------------------------ loss
+// loss = mean_n [logsumexp(z_n) - z_n[label_n]]; one block per sample row.
+__global__ void xent_fwd_kernel(const float* __restrict__ z, const int* __restrict__ labels, float* row_loss,
+                                int N, int K) {
+  int n = blockIdx.x;
+  const float* row = z + (long long)n * K;
+  __shared__ float sh[32];
+  float m = -INFINITY;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) m = fmaxf(m, row[k]);
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < blockDim.x / 32 ? sh[threadIdx.x] : -INFINITY;
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (threadIdx.x == 0) sh[0] = v;
+  }
+  __syncthreads();
+  m = sh[0];
+  __syncthreads();
+  float s = 0.f;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) s += expf(row[k] - m);
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float tot = 0.f;
+    for (int j = 0; j < blockDim.x / 32; ++j) tot += sh[j];
+    row_loss[n] = logf(tot) + m - row[labels[n]];
+  }
+}
+
+__global__ void mean_kernel(const float* __restrict__ v, int n, float* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += v[i];
+    *out = (float)(s / n);
+  }
+}
+
+// dz (=|+=) dloss * (softmax(z) - onehot) / N
+__global__ void xent_bwd_kernel(const float* __restrict__ z, const int* __restrict__ labels,
+                                const float* __restrict__ dloss, float* dz, int N, int K, int accumulate) {
+  int n = blockIdx.x;
+  const float* row = z + (long long)n * K;
+  __shared__ float sh[32];
+  float m = -INFINITY;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) m = fmaxf(m, row[k]);
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < blockDim.x / 32 ? sh[threadIdx.x] : -INFINITY;
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (threadIdx.x == 0) sh[0] = v;
+  }
+  __syncthreads();
+  m = sh[0];
+  __syncthreads();
+  float s = 0.f;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) s += expf(row[k] - m);
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float tot = 0.f;
+    for (int j = 0; j < blockDim.x / 32; ++j) tot += sh[j];
+    sh[0] = tot;
+  }
+  __syncthreads();
+  const float inv = 1.0f / sh[0];
+  const float scale = dloss[0] / (float)N;
+  const int lab = labels[n];
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    float g = (expf(row[k] - m) * inv - (k == lab ? 1.f : 0.f)) * scale;
+    float* o = dz + (long long)n * K + k;
+    *o = accumulate ? *o + g : g;
+  }
+}
+
+// ------------------------------------------------------------------ linear helpers
+__global__ void bias_fill_kernel(float* y, const float* __restrict__ b, int N, int K) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < (long long)N * K) y[i] = b[i % K];
+}
+
+// db[k] = sum_n dy[n, k]  (fixed order)
+__global__ void col_sum_kernel(const float* __restrict__ dy, float* db, int N, int K) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  float s = 0.f;
+  for (int n = 0; n < N; ++n) s += dy[(long long)n * K + k];
+  db[k] = s;
+}
+
+// ------------------------------------------------------------------ optimizer
+// torch.optim.SGD semantics: g' = g*grad_scale + wd*w; buf = momentum*buf + g'
+// (buf = g' on the first step); w -= lr*buf
+__global__ void sgd_kernel(float* w, const float* __restrict__ g, float* buf, long long n, float lr, float momentum,
+                           float wd, float grad_scale, int first) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    float d = g[i] * grad_scale + wd * w[i];
+    float b = first ? d : momentum * buf[i] + d;
+    buf[i] = b;
+    w[i] -= lr * b;
+  }
+}
+
+}  // namespace monet

@@ -1,0 +1,487 @@
+"""The recompute executor (SURVEY.md §2.2 R1 + R2): replays a Schedule on a B200.
+
+``execute(schedule, g, catalog, runtime=rt)`` is the GPU counterpart of the
+reference ``simulate(schedule, g, catalog)`` (pkg/src/remsched/schedule.py:320):
+the same plan goes in, the same ``Trace`` comes out, and in between every
+ledger step launches the sm_100a kernel of the chosen catalog variant.
+
+* Ledger.  Steps come from :func:`schedule.walk`, the one replay of Alg. 1-2
+  shared with ``simulate``; the executed trace is therefore byte-identical to
+  the simulator's (tests/test_engine_*.py check it against the reference).
+* Memory.  Everything the graph folds into ``params_bytes`` (parameters,
+  grads, momenta, BN statistics, kernel scratch, the staged input batch,
+  labels) lives in one fixed region of exactly that size.  Every activation,
+  intermediate, gradient and workspace instance of the ledger lives in one
+  arena whose offsets are planned statically from the ledger's alloc/free
+  points (csrc/arena.cpp); the arena is sized by the plan and capped by the
+  budget, so the physical peak is params_bytes + arena high-water mark.
+* Launch.  Each step is pre-bound to a ctypes call with resolved device
+  pointers; ``Runtime.step`` just runs the list (and can be captured into a
+  CUDA graph, ``Runtime.capture``).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _native
+from .bound import check_schedule
+from .costmodel import Catalog
+from .graph import Graph, compute_dependency_sets
+from .schedule import Schedule, SimulationError, Trace, ledger, validate
+
+__all__ = ["Runtime", "Plan", "ExecResult", "BudgetExceeded", "execute"]
+
+ALIGN = 256
+
+
+class BudgetExceeded(RuntimeError):
+    """The planned physical footprint exceeds the byte budget (CLI exit 6)."""
+
+
+def _round(v: int) -> int:
+    return (v + ALIGN - 1) // ALIGN * ALIGN
+
+
+@dataclass
+class Plan:
+    schedule: Schedule
+    trace: Trace
+    calls: list
+    arena_bytes: int
+    ledger_peak: int
+    bound_peak: int | None
+    n_blocks: int
+    launches: int
+    step_kinds: dict = field(default_factory=dict)
+
+
+@dataclass
+class ExecResult:
+    trace: Trace
+    loss: float
+    ledger_peak: int           # simulate()'s peak (logical bytes, incl. params_bytes)
+    physical_peak: int         # params_bytes + planned arena high-water mark
+    bound_peak: int | None     # check_schedule() modeled peak (the ILP bound)
+    arena_bytes: int
+    params_bytes: int
+    torch_peak_bytes: int      # torch.cuda.max_memory_allocated during the step
+    launches: int
+
+
+class Runtime:
+    """Device state for one network on one GPU: the fixed region and the kernels."""
+
+    def __init__(self, net, device="cuda:0", lr=0.1, momentum=0.9, weight_decay=0.0,
+                 grad_scale=1.0, budget_bytes: int | None = None):
+        self.net = net
+        self.device = torch.device(device)
+        self.lib = _native.lib()
+        if self.lib.device_check() != 0:
+            raise _native.NativeError("libmonet_b200 needs an sm_100 (B200) device")
+        self.lr, self.momentum, self.weight_decay = lr, momentum, weight_decay
+        self.grad_scale = grad_scale
+        self.budget_bytes = budget_bytes
+        self.params_bytes = net.params_bytes()
+        self.fixed = torch.zeros(self.params_bytes, dtype=torch.uint8, device=self.device)
+        self._carve()
+        self.arena = None
+        self._plans: dict[int, Plan] = {}
+        self.graph = None
+        self.comm = None  # set by dp.DataParallel for the gradient allreduce
+
+    # ------------------------------------------------------------ fixed region
+    def _carve(self):
+        lay = self.net.fixed_layout()
+        base = 0
+        self.region = {}
+        for name, nbytes in lay.items():
+            self.region[name] = (base, nbytes)
+            base += _round(nbytes)
+        assert base == self.params_bytes
+
+        def f32(name, count=None):
+            off, nb = self.region[name]
+            n = nb // 4 if count is None else count
+            return self.fixed[off:off + 4 * n].view(torch.float32)
+
+        self.params = f32("params")
+        self.grads = f32("grads")
+        self.mom = f32("momentum")
+        self.staging = f32("staging_input")
+        off, nb = self.region["labels"]
+        self.labels = self.fixed[off:off + nb].view(torch.int32)
+        self.consts = f32("consts", 4)
+        self.consts[0] = 1.0
+        self.scratch_ptr = self.fixed.data_ptr() + self.region["scratch"][0]
+        self.pview, self.gview = {}, {}
+        pos = 0
+        for nid, name, t in self.net.param_items():
+            n = t.numel()
+            self.params[pos:pos + n].copy_(t.reshape(-1))
+            self.pview[(nid, name)] = self.params[pos:pos + n]
+            self.gview[(nid, name)] = self.grads[pos:pos + n]
+            pos += n
+        stats = f32("bn_stats")
+        self.bn = {}
+        pos = 0
+        for op in self.net.ops:
+            if op.kind != "bn":
+                continue
+            c = op.shape[-1]
+            views = [stats[pos + j * c: pos + (j + 1) * c] for j in range(4)]
+            pos += 4 * c
+            views[2].copy_(op.attrs["running_mean"])
+            views[3].copy_(op.attrs["running_var"])
+            self.bn[op.id] = views  # saved_mean, saved_invstd, running_mean, running_var
+
+    def set_batch(self, images: torch.Tensor, labels: torch.Tensor):
+        """Stage one batch: images NCHW (any device), labels (N,) ints."""
+        n, c, h, w = images.shape
+        x = self.staging.view(n, h, w, -1)
+        if x.shape[3] != c:
+            x[..., c:].zero_()
+        x[..., :c].copy_(images.permute(0, 2, 3, 1), non_blocking=True)
+        self.labels.copy_(labels.to(torch.int32), non_blocking=True)
+
+    def set_batch_nhwc(self, images_nhwc: torch.Tensor, labels: torch.Tensor):
+        """Stage a batch already in the engine layout (N,H,W,Cpad) — one copy each."""
+        self.staging.copy_(images_nhwc.reshape(-1), non_blocking=True)
+        self.labels.copy_(labels, non_blocking=True)
+
+    def loss_value(self) -> float:
+        return float(self.consts[1].item())
+
+    # ------------------------------------------------------------ planning
+    def plan(self, schedule: Schedule, g: Graph, catalog: Catalog, check_bound: bool = True) -> Plan:
+        key = id(schedule)
+        if key in self._plans and self._plans[key].schedule is schedule:
+            return self._plans[key]
+        self._check_graph(g)
+        tags = validate(schedule, g, compute_dependency_sets(g), catalog)
+        if tags:
+            raise SimulationError(f"schedule is not executable: {tags}")
+        steps, trace = ledger(schedule, g, catalog)
+        blocks, step_blocks = self._lifetimes(steps, g)
+        arena_bytes, offsets = self._place(blocks)
+        fixed_peak = self.params_bytes + arena_bytes
+        if self.budget_bytes is not None and fixed_peak > self.budget_bytes:
+            raise BudgetExceeded(f"planned footprint {fixed_peak} B exceeds budget {self.budget_bytes} B "
+                                 f"(ledger peak {trace.peak_memory} B)")
+        if self.arena is None or self.arena.numel() < arena_bytes:
+            self.arena = None
+            torch.cuda.empty_cache()
+            self.arena = torch.empty(max(arena_bytes, ALIGN), dtype=torch.uint8, device=self.device)
+        bound = None
+        if check_bound:
+            ok, bound, _ = check_schedule(g, compute_dependency_sets(g), catalog, schedule,
+                                          self.budget_bytes if self.budget_bytes else 1 << 62)
+        base = self.arena.data_ptr()
+        calls = []
+        for s, sb in zip(steps, step_blocks):
+            ptrs = {k: base + offsets[b] for k, b in sb["blocks"].items()}
+            calls.extend(self._bind(s, sb, ptrs, catalog))
+        calls.extend(self._bind_optimizer())
+        plan = Plan(schedule, trace, calls, arena_bytes, trace.peak_memory, bound, len(blocks),
+                    sum(1 for c in calls if c[0] == "k"))
+        self._plans[key] = plan
+        return plan
+
+    def _check_graph(self, g: Graph):
+        net = self.net
+        if g.n != net.n or any(g.output_bytes(op.id) != op.nbytes for op in net.ops):
+            raise ValueError("graph does not describe this runtime's network")
+        if g.params_bytes != self.params_bytes:
+            raise ValueError(f"graph params_bytes {g.params_bytes} != runtime fixed region "
+                             f"{self.params_bytes}")
+
+    def _lifetimes(self, steps, g: Graph):
+        """Blocks [t_alloc, t_free) in half-step units and the blocks each step touches."""
+        sizes_of = {u.id: u.nbytes for u in g.storables}
+        live: dict[tuple, int] = {}
+        blocks: list[list[int]] = []  # [size, t_alloc, t_free]
+        per_step = []
+
+        def new_block(size, t):
+            blocks.append([size, t, None])
+            return len(blocks) - 1
+
+        def end(key, t):
+            b = live.pop(key)
+            blocks[b][2] = t
+
+        for s_idx, s in enumerate(steps):
+            t0, t1 = 2 * s_idx, 2 * s_idx + 1
+            for key in s.drops:
+                end(key, t0)
+            touched = {}
+            # inputs read by the step (resolved before allocations; in-place takes one over)
+            if s.kind in ("forward", "recompute"):
+                for j in g.deps(s.node):
+                    touched[("in", j)] = live[("a", j)]
+            else:
+                for d in s.variant.deps:
+                    touched[("in", d)] = live[("a", d)]
+                for j in g.deps(s.node):
+                    if ("a", j) in live:
+                        touched[("in", j)] = live[("a", j)]
+                if s.node in g.backward_by_node and ("a", s.node) in live:
+                    touched[("in", s.node)] = live[("a", s.node)]
+            for key in s.allocs:
+                if key[0] == "a":
+                    if s.inplace_from is not None and key[1] == s.node:
+                        b = live.pop(("a", s.inplace_from))
+                        live[key] = b
+                    else:
+                        live[key] = new_block(sizes_of[key[1]], t0)
+                else:
+                    live[key] = new_block(g.grad_bytes(key[1]), t0)
+                touched[key] = live[key]
+            if s.kind == "backward":
+                touched[("g", s.node)] = live[("g", s.node)]
+                for j in g.deps(s.node):
+                    if ("g", j) in live:
+                        touched[("g", j)] = live[("g", j)]
+            if s.workspace:
+                touched[("ws",)] = new_block(s.workspace, t0)
+                blocks[touched[("ws",)]][2] = t1
+            for key in s.frees:
+                end(key, t1)
+            per_step.append({"blocks": touched})
+        for key in list(live):
+            end(key, 2 * len(steps))
+        return blocks, per_step
+
+    def _place(self, blocks):
+        n = len(blocks)
+        arr = lambda vals: (C.c_int64 * max(n, 1))(*vals)
+        sizes = arr([b[0] for b in blocks])
+        ta = arr([b[1] for b in blocks])
+        tf = arr([b[2] for b in blocks])
+        offs = (C.c_int64 * max(n, 1))()
+        peak = C.c_int64(0)
+        cap = 0
+        if self.budget_bytes is not None:
+            cap = max(0, self.budget_bytes - self.params_bytes)
+        rc = self.lib.dll.monet_arena_plan(n, C.cast(sizes, C.c_void_p), C.cast(ta, C.c_void_p),
+                                           C.cast(tf, C.c_void_p), ALIGN, cap, C.cast(offs, C.c_void_p),
+                                           C.byref(peak))
+        if rc == -12:
+            raise BudgetExceeded(f"arena plan needs {peak.value} B, only {cap} B left under the budget")
+        if rc:
+            raise RuntimeError(f"arena planner failed ({rc})")
+        return peak.value, list(offs)[:n]
+
+    # ------------------------------------------------------------ binding
+    def _bind(self, s, sb, ptrs, catalog):
+        """Kernel calls of one ledger step: list of ("k", fn, args) / ("py", callable)."""
+        net, lib = self.net, self.lib.dll
+        op = net.op(s.node)
+        st = lambda: torch.cuda.current_stream(self.device).cuda_stream
+        out = []
+        P = lambda key: ptrs[key]
+        if s.kind in ("forward", "recompute"):
+            y = P(("a", op.id))
+            xs = [P(("in", j)) for j in op.deps]
+            ws = ptrs.get(("ws",))
+            if op.kind == "input":
+                nb = op.nbytes
+                out.append(("copy", y, self.staging.data_ptr(), nb))
+            elif op.kind == "conv":
+                d = net.conv_desc(op)
+                v = _native.CONV_VARIANTS[s.impl]
+                out.append(("k", lib.monet_conv_fwd, (v, C.byref(d), xs[0], self.pview[(op.id, "weight")].data_ptr(),
+                                                      y, ws, s.workspace, None), d))
+            elif op.kind == "bn":
+                c = op.shape[-1]
+                rows = op.numel // c
+                sm, si, rm, rv = (t.data_ptr() for t in self.bn[op.id])
+                gma = self.pview[(op.id, "weight")].data_ptr()
+                bta = self.pview[(op.id, "bias")].data_ptr()
+                if s.kind == "forward":
+                    out.append(("k", lib.monet_bn_fwd_train,
+                                (xs[0], y, gma, bta, sm, si, rm, rv, rows, c, C.c_float(op.attrs["eps"]),
+                                 C.c_float(op.attrs["momentum"]), 1, self.scratch_ptr, None)))
+                else:  # recompute: reuse saved statistics, running stats untouched
+                    out.append(("k", lib.monet_bn_fwd_replay, (xs[0], y, gma, bta, sm, si, rows, c, None)))
+            elif op.kind == "relu":
+                mid = net.intermediate_of[op.id]
+                mask = P(("a", mid)) if mid in s.planned_ints else None
+                out.append(("k", lib.monet_relu_fwd, (xs[0], y, mask, op.numel, None)))
+            elif op.kind == "add":
+                out.append(("k", lib.monet_add_fwd, (xs[0], xs[1], y, op.numel, None)))
+            elif op.kind == "maxpool":
+                d = net.pool_desc(op)
+                mid = net.intermediate_of[op.id]
+                idx = P(("a", mid)) if mid in s.planned_ints else None
+                out.append(("k", lib.monet_maxpool_fwd, (C.byref(d), xs[0], y, idx, None), d))
+            elif op.kind == "avgpool":
+                n, h, w, c = net.op(op.deps[0]).shape
+                out.append(("k", lib.monet_avgpool_fwd, (xs[0], y, n, h * w, c, None)))
+            elif op.kind == "fc":
+                n, fi = net.op(op.deps[0]).shape
+                fo = op.shape[1]
+                v = 1 if s.impl == "gemm-splitk" else 0
+                out.append(("k", lib.monet_linear_fwd,
+                            (v, xs[0], self.pview[(op.id, "weight")].data_ptr(),
+                             self.pview[(op.id, "bias")].data_ptr(), y, n, fi, fo, ws, s.workspace, None)))
+            elif op.kind == "xent":
+                out.append(("k", lib.monet_xent_fwd, (xs[0], self.labels.data_ptr(), y, net.batch,
+                                                      net.num_classes, self.scratch_ptr, None)))
+                out.append(("copy", self.consts.data_ptr() + 4, y, 4))
+            else:
+                raise ValueError(op.kind)
+            return out
+
+        # backward
+        dy = P(("g", op.id))
+        ws = ptrs.get(("ws",))
+        acc = lambda j: 0 if j in s.new_grads else 1
+        if op.id == net.n:
+            out.append(("copy", dy, self.consts.data_ptr(), 4))  # seed dL/dL = 1
+        if op.kind == "input":
+            return out
+        if op.kind == "conv":
+            d = net.conv_desc(op)
+            v = _native.CONV_VARIANTS[s.impl]
+            j = op.deps[0]
+            wt = self.pview[(op.id, "weight")].data_ptr()
+            if net.grad_bytes(net.op(j)) > 0:
+                out.append(("k", lib.monet_conv_dgrad, (v, C.byref(d), dy, wt, P(("g", j)), acc(j), ws,
+                                                        s.workspace, None), d))
+            out.append(("k", lib.monet_conv_wgrad, (v, C.byref(d), P(("in", j)), dy,
+                                                    self.gview[(op.id, "weight")].data_ptr(), 0, ws,
+                                                    s.workspace, None), d))
+        elif op.kind == "bn":
+            c = op.shape[-1]
+            rows = op.numel // c
+            j = op.deps[0]
+            sm, si, _, _ = (t.data_ptr() for t in self.bn[op.id])
+            gma = self.pview[(op.id, "weight")].data_ptr()
+            bta = self.pview[(op.id, "bias")].data_ptr()
+            dg = self.gview[(op.id, "weight")].data_ptr()
+            db = self.gview[(op.id, "bias")].data_ptr()
+            if s.impl == "bwd-in":
+                out.append(("k", lib.monet_bn_bwd_in, (P(("in", j)), dy, P(("g", j)), acc(j), gma, sm, si, dg, db,
+                                                      rows, c, self.scratch_ptr, None)))
+            else:
+                out.append(("k", lib.monet_bn_bwd_out, (P(("in", op.id)), dy, P(("g", j)), acc(j), gma, bta, si,
+                                                       dg, db, rows, c, self.scratch_ptr, None)))
+        elif op.kind == "relu":
+            j = op.deps[0]
+            if s.impl == "bwd-mask":
+                src, fn = P(("in", net.intermediate_of[op.id])), lib.monet_relu_bwd_mask
+            elif s.impl == "bwd-out":
+                src, fn = P(("in", op.id)), lib.monet_relu_bwd_out
+            else:
+                src, fn = P(("in", j)), lib.monet_relu_bwd_in
+            out.append(("k", fn, (src, dy, P(("g", j)), op.numel, acc(j), None)))
+        elif op.kind == "add":
+            for j in op.deps:
+                out.append(("k", lib.monet_grad_pass, (dy, P(("g", j)), op.numel, C.c_float(1.0), acc(j), None)))
+        elif op.kind == "maxpool":
+            d = net.pool_desc(op)
+            j = op.deps[0]
+            if s.impl == "bwd-idx":
+                args = (C.byref(d), P(("in", net.intermediate_of[op.id])), None, dy, P(("g", j)), acc(j), None)
+            else:
+                args = (C.byref(d), None, P(("in", j)), dy, P(("g", j)), acc(j), None)
+            out.append(("k", lib.monet_maxpool_bwd, args, d))
+        elif op.kind == "avgpool":
+            j = op.deps[0]
+            n, h, w, c = net.op(j).shape
+            out.append(("k", lib.monet_avgpool_bwd, (dy, P(("g", j)), n, h * w, c, acc(j), None)))
+        elif op.kind == "fc":
+            j = op.deps[0]
+            n, fi = net.op(j).shape
+            fo = op.shape[1]
+            v = 1 if s.impl == "gemm-splitk" else 0
+            out.append(("k", lib.monet_linear_bwd,
+                        (v, P(("in", j)), self.pview[(op.id, "weight")].data_ptr(), dy, P(("g", j)), acc(j),
+                         self.gview[(op.id, "weight")].data_ptr(), self.gview[(op.id, "bias")].data_ptr(),
+                         n, fi, fo, ws, s.workspace, None)))
+        elif op.kind == "xent":
+            j = op.deps[0]
+            out.append(("k", lib.monet_xent_bwd, (P(("in", j)), self.labels.data_ptr(), dy, P(("g", j)),
+                                                  net.batch, net.num_classes, acc(j), None)))
+        else:
+            raise ValueError(op.kind)
+        return out
+
+    def _bind_optimizer(self):
+        calls = []
+        if self.comm is not None:
+            calls.append(("py", self.comm.allreduce_grads))
+        calls.append(("k", self.lib.dll.monet_sgd_step,
+                      (self.params.data_ptr(), self.grads.data_ptr(), self.mom.data_ptr(), self.params.numel(),
+                       C.c_float(self.lr), C.c_float(self.momentum), C.c_float(self.weight_decay),
+                       C.c_float(self.grad_scale), 0, None)))
+        return calls
+
+    # ------------------------------------------------------------ running
+    def run(self, plan: Plan):
+        """Enqueue one training step (forward, scheduled backward, SGD) on the current stream."""
+        stream = torch.cuda.current_stream(self.device)
+        sp = C.c_void_p(stream.cuda_stream)
+        cudart = _cudart()
+        for c in plan.calls:
+            kind = c[0]
+            if kind == "k":
+                fn, args = c[1], c[2]
+                rc = fn(*args[:-1], sp)
+                if rc != 0:
+                    raise _native.NativeError(f"{fn.__name__} failed with code {rc}")
+            elif kind == "copy":
+                rc = cudart.cudaMemcpyAsync(C.c_void_p(c[1]), C.c_void_p(c[2]), C.c_size_t(c[3]), 3, sp)
+                if rc != 0:
+                    raise _native.NativeError(f"cudaMemcpyAsync failed ({rc})")
+            else:
+                c[1]()
+
+
+_CUDART = None
+
+
+def _cudart():
+    global _CUDART
+    if _CUDART is None:
+        lib = C.CDLL(str(_native.LIB_PATH))  # libmonet links cudart; resolve through it
+        try:
+            fn = lib.cudaMemcpyAsync
+        except AttributeError:
+            lib = C.CDLL("libcudart.so")
+            fn = lib.cudaMemcpyAsync
+        fn.restype = C.c_int
+        fn.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p]
+        _CUDART = lib
+    return _CUDART
+
+
+def execute(schedule: Schedule, g: Graph, catalog: Catalog, *, runtime: Runtime,
+            images: torch.Tensor | None = None, labels: torch.Tensor | None = None) -> ExecResult:
+    """Run one scheduled training step on the GPU and return its ledger and measurements.
+
+    Raises SimulationError for schedules the simulator rejects and
+    BudgetExceeded when the planned footprint exceeds the runtime's budget.
+    """
+    if images is not None:
+        runtime.set_batch(images, labels)
+    plan = runtime.plan(schedule, g, catalog)
+    torch.cuda.synchronize(runtime.device)
+    torch.cuda.reset_peak_memory_stats(runtime.device)
+    runtime.run(plan)
+    torch.cuda.synchronize(runtime.device)
+    return ExecResult(
+        trace=plan.trace,
+        loss=runtime.loss_value(),
+        ledger_peak=plan.ledger_peak,
+        physical_peak=runtime.params_bytes + plan.arena_bytes,
+        bound_peak=plan.bound_peak,
+        arena_bytes=plan.arena_bytes,
+        params_bytes=runtime.params_bytes,
+        torch_peak_bytes=torch.cuda.max_memory_allocated(runtime.device),
+        launches=plan.launches,
+    )

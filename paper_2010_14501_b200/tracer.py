@@ -1,0 +1,353 @@
+"""Model tracer: torch model -> Network -> graph document.
+
+``trace_graph(model, example_input)`` walks ``torch.fx.symbolic_trace(model)``
+and emits a :class:`Network`, one op per graph node in execution order, with
+the conventions the reference graph format imposes (graph.py:251-360,
+SURVEY.md §7 hard part 7):
+
+* node 1 is the input batch, with a dependency-free backward and a zero-byte
+  gradient (no dgrad of the stem is ever needed);
+* the softmax cross-entropy loss is appended as the unique sink N;
+* ReLU sign bitmasks and maxpool 8-bit window indices are *intermediates* of
+  their creator, stored or recomputed like any other storable;
+* sizes are the executor's real allocation sizes: NHWC fp32 activations,
+  ceil(numel/32)*4 bytes per mask, numel bytes per maxpool index (rounded up
+  to 4), the stem input padded from 3 to 4 channels;
+* parameters, their gradients and momenta, BN statistics, the staging input
+  batch, labels and kernel scratch are all folded into ``params_bytes``.
+
+``Network.graph_doc()`` / ``Network.catalog_doc(costs)`` emit the two
+documents the planner consumes.
+"""
+
+from __future__ import annotations
+
+import math
+import operator
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _native
+
+__all__ = ["Op", "Network", "trace_graph", "build_network"]
+
+F32 = 4
+
+
+@dataclass
+class Op:
+    id: int
+    kind: str                    # input conv bn relu add maxpool avgpool fc xent
+    deps: tuple
+    shape: tuple                 # output shape: NHWC for maps, (N, F) for vectors, () for loss
+    attrs: dict = field(default_factory=dict)
+    params: dict = field(default_factory=dict)   # name -> torch tensor (CPU, engine layout)
+    name: str = ""
+
+    @property
+    def numel(self) -> int:
+        return int(math.prod(self.shape)) if self.shape else 1
+
+    @property
+    def nbytes(self) -> int:
+        return self.numel * F32
+
+
+def mask_bytes(numel: int) -> int:
+    return (numel + 31) // 32 * 4
+
+
+def idx_bytes(numel: int) -> int:
+    return (numel + 3) // 4 * 4
+
+
+class Network:
+    """Executable op list in node order plus its parameters (engine layout)."""
+
+    def __init__(self, ops: list[Op], batch: int, num_classes: int):
+        self.ops = ops
+        self.batch = batch
+        self.num_classes = num_classes
+        self.n = len(ops)
+        # intermediates: one per ReLU (sign mask) and per maxpool (8-bit index)
+        self.intermediate_of: dict[int, int] = {}
+        self.intermediate_bytes: dict[int, int] = {}
+        nid = self.n + 1
+        for op in ops:
+            if op.kind == "relu":
+                self.intermediate_of[op.id] = nid
+                self.intermediate_bytes[nid] = mask_bytes(op.numel)
+                nid += 1
+            elif op.kind == "maxpool":
+                self.intermediate_of[op.id] = nid
+                self.intermediate_bytes[nid] = idx_bytes(op.numel)
+                nid += 1
+
+    def op(self, i: int) -> Op:
+        return self.ops[i - 1]
+
+    # -------------------------------------------------------------- fixed region
+    def param_items(self):
+        for op in self.ops:
+            for name, t in op.params.items():
+                yield op.id, name, t
+
+    def n_param_elems(self) -> int:
+        return sum(t.numel() for _, _, t in self.param_items())
+
+    def bn_channels(self) -> int:
+        return sum(op.shape[-1] for op in self.ops if op.kind == "bn")
+
+    def scratch_bytes(self) -> int:
+        lib = _native.lib()
+        s = 0
+        for op in self.ops:
+            if op.kind == "bn":
+                rows = op.numel // op.shape[-1]
+                s = max(s, lib.bn_scratch_bytes(rows, op.shape[-1]))
+        s = max(s, lib.xent_scratch_bytes(self.batch))
+        return (s + 255) // 256 * 256
+
+    def input_bytes(self) -> int:
+        return self.ops[0].nbytes
+
+    def fixed_layout(self) -> dict:
+        """Byte sizes of everything outside the arena (all folded into params_bytes)."""
+        p = self.n_param_elems() * F32
+        return {
+            "params": p, "grads": p, "momentum": p,
+            "bn_stats": 4 * self.bn_channels() * F32,   # saved mean/invstd, running mean/var
+            "scratch": self.scratch_bytes(),
+            "staging_input": self.input_bytes(),
+            "labels": self.batch * 4,
+            "consts": 256,
+        }
+
+    def params_bytes(self) -> int:
+        return sum((v + 255) // 256 * 256 for v in self.fixed_layout().values())
+
+    # -------------------------------------------------------------- documents
+    def grad_bytes(self, op: Op) -> int:
+        if op.kind == "input":
+            return 0
+        return op.nbytes
+
+    def graph_doc(self) -> dict:
+        nodes, backward, inters = [], [], []
+        for op in self.ops:
+            nodes.append({"id": op.id, "output_bytes": op.nbytes, "deps": list(op.deps)})
+            impls = [{"name": n, "deps_kind": k, "extra_deps": []} for n, k in BWD_IMPLS[op.kind]]
+            backward.append({"node": op.id, "grad_bytes": self.grad_bytes(op), "impls": impls})
+            if op.id in self.intermediate_of:
+                u = self.intermediate_of[op.id]
+                inters.append({"id": u, "bytes": self.intermediate_bytes[u], "creator": op.id})
+        return {"format": 1, "params_bytes": self.params_bytes(), "nodes": nodes,
+                "backward": backward, "intermediates": inters}
+
+    def variants(self, op: Op):
+        """(forward variants, backward variants) as (name, workspace_bytes, deps) tuples."""
+        lib = _native.lib()
+        fwd, bwd = [], []
+        x = list(op.deps)
+        if op.kind == "conv":
+            d = self.conv_desc(op)
+            fwd.append(("implicit", 0))
+            ws = lib.conv_ws_bytes(1, 0, d)
+            if ws:
+                fwd.append(("splitk", ws))
+            bwd.append(("splitk", lib.conv_ws_bytes(1, 3, d), x))
+            bwd.append(("implicit", lib.conv_ws_bytes(0, 3, d), x))
+        elif op.kind == "fc":
+            n, fi = self.op(op.deps[0]).shape
+            fo = op.shape[1]
+            fwd.append(("gemm", 0))
+            ws = lib.linear_ws_bytes(1, 0, n, fi, fo)
+            if ws:
+                fwd.append(("gemm-splitk", ws))
+            bwd.append(("gemm-splitk", lib.linear_ws_bytes(1, 3, n, fi, fo), x))
+            bwd.append(("gemm", lib.linear_ws_bytes(0, 3, n, fi, fo), x))
+        elif op.kind == "relu":
+            fwd.append(("relu", 0))
+            bwd += [("bwd-in", 0, x), ("bwd-out", 0, [op.id]),
+                    ("bwd-mask", 0, [self.intermediate_of[op.id]])]
+        elif op.kind == "bn":
+            fwd.append(("bn", 0))
+            bwd += [("bwd-in", 0, x), ("bwd-out", 0, [op.id])]
+        elif op.kind == "maxpool":
+            fwd.append(("maxpool", 0))
+            bwd += [("bwd-in", 0, x), ("bwd-idx", 0, [self.intermediate_of[op.id]])]
+        elif op.kind == "input":
+            fwd.append(("load", 0))
+            bwd.append(("none", 0, []))
+        elif op.kind in ("add", "avgpool"):
+            fwd.append((op.kind, 0))
+            bwd.append(("bwd", 0, []))
+        elif op.kind == "xent":
+            fwd.append(("xent", 0))
+            bwd.append(("bwd", 0, x))
+        else:
+            raise ValueError(op.kind)
+        return fwd, bwd
+
+    def catalog_doc(self, costs=None) -> dict:
+        """Catalog with measured costs (``costs[(node, pass, name)]`` -> int ns) or the
+        analytic roofline estimate when a cost is not supplied."""
+        from .costs import analytic_cost
+        fwd_doc, bwd_doc = [], []
+        for op in self.ops:
+            fv, bv = self.variants(op)
+            fwd_doc.append({"node": op.id, "variants": [
+                {"name": n, "workspace_bytes": ws,
+                 "cost": _cost(costs, (op.id, "fwd", n), lambda: analytic_cost(self, op, "fwd", n))}
+                for n, ws in fv]})
+            bwd_doc.append({"node": op.id, "variants": [
+                {"name": n, "workspace_bytes": ws, "deps": sorted(deps),
+                 "cost": _cost(costs, (op.id, "bwd", n), lambda: analytic_cost(self, op, "bwd", n))}
+                for n, ws, deps in bv]})
+        return {"format": 1, "forward": fwd_doc, "backward": bwd_doc}
+
+    def conv_desc(self, op: Op):
+        n, h, w, c = self.op(op.deps[0]).shape
+        a = op.attrs
+        return _native.ConvDesc(n, h, w, c, op.shape[3], a["r"], a["s"], op.shape[1], op.shape[2],
+                                a["stride"], a["stride"], a["pad"], a["pad"])
+
+    def pool_desc(self, op: Op):
+        n, h, w, c = self.op(op.deps[0]).shape
+        a = op.attrs
+        return _native.ConvDesc(n, h, w, c, c, a["r"], a["s"], op.shape[1], op.shape[2],
+                                a["stride"], a["stride"], a["pad"], a["pad"])
+
+    def conv_flops(self) -> int:
+        tot = 0
+        for op in self.ops:
+            if op.kind == "conv":
+                cin = self.op(op.deps[0]).shape[3]
+                tot += 2 * op.numel * cin * op.attrs["r"] * op.attrs["s"]
+            elif op.kind == "fc":
+                tot += 2 * op.numel * self.op(op.deps[0]).shape[1]
+        return tot
+
+
+def _cost(costs, key, fallback):
+    if costs is not None and key in costs:
+        return int(costs[key])
+    return int(fallback())
+
+
+BWD_IMPLS = {
+    "input": [("none", "input")],
+    "conv": [("splitk", "input"), ("implicit", "input")],
+    "fc": [("gemm-splitk", "input"), ("gemm", "input")],
+    "bn": [("bwd-in", "input"), ("bwd-out", "output")],
+    "relu": [("bwd-in", "input"), ("bwd-out", "output"), ("bwd-mask", "intermediate")],
+    "maxpool": [("bwd-in", "input"), ("bwd-idx", "intermediate")],
+    "add": [("bwd", "input")],
+    "avgpool": [("bwd", "input")],
+    "xent": [("bwd", "input")],
+}
+
+
+# ---------------------------------------------------------------------- tracing
+
+def _pair(v):
+    return v if isinstance(v, int) else v[0]
+
+
+def trace_graph(model: torch.nn.Module, example_input: torch.Tensor, num_classes: int | None = None) -> Network:
+    """Trace a torchvision-style CNN into a Network (engine layout parameters).
+
+    Supported modules: Conv2d (no bias, groups=1), BatchNorm2d, ReLU,
+    MaxPool2d, AdaptiveAvgPool2d((1,1)), Linear; functions: add / iadd,
+    flatten.  Parameters are copied (conv OIHW -> KRSC, stem channels
+    padded to a multiple of 4).
+    """
+    import torch.fx
+
+    gm = torch.fx.symbolic_trace(model)
+    modules = dict(gm.named_modules())
+    n, c, h, w = example_input.shape
+    c_pad = (c + 3) // 4 * 4
+    ops: list[Op] = [Op(1, "input", (), (n, h, w, c_pad), {"channels": c}, name="input")]
+    where: dict[str, int] = {}
+    for node in gm.graph.nodes:
+        if node.op == "placeholder":
+            where[node.name] = 1
+            continue
+        if node.op == "output":
+            src = where[node.args[0].name]
+            break
+        if node.op == "call_module":
+            mod = modules[node.target]
+            src = where[node.args[0].name]
+            x = ops[src - 1]
+            nid = len(ops) + 1
+            if isinstance(mod, torch.nn.Conv2d):
+                if mod.groups != 1 or mod.bias is not None or _pair(mod.dilation) != 1:
+                    raise NotImplementedError(f"{node.target}: only dense bias-free convs")
+                r, s = mod.kernel_size
+                st, pd = _pair(mod.stride), _pair(mod.padding)
+                _, hh, ww, cin = x.shape
+                p = (hh + 2 * pd - r) // st + 1
+                q = (ww + 2 * pd - s) // st + 1
+                wt = mod.weight.detach().float().permute(0, 2, 3, 1).contiguous()  # KRSC
+                if wt.shape[3] != cin:
+                    wt = torch.nn.functional.pad(wt, (0, cin - wt.shape[3]))
+                ops.append(Op(nid, "conv", (src,), (n, p, q, mod.out_channels),
+                              {"r": r, "s": s, "stride": st, "pad": pd}, {"weight": wt}, node.target))
+            elif isinstance(mod, torch.nn.BatchNorm2d):
+                ops.append(Op(nid, "bn", (src,), x.shape, {"eps": mod.eps, "momentum": mod.momentum},
+                              {"weight": mod.weight.detach().float().clone(),
+                               "bias": mod.bias.detach().float().clone()},
+                              node.target))
+                ops[-1].attrs["running_mean"] = mod.running_mean.detach().float().clone()
+                ops[-1].attrs["running_var"] = mod.running_var.detach().float().clone()
+            elif isinstance(mod, torch.nn.ReLU):
+                ops.append(Op(nid, "relu", (src,), x.shape, name=node.target))
+            elif isinstance(mod, torch.nn.MaxPool2d):
+                r = _pair(mod.kernel_size)
+                st, pd = _pair(mod.stride), _pair(mod.padding)
+                _, hh, ww, cc = x.shape
+                p = (hh + 2 * pd - r) // st + 1
+                q = (ww + 2 * pd - r) // st + 1
+                ops.append(Op(nid, "maxpool", (src,), (n, p, q, cc),
+                              {"r": r, "s": r, "stride": st, "pad": pd}, name=node.target))
+            elif isinstance(mod, torch.nn.AdaptiveAvgPool2d):
+                ops.append(Op(nid, "avgpool", (src,), (n, x.shape[3]), name=node.target))
+            elif isinstance(mod, torch.nn.Linear):
+                ops.append(Op(nid, "fc", (src,), (n, mod.out_features), {},
+                              {"weight": mod.weight.detach().float().clone(),
+                               "bias": mod.bias.detach().float().clone()}, node.target))
+            else:
+                raise NotImplementedError(f"module {type(mod).__name__} at {node.target}")
+            where[node.name] = nid
+        elif node.op == "call_function":
+            if node.target in (operator.add, operator.iadd, torch.add):
+                a, b = (where[arg.name] for arg in node.args[:2])
+                nid = len(ops) + 1
+                ops.append(Op(nid, "add", tuple(sorted((a, b))), ops[a - 1].shape, name=node.name))
+                where[node.name] = nid
+            elif node.target is torch.flatten:
+                where[node.name] = where[node.args[0].name]  # avgpool already emits (N, C)
+            else:
+                raise NotImplementedError(f"function {node.target}")
+        elif node.op == "call_method" and node.target in ("flatten", "view", "reshape"):
+            where[node.name] = where[node.args[0].name]
+        else:
+            raise NotImplementedError(f"{node.op} {node.target}")
+    logits = ops[src - 1]
+    k = num_classes or logits.shape[1]
+    ops.append(Op(len(ops) + 1, "xent", (src,), (), name="loss"))
+    return Network(ops, n, k)
+
+
+def build_network(arch: str, batch: int, image: int | tuple = 224, num_classes: int = 1000,
+                  seed: int = 0) -> Network:
+    """torchvision ``arch`` with default init under ``torch.manual_seed(seed)``, traced."""
+    import torchvision
+
+    torch.manual_seed(seed)
+    model = getattr(torchvision.models, arch)(num_classes=num_classes)
+    hw = (image, image) if isinstance(image, int) else image
+    return trace_graph(model, torch.empty(batch, 3, *hw, device="meta"), num_classes)

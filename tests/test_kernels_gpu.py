@@ -1,0 +1,293 @@
+"""Numerics of every sm_100a kernel against a plain PyTorch reference of the same op.
+
+Floating-point ops are compared with a float64 CPU torch computation of the
+same formula; the tolerance is max|gpu - ref| / max|ref| <= 2e-5 for the
+3xTF32 tensor-core paths (fp32-level accuracy) and 1e-5 for fp32 CUDA-core
+ops.  Bit-level outputs (ReLU sign masks, maxpool indices) are exact.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+from paper_2010_14501_b200 import _native as N
+
+pytestmark = pytest.mark.gpu
+
+REL_TC = 2e-5     # 3xTF32 tensor-core conv / gemm
+REL_TF32 = 3e-3   # single-pass tf32 variant
+REL_EW = 1e-5     # CUDA-core fp32 kernels
+
+
+def rel_err(out, ref):
+    out = out.detach().double().cpu()
+    ref = ref.detach().double().cpu()
+    return (out - ref).abs().max().item() / max(ref.abs().max().item(), 1e-30)
+
+
+def stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def conv_ref(x, w, stride, pad):
+    # x NHWC, w KRSC -> y NHWC (float64 CPU)
+    y = F.conv2d(x.double().cpu().permute(0, 3, 1, 2), w.double().cpu().permute(0, 3, 1, 2),
+                 stride=stride, padding=pad)
+    return y.permute(0, 2, 3, 1)
+
+
+CONV_CASES = [
+    # n, h, w, c, k, r, s, stride, pad
+    (2, 8, 8, 64, 64, 1, 1, 1, 0),
+    (2, 9, 7, 32, 64, 3, 3, 1, 1),
+    (3, 14, 14, 64, 128, 3, 3, 2, 1),
+    (2, 15, 15, 128, 256, 1, 1, 2, 0),
+    (2, 32, 32, 4, 64, 7, 7, 2, 3),
+    (4, 7, 7, 256, 96, 3, 3, 1, 1),
+    (1, 5, 6, 8, 12, 3, 3, 1, 1),
+]
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+@pytest.mark.parametrize("variant", ["implicit", "splitk"])
+def test_conv_passes(cuda, case, variant):
+    n, h, w, c, k, r, s, stride, pad = case
+    g = torch.Generator().manual_seed(0)
+    x = torch.randn(n, h, w, c, generator=g)
+    wt = torch.randn(k, r, s, c, generator=g) / math.sqrt(r * s * c)
+    d = N.conv_desc(n, h, w, c, k, r, s, stride, pad)
+    lib = N.lib()
+    v = N.CONV_VARIANTS[variant]
+    xd, wd = x.to(cuda), wt.to(cuda)
+    y = torch.empty(n, d.p, d.q, k, device=cuda)
+    ws_f = lib.conv_ws_bytes(v, 0, d)
+    ws = torch.empty(max(ws_f, 4) // 4 + 1, device=cuda)
+    lib.conv_fwd(v, d, xd.data_ptr(), wd.data_ptr(), y.data_ptr(), ws.data_ptr(), ws_f, stream())
+    ref = conv_ref(x, wt, stride, pad)
+    assert rel_err(y, ref) < REL_TC
+
+    dy = torch.randn(n, d.p, d.q, k, generator=g)
+    dyd = dy.to(cuda)
+    ws_b = lib.conv_ws_bytes(v, 3, d)
+    ws = torch.empty(max(ws_b, 4) // 4 + 1, device=cuda)
+    dx = torch.full((n, h, w, c), 7.0, device=cuda)
+    lib.conv_dgrad(v, d, dyd.data_ptr(), wd.data_ptr(), dx.data_ptr(), 0, ws.data_ptr(), ws_b, stream())
+    xr = x.double().permute(0, 3, 1, 2).requires_grad_()
+    yr = F.conv2d(xr, wt.double().permute(0, 3, 1, 2), stride=stride, padding=pad)
+    yr.backward(dy.double().permute(0, 3, 1, 2))
+    assert rel_err(dx, xr.grad.permute(0, 2, 3, 1)) < REL_TC
+    # accumulate mode adds onto the existing gradient
+    lib.conv_dgrad(v, d, dyd.data_ptr(), wd.data_ptr(), dx.data_ptr(), 1, ws.data_ptr(), ws_b, stream())
+    assert rel_err(dx, 2 * xr.grad.permute(0, 2, 3, 1)) < REL_TC
+
+    dw = torch.empty(k, r, s, c, device=cuda)
+    lib.conv_wgrad(v, d, xd.data_ptr(), dyd.data_ptr(), dw.data_ptr(), 0, ws.data_ptr(), ws_b, stream())
+    wr = wt.double().permute(0, 3, 1, 2).requires_grad_()
+    yr = F.conv2d(x.double().permute(0, 3, 1, 2), wr, stride=stride, padding=pad)
+    yr.backward(dy.double().permute(0, 3, 1, 2))
+    assert rel_err(dw, wr.grad.permute(0, 2, 3, 1)) < REL_TC
+
+
+def test_conv_tf32_variant(cuda):
+    n, h, w, c, k, r, s, stride, pad = CONV_CASES[1]
+    g = torch.Generator().manual_seed(1)
+    x = torch.randn(n, h, w, c, generator=g)
+    wt = torch.randn(k, r, s, c, generator=g) / math.sqrt(r * s * c)
+    d = N.conv_desc(n, h, w, c, k, r, s, stride, pad)
+    y = torch.empty(n, d.p, d.q, k, device=cuda)
+    xd, wd = x.to(cuda), wt.to(cuda)  # keep the device copies alive while the kernel reads them
+    N.lib().conv_fwd(2, d, xd.data_ptr(), wd.data_ptr(), y.data_ptr(), None, 0, stream())
+    e = rel_err(y, conv_ref(x, wt, stride, pad))
+    assert 1e-7 < e < REL_TF32  # visibly less accurate than 3xTF32, still tf32-accurate
+
+
+@pytest.mark.parametrize("mnk", [(200, 1000, 2048), (128, 128, 32), (77, 36, 20), (300, 260, 1000)])
+@pytest.mark.parametrize("amn,bmn", [(0, 0), (0, 1), (1, 1), (1, 0)])
+def test_gemm_layouts(cuda, mnk, amn, bmn):
+    m, n, k = mnk
+    if (amn and m % 4) or (bmn and n % 4) or (not amn and k % 4) or (not bmn and k % 4):
+        pytest.skip("16B operand groups need the contiguous extent % 4 == 0")
+    g = torch.Generator().manual_seed(2)
+    A = torch.randn(m, k, generator=g)
+    B = torch.randn(n, k, generator=g)
+    a_store = A.t().contiguous() if amn else A
+    b_store = B.t().contiguous() if bmn else B
+    lda = m if amn else k
+    ldb = n if bmn else k
+    C = torch.zeros(m, n, device=cuda)
+    ad, bd = a_store.to(cuda), b_store.to(cuda)
+    for variant in (0, 1):
+        wsb = N.lib().gemm_ws_bytes(variant, m, n, k)
+        ws = torch.empty(wsb // 4 + 1, device=cuda)
+        N.lib().gemm(variant, ad.data_ptr(), amn, lda, bd.data_ptr(), bmn, ldb,
+                     C.data_ptr(), n, m, n, k, 0, ws.data_ptr(), wsb, stream())
+        assert rel_err(C, A.double() @ B.double().t()) < REL_TC
+
+
+def test_linear(cuda):
+    n, fi, fo = 24, 512, 1000
+    g = torch.Generator().manual_seed(3)
+    x, W, b = torch.randn(n, fi, generator=g), torch.randn(fo, fi, generator=g) * 0.05, torch.randn(fo, generator=g)
+    dy = torch.randn(n, fo, generator=g)
+    lib = N.lib()
+    xd, Wd, bd, dyd = (t.to(cuda) for t in (x, W, b, dy))
+    y = torch.empty(n, fo, device=cuda)
+    for variant in (0, 1):
+        wsb = max(lib.linear_ws_bytes(variant, 0, n, fi, fo), lib.linear_ws_bytes(variant, 3, n, fi, fo))
+        ws = torch.empty(wsb // 4 + 1, device=cuda)
+        lib.linear_fwd(variant, xd.data_ptr(), Wd.data_ptr(), bd.data_ptr(), y.data_ptr(), n, fi, fo,
+                       ws.data_ptr(), wsb, stream())
+        xr, Wr, br = (t.double().requires_grad_() for t in (x, W, b))
+        yr = F.linear(xr, Wr, br)
+        assert rel_err(y, yr) < REL_TC
+        yr.backward(dy.double())
+        dx, dW, db = torch.empty_like(xd), torch.empty_like(Wd), torch.empty_like(bd)
+        lib.linear_bwd(variant, xd.data_ptr(), Wd.data_ptr(), dyd.data_ptr(), dx.data_ptr(), 0, dW.data_ptr(),
+                       db.data_ptr(), n, fi, fo, ws.data_ptr(), wsb, stream())
+        assert rel_err(dx, xr.grad) < REL_TC
+        assert rel_err(dW, Wr.grad) < REL_TC
+        assert rel_err(db, br.grad) < REL_EW
+
+
+def pack_mask_np(x):
+    bits = (x.reshape(-1).numpy() > 0).astype(np.uint8)
+    pad = (-len(bits)) % 32
+    bits = np.concatenate([bits, np.zeros(pad, np.uint8)])
+    return np.packbits(bits.reshape(-1, 32)[:, ::-1], axis=1).view(">u4").reshape(-1).astype(np.uint32)
+
+
+@pytest.mark.parametrize("n", [1, 31, 32, 1000, 4099, 1 << 20])
+def test_relu_mask_exact(cuda, n):
+    g = torch.Generator().manual_seed(n)
+    x = torch.randn(n, generator=g)
+    x[::7] = 0.0
+    x[::11] = -0.0
+    if n > 20:
+        x[13] = float("nan")
+    lib = N.lib()
+    xd = x.to(cuda)
+    y = torch.empty_like(xd)
+    mask = torch.zeros((n + 31) // 32, dtype=torch.int32, device=cuda)
+    lib.relu_fwd(xd.data_ptr(), y.data_ptr(), mask.data_ptr(), n, stream())
+    ref_y = torch.where(x > 0, x, torch.zeros_like(x))
+    assert torch.equal(y.cpu(), ref_y)
+    assert np.array_equal(mask.cpu().numpy().view(np.uint32), pack_mask_np(x))
+    dy = torch.randn(n, generator=g)
+    dyd = dy.to(cuda)
+    ref_dx = torch.where(x > 0, dy, torch.zeros_like(dy))
+    for fn, src in (("relu_bwd_mask", mask), ("relu_bwd_out", y), ("relu_bwd_in", xd)):
+        dx = torch.empty_like(dyd)
+        getattr(lib, fn)(src.data_ptr(), dyd.data_ptr(), dx.data_ptr(), n, 0, stream())
+        assert torch.equal(dx.cpu(), ref_dx), fn
+        getattr(lib, fn)(src.data_ptr(), dyd.data_ptr(), dx.data_ptr(), n, 1, stream())
+        assert torch.equal(dx.cpu(), ref_dx + ref_dx), fn
+
+
+@pytest.mark.parametrize("shape", [(8, 16, 16, 64), (4, 7, 7, 2048), (3, 5, 5, 96), (2, 3, 3, 1024)])
+def test_batchnorm(cuda, shape):
+    n, h, w, c = shape
+    rows = n * h * w
+    g = torch.Generator().manual_seed(4)
+    x = torch.randn(n, h, w, c, generator=g) * 3 + 1.5
+    gamma = torch.rand(c, generator=g) + 0.5
+    beta = torch.randn(c, generator=g)
+    dy = torch.randn(n, h, w, c, generator=g)
+    lib = N.lib()
+    xd, gd, bd, dyd = (t.to(cuda) for t in (x, gamma, beta, dy))
+    y = torch.empty_like(xd)
+    mean, invstd = torch.empty(c, device=cuda), torch.empty(c, device=cuda)
+    rm, rv = torch.zeros(c, device=cuda), torch.ones(c, device=cuda)
+    scratch = torch.empty(lib.bn_scratch_bytes(rows, c) // 4 + 1, device=cuda)
+    lib.bn_fwd_train(xd.data_ptr(), y.data_ptr(), gd.data_ptr(), bd.data_ptr(), mean.data_ptr(), invstd.data_ptr(),
+                     rm.data_ptr(), rv.data_ptr(), rows, c, 1e-5, 0.1, 1, scratch.data_ptr(), stream())
+    xr = x.double().permute(0, 3, 1, 2).requires_grad_()
+    gr, br = gamma.double().requires_grad_(), beta.double().requires_grad_()
+    rmr, rvr = torch.zeros(c, dtype=torch.float64), torch.ones(c, dtype=torch.float64)
+    yr = F.batch_norm(xr, rmr, rvr, gr, br, training=True, momentum=0.1, eps=1e-5)
+    assert rel_err(y, yr.permute(0, 2, 3, 1)) < REL_EW
+    assert rel_err(rm, rmr) < REL_EW and rel_err(rv, rvr) < REL_EW
+    # replay with saved statistics is bit-identical and leaves running stats alone
+    y2 = torch.empty_like(y)
+    rm_before = rm.clone()
+    lib.bn_fwd_replay(xd.data_ptr(), y2.data_ptr(), gd.data_ptr(), bd.data_ptr(), mean.data_ptr(),
+                      invstd.data_ptr(), rows, c, stream())
+    assert torch.equal(y, y2) and torch.equal(rm, rm_before)
+    yr.backward(dy.double().permute(0, 3, 1, 2))
+    ref_dx = xr.grad.permute(0, 2, 3, 1)
+    for fn in ("bn_bwd_in", "bn_bwd_out"):
+        dx = torch.empty_like(xd)
+        dg, db = torch.empty(c, device=cuda), torch.empty(c, device=cuda)
+        if fn == "bn_bwd_in":
+            lib.bn_bwd_in(xd.data_ptr(), dyd.data_ptr(), dx.data_ptr(), 0, gd.data_ptr(), mean.data_ptr(),
+                          invstd.data_ptr(), dg.data_ptr(), db.data_ptr(), rows, c, scratch.data_ptr(), stream())
+            tol = REL_EW
+        else:
+            lib.bn_bwd_out(y.data_ptr(), dyd.data_ptr(), dx.data_ptr(), 0, gd.data_ptr(), bd.data_ptr(),
+                           invstd.data_ptr(), dg.data_ptr(), db.data_ptr(), rows, c, scratch.data_ptr(), stream())
+            tol = 2e-5  # xhat reconstructed from the output costs one extra rounding
+        assert rel_err(dx, ref_dx) < tol, fn
+        assert rel_err(dg, gr.grad) < tol, fn
+        assert rel_err(db, br.grad) < REL_EW, fn
+
+
+def test_maxpool_and_avgpool(cuda):
+    n, h, w, c = 3, 13, 12, 64
+    g = torch.Generator().manual_seed(5)
+    x = torch.randn(n, h, w, c, generator=g)
+    d = N.conv_desc(n, h, w, c, c, 3, 3, 2, 1)
+    lib = N.lib()
+    xd = x.to(cuda)
+    y = torch.empty(n, d.p, d.q, c, device=cuda)
+    idx = torch.empty(n, d.p, d.q, c, dtype=torch.uint8, device=cuda)
+    lib.maxpool_fwd(d, xd.data_ptr(), y.data_ptr(), idx.data_ptr(), stream())
+    xr = x.double().permute(0, 3, 1, 2).requires_grad_()
+    yr, ir = F.max_pool2d(xr, 3, 2, 1, return_indices=True)
+    assert torch.equal(y.cpu().double(), yr.permute(0, 2, 3, 1))
+    # 8-bit window index -> torch's flat input index
+    ii = idx.cpu().long().permute(0, 3, 1, 2)
+    pp = torch.arange(d.p).view(1, 1, -1, 1) * 2 - 1 + ii // 3
+    qq = torch.arange(d.q).view(1, 1, 1, -1) * 2 - 1 + ii % 3
+    assert torch.equal(pp * w + qq, ir)
+    dy = torch.randn(n, d.p, d.q, c, generator=g)
+    yr.backward(dy.double().permute(0, 3, 1, 2))
+    for use_idx in (True, False):
+        dx = torch.empty_like(xd)
+        lib.maxpool_bwd(d, idx.data_ptr() if use_idx else None, xd.data_ptr(), dy.to(cuda).data_ptr(),
+                        dx.data_ptr(), 0, stream())
+        assert rel_err(dx, xr.grad.permute(0, 2, 3, 1)) < REL_EW
+    ya = torch.empty(n, c, device=cuda)
+    lib.avgpool_fwd(xd.data_ptr(), ya.data_ptr(), n, h * w, c, stream())
+    assert rel_err(ya, x.double().mean(dim=(1, 2))) < REL_EW
+
+
+def test_xent_and_sgd(cuda):
+    n, k = 16, 1000
+    g = torch.Generator().manual_seed(6)
+    z = torch.randn(n, k, generator=g) * 3
+    lab = torch.randint(0, k, (n,), generator=g)
+    lib = N.lib()
+    zd, ld = z.to(cuda), lab.to(torch.int32).to(cuda)
+    loss = torch.empty(1, device=cuda)
+    scratch = torch.empty(n, device=cuda)
+    lib.xent_fwd(zd.data_ptr(), ld.data_ptr(), loss.data_ptr(), n, k, scratch.data_ptr(), stream())
+    zr = z.double().requires_grad_()
+    lr = F.cross_entropy(zr, lab)
+    assert abs(loss.item() - lr.item()) / abs(lr.item()) < REL_EW
+    lr.backward()
+    one = torch.ones(1, device=cuda)
+    dz = torch.empty_like(zd)
+    lib.xent_bwd(zd.data_ptr(), ld.data_ptr(), one.data_ptr(), dz.data_ptr(), n, k, 0, stream())
+    assert rel_err(dz, zr.grad) < REL_EW
+    w = torch.randn(1000, generator=g)
+    gr = torch.randn(1000, generator=g)
+    wd, gd, buf = w.to(cuda), gr.to(cuda), torch.zeros(1000, device=cuda)
+    ref = w.clone().requires_grad_()
+    opt = torch.optim.SGD([ref], lr=0.1, momentum=0.9, weight_decay=1e-4)
+    for step in range(3):
+        ref.grad = gr.clone()
+        opt.step()
+        lib.sgd_step(wd.data_ptr(), gd.data_ptr(), buf.data_ptr(), 1000, 0.1, 0.9, 1e-4, 1.0, int(step == 0),
+                     stream())
+    assert rel_err(wd, ref) < REL_EW
