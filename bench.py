@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""Benchmark: ResNet-50 (224x224, batch 184 per GPU) trained under a fixed
+per-GPU memory budget with a MONeT schedule, on 1..8 B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--budget-gib 8]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (data parallel)
+    python bench.py --impl reference ...                  (CPU oracle arm)
+
+One JSON line (rank 0).  ``value``: training images/s over all ranks with the
+batch resident in HBM; ``e2e``: the same through the public per-step call
+(Runtime.train_step) with the batch copied from pinned host memory and the
+loss read back every step.  ``roofline``: the dominant kernel (the tcgen05
+implicit-GEMM convolution) timed live with CUDA events; ``cpu_baseline``: the
+CPU oracle replay of the same kind of schedule on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "train imgs/s at fixed per-GPU memory budget"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--arch", default="resnet50")
+    ap.add_argument("--batch", type=int, default=184)
+    ap.add_argument("--image", type=int, default=224)
+    ap.add_argument("--budget-gib", type=float, default=8.0)
+    ap.add_argument("--no-graph", action="store_true", help="launch kernels from Python instead of a CUDA graph")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=8, help="images per CPU baseline step")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- helpers
+
+def load_or_plan(net, g, cat, budget, arch, batch, image, gib):
+    import hashlib
+
+    import paper_2010_14501_b200 as M
+    from paper_2010_14501_b200.planner import plan_schedule
+
+    path = ROOT / "schedules" / f"{arch}_b{batch}_{image}_{gib:g}gib.json"
+    digest = lambda d: hashlib.sha256(json.dumps(d, sort_keys=True).encode()).hexdigest()[:16]  # noqa: E731
+    if path.exists():
+        doc = json.loads(path.read_text())
+        if doc["graph_digest"] == digest(net.graph_doc()):
+            return M.schedule_from_doc(doc["schedule"]), doc.get("planner", {}), str(path.relative_to(ROOT))
+    sched, info = plan_schedule(g, cat, budget, kinds=net.storable_kinds())
+    if sched is None:
+        raise SystemExit(f"no schedule fits {gib} GiB")
+    return sched, info, "planned at startup"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        except OSError:
+            rows = []
+        rows = [[c.strip() for c in r] for r in rows if len(r) >= 7]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in rows for j in range(4) if r[3 + j].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())}
+
+
+def conv_flops(net, op):
+    x = net.op(op.deps[0])
+    return 2.0 * op.numel * x.shape[3] * op.attrs["r"] * op.attrs["s"]
+
+
+LOCAL_BYTES = {  # minimal fp32 HBM bytes per element
+    ("relu", "forward", True): 8.125, ("relu", "forward", False): 8.0, ("relu", "bwd-mask"): 8.125,
+    ("relu", "bwd-in"): 12.0, ("relu", "bwd-out"): 12.0, ("bn", "train"): 12.0, ("bn", "replay"): 8.0,
+    ("bn", "bwd"): 20.0, ("add", "forward"): 12.0, ("add", "bwd"): 16.0,
+}
+
+
+def kernel_roofline(rt, plan, net, peaks):
+    """Time every ledger step's launches with CUDA events (one extra, untimed step)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2010_14501_b200.engine import _cudart
+
+    stream = torch.cuda.current_stream()
+    sp = C.c_void_p(stream.cuda_stream)
+    cudart = _cudart()
+    evs = []
+    for group in plan.calls:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        rt._run_group(group, sp, cudart)
+        b.record(stream)
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    conv_t = conv_f = 0.0
+    local_t = local_b = 0.0
+    total_t = 0.0
+    n_conv = 0
+    for (a, b), s in zip(evs, plan.steps):
+        ms = a.elapsed_time(b)
+        total_t += ms
+        op = net.op(s.node)
+        if op.kind == "conv":
+            f = conv_flops(net, op)
+            if s.kind == "backward":
+                f *= 1 if net.op(op.deps[0]).kind == "input" else 2
+            conv_t += ms
+            conv_f += f
+            n_conv += 1
+        elif op.kind in ("relu", "bn", "add"):
+            if s.kind == "backward":
+                key = (op.kind, "bwd") if op.kind != "relu" else ("relu", s.impl)
+            elif op.kind == "bn":
+                key = ("bn", "train" if s.kind == "forward" else "replay")
+            elif op.kind == "relu":
+                key = ("relu", "forward", net.intermediate_of[op.id] in s.planned_ints)
+            else:
+                key = ("add", "forward")
+            local_t += ms
+            local_b += LOCAL_BYTES[key] * op.numel
+    opt = evs[-1]
+    total_t += opt[0].elapsed_time(opt[1])
+    tf32_peak = peaks.get("bf16_tflops_sustained", 1437.7) / 2.0
+    achieved = conv_f / (conv_t * 1e-3) / 1e12
+    roof = {"bound": "tensor", "kernel": "gemm_tf32_kernel (implicit-GEMM conv, 3xTF32)",
+            "achieved": round(achieved, 1), "peak": round(tf32_peak, 1), "unit": "TFLOP/s",
+            "frac": round(achieved / tf32_peak, 4),
+            "peak_basis": "dense TF32 = 1/2 x measured bf16_tflops_sustained (MEASURED_PEAKS.json)",
+            "flops_per_step": conv_f, "conv_ms_per_step": round(conv_t, 3), "conv_share_of_step": round(conv_t / total_t, 3),
+            "conv_launch_groups": n_conv, "note": "3xTF32 issues 3 tensor-core MMAs per useful MMA; achieved counts "
+                                                  "algorithmic 2*N*K*P*Q*C*R*S flops only"}
+    hbm = peaks.get("hbm_gbs", 6452.5)
+    local = {"bound": "hbm", "achieved": round(local_b / (local_t * 1e-3) / 1e9, 1), "peak": hbm, "unit": "GB/s",
+             "frac": round(local_b / (local_t * 1e-3) / 1e9 / hbm, 4), "ms_per_step": round(local_t, 3),
+             "share_of_step": round(local_t / total_t, 3), "kernels": "relu/bn/add (SURVEY §8d algorithmic bytes)"}
+    return roof, local, total_t
+
+
+def cpu_baseline_run(args, budget_frac, steps=2):
+    """The CPU oracle replaying a schedule of the same kind on a bounded sample."""
+    import torch
+
+    import paper_2010_14501_b200 as M
+    from oracle.cpu_executor import CpuState, run_step
+    from paper_2010_14501_b200.planner import plan_schedule
+    from paper_2010_14501_b200.tracer import build_network
+
+    torch.set_num_threads(os.cpu_count() or 1)
+    n = args.cpu_sample
+    net = build_network(args.arch, n, args.image)
+    g = M.load_graph(net.graph_doc())
+    cat = M.load_catalog(net.catalog_doc(), g)
+    se_peak = M.simulate(M.store_everything_schedule(g, cat), g, cat).peak_memory
+    budget = g.params_bytes + int(budget_frac * (se_peak - g.params_bytes))
+    sched, info = plan_schedule(g, cat, budget, kinds=net.storable_kinds())
+    if sched is None:
+        sched = M.store_everything_schedule(g, cat)
+    doc = M.schedule_to_doc(sched)
+    gen = torch.Generator().manual_seed(0)
+    x = torch.randn(n, 3, args.image, args.image, generator=gen)
+    y = torch.randint(0, 1000, (n,), generator=gen)
+    st = CpuState(net)
+    run_step(st, doc, x, y)  # warm-up
+    t = time.perf_counter()
+    for _ in range(steps):
+        run_step(st, doc, x, y)
+    dt = (time.perf_counter() - t) / steps
+    return {"value": round(n / dt, 3), "unit": "img/s", "cores": torch.get_num_threads(), "kind": "port",
+            "sample": f"{args.arch} batch {n} at {args.image}x{args.image}, one scheduled training step "
+                      f"(budget fraction {budget_frac:.3f} of its store-everything activations), "
+                      f"torch CPU fp32 oracle replay, mean of {steps} steps after 1 warm-up"}
+
+
+# --------------------------------------------------------------------------- arms
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+
+    base = 26.55 * (1 << 30)  # ResNet-50 b184 store-everything ledger peak (for the budget fraction)
+    frac = max(0.05, min(1.0, (args.budget_gib * (1 << 30)) / base))
+    steps = max(1, args.steps)
+    res = cpu_baseline_run(args, frac, steps=min(steps, 3))
+    out = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": "img/s", "n_gpus": args.gpus,
+           "steps": min(steps, 3), "warmup": 1, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f32", "data": "synthetic",
+           "config": {"workload": f"{args.arch} {args.image}x{args.image} scheduled training step under a "
+                                  f"{args.budget_gib:g} GiB-equivalent budget fraction, CPU sample batch "
+                                  f"{args.cpu_sample}", "parallelism": "host cores"},
+           "cpu_baseline": res, "e2e": {"value": res["value"], "unit": "img/s", "h2d_bytes_per_step": 0,
+                                        "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def ours_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2010_14501_b200 as M
+    from paper_2010_14501_b200.engine import Runtime
+    from paper_2010_14501_b200.tracer import build_network
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    peaks = {}
+    pk = ROOT / "MEASURED_PEAKS.json"
+    if pk.exists():
+        peaks = json.loads(pk.read_text())
+
+    gib = args.budget_gib
+    budget = int(gib * (1 << 30))
+    net = build_network(args.arch, args.batch, args.image)
+    gdoc = net.graph_doc()
+    g = M.load_graph(gdoc)
+    cat = M.load_catalog(net.catalog_doc(), g)
+    sched, pinfo, source = load_or_plan(net, g, cat, budget, args.arch, args.batch, args.image, gib)
+    se = M.store_everything_schedule(g, cat)
+
+    rt = Runtime(net, device=dev, budget_bytes=budget)
+    if world > 1:
+        from paper_2010_14501_b200.dp import DataParallel
+        DataParallel(rt)
+    plan = rt.plan(sched, g, cat)
+
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    x = torch.randn(args.batch, 3, args.image, args.image, device=dev, generator=gen)
+    y = torch.randint(0, 1000, (args.batch,), device=dev, generator=gen)
+    rt.set_batch(x, y)
+    del x
+    torch.cuda.synchronize()
+
+    graph = None
+    use_graph = not args.no_graph and world == 1
+    if use_graph:
+        graph = rt.capture(plan)
+
+    def step():
+        if graph is not None:
+            graph.replay()
+        else:
+            rt.run(plan)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats(dev)
+
+    sampler = ClockSampler(local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = world * args.batch / (ms * 1e-3)
+    loss = rt.loss_value()
+    torch_peak = torch.cuda.max_memory_allocated(dev)
+
+    # ---- end to end: pinned host batch in, loss out, through Runtime.train_step
+    c_pad = net.ops[0].shape[3]
+    host = torch.zeros(args.batch, args.image, args.image, c_pad, pin_memory=True)
+    host[..., :3].normal_()
+    host_y = torch.randint(0, 1000, (args.batch,), dtype=torch.int32).pin_memory()
+    loss_host = torch.empty(1, pin_memory=True)
+    for _ in range(2):
+        rt.train_step(plan, host, host_y)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(args.steps):
+        lt = rt.train_step(plan, host, host_y)
+        loss_host.copy_(lt, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    b.record()
+    torch.cuda.synchronize()
+    e2e_ms = a.elapsed_time(b) / args.steps
+    t = torch.tensor([e2e_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+
+    # ---- roofline of the dominant kernel (one extra instrumented step)
+    roof, local_roof, instr_ms = kernel_roofline(rt, plan, net, peaks)
+
+    # ---- overhead vs the no-recompute schedule on the same kernels (analytic costs)
+    overhead_model = float(plan.trace.total_cost / M.simulate(se, g, cat).total_cost - 1)
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline:
+            frac = (budget - g.params_bytes) / (M.simulate(se, g, cat).peak_memory - g.params_bytes)
+            try:
+                cpu = cpu_baseline_run(args, frac)
+            except Exception as exc:  # keep the GPU line even if the host run fails
+                cpu = {"value": None, "error": str(exc)[:200]}
+        n_rec = sum(sum(1 for u, impl in s.recompute if impl is not None) for s in sched.stages)
+        out = {
+            "metric": METRIC, "value": round(value, 2), "unit": "img/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": round(ms, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 (3xTF32 tensor-core convs)",
+            "data": "synthetic N(0,1) images, uniform labels; random-init torchvision weights (seed 0)",
+            "config": {"workload": f"{args.arch} {args.image}x{args.image} batch {args.batch}/GPU, "
+                                   f"{gib:g} GiB per-GPU budget, MONeT schedule ({source})",
+                       "model": args.arch, "global_batch": world * args.batch, "per_gpu_batch": args.batch,
+                       "image": args.image, "budget_bytes": budget, "parallelism": f"dp{world}",
+                       "cuda_graph": use_graph,
+                       "l2": "inputs larger than L2 (activations ~26 GB per step); no explicit flush"},
+            "memory": {"ledger_peak_bytes": plan.ledger_peak, "ilp_bound_bytes": plan.bound_peak,
+                       "physical_peak_bytes": g.params_bytes + plan.arena_bytes,
+                       "params_bytes": g.params_bytes, "arena_bytes": plan.arena_bytes,
+                       "torch_max_allocated_bytes": torch_peak,
+                       "within_bound": g.params_bytes + plan.arena_bytes <= (plan.bound_peak or 0) + (1 << 20),
+                       "store_everything_ledger_peak_bytes": M.simulate(se, g, cat).peak_memory},
+            "overhead": {"modeled_pct": round(100 * overhead_model, 2), "recomputes": n_rec,
+                         "planner": pinfo},
+            "e2e": {"value": round(world * args.batch / (e2e_ms * 1e-3), 2), "unit": "img/s",
+                    "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": host.numel() * 4 + args.batch * 4,
+                    "d2h_bytes_per_step": 4, "api": "Runtime.train_step(plan, pinned host batch) + loss D2H"},
+            "gpu_launches": plan.launches * args.steps,
+            "roofline": roof, "roofline_local_ops": local_roof,
+            "cpu_baseline": cpu,
+            "clocks": sampler.summary(), "loss": loss,
+        }
+        tr = ROOT / "profiles" / "traffic.json"
+        if tr.exists():
+            roof["traffic"] = json.loads(tr.read_text()).get("gemm_bytes_per_launch")
+        else:
+            roof["traffic"] = None
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        ours_arm(args)
+
+
+if __name__ == "__main__":
+    main()

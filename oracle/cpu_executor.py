@@ -59,8 +59,18 @@ def _bn_apply(x, mean, invstd, g, b):
     return (x - v(mean)) * v(invstd) * v(g) + v(b)
 
 
-def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torch.Tensor):
-    """One training step following ``schedule`` (a schedule document). Returns the loss."""
+def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torch.Tensor, record=None,
+             forced=None, fwd_record=None):
+    """One training step following ``schedule`` (a schedule document). Returns the loss.
+
+    ``forced`` (node id -> NCHW tensor) substitutes the given forward outputs
+    for the oracle's own (first forward and every recompute alike).  Parity
+    tests use it to feed the GPU's activations so that ReLU/maxpool
+    derivatives, which are discontinuous, are evaluated on the same inputs on
+    both sides (SURVEY.md §8c); ``record`` collects input gradients per stage;
+    ``fwd_record`` collects the oracle's own forward outputs (computed from the
+    possibly forced inputs) before any substitution.
+    """
     net = state.net
     dt = state.dtype
     P = state.params
@@ -81,6 +91,14 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
         return act[i]
 
     def fwd(op, mode, want_int):
+        y, extra = _fwd(op, mode, want_int)
+        if fwd_record is not None and mode == "forward":
+            fwd_record[op.id] = y
+        if forced is not None and op.id in forced and op.kind != "xent":
+            y = forced[op.id].to(dt)
+        return y, extra
+
+    def _fwd(op, mode, want_int):
         nonlocal loss_val
         xs = [x_of(j) for j in op.deps]
         extra = None
@@ -260,6 +278,8 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
             if j not in grad:
                 created.add(j)
         bwd(net.op(k), impl_b, created)
+        if record is not None:
+            record[t] = {j: grad[j].clone() for j in net.op(k).deps if j in grad}
         grad.pop(k, None)
         release(len(entries))
         carried = keep

@@ -71,11 +71,16 @@ int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_b
   return last_error();
 }
 
-Operand op_kmajor(const float* ptr, int rows, long long ld) {
-  return Operand{OP_KMAJOR, rows, ptr, ld, 1 << 30, 0};
+bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+Operand op_kmajor(const float* ptr, int rows, long long ld, int kd) {
+  return Operand{OP_KMAJOR, rows, ptr, ld, 1 << 30, 0, (al16(ptr) && ld % 4 == 0 && kd % 4 == 0) ? 1 : 0};
 }
 Operand op_mnmajor(const float* ptr, int rows, long long ld) {
-  return Operand{OP_MNMAJOR, rows, ptr, ld, 1 << 30, 0};
+  return Operand{OP_MNMAJOR, rows, ptr, ld, 1 << 30, 0, (al16(ptr) && ld % 4 == 0 && rows % 4 == 0) ? 1 : 0};
+}
+Operand op_gather(int mode, const float* ptr, int rows) {
+  return Operand{mode, rows, ptr, 0, 1 << 30, 0, 1};  // conv gathers: C, K % 4 == 0 checked by check_desc
 }
 
 ConvGeom geom(const monet_conv_desc* d) {
@@ -94,17 +99,17 @@ GemmParams conv_params(int pass, const monet_conv_desc* d, const float* in0, con
     p.M = d->n * d->p * d->q;
     p.N = d->k;
     p.Kd = rsc;
-    p.a = is_pointwise(d) ? op_kmajor(in0, p.M, d->c) : Operand{OP_IM2COL_FPROP, p.M, in0, 0, 1 << 30, 0};
-    p.b = op_kmajor(in1, d->k, rsc);
+    p.a = is_pointwise(d) ? op_kmajor(in0, p.M, d->c, p.Kd) : op_gather(OP_IM2COL_FPROP, in0, p.M);
+    p.b = op_kmajor(in1, d->k, rsc, p.Kd);
     p.c = out;
     p.ldc = d->k;
   } else if (pass == MONET_PASS_DGRAD) {  // in0 = dy, in1 = w
     p.M = d->n * d->h * d->w;
     p.N = d->c;
     p.Kd = d->r * d->s * d->k;
-    p.a = is_pointwise(d) ? op_kmajor(in0, p.M, d->k) : Operand{OP_IM2COL_DGRAD, p.M, in0, 0, 1 << 30, 0};
+    p.a = is_pointwise(d) ? op_kmajor(in0, p.M, d->k, p.Kd) : op_gather(OP_IM2COL_DGRAD, in0, p.M);
     // B[c, (tap, kout)] = w[kout, tap, c]
-    p.b = Operand{OP_MNMAJOR, d->c, in1, (long long)rsc, d->k, (long long)d->c};
+    p.b = Operand{OP_MNMAJOR, d->c, in1, (long long)rsc, d->k, (long long)d->c, al16(in1) ? 1 : 0};
     p.c = out;
     p.ldc = d->c;
   } else {  // wgrad: in0 = x, in1 = dy
@@ -112,7 +117,7 @@ GemmParams conv_params(int pass, const monet_conv_desc* d, const float* in0, con
     p.N = rsc;
     p.Kd = d->n * d->p * d->q;
     p.a = op_mnmajor(in1, d->k, d->k);  // A[kout, pix] = dy[pix, kout]
-    p.b = is_pointwise(d) ? op_mnmajor(in0, d->c, d->c) : Operand{OP_IM2COL_WGRAD, rsc, in0, 0, 1 << 30, 0};
+    p.b = is_pointwise(d) ? op_mnmajor(in0, d->c, d->c) : op_gather(OP_IM2COL_WGRAD, in0, rsc);
     p.c = out;
     p.ldc = rsc;
   }
@@ -180,8 +185,8 @@ int monet_linear_fwd(int variant, const float* x, const float* w, const float* b
   p.M = n;
   p.N = out_f;
   p.Kd = in_f;
-  p.a = op_kmajor(x, n, in_f);
-  p.b = op_kmajor(w, out_f, in_f);
+  p.a = op_kmajor(x, n, in_f, in_f);
+  p.b = op_kmajor(w, out_f, in_f, in_f);
   p.c = y;
   p.ldc = out_f;
   return launch_gemm(p, variant, 1, ws, ws_bytes, st);
@@ -195,7 +200,7 @@ int monet_linear_bwd(int variant, const float* x, const float* w, const float* d
     p.M = n;
     p.N = in_f;
     p.Kd = out_f;
-    p.a = op_kmajor(dy, n, out_f);
+    p.a = op_kmajor(dy, n, out_f, out_f);
     p.b = op_mnmajor(w, in_f, in_f);  // B[i, o] = W[o, i]
     p.c = dx;
     p.ldc = in_f;
@@ -223,8 +228,8 @@ int monet_gemm(int variant, const float* a, int a_mn, int64_t lda, const float* 
   p.M = m;
   p.N = n;
   p.Kd = k;
-  p.a = a_mn ? op_mnmajor(a, m, lda) : op_kmajor(a, m, lda);
-  p.b = b_mn ? op_mnmajor(b, n, ldb) : op_kmajor(b, n, ldb);
+  p.a = a_mn ? op_mnmajor(a, m, lda) : op_kmajor(a, m, lda, k);
+  p.b = b_mn ? op_mnmajor(b, n, ldb) : op_kmajor(b, n, ldb, k);
   p.c = c;
   p.ldc = ldc;
   return launch_gemm(p, variant, accumulate, ws, ws_bytes, S(stream));

@@ -37,7 +37,17 @@ struct Operand {
   long long ld;
   int kdiv;
   long long ks1;
+  int aligned;  // 16B groups are aligned and never straddle an edge (host-checked)
 };
+
+// Scalar fallback for operands whose 16B groups are misaligned or ragged:
+// element e of the group sits at base + e*step and exists iff e < count.
+MONET_DEV float4 load4_scalar(const float* base, long long step, int count) {
+  float v[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) v[e] = e < count ? __ldg(base + e * step) : 0.f;
+  return make_float4(v[0], v[1], v[2], v[3]);
+}
 
 enum EpiMode : int { EPI_STORE = 0, EPI_ACCUM = 1, EPI_PARTIAL = 2 };
 
@@ -62,6 +72,11 @@ constexpr int kStageBytes = 4 * kTileBytes;  // A_hi, A_lo, B_hi, B_lo
 constexpr int kProducerWarps = 4, kEpilogueWarps = 4;
 constexpr int kThreads = (kProducerWarps + kEpilogueWarps + 1) * 32;
 constexpr int kAccStages = 2;
+// TMEM accumulation is flushed to the fp32 output every kChunk k-blocks: the
+// tensor core's accumulator does not round-to-nearest, so very long single
+// accumulation chains (wgrad reduces over up to 577k pixels) drift; chunk
+// partial sums are combined in the epilogue with ordinary fp32 adds.
+constexpr int kChunk = 16;
 constexpr int kTmemCols = kAccStages * BN;  // 256
 constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 
@@ -115,6 +130,7 @@ MONET_DEV float4 fetch_kmajor(const GemmParams& p, const Operand& op, const KRow
   if (!((st.valid >> i) & 1) || k >= p.Kd) return z;
   const ConvGeom& g = p.g;
   if (op.mode == OP_KMAJOR) {
+    if (!op.aligned) return load4_scalar(op.ptr + st.base[i] + k, 1, min(4, p.Kd - k));
     return __ldg(reinterpret_cast<const float4*>(op.ptr + st.base[i] + k));
   } else if (op.mode == OP_IM2COL_FPROP) {
     int h = st.hb[i] + tap_r, w = st.wb[i] + tap_s;
@@ -183,7 +199,9 @@ MONET_DEV float4 fetch_mnmajor(const GemmParams& p, const Operand& op, const MRo
   if (!st.gvalid || k >= p.Kd) return z;
   if (op.mode == OP_MNMAJOR) {
     int kh = k / op.kdiv, kl = k - kh * op.kdiv;
-    return __ldg(reinterpret_cast<const float4*>(op.ptr + kh * op.ks1 + (long long)kl * op.ld + st.gbase));
+    const float* src = op.ptr + kh * op.ks1 + (long long)kl * op.ld + st.gbase;
+    if (!op.aligned) return load4_scalar(src, 1, min(4, op.rows - (int)st.gbase));
+    return __ldg(reinterpret_cast<const float4*>(src));
   }
   const ConvGeom& g = p.g;
   int h = st.kp[i] * g.sh - g.ph + st.tap_r;
@@ -354,8 +372,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32_kernel(const GemmParams
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < n_tiles_total; tile += gridDim.x) {
-      int mt, nt, sp;
+      int mt, nt, sp, kb0, kb1;
       tile_coords(p, tile, mt, nt, sp);
+      kb_range(p, sp, kb0, kb1);
+      const int nchunks = (kb1 - kb0 + kChunk - 1) / kChunk;
+      for (int chunk = 0; chunk < nchunks; ++chunk) {
+      const bool add_old = chunk > 0 || p.epi == EPI_ACCUM;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const int m = mt * BM + quarter * 32 + lane;
@@ -379,7 +401,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32_kernel(const GemmParams
 #pragma unroll
             for (int j = 0; j < 32; j += 4) {
               float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-              if (p.epi == EPI_ACCUM) {
+              if (add_old) {
                 float4 c = *reinterpret_cast<const float4*>(dst + j);
                 o.x += c.x;
                 o.y += c.y;
@@ -393,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32_kernel(const GemmParams
             for (int j = 0; j < 32; ++j) {
               if (j < ncols) {
                 float o = v[j];
-                if (p.epi == EPI_ACCUM) o += dst[j];
+                if (add_old) o += dst[j];
                 dst[j] = o;
               }
             }
@@ -407,6 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32_kernel(const GemmParams
         acc = 0;
         acc_phase ^= 1;
       }
+      }  // chunk
     }
   } else {
     // ------------------------------------------------------------ MMA issuer
@@ -419,10 +442,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32_kernel(const GemmParams
       int mt, nt, sp, kb0, kb1;
       tile_coords(p, tile, mt, nt, sp);
       kb_range(p, sp, kb0, kb1);
+      for (int c0 = kb0; c0 < kb1; c0 += kChunk) {
+      const int c1 = min(kb1, c0 + kChunk);
       mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = kb0; kb < kb1; ++kb) {
+      for (int kb = c0; kb < c1; ++kb) {
         mbar_wait(&full_bar[stage], phase);
         tc_fence_after();
         if (lane == 0) {
@@ -431,7 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32_kernel(const GemmParams
           const uint32_t b_hi = base + 2 * kTileBytes, b_lo = base + 3 * kTileBytes;
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint32_t first = (kb == kb0 && kk == 0) ? 0u : 1u;
+            const uint32_t first = (kb == c0 && kk == 0) ? 0u : 1u;
             if (p.split_tf32) {
               mma_tf32(d_tmem, operand_desc(a_lo, a_mn, kk), operand_desc(b_hi, b_mn, kk), idesc, first);
               mma_tf32(d_tmem, operand_desc(a_hi, a_mn, kk), operand_desc(b_lo, b_mn, kk), idesc, 1u);
@@ -441,7 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32_kernel(const GemmParams
             }
           }
           mma_commit(&empty_bar[stage]);
-          if (kb == kb1 - 1) mma_commit(&tfull_bar[acc]);
+          if (kb == c1 - 1) mma_commit(&tfull_bar[acc]);
         }
         __syncwarp();
         if (++stage == kStages) {
@@ -453,6 +478,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32_kernel(const GemmParams
         acc = 0;
         acc_phase ^= 1;
       }
+      }  // chunk
     }
   }
 

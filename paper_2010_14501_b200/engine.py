@@ -33,7 +33,7 @@ from .costmodel import Catalog
 from .graph import Graph, compute_dependency_sets
 from .schedule import Schedule, SimulationError, Trace, ledger, validate
 
-__all__ = ["Runtime", "Plan", "ExecResult", "BudgetExceeded", "execute"]
+__all__ = ["Runtime", "Plan", "ExecResult", "BudgetExceeded", "execute", "lifetimes", "place_blocks"]
 
 ALIGN = 256
 
@@ -155,6 +155,43 @@ class Runtime:
     def loss_value(self) -> float:
         return float(self.consts[1].item())
 
+    def loss_tensor(self) -> torch.Tensor:
+        """The last step's loss as a 1-element device tensor (no host sync)."""
+        return self.consts[1:2]
+
+    def train_step(self, plan: "Plan", images: torch.Tensor | None = None,
+                   labels: torch.Tensor | None = None) -> torch.Tensor:
+        """Public per-step call: stage the batch (host or device, NCHW or engine NHWC
+        layout), run the scheduled forward/backward/SGD, return the device loss."""
+        if images is not None:
+            if images.dim() == 4 and images.shape[1] in (1, 2, 3) and images.shape[-1] not in (1, 2, 3, 4):
+                self.set_batch(images, labels)
+            else:
+                self.set_batch_nhwc(images, labels)
+        if getattr(plan, "graph", None) is not None:
+            plan.graph.replay()
+        else:
+            self.run(plan)
+        return self.loss_tensor()
+
+    def capture(self, plan: "Plan"):
+        """Capture the whole training step into a CUDA graph (plan.graph); the
+        kernels' device pointers are static because the arena is planned."""
+        if self.comm is not None:
+            raise RuntimeError("CUDA-graph capture with a Python-side collective is not supported")
+        self.run(plan)  # first launches set kernel attributes outside capture
+        torch.cuda.synchronize(self.device)
+        graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(graph, stream=side):
+                self.run(plan)
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        torch.cuda.synchronize(self.device)
+        plan.graph = graph
+        return graph
+
     # ------------------------------------------------------------ planning
     def plan(self, schedule: Schedule, g: Graph, catalog: Catalog, check_bound: bool = True) -> Plan:
         key = id(schedule)
@@ -165,8 +202,9 @@ class Runtime:
         if tags:
             raise SimulationError(f"schedule is not executable: {tags}")
         steps, trace = ledger(schedule, g, catalog)
-        blocks, step_blocks = self._lifetimes(steps, g)
-        arena_bytes, offsets = self._place(blocks)
+        blocks, step_blocks = lifetimes(steps, g)
+        cap = 0 if self.budget_bytes is None else max(1, self.budget_bytes - self.params_bytes)
+        arena_bytes, offsets = place_blocks(blocks, cap)
         fixed_peak = self.params_bytes + arena_bytes
         if self.budget_bytes is not None and fixed_peak > self.budget_bytes:
             raise BudgetExceeded(f"planned footprint {fixed_peak} B exceeds budget {self.budget_bytes} B "
@@ -180,13 +218,15 @@ class Runtime:
             ok, bound, _ = check_schedule(g, compute_dependency_sets(g), catalog, schedule,
                                           self.budget_bytes if self.budget_bytes else 1 << 62)
         base = self.arena.data_ptr()
-        calls = []
+        calls, step_ptrs = [], []
         for s, sb in zip(steps, step_blocks):
             ptrs = {k: base + offsets[b] for k, b in sb["blocks"].items()}
-            calls.extend(self._bind(s, sb, ptrs, catalog))
-        calls.extend(self._bind_optimizer())
+            calls.append(self._bind(s, sb, ptrs, catalog))
+            step_ptrs.append(ptrs)
+        calls.append(self._bind_optimizer())
         plan = Plan(schedule, trace, calls, arena_bytes, trace.peak_memory, bound, len(blocks),
-                    sum(1 for c in calls if c[0] == "k"))
+                    sum(1 for group in calls for c in group if c[0] == "k"))
+        plan.steps, plan.step_ptrs = steps, step_ptrs
         self._plans[key] = plan
         return plan
 
@@ -197,83 +237,6 @@ class Runtime:
         if g.params_bytes != self.params_bytes:
             raise ValueError(f"graph params_bytes {g.params_bytes} != runtime fixed region "
                              f"{self.params_bytes}")
-
-    def _lifetimes(self, steps, g: Graph):
-        """Blocks [t_alloc, t_free) in half-step units and the blocks each step touches."""
-        sizes_of = {u.id: u.nbytes for u in g.storables}
-        live: dict[tuple, int] = {}
-        blocks: list[list[int]] = []  # [size, t_alloc, t_free]
-        per_step = []
-
-        def new_block(size, t):
-            blocks.append([size, t, None])
-            return len(blocks) - 1
-
-        def end(key, t):
-            b = live.pop(key)
-            blocks[b][2] = t
-
-        for s_idx, s in enumerate(steps):
-            t0, t1 = 2 * s_idx, 2 * s_idx + 1
-            for key in s.drops:
-                end(key, t0)
-            touched = {}
-            # inputs read by the step (resolved before allocations; in-place takes one over)
-            if s.kind in ("forward", "recompute"):
-                for j in g.deps(s.node):
-                    touched[("in", j)] = live[("a", j)]
-            else:
-                for d in s.variant.deps:
-                    touched[("in", d)] = live[("a", d)]
-                for j in g.deps(s.node):
-                    if ("a", j) in live:
-                        touched[("in", j)] = live[("a", j)]
-                if s.node in g.backward_by_node and ("a", s.node) in live:
-                    touched[("in", s.node)] = live[("a", s.node)]
-            for key in s.allocs:
-                if key[0] == "a":
-                    if s.inplace_from is not None and key[1] == s.node:
-                        b = live.pop(("a", s.inplace_from))
-                        live[key] = b
-                    else:
-                        live[key] = new_block(sizes_of[key[1]], t0)
-                else:
-                    live[key] = new_block(g.grad_bytes(key[1]), t0)
-                touched[key] = live[key]
-            if s.kind == "backward":
-                touched[("g", s.node)] = live[("g", s.node)]
-                for j in g.deps(s.node):
-                    if ("g", j) in live:
-                        touched[("g", j)] = live[("g", j)]
-            if s.workspace:
-                touched[("ws",)] = new_block(s.workspace, t0)
-                blocks[touched[("ws",)]][2] = t1
-            for key in s.frees:
-                end(key, t1)
-            per_step.append({"blocks": touched})
-        for key in list(live):
-            end(key, 2 * len(steps))
-        return blocks, per_step
-
-    def _place(self, blocks):
-        n = len(blocks)
-        arr = lambda vals: (C.c_int64 * max(n, 1))(*vals)
-        sizes = arr([b[0] for b in blocks])
-        ta = arr([b[1] for b in blocks])
-        tf = arr([b[2] for b in blocks])
-        offs = (C.c_int64 * max(n, 1))()
-        peak = C.c_int64(0)
-        cap = 0
-        if self.budget_bytes is not None:
-            cap = max(0, self.budget_bytes - self.params_bytes)
-        rc = self.lib.dll.monet_arena_plan(n, C.cast(sizes, C.c_void_p), C.cast(ta, C.c_void_p),
-                                           C.cast(tf, C.c_void_p), ALIGN, cap, C.cast(offs, C.c_void_p),
-                                           C.byref(peak))
-        if rc == -12:
-            raise BudgetExceeded(f"arena plan needs {peak.value} B, only {cap} B left under the budget")
-        if rc:
-            raise RuntimeError(f"arena planner failed ({rc})")
-        return peak.value, list(offs)[:n]
 
     # ------------------------------------------------------------ binding
     def _bind(self, s, sb, ptrs, catalog):
@@ -422,12 +385,21 @@ class Runtime:
         return calls
 
     # ------------------------------------------------------------ running
-    def run(self, plan: Plan):
-        """Enqueue one training step (forward, scheduled backward, SGD) on the current stream."""
+    def run(self, plan: Plan, after_step=None):
+        """Enqueue one training step (forward, scheduled backward, SGD) on the current stream.
+
+        ``after_step(i)`` (debugging) is called after ledger step i is enqueued.
+        """
         stream = torch.cuda.current_stream(self.device)
         sp = C.c_void_p(stream.cuda_stream)
         cudart = _cudart()
-        for c in plan.calls:
+        for i, group in enumerate(plan.calls):
+            self._run_group(group, sp, cudart)
+            if after_step is not None and i < len(plan.calls) - 1:
+                after_step(i)
+
+    def _run_group(self, group, sp, cudart):
+        for c in group:
             kind = c[0]
             if kind == "k":
                 fn, args = c[1], c[2]
@@ -440,6 +412,83 @@ class Runtime:
                     raise _native.NativeError(f"cudaMemcpyAsync failed ({rc})")
             else:
                 c[1]()
+
+
+def lifetimes(steps, g: Graph):
+    """Blocks [t_alloc, t_free) in half-step units and the blocks each step touches."""
+    sizes_of = {u.id: u.nbytes for u in g.storables}
+    live: dict[tuple, int] = {}
+    blocks: list[list[int]] = []  # [size, t_alloc, t_free]
+    per_step = []
+
+    def new_block(size, t):
+        blocks.append([size, t, None])
+        return len(blocks) - 1
+
+    def end(key, t):
+        b = live.pop(key)
+        blocks[b][2] = t
+
+    for s_idx, s in enumerate(steps):
+        t0, t1 = 2 * s_idx, 2 * s_idx + 1
+        for key in s.drops:
+            end(key, t0)
+        touched = {}
+        # inputs read by the step (resolved before allocations; in-place takes one over)
+        if s.kind in ("forward", "recompute"):
+            for j in g.deps(s.node):
+                touched[("in", j)] = live[("a", j)]
+        else:
+            for d in s.variant.deps:
+                touched[("in", d)] = live[("a", d)]
+            for j in g.deps(s.node):
+                if ("a", j) in live:
+                    touched[("in", j)] = live[("a", j)]
+            if s.node in g.backward_by_node and ("a", s.node) in live:
+                touched[("in", s.node)] = live[("a", s.node)]
+        for key in s.allocs:
+            if key[0] == "a":
+                if s.inplace_from is not None and key[1] == s.node:
+                    b = live.pop(("a", s.inplace_from))
+                    live[key] = b
+                else:
+                    live[key] = new_block(sizes_of[key[1]], t0)
+            else:
+                live[key] = new_block(g.grad_bytes(key[1]), t0)
+            touched[key] = live[key]
+        if s.kind == "backward":
+            touched[("g", s.node)] = live[("g", s.node)]
+            for j in g.deps(s.node):
+                if ("g", j) in live:
+                    touched[("g", j)] = live[("g", j)]
+        if s.workspace:
+            touched[("ws",)] = new_block(s.workspace, t0)
+            blocks[touched[("ws",)]][2] = t1
+        for key in s.frees:
+            end(key, t1)
+        per_step.append({"blocks": touched})
+    for key in list(live):
+        end(key, 2 * len(steps))
+    return blocks, per_step
+
+def place_blocks(blocks, capacity: int = 0):
+    n = len(blocks)
+    arr = lambda vals: (C.c_int64 * max(n, 1))(*vals)
+    sizes = arr([b[0] for b in blocks])
+    ta = arr([b[1] for b in blocks])
+    tf = arr([b[2] for b in blocks])
+    offs = (C.c_int64 * max(n, 1))()
+    peak = C.c_int64(0)
+    cap = capacity
+    rc = _native.lib().dll.monet_arena_plan(n, C.cast(sizes, C.c_void_p), C.cast(ta, C.c_void_p),
+                                       C.cast(tf, C.c_void_p), ALIGN, cap, C.cast(offs, C.c_void_p),
+                                       C.byref(peak))
+    if rc == -12:
+        raise BudgetExceeded(f"arena plan needs {peak.value} B, only {cap} B left under the budget")
+    if rc:
+        raise RuntimeError(f"arena planner failed ({rc})")
+    return peak.value, list(offs)[:n]
+
 
 
 _CUDART = None

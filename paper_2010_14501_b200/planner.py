@@ -1,0 +1,247 @@
+"""Host planner: budget-feasible schedules for large graphs.
+
+The reference's exact 0-1 branch-and-bound does not find incumbents at
+ResNet-50 scale (226k variables, SURVEY.md §7 hard part 5) and its warm-start
+heuristic (schedule.py:634-667) both takes minutes there and emits schedules
+its own simulator rejects (it rebuilds a creator that is still live to recover
+an intermediate).  This planner builds schedules in the
+same format from a *demand* construction that is valid by design:
+
+* the forward pass keeps a checkpoint set S0 chosen by tensor family (conv
+  outputs, BN outputs, ReLU outputs, residual sums, sign masks, pool
+  indices) and optionally thinned per residual block;
+* each backward stage picks the cheapest backward variant whose inputs can be
+  made available — kept in the carried row, or rebuilt in-stage from what is
+  available (never rebuilding a tensor that is still live);
+* a stage's row keeps what the stage itself reads from the carried row plus
+  what later stages read, optionally only within a window.
+
+Every candidate is screened with the exact modeled bound
+(bound.FastBound == check_schedule) and the simulator; the cheapest feasible
+schedule under the catalog's costs wins.  The result can seed the
+reference-exact ILP solver as its incumbent.
+"""
+
+from __future__ import annotations
+
+from fractions import Fraction
+
+from .bound import FastBound
+from .costmodel import Catalog
+from .graph import Graph, compute_dependency_sets
+from .memmodel import schedule_cost
+from .schedule import Schedule, SimulationError, StagePlan, simulate, store_everything_schedule
+
+__all__ = ["plan_schedule", "demand_schedule", "FAMILIES"]
+
+
+def _cheapest_fwd(cat: Catalog, i: int, ws_cap: int | None = None) -> int:
+    vs = cat.fwd(i)
+    ok = [l for l in range(len(vs)) if ws_cap is None or vs[l].workspace_bytes <= ws_cap]
+    return min(ok or range(len(vs)), key=lambda l: (vs[l].cost, l))
+
+
+def demand_schedule(g: Graph, cat: Catalog, store0: set, window: int | None = None,
+                    prefer: str = "cost") -> Schedule | None:
+    """Build a schedule that keeps ``store0`` from the forward pass.
+
+    window: a tensor rebuilt in a stage is kept for later stages only if it is
+    read again within ``window`` stages (None = until its last use).
+    prefer: "cost" picks the cheapest backward variant; "lean" the one whose
+    dependencies are already available, then the cheapest.
+    """
+    by_id = g.storable_by_id
+    ints_of = g.intermediates_of
+    fwd_impl = [cat.fwd(i)[_cheapest_fwd(cat, i)].name for i in range(1, g.n + 1)]
+    stages = g.stage_nodes
+    n_st = len(stages)
+    store0 = set(store0)
+    # the forward pass can only store what it produces: node outputs and the
+    # intermediates of nodes (both always producible in forward)
+    prev = set(store0)
+    plans = []
+    chosen_bwd: list = []
+    # needs of later stages are only known after their variants are chosen; use
+    # the default-variant needs of every variant as the future-need estimate
+    future_need: list[dict] = [dict() for _ in range(n_st + 1)]
+    for t in range(n_st - 1, -1, -1):
+        fut = dict(future_need[t + 1])
+        for v in cat.bwd(stages[t]):
+            for d in v.deps:
+                fut[d] = t  # stage index (0-based) of the soonest later reader
+        future_need[t] = fut
+
+    for t in range(1, n_st + 1):
+        k = stages[t - 1]
+        best = None
+        for l, v in sorted(enumerate(cat.bwd(k)), key=lambda e: (e[1].cost, e[0])):
+            rec: set = set()
+            used_prev: set = set()
+            ok = True
+
+            def ensure(x, depth=0):
+                nonlocal ok
+                if not ok:
+                    return
+                if x in prev:
+                    used_prev.add(x)
+                    return
+                if x in rec:
+                    return
+                u = by_id[x]
+                if u.is_intermediate:
+                    c = u.creator
+                    if c in prev:  # creator live: rebuilding it would double-allocate
+                        ok = False
+                        return
+                    ensure_node(c)
+                    rec.add(x)
+                else:
+                    ensure_node(x)
+
+            def ensure_node(i):
+                nonlocal ok
+                if i in prev:
+                    used_prev.add(i)
+                    return
+                if i in rec:
+                    return
+                for j in g.deps(i):
+                    ensure(j)
+                rec.add(i)
+
+            for d in v.deps:
+                ensure(d)
+            if not ok:
+                continue
+            if prefer == "lean":
+                key = (len(rec), v.cost, l)
+            else:
+                key = (v.cost + sum(cat.fwd(i)[cat.fwd_index(i, fwd_impl[i - 1])].cost
+                                    for i in rec if not by_id[i].is_intermediate), l)
+            if best is None or key < best[0]:
+                best = (key, l, rec, used_prev)
+        if best is None:
+            return None
+        _, l, rec, used_prev = best
+        v = cat.bwd(k)[l]
+        if t == n_st:
+            cur = set()
+            if used_prev or rec - set(v.deps):
+                # the final row must be empty: everything read must be rebuilt
+                if used_prev:
+                    return None
+        else:
+            later = future_need[t]  # readers in stages t+1.. (0-based index t)
+            cur = set(used_prev)
+            for x in (prev | rec):
+                if x in later:
+                    soon = later[x] - (t - 1)
+                    if x in store0 or window is None or soon <= window:
+                        cur.add(x)
+            # intermediates rebuilt here must be kept or read by this backward
+            for x in list(rec):
+                if by_id[x].is_intermediate and x not in cur and x not in v.deps:
+                    rec.discard(x)
+        order = sorted(rec, key=lambda x: (by_id[x].pos, by_id[x].is_intermediate, x))
+        entries = tuple((x, None if by_id[x].is_intermediate else fwd_impl[x - 1]) for x in order)
+        plans.append(StagePlan(k, entries, tuple(u.id for u in g.storables if u.id in cur), v.name, ()))
+        chosen_bwd.append(l)
+        prev = cur
+    sched = Schedule(tuple(fwd_impl), tuple(u.id for u in g.storables if u.id in store0), tuple(plans), None)
+    return Schedule(sched.forward_impls, sched.forward_store, sched.stages, schedule_cost(g, cat, sched))
+
+
+def _families(g: Graph, kind_of) -> dict:
+    """Named checkpoint sets by tensor family."""
+    ids = [u.id for u in g.storables]
+    fam = {}
+
+    def pick(kinds):
+        if "relu" in kinds:
+            kinds = kinds | {"relu-join"}
+        return {x for x in ids if kind_of(x) in kinds}
+
+    base = {"input", "maxpool", "avgpool", "fc", "xent"}
+    fam["all"] = set(ids)
+    fam["conv+relu+mask"] = pick(base | {"conv", "relu", "mask", "idx"})
+    fam["conv+mask"] = pick(base | {"conv", "mask", "idx"})
+    fam["bn+relu+mask"] = pick(base | {"bn", "relu", "mask", "idx"})
+    fam["bn+mask"] = pick(base | {"bn", "mask", "idx"})
+    fam["relu+mask"] = pick(base | {"relu", "mask", "idx"})
+    fam["conv+add+mask"] = pick(base | {"conv", "add", "mask", "idx"})
+    fam["add+mask"] = pick(base | {"add", "mask", "idx"})
+    fam["join"] = pick(base | {"relu-join", "mask", "idx"})
+    return fam
+
+
+FAMILIES = ("all", "conv+relu+mask", "conv+mask", "bn+relu+mask", "bn+mask", "relu+mask",
+            "conv+add+mask", "add+mask", "join")
+
+
+def plan_schedule(g: Graph, cat: Catalog, budget: int, kinds: dict | None = None):
+    """Cheapest feasible schedule among the demand-construction candidates.
+
+    ``kinds`` maps storable id -> family label; by default inferred from the
+    graph structure is not possible, so the tracer's op kinds are expected via
+    ``Network.storable_kinds()``; without it every storable counts as "all".
+    Returns (schedule or None, info dict).
+    """
+    sets = compute_dependency_sets(g, "upper")
+    fb = FastBound(g, sets, cat)
+    kind_of = (lambda x: kinds.get(x, "other")) if kinds else (lambda x: "other")
+    fams = _families(g, kind_of)
+    # thinned variants: drop the family's tensors in every other "segment" of
+    # the residual chain (nodes between consecutive joins)
+    joins = sorted(x for x in fams["join"] if not g.storable_by_id[x].is_intermediate)
+    cands = []
+    try:
+        cands.append(("store_everything", store_everything_schedule(g, cat)))
+    except ValueError:
+        pass
+    for name in FAMILIES:
+        s0 = fams.get(name)
+        if not s0:
+            continue
+        variants = [(name, s0)]
+        for stride in (2, 3):
+            for phase in range(stride):
+                keep_segs = set()
+                for si, (a, b) in enumerate(zip([0] + joins, joins + [g.n + 1])):
+                    if si % stride == phase:
+                        keep_segs.update(range(a + 1, b))
+                thin = {x for x in s0 if g.storable_by_id[x].pos not in keep_segs or x in fams["join"]}
+                variants.append((f"{name}/thin{stride}.{phase}", thin))
+        for vname, s0v in variants:
+            for window in (None, 8, 2):
+                for prefer in ("cost", "lean"):
+                    sch = demand_schedule(g, cat, s0v, window=window, prefer=prefer)
+                    if sch is not None:
+                        cands.append((f"{vname}/w{window}/{prefer}", sch))
+    best = None
+    tried = 0
+    for name, sch in cands:
+        tried += 1
+        ok, peak, _ = fb.check(sch, budget)
+        if not ok:
+            continue
+        if best is not None and sch.objective >= best[1].objective:
+            continue
+        try:
+            simulate(sch, g, cat)
+        except SimulationError:
+            continue
+        best = (name, sch, peak)
+    if best is None:
+        return None, {"candidates": tried}
+    se_cost = None
+    try:
+        se_cost = store_everything_schedule(g, cat).objective
+    except ValueError:
+        pass
+    name, sch, peak = best
+    info = {"family": name, "candidates": tried, "modeled_peak": peak,
+            "objective": str(sch.objective),
+            "overhead_vs_store_everything": None if se_cost is None
+            else float(Fraction(sch.objective) / se_cost - 1)}
+    return sch, info

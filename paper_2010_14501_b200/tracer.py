@@ -87,6 +87,18 @@ class Network:
     def op(self, i: int) -> Op:
         return self.ops[i - 1]
 
+    def storable_kinds(self) -> dict:
+        """Storable id -> family label used by the planner (planner.FAMILIES)."""
+        out = {}
+        for op in self.ops:
+            kind = op.kind
+            if kind == "relu" and self.op(op.deps[0]).kind == "add":
+                kind = "relu-join"
+            out[op.id] = kind
+            if op.id in self.intermediate_of:
+                out[self.intermediate_of[op.id]] = "mask" if op.kind == "relu" else "idx"
+        return out
+
     # -------------------------------------------------------------- fixed region
     def param_items(self):
         for op in self.ops:

@@ -1,0 +1,111 @@
+"""End-to-end parity of the GPU executor (config 1: ResNet-18, batch 8, 64x64).
+
+For the store-everything schedule and the reference-planned recompute
+schedule at a tight budget (tests/golden/r18_b8_64.json):
+  * the executed ledger equals the reference simulate() trace byte for byte;
+  * the planned physical footprint (params_bytes + arena high-water mark)
+    stays within the budget, and the ledger peak within the ILP bound;
+  * every recompute reproduces its forward activation bit for bit (BN replays
+    saved statistics);
+  * forward activations and the loss match the CPU oracle within
+    rel 1e-4 (max|gpu-cpu| / max|cpu| per tensor);
+  * with the GPU's activations fed to the oracle (ReLU/maxpool derivatives are
+    discontinuous: a 1-ulp difference in x near 0 flips a mask bit), every
+    parameter gradient, updated weight and BN running statistic matches within
+    rel 1e-4 (fp32 storage, 3xTF32 tensor-core convolutions).
+"""
+import json
+from pathlib import Path
+
+import pytest
+import torch
+
+import paper_2010_14501_b200 as M
+from oracle.cpu_executor import CpuState, params_nhwc, run_step
+from paper_2010_14501_b200.engine import Runtime
+from paper_2010_14501_b200.tracer import build_network
+from oracle.parity import capture, rel
+
+pytestmark = pytest.mark.gpu
+GOLD = Path(__file__).resolve().parent / "golden"
+REL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def r18():
+    doc = json.loads((GOLD / "r18_b8_64.json").read_text())
+    net = build_network("resnet18", 8, 64)
+    assert net.graph_doc() == doc["graph"], "tracer output drifted from the frozen graph"
+    g = M.load_graph(doc["graph"])
+    cat = M.load_catalog(doc["catalog"], g)
+    gen = torch.Generator().manual_seed(0)
+    x = torch.randn(8, 3, 64, 64, generator=gen)
+    y = torch.randint(0, 1000, (8,), generator=gen)
+    cases = [("store_everything", doc["store_everything"], None)]
+    cases += [(f"{c['status']}-{c['budget']}", c, c["budget"]) for c in doc["cases"] if "trace_csv" in c]
+    return net, g, cat, x, y, cases
+
+
+@pytest.mark.parametrize("which", [0, 1])
+def test_engine_matches_reference_ledger_and_oracle(cuda, r18, which):
+    net, g, cat, x, y, cases = r18
+    name, case, budget = cases[which]
+    sched = M.schedule_from_doc(case["schedule"])
+    rt = Runtime(net, budget_bytes=budget)
+    rt.set_batch(x.to(cuda), y.to(cuda))
+    plan = rt.plan(sched, g, cat)
+    acts, mismatched = capture(rt, plan)
+    assert not mismatched, f"recompute not bit-identical for nodes {mismatched}"
+    assert M.trace_report(plan.trace) == case["trace_csv"]
+    assert plan.ledger_peak == case["peak"]
+    if budget is not None:
+        assert g.params_bytes + plan.arena_bytes <= budget
+        assert plan.ledger_peak <= plan.bound_peak <= budget
+    # free-running oracle: forward and loss
+    free = CpuState(net)
+    loss = run_step(free, case["schedule"], x, y)
+    assert abs(rt.loss_value() - loss) <= REL * abs(loss)
+    # oracle fed with the GPU activations: backward, weights, statistics
+    st = CpuState(net)
+    run_step(st, case["schedule"], x, y, forced=acts)
+    for (nid, pname), v in params_nhwc(st).items():
+        got = rt.pview[(nid, pname)].view(v.shape)
+        assert rel(got, v) <= REL, (name, net.op(nid).name, pname, rel(got, v))
+        gg = st.grads[(nid, pname)]
+        if net.op(nid).kind == "conv" and pname == "weight":
+            gg = gg.permute(0, 2, 3, 1)
+        assert rel(rt.gview[(nid, pname)].view(gg.shape), gg) <= REL, (name, net.op(nid).name, pname, "grad")
+    for op in net.ops:
+        if op.kind == "bn":
+            rm, rv = free.running[op.id]
+            assert rel(rt.bn[op.id][2], rm) <= REL and rel(rt.bn[op.id][3], rv) <= REL
+
+
+def test_forward_ops_match_oracle(cuda, r18):
+    """Each forward op, evaluated by the oracle on the GPU's own inputs, matches the GPU output."""
+    net, g, cat, x, y, cases = r18
+    sched = M.schedule_from_doc(cases[0][1]["schedule"])
+    rt = Runtime(net)
+    rt.set_batch(x.to(cuda), y.to(cuda))
+    acts, _ = capture(rt, rt.plan(sched, g, cat))
+    mine = {}
+    run_step(CpuState(net), cases[0][1]["schedule"], x, y, forced=acts, fwd_record=mine)
+    worst = max((rel(acts[i], mine[i]), net.op(i).name) for i in acts if i in mine)
+    assert worst[0] <= REL, worst
+
+
+def test_budget_exceeded_raises(cuda, r18):
+    net, g, cat, x, y, cases = r18
+    se = M.schedule_from_doc(cases[0][1]["schedule"])
+    rt = Runtime(net, budget_bytes=g.params_bytes + 1024)
+    with pytest.raises(M.BudgetExceeded):
+        rt.plan(se, g, cat)
+
+
+def test_invalid_schedule_raises(cuda, r18):
+    net, g, cat, x, y, cases = r18
+    doc = json.loads(json.dumps(cases[0][1]["schedule"]))
+    doc["stages"][3]["store"] = []  # drop a dependency the backward still needs
+    rt = Runtime(net)
+    with pytest.raises(M.SimulationError):
+        rt.plan(M.schedule_from_doc(doc), g, cat)

@@ -1,0 +1,103 @@
+"""Pin the CPU oracle executor's numerics against plain torch autograd.
+
+The reference package has no numeric implementation ("parity unpinned",
+SURVEY.md §8c), so the oracle is pinned here instead: replaying ANY valid
+schedule (store-everything or with recomputation and memory-efficient
+backward variants) must give the same loss, updated weights and BN running
+statistics as one ordinary autograd + SGD step of the same torchvision model.
+"""
+import numpy as np
+import pytest
+import torch
+import torchvision
+
+import paper_2010_14501_b200 as M
+from oracle.bitmask import pack_sign_mask, unpack_sign_mask
+from oracle.cpu_executor import CpuState, params_nhwc, run_step
+from paper_2010_14501_b200.tracer import trace_graph
+
+TOL = 1e-9  # both sides in float64: pins the algorithm, not fp32 rounding (small-batch BN is ill-conditioned)
+
+
+def _rel(a, b):
+    return (a.double() - b.double()).abs().max().item() / max(b.double().abs().max().item(), 1e-30)
+
+
+def _setup(batch=2, hw=32, arch="resnet18"):
+    torch.manual_seed(0)
+    model = getattr(torchvision.models, arch)(num_classes=10)
+    net = trace_graph(model, torch.empty(batch, 3, hw, hw, device="meta"), 10)
+    g = M.load_graph(net.graph_doc())
+    cat = M.load_catalog(net.catalog_doc(), g)
+    gen = torch.Generator().manual_seed(1)
+    x = torch.randn(batch, 3, hw, hw, generator=gen)
+    y = torch.randint(0, 10, (batch,), generator=gen)
+    return model, net, g, cat, x, y
+
+
+def _autograd_step(model, x, y):
+    model.double().train()
+    x = x.double()
+    opt = torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9)
+    loss = torch.nn.functional.cross_entropy(model(x), y)
+    opt.zero_grad()
+    loss.backward()
+    opt.step()
+    return loss.item()
+
+
+def _schedules(g, cat):
+    se = M.store_everything_schedule(g, cat)
+    sets = M.compute_dependency_sets(g)
+    peak = M.simulate(se, g, cat).peak_memory
+    act = peak - g.params_bytes
+    out = [("store_everything", se)]
+    for f in (0.6, 0.45):
+        h = M.checkpoint_heuristic(g, sets, cat, g.params_bytes + int(f * act))
+        if h is None:
+            continue
+        try:
+            M.simulate(h, g, cat)
+        except M.SimulationError:
+            continue
+        out.append((f"heuristic-{f}", h))
+    return out
+
+
+@pytest.mark.parametrize("arch", ["resnet18"])
+def test_oracle_replay_equals_autograd(arch):
+    model, net, g, cat, x, y = _setup(arch=arch)
+    ref_loss = _autograd_step(model, x, y)
+    ref = {n: p.detach() for n, p in model.named_parameters()}
+    ref_bn = {n: b for n, b in model.named_buffers() if "running" in n}
+    scheds = _schedules(g, cat)
+    assert any(n != "store_everything" for n, _ in scheds), "no recompute schedule to test"
+    for name, sched in scheds:
+        st = CpuState(net, dtype=torch.float64)
+        loss = run_step(st, M.schedule_to_doc(sched), x.double(), y)
+        assert abs(loss - ref_loss) <= TOL * abs(ref_loss), name
+        got = params_nhwc(st)
+        for op in net.ops:
+            for pname in op.params:
+                want = ref[f"{op.name}.{pname}"]
+                have = got[(op.id, pname)]
+                if op.kind == "conv":
+                    have = have[..., : want.shape[1]].permute(0, 3, 1, 2)
+                assert _rel(have, want) < TOL, (name, op.name, pname)
+            if op.kind == "bn":
+                rm, rv = st.running[op.id]
+                assert _rel(rm, ref_bn[f"{op.name}.running_mean"]) < TOL
+                assert _rel(rv, ref_bn[f"{op.name}.running_var"]) < TOL
+
+
+def test_bitmask_roundtrip():
+    rng = np.random.default_rng(0)
+    for n in (1, 31, 32, 33, 1000):
+        x = rng.standard_normal(n).astype(np.float32)
+        x[::5] = 0
+        w = pack_sign_mask(x)
+        assert w.dtype == np.uint32 and len(w) == (n + 31) // 32
+        assert np.array_equal(unpack_sign_mask(w, n), x > 0)
+        # bit b of word k <-> element 32k+b
+        for e in range(n):
+            assert ((w[e // 32] >> (e % 32)) & 1) == (x[e] > 0)

@@ -1,0 +1,55 @@
+"""Randomised cross-check against the live reference (only where /root/reference exists).
+
+On the GPU box the reference is absent and this module skips; the committed
+golden fixtures (test_planner_golden.py) carry the same evidence there.
+"""
+import os
+import sys
+
+import pytest
+
+REF = "/root/reference/pkg/src"
+if not os.path.isdir(REF):
+    pytest.skip("reference not mounted", allow_module_level=True)
+sys.path.insert(0, REF)
+import remsched as R  # noqa: E402
+
+import paper_2010_14501_b200 as M  # noqa: E402
+from paper_2010_14501_b200.memmodel import MemModel  # noqa: E402
+from paper_2010_14501_b200.units import canonical_json_dumps as cj  # noqa: E402
+
+ATTRS = ["sweep_mask_strict", "sweep_mask_incl", "tail_mask", "forward_extra_mask", "local_bytes", "d_mask",
+         "bwd_const", "bwd_alpha_mask", "active_dep_bytes", "active_alpha_mask", "active_base",
+         "inactive_dep_bytes", "inactive_alpha_mask"]
+
+
+@pytest.mark.parametrize("kind", ["chain", "residual", "inception-toy", "unet-toy"])
+@pytest.mark.parametrize("seed", [0, 5])
+def test_planner_matches_reference(kind, seed):
+    for n, fv, bv, ie in [(5, 2, 2, 2), (9, 3, 3, 3)]:
+        rg, rc = R.generate_synthetic(kind, n, seed, fwd_variants=fv, bwd_variants=bv, intermediate_every=ie,
+                                      inplace_marks=True)
+        mg, mc = M.generate_synthetic(kind, n, seed, fwd_variants=fv, bwd_variants=bv, intermediate_every=ie,
+                                      inplace_marks=True)
+        assert cj(R.catalog_to_doc(rc)) == cj(M.catalog_to_doc(mc))
+        for bk in ("upper", "tight"):
+            rs, ms = R.compute_dependency_sets(rg, bk), M.compute_dependency_sets(mg, bk)
+            rmm, mmm = R.MemModel(rg, rs, rc), MemModel(mg, ms, mc)
+            for a in ATTRS:
+                assert getattr(rmm, a) == getattr(mmm, a), a
+            for budget in (6, 12, 25, 60):
+                rh = R.checkpoint_heuristic(rg, rs, rc, budget)
+                mh = M.checkpoint_heuristic(mg, ms, mc, budget)
+                assert (rh is None) == (mh is None)
+                if rh is None:
+                    continue
+                assert cj(R.schedule_to_doc(rh)) == cj(M.schedule_to_doc(mh))
+                assert R.check_schedule(rg, rs, rc, rh, budget) == M.check_schedule(mg, ms, mc, mh, budget)
+                assert R.validate(rh, rg, rs, rc) == M.validate(mh, mg, ms, mc)
+                try:
+                    rt = R.trace_report(R.simulate(rh, rg, rc))
+                except R.schedule.SimulationError as exc:
+                    with pytest.raises(M.SimulationError, match=str(exc)):
+                        M.simulate(mh, mg, mc)
+                    continue
+                assert rt == M.trace_report(M.simulate(mh, mg, mc))

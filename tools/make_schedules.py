@@ -1,0 +1,52 @@
+"""Plan the benchmark schedules offline and freeze them (host planner, deterministic).
+
+    python tools/make_schedules.py
+
+Writes schedules/<arch>_b<batch>_<img>_<budget>gib.json with the graph and
+catalog digests they were planned against.  Planning ResNet-50 takes about a
+minute per budget, so bench.py loads these instead of planning in the timed run.
+"""
+import hashlib
+import json
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import paper_2010_14501_b200 as M  # noqa: E402
+from paper_2010_14501_b200.planner import plan_schedule  # noqa: E402
+from paper_2010_14501_b200.tracer import build_network  # noqa: E402
+
+OUT = ROOT / "schedules"
+
+
+def digest(doc):
+    return hashlib.sha256(json.dumps(doc, sort_keys=True).encode()).hexdigest()[:16]
+
+
+def main(jobs):
+    OUT.mkdir(exist_ok=True)
+    for arch, batch, img, gib in jobs:
+        net = build_network(arch, batch, img)
+        gdoc, cdoc = net.graph_doc(), net.catalog_doc()
+        g = M.load_graph(gdoc)
+        cat = M.load_catalog(cdoc, g)
+        budget = int(gib * (1 << 30))
+        t = time.time()
+        sched, info = plan_schedule(g, cat, budget, kinds=net.storable_kinds())
+        dt = time.time() - t
+        if sched is None:
+            print(arch, batch, img, gib, "no feasible schedule", info)
+            continue
+        doc = {"arch": arch, "batch": batch, "image": img, "budget_bytes": budget,
+               "graph_digest": digest(gdoc), "catalog_digest": digest(cdoc), "planner": info,
+               "plan_seconds": round(dt, 1), "schedule": M.schedule_to_doc(sched)}
+        path = OUT / f"{arch}_b{batch}_{img}_{gib:g}gib.json"
+        path.write_text(json.dumps(doc, indent=1, sort_keys=True) + "\n")
+        print(path.name, info, f"{dt:.1f}s")
+
+
+if __name__ == "__main__":
+    main([("resnet50", 184, 224, 10), ("resnet50", 184, 224, 8), ("resnet50", 184, 224, 6)])
