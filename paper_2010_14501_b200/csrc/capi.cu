@@ -39,7 +39,29 @@ size_t gemm_ws(int variant, int M, int N, int Kd) {
   return s > 1 ? (size_t)s * M * N * sizeof(float) : 0;
 }
 
-bool g_attr_set = false;
+// One instantiation per (A mode, B mode) pair used by conv / linear / gemm.
+template <int AM, int BMODE>
+int launch_inst(const GemmParams& p, int grid, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_tf32_kernel<AM, BMODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    attr = true;
+  }
+  gemm_tf32_kernel<AM, BMODE><<<grid, kThreads, kSmemBytes, st>>>(p);
+  return 0;
+}
+
+int dispatch_gemm(const GemmParams& p, int grid, cudaStream_t st) {
+  const int a = p.a.mode, b = p.b.mode;
+  if (a == OP_IM2COL_FPROP && b == OP_KMAJOR) return launch_inst<OP_IM2COL_FPROP, OP_KMAJOR>(p, grid, st);
+  if (a == OP_KMAJOR && b == OP_KMAJOR) return launch_inst<OP_KMAJOR, OP_KMAJOR>(p, grid, st);
+  if (a == OP_IM2COL_DGRAD && b == OP_MNMAJOR) return launch_inst<OP_IM2COL_DGRAD, OP_MNMAJOR>(p, grid, st);
+  if (a == OP_KMAJOR && b == OP_MNMAJOR) return launch_inst<OP_KMAJOR, OP_MNMAJOR>(p, grid, st);
+  if (a == OP_MNMAJOR && b == OP_IM2COL_WGRAD) return launch_inst<OP_MNMAJOR, OP_IM2COL_WGRAD>(p, grid, st);
+  if (a == OP_MNMAJOR && b == OP_MNMAJOR) return launch_inst<OP_MNMAJOR, OP_MNMAJOR>(p, grid, st);
+  if (a == OP_MNMAJOR && b == OP_KMAJOR) return launch_inst<OP_MNMAJOR, OP_KMAJOR>(p, grid, st);
+  return -(int)cudaErrorInvalidValue;
+}
 
 int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (p.M <= 0 || p.N <= 0) return 0;
@@ -57,13 +79,9 @@ int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_b
   p.splits = (kblocks + p.kb_per_split - 1) / p.kb_per_split;
   p.ws = static_cast<float*>(ws);
   p.epi = p.splits > 1 ? EPI_PARTIAL : (accumulate ? EPI_ACCUM : EPI_STORE);
-  if (!g_attr_set) {
-    cudaFuncSetAttribute(gemm_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    g_attr_set = true;
-  }
   const int tiles = p.m_tiles * p.n_tiles * p.splits;
   const int grid = std::min(tiles, kNumSMs);
-  gemm_tf32_kernel<<<grid, kThreads, kSmemBytes, st>>>(p);
+  if (int e = dispatch_gemm(p, grid, st)) return e;
   if (p.splits > 1) {
     long long total = (long long)p.M * p.N;
     splitk_reduce_kernel<<<ew_blocks(total), kEwThreads, 0, st>>>(p.ws, p.c, p.M, p.N, p.ldc, p.splits, accumulate);
