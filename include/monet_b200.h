@@ -46,6 +46,9 @@ enum { MONET_PASS_FWD = 0, MONET_PASS_DGRAD = 1, MONET_PASS_WGRAD = 2, MONET_PAS
 /* --- library --------------------------------------------------------------- */
 const char* monet_version(void);
 int monet_device_check(void); /* 0 if the current device is sm_100 */
+/* device-to-device byte copy on `stream` (staging the input batch into the arena,
+ * the loss seed); the executor needs no other CUDA runtime entry point */
+int monet_copy_async(void* dst, const void* src, size_t bytes, void* stream);
 
 /* --- convolution (K1-K3; replaces conv entries of Catalog, costmodel.py:30-44) */
 size_t monet_conv_ws_bytes(int variant, int pass, const monet_conv_desc* d);

@@ -26,6 +26,7 @@ _PCONV = C.POINTER(ConvDesc)
 SIGNATURES = {
     "monet_version": (C.c_char_p, []),
     "monet_device_check": (_i32, []),
+    "monet_copy_async": (_i32, [_vp, _vp, _sz, _vp]),
     "monet_conv_ws_bytes": (_sz, [_i32, _i32, _PCONV]),
     "monet_conv_fwd": (_i32, [_i32, _PCONV, _vp, _vp, _vp, _vp, _sz, _vp]),
     "monet_conv_dgrad": (_i32, [_i32, _PCONV, _vp, _vp, _vp, _i32, _vp, _sz, _vp]),

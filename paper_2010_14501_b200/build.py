@@ -27,7 +27,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 def _sources():
     files = [CSRC / f for f in CU_SOURCES + CPP_SOURCES]
-    files += list(CSRC.glob("*.cuh")) + [INCLUDE / "monet_b200.h"]
+    files += list(CSRC.glob("*.cuh")) + [INCLUDE / "monet_b200.h", CSRC / "exports.map"]
     return files
 
 
@@ -57,7 +57,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
               "-o", str(obj)], verbose)
         objs.append(obj)
     tmp = LIB.with_suffix(".so.tmp")
-    _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart"], verbose)
+    # export only the extern "C" monet_* boundary (exports.map)
+    _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart",
+          "-Xlinker", f"--version-script={CSRC / 'exports.map'}"], verbose)
     os.replace(tmp, LIB)
     return LIB
 

@@ -161,6 +161,12 @@ int monet_device_check(void) {
   return (major == 10 && minor == 0) ? 0 : -2;
 }
 
+int monet_copy_async(void* dst, const void* src, size_t bytes, void* stream) {
+  if (bytes == 0) return 0;
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, S(stream));
+  return e == cudaSuccess ? 0 : -static_cast<int>(e);
+}
+
 // ------------------------------------------------------------------- conv
 size_t monet_conv_ws_bytes(int variant, int pass, const monet_conv_desc* d) {
   if (check_desc(d)) return 0;

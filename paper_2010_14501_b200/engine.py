@@ -407,9 +407,9 @@ class Runtime:
                 if rc != 0:
                     raise _native.NativeError(f"{fn.__name__} failed with code {rc}")
             elif kind == "copy":
-                rc = cudart.cudaMemcpyAsync(C.c_void_p(c[1]), C.c_void_p(c[2]), C.c_size_t(c[3]), 3, sp)
+                rc = cudart.monet_copy_async(c[1], c[2], c[3], sp)
                 if rc != 0:
-                    raise _native.NativeError(f"cudaMemcpyAsync failed ({rc})")
+                    raise _native.NativeError(f"monet_copy_async failed ({rc})")
             else:
                 c[1]()
 
@@ -491,22 +491,10 @@ def place_blocks(blocks, capacity: int = 0):
 
 
 
-_CUDART = None
-
-
 def _cudart():
-    global _CUDART
-    if _CUDART is None:
-        lib = C.CDLL(str(_native.LIB_PATH))  # libmonet links cudart; resolve through it
-        try:
-            fn = lib.cudaMemcpyAsync
-        except AttributeError:
-            lib = C.CDLL("libcudart.so")
-            fn = lib.cudaMemcpyAsync
-        fn.restype = C.c_int
-        fn.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p]
-        _CUDART = lib
-    return _CUDART
+    """The copy entry point of the C ABI (monet_copy_async); kept as a callable
+    object so ``_run_group`` does not look it up per launch."""
+    return _native.lib().dll
 
 
 def execute(schedule: Schedule, g: Graph, catalog: Catalog, *, runtime: Runtime,
