@@ -36,11 +36,13 @@ typedef struct {
 } monet_conv_desc;
 
 /* conv variants (catalog ForwardVariant / BackwardVariant names):
- *   MONET_CONV_IMPLICIT  "implicit"  tcgen05 3xTF32 implicit GEMM, im2col in registers
+ *   MONET_CONV_IMPLICIT  "implicit"  tcgen05 bf16x3 implicit GEMM (fp32 = bf16 hi + lo, three
+ *                                    MMAs, ~1e-5 relative), A operand staged in TMEM
  *   MONET_CONV_SPLITK    "splitk"    as implicit, plus split-K over the reduction with
  *                                    fp32 partials in workspace (honest ws/speed trade)
- *   MONET_CONV_TF32      "tf32"      single-pass TF32 (faster, ~1e-3 relative error) */
-enum { MONET_CONV_IMPLICIT = 0, MONET_CONV_SPLITK = 1, MONET_CONV_TF32 = 2 };
+ *   MONET_CONV_TF32      "tf32"      single-pass TF32 (faster, ~1e-3 relative error; tests only)
+ *   MONET_CONV_TF32X3    "tf32x3"    3xTF32 all-shared-memory kernel (round-1 baseline) */
+enum { MONET_CONV_IMPLICIT = 0, MONET_CONV_SPLITK = 1, MONET_CONV_TF32 = 2, MONET_CONV_TF32X3 = 3 };
 enum { MONET_PASS_FWD = 0, MONET_PASS_DGRAD = 1, MONET_PASS_WGRAD = 2, MONET_PASS_BWD = 3 };
 
 /* --- library --------------------------------------------------------------- */
@@ -49,6 +51,9 @@ int monet_device_check(void); /* 0 if the current device is sm_100 */
 /* device-to-device byte copy on `stream` (staging the input batch into the arena,
  * the loss seed); the executor needs no other CUDA runtime entry point */
 int monet_copy_async(void* dst, const void* src, size_t bytes, void* stream);
+/* debug only: make the bf16x3 GEMM dump the raw A / B operands it consumes
+ * ([rows][K rounded up to 64] fp32 device buffers; NULL disables) */
+void monet_debug_dump(float* a_dump, float* b_dump);
 
 /* --- convolution (K1-K3; replaces conv entries of Catalog, costmodel.py:30-44) */
 size_t monet_conv_ws_bytes(int variant, int pass, const monet_conv_desc* d);

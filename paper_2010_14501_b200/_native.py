@@ -27,6 +27,7 @@ SIGNATURES = {
     "monet_version": (C.c_char_p, []),
     "monet_device_check": (_i32, []),
     "monet_copy_async": (_i32, [_vp, _vp, _sz, _vp]),
+    "monet_debug_dump": (None, [_vp, _vp]),
     "monet_conv_ws_bytes": (_sz, [_i32, _i32, _PCONV]),
     "monet_conv_fwd": (_i32, [_i32, _PCONV, _vp, _vp, _vp, _vp, _sz, _vp]),
     "monet_conv_dgrad": (_i32, [_i32, _PCONV, _vp, _vp, _vp, _i32, _vp, _sz, _vp]),
@@ -60,7 +61,7 @@ SIGNATURES = {
     "monet_arena_plan": (_i32, [_i64, _vp, _vp, _vp, _i64, _i64, _vp, _vp]),
 }
 
-CONV_VARIANTS = {"implicit": 0, "splitk": 1, "tf32": 2}
+CONV_VARIANTS = {"implicit": 0, "splitk": 1, "tf32": 2, "tf32x3": 3}
 PASS = {"fwd": 0, "dgrad": 1, "wgrad": 2, "bwd": 3}
 
 

@@ -1,9 +1,13 @@
 // extern "C" boundary of libmonet_b200.so (declared in include/monet_b200.h).
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/monet_b200.h"
+#include "gemm_bf16x3.cuh"
 #include "gemm_tc.cuh"
 #include "local_ops.cuh"
 
@@ -40,31 +44,150 @@ size_t gemm_ws(int variant, int M, int N, int Kd) {
 }
 
 // One instantiation per (A mode, B mode) pair used by conv / linear / gemm.
-template <int AM, int BMODE>
+// kBx3 selects the bf16x3 A-in-TMEM kernel (gemm_bf16x3.cuh, the product
+// path); otherwise the 3xTF32 / TF32 all-smem kernel (gemm_tc.cuh).
+template <bool kBx3, int AM, int BMODE>
 int launch_inst(const GemmParams& p, int grid, cudaStream_t st) {
   static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gemm_tf32_kernel<AM, BMODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    attr = true;
+  if constexpr (kBx3) {
+    if (!attr) {
+      cudaFuncSetAttribute(bx3::gemm_bf16x3_kernel<AM, BMODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           bx3::kSmemBytes);
+      attr = true;
+    }
+    bx3::gemm_bf16x3_kernel<AM, BMODE><<<grid, bx3::kThreads, bx3::kSmemBytes, st>>>(p);
+  } else {
+    if (!attr) {
+      cudaFuncSetAttribute(gemm_tf32_kernel<AM, BMODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+      attr = true;
+    }
+    gemm_tf32_kernel<AM, BMODE><<<grid, kThreads, kSmemBytes, st>>>(p);
   }
-  gemm_tf32_kernel<AM, BMODE><<<grid, kThreads, kSmemBytes, st>>>(p);
   return 0;
 }
 
-int dispatch_gemm(const GemmParams& p, int grid, cudaStream_t st) {
+template <bool kBx3>
+int dispatch_modes(const GemmParams& p, int grid, cudaStream_t st) {
   const int a = p.a.mode, b = p.b.mode;
-  if (a == OP_IM2COL_FPROP && b == OP_KMAJOR) return launch_inst<OP_IM2COL_FPROP, OP_KMAJOR>(p, grid, st);
-  if (a == OP_KMAJOR && b == OP_KMAJOR) return launch_inst<OP_KMAJOR, OP_KMAJOR>(p, grid, st);
-  if (a == OP_IM2COL_DGRAD && b == OP_MNMAJOR) return launch_inst<OP_IM2COL_DGRAD, OP_MNMAJOR>(p, grid, st);
-  if (a == OP_KMAJOR && b == OP_MNMAJOR) return launch_inst<OP_KMAJOR, OP_MNMAJOR>(p, grid, st);
-  if (a == OP_MNMAJOR && b == OP_IM2COL_WGRAD) return launch_inst<OP_MNMAJOR, OP_IM2COL_WGRAD>(p, grid, st);
-  if (a == OP_MNMAJOR && b == OP_MNMAJOR) return launch_inst<OP_MNMAJOR, OP_MNMAJOR>(p, grid, st);
-  if (a == OP_MNMAJOR && b == OP_KMAJOR) return launch_inst<OP_MNMAJOR, OP_KMAJOR>(p, grid, st);
+  if (a == OP_IM2COL_FPROP && b == OP_KMAJOR) return launch_inst<kBx3, OP_IM2COL_FPROP, OP_KMAJOR>(p, grid, st);
+  if (a == OP_KMAJOR && b == OP_KMAJOR) return launch_inst<kBx3, OP_KMAJOR, OP_KMAJOR>(p, grid, st);
+  if (a == OP_IM2COL_DGRAD && b == OP_MNMAJOR) return launch_inst<kBx3, OP_IM2COL_DGRAD, OP_MNMAJOR>(p, grid, st);
+  if (a == OP_KMAJOR && b == OP_MNMAJOR) return launch_inst<kBx3, OP_KMAJOR, OP_MNMAJOR>(p, grid, st);
+  if (a == OP_MNMAJOR && b == OP_IM2COL_WGRAD) return launch_inst<kBx3, OP_MNMAJOR, OP_IM2COL_WGRAD>(p, grid, st);
+  if (a == OP_MNMAJOR && b == OP_MNMAJOR) return launch_inst<kBx3, OP_MNMAJOR, OP_MNMAJOR>(p, grid, st);
+  if (a == OP_MNMAJOR && b == OP_KMAJOR) return launch_inst<kBx3, OP_MNMAJOR, OP_KMAJOR>(p, grid, st);
   return -(int)cudaErrorInvalidValue;
 }
 
+bool uses_bx3(int variant) { return variant == MONET_CONV_IMPLICIT || variant == MONET_CONV_SPLITK; }
+
+// ----------------------------------------------------------------- TMA maps
+// The driver's tensor-map encoders, resolved through the runtime (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 g_enc_tiled = nullptr;
+PFN_cuTensorMapEncodeIm2col_v12000 g_enc_im2col = nullptr;
+
+bool tma_available() {
+  static int state = 0;
+  if (state == 0) {
+    cudaDriverEntryPointQueryResult q1, q2;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&g_enc_tiled), cudaEnableDefault, &q1);
+    cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", reinterpret_cast<void**>(&g_enc_im2col), cudaEnableDefault,
+                            &q2);
+    state = (g_enc_tiled && g_enc_im2col) ? 1 : -1;
+    cudaGetLastError();
+  }
+  return state == 1;
+}
+
+int tiled_map(CUtensorMap* m, const float* ptr, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+              const cuuint32_t* box, CUtensorMapSwizzle sw) {
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_enc_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<float*>(ptr), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 1 : 0;
+}
+
+// im2col map over an NHWC tensor [n][h][w][c]; corners / offsets index 0 = W, 1 = H
+// (pinned on the B200 by tools/tma_probe.cu)
+int im2col_map(CUtensorMap* m, const float* ptr, int n, int h, int w, int c, int lo_w, int lo_h, int up_w, int up_h,
+               int es_w, int es_h, int channels, int pixels, CUtensorMapSwizzle sw) {
+  const int corners[4] = {lo_w, lo_h, up_w, up_h};
+  for (int v : corners)
+    if (v < -128 || v > 127) return 0;
+  cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+  cuuint64_t strides[3] = {(cuuint64_t)c * 4, (cuuint64_t)w * c * 4, (cuuint64_t)h * w * c * 4};
+  int lo[2] = {lo_w, lo_h}, up[2] = {up_w, up_h};
+  cuuint32_t es[4] = {1, (cuuint32_t)es_w, (cuuint32_t)es_h, 1};
+  CUresult r = g_enc_im2col(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(ptr), dims, strides, lo, up,
+                            channels, pixels, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 2 : 0;
+}
+
+// TMA descriptor for one bf16x3 operand; returns Operand::tma (0 = use the
+// 16B cp.async fallback).  Raw layouts: K-major boxes are 32 fp32 x 128 rows
+// with SWIZZLE_128B, MN-major boxes 128 (or p.mn_seg) rows x 32 k, unswizzled.
+int make_tma(GemmParams& p, const Operand& op, CUtensorMap* m) {
+  if (!tma_available() || (reinterpret_cast<uintptr_t>(op.ptr) & 15) != 0) return 0;
+  const ConvGeom& g = p.g;
+  switch (op.mode) {
+    case OP_KMAJOR: {
+      if (op.ld % 4) return 0;
+      cuuint64_t dims[2] = {(cuuint64_t)p.Kd, (cuuint64_t)op.rows};
+      cuuint64_t strides[1] = {(cuuint64_t)op.ld * 4};
+      cuuint32_t box[2] = {32, 128};
+      return tiled_map(m, op.ptr, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    }
+    case OP_MNMAJOR: {
+      if (op.ld % 4) return 0;
+      if (op.kdiv >= p.Kd) {
+        cuuint64_t dims[2] = {(cuuint64_t)op.rows, (cuuint64_t)p.Kd};
+        cuuint64_t strides[1] = {(cuuint64_t)op.ld * 4};
+        cuuint32_t box[2] = {128, 32};
+        return tiled_map(m, op.ptr, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+      }
+      if (op.kdiv % 32 || op.ks1 % 4 || p.Kd % op.kdiv) return 0;
+      cuuint64_t dims[3] = {(cuuint64_t)op.rows, (cuuint64_t)(p.Kd / op.kdiv), (cuuint64_t)op.kdiv};
+      cuuint64_t strides[2] = {(cuuint64_t)op.ks1 * 4, (cuuint64_t)op.ld * 4};
+      cuuint32_t box[3] = {128, 1, 32};
+      return tiled_map(m, op.ptr, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+    }
+    case OP_IM2COL_FPROP:
+      if (g.C % 32) return 0;
+      return im2col_map(m, op.ptr, g.N, g.H, g.W, g.C, -g.pw, -g.ph, g.pw - (g.S - 1), g.ph - (g.R - 1), g.sw, g.sh,
+                        32, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+    case OP_IM2COL_DGRAD:  // forward conv over dy with flipped taps; stride 1 only
+      if (g.K % 32 || g.sh != 1 || g.sw != 1) return 0;
+      return im2col_map(m, op.ptr, g.N, g.P, g.Q, g.K, -(g.S - 1 - g.pw), -(g.R - 1 - g.ph), -g.pw, -g.ph, 1, 1, 32,
+                        128, CU_TENSOR_MAP_SWIZZLE_128B);
+    case OP_IM2COL_WGRAD: {
+      if (g.C % 32 || (g.C < 128 ? 128 % g.C : g.C % 128)) return 0;
+      const int seg = std::min(g.C, 128);
+      const int r = im2col_map(m, op.ptr, g.N, g.H, g.W, g.C, -g.pw, -g.ph, g.pw - (g.S - 1), g.ph - (g.R - 1),
+                               g.sw, g.sh, seg, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
+      if (r) p.mn_seg = seg;
+      return r;
+    }
+  }
+  return 0;
+}
+
+float* g_dbg_a = nullptr;
+float* g_dbg_b = nullptr;
+
 int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (p.M <= 0 || p.N <= 0) return 0;
+  p.dbg_a = g_dbg_a;
+  p.dbg_b = g_dbg_b;
+  const bool bx = uses_bx3(variant);
+  if (bx) {
+    // MONET_TMA_MASK (debug): bit 0 enables TMA for A, bit 1 for B (default 3)
+    static const int mask = getenv("MONET_TMA_MASK") ? atoi(getenv("MONET_TMA_MASK")) : 3;
+    p.mn_seg = 128;
+    p.a.tma = (mask & 1) ? make_tma(p, p.a, &p.tma_a) : 0;
+    p.b.tma = (mask & 2) ? make_tma(p, p.b, &p.tma_b) : 0;
+  }
   p.split_tf32 = variant == MONET_CONV_TF32 ? 0 : 1;
   p.m_tiles = (p.M + BM - 1) / BM;
   p.n_tiles = (p.N + BN - 1) / BN;
@@ -76,12 +199,13 @@ int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_b
     need = 0;
   }
   p.kb_per_split = (kblocks + splits - 1) / splits;
+  if (bx) p.kb_per_split = (p.kb_per_split + 1) & ~1;  // bf16x3 stages hold two raw k-blocks
   p.splits = (kblocks + p.kb_per_split - 1) / p.kb_per_split;
   p.ws = static_cast<float*>(ws);
   p.epi = p.splits > 1 ? EPI_PARTIAL : (accumulate ? EPI_ACCUM : EPI_STORE);
   const int tiles = p.m_tiles * p.n_tiles * p.splits;
   const int grid = std::min(tiles, kNumSMs);
-  if (int e = dispatch_gemm(p, grid, st)) return e;
+  if (int e = bx ? dispatch_modes<true>(p, grid, st) : dispatch_modes<false>(p, grid, st)) return e;
   if (p.splits > 1) {
     long long total = (long long)p.M * p.N;
     splitk_reduce_kernel<<<ew_blocks(total), kEwThreads, 0, st>>>(p.ws, p.c, p.M, p.N, p.ldc, p.splits, accumulate);
@@ -159,6 +283,13 @@ int monet_device_check(void) {
   cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
   cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
   return (major == 10 && minor == 0) ? 0 : -2;
+}
+
+// debug hook (not part of the product path): the bf16x3 splitters dump the raw
+// operands they consume to these device buffers ([rows][K padded to 64])
+void monet_debug_dump(float* a_dump, float* b_dump) {
+  g_dbg_a = a_dump;
+  g_dbg_b = b_dump;
 }
 
 int monet_copy_async(void* dst, const void* src, size_t bytes, void* stream) {

@@ -1,0 +1,654 @@
+// bf16x3 tcgen05 persistent GEMM with the A operand staged in TMEM.
+//
+// Why this shape (profiles/ncu_gemm_r1.md): the 3xTF32 kernel (gemm_tc.cuh)
+// is shared-memory-bandwidth bound -- every operand element crosses the
+// 128 B/clk smem port five times (cp.async in, read back, hi + lo written,
+// read three times by the MMAs) and the tensor pipe idles at ~25%.  Here:
+//
+//   * fp32 x = b0 + b1 with b0 = bf16(x), b1 = bf16(x - b0); the product
+//     x*y ~= a0*b0 + a0*b1 + a1*b0 drops only terms of relative size 2^-18,
+//     so three kind::f16 (bf16) MMAs -- at twice the TF32 rate -- give ~1e-5
+//     relative accuracy, inside the rel 1e-4 parity bar;
+//   * the A tile never goes back to shared memory: four "A-split" warps read
+//     their own row of the raw fp32 tile, split it in registers and write
+//     a_hi / a_lo straight into TMEM with tcgen05.st; the MMAs read A from
+//     TMEM and only B (bf16 hi / lo, half the bytes of fp32) from smem.
+//
+// Warp roles (672 threads, one CTA per SM, persistent over output tiles):
+//   warps 0-7   loaders (threads 0-127 A, 128-255 B): the raw fp32 k-block
+//               (BK = 32) of each operand arrives by TMA -- tiled 2D / 3D maps
+//               for plain operands, im2col maps (zero fill for padding) for
+//               the fprop / stride-1 dgrad / wgrad gathers -- issued by one
+//               thread and completing on the slot's mbarrier (expect_tx);
+//               shapes TMA cannot express (the 4-channel stem, stride-2
+//               dgrad) fall back to 16B cp.async groups from 128 threads
+//               (cp.async.mbarrier.arrive.noinc)
+//   warps 8-11  A-split: row r = lane quarter; LDS the row, split, tcgen05.st
+//               into the TMEM A stage (two raw k-blocks = one BK=64 stage)
+//   warps 12-15 B-split: raw fp32 -> bf16 hi / lo SWIZZLE_128B tiles
+//   warps 16-19 epilogue: tcgen05.ld the 128x128 fp32 accumulator
+//   warp  20    MMA issuer (one lane) and TMEM owner
+#pragma once
+#include "gemm_tc.cuh"
+
+namespace monet {
+namespace bx3 {
+
+constexpr int BM = 128, BN = 128;
+constexpr int BKR = 32;              // raw k-block (fp32, 128B rows)
+constexpr int BKS = 64;              // MMA stage (bf16, 128B rows) = 2 raw k-blocks
+constexpr int kRawSlots = 4;
+constexpr int kRawTile = BM * BKR * 4;          // 16 KB (A or B raw, fp32)
+constexpr int kRawBytes = 2 * kRawTile;          // A + B
+constexpr int kStages = 2;                       // MMA stages (TMEM A + smem B)
+constexpr int kBTile = BN * BKS * 2;             // 16 KB (bf16 hi or lo)
+constexpr int kStageBytes = 2 * kBTile;          // B hi + B lo
+constexpr int kLoaderWarps = 8, kASplitWarps = 4, kBSplitWarps = 4, kEpiWarps = 4;
+constexpr int kLoaderThreads = kLoaderWarps * 32;
+constexpr int kWarpASplit = kLoaderWarps;                       // 8
+constexpr int kWarpBSplit = kWarpASplit + kASplitWarps;         // 12
+constexpr int kWarpEpi = kWarpBSplit + kBSplitWarps;            // 16
+constexpr int kWarpMma = kWarpEpi + kEpiWarps;                  // 20
+constexpr int kThreads = (kWarpMma + 1) * 32;                   // 672
+constexpr int kAccStages = 2;
+constexpr int kTmemCols = 512;
+constexpr int kTmemA = kAccStages * BN;          // A stages start at column 256
+constexpr int kAStageCols = 64;                  // 32 cols hi + 32 cols lo (bf16x2 per column)
+constexpr int kChunkStages = 8;                  // flush the TMEM accumulation chain every 8 stages
+constexpr int kNumBars = 2 * kRawSlots + 3 * kStages + 2 * kAccStages;
+constexpr int kSmemBytes = kRawSlots * kRawBytes + kStages * kStageBytes + 1024 + 8 * kNumBars + 16;
+static_assert(kLoaderThreads == 256, "loader threads: 128 per operand");
+static_assert(kTmemA + kStages * kAStageCols <= kTmemCols, "TMEM budget");
+
+MONET_DEV void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// two fp32 -> packed bf16x2 (lo half = first argument), round to nearest even
+MONET_DEV uint32_t pack_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// split a pair: hi2 = bf16x2(a, b); lo2 = bf16x2(a - hi(a), b - hi(b))
+MONET_DEV void split_pair(float a, float b, uint32_t& hi2, uint32_t& lo2) {
+  hi2 = pack_bf16x2(a, b);
+  const float ah = __uint_as_float(hi2 << 16);
+  const float bh = __uint_as_float(hi2 & 0xFFFF0000u);
+  lo2 = pack_bf16x2(a - ah, b - bh);
+}
+
+template <int N>
+MONET_DEV void tmem_st(uint32_t taddr, const uint32_t (&r)[N]);
+
+template <>
+MONET_DEV void tmem_st<16>(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+MONET_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// D[tmem] (+)= A[tmem] * B[smem]^T, kind::f16 (bf16 in, fp32 accumulate), one CTA.
+MONET_DEV void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int b_mn_major) {
+  return (1u << 4)                 // D format F32
+         | (1u << 7)               // A format BF16
+         | (1u << 10)              // B format BF16
+         | ((uint32_t)b_mn_major << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// B stage tile descriptors (bf16, SWIZZLE_128B), k16 slice kk (0..3).
+//   K-major : rows n (128B = 64 k each), 8-row groups every 1024 B; k16 = +32 B
+//   MN-major: 64-element MN chunks of 64 k-rows x 128 B (8 KB, LBO), 8-row
+//             k groups every 1024 B (SBO); k16 = 16 rows = +2048 B
+MONET_DEV uint64_t b_desc(uint32_t tile, bool mn, int kk) {
+  if (mn) return smem_desc(tile + kk * 2048, BKS * 128, 1024, 2);
+  return smem_desc(tile + kk * 32, 16, 1024, 2);
+}
+
+// byte offset of bf16 element (n, k) inside a B stage tile (k in 0..63)
+MONET_DEV uint32_t b_off_kmajor(int n, int k) {
+  const int g = k >> 3;  // 16B granule = 8 bf16
+  return n * 128 + (((g ^ (n & 7)) << 4) | ((k & 7) << 1));
+}
+MONET_DEV uint32_t b_off_mnmajor(int n, int k) {
+  const int g = (n & 63) >> 3;
+  return (n >> 6) * (BKS * 128) + k * 128 + (((g ^ (k & 7)) << 4) | ((n & 7) << 1));
+}
+
+MONET_DEV void tile_range(const GemmParams& p, int tile, int& mt, int& nt, int& kb0, int& nstage) {
+  int sp;
+  tile_coords(p, tile, mt, nt, sp);
+  int kb1;
+  kb_range(p, sp, kb0, kb1);
+  nstage = (kb1 - kb0 + 1) / 2;  // kb_per_split is even; only the last split may be odd -> zero-padded
+}
+
+
+// ------------------------------------------------------------------ loaders
+MONET_DEV void mbar_arrive_tx(uint64_t* bar, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(tx) : "memory");
+}
+MONET_DEV void tma_2d(uint32_t dst, const CUtensorMap* m, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(dst),
+      "l"(m), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+MONET_DEV void tma_3d(uint32_t dst, const CUtensorMap* m, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(dst),
+      "l"(m), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+// im2col: coordinates {c, w, h, n} of the base pixel, offsets {w, h} of the filter tap
+MONET_DEV void tma_im2col(uint32_t dst, const CUtensorMap* m, int c, int w, int h, int n, int ow, int oh,
+                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+      "%5}], [%6], {%7, %8};" ::"r"(dst),
+      "l"(m), "r"(c), "r"(w), "r"(h), "r"(n), "r"(smem_u32(bar)), "h"((uint16_t)ow), "h"((uint16_t)oh)
+      : "memory");
+}
+
+// Address of the 4-element group starting at (row, k) -- generic fallback with
+// divisions.  K-major modes: k..k+3 contiguous; MN-major: row..row+3 contiguous.
+// Returns nullptr for padding / out-of-range groups (zero fill).
+template <int MODE>
+MONET_DEV const float* group_ptr(const GemmParams& p, const Operand& op, int row, int k) {
+  const ConvGeom& g = p.g;
+  if (row >= op.rows || k >= p.Kd) return nullptr;
+  if constexpr (MODE == OP_KMAJOR) {
+    return op.ptr + (long long)row * op.ld + k;
+  } else if constexpr (MODE == OP_MNMAJOR) {
+    const int kh = k / op.kdiv, kl = k - kh * op.kdiv;
+    return op.ptr + kh * op.ks1 + (long long)kl * op.ld + row;
+  } else if constexpr (MODE == OP_IM2COL_FPROP) {
+    const int q = row % g.Q, t = row / g.Q, pp = t % g.P, n = t / g.P;
+    const int tap = k / g.C, c = k - tap * g.C, r = tap / g.S, s = tap - r * g.S;
+    const int h = pp * g.sh - g.ph + r, w = q * g.sw - g.pw + s;
+    if ((unsigned)h >= (unsigned)g.H || (unsigned)w >= (unsigned)g.W) return nullptr;
+    return op.ptr + (((long long)n * g.H + h) * g.W + w) * g.C + c;
+  } else if constexpr (MODE == OP_IM2COL_DGRAD) {
+    const int w = row % g.W, t = row / g.W, h = t % g.H, n = t / g.H;
+    const int tap = k / g.K, ko = k - tap * g.K, r = tap / g.S, s = tap - r * g.S;
+    const int hp = h + g.ph - r, wp = w + g.pw - s;
+    if (hp < 0 || wp < 0) return nullptr;
+    const int pp = hp / g.sh, q = wp / g.sw;
+    if (pp * g.sh != hp || q * g.sw != wp || pp >= g.P || q >= g.Q) return nullptr;
+    return op.ptr + (((long long)n * g.P + pp) * g.Q + q) * g.K + ko;
+  } else {  // OP_IM2COL_WGRAD: rows (tap, c), k = output pixel
+    const int tap = row / g.C, c = row - tap * g.C, r = tap / g.S, s = tap - r * g.S;
+    const int q = k % g.Q, t = k / g.Q, pp = t % g.P, n = t / g.P;
+    const int h = pp * g.sh - g.ph + r, w = q * g.sw - g.pw + s;
+    if ((unsigned)h >= (unsigned)g.H || (unsigned)w >= (unsigned)g.W) return nullptr;
+    return op.ptr + (((long long)n * g.H + h) * g.W + w) * g.C + c;
+  }
+}
+
+// Raw k-block layouts in smem (what the splitters read):
+//   K-major : 128 rows x 128 B, SWIZZLE_128B (16B chunk c of row r at
+//             r*128 + ((c ^ (r & 7)) << 4)) -- TMA tiled / im2col box layout
+//   MN-major: segment-major, `seg` rows per segment (128, or C = 32 / 64 for a
+//             wgrad tile spanning several taps): element (row, k) at
+//             (row / seg) * 32 * seg * 4 + k * seg * 4 + (row % seg) * 4
+MONET_DEV uint32_t mn_off(int row, int kr, int seg) {
+  const int sg = row / seg;
+  return sg * (BKR * seg * 4) + kr * seg * 4 + (row - sg * seg) * 4;
+}
+
+// One operand's loader.  TMA operands: one elected thread (sub == 0) issues
+// the whole k-block; fallback operands: 128 threads issue 16B cp.async groups.
+template <int MODE>
+struct Loader {
+  static constexpr bool kMN = mode_is_mn(MODE);
+  int row0, k0;
+  int cw, chh, cn;          // im2col base pixel of the tile (FPROP / DGRAD)
+  int kin0, tap_r, tap_s;   // k-block decomposition (FPROP / DGRAD)
+
+  MONET_DEV void init(const GemmParams& p, const Operand& op, int row0_, int k0_) {
+    const ConvGeom& g = p.g;
+    row0 = row0_;
+    k0 = k0_;
+    if (op.tma != 2) return;
+    if constexpr (MODE == OP_IM2COL_FPROP || MODE == OP_IM2COL_DGRAD) {
+      const bool fp = MODE == OP_IM2COL_FPROP;
+      const int X = fp ? g.Q : g.W, Y = fp ? g.P : g.H;
+      const int x = row0 % X, t = row0 / X, y = t % Y;
+      cn = t / Y;
+      if (fp) {
+        cw = x * g.sw - g.pw;
+        chh = y * g.sh - g.ph;
+      } else {
+        cw = x - (g.S - 1 - g.pw);
+        chh = y - (g.R - 1 - g.ph);
+      }
+      const int cx = fp ? g.C : g.K;
+      const int tap = k0 / cx;
+      kin0 = k0 - tap * cx;
+      tap_r = tap / g.S;
+      tap_s = tap - tap_r * g.S;
+    }
+  }
+
+  MONET_DEV void issue_tma(const GemmParams& p, const Operand& op, const CUtensorMap* m, int kb, uint8_t* tile,
+                           uint64_t* bar) {
+    const ConvGeom& g = p.g;
+    const uint32_t dst = smem_u32(tile);
+    const int k = kb * BKR;
+    if constexpr (MODE == OP_KMAJOR) {
+      mbar_arrive_tx(bar, BM * BKR * 4);
+      tma_2d(dst, m, k, row0, bar);
+    } else if constexpr (MODE == OP_MNMAJOR) {
+      mbar_arrive_tx(bar, BM * BKR * 4);
+      if (op.kdiv >= p.Kd) {
+        tma_2d(dst, m, row0, k, bar);
+      } else {  // k = tap * kdiv + kout, kdiv % 32 == 0: tensor {rows, taps, kdiv}
+        const int kh = k / op.kdiv;
+        tma_3d(dst, m, row0, kh, k - kh * op.kdiv, bar);
+      }
+    } else if constexpr (MODE == OP_IM2COL_FPROP || MODE == OP_IM2COL_DGRAD) {
+      mbar_arrive_tx(bar, BM * BKR * 4);
+      if (k < p.Kd) {
+        const int ow = MODE == OP_IM2COL_FPROP ? tap_s : g.S - 1 - tap_s;
+        const int oh = MODE == OP_IM2COL_FPROP ? tap_r : g.R - 1 - tap_r;
+        tma_im2col(dst, m, kin0, cw, chh, cn, ow, oh, bar);
+      } else {  // zero-padded tail k-block: out-of-range channel coordinate -> zero fill
+        tma_im2col(dst, m, MODE == OP_IM2COL_FPROP ? g.C : g.K, cw, chh, cn, 0, 0, bar);
+      }
+      const int cx = MODE == OP_IM2COL_FPROP ? g.C : g.K;
+      kin0 += BKR;
+      if (kin0 >= cx) {
+        kin0 = 0;
+        if (++tap_s == g.S) {
+          tap_s = 0;
+          ++tap_r;
+        }
+      }
+    } else {  // IM2COL_WGRAD: rows (tap, c) in segments of p.mn_seg channels, k = 32 output pixels
+      const int seg = p.mn_seg;
+      mbar_arrive_tx(bar, BN * BKR * 4);
+      const int q = k % g.Q, t = k / g.Q, pp = t % g.P, n = t / g.P;
+      const int w0 = q * g.sw - g.pw, h0 = pp * g.sh - g.ph;
+      for (int sg = 0; sg < BN / seg; ++sg) {
+        const int row = row0 + sg * seg;
+        const int tap = row / g.C, c = row - tap * g.C;
+        const int r = tap / g.S, s = tap - r * g.S;
+        // rows past R*S*C: the tap offset stays in range, the channel
+        // coordinate is pushed out of bounds (zero fill)
+        const bool valid = tap < g.R * g.S && k < p.Kd;
+        tma_im2col(dst + sg * (BKR * seg * 4), m, valid ? c : g.C, w0, h0, n, valid ? s : 0, valid ? r : 0, bar);
+      }
+    }
+  }
+
+  MONET_DEV void issue_fallback(const GemmParams& p, const Operand& op, int kb, int sub, uint8_t* tile,
+                                uint64_t* bar) {
+    const int kk0 = kb * BKR;
+#pragma unroll 2
+    for (int i = 0; i < 8; ++i) {
+      int row, k;
+      uint32_t off;
+      if constexpr (kMN) {
+        const int kr = (sub >> 5) + 4 * i;
+        const int r = 4 * (sub & 31);
+        row = row0 + r;
+        k = kk0 + kr;
+        off = mn_off(r, kr, MODE == OP_IM2COL_WGRAD ? p.mn_seg : BN);
+      } else {
+        const int r = (sub >> 3) + 16 * i;
+        row = row0 + r;
+        k = kk0 + 4 * (sub & 7);
+        off = sw128_offset(r, sub & 7);
+      }
+      const float* src = group_ptr<MODE>(p, op, row, k);
+      const uint32_t dst = smem_u32(tile + off);
+      if (op.aligned || src == nullptr) {
+        cp_async16(dst, src, op.ptr);
+      } else {
+        const int cnt = kMN ? op.rows - row : p.Kd - k;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) cp_async4(dst + 4 * e, e < cnt ? src + e : op.ptr, e < cnt);
+      }
+    }
+    cp_async_mbar_arrive(bar);
+  }
+};
+template <int AM, int BMODE>
+__global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_constant__ GemmParams p) {
+  constexpr bool a_mn = mode_is_mn(AM), b_mn = mode_is_mn(BMODE);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* raw = smem;                                  // kRawSlots x (A, B) fp32
+  uint8_t* bst = smem + kRawSlots * kRawBytes;          // kStages x (B hi, B lo) bf16
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bst + kStages * kStageBytes);
+  uint64_t* raw_full = bars;                            // loaders -> splitters
+  uint64_t* raw_empty = raw_full + kRawSlots;           // splitters -> loaders
+  uint64_t* a_full = raw_empty + kRawSlots;             // A-split -> MMA
+  uint64_t* b_full = a_full + kStages;                  // B-split -> MMA
+  uint64_t* st_empty = b_full + kStages;                // MMA commit -> splitters
+  uint64_t* tfull = st_empty + kStages;                 // MMA commit -> epilogue
+  uint64_t* tempty = tfull + kAccStages;                // epilogue -> MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAccStages);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int n_tiles_total = p.m_tiles * p.n_tiles * p.splits;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRawSlots; ++s) {
+      mbar_init(&raw_full[s], (p.a.tma ? 1 : 128) + (p.b.tma ? 1 : 128));
+      mbar_init(&raw_empty[s], (kASplitWarps + kBSplitWarps) * 32);
+    }
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&a_full[s], kASplitWarps * 32);
+      mbar_init(&b_full[s], kBSplitWarps * 32);
+      mbar_init(&st_empty[s], 1);
+    }
+    for (int a = 0; a < kAccStages; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], kEpiWarps * 32);
+    }
+    mbar_fence_init();
+  }
+  if (warp == kWarpMma) tmem_alloc(tmem_slot, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp < kLoaderWarps) {
+    // ---------------------------------------------------------------- loaders
+    const int sub = threadIdx.x & 127;
+    const bool is_b = threadIdx.x >= 128;
+    const Operand& op = is_b ? p.b : p.a;
+    const bool active = !op.tma || sub == 0;  // one thread issues a TMA operand
+    Loader<AM> la;
+    Loader<BMODE> lb;
+    int item = 0;
+    for (int tile = active ? (int)blockIdx.x : n_tiles_total; tile < n_tiles_total; tile += gridDim.x) {
+      int mt, nt, kb0, nst;
+      tile_range(p, tile, mt, nt, kb0, nst);
+      if (is_b)
+        lb.init(p, p.b, nt * BN, kb0 * BKR);
+      else
+        la.init(p, p.a, mt * BM, kb0 * BKR);
+      for (int kb = kb0; kb < kb0 + 2 * nst; ++kb, ++item) {
+        const int slot = item % kRawSlots;
+        mbar_wait(&raw_empty[slot], ((item / kRawSlots) & 1) ^ 1);
+        uint8_t* base = raw + slot * kRawBytes;
+        if (is_b) {
+          if (op.tma)
+            lb.issue_tma(p, op, &p.tma_b, kb, base + kRawTile, &raw_full[slot]);
+          else
+            lb.issue_fallback(p, op, kb, sub, base + kRawTile, &raw_full[slot]);
+        } else {
+          if (op.tma)
+            la.issue_tma(p, op, &p.tma_a, kb, base, &raw_full[slot]);
+          else
+            la.issue_fallback(p, op, kb, sub, base, &raw_full[slot]);
+        }
+      }
+    }
+    cp_async_wait<0>();
+  } else if (warp < kWarpBSplit) {
+    // ---------------------------------------------------------------- A split -> TMEM
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_sel = (uint32_t)(quarter * 32) << 16;
+    int item = 0, stage_item = 0;
+    for (int tile = blockIdx.x; tile < n_tiles_total; tile += gridDim.x) {
+      int mt, nt, kb0, nst;
+      tile_range(p, tile, mt, nt, kb0, nst);
+      const int item_kb0 = kb0;
+      for (int s = 0; s < nst; ++s, ++stage_item) {
+        const int stage = stage_item % kStages;
+        mbar_wait(&st_empty[stage], ((stage_item / kStages) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t a_hi = tmem_base + lane_sel + kTmemA + stage * kAStageCols;
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half, ++item) {
+          const int slot = item % kRawSlots;
+          mbar_wait(&raw_full[slot], (item / kRawSlots) & 1);
+          const uint8_t* rt = raw + slot * kRawBytes;
+          float v[32];
+          if constexpr (a_mn) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) v[k] = *reinterpret_cast<const float*>(rt + k * (BM * 4) + row * 4);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const float4 q = *reinterpret_cast<const float4*>(rt + sw128_offset(row, c));
+              v[4 * c] = q.x;
+              v[4 * c + 1] = q.y;
+              v[4 * c + 2] = q.z;
+              v[4 * c + 3] = q.w;
+            }
+          }
+          if (p.dbg_a != nullptr) {
+            const long long kpad = (long long)((p.Kd + 63) / 64) * 64;
+            const int kb = (item_kb0 + 2 * s + half);
+            const int m = mt * BM + row;
+            if (m < p.M)
+              for (int k = 0; k < 32; ++k) p.dbg_a[m * kpad + kb * 32 + k] = v[k];
+          }
+          uint32_t hi[16], lo[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) split_pair(v[2 * j], v[2 * j + 1], hi[j], lo[j]);
+          // release the raw slot only once every loaded value has been consumed:
+          // the next TMA into it is an async-proxy write that is not ordered
+          // behind LDS still in flight
+          mbar_arrive(&raw_empty[slot]);
+          tmem_st<16>(a_hi + half * 16, hi);
+          tmem_st<16>(a_hi + 32 + half * 16, lo);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&a_full[stage]);
+      }
+    }
+  } else if (warp < kWarpEpi) {
+    // ---------------------------------------------------------------- B split -> smem bf16
+    const int t = threadIdx.x - kWarpBSplit * 32;  // 0..127
+    int item = 0, stage_item = 0;
+    for (int tile = blockIdx.x; tile < n_tiles_total; tile += gridDim.x) {
+      int mt, nt, kb0, nst;
+      tile_range(p, tile, mt, nt, kb0, nst);
+      for (int s = 0; s < nst; ++s, ++stage_item) {
+        const int stage = stage_item % kStages;
+        mbar_wait(&st_empty[stage], ((stage_item / kStages) & 1) ^ 1);
+        uint8_t* bhi = bst + stage * kStageBytes;
+        uint8_t* blo = bhi + kBTile;
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half, ++item) {
+          const int slot = item % kRawSlots;
+          mbar_wait(&raw_full[slot], (item / kRawSlots) & 1);
+          const uint8_t* rt = raw + slot * kRawBytes + kRawTile;
+          // K-major: a warp covers rows {0,4,1,5}+base so that the two rows of
+          // one 16-lane STS.64 phase land in opposite swizzle halves
+          const int w4 = t >> 5, l = t & 31;
+          const int rbase = 8 * (w4 >> 1) + 2 * (w4 & 1) + (((l >> 3) & 1) << 2) + (l >> 4);
+          float4 q[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            uint32_t off;
+            if constexpr (b_mn) {
+              off = mn_off(4 * (t & 31), (t >> 5) + 4 * i, p.mn_seg);
+            } else {
+              off = sw128_offset(rbase + 16 * i, t & 7);
+            }
+            q[i] = *reinterpret_cast<const float4*>(rt + off);
+          }
+          if (p.dbg_b != nullptr) {
+            const long long kpad = (long long)((p.Kd + 63) / 64) * 64;
+            const int kb = kb0 + 2 * s + half;
+            for (int i = 0; i < 8; ++i) {
+              const float e[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
+              for (int j = 0; j < 4; ++j) {
+                int n, k;
+                if (b_mn) {
+                  n = 4 * (t & 31) + j;
+                  k = (t >> 5) + 4 * i;
+                } else {
+                  n = rbase + 16 * i;
+                  k = 4 * (t & 7) + j;
+                }
+                n += nt * BN;
+                if (n < p.N) p.dbg_b[n * kpad + kb * 32 + k] = e[j];
+              }
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            uint2 h, lw;
+            split_pair(q[i].x, q[i].y, h.x, lw.x);
+            split_pair(q[i].z, q[i].w, h.y, lw.y);
+            uint32_t off;
+            if constexpr (b_mn) {
+              off = b_off_mnmajor(4 * (t & 31), 32 * half + (t >> 5) + 4 * i);
+            } else {
+              off = b_off_kmajor(rbase + 16 * i, 32 * half + 4 * (t & 7));
+            }
+            *reinterpret_cast<uint2*>(bhi + off) = h;
+            *reinterpret_cast<uint2*>(blo + off) = lw;
+          }
+          mbar_arrive(&raw_empty[slot]);  // after all loaded values are consumed (see A split)
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&b_full[stage]);
+      }
+    }
+  } else if (warp < kWarpMma) {
+    // ---------------------------------------------------------------- epilogue
+    const int quarter = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < n_tiles_total; tile += gridDim.x) {
+      int mt, nt, sp, kb0, kb1;
+      tile_coords(p, tile, mt, nt, sp);
+      kb_range(p, sp, kb0, kb1);
+      const int nst = (kb1 - kb0 + 1) / 2;
+      const int nchunks = (nst + kChunkStages - 1) / kChunkStages;
+      const int m = mt * BM + quarter * 32 + lane;
+      for (int chunk = 0; chunk < nchunks; ++chunk) {
+        const bool add_old = chunk > 0 || p.epi == EPI_ACCUM;
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        for (int cc = 0; cc < BN / 32; ++cc) {
+          float v[32];
+          tmem_ld32(tmem_base + acc * BN + cc * 32 + ((uint32_t)(quarter * 32) << 16), v);
+          const int n0 = nt * BN + cc * 32;
+          if (m < p.M && n0 < p.N) {
+            float* dst;
+            long long ld;
+            if (p.epi == EPI_PARTIAL) {
+              dst = p.ws + (long long)sp * p.M * p.N + (long long)m * p.N + n0;
+              ld = p.N;
+            } else {
+              dst = p.c + (long long)m * p.ldc + n0;
+              ld = p.ldc;
+            }
+            const int ncols = min(32, p.N - n0);
+            const bool vec = (ncols == 32) && ((ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
+            if (vec) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) {
+                float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                if (add_old) {
+                  const float4 c = *reinterpret_cast<const float4*>(dst + j);
+                  o.x += c.x;
+                  o.y += c.y;
+                  o.z += c.z;
+                  o.w += c.w;
+                }
+                *reinterpret_cast<float4*>(dst + j) = o;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                if (j < ncols) {
+                  float o = v[j];
+                  if (add_old) o += dst[j];
+                  dst[j] = o;
+                }
+              }
+            }
+          }
+          __syncwarp();
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        if (++acc == kAccStages) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- MMA issuer
+    const uint32_t idesc = idesc_bf16(BM, BN, b_mn ? 1 : 0);
+    int stage_item = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < n_tiles_total; tile += gridDim.x) {
+      int mt, nt, kb0, nst;
+      tile_range(p, tile, mt, nt, kb0, nst);
+      for (int c0 = 0; c0 < nst; c0 += kChunkStages) {
+        const int c1 = min(nst, c0 + kChunkStages);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int s = c0; s < c1; ++s, ++stage_item) {
+          const int stage = stage_item % kStages;
+          const uint32_t ph = (stage_item / kStages) & 1;
+          mbar_wait(&a_full[stage], ph);
+          mbar_wait(&b_full[stage], ph);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a_hi = tmem_base + kTmemA + stage * kAStageCols;
+            const uint32_t a_lo = a_hi + 32;
+            const uint32_t bhi = smem_u32(bst + stage * kStageBytes);
+            const uint32_t blo = bhi + kBTile;
+#pragma unroll
+            for (int kk = 0; kk < BKS / 16; ++kk) {
+              const uint32_t first = (s == c0 && kk == 0) ? 0u : 1u;
+              mma_bf16_ts(d_tmem, a_lo + kk * 8, b_desc(bhi, b_mn, kk), idesc, first);
+              mma_bf16_ts(d_tmem, a_hi + kk * 8, b_desc(blo, b_mn, kk), idesc, 1u);
+              mma_bf16_ts(d_tmem, a_hi + kk * 8, b_desc(bhi, b_mn, kk), idesc, 1u);
+            }
+            mma_commit(&st_empty[stage]);
+            if (s == c1 - 1) mma_commit(&tfull[acc]);
+          }
+          __syncwarp();
+        }
+        if (++acc == kAccStages) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kWarpMma) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, kTmemCols);
+  }
+}
+
+}  // namespace bx3
+}  // namespace monet

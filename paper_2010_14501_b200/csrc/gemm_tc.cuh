@@ -17,6 +17,8 @@
 // modes are template parameters so every instantiation is branch-free in its
 // producer loop.
 #pragma once
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace monet {
@@ -45,6 +47,7 @@ struct Operand {
   int kdiv;
   long long ks1;
   int aligned;  // 16B groups are aligned and never straddle an edge (host-checked)
+  int tma;      // bf16x3 kernel: 0 = 16B cp.async groups, 1 = TMA tiled map, 2 = TMA im2col map
 };
 
 enum EpiMode : int { EPI_STORE = 0, EPI_ACCUM = 1, EPI_PARTIAL = 2 };
@@ -61,6 +64,10 @@ struct GemmParams {
   int kb_per_split;
   int m_tiles, n_tiles;
   int split_tf32;   // 1: 3xTF32 (hi/lo), 0: plain tf32
+  int mn_seg;       // bf16x3: rows per segment of the MN-major raw B layout (128, or C for wgrad)
+  float* dbg_a;     // debug: bf16x3 A-split dumps the raw A operand [M][Kpad] here (nullptr = off)
+  float* dbg_b;     // debug: bf16x3 B-split dumps the raw B operand [N][Kpad]
+  CUtensorMap tma_a, tma_b;  // bf16x3: TMA descriptors (valid when Operand::tma != 0)
 };
 
 constexpr int BM = 128, BN = 128, BK = 32;

@@ -1,9 +1,10 @@
 """Numerics of every sm_100a kernel against a plain PyTorch reference of the same op.
 
 Floating-point ops are compared with a float64 CPU torch computation of the
-same formula; the tolerance is max|gpu - ref| / max|ref| <= 2e-5 for the
-3xTF32 tensor-core paths (fp32-level accuracy) and 1e-5 for fp32 CUDA-core
-ops.  Bit-level outputs (ReLU sign masks, maxpool indices) are exact.
+same formula; the tolerance is max|gpu - ref| / max|ref| <= 5e-5 for the
+bf16x3 / 3xTF32 tensor-core paths (products carry ~2^-17 relative error, so
+the sums land near 1e-5; the engine-level parity bar is 1e-4) and 1e-5 for
+fp32 CUDA-core ops.  Bit-level outputs (ReLU sign masks, maxpool indices) are exact.
 """
 import math
 
@@ -16,7 +17,7 @@ from paper_2010_14501_b200 import _native as N
 
 pytestmark = pytest.mark.gpu
 
-REL_TC = 2e-5     # 3xTF32 tensor-core conv / gemm
+REL_TC = 5e-5     # bf16x3 / 3xTF32 tensor-core conv / gemm
 REL_TF32 = 3e-3   # single-pass tf32 variant
 REL_EW = 1e-5     # CUDA-core fp32 kernels
 
@@ -47,11 +48,14 @@ CONV_CASES = [
     (2, 32, 32, 4, 64, 7, 7, 2, 3),
     (4, 7, 7, 256, 96, 3, 3, 1, 1),
     (1, 5, 6, 8, 12, 3, 3, 1, 1),
+    (2, 10, 10, 64, 64, 3, 3, 1, 1),     # wgrad row tile spans two taps (bulk segments)
+    (1, 6, 6, 192, 64, 3, 3, 1, 1),      # C % 128 != 0: wgrad falls back to 16B groups
+    (2, 12, 12, 64, 32, 3, 3, 2, 1),     # stride-2 dgrad gather, K = 32
 ]
 
 
 @pytest.mark.parametrize("case", CONV_CASES)
-@pytest.mark.parametrize("variant", ["implicit", "splitk"])
+@pytest.mark.parametrize("variant", ["implicit", "splitk", "tf32x3"])
 def test_conv_passes(cuda, case, variant):
     n, h, w, c, k, r, s, stride, pad = case
     g = torch.Generator().manual_seed(0)
@@ -118,7 +122,7 @@ def test_gemm_layouts(cuda, mnk, amn, bmn):
     ldb = n if bmn else k
     C = torch.zeros(m, n, device=cuda)
     ad, bd = a_store.to(cuda), b_store.to(cuda)
-    for variant in (0, 1):
+    for variant in (0, 1, 3):
         wsb = N.lib().gemm_ws_bytes(variant, m, n, k)
         ws = torch.empty(wsb // 4 + 1, device=cuda)
         N.lib().gemm(variant, ad.data_ptr(), amn, lda, bd.data_ptr(), bmn, ldb,

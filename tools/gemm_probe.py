@@ -1,5 +1,10 @@
 """GPU probe of the tcgen05 GEMM layouts (debug tool)."""
+import sys
+from pathlib import Path
+
 import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2010_14501_b200 import _native as N
 
 lib = N.lib()
@@ -26,7 +31,7 @@ for (m, n, k) in [(128, 128, 32), (128, 128, 64), (200, 1000, 2048), (256, 128, 
     for amn, bmn in [(0, 0), (0, 1), (1, 0), (1, 1)]:
         if (amn and m % 4) or (bmn and n % 4):
             continue
-        for v in (0, 2):
+        for v in (0, 3, 2):
             C = run(A, B, amn, bmn, v)
             err = (C.double() - ref).abs().max().item() / ref.abs().max().item()
             print(f"m{m} n{n} k{k} amn{amn} bmn{bmn} v{v}: rel {err:.3e} untouched {(C == -7).sum().item()} zeros {(C == 0).sum().item()}")
@@ -37,8 +42,8 @@ A = torch.zeros(m, k)
 for i in range(m):
     A[i, i % k] = 1.0
 B = torch.arange(n * k, dtype=torch.float32).view(n, k)  # B[n,k] = n*k + k
-for amn, bmn in [(0, 0), (0, 1), (1, 0)]:
-    C = run(A, B, amn, bmn, 2)
+for amn, bmn in [(0, 0), (0, 1), (1, 0), (1, 1)]:
+    C = run(A, B, amn, bmn, 0)
     ref = (A @ B.t())
     bad = (C != ref).nonzero()
     print("pattern", amn, bmn, "mismatches", bad.shape[0])
