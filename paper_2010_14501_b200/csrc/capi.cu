@@ -141,14 +141,16 @@ int make_tma(GemmParams& p, const Operand& op, CUtensorMap* m) {
     }
     case OP_MNMAJOR: {
       if (op.ld % 4) return 0;
-      if (op.kdiv >= p.Kd) {
+      if (op.kdiv >= p.Kd && !p.ph.on) {
         cuuint64_t dims[2] = {(cuuint64_t)op.rows, (cuuint64_t)p.Kd};
         cuuint64_t strides[1] = {(cuuint64_t)op.ld * 4};
         cuuint32_t box[2] = {128, 32};
         return tiled_map(m, op.ptr, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
       }
       if (op.kdiv % 32 || op.ks1 % 4 || p.Kd % op.kdiv) return 0;
-      cuuint64_t dims[3] = {(cuuint64_t)op.rows, (cuuint64_t)(p.Kd / op.kdiv), (cuuint64_t)op.kdiv};
+      // taps dimension: every filter tap (a stride phase addresses a subset by tap id)
+      const int ntaps = p.ph.on ? g.R * g.S : p.Kd / op.kdiv;
+      cuuint64_t dims[3] = {(cuuint64_t)op.rows, (cuuint64_t)ntaps, (cuuint64_t)op.kdiv};
       cuuint64_t strides[2] = {(cuuint64_t)op.ks1 * 4, (cuuint64_t)op.ld * 4};
       cuuint32_t box[3] = {128, 1, 32};
       return tiled_map(m, op.ptr, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
@@ -157,8 +159,12 @@ int make_tma(GemmParams& p, const Operand& op, CUtensorMap* m) {
       if (g.C % 32) return 0;
       return im2col_map(m, op.ptr, g.N, g.H, g.W, g.C, -g.pw, -g.ph, g.pw - (g.S - 1), g.ph - (g.R - 1), g.sw, g.sh,
                         32, 128, CU_TENSOR_MAP_SWIZZLE_128B);
-    case OP_IM2COL_DGRAD:  // forward conv over dy with flipped taps; stride 1 only
-      if (g.K % 32 || g.sh != 1 || g.sw != 1) return 0;
+    case OP_IM2COL_DGRAD:  // forward conv over dy with flipped taps; stride 1, or one stride phase
+      if (g.K % 32) return 0;
+      if (p.ph.on)
+        return im2col_map(m, op.ptr, g.N, g.P, g.Q, g.K, p.ph.lo_w, p.ph.lo_h, p.ph.Wp - g.Q + p.ph.lo_w,
+                          p.ph.Hp - g.P + p.ph.lo_h, 1, 1, 32, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+      if (g.sh != 1 || g.sw != 1) return 0;
       return im2col_map(m, op.ptr, g.N, g.P, g.Q, g.K, -(g.S - 1 - g.pw), -(g.R - 1 - g.ph), -g.pw, -g.ph, 1, 1, 32,
                         128, CU_TENSOR_MAP_SWIZZLE_128B);
     case OP_IM2COL_WGRAD: {
@@ -185,6 +191,9 @@ int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_b
     // MONET_TMA_MASK (debug): bit 0 enables TMA for A, bit 1 for B (default 3)
     static const int mask = getenv("MONET_TMA_MASK") ? atoi(getenv("MONET_TMA_MASK")) : 3;
     p.mn_seg = 128;
+    // MONET_CHUNK (debug): MMA stages (64 k each) per TMEM accumulation chain
+    static const int chunk = getenv("MONET_CHUNK") ? atoi(getenv("MONET_CHUNK")) : 16;
+    p.chunk_stages = chunk > 0 ? chunk : 16;
     p.a.tma = (mask & 1) ? make_tma(p, p.a, &p.tma_a) : 0;
     p.b.tma = (mask & 2) ? make_tma(p, p.b, &p.tma_b) : 0;
   }
@@ -192,7 +201,7 @@ int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_b
   p.m_tiles = (p.M + BM - 1) / BM;
   p.n_tiles = (p.N + BN - 1) / BN;
   const int kblocks = std::max(1, (p.Kd + BK - 1) / BK);
-  int splits = choose_splits(variant, p.M, p.N, p.Kd);
+  int splits = p.ph.on ? 1 : choose_splits(variant, p.M, p.N, p.Kd);  // phase rows scatter: no split-K
   size_t need = splits > 1 ? (size_t)splits * p.M * p.N * sizeof(float) : 0;
   if (need > ws_bytes || (need && ws == nullptr)) {
     splits = 1;  // never write outside the caller's workspace
@@ -266,6 +275,73 @@ GemmParams conv_params(int pass, const monet_conv_desc* d, const float* in0, con
   return p;
 }
 
+// Sub-pixel phases of a strided dgrad (bf16x3 path).  Returns false for an
+// empty phase grid; ntap == 0 means the phase's dx pixels receive no gradient.
+bool make_phase(const monet_conv_desc* d, int a, int b, PhaseInfo& ph) {
+  ph = PhaseInfo{};
+  ph.on = 1;
+  ph.a = a;
+  ph.b = b;
+  ph.Hp = (d->h - a + d->stride_h - 1) / d->stride_h;
+  ph.Wp = (d->w - b + d->stride_w - 1) / d->stride_w;
+  if (ph.Hp <= 0 || ph.Wp <= 0) return false;
+  ph.lo_h = ph.lo_w = 1 << 20;
+  for (int r = 0; r < d->r; ++r) {
+    const int nr = a + d->pad_h - r;
+    if (((nr % d->stride_h) + d->stride_h) % d->stride_h) continue;
+    for (int s = 0; s < d->s; ++s) {
+      const int ns = b + d->pad_w - s;
+      if (((ns % d->stride_w) + d->stride_w) % d->stride_w) continue;
+      const int dr = nr >= 0 ? nr / d->stride_h : -((-nr) / d->stride_h);
+      const int ds = ns >= 0 ? ns / d->stride_w : -((-ns) / d->stride_w);
+      ph.dr[ph.ntap] = (signed char)dr;
+      ph.ds[ph.ntap] = (signed char)ds;
+      ph.tap[ph.ntap] = (signed char)(r * d->s + s);
+      ph.lo_h = std::min(ph.lo_h, dr);
+      ph.lo_w = std::min(ph.lo_w, ds);
+      ++ph.ntap;
+    }
+  }
+  if (ph.ntap == 0) ph.lo_h = ph.lo_w = 0;
+  return true;
+}
+
+// stride >= 2 and R, S <= 8 keep every phase at <= 16 taps (PhaseInfo tables)
+bool use_phases(int variant, const monet_conv_desc* d) {
+  return uses_bx3(variant) && (d->stride_h > 1 || d->stride_w > 1) && d->r <= 8 && d->s <= 8;
+}
+
+GemmParams phase_params(const monet_conv_desc* d, const PhaseInfo& ph, const float* dy, const float* w, float* dx) {
+  GemmParams p{};
+  p.g = geom(d);
+  p.ph = ph;
+  p.M = d->n * ph.Hp * ph.Wp;
+  p.N = d->c;
+  p.Kd = ph.ntap * d->k;
+  p.a = op_gather(OP_IM2COL_DGRAD, dy, p.M);
+  // B[c, (t, kout)] = w[kout][tap[t]][c]
+  p.b = Operand{OP_MNMAJOR, d->c, w, (long long)d->r * d->s * d->c, d->k, (long long)d->c, al16(w) ? 1 : 0, 0};
+  p.c = dx;
+  p.ldc = d->c;
+  return p;
+}
+
+__global__ void dgrad_phase_zero_kernel(float* dx, int n, int h, int w, int c, int a, int b, int sh, int sw) {
+  const int hp = (h - a + sh - 1) / sh, wp = (w - b + sw - 1) / sw;
+  const long long total = (long long)n * hp * wp * (c / 4);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c4 = (int)(i % (c / 4));
+    long long t = i / (c / 4);
+    const int j = (int)(t % wp);
+    t /= wp;
+    const int ii = (int)(t % hp);
+    const int nn = (int)(t / hp);
+    float* dst = dx + (((long long)nn * h + ii * sh + a) * w + j * sw + b) * c + 4 * c4;
+    *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
 int check_desc(const monet_conv_desc* d) {
   if (!d || d->c % 4 || d->k % 4 || d->n <= 0) return -(int)cudaErrorInvalidValue;
   return 0;
@@ -303,6 +379,7 @@ size_t monet_conv_ws_bytes(int variant, int pass, const monet_conv_desc* d) {
   if (check_desc(d)) return 0;
   if (pass == MONET_PASS_BWD)
     return std::max(monet_conv_ws_bytes(variant, MONET_PASS_DGRAD, d), monet_conv_ws_bytes(variant, MONET_PASS_WGRAD, d));
+  if (pass == MONET_PASS_DGRAD && use_phases(variant, d)) return 0;  // phase GEMMs never split K
   GemmParams p = conv_params(pass, d, nullptr, nullptr, nullptr);
   return gemm_ws(variant, p.M, p.N, p.Kd);
 }
@@ -316,6 +393,22 @@ int monet_conv_fwd(int variant, const monet_conv_desc* d, const float* x, const 
 int monet_conv_dgrad(int variant, const monet_conv_desc* d, const float* dy, const float* w, float* dx,
                      int accumulate, void* ws, size_t ws_bytes, void* stream) {
   if (int e = check_desc(d)) return e;
+  if (use_phases(variant, d)) {  // stride > 1: one stride-1 GEMM per output parity class
+    for (int a = 0; a < d->stride_h; ++a)
+      for (int b = 0; b < d->stride_w; ++b) {
+        PhaseInfo ph;
+        if (!make_phase(d, a, b, ph)) continue;  // no dx pixels of this parity
+        if (ph.ntap == 0) {                      // pixels no tap reaches: zero gradient
+          if (!accumulate)
+            dgrad_phase_zero_kernel<<<ew_blocks((long long)d->n * ph.Hp * ph.Wp * d->c / 4), kEwThreads, 0,
+                                      S(stream)>>>(dx, d->n, d->h, d->w, d->c, a, b, d->stride_h, d->stride_w);
+          continue;
+        }
+        if (int e = launch_gemm(phase_params(d, ph, dy, w, dx), variant, accumulate, ws, ws_bytes, S(stream)))
+          return e;
+      }
+    return last_error();
+  }
   return launch_gemm(conv_params(MONET_PASS_DGRAD, d, dy, w, dx), variant, accumulate, ws, ws_bytes, S(stream));
 }
 

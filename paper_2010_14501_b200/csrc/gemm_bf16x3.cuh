@@ -54,7 +54,6 @@ constexpr int kAccStages = 2;
 constexpr int kTmemCols = 512;
 constexpr int kTmemA = kAccStages * BN;          // A stages start at column 256
 constexpr int kAStageCols = 64;                  // 32 cols hi + 32 cols lo (bf16x2 per column)
-constexpr int kChunkStages = 8;                  // flush the TMEM accumulation chain every 8 stages
 constexpr int kNumBars = 2 * kRawSlots + 3 * kStages + 2 * kAccStages;
 constexpr int kSmemBytes = kRawSlots * kRawBytes + kStages * kStageBytes + 1024 + 8 * kNumBars + 16;
 static_assert(kLoaderThreads == 256, "loader threads: 128 per operand");
@@ -175,7 +174,8 @@ MONET_DEV const float* group_ptr(const GemmParams& p, const Operand& op, int row
     return op.ptr + (long long)row * op.ld + k;
   } else if constexpr (MODE == OP_MNMAJOR) {
     const int kh = k / op.kdiv, kl = k - kh * op.kdiv;
-    return op.ptr + kh * op.ks1 + (long long)kl * op.ld + row;
+    const int th = p.ph.on ? p.ph.tap[kh] : kh;  // phase dgrad: phase tap -> filter tap
+    return op.ptr + th * op.ks1 + (long long)kl * op.ld + row;
   } else if constexpr (MODE == OP_IM2COL_FPROP) {
     const int q = row % g.Q, t = row / g.Q, pp = t % g.P, n = t / g.P;
     const int tap = k / g.C, c = k - tap * g.C, r = tap / g.S, s = tap - r * g.S;
@@ -183,6 +183,13 @@ MONET_DEV const float* group_ptr(const GemmParams& p, const Operand& op, int row
     if ((unsigned)h >= (unsigned)g.H || (unsigned)w >= (unsigned)g.W) return nullptr;
     return op.ptr + (((long long)n * g.H + h) * g.W + w) * g.C + c;
   } else if constexpr (MODE == OP_IM2COL_DGRAD) {
+    if (p.ph.on) {
+      const int j = row % p.ph.Wp, t = row / p.ph.Wp, i = t % p.ph.Hp, n = t / p.ph.Hp;
+      const int tp = k / g.K, ko = k - tp * g.K;
+      const int pp = i + p.ph.dr[tp], q = j + p.ph.ds[tp];
+      if ((unsigned)pp >= (unsigned)g.P || (unsigned)q >= (unsigned)g.Q) return nullptr;
+      return op.ptr + (((long long)n * g.P + pp) * g.Q + q) * g.K + ko;
+    }
     const int w = row % g.W, t = row / g.W, h = t % g.H, n = t / g.H;
     const int tap = k / g.K, ko = k - tap * g.K, r = tap / g.S, s = tap - r * g.S;
     const int hp = h + g.ph - r, wp = w + g.pw - s;
@@ -226,12 +233,16 @@ struct Loader {
     if (op.tma != 2) return;
     if constexpr (MODE == OP_IM2COL_FPROP || MODE == OP_IM2COL_DGRAD) {
       const bool fp = MODE == OP_IM2COL_FPROP;
-      const int X = fp ? g.Q : g.W, Y = fp ? g.P : g.H;
+      const bool phs = !fp && p.ph.on;
+      const int X = fp ? g.Q : (phs ? p.ph.Wp : g.W), Y = fp ? g.P : (phs ? p.ph.Hp : g.H);
       const int x = row0 % X, t = row0 / X, y = t % Y;
       cn = t / Y;
       if (fp) {
         cw = x * g.sw - g.pw;
         chh = y * g.sh - g.ph;
+      } else if (phs) {
+        cw = x + p.ph.lo_w;
+        chh = y + p.ph.lo_h;
       } else {
         cw = x - (g.S - 1 - g.pw);
         chh = y - (g.R - 1 - g.ph);
@@ -239,8 +250,13 @@ struct Loader {
       const int cx = fp ? g.C : g.K;
       const int tap = k0 / cx;
       kin0 = k0 - tap * cx;
-      tap_r = tap / g.S;
-      tap_s = tap - tap_r * g.S;
+      if (phs) {  // phase dgrad: tap_s walks the phase's tap list
+        tap_r = 0;
+        tap_s = tap;
+      } else {
+        tap_r = tap / g.S;
+        tap_s = tap - tap_r * g.S;
+      }
     }
   }
 
@@ -254,17 +270,27 @@ struct Loader {
       tma_2d(dst, m, k, row0, bar);
     } else if constexpr (MODE == OP_MNMAJOR) {
       mbar_arrive_tx(bar, BM * BKR * 4);
-      if (op.kdiv >= p.Kd) {
+      if (op.kdiv >= p.Kd && !p.ph.on) {
         tma_2d(dst, m, row0, k, bar);
       } else {  // k = tap * kdiv + kout, kdiv % 32 == 0: tensor {rows, taps, kdiv}
         const int kh = k / op.kdiv;
-        tma_3d(dst, m, row0, kh, k - kh * op.kdiv, bar);
+        tma_3d(dst, m, row0, p.ph.on ? p.ph.tap[kh] : kh, k - kh * op.kdiv, bar);
       }
     } else if constexpr (MODE == OP_IM2COL_FPROP || MODE == OP_IM2COL_DGRAD) {
       mbar_arrive_tx(bar, BM * BKR * 4);
+      const bool phs = MODE == OP_IM2COL_DGRAD && p.ph.on;
       if (k < p.Kd) {
-        const int ow = MODE == OP_IM2COL_FPROP ? tap_s : g.S - 1 - tap_s;
-        const int oh = MODE == OP_IM2COL_FPROP ? tap_r : g.R - 1 - tap_r;
+        int ow, oh;
+        if (MODE == OP_IM2COL_FPROP) {
+          ow = tap_s;
+          oh = tap_r;
+        } else if (phs) {
+          ow = p.ph.ds[tap_s] - p.ph.lo_w;
+          oh = p.ph.dr[tap_s] - p.ph.lo_h;
+        } else {
+          ow = g.S - 1 - tap_s;
+          oh = g.R - 1 - tap_r;
+        }
         tma_im2col(dst, m, kin0, cw, chh, cn, ow, oh, bar);
       } else {  // zero-padded tail k-block: out-of-range channel coordinate -> zero fill
         tma_im2col(dst, m, MODE == OP_IM2COL_FPROP ? g.C : g.K, cw, chh, cn, 0, 0, bar);
@@ -273,7 +299,7 @@ struct Loader {
       kin0 += BKR;
       if (kin0 >= cx) {
         kin0 = 0;
-        if (++tap_s == g.S) {
+        if (++tap_s == g.S && !phs) {
           tap_s = 0;
           ++tap_r;
         }
@@ -541,9 +567,17 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
       tile_coords(p, tile, mt, nt, sp);
       kb_range(p, sp, kb0, kb1);
       const int nst = (kb1 - kb0 + 1) / 2;
-      const int nchunks = (nst + kChunkStages - 1) / kChunkStages;
+      const int nchunks = (nst + p.chunk_stages - 1) / p.chunk_stages;
       const int m = mt * BM + quarter * 32 + lane;
+      long long out_row = m;  // phase dgrad: scatter row (n, i, j) to dx[n][i*sh + a][j*sw + b]
+      if (p.ph.on && m < p.M) {
+        const int j = m % p.ph.Wp, t = m / p.ph.Wp, i = t % p.ph.Hp, n = t / p.ph.Hp;
+        out_row = ((long long)n * p.g.H + i * p.g.sh + p.ph.a) * p.g.W + j * p.g.sw + p.ph.b;
+      }
       for (int chunk = 0; chunk < nchunks; ++chunk) {
+        // later chunks (and accumulate mode) add with fire-and-forget vector
+        // reductions: no read-back latency, and one thread owns each element,
+        // so the order of the adds is fixed (deterministic)
         const bool add_old = chunk > 0 || p.epi == EPI_ACCUM;
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
@@ -558,7 +592,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
               dst = p.ws + (long long)sp * p.M * p.N + (long long)m * p.N + n0;
               ld = p.N;
             } else {
-              dst = p.c + (long long)m * p.ldc + n0;
+              dst = p.c + out_row * p.ldc + n0;
               ld = p.ldc;
             }
             const int ncols = min(32, p.N - n0);
@@ -566,23 +600,22 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
             if (vec) {
 #pragma unroll
               for (int j = 0; j < 32; j += 4) {
-                float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
                 if (add_old) {
-                  const float4 c = *reinterpret_cast<const float4*>(dst + j);
-                  o.x += c.x;
-                  o.y += c.y;
-                  o.z += c.z;
-                  o.w += c.w;
+                  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + j), "f"(v[j]),
+                               "f"(v[j + 1]), "f"(v[j + 2]), "f"(v[j + 3])
+                               : "memory");
+                } else {
+                  *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
                 }
-                *reinterpret_cast<float4*>(dst + j) = o;
               }
             } else {
 #pragma unroll
               for (int j = 0; j < 32; ++j) {
                 if (j < ncols) {
-                  float o = v[j];
-                  if (add_old) o += dst[j];
-                  dst[j] = o;
+                  if (add_old)
+                    atomicAdd(dst + j, v[j]);
+                  else
+                    dst[j] = v[j];
                 }
               }
             }
@@ -606,8 +639,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
     for (int tile = blockIdx.x; tile < n_tiles_total; tile += gridDim.x) {
       int mt, nt, kb0, nst;
       tile_range(p, tile, mt, nt, kb0, nst);
-      for (int c0 = 0; c0 < nst; c0 += kChunkStages) {
-        const int c1 = min(nst, c0 + kChunkStages);
+      for (int c0 = 0; c0 < nst; c0 += p.chunk_stages) {
+        const int c1 = min(nst, c0 + p.chunk_stages);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;

@@ -52,6 +52,17 @@ struct Operand {
 
 enum EpiMode : int { EPI_STORE = 0, EPI_ACCUM = 1, EPI_PARTIAL = 2 };
 
+// Strided-conv dgrad as sub-pixel phases (bf16x3 kernel): output pixels with
+// (h % sh, w % sw) == (a, b) form a stride-1 problem over dy that uses only the
+// filter taps of matching parity.  GEMM row m = (n, i, j) of the Hp x Wp phase
+// grid writes dx[n][i*sh + a][j*sw + b]; phase tap t reads dy[n][i + dr[t]][j + ds[t]]
+// and filter tap tap[t] = r*S + s.
+struct PhaseInfo {
+  int on;
+  int a, b, Hp, Wp, ntap, lo_h, lo_w;
+  signed char dr[16], ds[16], tap[16];
+};
+
 struct GemmParams {
   int M, N, Kd;
   Operand a, b;
@@ -65,6 +76,8 @@ struct GemmParams {
   int m_tiles, n_tiles;
   int split_tf32;   // 1: 3xTF32 (hi/lo), 0: plain tf32
   int mn_seg;       // bf16x3: rows per segment of the MN-major raw B layout (128, or C for wgrad)
+  PhaseInfo ph;     // bf16x3: strided dgrad phase (ph.on == 0 otherwise)
+  int chunk_stages; // bf16x3: MMA stages accumulated in TMEM before a flush to fp32 memory
   float* dbg_a;     // debug: bf16x3 A-split dumps the raw A operand [M][Kpad] here (nullptr = off)
   float* dbg_b;     // debug: bf16x3 B-split dumps the raw B operand [N][Kpad]
   CUtensorMap tma_a, tma_b;  // bf16x3: TMA descriptors (valid when Operand::tma != 0)

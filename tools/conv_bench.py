@@ -28,7 +28,11 @@ def main():
     ap.add_argument("--only", default=None)
     ap.add_argument("--passes", default="fwd,dgrad,wgrad")
     ap.add_argument("--variants", default="splitk")
+    ap.add_argument("--resnet50", action="store_true",
+                    help="every unique conv shape of ResNet-50 b184 224^2, weighted by its count")
     a = ap.parse_args()
+    if a.resnet50:
+        return resnet50_table(a)
     lib = N.lib()
     dev = torch.device("cuda:0")
     st = torch.cuda.current_stream().cuda_stream
@@ -64,6 +68,64 @@ def main():
                 torch.cuda.synchronize()
                 ms = e0.elapsed_time(e1) / a.iters
                 print(f"{name:18s} {pss:6s} {vname:8s} {ms:8.3f} ms  {flops / ms / 1e9:8.1f} TFLOP/s  ws {wsb/2**20:.1f} MiB")
+
+
+def resnet50_table(a):
+    """Per-shape and total conv time of one ResNet-50 training step (fwd + dgrad + wgrad)."""
+    from collections import Counter
+
+    from paper_2010_14501_b200.tracer import build_network
+    net = build_network("resnet50", 184, 224)
+    shapes = Counter()
+    for op in net.ops:
+        if op.kind == "conv":
+            d = net.conv_desc(op)
+            first = net.op(op.deps[0]).kind == "input"
+            shapes[(d.n, d.h, d.w, d.c, d.k, d.r, d.s, d.stride_h, d.pad_h, first)] += 1
+    lib = N.lib()
+    dev = torch.device("cuda:0")
+    st = torch.cuda.current_stream().cuda_stream
+    totals = {}
+    for (n, h, w, c, k, r, s, stride, pad, first), cnt in sorted(shapes.items()):
+        d = N.conv_desc(n, h, w, c, k, r, s, stride, pad)
+        x = torch.randn(n, h, w, c, device=dev)
+        wt = torch.randn(k, r, s, c, device=dev)
+        y = torch.randn(n, d.p, d.q, k, device=dev)
+        dw, dx = torch.empty_like(wt), torch.empty_like(x)
+        flops = 2.0 * n * d.p * d.q * k * c * r * s
+        line = f"{cnt:2d}x n{n} {h}x{w} c{c:4d} k{k:4d} {r}x{s}/{stride}"
+        for vname in a.variants.split(","):
+            v = N.CONV_VARIANTS[vname]
+            tot = 0.0
+            for pss in ("fwd", "dgrad", "wgrad"):
+                if pss == "dgrad" and first:
+                    continue
+                pid = N.PASS[pss]
+                wsb = lib.conv_ws_bytes(v, pid, d)
+                ws = torch.empty(max(wsb, 16) // 4, device=dev)
+                if pss == "fwd":
+                    fn = lambda: lib.conv_fwd(v, d, x.data_ptr(), wt.data_ptr(), y.data_ptr(), ws.data_ptr(), wsb, st)
+                elif pss == "dgrad":
+                    fn = lambda: lib.conv_dgrad(v, d, y.data_ptr(), wt.data_ptr(), dx.data_ptr(), 0, ws.data_ptr(), wsb, st)
+                else:
+                    fn = lambda: lib.conv_wgrad(v, d, x.data_ptr(), y.data_ptr(), dw.data_ptr(), 0, ws.data_ptr(), wsb, st)
+                fn()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(a.iters):
+                    fn()
+                e1.record()
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1) / a.iters
+                tot += ms * cnt
+                totals[(vname, pss)] = totals.get((vname, pss), 0.0) + ms * cnt
+                line += f" | {vname[:6]} {pss[:2]} {ms:6.3f} ({flops / ms / 1e9:5.0f})"
+        print(line, flush=True)
+    for vname in a.variants.split(","):
+        t = {p: totals.get((vname, p), 0.0) for p in ("fwd", "dgrad", "wgrad")}
+        print(f"TOTAL {vname}: fwd {t['fwd']:.2f} ms  dgrad {t['dgrad']:.2f} ms  wgrad {t['wgrad']:.2f} ms  "
+              f"sum {sum(t.values()):.2f} ms")
 
 
 if __name__ == "__main__":
