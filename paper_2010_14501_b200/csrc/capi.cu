@@ -156,6 +156,11 @@ int make_tma(GemmParams& p, const Operand& op, CUtensorMap* m) {
       return tiled_map(m, op.ptr, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
     }
     case OP_IM2COL_FPROP:
+      if (g.C == 4 || g.C == 8 || g.C == 16)  // one box of C channels per filter tap
+        return im2col_map(m, op.ptr, g.N, g.H, g.W, g.C, -g.pw, -g.ph, g.pw - (g.S - 1), g.ph - (g.R - 1), g.sw,
+                          g.sh, g.C, 128, CU_TENSOR_MAP_SWIZZLE_NONE)
+                   ? 3
+                   : 0;
       if (g.C % 32) return 0;
       return im2col_map(m, op.ptr, g.N, g.H, g.W, g.C, -g.pw, -g.ph, g.pw - (g.S - 1), g.ph - (g.R - 1), g.sw, g.sh,
                         32, 128, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -168,7 +173,9 @@ int make_tma(GemmParams& p, const Operand& op, CUtensorMap* m) {
       return im2col_map(m, op.ptr, g.N, g.P, g.Q, g.K, -(g.S - 1 - g.pw), -(g.R - 1 - g.ph), -g.pw, -g.ph, 1, 1, 32,
                         128, CU_TENSOR_MAP_SWIZZLE_128B);
     case OP_IM2COL_WGRAD: {
-      if (g.C % 32 || (g.C < 128 ? 128 % g.C : g.C % 128)) return 0;
+      // segments of C (< 128) or 128 channels; below 32 channels (the stem) the
+      // 32-TMA-per-k-block segment loop loses to the 16B cp.async fallback
+      if (g.C < 128 ? 128 % g.C || g.C < 32 : g.C % 128) return 0;
       const int seg = std::min(g.C, 128);
       const int r = im2col_map(m, op.ptr, g.N, g.H, g.W, g.C, -g.pw, -g.ph, g.pw - (g.S - 1), g.ph - (g.R - 1),
                                g.sw, g.sh, seg, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
@@ -519,7 +526,7 @@ int monet_bn_fwd_train(const float* x, float* y, const float* gamma, const float
   float* ws = static_cast<float*>(scratch);
   int nb = bn_blocks(rows);
   bn_reduce_kernel<<<nb, kEwThreads, 0, st>>>(0, x, nullptr, nullptr, nullptr, rows, c, ws);
-  bn_finalize_fwd_kernel<<<(c + 255) / 256, 256, 0, st>>>(ws, nb, rows, c, eps, momentum, update_running, saved_mean,
+  bn_finalize_fwd_kernel<<<(c + 7) / 8, 256, 0, st>>>(ws, nb, rows, c, eps, momentum, update_running, saved_mean,
                                                           saved_invstd, running_mean, running_var);
   bn_apply_kernel<<<ew_blocks(rows * c / 4), kEwThreads, 0, st>>>(x, y, saved_mean, saved_invstd, gamma, beta, rows,
                                                                   c);
@@ -541,7 +548,7 @@ static int bn_bwd_common(const float* src, const float* dy, float* dx, int accum
   float* sum_dy = ws + (size_t)nb * 2 * c;
   float* sum_dyx = sum_dy + c;
   bn_reduce_kernel<<<nb, kEwThreads, 0, st>>>(mode, src, dy, p0, p1, rows, c, ws);
-  bn_finalize_bwd_kernel<<<(c + 255) / 256, 256, 0, st>>>(ws, nb, c, sum_dy, sum_dyx, dgamma, dbeta);
+  bn_finalize_bwd_kernel<<<(c + 7) / 8, 256, 0, st>>>(ws, nb, c, sum_dy, sum_dyx, dgamma, dbeta);
   bn_bwd_apply_kernel<<<ew_blocks(rows * c / 4), kEwThreads, 0, st>>>(src, dy, dx, p0, p1, gamma, invstd, sum_dy,
                                                                       sum_dyx, rows, c, accumulate);
   return last_error();
@@ -587,7 +594,8 @@ int monet_maxpool_fwd(const monet_conv_desc* d, const float* x, float* y, uint8_
 }
 int monet_maxpool_bwd(const monet_conv_desc* d, const uint8_t* idx8, const float* x, const float* dy, float* dx,
                       int accumulate, void* stream) {
-  long long total = (long long)d->n * d->h * d->w * d->c;
+  if (d->c % 4) return -(int)cudaErrorInvalidValue;
+  long long total = (long long)d->n * d->h * d->w * (d->c / 4);
   maxpool_bwd_kernel<<<ew_blocks(total), kEwThreads, 0, S(stream)>>>(idx8, x, dy, dx, d->n, d->h, d->w, d->c, d->p,
                                                                      d->q, d->r, d->s, d->stride_h, d->stride_w,
                                                                      d->pad_h, d->pad_w, accumulate);

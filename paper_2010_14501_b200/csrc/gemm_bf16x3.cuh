@@ -230,7 +230,7 @@ struct Loader {
     const ConvGeom& g = p.g;
     row0 = row0_;
     k0 = k0_;
-    if (op.tma != 2) return;
+    if (op.tma < 2) return;
     if constexpr (MODE == OP_IM2COL_FPROP || MODE == OP_IM2COL_DGRAD) {
       const bool fp = MODE == OP_IM2COL_FPROP;
       const bool phs = !fp && p.ph.on;
@@ -276,6 +276,24 @@ struct Loader {
         const int kh = k / op.kdiv;
         tma_3d(dst, m, row0, p.ph.on ? p.ph.tap[kh] : kh, k - kh * op.kdiv, bar);
       }
+    } else if constexpr (MODE == OP_IM2COL_FPROP) {
+      if (op.tma == 3) {  // C < 32: the k-block spans 32 / C filter taps, one C-channel box each
+        mbar_arrive_tx(bar, BM * BKR * 4);
+        const int ntb = BKR / g.C;
+        for (int j = 0; j < ntb; ++j) {
+          const bool valid = tap_r < g.R;
+          tma_im2col(dst + j * (BM * g.C * 4), m, valid ? 0 : g.C, cw, chh, cn, valid ? tap_s : 0,
+                     valid ? tap_r : 0, bar);
+          if (++tap_s == g.S) {
+            tap_s = 0;
+            ++tap_r;
+          }
+        }
+        return;
+      }
+    }
+    if constexpr (MODE == OP_KMAJOR || MODE == OP_MNMAJOR) {
+      // issued above
     } else if constexpr (MODE == OP_IM2COL_FPROP || MODE == OP_IM2COL_DGRAD) {
       mbar_arrive_tx(bar, BM * BKR * 4);
       const bool phs = MODE == OP_IM2COL_DGRAD && p.ph.on;
@@ -454,6 +472,17 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
           if constexpr (a_mn) {
 #pragma unroll
             for (int k = 0; k < 32; ++k) v[k] = *reinterpret_cast<const float*>(rt + k * (BM * 4) + row * 4);
+          } else if (p.a.tma == 3) {  // chunk-major: tap box j holds C channels per row
+            const int cb = p.g.C * 4;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const int e = 4 * c, j = e / p.g.C, ch = e - j * p.g.C;
+              const float4 q = *reinterpret_cast<const float4*>(rt + j * (BM * cb) + row * cb + ch * 4);
+              v[4 * c] = q.x;
+              v[4 * c + 1] = q.y;
+              v[4 * c + 2] = q.z;
+              v[4 * c + 3] = q.w;
+            }
           } else {
 #pragma unroll
             for (int c = 0; c < 8; ++c) {

@@ -47,7 +47,8 @@ struct Operand {
   int kdiv;
   long long ks1;
   int aligned;  // 16B groups are aligned and never straddle an edge (host-checked)
-  int tma;      // bf16x3 kernel: 0 = 16B cp.async groups, 1 = TMA tiled map, 2 = TMA im2col map
+  int tma;      // bf16x3 kernel: 0 = 16B cp.async groups, 1 = TMA tiled map, 2 = TMA im2col map,
+                //   3 = TMA im2col with C < 32: one box per filter tap, chunk-major raw layout
 };
 
 enum EpiMode : int { EPI_STORE = 0, EPI_ACCUM = 1, EPI_PARTIAL = 2 };

@@ -236,17 +236,35 @@ __global__ void bn_reduce_kernel(int mode, const float* __restrict__ x, const fl
   }
 }
 
-// forward: mean/invstd from sums; running-stat update (momentum, unbiased var)
-__global__ void bn_finalize_fwd_kernel(const float* __restrict__ ws, int nblocks, long long rows, int C, float eps,
-                                       float momentum, int update_running, float* mean_out, float* invstd_out,
-                                       float* running_mean, float* running_var) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  double s1 = 0.0, s2 = 0.0;
-  for (int b = 0; b < nblocks; ++b) {
+// Sum the per-block partials of channel c with one warp: lane l adds blocks
+// l, l+32, ... in fp64, then a fixed xor tree combines the lanes -- the same
+// order on every run (deterministic) and ~nblocks/32 loads per lane.
+__device__ __forceinline__ void bn_warp_sum(const float* __restrict__ ws, int nblocks, int C, int c, double& s1,
+                                            double& s2) {
+  const int lane = threadIdx.x & 31;
+  s1 = 0.0;
+  s2 = 0.0;
+  for (int b = lane; b < nblocks; b += 32) {
     s1 += ws[(long long)b * 2 * C + c];
     s2 += ws[(long long)b * 2 * C + C + c];
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+}
+
+// forward: mean/invstd from sums; running-stat update (momentum, unbiased var).
+// One warp per channel (launch C warps).
+__global__ void bn_finalize_fwd_kernel(const float* __restrict__ ws, int nblocks, long long rows, int C, float eps,
+                                       float momentum, int update_running, float* mean_out, float* invstd_out,
+                                       float* running_mean, float* running_var) {
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (c >= C) return;
+  double s1, s2;
+  bn_warp_sum(ws, nblocks, C, c, s1, s2);
+  if ((threadIdx.x & 31) != 0) return;
   double mean = s1 / (double)rows;
   double var = s2 / (double)rows - mean * mean;
   if (var < 0.0) var = 0.0;
@@ -262,13 +280,11 @@ __global__ void bn_finalize_fwd_kernel(const float* __restrict__ ws, int nblocks
 // backward: dgamma = sum dy*xhat, dbeta = sum dy (parameter grads overwrite)
 __global__ void bn_finalize_bwd_kernel(const float* __restrict__ ws, int nblocks, int C, float* sum_dy,
                                        float* sum_dyxhat, float* dgamma, float* dbeta) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (c >= C) return;
-  double s1 = 0.0, s2 = 0.0;
-  for (int b = 0; b < nblocks; ++b) {
-    s1 += ws[(long long)b * 2 * C + c];
-    s2 += ws[(long long)b * 2 * C + C + c];
-  }
+  double s1, s2;
+  bn_warp_sum(ws, nblocks, C, c, s1, s2);
+  if ((threadIdx.x & 31) != 0) return;
   sum_dy[c] = (float)s1;
   sum_dyxhat[c] = (float)s2;
   if (dgamma) dgamma[c] = (float)s2;
@@ -385,54 +401,73 @@ __global__ void maxpool_fwd_kernel(const float* __restrict__ x, float* __restric
 // gather-form backward (deterministic): dx[n,h,w,c] = sum over windows (p,q)
 // covering (h,w) whose argmax is (h,w) of dy[n,p,q,c].  The argmax comes from
 // the saved 8-bit index, or is recomputed from x (input-activated variant).
+// One thread per (n, h, w, channel quad): 16B loads of x / dy, 4B of idx.
 __global__ void maxpool_bwd_kernel(const uint8_t* __restrict__ idx, const float* __restrict__ x,
                                    const float* __restrict__ dy, float* dx, int N, int H, int W, int C, int P,
                                    int Q, int R, int S, int sh, int sw, int ph, int pw, int accumulate) {
-  const long long total = (long long)N * H * W * C;
+  const int cq = C / 4;
+  const long long total = (long long)N * H * W * cq;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
-    int c = (int)(i % C);
-    long long pix = i / C;
-    int w = (int)(pix % W);
-    int h = (int)((pix / W) % H);
-    int n = (int)(pix / ((long long)H * W));
-    float g = 0.f;
+    const int c4 = (int)(i % cq);
+    const long long pix = i / cq;
+    const int w = (int)(pix % W);
+    const int h = (int)((pix / W) % H);
+    const int n = (int)(pix / ((long long)H * W));
+    float g[4] = {0.f, 0.f, 0.f, 0.f};
     // output rows p with p*sh - ph <= h <= p*sh - ph + R - 1
-    int p_lo = max(0, (h + ph - R + sh) / sh);
-    int p_hi = min(P - 1, (h + ph) / sh);
-    int q_lo = max(0, (w + pw - S + sw) / sw);
-    int q_hi = min(Q - 1, (w + pw) / sw);
+    const int p_lo = max(0, (h + ph - R + sh) / sh);
+    const int p_hi = min(P - 1, (h + ph) / sh);
+    const int q_lo = max(0, (w + pw - S + sw) / sw);
+    const int q_hi = min(Q - 1, (w + pw) / sw);
     for (int p = p_lo; p <= p_hi; ++p) {
-      int r = h - (p * sh - ph);
+      const int r = h - (p * sh - ph);
       if (r < 0 || r >= R) continue;
       for (int q = q_lo; q <= q_hi; ++q) {
-        int s = w - (q * sw - pw);
+        const int s = w - (q * sw - pw);
         if (s < 0 || s >= S) continue;
-        long long o = (((long long)n * P + p) * Q + q) * C + c;
-        int a;
+        const long long o = (((long long)n * P + p) * Q + q) * C + 4 * c4;
+        int a[4];
         if (idx) {
-          a = idx[o];
+          const uint32_t packed = *reinterpret_cast<const uint32_t*>(idx + o);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) a[c] = (packed >> (8 * c)) & 0xFF;
         } else {
-          float best = -INFINITY;
-          a = 0;
+          float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+          a[0] = a[1] = a[2] = a[3] = 0;
           for (int rr = 0; rr < R; ++rr) {
-            int hh = p * sh - ph + rr;
+            const int hh = p * sh - ph + rr;
             if ((unsigned)hh >= (unsigned)H) continue;
             for (int ss = 0; ss < S; ++ss) {
-              int ww = q * sw - pw + ss;
+              const int ww = q * sw - pw + ss;
               if ((unsigned)ww >= (unsigned)W) continue;
-              float v = x[(((long long)n * H + hh) * W + ww) * C + c];
-              if (v > best || isnan(v)) {
-                best = v;
-                a = rr * S + ss;
-              }
+              const float4 v4 = *reinterpret_cast<const float4*>(x + (((long long)n * H + hh) * W + ww) * C + 4 * c4);
+              const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+              for (int c = 0; c < 4; ++c)
+                if (v[c] > best[c] || isnan(v[c])) {
+                  best[c] = v[c];
+                  a[c] = rr * S + ss;
+                }
             }
           }
         }
-        if (a == r * S + s) g += dy[o];
+        const float4 d4 = *reinterpret_cast<const float4*>(dy + o);
+        const float d[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (a[c] == r * S + s) g[c] += d[c];
       }
     }
-    dx[i] = accumulate ? dx[i] + g : g;
+    float* out = dx + pix * C + 4 * c4;
+    if (accumulate) {
+      const float4 o4 = *reinterpret_cast<const float4*>(out);
+      g[0] += o4.x;
+      g[1] += o4.y;
+      g[2] += o4.z;
+      g[3] += o4.w;
+    }
+    *reinterpret_cast<float4*>(out) = make_float4(g[0], g[1], g[2], g[3]);
   }
 }
 

@@ -8,6 +8,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -37,8 +38,9 @@ __global__ void probe_kernel(const __grid_constant__ CUtensorMap tmap, float* ou
   for (int i = threadIdx.x; i < bytes / 4; i += blockDim.x) out[i] = buf[i];
 }
 
-int main() {
-  const int N = 2, H = 5, W = 7, C = 32;
+int main(int argc, char** argv) {
+  const int N = 2, H = 5, W = 7, C = argc > 1 ? atoi(argv[1]) : 32;
+  const int CH = argc > 2 ? atoi(argv[2]) : C;
   std::vector<float> hx(N * H * W * C);
   for (int n = 0; n < N; ++n)
     for (int h = 0; h < H; ++h)
@@ -75,27 +77,27 @@ int main() {
     cuuint64_t strides[3] = {(cuuint64_t)C * 4, (cuuint64_t)W * C * 4, (cuuint64_t)H * W * C * 4};
     int lo[2] = {cs.lo0, cs.lo1}, up[2] = {cs.up0, cs.up1};
     cuuint32_t es[4] = {1, (cuuint32_t)cs.es1, (cuuint32_t)cs.es2, 1};
-    CUresult r = encode(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dx, dims, strides, lo, up, 32, 24, es,
+    CUresult r = encode(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dx, dims, strides, lo, up, CH, 24, es,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     printf("== %s  (encode rc=%d)\n", cs.what, (int)r);
     if (r != CUDA_SUCCESS) continue;
     cudaMemset(dout, 0xff, 32 * 64 * 4);
-    probe_kernel<<<1, 128>>>(tm, dout, cs.c0, cs.w0, cs.h0, cs.n0, cs.ow, cs.oh, 24 * 32 * 4);
+    probe_kernel<<<1, 128>>>(tm, dout, cs.c0, cs.w0, cs.h0, cs.n0, cs.ow, cs.oh, 24 * CH * 4);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
       printf("kernel error %s\n", cudaGetErrorString(e));
       continue;
     }
-    std::vector<float> ho(24 * 32);
+    std::vector<float> ho(24 * CH);
     cudaMemcpy(ho.data(), dout, ho.size() * 4, cudaMemcpyDeviceToHost);
-    for (int p = 0; p < 24; ++p) {
-      float v = ho[p * 32];
+    for (int p = 0; p < 24; p += 7) {
+      float v = ho[p * CH];
       if (v == 0) {
         printf("  px%2d: zero\n", p);
       } else {
         int iv = (int)(v - 1 + 0.5f);
-        printf("  px%2d: n%d h%d w%d  (c1 %.2f)\n", p, iv / 1000, (iv / 100) % 10, (iv / 10) % 10, ho[p * 32 + 1]);
+        printf("  px%2d: n%d h%d w%d  (c1 %.2f)\n", p, iv / 1000, (iv / 100) % 10, (iv / 10) % 10, ho[p * CH + 1]);
       }
     }
   }
