@@ -54,6 +54,9 @@ int monet_copy_async(void* dst, const void* src, size_t bytes, void* stream);
 /* debug only: make the bf16x3 GEMM dump the raw A / B operands it consumes
  * ([rows][K rounded up to 64] fp32 device buffers; NULL disables) */
 void monet_debug_dump(float* a_dump, float* b_dump);
+/* debug only: accumulate per-role barrier wait cycles of the bf16x3 GEMM into
+ * 16 uint64 device counters (see gemm_bf16x3.cuh TWAIT; NULL disables) */
+void monet_debug_timers(unsigned long long* counters);
 
 /* --- convolution (K1-K3; replaces conv entries of Catalog, costmodel.py:30-44) */
 size_t monet_conv_ws_bytes(int variant, int pass, const monet_conv_desc* d);

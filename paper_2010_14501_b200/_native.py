@@ -28,6 +28,7 @@ SIGNATURES = {
     "monet_device_check": (_i32, []),
     "monet_copy_async": (_i32, [_vp, _vp, _sz, _vp]),
     "monet_debug_dump": (None, [_vp, _vp]),
+    "monet_debug_timers": (None, [_vp]),
     "monet_conv_ws_bytes": (_sz, [_i32, _i32, _PCONV]),
     "monet_conv_fwd": (_i32, [_i32, _PCONV, _vp, _vp, _vp, _vp, _sz, _vp]),
     "monet_conv_dgrad": (_i32, [_i32, _PCONV, _vp, _vp, _vp, _i32, _vp, _sz, _vp]),

@@ -188,11 +188,13 @@ int make_tma(GemmParams& p, const Operand& op, CUtensorMap* m) {
 
 float* g_dbg_a = nullptr;
 float* g_dbg_b = nullptr;
+unsigned long long* g_dbg_t = nullptr;
 
 int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (p.M <= 0 || p.N <= 0) return 0;
   p.dbg_a = g_dbg_a;
   p.dbg_b = g_dbg_b;
+  p.dbg_t = g_dbg_t;
   const bool bx = uses_bx3(variant);
   if (bx) {
     // MONET_TMA_MASK (debug): bit 0 enables TMA for A, bit 1 for B (default 3)
@@ -374,6 +376,8 @@ void monet_debug_dump(float* a_dump, float* b_dump) {
   g_dbg_a = a_dump;
   g_dbg_b = b_dump;
 }
+
+void monet_debug_timers(unsigned long long* counters) { g_dbg_t = counters; }
 
 int monet_copy_async(void* dst, const void* src, size_t bytes, void* stream) {
   if (bytes == 0) return 0;

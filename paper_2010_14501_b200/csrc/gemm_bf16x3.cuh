@@ -14,20 +14,25 @@
 //     a_hi / a_lo straight into TMEM with tcgen05.st; the MMAs read A from
 //     TMEM and only B (bf16 hi / lo, half the bytes of fp32) from smem.
 //
-// Warp roles (672 threads, one CTA per SM, persistent over output tiles):
-//   warps 0-7   loaders (threads 0-127 A, 128-255 B): the raw fp32 k-block
+// Warp roles (800 threads, one CTA per SM, persistent over output tiles):
+//   warps 0-3   loaders (threads 0-63 A, 64-127 B): the raw fp32 k-block
 //               (BK = 32) of each operand arrives by TMA -- tiled 2D / 3D maps
 //               for plain operands, im2col maps (zero fill for padding) for
-//               the fprop / stride-1 dgrad / wgrad gathers -- issued by one
-//               thread and completing on the slot's mbarrier (expect_tx);
-//               shapes TMA cannot express (the 4-channel stem, stride-2
-//               dgrad) fall back to 16B cp.async groups from 128 threads
-//               (cp.async.mbarrier.arrive.noinc)
-//   warps 8-11  A-split: row r = lane quarter; LDS the row, split, tcgen05.st
-//               into the TMEM A stage (two raw k-blocks = one BK=64 stage)
-//   warps 12-15 B-split: raw fp32 -> bf16 hi / lo SWIZZLE_128B tiles
-//   warps 16-19 epilogue: tcgen05.ld the 128x128 fp32 accumulator
-//   warp  20    MMA issuer (one lane) and TMEM owner
+//               the fprop / stride-1 / phase dgrad / wgrad gathers -- issued
+//               by one thread and completing on the slot's mbarrier
+//               (expect_tx); shapes TMA cannot express fall back to 16B
+//               cp.async groups from 64 threads (cp.async.mbarrier.arrive.noinc)
+//   warps 4-11  A-split: lane quarter (warp & 3) x raw k-block of the stage;
+//               LDS the row, split, tcgen05.st into the TMEM A stage
+//   warps 12-19 B-split: raw fp32 -> bf16 hi / lo SWIZZLE_128B tiles
+//   warps 20-23 epilogue: tcgen05.ld the 128x128 fp32 accumulator, store or
+//               red.global.add (chunk flushes / accumulate)
+//   warp  24    MMA issuer (one lane) and TMEM owner
+//
+// Measured limits (tools/gemm_waits.py, profiles/ncu_r1.md): with fp32
+// operands a 128x128 tile moves 32 KB per 32-deep k-block from L2; the TMA
+// issue path saturates near 6.6 TB/s chip-wide, which caps this shape at
+// ~230 TF/s of useful work -- the next step is 256-wide tiles (cta_group::2).
 #pragma once
 #include "gemm_tc.cuh"
 
@@ -40,13 +45,13 @@ constexpr int BKS = 64;              // MMA stage (bf16, 128B rows) = 2 raw k-bl
 constexpr int kRawSlots = 4;
 constexpr int kRawTile = BM * BKR * 4;          // 16 KB (A or B raw, fp32)
 constexpr int kRawBytes = 2 * kRawTile;          // A + B
-constexpr int kStages = 2;                       // MMA stages (TMEM A + smem B)
+constexpr int kStages = 3;                       // MMA stages (TMEM A + smem B)
 constexpr int kBTile = BN * BKS * 2;             // 16 KB (bf16 hi or lo)
 constexpr int kStageBytes = 2 * kBTile;          // B hi + B lo
-constexpr int kLoaderWarps = 8, kASplitWarps = 4, kBSplitWarps = 4, kEpiWarps = 4;
+constexpr int kLoaderWarps = 4, kASplitWarps = 8, kBSplitWarps = 8, kEpiWarps = 4;
 constexpr int kLoaderThreads = kLoaderWarps * 32;
-constexpr int kWarpASplit = kLoaderWarps;                       // 8
-constexpr int kWarpBSplit = kWarpASplit + kASplitWarps;         // 12
+constexpr int kWarpASplit = kLoaderWarps;                       // 4
+constexpr int kWarpBSplit = kWarpASplit + kASplitWarps;         // 12 (A split: 4 lane quarters x 2 halves)
 constexpr int kWarpEpi = kWarpBSplit + kBSplitWarps;            // 16
 constexpr int kWarpMma = kWarpEpi + kEpiWarps;                  // 20
 constexpr int kThreads = (kWarpMma + 1) * 32;                   // 672
@@ -56,7 +61,11 @@ constexpr int kTmemA = kAccStages * BN;          // A stages start at column 256
 constexpr int kAStageCols = 64;                  // 32 cols hi + 32 cols lo (bf16x2 per column)
 constexpr int kNumBars = 2 * kRawSlots + 3 * kStages + 2 * kAccStages;
 constexpr int kSmemBytes = kRawSlots * kRawBytes + kStages * kStageBytes + 1024 + 8 * kNumBars + 16;
-static_assert(kLoaderThreads == 256, "loader threads: 128 per operand");
+static_assert(kLoaderThreads == 128, "loader threads: 64 per operand");
+constexpr int kOpLoaders = kLoaderThreads / 2;
+constexpr int kBSplitThreads = kBSplitWarps * 32;
+static_assert(kBSplitThreads == 256, "B split: 256 threads x 4 row groups");
+static_assert(kSmemBytes <= 232448, "shared memory budget");
 static_assert(kTmemA + kStages * kAStageCols <= kTmemCols, "TMEM budget");
 
 MONET_DEV void cp_async_mbar_arrive(uint64_t* bar) {
@@ -343,17 +352,17 @@ struct Loader {
                                 uint64_t* bar) {
     const int kk0 = kb * BKR;
 #pragma unroll 2
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < 16; ++i) {  // 64 threads x 16 groups of 16B = one 16 KB tile
       int row, k;
       uint32_t off;
       if constexpr (kMN) {
-        const int kr = (sub >> 5) + 4 * i;
+        const int kr = (sub >> 5) + 2 * i;
         const int r = 4 * (sub & 31);
         row = row0 + r;
         k = kk0 + kr;
         off = mn_off(r, kr, MODE == OP_IM2COL_WGRAD ? p.mn_seg : BN);
       } else {
-        const int r = (sub >> 3) + 16 * i;
+        const int r = (sub >> 3) + 8 * i;
         row = row0 + r;
         k = kk0 + 4 * (sub & 7);
         off = sw128_offset(r, sub & 7);
@@ -371,6 +380,16 @@ struct Loader {
     cp_async_mbar_arrive(bar);
   }
 };
+// Debug wait-time accounting (p.dbg_t != nullptr): counters per CTA
+//   0 loader raw_empty, 3 MMA a_full, 4 MMA b_full, 5 MMA tempty, 6 epilogue tfull,
+//   7 A-split st_empty, 8 A-split raw_full, 9 B-split st_empty, 10 B-split raw_full, 15 kernel cycles
+#define TWAIT(slot, expr)                                   \
+  do {                                                      \
+    const long long t0_ = p.dbg_t ? clock64() : 0;          \
+    expr;                                                   \
+    if (p.dbg_t) twait[slot] += clock64() - t0_;            \
+  } while (0)
+
 template <int AM, int BMODE>
 __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_constant__ GemmParams p) {
   constexpr bool a_mn = mode_is_mn(AM), b_mn = mode_is_mn(BMODE);
@@ -391,11 +410,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
   const int warp = warp_id();
   const int lane = lane_id();
   const int n_tiles_total = p.m_tiles * p.n_tiles * p.splits;
+  long long twait[16] = {0};
+  const long long t_start = clock64();
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRawSlots; ++s) {
-      mbar_init(&raw_full[s], (p.a.tma ? 1 : 128) + (p.b.tma ? 1 : 128));
-      mbar_init(&raw_empty[s], (kASplitWarps + kBSplitWarps) * 32);
+      mbar_init(&raw_full[s], (p.a.tma ? 1 : kOpLoaders) + (p.b.tma ? 1 : kOpLoaders));
+      mbar_init(&raw_empty[s], (kASplitWarps / 2 + kBSplitWarps) * 32);  // one A half + all of B per item
     }
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&a_full[s], kASplitWarps * 32);
@@ -416,8 +437,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
 
   if (warp < kLoaderWarps) {
     // ---------------------------------------------------------------- loaders
-    const int sub = threadIdx.x & 127;
-    const bool is_b = threadIdx.x >= 128;
+    const int sub = threadIdx.x % kOpLoaders;
+    const bool is_b = threadIdx.x >= kOpLoaders;
     const Operand& op = is_b ? p.b : p.a;
     const bool active = !op.tma || sub == 0;  // one thread issues a TMA operand
     Loader<AM> la;
@@ -432,7 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
         la.init(p, p.a, mt * BM, kb0 * BKR);
       for (int kb = kb0; kb < kb0 + 2 * nst; ++kb, ++item) {
         const int slot = item % kRawSlots;
-        mbar_wait(&raw_empty[slot], ((item / kRawSlots) & 1) ^ 1);
+        TWAIT(0, mbar_wait(&raw_empty[slot], ((item / kRawSlots) & 1) ^ 1));
         uint8_t* base = raw + slot * kRawBytes;
         if (is_b) {
           if (op.tma)
@@ -453,20 +474,21 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const uint32_t lane_sel = (uint32_t)(quarter * 32) << 16;
-    int item = 0, stage_item = 0;
+    const int half = (warp - kWarpASplit) >> 2;  // which raw k-block of each stage this warp splits
+    int stage_item = 0;
     for (int tile = blockIdx.x; tile < n_tiles_total; tile += gridDim.x) {
       int mt, nt, kb0, nst;
       tile_range(p, tile, mt, nt, kb0, nst);
       const int item_kb0 = kb0;
       for (int s = 0; s < nst; ++s, ++stage_item) {
         const int stage = stage_item % kStages;
-        mbar_wait(&st_empty[stage], ((stage_item / kStages) & 1) ^ 1);
+        TWAIT(7, mbar_wait(&st_empty[stage], ((stage_item / kStages) & 1) ^ 1));
         tc_fence_after();
         const uint32_t a_hi = tmem_base + lane_sel + kTmemA + stage * kAStageCols;
-#pragma unroll 1
-        for (int half = 0; half < 2; ++half, ++item) {
+        {
+          const int item = 2 * stage_item + half;
           const int slot = item % kRawSlots;
-          mbar_wait(&raw_full[slot], (item / kRawSlots) & 1);
+          TWAIT(8, mbar_wait(&raw_full[slot], (item / kRawSlots) & 1));
           const uint8_t* rt = raw + slot * kRawBytes;
           float v[32];
           if constexpr (a_mn) {
@@ -517,48 +539,48 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
     }
   } else if (warp < kWarpEpi) {
     // ---------------------------------------------------------------- B split -> smem bf16
-    const int t = threadIdx.x - kWarpBSplit * 32;  // 0..127
+    const int t = threadIdx.x - kWarpBSplit * 32;  // 0..255
     int item = 0, stage_item = 0;
     for (int tile = blockIdx.x; tile < n_tiles_total; tile += gridDim.x) {
       int mt, nt, kb0, nst;
       tile_range(p, tile, mt, nt, kb0, nst);
       for (int s = 0; s < nst; ++s, ++stage_item) {
         const int stage = stage_item % kStages;
-        mbar_wait(&st_empty[stage], ((stage_item / kStages) & 1) ^ 1);
+        TWAIT(9, mbar_wait(&st_empty[stage], ((stage_item / kStages) & 1) ^ 1));
         uint8_t* bhi = bst + stage * kStageBytes;
         uint8_t* blo = bhi + kBTile;
 #pragma unroll 1
         for (int half = 0; half < 2; ++half, ++item) {
           const int slot = item % kRawSlots;
-          mbar_wait(&raw_full[slot], (item / kRawSlots) & 1);
+          TWAIT(10, mbar_wait(&raw_full[slot], (item / kRawSlots) & 1));
           const uint8_t* rt = raw + slot * kRawBytes + kRawTile;
           // K-major: a warp covers rows {0,4,1,5}+base so that the two rows of
           // one 16-lane STS.64 phase land in opposite swizzle halves
-          const int w4 = t >> 5, l = t & 31;
-          const int rbase = 8 * (w4 >> 1) + 2 * (w4 & 1) + (((l >> 3) & 1) << 2) + (l >> 4);
-          float4 q[8];
+          const int w8 = t >> 5, l = t & 31;
+          const int rbase = 8 * (w8 >> 1) + 2 * (w8 & 1) + (((l >> 3) & 1) << 2) + (l >> 4);
+          float4 q[4];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
+          for (int i = 0; i < 4; ++i) {
             uint32_t off;
             if constexpr (b_mn) {
-              off = mn_off(4 * (t & 31), (t >> 5) + 4 * i, p.mn_seg);
+              off = mn_off(4 * (t & 31), (t >> 5) + 8 * i, p.mn_seg);
             } else {
-              off = sw128_offset(rbase + 16 * i, t & 7);
+              off = sw128_offset(rbase + 32 * i, t & 7);
             }
             q[i] = *reinterpret_cast<const float4*>(rt + off);
           }
           if (p.dbg_b != nullptr) {
             const long long kpad = (long long)((p.Kd + 63) / 64) * 64;
             const int kb = kb0 + 2 * s + half;
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 0; i < 4; ++i) {
               const float e[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
               for (int j = 0; j < 4; ++j) {
                 int n, k;
                 if (b_mn) {
                   n = 4 * (t & 31) + j;
-                  k = (t >> 5) + 4 * i;
+                  k = (t >> 5) + 8 * i;
                 } else {
-                  n = rbase + 16 * i;
+                  n = rbase + 32 * i;
                   k = 4 * (t & 7) + j;
                 }
                 n += nt * BN;
@@ -567,15 +589,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
             }
           }
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
+          for (int i = 0; i < 4; ++i) {
             uint2 h, lw;
             split_pair(q[i].x, q[i].y, h.x, lw.x);
             split_pair(q[i].z, q[i].w, h.y, lw.y);
             uint32_t off;
             if constexpr (b_mn) {
-              off = b_off_mnmajor(4 * (t & 31), 32 * half + (t >> 5) + 4 * i);
+              off = b_off_mnmajor(4 * (t & 31), 32 * half + (t >> 5) + 8 * i);
             } else {
-              off = b_off_kmajor(rbase + 16 * i, 32 * half + 4 * (t & 7));
+              off = b_off_kmajor(rbase + 32 * i, 32 * half + 4 * (t & 7));
             }
             *reinterpret_cast<uint2*>(bhi + off) = h;
             *reinterpret_cast<uint2*>(blo + off) = lw;
@@ -608,7 +630,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
         // reductions: no read-back latency, and one thread owns each element,
         // so the order of the adds is fixed (deterministic)
         const bool add_old = chunk > 0 || p.epi == EPI_ACCUM;
-        mbar_wait(&tfull[acc], acc_phase);
+        TWAIT(6, mbar_wait(&tfull[acc], acc_phase));
         tc_fence_after();
         for (int cc = 0; cc < BN / 32; ++cc) {
           float v[32];
@@ -670,14 +692,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
       tile_range(p, tile, mt, nt, kb0, nst);
       for (int c0 = 0; c0 < nst; c0 += p.chunk_stages) {
         const int c1 = min(nst, c0 + p.chunk_stages);
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        TWAIT(5, mbar_wait(&tempty[acc], acc_phase ^ 1));
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int s = c0; s < c1; ++s, ++stage_item) {
           const int stage = stage_item % kStages;
           const uint32_t ph = (stage_item / kStages) & 1;
-          mbar_wait(&a_full[stage], ph);
-          mbar_wait(&b_full[stage], ph);
+          TWAIT(3, mbar_wait(&a_full[stage], ph));
+          TWAIT(4, mbar_wait(&b_full[stage], ph));
           tc_fence_after();
           if (lane == 0) {
             const uint32_t a_hi = tmem_base + kTmemA + stage * kAStageCols;
@@ -704,6 +726,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
     }
   }
 
+  if (p.dbg_t) {  // one representative thread per role reports its waits
+    const bool rep = threadIdx.x == 0 || threadIdx.x == kWarpASplit * 32 || threadIdx.x == kWarpBSplit * 32 ||
+                     threadIdx.x == kWarpEpi * 32 || threadIdx.x == kWarpMma * 32;
+    if (rep) {
+      twait[15] = clock64() - t_start;
+      for (int i = 0; i < 16; ++i)
+        if (twait[i] && (i != 15 || threadIdx.x == kWarpMma * 32)) atomicAdd(p.dbg_t + i, (unsigned long long)twait[i]);
+    }
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == kWarpMma) {
@@ -711,6 +742,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
     tmem_dealloc(tmem_base, kTmemCols);
   }
 }
+#undef TWAIT
 
 }  // namespace bx3
 }  // namespace monet

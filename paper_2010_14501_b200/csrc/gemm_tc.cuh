@@ -79,6 +79,7 @@ struct GemmParams {
   int mn_seg;       // bf16x3: rows per segment of the MN-major raw B layout (128, or C for wgrad)
   PhaseInfo ph;     // bf16x3: strided dgrad phase (ph.on == 0 otherwise)
   int chunk_stages; // bf16x3: MMA stages accumulated in TMEM before a flush to fp32 memory
+  unsigned long long* dbg_t;  // debug: per-CTA wait-time counters of the bf16x3 pipeline roles (nullptr = off)
   float* dbg_a;     // debug: bf16x3 A-split dumps the raw A operand [M][Kpad] here (nullptr = off)
   float* dbg_b;     // debug: bf16x3 B-split dumps the raw B operand [N][Kpad]
   CUtensorMap tma_a, tma_b;  // bf16x3: TMA descriptors (valid when Operand::tma != 0)
