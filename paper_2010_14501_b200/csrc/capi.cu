@@ -518,7 +518,7 @@ static int bn_blocks(int64_t rows) {
 }
 
 size_t monet_bn_scratch_bytes(int64_t rows, int c) {
-  // partials [blocks][2][c] + sum_dy[c] + sum_dyxhat[c] + inv_gamma[c]
+  // partials [blocks][2][c] + coef_b[c] + coef_c[c] + inv_gamma[c] (bn_bwd_common)
   return ((size_t)bn_blocks(rows) * 2 * c + 3 * (size_t)c) * sizeof(float);
 }
 
@@ -549,12 +549,13 @@ static int bn_bwd_common(const float* src, const float* dy, float* dx, int accum
                          const float* p0, const float* p1, const float* invstd, float* dgamma, float* dbeta,
                          int64_t rows, int c, int mode, float* ws, cudaStream_t st) {
   int nb = bn_blocks(rows);
-  float* sum_dy = ws + (size_t)nb * 2 * c;
-  float* sum_dyx = sum_dy + c;
+  float* coef_b = ws + (size_t)nb * 2 * c;  // scratch layout: partials, coef_b[c], coef_c[c], inv_gamma[c]
+  float* coef_c = coef_b + c;
   bn_reduce_kernel<<<nb, kEwThreads, 0, st>>>(mode, src, dy, p0, p1, rows, c, ws);
-  bn_finalize_bwd_kernel<<<(c + 7) / 8, 256, 0, st>>>(ws, nb, c, sum_dy, sum_dyx, dgamma, dbeta);
-  bn_bwd_apply_kernel<<<ew_blocks(rows * c / 4), kEwThreads, 0, st>>>(src, dy, dx, p0, p1, gamma, invstd, sum_dy,
-                                                                      sum_dyx, rows, c, accumulate);
+  bn_finalize_bwd_kernel<<<(c + 7) / 8, 256, 0, st>>>(ws, nb, c, rows, p0, p1, gamma, invstd, coef_b, coef_c, dgamma,
+                                                      dbeta);
+  bn_bwd_apply_kernel<<<ew_blocks(rows * c / 4), kEwThreads, 0, st>>>(src, dy, dx, gamma, invstd, coef_b, coef_c,
+                                                                      rows, c, accumulate);
   return last_error();
 }
 

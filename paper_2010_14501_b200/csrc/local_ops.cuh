@@ -200,18 +200,33 @@ __global__ void bn_reduce_kernel(int mode, const float* __restrict__ x, const fl
         a = *reinterpret_cast<const float4*>(p0 + 4 * q);  // mean | beta
         b = *reinterpret_cast<const float4*>(p1 + 4 * q);  // invstd | 1/gamma
       }
-      for (long long r = r_begin + rsub; r < r_end; r += L.rpi) {
-        const long long off = r * C + 4 * q;
-        float4 v = *reinterpret_cast<const float4*>(x + off);
+      auto acc = [&](const float4& v, const float4& g) {
         if (mode == 0) {
           s1[0] += v.x; s1[1] += v.y; s1[2] += v.z; s1[3] += v.w;
           s2[0] += v.x * v.x; s2[1] += v.y * v.y; s2[2] += v.z * v.z; s2[3] += v.w * v.w;
         } else {
-          float4 g = *reinterpret_cast<const float4*>(dy + off);
           float h0 = (v.x - a.x) * b.x, h1 = (v.y - a.y) * b.y, h2 = (v.z - a.z) * b.z, h3 = (v.w - a.w) * b.w;
           s1[0] += g.x; s1[1] += g.y; s1[2] += g.z; s1[3] += g.w;
           s2[0] += g.x * h0; s2[1] += g.y * h1; s2[2] += g.z * h2; s2[3] += g.w * h3;
         }
+      };
+      const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      long long r = r_begin + rsub;
+      // four rows in flight per thread (same accumulation order as one at a time)
+      for (; r + 3 * L.rpi < r_end; r += 4 * L.rpi) {
+        float4 v[4], g[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const long long off = (r + u * L.rpi) * C + 4 * q;
+          v[u] = *reinterpret_cast<const float4*>(x + off);
+          g[u] = mode == 0 ? z4 : *reinterpret_cast<const float4*>(dy + off);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc(v[u], g[u]);
+      }
+      for (; r < r_end; r += L.rpi) {
+        const long long off = r * C + 4 * q;
+        acc(*reinterpret_cast<const float4*>(x + off), mode == 0 ? z4 : *reinterpret_cast<const float4*>(dy + off));
       }
     }
     // combine the rpi row-subgroups of each channel quad in shared memory
@@ -277,18 +292,27 @@ __global__ void bn_finalize_fwd_kernel(const float* __restrict__ ws, int nblocks
   }
 }
 
-// backward: dgamma = sum dy*xhat, dbeta = sum dy (parameter grads overwrite)
-__global__ void bn_finalize_bwd_kernel(const float* __restrict__ ws, int nblocks, int C, float* sum_dy,
-                                       float* sum_dyxhat, float* dgamma, float* dbeta) {
+// backward: dgamma = sum dy*xhat, dbeta = sum dy (parameter grads overwrite),
+// and the per-channel affine form of the input gradient
+//   dx = k*dy + cb*v + cc,  k = gamma*invstd,  xhat = (v - p0)*p1,
+//   cb = -k*p1*S2/M,  cc = -k*S1/M + k*p1*p0*S2/M        (S1 = sum dy, S2 = sum dy*xhat)
+// so the apply pass is two FMAs per element.  cb / cc overwrite coef_b / coef_c.
+__global__ void bn_finalize_bwd_kernel(const float* __restrict__ ws, int nblocks, int C, long long rows,
+                                       const float* __restrict__ p0, const float* __restrict__ p1,
+                                       const float* __restrict__ gamma, const float* __restrict__ invstd,
+                                       float* coef_b, float* coef_c, float* dgamma, float* dbeta) {
   const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (c >= C) return;
   double s1, s2;
   bn_warp_sum(ws, nblocks, C, c, s1, s2);
   if ((threadIdx.x & 31) != 0) return;
-  sum_dy[c] = (float)s1;
-  sum_dyxhat[c] = (float)s2;
   if (dgamma) dgamma[c] = (float)s2;
   if (dbeta) dbeta[c] = (float)s1;
+  const double k = (double)gamma[c] * (double)invstd[c];
+  const double inv_m = 1.0 / (double)rows;
+  const double a0 = p0[c], a1 = p1[c];
+  coef_b[c] = (float)(-k * a1 * s2 * inv_m);
+  coef_c[c] = (float)(-k * s1 * inv_m + k * a1 * a0 * s2 * inv_m);
 }
 
 // y = (x - mean) * invstd * gamma + beta   (train and replay share this kernel,
@@ -314,36 +338,33 @@ __global__ void bn_apply_kernel(const float* __restrict__ x, float* y, const flo
   }
 }
 
-// dx (=|+=) gamma*invstd*(dy - sum_dy/M - xhat*sum_dyxhat/M)
-// xhat from x (p0 = mean, p1 = invstd) or from y (p0 = beta, p1 = 1/gamma)
+// dx (=|+=) gamma*invstd*(dy - sum_dy/M - xhat*sum_dyxhat/M) = k*dy + cb*v + cc
+// (coefficients from bn_finalize_bwd; v = x or y, see there)
 __global__ void bn_bwd_apply_kernel(const float* __restrict__ s, const float* __restrict__ dy, float* dx,
-                                    const float* __restrict__ p0, const float* __restrict__ p1,
                                     const float* __restrict__ gamma, const float* __restrict__ invstd,
-                                    const float* __restrict__ sum_dy, const float* __restrict__ sum_dyxhat,
+                                    const float* __restrict__ coef_b, const float* __restrict__ coef_c,
                                     long long rows, int C, int accumulate) {
   const int cq = C / 4;
   const long long n4 = rows * cq;
-  const float inv_m = 1.0f / (float)rows;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
        i += (long long)gridDim.x * blockDim.x) {
     const int q = (int)(i % cq);
-    float4 v = *reinterpret_cast<const float4*>(s + 4 * i);
-    float4 g = *reinterpret_cast<const float4*>(dy + 4 * i);
-    float out[4];
-    const float vv[4] = {v.x, v.y, v.z, v.w};
-    const float gg[4] = {g.x, g.y, g.z, g.w};
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int ch = 4 * q + c;
-      const float xhat = (vv[c] - p0[ch]) * p1[ch];
-      const float k = gamma[ch] * invstd[ch];
-      out[c] = k * (gg[c] - sum_dy[ch] * inv_m - xhat * sum_dyxhat[ch] * inv_m);
-    }
+    const float4 v = *reinterpret_cast<const float4*>(s + 4 * i);
+    const float4 g = *reinterpret_cast<const float4*>(dy + 4 * i);
+    const float4 ga = *reinterpret_cast<const float4*>(gamma + 4 * q);
+    const float4 is = *reinterpret_cast<const float4*>(invstd + 4 * q);
+    const float4 cb = *reinterpret_cast<const float4*>(coef_b + 4 * q);
+    const float4 cc = *reinterpret_cast<const float4*>(coef_c + 4 * q);
+    float4 o;
+    o.x = fmaf(ga.x * is.x, g.x, fmaf(cb.x, v.x, cc.x));
+    o.y = fmaf(ga.y * is.y, g.y, fmaf(cb.y, v.y, cc.y));
+    o.z = fmaf(ga.z * is.z, g.z, fmaf(cb.z, v.z, cc.z));
+    o.w = fmaf(ga.w * is.w, g.w, fmaf(cb.w, v.w, cc.w));
     if (accumulate) {
-      float4 o = *reinterpret_cast<const float4*>(dx + 4 * i);
-      out[0] += o.x; out[1] += o.y; out[2] += o.z; out[3] += o.w;
+      const float4 d = *reinterpret_cast<const float4*>(dx + 4 * i);
+      o.x += d.x; o.y += d.y; o.z += d.z; o.w += d.w;
     }
-    *reinterpret_cast<float4*>(dx + 4 * i) = make_float4(out[0], out[1], out[2], out[3]);
+    *reinterpret_cast<float4*>(dx + 4 * i) = o;
   }
 }
 
