@@ -132,6 +132,30 @@ size_t monet_gemm_ws_bytes(int variant, int m, int n, int k);
 int monet_arena_plan(int64_t count, const int64_t* sizes, const int64_t* t_alloc, const int64_t* t_free,
                      int64_t align, int64_t capacity_bytes, int64_t* offsets, int64_t* peak_bytes);
 
+/* --- host ILP: exact 0-1 branch-and-bound (replaces solver.solve, solver.py:441) ---
+ * Same propagation, bound (+ capacity surrogate), branch order, dives and
+ * limits as the reference, so decisions are bit-exact; costs are integers
+ * (the objective scaled by the lcm of its denominators), 128-bit values are
+ * (hi, lo) int64 pairs.  See paper_2010_14501_b200/solver.py for the packing. */
+void* monet_bnb_create(int n_vars, int n_rows, const int* row_ptr, const int* row_var, const int64_t* row_coef,
+                       const int64_t* row_rhs, const int* row_is_eq, int n_fix, const int* fix_var, const int* fix_val,
+                       int n_obj, const int* obj_var, const int64_t* obj_cost128, int n_fwd, int n_bwd, int n_re,
+                       const int* grp_ptr, const int* grp_var, const int64_t* grp_cost128, const int* re_rvar);
+int monet_bnb_set_surrogate(void* h, int64_t cap_base, int n_stages, const int64_t* grad, const int* var_ptr,
+                            const int* var_db, const int64_t* var_ws, const int* dep_ptr, const int* dep_idx,
+                            int n_storables, const int64_t* size, const int64_t* recost, const int* rcol);
+void monet_bnb_destroy(void* h);
+int monet_bnb_propagate(void* h, int n_partial, const int* pvar, const int* pval, signed char* out);
+int monet_bnb_lower_bound(void* h, int n_partial, const int* pvar, const int* pval, int64_t scale, int64_t* out128);
+/* opts: node_limit (-1 none), telemetry_every, dive_bound, most_tight, gap_num, gap_den (0 none), scale.
+ * Returns 0 optimal, 1 feasible-gap, 2 infeasible, 3 timeout-no-incumbent. */
+int monet_bnb_solve(void* h, const int64_t* opts, double time_limit_s, const int* order, int n_order,
+                    const signed char* pref, int has_inc, const int64_t* inc_obj128, const signed char* inc_vals,
+                    int64_t* nodes_out, int64_t* res128);
+int monet_bnb_best(void* h, signed char* out);
+int monet_bnb_n_events(void* h);
+int monet_bnb_event(void* h, int i, int* kinds, int64_t* counts, int64_t* vals128);
+
 #ifdef __cplusplus
 }
 #endif

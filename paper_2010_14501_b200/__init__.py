@@ -21,13 +21,12 @@ from .schedule import (Schedule, SimulationError, StagePlan, Trace, checkpoint_h
                        decode, schedule_from_doc, schedule_to_doc, simulate,
                        store_everything_schedule, trace_report, validate)
 
-try:  # planner modules land incrementally; the executor does not need them
-    from .ilp import (Model, assignment_from_schedule, build_model, evaluate_assignment,
-                      export_lp, export_lp_string)
-    from .solver import SolveResult, lower_bound, propagate, solve
-    from .enumerate import OracleResult, cross_check, enumerate_schedules
-except ImportError:  # pragma: no cover
-    pass
+from .ilp import (Model, assignment_from_schedule, build_model, evaluate_assignment,
+                  export_lp, export_lp_string)
+from .solver import SolveResult, lower_bound, propagate, solve
+from .enumerate import ORACLE_DEFAULTS, OracleResult, cross_check, enumerate_schedules
+from . import enumerate as oracle  # the reference names this module `oracle` (oracle.py)
+from . import ilp, solver  # noqa: E402  (module attributes, as in remsched/__init__.py)
 
 
 def __getattr__(name):

@@ -60,6 +60,17 @@ SIGNATURES = {
                           _vp]),
     "monet_gemm_ws_bytes": (_sz, [_i32, _i32, _i32, _i32]),
     "monet_arena_plan": (_i32, [_i64, _vp, _vp, _vp, _i64, _i64, _vp, _vp]),
+    # host ILP branch-and-bound (csrc/bnb.cpp)
+    "monet_bnb_create": (_vp, [_i32, _i32] + [_vp] * 5 + [_i32, _vp, _vp, _i32, _vp, _vp, _i32, _i32, _i32] +
+                         [_vp] * 4),
+    "monet_bnb_set_surrogate": (_i32, [_vp, _i64, _i32] + [_vp] * 6 + [_i32] + [_vp] * 3),
+    "monet_bnb_destroy": (None, [_vp]),
+    "monet_bnb_propagate": (_i32, [_vp, _i32, _vp, _vp, _vp]),
+    "monet_bnb_lower_bound": (_i32, [_vp, _i32, _vp, _vp, _i64, _vp]),
+    "monet_bnb_solve": (_i32, [_vp, _vp, C.c_double, _vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp]),
+    "monet_bnb_best": (_i32, [_vp, _vp]),
+    "monet_bnb_n_events": (_i32, [_vp]),
+    "monet_bnb_event": (_i32, [_vp, _i32, _vp, _vp, _vp]),
 }
 
 CONV_VARIANTS = {"implicit": 0, "splitk": 1, "tf32": 2, "tf32x3": 3}

@@ -21,7 +21,7 @@ LIB = PKG / "libmonet_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 CU_SOURCES = ["capi.cu"]
-CPP_SOURCES = ["arena.cpp"]
+CPP_SOURCES = ["arena.cpp", "bnb.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
