@@ -7,7 +7,9 @@
 // plan is "greedy by size": place blocks in decreasing size order at the
 // lowest aligned offset that does not overlap any already placed block whose
 // lifetime intersects.  The high-water mark is reported and must stay below
-// the byte budget (and is compared with the ILP bound by the engine).
+// the byte budget; the engine compares params + high-water with the ILP bound
+// (check_schedule), which equals the ledger peak on the ResNet-50 schedules,
+// so the packing has to be gap-free at the peak instant.
 #include <algorithm>
 #include <cstdint>
 #include <numeric>
@@ -15,32 +17,28 @@
 
 #include "../../include/monet_b200.h"
 
-extern "C" int monet_arena_plan(int64_t count, const int64_t* sizes, const int64_t* t_alloc, const int64_t* t_free,
-                                int64_t align, int64_t capacity_bytes, int64_t* offsets, int64_t* peak_bytes) {
-  if (count < 0 || align <= 0) return -22;
-  std::vector<int64_t> order(count);
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
-    if (sizes[a] != sizes[b]) return sizes[a] > sizes[b];
-    return t_alloc[a] < t_alloc[b];
-  });
+namespace {
+
+// Place blocks in the given order, each at the best-fitting gap among the
+// already placed blocks whose lifetimes intersect it (else on top).
+int64_t place(const std::vector<int64_t>& order, const int64_t* sizes, const int64_t* t_alloc,
+              const int64_t* t_free, int64_t align, std::vector<int64_t>& offs) {
   auto rnd = [&](int64_t v) { return (v + align - 1) / align * align; };
-  std::vector<int64_t> placed;  // indices already assigned, kept sorted by offset
-  placed.reserve(count);
+  std::vector<int64_t> placed;
+  placed.reserve(order.size());
+  std::vector<std::pair<int64_t, int64_t>> busy;
   int64_t peak = 0;
-  std::vector<std::pair<int64_t, int64_t>> busy;  // [begin, end) of conflicting placed blocks
   for (int64_t idx : order) {
     const int64_t need = rnd(std::max<int64_t>(sizes[idx], 1));
     busy.clear();
-    for (int64_t j : placed) {
-      if (t_alloc[j] < t_free[idx] && t_alloc[idx] < t_free[j]) busy.emplace_back(offsets[j], offsets[j] + rnd(std::max<int64_t>(sizes[j], 1)));
-    }
+    for (int64_t j : placed)
+      if (t_alloc[j] < t_free[idx] && t_alloc[idx] < t_free[j])
+        busy.emplace_back(offs[j], offs[j] + rnd(std::max<int64_t>(sizes[j], 1)));
     std::sort(busy.begin(), busy.end());
-    // best fit: smallest gap that holds the block, else the end
     int64_t best = -1, best_gap = INT64_MAX, cursor = 0;
     for (auto& b : busy) {
       if (b.first > cursor) {
-        int64_t gap = b.first - cursor;
+        const int64_t gap = b.first - cursor;
         if (gap >= need && gap < best_gap) {
           best = cursor;
           best_gap = gap;
@@ -49,11 +47,82 @@ extern "C" int monet_arena_plan(int64_t count, const int64_t* sizes, const int64
       cursor = std::max(cursor, b.second);
     }
     if (best < 0) best = cursor;
-    offsets[idx] = best;
+    offs[idx] = best;
     peak = std::max(peak, best + need);
     placed.push_back(idx);
   }
-  *peak_bytes = peak;
-  if (capacity_bytes > 0 && peak > capacity_bytes) return -12;
+  return peak;
+}
+
+}  // namespace
+
+// Several deterministic orderings are tried and the lowest high-water mark
+// wins (ties: the earlier strategy):
+//   0 size descending (classic greedy)
+//   1 "heat" descending -- the largest live-byte total over the block's
+//     lifetime first, so the blocks of the global peak pack gap-free at the
+//     bottom -- then size
+//   2 blocks live at the peak instant first (by allocation time), then size
+//   3 allocation order (what a first-fit runtime allocator would see)
+extern "C" int monet_arena_plan(int64_t count, const int64_t* sizes, const int64_t* t_alloc, const int64_t* t_free,
+                                int64_t align, int64_t capacity_bytes, int64_t* offsets, int64_t* peak_bytes) {
+  if (count < 0 || align <= 0) return -22;
+  int64_t horizon = 1;
+  for (int64_t i = 0; i < count; ++i) horizon = std::max(horizon, t_free[i] + 1);
+  auto rnd = [&](int64_t v) { return (v + align - 1) / align * align; };
+  std::vector<int64_t> live(horizon + 1, 0);  // live rounded bytes per event time
+  for (int64_t i = 0; i < count; ++i) {
+    live[t_alloc[i]] += rnd(std::max<int64_t>(sizes[i], 1));
+    live[t_free[i]] -= rnd(std::max<int64_t>(sizes[i], 1));
+  }
+  int64_t t_peak = 0, run = 0, best_live = -1;
+  for (int64_t t = 0; t < horizon; ++t) {
+    run += live[t];
+    live[t] = run;
+    if (run > best_live) {
+      best_live = run;
+      t_peak = t;
+    }
+  }
+  std::vector<int64_t> heat(count, 0);
+  for (int64_t i = 0; i < count; ++i)
+    for (int64_t t = t_alloc[i]; t < t_free[i]; ++t) heat[i] = std::max(heat[i], live[t]);
+
+  std::vector<int64_t> base(count);
+  std::iota(base.begin(), base.end(), 0);
+  auto by_size = [&](int64_t a, int64_t b) {
+    if (sizes[a] != sizes[b]) return sizes[a] > sizes[b];
+    return t_alloc[a] < t_alloc[b];
+  };
+  std::vector<std::vector<int64_t>> orders(4, base);
+  std::stable_sort(orders[0].begin(), orders[0].end(), by_size);
+  std::stable_sort(orders[1].begin(), orders[1].end(), [&](int64_t a, int64_t b) {
+    if (heat[a] != heat[b]) return heat[a] > heat[b];
+    return by_size(a, b);
+  });
+  std::stable_sort(orders[2].begin(), orders[2].end(), [&](int64_t a, int64_t b) {
+    const bool pa = t_alloc[a] <= t_peak && t_peak < t_free[a], pb = t_alloc[b] <= t_peak && t_peak < t_free[b];
+    if (pa != pb) return pa;
+    if (pa) return t_alloc[a] < t_alloc[b];
+    return by_size(a, b);
+  });
+  std::stable_sort(orders[3].begin(), orders[3].end(), [&](int64_t a, int64_t b) {
+    if (t_alloc[a] != t_alloc[b]) return t_alloc[a] < t_alloc[b];
+    return a < b;
+  });
+  std::vector<int64_t> offs(count), best_offs;
+  int64_t best = INT64_MAX;
+  for (const auto& order : orders) {
+    const int64_t peak = place(order, sizes, t_alloc, t_free, align, offs);
+    if (peak < best) {
+      best = peak;
+      best_offs = offs;
+    }
+    if (best == best_live) break;  // gap-free at the peak: optimal
+  }
+  if (count == 0) best = 0;
+  std::copy(best_offs.begin(), best_offs.end(), offsets);
+  *peak_bytes = best;
+  if (capacity_bytes > 0 && best > capacity_bytes) return -12;
   return 0;
 }

@@ -1,0 +1,229 @@
+"""On-device profiler: measured catalog for the planner.
+
+``profile(model, batch, device)`` times every (operator, variant) of a traced
+network on the B200 with CUDA events -- the same sm_100a kernels and the same
+argument shapes the executor launches -- and emits the catalog document the
+reference planner consumes (costmodel.py:85-181): per node, ordered forward /
+backward variants with integer ``workspace_bytes`` (the bytes the variant
+takes from the arena, from the library's own workspace queries) and an
+integer ``cost`` in nanoseconds (units.py:46-67 forbids floats).
+
+Timing: after `warmup` launches, the median of `reps` event-timed groups of
+`iters` launches; identical shapes are measured once.  Catalogs are frozen to
+JSON for planning (costs vary run to run).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import statistics
+
+import torch
+
+from . import _native
+
+__all__ = ["profile", "profile_network"]
+
+
+class _Bench:
+    def __init__(self, device, warmup=2, iters=5, reps=3):
+        self.dev = torch.device(device)
+        self.warmup, self.iters, self.reps = warmup, iters, reps
+        self.lib = _native.lib().dll
+        self.stream = torch.cuda.current_stream(self.dev)
+        self.sp = C.c_void_p(self.stream.cuda_stream)
+
+    def time_ns(self, fn) -> int:
+        for _ in range(self.warmup):
+            fn()
+        samples = []
+        for _ in range(self.reps):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(self.stream)
+            for _ in range(self.iters):
+                fn()
+            b.record(self.stream)
+            b.synchronize()
+            samples.append(a.elapsed_time(b) * 1e6 / self.iters)
+        return max(1, int(round(statistics.median(samples))))
+
+    def buf(self, nbytes: int) -> torch.Tensor:
+        t = torch.empty(max(int(nbytes), 16) // 4 + 1, dtype=torch.float32, device=self.dev)
+        return t.normal_()
+
+    def check(self, rc):
+        if rc != 0:
+            raise _native.NativeError(f"profiled kernel failed with code {rc}")
+
+
+def _conv_calls(bx: _Bench, net, op, variant: str):
+    """(fwd closure, bwd closure, fwd ws, bwd ws) of a conv variant."""
+    lib, sp = bx.lib, bx.sp
+    d = net.conv_desc(op)
+    v = _native.CONV_VARIANTS[variant]
+    xin = net.op(op.deps[0])
+    x = bx.buf(xin.nbytes)
+    w = bx.buf(4 * op.attrs["r"] * op.attrs["s"] * xin.shape[3] * op.shape[3])
+    y = bx.buf(op.nbytes)
+    dy = bx.buf(op.nbytes)
+    dx = bx.buf(xin.nbytes)
+    dw = bx.buf(w.numel() * 4)
+    ws_f = lib.monet_conv_ws_bytes(v, 0, C.byref(d))
+    ws_b = lib.monet_conv_ws_bytes(v, 3, C.byref(d))
+    ws = bx.buf(max(ws_f, ws_b))
+    need_dx = xin.kind != "input"
+
+    def fwd():
+        bx.check(lib.monet_conv_fwd(v, C.byref(d), x.data_ptr(), w.data_ptr(), y.data_ptr(), ws.data_ptr(), ws_f, sp))
+
+    def bwd():
+        if need_dx:
+            bx.check(lib.monet_conv_dgrad(v, C.byref(d), dy.data_ptr(), w.data_ptr(), dx.data_ptr(), 0,
+                                          ws.data_ptr(), ws_b, sp))
+        bx.check(lib.monet_conv_wgrad(v, C.byref(d), x.data_ptr(), dy.data_ptr(), dw.data_ptr(), 0, ws.data_ptr(),
+                                      ws_b, sp))
+    return fwd, bwd
+
+
+def _local_calls(bx: _Bench, net, op):
+    """{(pass, variant): closure} for the non-conv operators (engine.Runtime._bind)."""
+    lib, sp = bx.lib, bx.sp
+    out = {}
+    n = op.numel
+    kind = op.kind
+    if kind == "input":
+        y, src = bx.buf(op.nbytes), bx.buf(op.nbytes)
+        out[("fwd", "load")] = lambda: bx.check(lib.monet_copy_async(y.data_ptr(), src.data_ptr(), op.nbytes, sp))
+        return out
+    xin = net.op(op.deps[0])
+    x, y, dy, dx = bx.buf(xin.nbytes), bx.buf(op.nbytes), bx.buf(op.nbytes), bx.buf(xin.nbytes)
+    if kind == "relu":
+        mask = bx.buf((n + 31) // 32 * 4)
+        out[("fwd", "relu")] = lambda: bx.check(lib.monet_relu_fwd(x.data_ptr(), y.data_ptr(), mask.data_ptr(), n, sp))
+        out[("bwd", "bwd-in")] = lambda: bx.check(lib.monet_relu_bwd_in(x.data_ptr(), dy.data_ptr(), dx.data_ptr(), n,
+                                                                         0, sp))
+        out[("bwd", "bwd-out")] = lambda: bx.check(lib.monet_relu_bwd_out(y.data_ptr(), dy.data_ptr(), dx.data_ptr(),
+                                                                           n, 0, sp))
+        out[("bwd", "bwd-mask")] = lambda: bx.check(lib.monet_relu_bwd_mask(mask.data_ptr(), dy.data_ptr(),
+                                                                             dx.data_ptr(), n, 0, sp))
+    elif kind == "bn":
+        c = op.shape[-1]
+        rows = n // c
+        ch = [bx.buf(4 * c) for _ in range(8)]  # gamma beta mean invstd rmean rvar dgamma dbeta
+        for t in ch[:4]:
+            t.abs_().add_(0.5)
+        scratch = bx.buf(lib.monet_bn_scratch_bytes(rows, c))
+        g_, b_, m_, s_, rm, rv, dg, db = (t.data_ptr() for t in ch)
+        out[("fwd", "bn")] = lambda: bx.check(lib.monet_bn_fwd_train(
+            x.data_ptr(), y.data_ptr(), g_, b_, m_, s_, rm, rv, rows, c, C.c_float(1e-5), C.c_float(0.1), 1,
+            scratch.data_ptr(), sp))
+        out[("bwd", "bwd-in")] = lambda: bx.check(lib.monet_bn_bwd_in(
+            x.data_ptr(), dy.data_ptr(), dx.data_ptr(), 0, g_, m_, s_, dg, db, rows, c, scratch.data_ptr(), sp))
+        out[("bwd", "bwd-out")] = lambda: bx.check(lib.monet_bn_bwd_out(
+            y.data_ptr(), dy.data_ptr(), dx.data_ptr(), 0, g_, b_, s_, dg, db, rows, c, scratch.data_ptr(), sp))
+    elif kind == "add":
+        x2 = bx.buf(op.nbytes)
+        out[("fwd", "add")] = lambda: bx.check(lib.monet_add_fwd(x.data_ptr(), x2.data_ptr(), y.data_ptr(), n, sp))
+
+        def add_bwd():
+            for _ in range(2):
+                bx.check(lib.monet_grad_pass(dy.data_ptr(), dx.data_ptr(), n, C.c_float(1.0), 0, sp))
+        out[("bwd", "bwd")] = add_bwd
+    elif kind == "maxpool":
+        d = net.pool_desc(op)
+        idx = bx.buf(op.numel)
+        out[("fwd", "maxpool")] = lambda: bx.check(lib.monet_maxpool_fwd(C.byref(d), x.data_ptr(), y.data_ptr(),
+                                                                          idx.data_ptr(), sp))
+        out[("bwd", "bwd-in")] = lambda: bx.check(lib.monet_maxpool_bwd(C.byref(d), None, x.data_ptr(),
+                                                                         dy.data_ptr(), dx.data_ptr(), 0, sp))
+
+        def bwd_idx():  # a valid index tensor first (window positions 0..R*S-1)
+            bx.check(lib.monet_maxpool_bwd(C.byref(d), idx.data_ptr(), None, dy.data_ptr(), dx.data_ptr(), 0, sp))
+        lib.monet_maxpool_fwd(C.byref(d), x.data_ptr(), y.data_ptr(), idx.data_ptr(), sp)
+        out[("bwd", "bwd-idx")] = bwd_idx
+    elif kind == "avgpool":
+        nb, h, w, c = xin.shape
+        out[("fwd", "avgpool")] = lambda: bx.check(lib.monet_avgpool_fwd(x.data_ptr(), y.data_ptr(), nb, h * w, c, sp))
+        out[("bwd", "bwd")] = lambda: bx.check(lib.monet_avgpool_bwd(dy.data_ptr(), dx.data_ptr(), nb, h * w, c, 0,
+                                                                       sp))
+    elif kind == "fc":
+        nb, fi = xin.shape
+        fo = op.shape[1]
+        wgt, bias, dw, dbias = bx.buf(4 * fi * fo), bx.buf(4 * fo), bx.buf(4 * fi * fo), bx.buf(4 * fo)
+        for name, v in (("gemm", 0), ("gemm-splitk", 1)):
+            wf = lib.monet_linear_ws_bytes(v, 0, nb, fi, fo)
+            wb = lib.monet_linear_ws_bytes(v, 3, nb, fi, fo)
+            ws = bx.buf(max(wf, wb))
+            out[("fwd", name)] = (lambda v=v, wf=wf, ws=ws: bx.check(lib.monet_linear_fwd(
+                v, x.data_ptr(), wgt.data_ptr(), bias.data_ptr(), y.data_ptr(), nb, fi, fo, ws.data_ptr(), wf, sp)))
+            out[("bwd", name)] = (lambda v=v, wb=wb, ws=ws: bx.check(lib.monet_linear_bwd(
+                v, x.data_ptr(), wgt.data_ptr(), dy.data_ptr(), dx.data_ptr(), 0, dw.data_ptr(), dbias.data_ptr(),
+                nb, fi, fo, ws.data_ptr(), wb, sp)))
+    elif kind == "xent":
+        nb, classes = xin.shape
+        labels = torch.randint(0, classes, (nb,), dtype=torch.int32, device=bx.dev)
+        loss = bx.buf(4)
+        scratch = bx.buf(lib.monet_xent_scratch_bytes(nb))
+        one = torch.ones(1, device=bx.dev)
+        out[("fwd", "xent")] = lambda: bx.check(lib.monet_xent_fwd(x.data_ptr(), labels.data_ptr(), loss.data_ptr(),
+                                                                    nb, classes, scratch.data_ptr(), sp))
+        out[("bwd", "bwd")] = lambda: bx.check(lib.monet_xent_bwd(x.data_ptr(), labels.data_ptr(), one.data_ptr(),
+                                                                   dx.data_ptr(), nb, classes, 0, sp))
+    else:
+        raise ValueError(f"profiler: unsupported op kind {kind!r}")
+    return out
+
+
+def _signature(net, op):
+    ins = tuple((net.op(j).kind == "input", net.op(j).shape) for j in op.deps)
+    attrs = tuple(sorted((k, v) for k, v in op.attrs.items() if isinstance(v, (int, float, str))))
+    return op.kind, ins, op.shape, attrs
+
+
+def profile_network(net, device="cuda:0", warmup=2, iters=5, reps=3, log=None) -> dict:
+    """{(node, "fwd"|"bwd", variant name): ns} for every variant of every node."""
+    bx = _Bench(device, warmup, iters, reps)
+    cache: dict[tuple, dict] = {}
+    costs: dict[tuple, int] = {}
+    for op in net.ops:
+        fv, bv = net.variants(op)
+        sig = _signature(net, op)
+        if sig not in cache:
+            res = {}
+            if op.kind == "conv":
+                for name, _ in fv:
+                    f, _b = _conv_calls(bx, net, op, name)
+                    res[("fwd", name)] = bx.time_ns(f)
+                for name, _, _ in bv:
+                    _f, b = _conv_calls(bx, net, op, name)
+                    res[("bwd", name)] = bx.time_ns(b)
+            else:
+                calls = _local_calls(bx, net, op)
+                for name, _ in fv:
+                    res[("fwd", name)] = bx.time_ns(calls[("fwd", name)])
+                for name, _, _ in bv:
+                    key = ("bwd", name)
+                    res[key] = bx.time_ns(calls[key]) if key in calls else 1  # e.g. the input's "none"
+            cache[sig] = res
+            torch.cuda.empty_cache()
+            if log:
+                log(f"{op.name or op.kind:28s} {op.kind:8s} {res}")
+        for (pss, name), ns in cache[sig].items():
+            costs[(op.id, pss, name)] = ns
+    return costs
+
+
+def profile(model, batch: int | None = None, device="cuda:0", image: int = 224, num_classes: int = 1000,
+            **kw) -> dict:
+    """Measured catalog document of `model` (a traced Network, a torchvision
+    architecture name, or a torch module traced at [batch, 3, image, image])."""
+    from .tracer import Network, build_network, trace_graph
+
+    if isinstance(model, Network):
+        net = model
+    elif isinstance(model, str):
+        net = build_network(model, batch, image, num_classes)
+    else:
+        net = trace_graph(model, torch.empty(batch, 3, image, image, device="meta"), num_classes)
+    return net.catalog_doc(profile_network(net, device, **kw))

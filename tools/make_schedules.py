@@ -31,6 +31,12 @@ def main(jobs):
     for arch, batch, img, gib in jobs:
         net = build_network(arch, batch, img)
         gdoc, cdoc = net.graph_doc(), net.catalog_doc()
+        measured = ROOT / "profiles" / f"catalog_{arch}_b{batch}_{img}.json"
+        if measured.exists():  # plan with the on-device profile when it matches this graph
+            mdoc = json.loads(measured.read_text())
+            if mdoc["graph_digest"] == digest(gdoc):
+                cdoc = mdoc["catalog"]
+                print("planning with measured catalog", measured.name)
         g = M.load_graph(gdoc)
         cat = M.load_catalog(cdoc, g)
         budget = int(gib * (1 << 30))
