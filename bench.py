@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--batch", type=int, default=184)
     ap.add_argument("--image", type=int, default=224)
     ap.add_argument("--budget-gib", type=float, default=8.0)
+    ap.add_argument("--no-fuse", dest="fuse", action="store_false",
+                    help="separate BN and ReLU operators (default: fused BN+ReLU ops, tracer fuse=True)")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels from Python instead of a CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-overhead-run", action="store_true", help="skip timing the store-everything schedule")
@@ -56,7 +58,7 @@ def load_or_plan(net, g, cat, budget, arch, batch, image, gib):
     import paper_2010_14501_b200 as M
     from paper_2010_14501_b200.planner import plan_schedule
 
-    path = ROOT / "schedules" / f"{arch}_b{batch}_{image}_{gib:g}gib.json"
+    path = ROOT / "schedules" / f"{arch}{'_fused' if net.fused else ''}_b{batch}_{image}_{gib:g}gib.json"
     digest = lambda d: hashlib.sha256(json.dumps(d, sort_keys=True).encode()).hexdigest()[:16]  # noqa: E731
     if path.exists():
         doc = json.loads(path.read_text())
@@ -72,7 +74,7 @@ def measured_catalog(net, args):
     """The frozen on-device profile (tools/profile_catalog.py) when it matches this graph."""
     import hashlib
 
-    path = ROOT / "profiles" / f"catalog_{args.arch}_b{args.batch}_{args.image}.json"
+    path = ROOT / "profiles" / f"catalog_{args.arch}{'_fused' if args.fuse else ''}_b{args.batch}_{args.image}.json"
     if not path.exists():
         return None
     doc = json.loads(path.read_text())
@@ -132,6 +134,7 @@ LOCAL_BYTES = {  # minimal fp32 HBM bytes per element
     ("relu", "forward", True): 8.125, ("relu", "forward", False): 8.0, ("relu", "bwd-mask"): 8.125,
     ("relu", "bwd-in"): 12.0, ("relu", "bwd-out"): 12.0, ("bn", "train"): 12.0, ("bn", "replay"): 8.0,
     ("bn", "bwd"): 20.0, ("add", "forward"): 12.0, ("add", "bwd"): 16.0,
+    ("bnrelu", "train"): 12.0, ("bnrelu", "replay"): 8.0, ("bnrelu", "bwd"): 20.0,
 }
 
 
@@ -169,11 +172,11 @@ def kernel_roofline(rt, plan, net, peaks):
             conv_t += ms
             conv_f += f
             n_conv += 1
-        elif op.kind in ("relu", "bn", "add"):
+        elif op.kind in ("relu", "bn", "bnrelu", "add"):
             if s.kind == "backward":
                 key = (op.kind, "bwd") if op.kind != "relu" else ("relu", s.impl)
-            elif op.kind == "bn":
-                key = ("bn", "train" if s.kind == "forward" else "replay")
+            elif op.kind in ("bn", "bnrelu"):
+                key = (op.kind, "train" if s.kind == "forward" else "replay")
             elif op.kind == "relu":
                 key = ("relu", "forward", net.intermediate_of[op.id] in s.planned_ints)
             else:
@@ -280,7 +283,7 @@ def ours_arm(args):
 
     gib = args.budget_gib
     budget = int(gib * (1 << 30))
-    net = build_network(args.arch, args.batch, args.image)
+    net = build_network(args.arch, args.batch, args.image, fuse=args.fuse)
     gdoc = net.graph_doc()
     g = M.load_graph(gdoc)
     cat = M.load_catalog(measured_catalog(net, args) or net.catalog_doc(), g)
@@ -408,7 +411,8 @@ def ours_arm(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f32 (convs: bf16x3-split tensor-core MMAs, fp32 accumulate)",
             "data": "synthetic N(0,1) images, uniform labels; random-init torchvision weights (seed 0)",
             "config": {"workload": f"{args.arch} {args.image}x{args.image} batch {args.batch}/GPU, "
-                                   f"{gib:g} GiB per-GPU budget, MONeT schedule ({source})",
+                                   f"{gib:g} GiB per-GPU budget, MONeT schedule ({source})"
+                                   + (", fused BN+ReLU operators" if args.fuse else ""),
                        "model": args.arch, "global_batch": world * args.batch, "per_gpu_batch": args.batch,
                        "image": args.image, "budget_bytes": budget, "parallelism": f"dp{world}",
                        "cuda_graph": use_graph,

@@ -43,7 +43,7 @@ class CpuState:
         self.mom = {k: torch.zeros_like(v) for k, v in self.params.items()}
         self.running = {op.id: [op.attrs["running_mean"].to(dtype).clone(),
                                 op.attrs["running_var"].to(dtype).clone()]
-                        for op in net.ops if op.kind == "bn"}
+                        for op in net.ops if op.kind in ("bn", "bnrelu")}
         self.saved = {}
         self.grads = {}
 
@@ -109,7 +109,7 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
         elif op.kind == "conv":
             a = op.attrs
             y = F.conv2d(xs[0], P[(op.id, "weight")], stride=a["stride"], padding=a["pad"])
-        elif op.kind == "bn":
+        elif op.kind in ("bn", "bnrelu"):
             g, b = P[(op.id, "weight")], P[(op.id, "bias")]
             if mode == "forward":
                 mean, invstd, var = _bn_stats(xs[0], op.attrs["eps"])
@@ -121,6 +121,8 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
                 rv.mul_(1 - m).add_(m * var * rows / max(rows - 1, 1))
             mean, invstd = state.saved[op.id]
             y = _bn_apply(xs[0], mean, invstd, g, b)
+            if op.kind == "bnrelu":  # fused: relu(BN(x)); the BN output is never kept
+                y = torch.where(y > 0, y, torch.zeros_like(y))
         elif op.kind == "relu":
             x = xs[0]
             y = torch.where(x > 0, x, torch.zeros_like(x))
@@ -164,11 +166,13 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
             if net.grad_bytes(net.op(j)) > 0:
                 put_grad(j, torch.nn.grad.conv2d_input(x.shape, w, dy, a["stride"], a["pad"]), created)
             state.grads[(op.id, "weight")] = torch.nn.grad.conv2d_weight(x, w.shape, dy, a["stride"], a["pad"])
-        elif op.kind == "bn":
+        elif op.kind in ("bn", "bnrelu"):
             j = op.deps[0]
             g, b = P[(op.id, "weight")], P[(op.id, "bias")]
             mean, invstd = state.saved[op.id]
             v = lambda t: t.view(1, -1, 1, 1)
+            if op.kind == "bnrelu":  # gate by the recomputed BN output's sign (PAPER App. D, K10)
+                dy = torch.where(_bn_apply(x_of(j), mean, invstd, g, b) > 0, dy, torch.zeros_like(dy))
             if impl == "bwd-in":
                 xhat = (x_of(j) - v(mean)) * v(invstd)
             else:

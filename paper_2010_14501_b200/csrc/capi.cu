@@ -578,6 +578,47 @@ int monet_bn_bwd_out(const float* y, const float* dy, float* dx, int accumulate,
   return bn_bwd_common(y, dy, dx, accumulate, gamma, beta, inv_gamma, saved_invstd, dgamma, dbeta, rows, c, 2, ws, st);
 }
 
+// ------------------------------------------------------------------- fused BN+ReLU (K9 / K10)
+int monet_bnrelu_fwd_train(const float* x, float* z, const float* gamma, const float* beta, float* saved_mean,
+                           float* saved_invstd, float* running_mean, float* running_var, int64_t rows, int c,
+                           float eps, float momentum, int update_running, void* scratch, void* stream) {
+  if (c % 4) return -(int)cudaErrorInvalidValue;
+  cudaStream_t st = S(stream);
+  float* ws = static_cast<float*>(scratch);
+  int nb = bn_blocks(rows);
+  bn_reduce_kernel<<<nb, kEwThreads, 0, st>>>(0, x, nullptr, nullptr, nullptr, rows, c, ws);
+  bn_finalize_fwd_kernel<<<(c + 7) / 8, 256, 0, st>>>(ws, nb, rows, c, eps, momentum, update_running, saved_mean,
+                                                      saved_invstd, running_mean, running_var);
+  bnrelu_apply_kernel<<<ew_blocks(rows * c / 4), kEwThreads, 0, st>>>(x, z, saved_mean, saved_invstd, gamma, beta,
+                                                                      rows, c);
+  return last_error();
+}
+
+int monet_bnrelu_fwd_replay(const float* x, float* z, const float* gamma, const float* beta, const float* saved_mean,
+                            const float* saved_invstd, int64_t rows, int c, void* stream) {
+  if (c % 4) return -(int)cudaErrorInvalidValue;
+  bnrelu_apply_kernel<<<ew_blocks(rows * c / 4), kEwThreads, 0, S(stream)>>>(x, z, saved_mean, saved_invstd, gamma,
+                                                                             beta, rows, c);
+  return last_error();
+}
+
+int monet_bnrelu_bwd(const float* x, const float* dz, float* dx, int accumulate, const float* gamma,
+                     const float* beta, const float* saved_mean, const float* saved_invstd, float* dgamma,
+                     float* dbeta, int64_t rows, int c, void* scratch, void* stream) {
+  if (c % 4) return -(int)cudaErrorInvalidValue;
+  cudaStream_t st = S(stream);
+  float* ws = static_cast<float*>(scratch);
+  int nb = bn_blocks(rows);
+  float* coef_b = ws + (size_t)nb * 2 * c;
+  float* coef_c = coef_b + c;
+  bn_reduce_kernel<<<nb, kEwThreads, 0, st>>>(3, x, dz, saved_mean, saved_invstd, rows, c, ws, gamma, beta);
+  bn_finalize_bwd_kernel<<<(c + 7) / 8, 256, 0, st>>>(ws, nb, c, rows, saved_mean, saved_invstd, gamma,
+                                                      saved_invstd, coef_b, coef_c, dgamma, dbeta);
+  bnrelu_bwd_apply_kernel<<<ew_blocks(rows * c / 4), kEwThreads, 0, st>>>(
+      x, dz, dx, saved_mean, beta, gamma, saved_invstd, coef_b, coef_c, rows, c, accumulate);
+  return last_error();
+}
+
 // ------------------------------------------------------------------- add / pass
 int monet_add_fwd(const float* a, const float* b, float* y, int64_t n, void* stream) {
   add_kernel<<<ew_blocks(n / 4 + 1), kEwThreads, 0, S(stream)>>>(a, b, y, n);

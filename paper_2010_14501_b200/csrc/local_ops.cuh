@@ -180,9 +180,12 @@ __host__ __device__ inline BnLayout bn_layout(int C) {
 // mode 0: sum x, sum x^2           (forward statistics)
 // mode 1: sum dy, sum dy*xhat      (backward, xhat = (x-mean)*invstd)
 // mode 2: sum dy, sum dy*xhat      (backward, xhat = (y-beta)/gamma)
+// mode 3: as mode 1 with dy = dz * [gamma*xhat + beta > 0]  (fused BN+ReLU
+//         backward from x; p2 / p3 = gamma / beta)
 __global__ void bn_reduce_kernel(int mode, const float* __restrict__ x, const float* __restrict__ dy,
                                  const float* __restrict__ p0, const float* __restrict__ p1, long long rows, int C,
-                                 float* __restrict__ ws) {
+                                 float* __restrict__ ws, const float* __restrict__ p2 = nullptr,
+                                 const float* __restrict__ p3 = nullptr) {
   const BnLayout L = bn_layout(C);
   const int t = threadIdx.x;
   const int rsub = t / L.tpr;
@@ -195,12 +198,22 @@ __global__ void bn_reduce_kernel(int mode, const float* __restrict__ x, const fl
     const int q = qbase + qi * L.tpr;
     float s1[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
     if (rsub < L.rpi && q < C / 4) {
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a, ga = a, be = a;
       if (mode != 0) {
         a = *reinterpret_cast<const float4*>(p0 + 4 * q);  // mean | beta
         b = *reinterpret_cast<const float4*>(p1 + 4 * q);  // invstd | 1/gamma
       }
-      auto acc = [&](const float4& v, const float4& g) {
+      if (mode == 3) {
+        ga = *reinterpret_cast<const float4*>(p2 + 4 * q);
+        be = *reinterpret_cast<const float4*>(p3 + 4 * q);
+      }
+      auto acc = [&](const float4& v, float4 g) {
+        if (mode == 3) {  // the ReLU's gradient gate, recomputed with the forward's formula
+          g.x = ((v.x - a.x) * b.x * ga.x + be.x > 0.f) ? g.x : 0.f;
+          g.y = ((v.y - a.y) * b.y * ga.y + be.y > 0.f) ? g.y : 0.f;
+          g.z = ((v.z - a.z) * b.z * ga.z + be.z > 0.f) ? g.z : 0.f;
+          g.w = ((v.w - a.w) * b.w * ga.w + be.w > 0.f) ? g.w : 0.f;
+        }
         if (mode == 0) {
           s1[0] += v.x; s1[1] += v.y; s1[2] += v.z; s1[3] += v.w;
           s2[0] += v.x * v.x; s2[1] += v.y * v.y; s2[2] += v.z * v.z; s2[3] += v.w * v.w;
@@ -355,6 +368,66 @@ __global__ void bn_bwd_apply_kernel(const float* __restrict__ s, const float* __
     const float4 is = *reinterpret_cast<const float4*>(invstd + 4 * q);
     const float4 cb = *reinterpret_cast<const float4*>(coef_b + 4 * q);
     const float4 cc = *reinterpret_cast<const float4*>(coef_c + 4 * q);
+    float4 o;
+    o.x = fmaf(ga.x * is.x, g.x, fmaf(cb.x, v.x, cc.x));
+    o.y = fmaf(ga.y * is.y, g.y, fmaf(cb.y, v.y, cc.y));
+    o.z = fmaf(ga.z * is.z, g.z, fmaf(cb.z, v.z, cc.z));
+    o.w = fmaf(ga.w * is.w, g.w, fmaf(cb.w, v.w, cc.w));
+    if (accumulate) {
+      const float4 d = *reinterpret_cast<const float4*>(dx + 4 * i);
+      o.x += d.x; o.y += d.y; o.z += d.z; o.w += d.w;
+    }
+    *reinterpret_cast<float4*>(dx + 4 * i) = o;
+  }
+}
+
+// Fused BN+ReLU forward apply: z = max((x - mean) * invstd * gamma + beta, 0)
+// (same expression as bn_apply, so a recompute is bit-identical and the
+// backward's recomputed gate matches the forward's sign exactly).
+__global__ void bnrelu_apply_kernel(const float* __restrict__ x, float* z, const float* __restrict__ mean,
+                                    const float* __restrict__ invstd, const float* __restrict__ gamma,
+                                    const float* __restrict__ beta, long long rows, int C) {
+  const int cq = C / 4;
+  const long long n4 = rows * cq;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int q = (int)(i % cq);
+    float4 v = *reinterpret_cast<const float4*>(x + 4 * i);
+    const float4 m = *reinterpret_cast<const float4*>(mean + 4 * q);
+    const float4 s = *reinterpret_cast<const float4*>(invstd + 4 * q);
+    const float4 g = *reinterpret_cast<const float4*>(gamma + 4 * q);
+    const float4 b = *reinterpret_cast<const float4*>(beta + 4 * q);
+    v.x = fmaxf((v.x - m.x) * s.x * g.x + b.x, 0.f);
+    v.y = fmaxf((v.y - m.y) * s.y * g.y + b.y, 0.f);
+    v.z = fmaxf((v.z - m.z) * s.z * g.z + b.z, 0.f);
+    v.w = fmaxf((v.w - m.w) * s.w * g.w + b.w, 0.f);
+    *reinterpret_cast<float4*>(z + 4 * i) = v;
+  }
+}
+
+// Fused BN+ReLU backward apply from x: dy = dz * [bn(x) > 0]; dx = k*dy + cb*x + cc
+__global__ void bnrelu_bwd_apply_kernel(const float* __restrict__ x, const float* __restrict__ dz, float* dx,
+                                        const float* __restrict__ mean, const float* __restrict__ beta,
+                                        const float* __restrict__ gamma, const float* __restrict__ invstd,
+                                        const float* __restrict__ coef_b, const float* __restrict__ coef_c,
+                                        long long rows, int C, int accumulate) {
+  const int cq = C / 4;
+  const long long n4 = rows * cq;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int q = (int)(i % cq);
+    const float4 v = *reinterpret_cast<const float4*>(x + 4 * i);
+    float4 g = *reinterpret_cast<const float4*>(dz + 4 * i);
+    const float4 m = *reinterpret_cast<const float4*>(mean + 4 * q);
+    const float4 be = *reinterpret_cast<const float4*>(beta + 4 * q);
+    const float4 ga = *reinterpret_cast<const float4*>(gamma + 4 * q);
+    const float4 is = *reinterpret_cast<const float4*>(invstd + 4 * q);
+    const float4 cb = *reinterpret_cast<const float4*>(coef_b + 4 * q);
+    const float4 cc = *reinterpret_cast<const float4*>(coef_c + 4 * q);
+    g.x = ((v.x - m.x) * is.x * ga.x + be.x > 0.f) ? g.x : 0.f;
+    g.y = ((v.y - m.y) * is.y * ga.y + be.y > 0.f) ? g.y : 0.f;
+    g.z = ((v.z - m.z) * is.z * ga.z + be.z > 0.f) ? g.z : 0.f;
+    g.w = ((v.w - m.w) * is.w * ga.w + be.w > 0.f) ? g.w : 0.f;
     float4 o;
     o.x = fmaf(ga.x * is.x, g.x, fmaf(cb.x, v.x, cc.x));
     o.y = fmaf(ga.y * is.y, g.y, fmaf(cb.y, v.y, cc.y));

@@ -122,6 +122,19 @@ def _local_calls(bx: _Bench, net, op):
             x.data_ptr(), dy.data_ptr(), dx.data_ptr(), 0, g_, m_, s_, dg, db, rows, c, scratch.data_ptr(), sp))
         out[("bwd", "bwd-out")] = lambda: bx.check(lib.monet_bn_bwd_out(
             y.data_ptr(), dy.data_ptr(), dx.data_ptr(), 0, g_, b_, s_, dg, db, rows, c, scratch.data_ptr(), sp))
+    elif kind == "bnrelu":
+        c = op.shape[-1]
+        rows = n // c
+        ch = [bx.buf(4 * c) for _ in range(8)]
+        for t in ch[:4]:
+            t.abs_().add_(0.5)
+        scratch = bx.buf(lib.monet_bn_scratch_bytes(rows, c))
+        g_, b_, m_, s_, rm, rv, dg, db = (t.data_ptr() for t in ch)
+        out[("fwd", "bnrelu")] = lambda: bx.check(lib.monet_bnrelu_fwd_train(
+            x.data_ptr(), y.data_ptr(), g_, b_, m_, s_, rm, rv, rows, c, C.c_float(1e-5), C.c_float(0.1), 1,
+            scratch.data_ptr(), sp))
+        out[("bwd", "bwd-in")] = lambda: bx.check(lib.monet_bnrelu_bwd(
+            x.data_ptr(), dy.data_ptr(), dx.data_ptr(), 0, g_, b_, m_, s_, dg, db, rows, c, scratch.data_ptr(), sp))
     elif kind == "add":
         x2 = bx.buf(op.nbytes)
         out[("fwd", "add")] = lambda: bx.check(lib.monet_add_fwd(x.data_ptr(), x2.data_ptr(), y.data_ptr(), n, sp))

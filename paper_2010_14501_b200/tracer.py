@@ -67,6 +67,7 @@ class Network:
 
     def __init__(self, ops: list[Op], batch: int, num_classes: int):
         self.ops = ops
+        self.fused = any(op.kind == "bnrelu" for op in ops)
         self.batch = batch
         self.num_classes = num_classes
         self.n = len(ops)
@@ -109,13 +110,13 @@ class Network:
         return sum(t.numel() for _, _, t in self.param_items())
 
     def bn_channels(self) -> int:
-        return sum(op.shape[-1] for op in self.ops if op.kind == "bn")
+        return sum(op.shape[-1] for op in self.ops if op.kind in ("bn", "bnrelu"))
 
     def scratch_bytes(self) -> int:
         lib = _native.lib()
         s = 0
         for op in self.ops:
-            if op.kind == "bn":
+            if op.kind in ("bn", "bnrelu"):
                 rows = op.numel // op.shape[-1]
                 s = max(s, lib.bn_scratch_bytes(rows, op.shape[-1]))
         s = max(s, lib.xent_scratch_bytes(self.batch))
@@ -186,6 +187,9 @@ class Network:
         elif op.kind == "bn":
             fwd.append(("bn", 0))
             bwd += [("bwd-in", 0, x), ("bwd-out", 0, [op.id])]
+        elif op.kind == "bnrelu":  # fused BN+ReLU: backward from the BN input only (K10)
+            fwd.append(("bnrelu", 0))
+            bwd.append(("bwd-in", 0, x))
         elif op.kind == "maxpool":
             fwd.append(("maxpool", 0))
             bwd += [("bwd-in", 0, x), ("bwd-idx", 0, [self.intermediate_of[op.id]])]
@@ -253,6 +257,7 @@ BWD_IMPLS = {
     "conv": [("splitk", "input"), ("implicit", "input")],
     "fc": [("gemm-splitk", "input"), ("gemm", "input")],
     "bn": [("bwd-in", "input"), ("bwd-out", "output")],
+    "bnrelu": [("bwd-in", "input")],
     "relu": [("bwd-in", "input"), ("bwd-out", "output"), ("bwd-mask", "intermediate")],
     "maxpool": [("bwd-in", "input"), ("bwd-idx", "intermediate")],
     "add": [("bwd", "input")],
@@ -267,7 +272,37 @@ def _pair(v):
     return v if isinstance(v, int) else v[0]
 
 
-def trace_graph(model: torch.nn.Module, example_input: torch.Tensor, num_classes: int | None = None) -> Network:
+def fuse_bn_relu(ops: list[Op]) -> list[Op]:
+    """Merge every BatchNorm whose only reader is a ReLU into one "bnrelu" op
+    (SURVEY.md §2.2 K9/K10): the BN output is never materialized, the fused
+    op's output is relu(BN(x)) and its backward reads x.  Ids are renumbered
+    in order; dependencies are remapped."""
+    readers: dict[int, list[int]] = {}
+    for op in ops:
+        for j in op.deps:
+            readers.setdefault(j, []).append(op.id)
+    fused_into: dict[int, int] = {}  # relu id -> bn id
+    for op in ops:
+        if op.kind == "bn" and len(readers.get(op.id, [])) == 1:
+            r = ops[readers[op.id][0] - 1]
+            if r.kind == "relu" and r.deps == (op.id,):
+                fused_into[r.id] = op.id
+    new_id: dict[int, int] = {}
+    out: list[Op] = []
+    for op in ops:
+        if op.id in fused_into:
+            new_id[op.id] = new_id[fused_into[op.id]]
+            continue
+        nid = len(out) + 1
+        new_id[op.id] = nid
+        kind = "bnrelu" if op.kind == "bn" and op.id in fused_into.values() else op.kind
+        name = op.name + "+relu" if kind == "bnrelu" else op.name
+        out.append(Op(nid, kind, tuple(new_id[j] for j in op.deps), op.shape, dict(op.attrs), op.params, name))
+    return out
+
+
+def trace_graph(model: torch.nn.Module, example_input: torch.Tensor, num_classes: int | None = None,
+                fuse: bool = False) -> Network:
     """Trace a torchvision-style CNN into a Network (engine layout parameters).
 
     Supported modules: Conv2d (no bias, groups=1), BatchNorm2d, ReLU,
@@ -351,15 +386,16 @@ def trace_graph(model: torch.nn.Module, example_input: torch.Tensor, num_classes
     logits = ops[src - 1]
     k = num_classes or logits.shape[1]
     ops.append(Op(len(ops) + 1, "xent", (src,), (), name="loss"))
-    return Network(ops, n, k)
+    return Network(fuse_bn_relu(ops) if fuse else ops, n, k)
 
 
 def build_network(arch: str, batch: int, image: int | tuple = 224, num_classes: int = 1000,
-                  seed: int = 0) -> Network:
-    """torchvision ``arch`` with default init under ``torch.manual_seed(seed)``, traced."""
+                  seed: int = 0, fuse: bool = False) -> Network:
+    """torchvision ``arch`` with default init under ``torch.manual_seed(seed)``, traced
+    (``fuse``: BN+ReLU pairs become single fused ops)."""
     import torchvision
 
     torch.manual_seed(seed)
     model = getattr(torchvision.models, arch)(num_classes=num_classes)
     hw = (image, image) if isinstance(image, int) else image
-    return trace_graph(model, torch.empty(batch, 3, *hw, device="meta"), num_classes)
+    return trace_graph(model, torch.empty(batch, 3, *hw, device="meta"), num_classes, fuse)

@@ -17,21 +17,25 @@ from paper_2010_14501_b200.schedule import ledger
 from paper_2010_14501_b200.tracer import build_network
 
 ROOT = Path(__file__).resolve().parent.parent
-SCHEDULES = sorted((ROOT / "schedules").glob("resnet50_b184_224_*gib.json"))
+SCHEDULES = sorted((ROOT / "schedules").glob("resnet50*_b184_224_*gib.json"))
 
 
-@pytest.fixture(scope="module")
-def r50():
-    net = build_network("resnet50", 184, 224)
-    g = M.load_graph(net.graph_doc())
-    path = ROOT / "profiles" / "catalog_resnet50_b184_224.json"
-    cdoc = json.loads(path.read_text())["catalog"] if path.exists() else net.catalog_doc()
-    return net, g, M.load_catalog(cdoc, g)
+_NETS = {}
+
+
+def _r50(fused: bool):
+    if fused not in _NETS:
+        net = build_network("resnet50", 184, 224, fuse=fused)
+        g = M.load_graph(net.graph_doc())
+        path = ROOT / "profiles" / f"catalog_resnet50{'_fused' if fused else ''}_b184_224.json"
+        cdoc = json.loads(path.read_text())["catalog"] if path.exists() else net.catalog_doc()
+        _NETS[fused] = (net, g, M.load_catalog(cdoc, g))
+    return _NETS[fused]
 
 
 @pytest.mark.parametrize("path", SCHEDULES, ids=[p.stem for p in SCHEDULES])
-def test_physical_peak_within_ilp_bound(r50, path):
-    net, g, cat = r50
+def test_physical_peak_within_ilp_bound(path):
+    net, g, cat = _r50("_fused" in path.name)
     doc = json.loads(path.read_text())
     digest = hashlib.sha256(json.dumps(net.graph_doc(), sort_keys=True).encode()).hexdigest()[:16]
     assert doc["graph_digest"] == digest, "schedule was planned for another graph"

@@ -81,6 +81,36 @@ def test_engine_matches_reference_ledger_and_oracle(cuda, r18, which):
             assert rel(rt.bn[op.id][2], rm) <= REL and rel(rt.bn[op.id][3], rv) <= REL
 
 
+def test_fused_bn_relu_engine(cuda):
+    """ResNet-18 with fused BN+ReLU ops under a recompute schedule: ledger = simulate(),
+    loss / weights / gradients = CPU oracle (fed the GPU activations)."""
+    net = build_network("resnet18", 4, 32, num_classes=10, fuse=True)
+    assert any(op.kind == "bnrelu" for op in net.ops)
+    g = M.load_graph(net.graph_doc())
+    cat = M.load_catalog(net.catalog_doc(), g)
+    se = M.store_everything_schedule(g, cat)
+    act = M.simulate(se, g, cat).peak_memory - g.params_bytes
+    from paper_2010_14501_b200.planner import plan_schedule
+    sched, _ = plan_schedule(g, cat, g.params_bytes + int(0.5 * act), kinds=net.storable_kinds())
+    assert sched is not None and any(s.recompute for s in sched.stages)
+    gen = torch.Generator().manual_seed(0)
+    x = torch.randn(4, 3, 32, 32, generator=gen)
+    y = torch.randint(0, 10, (4,), generator=gen)
+    rt = Runtime(net)
+    rt.set_batch(x.to(cuda), y.to(cuda))
+    plan = rt.plan(sched, g, cat)
+    assert M.trace_report(plan.trace) == M.trace_report(M.simulate(sched, g, cat))
+    acts, mismatched = capture(rt, plan)
+    assert not mismatched
+    doc = M.schedule_to_doc(sched)
+    loss = run_step(CpuState(net), doc, x, y)
+    assert abs(rt.loss_value() - loss) <= REL * abs(loss)
+    st = CpuState(net)
+    run_step(st, doc, x, y, forced=acts)
+    for (nid, pname), v in params_nhwc(st).items():
+        assert rel(rt.pview[(nid, pname)].view(v.shape), v) <= REL, (net.op(nid).name, pname)
+
+
 def test_forward_ops_match_oracle(cuda, r18):
     """Each forward op, evaluated by the oracle on the GPU's own inputs, matches the GPU output."""
     net, g, cat, x, y, cases = r18

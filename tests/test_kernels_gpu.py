@@ -236,6 +236,50 @@ def test_batchnorm(cuda, shape):
         assert rel_err(db, br.grad) < REL_EW, fn
 
 
+@pytest.mark.parametrize("shape", [(4, 7, 7, 64), (2, 9, 5, 256)])
+def test_fused_bn_relu(cuda, shape):
+    n, h, w, c = shape
+    rows = n * h * w
+    g = torch.Generator().manual_seed(5)
+    x = torch.randn(n, h, w, c, generator=g) * 2 + 0.3
+    gamma = torch.rand(c, generator=g) + 0.5
+    beta = torch.randn(c, generator=g) * 0.5
+    dz = torch.randn(n, h, w, c, generator=g)
+    lib = N.lib()
+    xd, gd, bd, dzd = (t.to(cuda) for t in (x, gamma, beta, dz))
+    z = torch.empty_like(xd)
+    mean, invstd = torch.empty(c, device=cuda), torch.empty(c, device=cuda)
+    rm, rv = torch.zeros(c, device=cuda), torch.ones(c, device=cuda)
+    scratch = torch.empty(lib.bn_scratch_bytes(rows, c) // 4 + 1, device=cuda)
+    lib.bnrelu_fwd_train(xd.data_ptr(), z.data_ptr(), gd.data_ptr(), bd.data_ptr(), mean.data_ptr(),
+                         invstd.data_ptr(), rm.data_ptr(), rv.data_ptr(), rows, c, 1e-5, 0.1, 1, scratch.data_ptr(),
+                         stream())
+    xr = x.double().permute(0, 3, 1, 2).requires_grad_()
+    gr, br = gamma.double().requires_grad_(), beta.double().requires_grad_()
+    rmr, rvr = torch.zeros(c, dtype=torch.float64), torch.ones(c, dtype=torch.float64)
+    zr = F.relu(F.batch_norm(xr, rmr, rvr, gr, br, training=True, momentum=0.1, eps=1e-5))
+    assert rel_err(z, zr.permute(0, 2, 3, 1)) < REL_EW
+    assert rel_err(rm, rmr) < REL_EW and rel_err(rv, rvr) < REL_EW
+    # the separate BN + ReLU kernels give the identical output (fusion changes no bits)
+    y = torch.empty_like(xd)
+    lib.bn_fwd_replay(xd.data_ptr(), y.data_ptr(), gd.data_ptr(), bd.data_ptr(), mean.data_ptr(), invstd.data_ptr(),
+                      rows, c, stream())
+    z2 = torch.empty_like(xd)
+    lib.relu_fwd(y.data_ptr(), z2.data_ptr(), None, y.numel(), stream())
+    assert torch.equal(z, z2)
+    z3 = torch.empty_like(xd)
+    lib.bnrelu_fwd_replay(xd.data_ptr(), z3.data_ptr(), gd.data_ptr(), bd.data_ptr(), mean.data_ptr(),
+                          invstd.data_ptr(), rows, c, stream())
+    assert torch.equal(z, z3)
+    zr.backward(dz.double().permute(0, 3, 1, 2))
+    dx = torch.full_like(xd, 2.0)
+    dg, db = torch.empty(c, device=cuda), torch.empty(c, device=cuda)
+    lib.bnrelu_bwd(xd.data_ptr(), dzd.data_ptr(), dx.data_ptr(), 1, gd.data_ptr(), bd.data_ptr(), mean.data_ptr(),
+                   invstd.data_ptr(), dg.data_ptr(), db.data_ptr(), rows, c, scratch.data_ptr(), stream())
+    assert rel_err(dx - 2.0, xr.grad.permute(0, 2, 3, 1)) < 2e-5  # accumulate mode
+    assert rel_err(dg, gr.grad) < 2e-5 and rel_err(db, br.grad) < REL_EW
+
+
 def test_maxpool_and_avgpool(cuda):
     n, h, w, c = 3, 13, 12, 64
     g = torch.Generator().manual_seed(5)

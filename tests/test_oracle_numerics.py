@@ -23,10 +23,10 @@ def _rel(a, b):
     return (a.double() - b.double()).abs().max().item() / max(b.double().abs().max().item(), 1e-30)
 
 
-def _setup(batch=2, hw=32, arch="resnet18"):
+def _setup(batch=2, hw=32, arch="resnet18", fuse=False):
     torch.manual_seed(0)
     model = getattr(torchvision.models, arch)(num_classes=10)
-    net = trace_graph(model, torch.empty(batch, 3, hw, hw, device="meta"), 10)
+    net = trace_graph(model, torch.empty(batch, 3, hw, hw, device="meta"), 10, fuse=fuse)
     g = M.load_graph(net.graph_doc())
     cat = M.load_catalog(net.catalog_doc(), g)
     gen = torch.Generator().manual_seed(1)
@@ -64,9 +64,10 @@ def _schedules(g, cat):
     return out
 
 
-@pytest.mark.parametrize("arch", ["resnet18"])
-def test_oracle_replay_equals_autograd(arch):
-    model, net, g, cat, x, y = _setup(arch=arch)
+@pytest.mark.parametrize("arch,fuse", [("resnet18", False), ("resnet18", True)])
+def test_oracle_replay_equals_autograd(arch, fuse):
+    model, net, g, cat, x, y = _setup(arch=arch, fuse=fuse)
+    assert fuse == any(op.kind == "bnrelu" for op in net.ops)
     ref_loss = _autograd_step(model, x, y)
     ref = {n: p.detach() for n, p in model.named_parameters()}
     ref_bn = {n: b for n, b in model.named_buffers() if "running" in n}
@@ -79,15 +80,30 @@ def test_oracle_replay_equals_autograd(arch):
         got = params_nhwc(st)
         for op in net.ops:
             for pname in op.params:
-                want = ref[f"{op.name}.{pname}"]
+                want = ref[f"{op.name.removesuffix('+relu')}.{pname}"]
                 have = got[(op.id, pname)]
                 if op.kind == "conv":
                     have = have[..., : want.shape[1]].permute(0, 3, 1, 2)
                 assert _rel(have, want) < TOL, (name, op.name, pname)
-            if op.kind == "bn":
+            if op.kind in ("bn", "bnrelu"):
                 rm, rv = st.running[op.id]
-                assert _rel(rm, ref_bn[f"{op.name}.running_mean"]) < TOL
-                assert _rel(rv, ref_bn[f"{op.name}.running_var"]) < TOL
+                base = op.name.removesuffix("+relu")
+                assert _rel(rm, ref_bn[f"{base}.running_mean"]) < TOL
+                assert _rel(rv, ref_bn[f"{base}.running_var"]) < TOL
+
+
+def test_fusion_pass():
+    _, net, g, cat, _, _ = _setup(fuse=True)
+    _, plain, _, _, _, _ = _setup(fuse=False)
+    fused = [op for op in net.ops if op.kind == "bnrelu"]
+    assert len(fused) == sum(1 for op in plain.ops if op.kind == "bn"
+                             and sum(1 for o in plain.ops if op.id in o.deps) == 1
+                             and next(o for o in plain.ops if op.id in o.deps).kind == "relu")
+    assert net.n == plain.n - len(fused)
+    for op in fused:  # backward reads the BN input only
+        (v,) = cat.bwd(op.id)
+        assert v.name == "bwd-in" and set(v.deps) == set(op.deps)
+    assert g.params_bytes == plain.params_bytes()
 
 
 def test_bitmask_roundtrip():

@@ -28,8 +28,9 @@ def digest(doc):
 
 def main(jobs):
     OUT.mkdir(exist_ok=True)
-    for arch, batch, img, gib in jobs:
-        net = build_network(arch, batch, img)
+    for arch, batch, img, gib, fuse in jobs:
+        net = build_network(arch, batch, img, fuse=fuse)
+        arch = arch + ("_fused" if fuse else "")
         gdoc, cdoc = net.graph_doc(), net.catalog_doc()
         measured = ROOT / "profiles" / f"catalog_{arch}_b{batch}_{img}.json"
         if measured.exists():  # plan with the on-device profile when it matches this graph
@@ -55,4 +56,5 @@ def main(jobs):
 
 
 if __name__ == "__main__":
-    main([("resnet50", 184, 224, 10), ("resnet50", 184, 224, 8), ("resnet50", 184, 224, 6)])
+    fuse = "--fused" in sys.argv
+    main([("resnet50", 184, 224, gib, fuse) for gib in (10, 8, 6)])

@@ -23,8 +23,9 @@ def digest(doc):
     return hashlib.sha256(json.dumps(doc, sort_keys=True).encode()).hexdigest()[:16]
 
 
-def main(arch="resnet50", batch=184, image=224):
-    net = build_network(arch, batch, image)
+def main(arch="resnet50", batch=184, image=224, fuse=False):
+    net = build_network(arch, batch, image, fuse=fuse)
+    arch = arch + ("_fused" if fuse else "")
     t = time.time()
     costs = profile_network(net, log=print)
     doc = {"arch": arch, "batch": batch, "image": image, "graph_digest": digest(net.graph_doc()),
@@ -35,5 +36,6 @@ def main(arch="resnet50", batch=184, image=224):
 
 
 if __name__ == "__main__":
-    a = sys.argv[1:]
-    main(a[0], int(a[1]), int(a[2])) if a else main()
+    fuse = "--fused" in sys.argv
+    a = [x for x in sys.argv[1:] if x != "--fused"]
+    main(a[0], int(a[1]), int(a[2]), fuse) if a else main(fuse=fuse)
