@@ -1,41 +1,98 @@
 """Batch-sharded data parallelism.
 
 One process per GPU; every rank replays the SAME schedule on its own shard of
-the global batch (per-GPU batch statistics, not SyncBN), under the same
-per-GPU budget.  The only exchange is the gradient all-reduce: parameter
-gradients live in one contiguous fp32 buffer of the fixed region, so the
-all-reduce is issued over that buffer in a fixed number of buckets in
-stage order (NCCL over NVLink/NVSwitch on the compute stream), and the
-1/world averaging is folded into the SGD kernel's ``grad_scale``.
+the global batch (per-GPU batch statistics, not SyncBN) under the same
+per-GPU budget.  The only exchange is the gradient all-reduce:
 
-The buffers NCCL allocates internally live outside the budgeted arena and are
-reported separately by the bench.
+* parameter gradients live in one contiguous fp32 buffer of the fixed
+  region, laid out in node order, so a bucket is a contiguous slice;
+* a parameter gradient is final once its node's backward stage has run and
+  stages run in descending node order, so the bucket holding the highest
+  nodes is complete first.  `plan_buckets` cuts the buffer into ~`bucket_bytes`
+  slices along node boundaries and records, per bucket, the node whose
+  backward completes it;
+* the executor calls `bucket_ready(node)` right after enqueuing that node's
+  backward kernels: the slice's all-reduce is launched asynchronously (NCCL
+  over NVLink / NVSwitch on its own stream, ordered after the producing
+  kernels), so it overlaps the remaining backward stages;
+* `finish()` (enqueued before SGD) waits for the outstanding reductions; the
+  1/world average is folded into the SGD kernel's ``grad_scale``.
+
+NCCL's internal buffers live outside the budgeted arena and are reported
+separately by the bench.  The same code runs on gloo (CPU tensors) for the
+world-size-2 tests.
 """
 
 from __future__ import annotations
 
-import torch
 import torch.distributed as dist
 
-__all__ = ["DataParallel", "bucket_ranges"]
+__all__ = ["DataParallel", "plan_buckets", "bucket_ranges"]
 
 
 def bucket_ranges(n_elems: int, n_buckets: int):
+    """Equal contiguous slices (kept for callers that do not know the layout)."""
     step = (n_elems + n_buckets - 1) // n_buckets
     return [(s, min(n_elems, s + step)) for s in range(0, n_elems, step)]
 
 
+def plan_buckets(net, bucket_bytes: int = 25 << 20):
+    """[(start, end, ready_node)] over the flat gradient buffer, highest nodes first.
+
+    Slices follow node boundaries; ready_node is the smallest node id in the
+    slice (its backward is the last of the slice to run)."""
+    spans = []  # (node, start, end) of every node with parameters, in buffer order
+    pos = 0
+    for nid, _, t in net.param_items():
+        if spans and spans[-1][0] == nid:
+            spans[-1][2] = pos + t.numel()
+        else:
+            spans.append([nid, pos, pos + t.numel()])
+        pos += t.numel()
+    buckets = []
+    cur = None
+    for nid, a, b in reversed(spans):
+        if cur is None:
+            cur = [a, b, nid]
+        else:
+            cur[0], cur[2] = a, nid
+        if (cur[1] - cur[0]) * 4 >= bucket_bytes:
+            buckets.append(tuple(cur))
+            cur = None
+    if cur is not None:
+        buckets.append(tuple(cur))
+    return buckets
+
+
 class DataParallel:
-    def __init__(self, runtime, group=None, buckets: int = 4):
+    def __init__(self, runtime, group=None, bucket_bytes: int = 25 << 20):
         self.rt = runtime
         self.group = group
         self.world = dist.get_world_size(group)
         runtime.grad_scale = 1.0 / self.world
         runtime.comm = self
-        # gradients are laid out in node order; stage order is descending, so the
-        # last bucket (deepest layers) completes first
-        self.ranges = bucket_ranges(runtime.grads.numel(), buckets)[::-1]
+        self.buckets = plan_buckets(runtime.net, bucket_bytes)
+        self.by_node: dict[int, list[tuple[int, int]]] = {}
+        for a, b, node in self.buckets:
+            self.by_node.setdefault(node, []).append((a, b))
+        self.works = []
+
+    def ready_nodes(self):
+        return set(self.by_node)
+
+    def bucket_ready(self, node: int):
+        """Launch the all-reduce of every bucket that `node`'s backward completes."""
+        for a, b in self.by_node.get(node, ()):
+            self.works.append(dist.all_reduce(self.rt.grads[a:b], op=dist.ReduceOp.SUM, group=self.group,
+                                              async_op=True))
+
+    def finish(self):
+        """Order the optimizer after every outstanding reduction."""
+        for w in self.works:
+            w.wait()
+        self.works.clear()
 
     def allreduce_grads(self):
-        for a, b in self.ranges:
+        """Blocking all-reduce of the whole buffer (no overlap; kept for tools)."""
+        for a, b, _ in self.buckets:
             dist.all_reduce(self.rt.grads[a:b], op=dist.ReduceOp.SUM, group=self.group)

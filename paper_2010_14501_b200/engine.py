@@ -312,6 +312,16 @@ class Runtime:
             return out
 
         # backward
+        out = self._bind_backward(s, op, P, ptrs)
+        if self.comm is not None and op.id in self.comm.ready_nodes():
+            # this stage finalizes a gradient bucket: start its all-reduce now (async,
+            # ordered after the kernels above) so it overlaps the remaining stages
+            out.append(("py", lambda node=op.id: self.comm.bucket_ready(node)))
+        return out
+
+    def _bind_backward(self, s, op, P, ptrs):
+        net, lib = self.net, self.lib.dll
+        out = []
         dy = P(("g", op.id))
         ws = ptrs.get(("ws",))
         acc = lambda j: 0 if j in s.new_grads else 1
@@ -398,7 +408,7 @@ class Runtime:
     def _bind_optimizer(self):
         calls = []
         if self.comm is not None:
-            calls.append(("py", self.comm.allreduce_grads))
+            calls.append(("py", self.comm.finish))  # SGD waits for the bucket reductions
         calls.append(("k", self.lib.dll.monet_sgd_step,
                       (self.params.data_ptr(), self.grads.data_ptr(), self.mom.data_ptr(), self.params.numel(),
                        C.c_float(self.lr), C.c_float(self.momentum), C.c_float(self.weight_decay),
