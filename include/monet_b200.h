@@ -113,6 +113,14 @@ int monet_bnrelu_bwd(const float* x, const float* dz, float* dx, int accumulate,
 /* --- residual add / gradient pass-through (K12) --------------------------- */
 int monet_add_fwd(const float* a, const float* b, float* y, int64_t n, void* stream);
 int monet_grad_pass(const float* dy, float* dx, int64_t n, float scale, int accumulate, void* stream);
+/* fused residual join + ReLU: z = max(a + b, 0); backward gates dz by z > 0
+ * (output-activated) or by a + b > 0 (input-activated) and writes / adds both
+ * input gradients in one pass */
+int monet_addrelu_fwd(const float* a, const float* b, float* z, int64_t n, void* stream);
+int monet_addrelu_bwd_out(const float* z, const float* dz, float* da, int acc_a, float* db, int acc_b, int64_t n,
+                          void* stream);
+int monet_addrelu_bwd_in(const float* a, const float* b, const float* dz, float* da, int acc_a, float* db, int acc_b,
+                         int64_t n, void* stream);
 
 /* --- pooling (K11, K13) ----------------------------------------------------- */
 int monet_maxpool_fwd(const monet_conv_desc* d, const float* x, float* y, uint8_t* idx8, void* stream);

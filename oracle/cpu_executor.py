@@ -130,6 +130,9 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
                 extra = pack_sign_mask(x.permute(0, 2, 3, 1).numpy())
         elif op.kind == "add":
             y = xs[0] + xs[1]
+        elif op.kind == "addrelu":
+            y = xs[0] + xs[1]
+            y = torch.where(y > 0, y, torch.zeros_like(y))
         elif op.kind == "maxpool":
             a = op.attrs
             y, flat = F.max_pool2d(xs[0], a["r"], a["stride"], a["pad"], return_indices=True)
@@ -198,6 +201,11 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
         elif op.kind == "add":
             for j in op.deps:
                 put_grad(j, dy.clone(), created)
+        elif op.kind == "addrelu":
+            gate = x_of(op.id) > 0 if impl == "bwd-out" else (x_of(op.deps[0]) + x_of(op.deps[1])) > 0
+            g = torch.where(gate, dy, torch.zeros_like(dy))
+            for j in op.deps:
+                put_grad(j, g.clone(), created)
         elif op.kind == "maxpool":
             a = op.attrs
             j = op.deps[0]

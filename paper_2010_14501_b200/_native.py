@@ -52,6 +52,9 @@ SIGNATURES = {
     "monet_bnrelu_bwd": (_i32, [_vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp]),
     "monet_add_fwd": (_i32, [_vp, _vp, _vp, _i64, _vp]),
     "monet_grad_pass": (_i32, [_vp, _vp, _i64, _f32, _i32, _vp]),
+    "monet_addrelu_fwd": (_i32, [_vp, _vp, _vp, _i64, _vp]),
+    "monet_addrelu_bwd_out": (_i32, [_vp, _vp, _vp, _i32, _vp, _i32, _i64, _vp]),
+    "monet_addrelu_bwd_in": (_i32, [_vp, _vp, _vp, _vp, _i32, _vp, _i32, _i64, _vp]),
     "monet_maxpool_fwd": (_i32, [_PCONV, _vp, _vp, _vp, _vp]),
     "monet_maxpool_bwd": (_i32, [_PCONV, _vp, _vp, _vp, _vp, _i32, _vp]),
     "monet_avgpool_fwd": (_i32, [_vp, _vp, _i32, _i32, _i32, _vp]),

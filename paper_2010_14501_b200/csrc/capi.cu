@@ -624,6 +624,20 @@ int monet_add_fwd(const float* a, const float* b, float* y, int64_t n, void* str
   add_kernel<<<ew_blocks(n / 4 + 1), kEwThreads, 0, S(stream)>>>(a, b, y, n);
   return last_error();
 }
+int monet_addrelu_fwd(const float* a, const float* b, float* z, int64_t n, void* stream) {
+  addrelu_kernel<<<ew_blocks(n / 4 + 1), kEwThreads, 0, S(stream)>>>(a, b, z, n);
+  return last_error();
+}
+int monet_addrelu_bwd_out(const float* z, const float* dz, float* da, int acc_a, float* db, int acc_b, int64_t n,
+                          void* stream) {
+  addrelu_bwd_kernel<<<ew_blocks(n / 4 + 1), kEwThreads, 0, S(stream)>>>(z, nullptr, dz, da, acc_a, db, acc_b, n);
+  return last_error();
+}
+int monet_addrelu_bwd_in(const float* a, const float* b, const float* dz, float* da, int acc_a, float* db, int acc_b,
+                         int64_t n, void* stream) {
+  addrelu_bwd_kernel<<<ew_blocks(n / 4 + 1), kEwThreads, 0, S(stream)>>>(a, b, dz, da, acc_a, db, acc_b, n);
+  return last_error();
+}
 int monet_grad_pass(const float* dy, float* dx, int64_t n, float scale, int accumulate, void* stream) {
   scale_acc_kernel<<<ew_blocks(n / 4 + 1), kEwThreads, 0, S(stream)>>>(dy, dx, n, scale, accumulate);
   return last_error();

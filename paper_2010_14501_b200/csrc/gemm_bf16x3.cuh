@@ -394,7 +394,10 @@ template <int AM, int BMODE>
 __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_constant__ GemmParams p) {
   constexpr bool a_mn = mode_is_mn(AM), b_mn = mode_is_mn(BMODE);
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B align by offsetting the __shared__ array itself (not via an integer
+  // round trip) so the compiler keeps the shared address space: LDS / STS
+  // instead of generic LD / ST in the splitters
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* raw = smem;                                  // kRawSlots x (A, B) fp32
   uint8_t* bst = smem + kRawSlots * kRawBytes;          // kStages x (B hi, B lo) bf16
   uint64_t* bars = reinterpret_cast<uint64_t*>(bst + kStages * kStageBytes);
@@ -411,6 +414,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
   const int lane = lane_id();
   const int n_tiles_total = p.m_tiles * p.n_tiles * p.splits;
   long long twait[16] = {0};
+  float* const dbg_a = p.dbg_a;  // hoisted: loop-invariant kernel parameters
+  float* const dbg_b = p.dbg_b;
   const long long t_start = clock64();
 
   if (threadIdx.x == 0) {
@@ -515,12 +520,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
               v[4 * c + 3] = q.w;
             }
           }
-          if (p.dbg_a != nullptr) {
+          if (dbg_a != nullptr) {
             const long long kpad = (long long)((p.Kd + 63) / 64) * 64;
             const int kb = (item_kb0 + 2 * s + half);
             const int m = mt * BM + row;
             if (m < p.M)
-              for (int k = 0; k < 32; ++k) p.dbg_a[m * kpad + kb * 32 + k] = v[k];
+              for (int k = 0; k < 32; ++k) dbg_a[m * kpad + kb * 32 + k] = v[k];
           }
           uint32_t hi[16], lo[16];
 #pragma unroll
@@ -569,7 +574,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
             }
             q[i] = *reinterpret_cast<const float4*>(rt + off);
           }
-          if (p.dbg_b != nullptr) {
+          if (dbg_b != nullptr) {
             const long long kpad = (long long)((p.Kd + 63) / 64) * 64;
             const int kb = kb0 + 2 * s + half;
             for (int i = 0; i < 4; ++i) {
@@ -584,7 +589,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
                   k = 4 * (t & 7) + j;
                 }
                 n += nt * BN;
-                if (n < p.N) p.dbg_b[n * kpad + kb * 32 + k] = e[j];
+                if (n < p.N) dbg_b[n * kpad + kb * 32 + k] = e[j];
               }
             }
           }

@@ -346,7 +346,7 @@ template <int AM, int BMODE>
 __global__ void __launch_bounds__(kThreads, 1) gemm_tf32_kernel(const GemmParams p) {
   constexpr bool a_mn = mode_is_mn(AM), b_mn = mode_is_mn(BMODE);
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* raw = smem;                                  // kRawStages x (A, B) fp32
   uint8_t* ready = smem + kRawStages * kRawBytes;       // kStages x (A_hi, A_lo, B_hi, B_lo)
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(ready + kStages * kStageBytes);

@@ -137,6 +137,62 @@ __global__ void add_kernel(const float* __restrict__ a, const float* __restrict_
   }
 }
 
+// Fused residual join + ReLU: z = max(a + b, 0)
+__global__ void addrelu_kernel(const float* __restrict__ a, const float* __restrict__ b, float* z, long long n) {
+  const long long n4 = n / 4;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float4 u = *reinterpret_cast<const float4*>(a + 4 * i);
+    const float4 v = *reinterpret_cast<const float4*>(b + 4 * i);
+    *reinterpret_cast<float4*>(z + 4 * i) = make_float4(fmaxf(u.x + v.x, 0.f), fmaxf(u.y + v.y, 0.f),
+                                                        fmaxf(u.z + v.z, 0.f), fmaxf(u.w + v.w, 0.f));
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+    const long long e = n4 * 4 + threadIdx.x;
+    z[e] = fmaxf(a[e] + b[e], 0.f);
+  }
+}
+
+// Its backward: g = dz * [gate > 0] with the gate from the output z (s1 = z,
+// s2 = nullptr) or recomputed from the inputs (s1 + s2 = a + b); both input
+// gradients in one pass, each stored or accumulated.
+__global__ void addrelu_bwd_kernel(const float* __restrict__ s1, const float* __restrict__ s2,
+                                   const float* __restrict__ dz, float* da, int acc_a, float* db, int acc_b,
+                                   long long n) {
+  const long long n4 = n / 4;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    float4 t = *reinterpret_cast<const float4*>(s1 + 4 * i);
+    if (s2) {
+      const float4 u = *reinterpret_cast<const float4*>(s2 + 4 * i);
+      t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
+    }
+    float4 g = *reinterpret_cast<const float4*>(dz + 4 * i);
+    g.x = t.x > 0.f ? g.x : 0.f;
+    g.y = t.y > 0.f ? g.y : 0.f;
+    g.z = t.z > 0.f ? g.z : 0.f;
+    g.w = t.w > 0.f ? g.w : 0.f;
+    float4 oa = g, ob = g;
+    if (acc_a) {
+      const float4 c = *reinterpret_cast<const float4*>(da + 4 * i);
+      oa.x += c.x; oa.y += c.y; oa.z += c.z; oa.w += c.w;
+    }
+    if (acc_b) {
+      const float4 c = *reinterpret_cast<const float4*>(db + 4 * i);
+      ob.x += c.x; ob.y += c.y; ob.z += c.z; ob.w += c.w;
+    }
+    *reinterpret_cast<float4*>(da + 4 * i) = oa;
+    *reinterpret_cast<float4*>(db + 4 * i) = ob;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+    const long long e = n4 * 4 + threadIdx.x;
+    const float t = s2 ? s1[e] + s2[e] : s1[e];
+    const float g = t > 0.f ? dz[e] : 0.f;
+    da[e] = acc_a ? da[e] + g : g;
+    db[e] = acc_b ? db[e] + g : g;
+  }
+}
+
 // dx (=|+=) scale * dy
 __global__ void scale_acc_kernel(const float* __restrict__ dy, float* dx, long long n, float scale, int accumulate) {
   const long long n4 = n / 4;

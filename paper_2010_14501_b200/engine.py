@@ -288,6 +288,8 @@ class Runtime:
                 out.append(("k", lib.monet_relu_fwd, (xs[0], y, mask, op.numel, None)))
             elif op.kind == "add":
                 out.append(("k", lib.monet_add_fwd, (xs[0], xs[1], y, op.numel, None)))
+            elif op.kind == "addrelu":
+                out.append(("k", lib.monet_addrelu_fwd, (xs[0], xs[1], y, op.numel, None)))
             elif op.kind == "maxpool":
                 d = net.pool_desc(op)
                 mid = net.intermediate_of[op.id]
@@ -376,6 +378,14 @@ class Runtime:
         elif op.kind == "add":
             for j in op.deps:
                 out.append(("k", lib.monet_grad_pass, (dy, P(("g", j)), op.numel, C.c_float(1.0), acc(j), None)))
+        elif op.kind == "addrelu":
+            j0, j1 = op.deps
+            if s.impl == "bwd-out":
+                out.append(("k", lib.monet_addrelu_bwd_out, (P(("in", op.id)), dy, P(("g", j0)), acc(j0),
+                                                             P(("g", j1)), acc(j1), op.numel, None)))
+            else:
+                out.append(("k", lib.monet_addrelu_bwd_in, (P(("in", j0)), P(("in", j1)), dy, P(("g", j0)), acc(j0),
+                                                            P(("g", j1)), acc(j1), op.numel, None)))
         elif op.kind == "maxpool":
             d = net.pool_desc(op)
             j = op.deps[0]

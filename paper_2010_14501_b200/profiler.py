@@ -143,6 +143,14 @@ def _local_calls(bx: _Bench, net, op):
             for _ in range(2):
                 bx.check(lib.monet_grad_pass(dy.data_ptr(), dx.data_ptr(), n, C.c_float(1.0), 0, sp))
         out[("bwd", "bwd")] = add_bwd
+    elif kind == "addrelu":
+        x2, dx2 = bx.buf(op.nbytes), bx.buf(op.nbytes)
+        out[("fwd", "addrelu")] = lambda: bx.check(lib.monet_addrelu_fwd(x.data_ptr(), x2.data_ptr(), y.data_ptr(),
+                                                                          n, sp))
+        out[("bwd", "bwd-out")] = lambda: bx.check(lib.monet_addrelu_bwd_out(
+            y.data_ptr(), dy.data_ptr(), dx.data_ptr(), 0, dx2.data_ptr(), 0, n, sp))
+        out[("bwd", "bwd-in")] = lambda: bx.check(lib.monet_addrelu_bwd_in(
+            x.data_ptr(), x2.data_ptr(), dy.data_ptr(), dx.data_ptr(), 0, dx2.data_ptr(), 0, n, sp))
     elif kind == "maxpool":
         d = net.pool_desc(op)
         idx = bx.buf(op.numel)

@@ -95,6 +95,10 @@ class Network:
             kind = op.kind
             if kind == "relu" and self.op(op.deps[0]).kind == "add":
                 kind = "relu-join"
+            elif kind == "bnrelu":   # a fused op's output is a ReLU output
+                kind = "relu"
+            elif kind == "addrelu":  # ... at a residual join
+                kind = "relu-join"
             out[op.id] = kind
             if op.id in self.intermediate_of:
                 out[self.intermediate_of[op.id]] = "mask" if op.kind == "relu" else "idx"
@@ -190,6 +194,9 @@ class Network:
         elif op.kind == "bnrelu":  # fused BN+ReLU: backward from the BN input only (K10)
             fwd.append(("bnrelu", 0))
             bwd.append(("bwd-in", 0, x))
+        elif op.kind == "addrelu":  # fused residual join + ReLU: gate from the output or the inputs
+            fwd.append(("addrelu", 0))
+            bwd += [("bwd-out", 0, [op.id]), ("bwd-in", 0, x)]
         elif op.kind == "maxpool":
             fwd.append(("maxpool", 0))
             bwd += [("bwd-in", 0, x), ("bwd-idx", 0, [self.intermediate_of[op.id]])]
@@ -258,6 +265,7 @@ BWD_IMPLS = {
     "fc": [("gemm-splitk", "input"), ("gemm", "input")],
     "bn": [("bwd-in", "input"), ("bwd-out", "output")],
     "bnrelu": [("bwd-in", "input")],
+    "addrelu": [("bwd-out", "output"), ("bwd-in", "input")],
     "relu": [("bwd-in", "input"), ("bwd-out", "output"), ("bwd-mask", "intermediate")],
     "maxpool": [("bwd-in", "input"), ("bwd-idx", "intermediate")],
     "add": [("bwd", "input")],
@@ -273,17 +281,18 @@ def _pair(v):
 
 
 def fuse_bn_relu(ops: list[Op]) -> list[Op]:
-    """Merge every BatchNorm whose only reader is a ReLU into one "bnrelu" op
-    (SURVEY.md §2.2 K9/K10): the BN output is never materialized, the fused
-    op's output is relu(BN(x)) and its backward reads x.  Ids are renumbered
-    in order; dependencies are remapped."""
+    """Merge every BatchNorm (residual add) whose only reader is a ReLU into one
+    "bnrelu" ("addrelu") op: the pre-activation tensor
+    is never materialized, the fused op's output is the ReLU's.  bnrelu's
+    backward reads x; addrelu's gates from its output (or its inputs).  Ids
+    are renumbered in order; dependencies are remapped."""
     readers: dict[int, list[int]] = {}
     for op in ops:
         for j in op.deps:
             readers.setdefault(j, []).append(op.id)
     fused_into: dict[int, int] = {}  # relu id -> bn id
     for op in ops:
-        if op.kind == "bn" and len(readers.get(op.id, [])) == 1:
+        if op.kind in ("bn", "add") and len(readers.get(op.id, [])) == 1 and len(set(op.deps)) == len(op.deps):
             r = ops[readers[op.id][0] - 1]
             if r.kind == "relu" and r.deps == (op.id,):
                 fused_into[r.id] = op.id
@@ -295,8 +304,9 @@ def fuse_bn_relu(ops: list[Op]) -> list[Op]:
             continue
         nid = len(out) + 1
         new_id[op.id] = nid
-        kind = "bnrelu" if op.kind == "bn" and op.id in fused_into.values() else op.kind
-        name = op.name + "+relu" if kind == "bnrelu" else op.name
+        fused = op.id in fused_into.values()
+        kind = {"bn": "bnrelu", "add": "addrelu"}[op.kind] if fused else op.kind
+        name = op.name + "+relu" if fused else op.name
         out.append(Op(nid, kind, tuple(new_id[j] for j in op.deps), op.shape, dict(op.attrs), op.params, name))
     return out
 

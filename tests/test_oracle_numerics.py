@@ -95,14 +95,21 @@ def test_oracle_replay_equals_autograd(arch, fuse):
 def test_fusion_pass():
     _, net, g, cat, _, _ = _setup(fuse=True)
     _, plain, _, _, _, _ = _setup(fuse=False)
-    fused = [op for op in net.ops if op.kind == "bnrelu"]
-    assert len(fused) == sum(1 for op in plain.ops if op.kind == "bn"
-                             and sum(1 for o in plain.ops if op.id in o.deps) == 1
-                             and next(o for o in plain.ops if op.id in o.deps).kind == "relu")
-    assert net.n == plain.n - len(fused)
-    for op in fused:  # backward reads the BN input only
-        (v,) = cat.bwd(op.id)
-        assert v.name == "bwd-in" and set(v.deps) == set(op.deps)
+
+    def fusable(op):  # a BN / add whose only reader is a ReLU of it
+        readers = [o for o in plain.ops if op.id in o.deps]
+        return op.kind in ("bn", "add") and len(readers) == 1 and readers[0].kind == "relu"
+    n_bn = sum(1 for op in plain.ops if op.kind == "bn" and fusable(op))
+    n_add = sum(1 for op in plain.ops if op.kind == "add" and fusable(op))
+    assert sum(op.kind == "bnrelu" for op in net.ops) == n_bn > 0
+    assert sum(op.kind == "addrelu" for op in net.ops) == n_add > 0
+    assert net.n == plain.n - n_bn - n_add
+    for op in net.ops:
+        if op.kind == "bnrelu":  # backward reads the BN input only
+            (v,) = cat.bwd(op.id)
+            assert v.name == "bwd-in" and set(v.deps) == set(op.deps)
+        elif op.kind == "addrelu":  # gate from the output or from both inputs
+            assert {v.name: set(v.deps) for v in cat.bwd(op.id)} == {"bwd-out": {op.id}, "bwd-in": set(op.deps)}
     assert g.params_bytes == plain.params_bytes()
 
 

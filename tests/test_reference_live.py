@@ -53,3 +53,33 @@ def test_planner_matches_reference(kind, seed):
                         M.simulate(mh, mg, mc)
                     continue
                 assert rt == M.trace_report(M.simulate(mh, mg, mc))
+
+
+def test_public_names_match():
+    """Every public name of remsched exists in the drop-in, with the same call signature."""
+    import inspect
+    names = [n for n in dir(R) if not n.startswith("_")]
+    assert not [n for n in names if not hasattr(M, n)]
+    for n in names:
+        r, m = getattr(R, n), getattr(M, n)
+        if inspect.isfunction(r):
+            rp = [p.name for p in inspect.signature(r).parameters.values()]
+            mp = [p.name for p in inspect.signature(m).parameters.values()]
+            assert rp == mp, n
+
+
+@pytest.mark.parametrize("kind,seed", [("residual", 3), ("unet-toy", 4)])
+def test_solver_live_random(kind, seed):
+    """Native branch-and-bound == reference solver on fresh random instances."""
+    rg, rc = R.generate_synthetic(kind, 6, seed, fwd_variants=2, bwd_variants=2, intermediate_every=2,
+                                  inplace_marks=True)
+    gd, cd = R.graph_to_doc(rg), R.catalog_to_doc(rc)
+    mg = M.load_graph(gd)
+    mc = M.load_catalog(cd, mg)
+    for budget in (8, 16, 40):
+        rm = R.build_model(rg, R.compute_dependency_sets(rg), rc, budget)
+        mm = M.build_model(mg, M.compute_dependency_sets(mg), mc, budget)
+        assert R.export_lp_string(rm) == M.export_lp_string(mm)
+        rr, mr = R.solve(rm, {"node_limit": 2000}), M.solve(mm, {"node_limit": 2000})
+        assert (rr.status, rr.objective, rr.nodes, rr.assignment) == (mr.status, mr.objective, mr.nodes,
+                                                                        mr.assignment)
