@@ -41,8 +41,11 @@ typedef struct {
  *   MONET_CONV_SPLITK    "splitk"    as implicit, plus split-K over the reduction with
  *                                    fp32 partials in workspace (honest ws/speed trade)
  *   MONET_CONV_TF32      "tf32"      single-pass TF32 (faster, ~1e-3 relative error; tests only)
- *   MONET_CONV_TF32X3    "tf32x3"    3xTF32 all-shared-memory kernel (round-1 baseline) */
-enum { MONET_CONV_IMPLICIT = 0, MONET_CONV_SPLITK = 1, MONET_CONV_TF32 = 2, MONET_CONV_TF32X3 = 3 };
+ *   MONET_CONV_TF32X3    "tf32x3"    3xTF32 all-shared-memory kernel (round-1 baseline)
+ *   MONET_CONV_PAIR      "pair"      as implicit, on CTA pairs (cta_group::2, 256 x 128 tiles, each
+ *                                    CTA holds half of B) -- the 1-CTA vs 2-CTA tile point */
+enum { MONET_CONV_IMPLICIT = 0, MONET_CONV_SPLITK = 1, MONET_CONV_TF32 = 2, MONET_CONV_TF32X3 = 3,
+       MONET_CONV_PAIR = 4 };
 enum { MONET_PASS_FWD = 0, MONET_PASS_DGRAD = 1, MONET_PASS_WGRAD = 2, MONET_PASS_BWD = 3 };
 
 /* --- library --------------------------------------------------------------- */

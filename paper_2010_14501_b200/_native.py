@@ -80,7 +80,7 @@ SIGNATURES = {
     "monet_bnb_event": (_i32, [_vp, _i32, _vp, _vp, _vp]),
 }
 
-CONV_VARIANTS = {"implicit": 0, "splitk": 1, "tf32": 2, "tf32x3": 3}
+CONV_VARIANTS = {"implicit": 0, "splitk": 1, "tf32": 2, "tf32x3": 3, "pair": 4}
 PASS = {"fwd": 0, "dgrad": 1, "wgrad": 2, "bwd": 3}
 
 

@@ -46,16 +46,33 @@ size_t gemm_ws(int variant, int M, int N, int Kd) {
 // One instantiation per (A mode, B mode) pair used by conv / linear / gemm.
 // kBx3 selects the bf16x3 A-in-TMEM kernel (gemm_bf16x3.cuh, the product
 // path); otherwise the 3xTF32 / TF32 all-smem kernel (gemm_tc.cuh).
-template <bool kBx3, int AM, int BMODE>
+template <bool kBx3, bool kPair, int AM, int BMODE>
 int launch_inst(const GemmParams& p, int grid, cudaStream_t st) {
   static bool attr = false;
   if constexpr (kBx3) {
+    auto kern = bx3::gemm_bf16x3_kernel<AM, BMODE, kPair>;
     if (!attr) {
-      cudaFuncSetAttribute(bx3::gemm_bf16x3_kernel<AM, BMODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           bx3::kSmemBytes);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bx3::kSmemBytes);
       attr = true;
     }
-    bx3::gemm_bf16x3_kernel<AM, BMODE><<<grid, bx3::kThreads, bx3::kSmemBytes, st>>>(p);
+    if constexpr (kPair) {  // CTA pairs: clusters of 2 (the two SMs of a TPC)
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(bx3::kThreads);
+      cfg.dynamicSmemBytes = bx3::kSmemBytes;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
+      return e == cudaSuccess ? 0 : -(int)e;
+    } else {
+      kern<<<grid, bx3::kThreads, bx3::kSmemBytes, st>>>(p);
+    }
   } else {
     if (!attr) {
       cudaFuncSetAttribute(gemm_tf32_kernel<AM, BMODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
@@ -66,20 +83,22 @@ int launch_inst(const GemmParams& p, int grid, cudaStream_t st) {
   return 0;
 }
 
-template <bool kBx3>
+template <bool kBx3, bool kPair>
 int dispatch_modes(const GemmParams& p, int grid, cudaStream_t st) {
   const int a = p.a.mode, b = p.b.mode;
-  if (a == OP_IM2COL_FPROP && b == OP_KMAJOR) return launch_inst<kBx3, OP_IM2COL_FPROP, OP_KMAJOR>(p, grid, st);
-  if (a == OP_KMAJOR && b == OP_KMAJOR) return launch_inst<kBx3, OP_KMAJOR, OP_KMAJOR>(p, grid, st);
-  if (a == OP_IM2COL_DGRAD && b == OP_MNMAJOR) return launch_inst<kBx3, OP_IM2COL_DGRAD, OP_MNMAJOR>(p, grid, st);
-  if (a == OP_KMAJOR && b == OP_MNMAJOR) return launch_inst<kBx3, OP_KMAJOR, OP_MNMAJOR>(p, grid, st);
-  if (a == OP_MNMAJOR && b == OP_IM2COL_WGRAD) return launch_inst<kBx3, OP_MNMAJOR, OP_IM2COL_WGRAD>(p, grid, st);
-  if (a == OP_MNMAJOR && b == OP_MNMAJOR) return launch_inst<kBx3, OP_MNMAJOR, OP_MNMAJOR>(p, grid, st);
-  if (a == OP_MNMAJOR && b == OP_KMAJOR) return launch_inst<kBx3, OP_MNMAJOR, OP_KMAJOR>(p, grid, st);
+  if (a == OP_IM2COL_FPROP && b == OP_KMAJOR) return launch_inst<kBx3, kPair, OP_IM2COL_FPROP, OP_KMAJOR>(p, grid, st);
+  if (a == OP_KMAJOR && b == OP_KMAJOR) return launch_inst<kBx3, kPair, OP_KMAJOR, OP_KMAJOR>(p, grid, st);
+  if (a == OP_IM2COL_DGRAD && b == OP_MNMAJOR) return launch_inst<kBx3, kPair, OP_IM2COL_DGRAD, OP_MNMAJOR>(p, grid, st);
+  if (a == OP_KMAJOR && b == OP_MNMAJOR) return launch_inst<kBx3, kPair, OP_KMAJOR, OP_MNMAJOR>(p, grid, st);
+  if (a == OP_MNMAJOR && b == OP_IM2COL_WGRAD) return launch_inst<kBx3, kPair, OP_MNMAJOR, OP_IM2COL_WGRAD>(p, grid, st);
+  if (a == OP_MNMAJOR && b == OP_MNMAJOR) return launch_inst<kBx3, kPair, OP_MNMAJOR, OP_MNMAJOR>(p, grid, st);
+  if (a == OP_MNMAJOR && b == OP_KMAJOR) return launch_inst<kBx3, kPair, OP_MNMAJOR, OP_KMAJOR>(p, grid, st);
   return -(int)cudaErrorInvalidValue;
 }
 
-bool uses_bx3(int variant) { return variant == MONET_CONV_IMPLICIT || variant == MONET_CONV_SPLITK; }
+bool uses_bx3(int variant) {
+  return variant == MONET_CONV_IMPLICIT || variant == MONET_CONV_SPLITK || variant == MONET_CONV_PAIR;
+}
 
 // ----------------------------------------------------------------- TMA maps
 // The driver's tensor-map encoders, resolved through the runtime (no -lcuda).
@@ -136,7 +155,7 @@ int make_tma(GemmParams& p, const Operand& op, CUtensorMap* m) {
       if (op.ld % 4) return 0;
       cuuint64_t dims[2] = {(cuuint64_t)p.Kd, (cuuint64_t)op.rows};
       cuuint64_t strides[1] = {(cuuint64_t)op.ld * 4};
-      cuuint32_t box[2] = {32, 128};
+      cuuint32_t box[2] = {32, (cuuint32_t)op.rows_box};
       return tiled_map(m, op.ptr, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
     }
     case OP_MNMAJOR: {
@@ -144,7 +163,7 @@ int make_tma(GemmParams& p, const Operand& op, CUtensorMap* m) {
       if (op.kdiv >= p.Kd && !p.ph.on) {
         cuuint64_t dims[2] = {(cuuint64_t)op.rows, (cuuint64_t)p.Kd};
         cuuint64_t strides[1] = {(cuuint64_t)op.ld * 4};
-        cuuint32_t box[2] = {128, 32};
+        cuuint32_t box[2] = {(cuuint32_t)op.rows_box, 32};
         return tiled_map(m, op.ptr, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
       }
       if (op.kdiv % 32 || op.ks1 % 4 || p.Kd % op.kdiv) return 0;
@@ -152,7 +171,7 @@ int make_tma(GemmParams& p, const Operand& op, CUtensorMap* m) {
       const int ntaps = p.ph.on ? g.R * g.S : p.Kd / op.kdiv;
       cuuint64_t dims[3] = {(cuuint64_t)op.rows, (cuuint64_t)ntaps, (cuuint64_t)op.kdiv};
       cuuint64_t strides[2] = {(cuuint64_t)op.ks1 * 4, (cuuint64_t)op.ld * 4};
-      cuuint32_t box[3] = {128, 1, 32};
+      cuuint32_t box[3] = {(cuuint32_t)op.rows_box, 1, 32};
       return tiled_map(m, op.ptr, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
     }
     case OP_IM2COL_FPROP:
@@ -175,8 +194,9 @@ int make_tma(GemmParams& p, const Operand& op, CUtensorMap* m) {
     case OP_IM2COL_WGRAD: {
       // segments of C (< 128) or 128 channels; below 32 channels (the stem) the
       // 32-TMA-per-k-block segment loop loses to the 16B cp.async fallback
-      if (g.C < 128 ? 128 % g.C || g.C < 32 : g.C % 128) return 0;
-      const int seg = std::min(g.C, 128);
+      const int rb = op.rows_box;
+      if (g.C < rb ? rb % g.C || g.C < 32 : g.C % rb) return 0;
+      const int seg = std::min(g.C, rb);
       const int r = im2col_map(m, op.ptr, g.N, g.H, g.W, g.C, -g.pw, -g.ph, g.pw - (g.S - 1), g.ph - (g.R - 1),
                                g.sw, g.sh, seg, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
       if (r) p.mn_seg = seg;
@@ -196,10 +216,14 @@ int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_b
   p.dbg_b = g_dbg_b;
   p.dbg_t = g_dbg_t;
   const bool bx = uses_bx3(variant);
+  // variant "pair": CTA pairs (cta_group::2, 256-row tiles) when M spans two tiles
+  const bool pair = variant == MONET_CONV_PAIR && p.M > BM;
+  p.a.rows_box = BM;
+  p.b.rows_box = pair ? BN / 2 : BN;
   if (bx) {
     // MONET_TMA_MASK (debug): bit 0 enables TMA for A, bit 1 for B (default 3)
     static const int mask = getenv("MONET_TMA_MASK") ? atoi(getenv("MONET_TMA_MASK")) : 3;
-    p.mn_seg = 128;
+    p.mn_seg = p.b.rows_box;
     // MONET_CHUNK (debug): MMA stages (64 k each) per TMEM accumulation chain
     static const int chunk = getenv("MONET_CHUNK") ? atoi(getenv("MONET_CHUNK")) : 16;
     p.chunk_stages = chunk > 0 ? chunk : 16;
@@ -207,7 +231,7 @@ int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_b
     p.b.tma = (mask & 2) ? make_tma(p, p.b, &p.tma_b) : 0;
   }
   p.split_tf32 = variant == MONET_CONV_TF32 ? 0 : 1;
-  p.m_tiles = (p.M + BM - 1) / BM;
+  p.m_tiles = (p.M + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM);
   p.n_tiles = (p.N + BN - 1) / BN;
   const int kblocks = std::max(1, (p.Kd + BK - 1) / BK);
   int splits = p.ph.on ? 1 : choose_splits(variant, p.M, p.N, p.Kd);  // phase rows scatter: no split-K
@@ -222,8 +246,10 @@ int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_b
   p.ws = static_cast<float*>(ws);
   p.epi = p.splits > 1 ? EPI_PARTIAL : (accumulate ? EPI_ACCUM : EPI_STORE);
   const int tiles = p.m_tiles * p.n_tiles * p.splits;
-  const int grid = std::min(tiles, kNumSMs);
-  if (int e = bx ? dispatch_modes<true>(p, grid, st) : dispatch_modes<false>(p, grid, st)) return e;
+  const int grid = pair ? 2 * std::min(tiles, kNumSMs / 2) : std::min(tiles, kNumSMs);
+  const int e = !bx ? dispatch_modes<false, false>(p, grid, st)
+                    : (pair ? dispatch_modes<true, true>(p, grid, st) : dispatch_modes<true, false>(p, grid, st));
+  if (e) return e;
   if (p.splits > 1) {
     long long total = (long long)p.M * p.N;
     splitk_reduce_kernel<<<ew_blocks(total), kEwThreads, 0, st>>>(p.ws, p.c, p.M, p.N, p.ldc, p.splits, accumulate);

@@ -100,13 +100,23 @@ MONET_DEV void tmem_st<16>(uint32_t taddr, const uint32_t (&r)[16]) {
 }
 MONET_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// D[tmem] (+)= A[tmem] * B[smem]^T, kind::f16 (bf16 in, fp32 accumulate), one CTA.
+// D[tmem] (+)= A[tmem] * B[smem]^T, kind::f16 (bf16 in, fp32 accumulate); one CTA,
+// or (PR) the CTA pair: M = 256, A rows / B columns split across the two CTAs.
+template <bool PR>
 MONET_DEV void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  if constexpr (PR) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  }
 }
 
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int b_mn_major) {
@@ -275,10 +285,10 @@ struct Loader {
     const uint32_t dst = smem_u32(tile);
     const int k = kb * BKR;
     if constexpr (MODE == OP_KMAJOR) {
-      mbar_arrive_tx(bar, BM * BKR * 4);
+      mbar_arrive_tx(bar, op.rows_box * BKR * 4);
       tma_2d(dst, m, k, row0, bar);
     } else if constexpr (MODE == OP_MNMAJOR) {
-      mbar_arrive_tx(bar, BM * BKR * 4);
+      mbar_arrive_tx(bar, op.rows_box * BKR * 4);
       if (op.kdiv >= p.Kd && !p.ph.on) {
         tma_2d(dst, m, row0, k, bar);
       } else {  // k = tap * kdiv + kout, kdiv % 32 == 0: tensor {rows, taps, kdiv}
@@ -333,10 +343,10 @@ struct Loader {
       }
     } else {  // IM2COL_WGRAD: rows (tap, c) in segments of p.mn_seg channels, k = 32 output pixels
       const int seg = p.mn_seg;
-      mbar_arrive_tx(bar, BN * BKR * 4);
+      mbar_arrive_tx(bar, op.rows_box * BKR * 4);
       const int q = k % g.Q, t = k / g.Q, pp = t % g.P, n = t / g.P;
       const int w0 = q * g.sw - g.pw, h0 = pp * g.sh - g.ph;
-      for (int sg = 0; sg < BN / seg; ++sg) {
+      for (int sg = 0; sg < op.rows_box / seg; ++sg) {
         const int row = row0 + sg * seg;
         const int tap = row / g.C, c = row - tap * g.C;
         const int r = tap / g.S, s = tap - r * g.S;
@@ -358,11 +368,13 @@ struct Loader {
       if constexpr (kMN) {
         const int kr = (sub >> 5) + 2 * i;
         const int r = 4 * (sub & 31);
+        if (r >= op.rows_box) continue;  // the B half of a CTA pair covers 64 rows
         row = row0 + r;
         k = kk0 + kr;
-        off = mn_off(r, kr, MODE == OP_IM2COL_WGRAD ? p.mn_seg : BN);
+        off = mn_off(r, kr, MODE == OP_IM2COL_WGRAD ? p.mn_seg : op.rows_box);
       } else {
         const int r = (sub >> 3) + 8 * i;
+        if (r >= op.rows_box) continue;
         row = row0 + r;
         k = kk0 + 4 * (sub & 7);
         off = sw128_offset(r, sub & 7);
@@ -382,7 +394,8 @@ struct Loader {
 };
 // Debug wait-time accounting (p.dbg_t != nullptr): counters per CTA
 //   0 loader raw_empty, 3 MMA a_full, 4 MMA b_full, 5 MMA tempty, 6 epilogue tfull,
-//   7 A-split st_empty, 8 A-split raw_full, 9 B-split st_empty, 10 B-split raw_full, 15 kernel cycles
+//   7 A-split st_empty, 8 A-split raw_full, 9 B-split st_empty, 10 B-split raw_full,
+//   11 MMA issue (first MMA to commit, lane 0), 15 kernel cycles
 #define TWAIT(slot, expr)                                   \
   do {                                                      \
     const long long t0_ = p.dbg_t ? clock64() : 0;          \
@@ -390,9 +403,19 @@ struct Loader {
     if (p.dbg_t) twait[slot] += clock64() - t0_;            \
   } while (0)
 
-template <int AM, int BMODE>
+// PR (CTA pair, cta_group::2): the two CTAs of a cluster compute a 256 x 128
+// tile -- each splits its own 128 A rows into its own TMEM and 64 of the 128 B
+// rows into its own smem; the leader (rank 0) issues M=256 MMAs that read both
+// halves, commits are multicast to both CTAs, and the producer / epilogue
+// arrivals the leader waits on come per warp from both CTAs.  Per SM the B
+// traffic through shared memory halves (the limiter of the 1-CTA kernel).
+template <int AM, int BMODE, bool PR>
 __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_constant__ GemmParams p) {
   constexpr bool a_mn = mode_is_mn(AM), b_mn = mode_is_mn(BMODE);
+  constexpr int kPairN = PR ? 2 : 1;          // CTAs per tile
+  constexpr int kBRows = BN / kPairN;         // B rows this CTA splits
+  constexpr int kBChunks = kBRows / 32;       // K-major 16B chunks per B-split thread per raw k-block
+  constexpr int kTileM = BM * kPairN;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B align by offsetting the __shared__ array itself (not via an integer
   // round trip) so the compiler keeps the shared address space: LDS / STS
@@ -413,6 +436,19 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
   const int warp = warp_id();
   const int lane = lane_id();
   const int n_tiles_total = p.m_tiles * p.n_tiles * p.splits;
+  const uint32_t rank = PR ? cluster_ctarank() : 0u;
+  const int unit0 = PR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;  // persistent tile loop: one unit per pair
+  const int n_units = PR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  // arrivals the MMA issuer waits on: per warp, to the leader CTA's barrier
+  auto arrive_leader = [&](uint64_t* bar) {
+    __syncwarp();
+    if (lane == 0) {
+      if constexpr (PR)
+        mbar_arrive_cluster(mapa_shared(bar, 0));
+      else
+        mbar_arrive(bar);
+    }
+  };
   long long twait[16] = {0};
   float* const dbg_a = p.dbg_a;  // hoisted: loop-invariant kernel parameters
   float* const dbg_b = p.dbg_b;
@@ -424,19 +460,27 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
       mbar_init(&raw_empty[s], (kASplitWarps / 2 + kBSplitWarps) * 32);  // one A half + all of B per item
     }
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&a_full[s], kASplitWarps * 32);
-      mbar_init(&b_full[s], kBSplitWarps * 32);
+      mbar_init(&a_full[s], kASplitWarps * kPairN);
+      mbar_init(&b_full[s], kBSplitWarps * kPairN);
       mbar_init(&st_empty[s], 1);
     }
     for (int a = 0; a < kAccStages; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], kEpiWarps * 32);
+      mbar_init(&tempty[a], kEpiWarps * kPairN);
     }
     mbar_fence_init();
   }
-  if (warp == kWarpMma) tmem_alloc(tmem_slot, kTmemCols);
+  if (warp == kWarpMma) {
+    if constexpr (PR)
+      tmem_alloc_pair(tmem_slot, kTmemCols);
+    else
+      tmem_alloc(tmem_slot, kTmemCols);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PR)
+    cluster_sync();  // the peer's barriers are initialised before any remote arrive
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -449,13 +493,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
     Loader<AM> la;
     Loader<BMODE> lb;
     int item = 0;
-    for (int tile = active ? (int)blockIdx.x : n_tiles_total; tile < n_tiles_total; tile += gridDim.x) {
+    for (int tile = active ? unit0 : n_tiles_total; tile < n_tiles_total; tile += n_units) {
       int mt, nt, kb0, nst;
       tile_range(p, tile, mt, nt, kb0, nst);
       if (is_b)
-        lb.init(p, p.b, nt * BN, kb0 * BKR);
+        lb.init(p, p.b, nt * BN + (int)rank * kBRows, kb0 * BKR);
       else
-        la.init(p, p.a, mt * BM, kb0 * BKR);
+        la.init(p, p.a, mt * kTileM + (int)rank * BM, kb0 * BKR);
       for (int kb = kb0; kb < kb0 + 2 * nst; ++kb, ++item) {
         const int slot = item % kRawSlots;
         TWAIT(0, mbar_wait(&raw_empty[slot], ((item / kRawSlots) & 1) ^ 1));
@@ -481,7 +525,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
     const uint32_t lane_sel = (uint32_t)(quarter * 32) << 16;
     const int half = (warp - kWarpASplit) >> 2;  // which raw k-block of each stage this warp splits
     int stage_item = 0;
-    for (int tile = blockIdx.x; tile < n_tiles_total; tile += gridDim.x) {
+    for (int tile = unit0; tile < n_tiles_total; tile += n_units) {
       int mt, nt, kb0, nst;
       tile_range(p, tile, mt, nt, kb0, nst);
       const int item_kb0 = kb0;
@@ -523,7 +567,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
           if (dbg_a != nullptr) {
             const long long kpad = (long long)((p.Kd + 63) / 64) * 64;
             const int kb = (item_kb0 + 2 * s + half);
-            const int m = mt * BM + row;
+            const int m = mt * kTileM + (int)rank * BM + row;
             if (m < p.M)
               for (int k = 0; k < 32; ++k) dbg_a[m * kpad + kb * 32 + k] = v[k];
           }
@@ -539,14 +583,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
         }
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(&a_full[stage]);
+        arrive_leader(&a_full[stage]);
       }
     }
   } else if (warp < kWarpEpi) {
     // ---------------------------------------------------------------- B split -> smem bf16
     const int t = threadIdx.x - kWarpBSplit * 32;  // 0..255
     int item = 0, stage_item = 0;
-    for (int tile = blockIdx.x; tile < n_tiles_total; tile += gridDim.x) {
+    for (int tile = unit0; tile < n_tiles_total; tile += n_units) {
       int mt, nt, kb0, nst;
       tile_range(p, tile, mt, nt, kb0, nst);
       for (int s = 0; s < nst; ++s, ++stage_item) {
@@ -560,15 +604,18 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
           TWAIT(10, mbar_wait(&raw_full[slot], (item / kRawSlots) & 1));
           const uint8_t* rt = raw + slot * kRawBytes + kRawTile;
           // K-major: a warp covers rows {0,4,1,5}+base so that the two rows of
-          // one 16-lane STS.64 phase land in opposite swizzle halves
+          // one 16-lane STS.64 phase land in opposite swizzle halves.
+          // MN-major: 4-row group g of k-rows kr0 + kstep * i.
           const int w8 = t >> 5, l = t & 31;
           const int rbase = 8 * (w8 >> 1) + 2 * (w8 & 1) + (((l >> 3) & 1) << 2) + (l >> 4);
-          float4 q[4];
+          constexpr int kGroups = kBRows / 4, kStep = 256 / kGroups;
+          const int g = t % kGroups, kr0 = t / kGroups;
+          float4 q[kBChunks];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
+          for (int i = 0; i < kBChunks; ++i) {
             uint32_t off;
             if constexpr (b_mn) {
-              off = mn_off(4 * (t & 31), (t >> 5) + 8 * i, p.mn_seg);
+              off = mn_off(4 * g, kr0 + kStep * i, p.mn_seg);
             } else {
               off = sw128_offset(rbase + 32 * i, t & 7);
             }
@@ -577,30 +624,30 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
           if (dbg_b != nullptr) {
             const long long kpad = (long long)((p.Kd + 63) / 64) * 64;
             const int kb = kb0 + 2 * s + half;
-            for (int i = 0; i < 4; ++i) {
+            for (int i = 0; i < kBChunks; ++i) {
               const float e[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
               for (int j = 0; j < 4; ++j) {
                 int n, k;
                 if (b_mn) {
-                  n = 4 * (t & 31) + j;
-                  k = (t >> 5) + 8 * i;
+                  n = 4 * g + j;
+                  k = kr0 + kStep * i;
                 } else {
                   n = rbase + 32 * i;
                   k = 4 * (t & 7) + j;
                 }
-                n += nt * BN;
+                n += nt * BN + (int)rank * kBRows;
                 if (n < p.N) dbg_b[n * kpad + kb * 32 + k] = e[j];
               }
             }
           }
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
+          for (int i = 0; i < kBChunks; ++i) {
             uint2 h, lw;
             split_pair(q[i].x, q[i].y, h.x, lw.x);
             split_pair(q[i].z, q[i].w, h.y, lw.y);
             uint32_t off;
             if constexpr (b_mn) {
-              off = b_off_mnmajor(4 * (t & 31), 32 * half + (t >> 5) + 8 * i);
+              off = b_off_mnmajor(4 * g, 32 * half + kr0 + kStep * i);
             } else {
               off = b_off_kmajor(rbase + 32 * i, 32 * half + 4 * (t & 7));
             }
@@ -610,7 +657,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
           mbar_arrive(&raw_empty[slot]);  // after all loaded values are consumed (see A split)
         }
         fence_proxy_async_smem();
-        mbar_arrive(&b_full[stage]);
+        arrive_leader(&b_full[stage]);
       }
     }
   } else if (warp < kWarpMma) {
@@ -618,13 +665,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
     const int quarter = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < n_tiles_total; tile += gridDim.x) {
+    for (int tile = unit0; tile < n_tiles_total; tile += n_units) {
       int mt, nt, sp, kb0, kb1;
       tile_coords(p, tile, mt, nt, sp);
       kb_range(p, sp, kb0, kb1);
       const int nst = (kb1 - kb0 + 1) / 2;
       const int nchunks = (nst + p.chunk_stages - 1) / p.chunk_stages;
-      const int m = mt * BM + quarter * 32 + lane;
+      const int m = mt * kTileM + (int)rank * BM + quarter * 32 + lane;
       long long out_row = m;  // phase dgrad: scatter row (n, i, j) to dx[n][i*sh + a][j*sw + b]
       if (p.ph.on && m < p.M) {
         const int j = m % p.ph.Wp, t = m / p.ph.Wp, i = t % p.ph.Hp, n = t / p.ph.Hp;
@@ -679,34 +726,41 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
           __syncwarp();
         }
         tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        arrive_leader(&tempty[acc]);
         if (++acc == kAccStages) {
           acc = 0;
           acc_phase ^= 1;
         }
       }
     }
-  } else {
-    // ---------------------------------------------------------------- MMA issuer
-    const uint32_t idesc = idesc_bf16(BM, BN, b_mn ? 1 : 0);
+  } else if (rank == 0) {
+    // ---------------------------------------------------------------- MMA issuer (leader CTA)
+    const uint32_t idesc = idesc_bf16(kTileM, BN, b_mn ? 1 : 0);
     int stage_item = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < n_tiles_total; tile += gridDim.x) {
+    auto wait = [&](uint64_t* bar, uint32_t ph) {
+      if constexpr (PR)
+        mbar_wait_cluster(bar, ph);
+      else
+        mbar_wait(bar, ph);
+    };
+    for (int tile = unit0; tile < n_tiles_total; tile += n_units) {
       int mt, nt, kb0, nst;
       tile_range(p, tile, mt, nt, kb0, nst);
       for (int c0 = 0; c0 < nst; c0 += p.chunk_stages) {
         const int c1 = min(nst, c0 + p.chunk_stages);
-        TWAIT(5, mbar_wait(&tempty[acc], acc_phase ^ 1));
+        TWAIT(5, wait(&tempty[acc], acc_phase ^ 1));
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int s = c0; s < c1; ++s, ++stage_item) {
           const int stage = stage_item % kStages;
           const uint32_t ph = (stage_item / kStages) & 1;
-          TWAIT(3, mbar_wait(&a_full[stage], ph));
-          TWAIT(4, mbar_wait(&b_full[stage], ph));
+          TWAIT(3, wait(&a_full[stage], ph));
+          TWAIT(4, wait(&b_full[stage], ph));
           tc_fence_after();
           if (lane == 0) {
+            const long long t_issue = p.dbg_t ? clock64() : 0;
             const uint32_t a_hi = tmem_base + kTmemA + stage * kAStageCols;
             const uint32_t a_lo = a_hi + 32;
             const uint32_t bhi = smem_u32(bst + stage * kStageBytes);
@@ -714,12 +768,18 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
 #pragma unroll
             for (int kk = 0; kk < BKS / 16; ++kk) {
               const uint32_t first = (s == c0 && kk == 0) ? 0u : 1u;
-              mma_bf16_ts(d_tmem, a_lo + kk * 8, b_desc(bhi, b_mn, kk), idesc, first);
-              mma_bf16_ts(d_tmem, a_hi + kk * 8, b_desc(blo, b_mn, kk), idesc, 1u);
-              mma_bf16_ts(d_tmem, a_hi + kk * 8, b_desc(bhi, b_mn, kk), idesc, 1u);
+              mma_bf16_ts<PR>(d_tmem, a_lo + kk * 8, b_desc(bhi, b_mn, kk), idesc, first);
+              mma_bf16_ts<PR>(d_tmem, a_hi + kk * 8, b_desc(blo, b_mn, kk), idesc, 1u);
+              mma_bf16_ts<PR>(d_tmem, a_hi + kk * 8, b_desc(bhi, b_mn, kk), idesc, 1u);
             }
-            mma_commit(&st_empty[stage]);
-            if (s == c1 - 1) mma_commit(&tfull[acc]);
+            if constexpr (PR) {
+              mma_commit_pair(&st_empty[stage]);
+              if (s == c1 - 1) mma_commit_pair(&tfull[acc]);
+            } else {
+              mma_commit(&st_empty[stage]);
+              if (s == c1 - 1) mma_commit(&tfull[acc]);
+            }
+            if (p.dbg_t) twait[11] += clock64() - t_issue;
           }
           __syncwarp();
         }
@@ -741,10 +801,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PR)
+    cluster_sync();  // the leader's MMAs read this CTA's TMEM / smem until the end
+  else
+    __syncthreads();
   if (warp == kWarpMma) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, kTmemCols);
+    if constexpr (PR)
+      tmem_dealloc_pair(tmem_base, kTmemCols);
+    else
+      tmem_dealloc(tmem_base, kTmemCols);
   }
 }
 #undef TWAIT

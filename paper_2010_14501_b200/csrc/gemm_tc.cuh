@@ -49,6 +49,8 @@ struct Operand {
   int aligned;  // 16B groups are aligned and never straddle an edge (host-checked)
   int tma;      // bf16x3 kernel: 0 = 16B cp.async groups, 1 = TMA tiled map, 2 = TMA im2col map,
                 //   3 = TMA im2col with C < 32: one box per filter tap, chunk-major raw layout
+  int rows_box; // bf16x3 kernel: rows of this operand one CTA loads per tile (128, or 64 for the
+                //   B half of a CTA pair)
 };
 
 enum EpiMode : int { EPI_STORE = 0, EPI_ACCUM = 1, EPI_PARTIAL = 2 };

@@ -68,6 +68,7 @@ class Network:
     def __init__(self, ops: list[Op], batch: int, num_classes: int):
         self.ops = ops
         self.fused = any(op.kind == "bnrelu" for op in ops)
+        self.pair_variants = False  # offer the cta_group::2 conv variant in the catalog
         self.batch = batch
         self.num_classes = num_classes
         self.n = len(ops)
@@ -154,7 +155,8 @@ class Network:
         nodes, backward, inters = [], [], []
         for op in self.ops:
             nodes.append({"id": op.id, "output_bytes": op.nbytes, "deps": list(op.deps)})
-            impls = [{"name": n, "deps_kind": k, "extra_deps": []} for n, k in BWD_IMPLS[op.kind]]
+            impls = [{"name": n, "deps_kind": k, "extra_deps": []} for n, k in BWD_IMPLS[op.kind]
+                     if n != "pair" or self.pair_variants]
             backward.append({"node": op.id, "grad_bytes": self.grad_bytes(op), "impls": impls})
             if op.id in self.intermediate_of:
                 u = self.intermediate_of[op.id]
@@ -173,8 +175,12 @@ class Network:
             ws = lib.conv_ws_bytes(1, 0, d)
             if ws:
                 fwd.append(("splitk", ws))
+            if self.pair_variants:  # 2-CTA (cta_group::2) tiles: same bytes, another speed point
+                fwd.append(("pair", 0))
             bwd.append(("splitk", lib.conv_ws_bytes(1, 3, d), x))
             bwd.append(("implicit", lib.conv_ws_bytes(0, 3, d), x))
+            if self.pair_variants:
+                bwd.append(("pair", lib.conv_ws_bytes(4, 3, d), x))
         elif op.kind == "fc":
             n, fi = self.op(op.deps[0]).shape
             fo = op.shape[1]
@@ -261,7 +267,7 @@ def _cost(costs, key, fallback):
 
 BWD_IMPLS = {
     "input": [("none", "input")],
-    "conv": [("splitk", "input"), ("implicit", "input")],
+    "conv": [("splitk", "input"), ("implicit", "input"), ("pair", "input")],
     "fc": [("gemm-splitk", "input"), ("gemm", "input")],
     "bn": [("bwd-in", "input"), ("bwd-out", "output")],
     "bnrelu": [("bwd-in", "input")],

@@ -55,7 +55,7 @@ CONV_CASES = [
 
 
 @pytest.mark.parametrize("case", CONV_CASES)
-@pytest.mark.parametrize("variant", ["implicit", "splitk", "tf32x3"])
+@pytest.mark.parametrize("variant", ["implicit", "splitk", "tf32x3", "pair"])
 def test_conv_passes(cuda, case, variant):
     n, h, w, c, k, r, s, stride, pad = case
     g = torch.Generator().manual_seed(0)
@@ -122,7 +122,7 @@ def test_gemm_layouts(cuda, mnk, amn, bmn):
     ldb = n if bmn else k
     C = torch.zeros(m, n, device=cuda)
     ad, bd = a_store.to(cuda), b_store.to(cuda)
-    for variant in (0, 1, 3):
+    for variant in (0, 1, 3, 4):
         wsb = N.lib().gemm_ws_bytes(variant, m, n, k)
         ws = torch.empty(wsb // 4 + 1, device=cuda)
         N.lib().gemm(variant, ad.data_ptr(), amn, lda, bd.data_ptr(), bmn, ldb,

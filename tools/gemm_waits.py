@@ -40,7 +40,8 @@ lib.dll.monet_debug_timers(None)
 c_ = cnt.cpu().tolist()
 tot = c_[15]
 names = {0: "loader raw_empty", 3: "MMA a_full", 4: "MMA b_full", 5: "MMA tempty", 6: "epi tfull",
-         7: "Asplit st_empty", 8: "Asplit raw_full", 9: "Bsplit st_empty", 10: "Bsplit raw_full"}
+         7: "Asplit st_empty", 8: "Asplit raw_full", 9: "Bsplit st_empty", 10: "Bsplit raw_full",
+         11: "MMA issue loop"}
 print(f"{name} {pss}: kernel cycles (sum over CTAs) {tot:.3e}")
 for i, nm in names.items():
     print(f"  {nm:18s} {100.0 * c_[i] / max(tot, 1):6.1f}%")
