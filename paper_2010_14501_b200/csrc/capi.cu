@@ -28,8 +28,8 @@ inline int ew_blocks(long long work_items) {
 }
 
 // ----------------------------------------------------------------- GEMM setup
-int choose_splits(int variant, int M, int N, int Kd) {
-  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+int choose_splits(int variant, int M, int N, int Kd, int n_pitch = BN) {
+  const int tiles = ((M + BM - 1) / BM) * ((N + n_pitch - 1) / n_pitch);
   const int kblocks = (Kd + BK - 1) / BK;
   if (variant != MONET_CONV_SPLITK) return 1;
   if (tiles >= kNumSMs) return 1;
@@ -38,19 +38,19 @@ int choose_splits(int variant, int M, int N, int Kd) {
   return std::max(1, std::min(want, cap));
 }
 
-size_t gemm_ws(int variant, int M, int N, int Kd) {
-  int s = choose_splits(variant, M, N, Kd);
+size_t gemm_ws(int variant, int M, int N, int Kd, int n_pitch = BN) {
+  int s = choose_splits(variant, M, N, Kd, n_pitch);
   return s > 1 ? (size_t)s * M * N * sizeof(float) : 0;
 }
 
 // One instantiation per (A mode, B mode) pair used by conv / linear / gemm.
 // kBx3 selects the bf16x3 A-in-TMEM kernel (gemm_bf16x3.cuh, the product
 // path); otherwise the 3xTF32 / TF32 all-smem kernel (gemm_tc.cuh).
-template <bool kBx3, bool kPair, int AM, int BMODE>
+template <bool kBx3, bool kPair, int AM, int BMODE, int NB = BN>
 int launch_inst(const GemmParams& p, int grid, cudaStream_t st) {
   static bool attr = false;
   if constexpr (kBx3) {
-    auto kern = bx3::gemm_bf16x3_kernel<AM, BMODE, kPair>;
+    auto kern = bx3::gemm_bf16x3_kernel<AM, BMODE, kPair, NB>;
     if (!attr) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bx3::kSmemBytes);
       attr = true;
@@ -83,16 +83,16 @@ int launch_inst(const GemmParams& p, int grid, cudaStream_t st) {
   return 0;
 }
 
-template <bool kBx3, bool kPair>
+template <bool kBx3, bool kPair, int NB = BN>
 int dispatch_modes(const GemmParams& p, int grid, cudaStream_t st) {
   const int a = p.a.mode, b = p.b.mode;
-  if (a == OP_IM2COL_FPROP && b == OP_KMAJOR) return launch_inst<kBx3, kPair, OP_IM2COL_FPROP, OP_KMAJOR>(p, grid, st);
-  if (a == OP_KMAJOR && b == OP_KMAJOR) return launch_inst<kBx3, kPair, OP_KMAJOR, OP_KMAJOR>(p, grid, st);
-  if (a == OP_IM2COL_DGRAD && b == OP_MNMAJOR) return launch_inst<kBx3, kPair, OP_IM2COL_DGRAD, OP_MNMAJOR>(p, grid, st);
-  if (a == OP_KMAJOR && b == OP_MNMAJOR) return launch_inst<kBx3, kPair, OP_KMAJOR, OP_MNMAJOR>(p, grid, st);
-  if (a == OP_MNMAJOR && b == OP_IM2COL_WGRAD) return launch_inst<kBx3, kPair, OP_MNMAJOR, OP_IM2COL_WGRAD>(p, grid, st);
-  if (a == OP_MNMAJOR && b == OP_MNMAJOR) return launch_inst<kBx3, kPair, OP_MNMAJOR, OP_MNMAJOR>(p, grid, st);
-  if (a == OP_MNMAJOR && b == OP_KMAJOR) return launch_inst<kBx3, kPair, OP_MNMAJOR, OP_KMAJOR>(p, grid, st);
+  if (a == OP_IM2COL_FPROP && b == OP_KMAJOR) return launch_inst<kBx3, kPair, OP_IM2COL_FPROP, OP_KMAJOR, NB>(p, grid, st);
+  if (a == OP_KMAJOR && b == OP_KMAJOR) return launch_inst<kBx3, kPair, OP_KMAJOR, OP_KMAJOR, NB>(p, grid, st);
+  if (a == OP_IM2COL_DGRAD && b == OP_MNMAJOR) return launch_inst<kBx3, kPair, OP_IM2COL_DGRAD, OP_MNMAJOR, NB>(p, grid, st);
+  if (a == OP_KMAJOR && b == OP_MNMAJOR) return launch_inst<kBx3, kPair, OP_KMAJOR, OP_MNMAJOR, NB>(p, grid, st);
+  if (a == OP_MNMAJOR && b == OP_IM2COL_WGRAD) return launch_inst<kBx3, kPair, OP_MNMAJOR, OP_IM2COL_WGRAD, NB>(p, grid, st);
+  if (a == OP_MNMAJOR && b == OP_MNMAJOR) return launch_inst<kBx3, kPair, OP_MNMAJOR, OP_MNMAJOR, NB>(p, grid, st);
+  if (a == OP_MNMAJOR && b == OP_KMAJOR) return launch_inst<kBx3, kPair, OP_MNMAJOR, OP_KMAJOR, NB>(p, grid, st);
   return -(int)cudaErrorInvalidValue;
 }
 
@@ -150,6 +150,28 @@ int im2col_map(CUtensorMap* m, const float* ptr, int n, int h, int w, int c, int
 int make_tma(GemmParams& p, const Operand& op, CUtensorMap* m) {
   if (!tma_available() || (reinterpret_cast<uintptr_t>(op.ptr) & 15) != 0) return 0;
   const ConvGeom& g = p.g;
+  if (p.wv_q) {  // wgrad tap view (k = (n, p, q < wv_q)); out-of-range q / r load as zeros
+    if (op.mode == OP_MNMAJOR) {  // dy[n][p][q][kout] as {kout, q, n*p}
+      cuuint64_t dims[3] = {(cuuint64_t)g.K, (cuuint64_t)g.Q, (cuuint64_t)g.N * g.P};
+      cuuint64_t strides[2] = {(cuuint64_t)g.K * 4, (cuuint64_t)g.Q * g.K * 4};
+      cuuint32_t box[3] = {(cuuint32_t)op.rows_box, 32, 1};
+      return tiled_map(m, op.ptr, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE) ? 4 : 0;
+    }
+    // zero-padded input xp[n][Hp][Wp][c]: element (s*C + c, q, r, p, n) = xp[n][p*sh + r][q*sw + s][c];
+    // the q stride (sw*C floats) is below the s*C extent -- overlapping rows, accepted by the
+    // encoder and pinned on the B200 by tools/tma_overlap_probe.cu
+    const long long Wp = (long long)(g.Q - 1) * g.sw + g.S, Hp = (long long)(g.P - 1) * g.sh + g.R;
+    cuuint64_t dims[5] = {(cuuint64_t)g.S * g.C, (cuuint64_t)g.Q, (cuuint64_t)g.R, (cuuint64_t)g.P,
+                          (cuuint64_t)g.N};
+    cuuint64_t strides[4] = {(cuuint64_t)g.sw * g.C * 4, (cuuint64_t)Wp * g.C * 4, (cuuint64_t)g.sh * Wp * g.C * 4,
+                             (cuuint64_t)Hp * Wp * g.C * 4};
+    cuuint32_t box[5] = {(cuuint32_t)g.S * g.C, 32, (cuuint32_t)(op.rows_box / (g.S * g.C)), 1, 1};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    CUresult r = g_enc_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(op.ptr), dims, strides, box,
+                             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 4 : 0;
+  }
   switch (op.mode) {
     case OP_KMAJOR: {
       if (op.ld % 4) return 0;
@@ -218,23 +240,28 @@ int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_b
   const bool bx = uses_bx3(variant);
   // variant "pair": CTA pairs (cta_group::2, 256-row tiles) when M spans two tiles
   const bool pair = variant == MONET_CONV_PAIR && p.M > BM;
+  // 64-wide N tiles when the whole problem is at most 64 columns wide (64-channel convs)
+  const bool narrow = bx && !pair && !p.wv_q && p.N <= 64;
+  if (p.n_pitch == 0) p.n_pitch = narrow ? 64 : BN;
   p.a.rows_box = BM;
-  p.b.rows_box = pair ? BN / 2 : BN;
+  p.b.rows_box = pair ? BN / 2 : (p.wv_q || narrow ? p.n_pitch : BN);
   if (bx) {
     // MONET_TMA_MASK (debug): bit 0 enables TMA for A, bit 1 for B (default 3)
     static const int mask = getenv("MONET_TMA_MASK") ? atoi(getenv("MONET_TMA_MASK")) : 3;
-    p.mn_seg = p.b.rows_box;
+    p.mn_seg = p.wv_q ? p.g.S * p.g.C : p.b.rows_box;
     // MONET_CHUNK (debug): MMA stages (64 k each) per TMEM accumulation chain
     static const int chunk = getenv("MONET_CHUNK") ? atoi(getenv("MONET_CHUNK")) : 16;
     p.chunk_stages = chunk > 0 ? chunk : 16;
     p.a.tma = (mask & 1) ? make_tma(p, p.a, &p.tma_a) : 0;
     p.b.tma = (mask & 2) ? make_tma(p, p.b, &p.tma_b) : 0;
+    // the tap view's k order (n, p, padded q) exists only as tensor maps: no cp.async fallback
+    if (p.wv_q && (p.a.tma != 4 || p.b.tma != 4)) return -(int)cudaErrorNotSupported;
   }
   p.split_tf32 = variant == MONET_CONV_TF32 ? 0 : 1;
   p.m_tiles = (p.M + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM);
-  p.n_tiles = (p.N + BN - 1) / BN;
+  p.n_tiles = (p.N + p.n_pitch - 1) / p.n_pitch;
   const int kblocks = std::max(1, (p.Kd + BK - 1) / BK);
-  int splits = p.ph.on ? 1 : choose_splits(variant, p.M, p.N, p.Kd);  // phase rows scatter: no split-K
+  int splits = p.ph.on ? 1 : choose_splits(variant, p.M, p.N, p.Kd, p.n_pitch);  // phase rows scatter: no split-K
   size_t need = splits > 1 ? (size_t)splits * p.M * p.N * sizeof(float) : 0;
   if (need > ws_bytes || (need && ws == nullptr)) {
     splits = 1;  // never write outside the caller's workspace
@@ -247,8 +274,10 @@ int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_b
   p.epi = p.splits > 1 ? EPI_PARTIAL : (accumulate ? EPI_ACCUM : EPI_STORE);
   const int tiles = p.m_tiles * p.n_tiles * p.splits;
   const int grid = pair ? 2 * std::min(tiles, kNumSMs / 2) : std::min(tiles, kNumSMs);
-  const int e = !bx ? dispatch_modes<false, false>(p, grid, st)
-                    : (pair ? dispatch_modes<true, true>(p, grid, st) : dispatch_modes<true, false>(p, grid, st));
+  const int e = !bx     ? dispatch_modes<false, false>(p, grid, st)
+                : pair   ? dispatch_modes<true, true>(p, grid, st)
+                : narrow ? dispatch_modes<true, false, 64>(p, grid, st)
+                         : dispatch_modes<true, false>(p, grid, st);
   if (e) return e;
   if (p.splits > 1) {
     long long total = (long long)p.M * p.N;
@@ -346,6 +375,55 @@ bool use_phases(int variant, const monet_conv_desc* d) {
   return uses_bx3(variant) && (d->stride_h > 1 || d->stride_w > 1) && d->r <= 8 && d->s <= 8;
 }
 
+// Wgrad "tap view" for inputs with C < 32 (the 7x7/2 stem): the reduction runs
+// over k = (n, p, q padded to a multiple of 32) so that every 32-deep k-block is
+// one TMA box per operand -- dy {kout, 32 q, 1} and, over a zero-padded copy of
+// the input in the workspace, {S*C, 32 q, R-segments} with overlapping q / s
+// strides.  An n-tile covers floor(128 / (S*C)) filter rows (112 columns for the
+// stem).  Replaces the 16B cp.async gather (per-group divisions) for these layers.
+struct WView {
+  bool on;
+  int qpad, n_pitch;
+  long long kd;
+  size_t pad_bytes;
+};
+
+WView wgrad_view(int variant, const monet_conv_desc* d) {
+  WView v{};
+  if (!uses_bx3(variant) || variant == MONET_CONV_PAIR || is_pointwise(d) || d->c >= 32 || d->s * d->c > 128)
+    return v;
+  v.on = true;
+  v.qpad = (d->q + 31) / 32 * 32;
+  v.n_pitch = (128 / (d->s * d->c)) * d->s * d->c;
+  v.kd = (long long)d->n * d->p * v.qpad;
+  const long long hp = (long long)(d->p - 1) * d->stride_h + d->r, wp = (long long)(d->q - 1) * d->stride_w + d->s;
+  v.pad_bytes = (size_t)d->n * hp * wp * d->c * sizeof(float);
+  return v;
+}
+
+size_t align256(size_t b) { return (b + 255) / 256 * 256; }
+
+// xp[n][hp][wp][c] = x[n][hp - pad_h][wp - pad_w][c], zero outside
+__global__ void wgrad_pad_kernel(const float* __restrict__ x, float* __restrict__ xp, int n, int h, int w, int c,
+                                 int hp, int wp, int pad_h, int pad_w) {
+  const int c4 = c / 4;
+  const long long total = (long long)n * hp * wp * c4;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int cc = (int)(i % c4);
+    long long t = i / c4;
+    const int j = (int)(t % wp);
+    t /= wp;
+    const int ii = (int)(t % hp);
+    const int nn = (int)(t / hp);
+    const int hh = ii - pad_h, ww = j - pad_w;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if ((unsigned)hh < (unsigned)h && (unsigned)ww < (unsigned)w)
+      v = __ldg(reinterpret_cast<const float4*>(x + (((long long)nn * h + hh) * w + ww) * c) + cc);
+    reinterpret_cast<float4*>(xp)[i] = v;
+  }
+}
+
 GemmParams phase_params(const monet_conv_desc* d, const PhaseInfo& ph, const float* dy, const float* w, float* dx) {
   GemmParams p{};
   p.g = geom(d);
@@ -418,6 +496,10 @@ size_t monet_conv_ws_bytes(int variant, int pass, const monet_conv_desc* d) {
     return std::max(monet_conv_ws_bytes(variant, MONET_PASS_DGRAD, d), monet_conv_ws_bytes(variant, MONET_PASS_WGRAD, d));
   if (pass == MONET_PASS_DGRAD && use_phases(variant, d)) return 0;  // phase GEMMs never split K
   GemmParams p = conv_params(pass, d, nullptr, nullptr, nullptr);
+  if (pass == MONET_PASS_WGRAD) {
+    const WView v = wgrad_view(variant, d);
+    if (v.on) return align256(gemm_ws(variant, p.M, p.N, (int)v.kd, v.n_pitch)) + v.pad_bytes;
+  }
   return gemm_ws(variant, p.M, p.N, p.Kd);
 }
 
@@ -452,7 +534,24 @@ int monet_conv_dgrad(int variant, const monet_conv_desc* d, const float* dy, con
 int monet_conv_wgrad(int variant, const monet_conv_desc* d, const float* x, const float* dy, float* dw,
                      int accumulate, void* ws, size_t ws_bytes, void* stream) {
   if (int e = check_desc(d)) return e;
-  return launch_gemm(conv_params(MONET_PASS_WGRAD, d, x, dy, dw), variant, accumulate, ws, ws_bytes, S(stream));
+  GemmParams p = conv_params(MONET_PASS_WGRAD, d, x, dy, dw);
+  const WView v = wgrad_view(variant, d);
+  if (v.on) {
+    const size_t part = align256(gemm_ws(variant, p.M, p.N, (int)v.kd, v.n_pitch));
+    // a workspace without room for the padded input (callers sizing it by hand) takes the gather path
+    if (ws != nullptr && ws_bytes >= part + v.pad_bytes && tma_available()) {
+      float* xp = reinterpret_cast<float*>(static_cast<char*>(ws) + part);
+      const int hp = (d->p - 1) * d->stride_h + d->r, wp = (d->q - 1) * d->stride_w + d->s;
+      wgrad_pad_kernel<<<ew_blocks((long long)d->n * hp * wp * (d->c / 4)), kEwThreads, 0, S(stream)>>>(
+          x, xp, d->n, d->h, d->w, d->c, hp, wp, d->pad_h, d->pad_w);
+      p.Kd = (int)v.kd;
+      p.b.ptr = xp;
+      p.wv_q = v.qpad;
+      p.n_pitch = v.n_pitch;
+      return launch_gemm(p, variant, accumulate, ws, part, S(stream));
+    }
+  }
+  return launch_gemm(p, variant, accumulate, ws, ws_bytes, S(stream));
 }
 
 // ------------------------------------------------------------------- linear

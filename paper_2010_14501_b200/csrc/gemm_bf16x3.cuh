@@ -172,6 +172,13 @@ MONET_DEV void tma_3d(uint32_t dst, const CUtensorMap* m, int x, int y, int z, u
       "l"(m), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
       : "memory");
 }
+MONET_DEV void tma_5d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2, int c3, int c4, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+      "%6}], [%7];" ::"r"(dst),
+      "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+      : "memory");
+}
 // im2col: coordinates {c, w, h, n} of the base pixel, offsets {w, h} of the filter tap
 MONET_DEV void tma_im2col(uint32_t dst, const CUtensorMap* m, int c, int w, int h, int n, int ow, int oh,
                           uint64_t* bar) {
@@ -249,6 +256,9 @@ struct Loader {
     const ConvGeom& g = p.g;
     row0 = row0_;
     k0 = k0_;
+    if constexpr (MODE == OP_IM2COL_WGRAD) {
+      if (op.tma == 4) tap_r = row0 / (g.S * g.C);  // tap view: first filter row of the n-tile
+    }
     if (op.tma < 2) return;
     if constexpr (MODE == OP_IM2COL_FPROP || MODE == OP_IM2COL_DGRAD) {
       const bool fp = MODE == OP_IM2COL_FPROP;
@@ -289,7 +299,10 @@ struct Loader {
       tma_2d(dst, m, k, row0, bar);
     } else if constexpr (MODE == OP_MNMAJOR) {
       mbar_arrive_tx(bar, op.rows_box * BKR * 4);
-      if (op.kdiv >= p.Kd && !p.ph.on) {
+      if (op.tma == 4) {  // wgrad tap view: dy as {kout, q, n*p}
+        const int np = k / p.wv_q;
+        tma_3d(dst, m, row0, k - np * p.wv_q, np, bar);
+      } else if (op.kdiv >= p.Kd && !p.ph.on) {
         tma_2d(dst, m, row0, k, bar);
       } else {  // k = tap * kdiv + kout, kdiv % 32 == 0: tensor {rows, taps, kdiv}
         const int kh = k / op.kdiv;
@@ -341,6 +354,10 @@ struct Loader {
           ++tap_r;
         }
       }
+    } else if (op.tma == 4) {  // wgrad tap view: one box {S*C, 32 q, R-segments, 1, 1}
+      mbar_arrive_tx(bar, op.rows_box * BKR * 4);
+      const int np = k / p.wv_q, pp = np % g.P;
+      tma_5d(dst, m, 0, k - np * p.wv_q, tap_r, pp, np / g.P, bar);
     } else {  // IM2COL_WGRAD: rows (tap, c) in segments of p.mn_seg channels, k = 32 output pixels
       const int seg = p.mn_seg;
       mbar_arrive_tx(bar, op.rows_box * BKR * 4);
@@ -409,11 +426,15 @@ struct Loader {
 // halves, commits are multicast to both CTAs, and the producer / epilogue
 // arrivals the leader waits on come per warp from both CTAs.  Per SM the B
 // traffic through shared memory halves (the limiter of the 1-CTA kernel).
-template <int AM, int BMODE, bool PR>
+//
+// NB (N-tile width): 128, or 64 for problems with N <= 64 (64-channel convs):
+// half the B rows and half the MMA width per stage, same A work.
+template <int AM, int BMODE, bool PR, int NB>
 __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_constant__ GemmParams p) {
+  static_assert(NB == BN || (NB == 64 && !PR), "tile widths: 128 (1 CTA or pair), 64 (1 CTA)");
   constexpr bool a_mn = mode_is_mn(AM), b_mn = mode_is_mn(BMODE);
   constexpr int kPairN = PR ? 2 : 1;          // CTAs per tile
-  constexpr int kBRows = BN / kPairN;         // B rows this CTA splits
+  constexpr int kBRows = NB / kPairN;         // B rows this CTA splits
   constexpr int kBChunks = kBRows / 32;       // K-major 16B chunks per B-split thread per raw k-block
   constexpr int kTileM = BM * kPairN;
   extern __shared__ uint8_t smem_raw[];
@@ -497,7 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
       int mt, nt, kb0, nst;
       tile_range(p, tile, mt, nt, kb0, nst);
       if (is_b)
-        lb.init(p, p.b, nt * BN + (int)rank * kBRows, kb0 * BKR);
+        lb.init(p, p.b, nt * p.n_pitch + (int)rank * kBRows, kb0 * BKR);
       else
         la.init(p, p.a, mt * kTileM + (int)rank * BM, kb0 * BKR);
       for (int kb = kb0; kb < kb0 + 2 * nst; ++kb, ++item) {
@@ -635,7 +656,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
                   n = rbase + 32 * i;
                   k = 4 * (t & 7) + j;
                 }
-                n += nt * BN + (int)rank * kBRows;
+                n += nt * p.n_pitch + (int)rank * kBRows;
                 if (n < p.N) dbg_b[n * kpad + kb * 32 + k] = e[j];
               }
             }
@@ -684,11 +705,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
         const bool add_old = chunk > 0 || p.epi == EPI_ACCUM;
         TWAIT(6, mbar_wait(&tfull[acc], acc_phase));
         tc_fence_after();
-        for (int cc = 0; cc < BN / 32; ++cc) {
+        for (int cc = 0; cc < NB / 32; ++cc) {
           float v[32];
-          tmem_ld32(tmem_base + acc * BN + cc * 32 + ((uint32_t)(quarter * 32) << 16), v);
-          const int n0 = nt * BN + cc * 32;
-          if (m < p.M && n0 < p.N) {
+          tmem_ld32(tmem_base + acc * NB + cc * 32 + ((uint32_t)(quarter * 32) << 16), v);
+          const int n0 = nt * p.n_pitch + cc * 32;
+          if (m < p.M && n0 < p.N && cc * 32 < p.n_pitch) {
             float* dst;
             long long ld;
             if (p.epi == EPI_PARTIAL) {
@@ -698,7 +719,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
               dst = p.c + out_row * p.ldc + n0;
               ld = p.ldc;
             }
-            const int ncols = min(32, p.N - n0);
+            const int ncols = min(min(32, p.N - n0), p.n_pitch - cc * 32);
             const bool vec = (ncols == 32) && ((ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
             if (vec) {
 #pragma unroll
@@ -735,7 +756,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
     }
   } else if (rank == 0) {
     // ---------------------------------------------------------------- MMA issuer (leader CTA)
-    const uint32_t idesc = idesc_bf16(kTileM, BN, b_mn ? 1 : 0);
+    const uint32_t idesc = idesc_bf16(kTileM, NB, b_mn ? 1 : 0);
     int stage_item = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -752,7 +773,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
         const int c1 = min(nst, c0 + p.chunk_stages);
         TWAIT(5, wait(&tempty[acc], acc_phase ^ 1));
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * NB;
         for (int s = c0; s < c1; ++s, ++stage_item) {
           const int stage = stage_item % kStages;
           const uint32_t ph = (stage_item / kStages) & 1;

@@ -48,7 +48,9 @@ struct Operand {
   long long ks1;
   int aligned;  // 16B groups are aligned and never straddle an edge (host-checked)
   int tma;      // bf16x3 kernel: 0 = 16B cp.async groups, 1 = TMA tiled map, 2 = TMA im2col map,
-                //   3 = TMA im2col with C < 32: one box per filter tap, chunk-major raw layout
+                //   3 = TMA im2col with C < 32: one box per filter tap, chunk-major raw layout,
+                //   4 = wgrad tap view (C < 32): tiled maps over k = (n, p, q padded to wv_q) --
+                //       A = dy as {kout, q, n*p}, B = the zero-padded input as {s*c, q, r, p, n}
   int rows_box; // bf16x3 kernel: rows of this operand one CTA loads per tile (128, or 64 for the
                 //   B half of a CTA pair)
 };
@@ -81,6 +83,8 @@ struct GemmParams {
   int mn_seg;       // bf16x3: rows per segment of the MN-major raw B layout (128, or C for wgrad)
   PhaseInfo ph;     // bf16x3: strided dgrad phase (ph.on == 0 otherwise)
   int chunk_stages; // bf16x3: MMA stages accumulated in TMEM before a flush to fp32 memory
+  int n_pitch;      // output columns per n-tile (BN, or R-segments x S*C for the wgrad tap view)
+  int wv_q;         // wgrad tap view: output-row length padded to a multiple of 32 (0 = off)
   unsigned long long* dbg_t;  // debug: per-CTA wait-time counters of the bf16x3 pipeline roles (nullptr = off)
   float* dbg_a;     // debug: bf16x3 A-split dumps the raw A operand [M][Kpad] here (nullptr = off)
   float* dbg_b;     // debug: bf16x3 B-split dumps the raw B operand [N][Kpad]
