@@ -380,7 +380,8 @@ bool use_phases(int variant, const monet_conv_desc* d) {
 // one TMA box per operand -- dy {kout, 32 q, 1} and, over a zero-padded copy of
 // the input in the workspace, {S*C, 32 q, R-segments} with overlapping q / s
 // strides.  An n-tile covers floor(128 / (S*C)) filter rows (112 columns for the
-// stem).  Replaces the 16B cp.async gather (per-group divisions) for these layers.
+// stem).  Replaces the 16B cp.async gather (per-group divisions) for these layers
+// when the reduction is long (>= 32K output pixels).
 struct WView {
   bool on;
   int qpad, n_pitch;
@@ -392,6 +393,8 @@ WView wgrad_view(int variant, const monet_conv_desc* d) {
   WView v{};
   if (!uses_bx3(variant) || variant == MONET_CONV_PAIR || is_pointwise(d) || d->c >= 32 || d->s * d->c > 128)
     return v;
+  // below 32K output pixels the gather is cheap and the padded copy is not worth its workspace
+  if ((long long)d->n * d->p * d->q < (1 << 15)) return v;
   v.on = true;
   v.qpad = (d->q + 31) / 32 * 32;
   v.n_pitch = (128 / (d->s * d->c)) * d->s * d->c;

@@ -51,8 +51,8 @@ CONV_CASES = [
     (2, 10, 10, 64, 64, 3, 3, 1, 1),     # wgrad row tile spans two taps (bulk segments)
     (1, 6, 6, 192, 64, 3, 3, 1, 1),      # C % 128 != 0: wgrad falls back to 16B groups
     (2, 12, 12, 64, 32, 3, 3, 2, 1),     # stride-2 dgrad gather, K = 32
-    (2, 20, 40, 4, 160, 3, 3, 1, 1),     # wgrad tap view: two m-tiles, q padded 40 -> 64
-    (2, 23, 37, 8, 64, 5, 5, 2, 2),      # wgrad tap view: 3 filter rows (120 columns) per n-tile
+    (21, 40, 40, 4, 160, 3, 3, 1, 1),    # wgrad tap view (>= 32K pixels): two m-tiles, q padded 40 -> 64
+    (2, 350, 202, 8, 64, 5, 5, 2, 2),    # wgrad tap view: 3 filter rows (120 columns) per n-tile, Q = 101
 ]
 
 
