@@ -70,6 +70,24 @@ int monet_conv_dgrad(int variant, const monet_conv_desc* d, const float* dy, con
 int monet_conv_wgrad(int variant, const monet_conv_desc* d, const float* x, const float* dy, float* dw,
                      int accumulate, void* ws, size_t ws_bytes, void* stream);
 
+/* conv with a per-output-channel bias (VGG-style convs): the bias is added in the
+ * GEMM epilogue (split-K: in the partial-sum reduce).  Its gradient is
+ * monet_bias_grad over dy ([rows = n*p*q, k]); scratch = monet_bn_scratch_bytes(rows, k). */
+int monet_conv_fwd_bias(int variant, const monet_conv_desc* d, const float* x, const float* w, const float* bias,
+                        float* y, void* ws, size_t ws_bytes, void* stream);
+int monet_bias_grad(const float* dy, float* db, int64_t rows, int c, int accumulate, void* scratch, void* stream);
+
+/* --- dropout (VGG / MobileNet-V2 / GoogleNet classifiers) ------------------------
+ * keep(i) <=> splitmix64(seed*0x9E3779B97F4A7C15 + salt*0xD1B54A32D192ED03 + i) >> 40 >= floor(p*2^24),
+ * i = element index in NHWC order; y = keep ? x / (1-p) : 0.  The mask is never stored:
+ * backward and recomputes regenerate it from *seed (device memory, read at run time),
+ * which monet_seed_advance increments once per training step. */
+int monet_dropout_fwd(const float* x, float* y, int64_t n, float p, const unsigned long long* seed, uint64_t salt,
+                      void* stream);
+int monet_dropout_bwd(const float* dy, float* dx, int64_t n, float p, const unsigned long long* seed, uint64_t salt,
+                      int accumulate, void* stream);
+int monet_seed_advance(unsigned long long* seed, void* stream);
+
 /* --- dense layer (fc) -------------------------------------------------------- */
 size_t monet_linear_ws_bytes(int variant, int pass, int n, int in_f, int out_f);
 int monet_linear_fwd(int variant, const float* x, const float* w, const float* b, float* y, int n, int in_f,

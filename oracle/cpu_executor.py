@@ -20,6 +20,7 @@ import torch
 import torch.nn.functional as F
 
 from .bitmask import pack_sign_mask, unpack_sign_mask
+from .dropout import keep_mask
 
 
 def _nchw(t):
@@ -46,6 +47,7 @@ class CpuState:
                         for op in net.ops if op.kind in ("bn", "bnrelu")}
         self.saved = {}
         self.grads = {}
+        self.seed = 0  # dropout step seed: the engine's device counter, advanced once per step
 
 
 def _bn_stats(x, eps):
@@ -108,7 +110,9 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
             y[:, :images.shape[1]] = images.to(dt)
         elif op.kind == "conv":
             a = op.attrs
-            y = F.conv2d(xs[0], P[(op.id, "weight")], stride=a["stride"], padding=a["pad"])
+            y = F.conv2d(xs[0], P[(op.id, "weight")], P.get((op.id, "bias")), stride=a["stride"], padding=a["pad"])
+        elif op.kind == "dropout":
+            y = xs[0] * _dropout_scale(op, xs[0], state.seed)
         elif op.kind in ("bn", "bnrelu"):
             g, b = P[(op.id, "weight")], P[(op.id, "bias")]
             if mode == "forward":
@@ -127,7 +131,7 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
             x = xs[0]
             y = torch.where(x > 0, x, torch.zeros_like(x))
             if want_int:
-                extra = pack_sign_mask(x.permute(0, 2, 3, 1).numpy())
+                extra = pack_sign_mask((x.permute(0, 2, 3, 1) if x.dim() == 4 else x).numpy())
         elif op.kind == "add":
             y = xs[0] + xs[1]
         elif op.kind == "addrelu":
@@ -141,7 +145,7 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
         elif op.kind == "avgpool":
             y = xs[0].mean(dim=(2, 3))
         elif op.kind == "fc":
-            y = F.linear(xs[0], P[(op.id, "weight")], P[(op.id, "bias")])
+            y = F.linear(_flat_nhwc(xs[0]), P[(op.id, "weight")], P[(op.id, "bias")])
         elif op.kind == "xent":
             y = F.cross_entropy(xs[0], labels.long())
             loss_val = float(y)
@@ -169,6 +173,10 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
             if net.grad_bytes(net.op(j)) > 0:
                 put_grad(j, torch.nn.grad.conv2d_input(x.shape, w, dy, a["stride"], a["pad"]), created)
             state.grads[(op.id, "weight")] = torch.nn.grad.conv2d_weight(x, w.shape, dy, a["stride"], a["pad"])
+            if (op.id, "bias") in P:
+                state.grads[(op.id, "bias")] = dy.sum(dim=(0, 2, 3))
+        elif op.kind == "dropout":
+            put_grad(op.deps[0], dy * _dropout_scale(op, dy, state.seed), created)
         elif op.kind in ("bn", "bnrelu"):
             j = op.deps[0]
             g, b = P[(op.id, "weight")], P[(op.id, "bias")]
@@ -190,9 +198,11 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
         elif op.kind == "relu":
             j = op.deps[0]
             if impl == "bwd-mask":
-                bits = unpack_sign_mask(x_of(net.intermediate_of[op.id]), dy.numel())
-                keep = torch.from_numpy(bits).view(dy.shape[0], dy.shape[2], dy.shape[3], dy.shape[1])
-                keep = keep.permute(0, 3, 1, 2)
+                bits = torch.from_numpy(unpack_sign_mask(x_of(net.intermediate_of[op.id]), dy.numel()))
+                if dy.dim() == 4:
+                    keep = bits.view(dy.shape[0], dy.shape[2], dy.shape[3], dy.shape[1]).permute(0, 3, 1, 2)
+                else:
+                    keep = bits.view(dy.shape)
             elif impl == "bwd-out":
                 keep = x_of(op.id) > 0
             else:
@@ -226,8 +236,12 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
         elif op.kind == "fc":
             j = op.deps[0]
             x = x_of(j)
-            put_grad(j, dy @ P[(op.id, "weight")], created)
-            state.grads[(op.id, "weight")] = dy.t() @ x
+            dx = dy @ P[(op.id, "weight")]
+            if x.dim() == 4:  # back to NCHW from the NHWC flattening
+                n, c, h, w = x.shape
+                dx = dx.view(n, h, w, c).permute(0, 3, 1, 2).contiguous()
+            put_grad(j, dx, created)
+            state.grads[(op.id, "weight")] = dy.t() @ _flat_nhwc(x)
             state.grads[(op.id, "bias")] = dy.sum(dim=0)
         elif op.kind == "xent":
             j = op.deps[0]
@@ -296,6 +310,7 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
         release(len(entries))
         carried = keep
 
+    state.seed += 1
     # ---------------------------------------------------------------- SGD
     for key, w in P.items():
         g = state.grads[key]
@@ -304,6 +319,25 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
         buf.mul_(state.momentum).add_(d)
         w.sub_(state.lr * buf)
     return loss_val
+
+
+def _flat_nhwc(x):
+    """fc input flattened in the engine's NHWC element order (2-D inputs unchanged)."""
+    return x.permute(0, 2, 3, 1).reshape(x.shape[0], -1) if x.dim() == 4 else x
+
+
+def _dropout_scale(op, like, seed):
+    """keep / (1 - p) as a tensor shaped like ``like`` (mask drawn over NHWC order)."""
+    import numpy as np
+
+    p = float(np.float32(op.attrs["p"]))
+    scale = np.float32(1.0 / (1.0 - p))
+    keep = torch.from_numpy(keep_mask(like.numel(), p, seed, op.id))
+    s = torch.where(keep, torch.tensor(scale, dtype=like.dtype), torch.tensor(0.0, dtype=like.dtype))
+    if like.dim() == 4:
+        n, c, h, w = like.shape
+        return s.view(n, h, w, c).permute(0, 3, 1, 2)
+    return s.view(like.shape)
 
 
 def _bwd_deps(net, k, impl):

@@ -33,6 +33,11 @@ SIGNATURES = {
     "monet_conv_fwd": (_i32, [_i32, _PCONV, _vp, _vp, _vp, _vp, _sz, _vp]),
     "monet_conv_dgrad": (_i32, [_i32, _PCONV, _vp, _vp, _vp, _i32, _vp, _sz, _vp]),
     "monet_conv_wgrad": (_i32, [_i32, _PCONV, _vp, _vp, _vp, _i32, _vp, _sz, _vp]),
+    "monet_conv_fwd_bias": (_i32, [_i32, _PCONV, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "monet_bias_grad": (_i32, [_vp, _vp, _i64, _i32, _i32, _vp, _vp]),
+    "monet_dropout_fwd": (_i32, [_vp, _vp, _i64, _f32, _vp, C.c_uint64, _vp]),
+    "monet_dropout_bwd": (_i32, [_vp, _vp, _i64, _f32, _vp, C.c_uint64, _i32, _vp]),
+    "monet_seed_advance": (_i32, [_vp, _vp]),
     "monet_linear_ws_bytes": (_sz, [_i32, _i32, _i32, _i32, _i32]),
     "monet_linear_fwd": (_i32, [_i32, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _sz, _vp]),
     "monet_linear_bwd": (_i32, [_i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _i32, _i32, _i32, _vp, _sz, _vp]),

@@ -26,9 +26,12 @@ def analytic_cost(net, op, pass_, name) -> int:
         if pass_ == "fwd":
             return _ns(flops, 4.0 * (x.numel + n))
         passes = 1 if net.op(op.deps[0]).kind == "input" else 2
-        return _ns(passes * flops, 8.0 * (x.numel + n), launches=3)
+        bias = 4.0 * n if "bias" in op.params else 0.0  # bias gradient: one more read of dy
+        return _ns(passes * flops, 8.0 * (x.numel + n) + bias, launches=3)
+    if op.kind == "dropout":  # r4 w4, mask regenerated (never stored)
+        return _ns(nbytes=8.0 * n)
     if op.kind == "fc":
-        fi = net.op(op.deps[0]).shape[1]
+        fi = net.fc_dims(op)[1]
         flops = 2.0 * n * fi
         return _ns(flops if pass_ == "fwd" else 2 * flops, launches=2 if pass_ == "fwd" else 4)
     if op.kind == "relu":

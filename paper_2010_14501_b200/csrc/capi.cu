@@ -281,7 +281,8 @@ int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_b
   if (e) return e;
   if (p.splits > 1) {
     long long total = (long long)p.M * p.N;
-    splitk_reduce_kernel<<<ew_blocks(total), kEwThreads, 0, st>>>(p.ws, p.c, p.M, p.N, p.ldc, p.splits, accumulate);
+    splitk_reduce_kernel<<<ew_blocks(total), kEwThreads, 0, st>>>(p.ws, p.c, p.M, p.N, p.ldc, p.splits, accumulate,
+                                                                  p.bias);
   }
   return last_error();
 }
@@ -510,6 +511,57 @@ int monet_conv_fwd(int variant, const monet_conv_desc* d, const float* x, const 
                    size_t ws_bytes, void* stream) {
   if (int e = check_desc(d)) return e;
   return launch_gemm(conv_params(MONET_PASS_FWD, d, x, w, y), variant, 0, ws, ws_bytes, S(stream));
+}
+
+static int bn_blocks(int64_t rows);
+
+int monet_conv_fwd_bias(int variant, const monet_conv_desc* d, const float* x, const float* w, const float* bias,
+                        float* y, void* ws, size_t ws_bytes, void* stream) {
+  if (int e = check_desc(d)) return e;
+  GemmParams p = conv_params(MONET_PASS_FWD, d, x, w, y);
+  if (uses_bx3(variant)) {  // bias added in the epilogue (or the split-K reduce)
+    p.bias = bias;
+    return launch_gemm(p, variant, 0, ws, ws_bytes, S(stream));
+  }
+  const long long tot = (long long)p.M * p.N;
+  bias_fill_kernel<<<(int)((tot + 255) / 256), 256, 0, S(stream)>>>(y, bias, p.M, p.N);
+  return launch_gemm(p, variant, 1, ws, ws_bytes, S(stream));
+}
+
+int monet_bias_grad(const float* dy, float* db, int64_t rows, int c, int accumulate, void* scratch, void* stream) {
+  if (c % 4 || rows <= 0) return -(int)cudaErrorInvalidValue;
+  cudaStream_t st = S(stream);
+  float* ws = static_cast<float*>(scratch);
+  const int nb = bn_blocks(rows);
+  bn_reduce_kernel<<<nb, kEwThreads, 0, st>>>(0, dy, nullptr, nullptr, nullptr, rows, c, ws);
+  chan_sum_finalize_kernel<<<(c + 7) / 8, 256, 0, st>>>(ws, nb, c, db, accumulate);
+  return last_error();
+}
+
+// thr = floor(p * 2^24); p in [0, 1)
+static unsigned dropout_thr(float p) { return (unsigned)((double)p * 16777216.0); }
+
+int monet_dropout_fwd(const float* x, float* y, int64_t n, float p, const unsigned long long* seed, uint64_t salt,
+                      void* stream) {
+  if (!(p >= 0.f && p < 1.f) || n < 0) return -(int)cudaErrorInvalidValue;
+  if (n == 0) return 0;
+  dropout_kernel<<<ew_blocks(n), kEwThreads, 0, S(stream)>>>(x, y, n, dropout_thr(p), (float)(1.0 / (1.0 - p)),
+                                                              seed, salt, 0);
+  return last_error();
+}
+
+int monet_dropout_bwd(const float* dy, float* dx, int64_t n, float p, const unsigned long long* seed, uint64_t salt,
+                      int accumulate, void* stream) {
+  if (!(p >= 0.f && p < 1.f) || n < 0) return -(int)cudaErrorInvalidValue;
+  if (n == 0) return 0;
+  dropout_kernel<<<ew_blocks(n), kEwThreads, 0, S(stream)>>>(dy, dx, n, dropout_thr(p), (float)(1.0 / (1.0 - p)),
+                                                              seed, salt, accumulate);
+  return last_error();
+}
+
+int monet_seed_advance(unsigned long long* seed, void* stream) {
+  seed_advance_kernel<<<1, 1, 0, S(stream)>>>(seed);
+  return last_error();
 }
 
 int monet_conv_dgrad(int variant, const monet_conv_desc* d, const float* dy, const float* w, float* dx,

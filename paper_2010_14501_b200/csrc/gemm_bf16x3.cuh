@@ -703,6 +703,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
         // reductions: no read-back latency, and one thread owns each element,
         // so the order of the adds is fixed (deterministic)
         const bool add_old = chunk > 0 || p.epi == EPI_ACCUM;
+        const bool add_bias = p.bias != nullptr && chunk == 0 && p.epi == EPI_STORE;
         TWAIT(6, mbar_wait(&tfull[acc], acc_phase));
         tc_fence_after();
         for (int cc = 0; cc < NB / 32; ++cc) {
@@ -720,6 +721,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
               ld = p.ldc;
             }
             const int ncols = min(min(32, p.N - n0), p.n_pitch - cc * 32);
+            if (add_bias) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] += j < ncols ? __ldg(p.bias + n0 + j) : 0.f;
+            }
             const bool vec = (ncols == 32) && ((ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
             if (vec) {
 #pragma unroll

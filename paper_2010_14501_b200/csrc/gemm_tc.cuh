@@ -85,6 +85,7 @@ struct GemmParams {
   int chunk_stages; // bf16x3: MMA stages accumulated in TMEM before a flush to fp32 memory
   int n_pitch;      // output columns per n-tile (BN, or R-segments x S*C for the wgrad tap view)
   int wv_q;         // wgrad tap view: output-row length padded to a multiple of 32 (0 = off)
+  const float* bias;  // bf16x3 EPI_STORE / split-K reduce: per-column bias added to the output (nullptr = none)
   unsigned long long* dbg_t;  // debug: per-CTA wait-time counters of the bf16x3 pipeline roles (nullptr = off)
   float* dbg_a;     // debug: bf16x3 A-split dumps the raw A operand [M][Kpad] here (nullptr = off)
   float* dbg_b;     // debug: bf16x3 B-split dumps the raw B operand [N][Kpad]
@@ -564,13 +565,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32_kernel(const GemmParams
 
 // Deterministic split-K reduction: out[m, n] (=|+=) sum_{s=0..S-1} ws[s, m, n].
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, float* __restrict__ out, int M, int N,
-                                     long long ldc, int splits, int accumulate) {
+                                     long long ldc, int splits, int accumulate, const float* __restrict__ bias) {
   const long long total = (long long)M * N;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     float s = 0.f;
     for (int k = 0; k < splits; ++k) s += ws[(long long)k * total + i];
     const long long m = i / N, n = i - m * N;
+    if (bias) s += bias[n];
     float* o = out + m * ldc + n;
     *o = accumulate ? (*o + s) : s;
   }

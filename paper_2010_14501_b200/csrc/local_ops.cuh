@@ -718,6 +718,43 @@ __global__ void bias_fill_kernel(float* y, const float* __restrict__ b, int N, i
   if (i < (long long)N * K) y[i] = b[i % K];
 }
 
+// per-channel sums of the block partials bn_reduce (mode 0) left in ws: the conv
+// bias gradient db[c] = sum over rows of dy[., c] (fixed order, fp64 combine)
+__global__ void chan_sum_finalize_kernel(const float* __restrict__ ws, int nblocks, int C, float* db, int accumulate) {
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (c >= C) return;
+  double s1, s2;
+  bn_warp_sum(ws, nblocks, C, c, s1, s2);
+  if ((threadIdx.x & 31) == 0) db[c] = accumulate ? db[c] + (float)s1 : (float)s1;
+}
+
+// ---------------------------------------------------------------- dropout
+// Keep-mask from a counter-based hash (splitmix64 finalizer) of (step seed,
+// op salt, element index in the engine's NHWC order): nothing is stored, the
+// backward and every recompute regenerate the same mask.  keep <=> the top 24
+// bits of the hash >= thr, thr = floor(p * 2^24).  oracle/dropout.py restates it.
+MONET_DEV bool dropout_keep(unsigned long long seed, unsigned long long salt, unsigned long long i, unsigned thr) {
+  unsigned long long z = seed * 0x9E3779B97F4A7C15ull + salt * 0xD1B54A32D192ED03ull + i;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return (unsigned)(z >> 40) >= thr;
+}
+
+// y = keep ? x * scale : 0   (backward: same with dy -> dx, optional accumulate)
+__global__ void dropout_kernel(const float* __restrict__ x, float* y, long long n, unsigned thr, float scale,
+                               const unsigned long long* __restrict__ seed_ptr, unsigned long long salt,
+                               int accumulate) {
+  const unsigned long long seed = *seed_ptr;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float v = dropout_keep(seed, salt, (unsigned long long)i, thr) ? x[i] * scale : 0.f;
+    y[i] = accumulate ? y[i] + v : v;
+  }
+}
+
+__global__ void seed_advance_kernel(unsigned long long* seed) { *seed += 1; }
+
 // db[k] = sum_n dy[n, k]  (fixed order)
 __global__ void col_sum_kernel(const float* __restrict__ dy, float* db, int N, int K) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;

@@ -116,6 +116,12 @@ class Runtime:
         self.labels = self.fixed[off:off + nb].view(torch.int32)
         self.consts = f32("consts", 4)
         self.consts[0] = 1.0
+        # dropout step seed (uint64 at consts + 8): read by the kernels at run time,
+        # advanced on the device after every optimizer step
+        off = self.region["consts"][0]
+        self.seed = self.fixed[off + 8:off + 16].view(torch.int64)
+        self.seed.zero_()
+        self.seed_ptr = self.fixed.data_ptr() + off + 8
         self.scratch_ptr = self.fixed.data_ptr() + self.region["scratch"][0]
         self.pview, self.gview = {}, {}
         pos = 0
@@ -256,8 +262,16 @@ class Runtime:
             elif op.kind == "conv":
                 d = net.conv_desc(op)
                 v = _native.CONV_VARIANTS[s.impl]
-                out.append(("k", lib.monet_conv_fwd, (v, C.byref(d), xs[0], self.pview[(op.id, "weight")].data_ptr(),
-                                                      y, ws, s.workspace, None), d))
+                wt = self.pview[(op.id, "weight")].data_ptr()
+                if "bias" in op.params:
+                    out.append(("k", lib.monet_conv_fwd_bias, (v, C.byref(d), xs[0], wt,
+                                                               self.pview[(op.id, "bias")].data_ptr(), y, ws,
+                                                               s.workspace, None), d))
+                else:
+                    out.append(("k", lib.monet_conv_fwd, (v, C.byref(d), xs[0], wt, y, ws, s.workspace, None), d))
+            elif op.kind == "dropout":
+                out.append(("k", lib.monet_dropout_fwd, (xs[0], y, op.numel, C.c_float(op.attrs["p"]),
+                                                         self.seed_ptr, op.id, None)))
             elif op.kind == "bn":
                 c = op.shape[-1]
                 rows = op.numel // c
@@ -299,7 +313,7 @@ class Runtime:
                 n, h, w, c = net.op(op.deps[0]).shape
                 out.append(("k", lib.monet_avgpool_fwd, (xs[0], y, n, h * w, c, None)))
             elif op.kind == "fc":
-                n, fi = net.op(op.deps[0]).shape
+                n, fi = net.fc_dims(op)
                 fo = op.shape[1]
                 v = 1 if s.impl == "gemm-splitk" else 0
                 out.append(("k", lib.monet_linear_fwd,
@@ -342,6 +356,14 @@ class Runtime:
             out.append(("k", lib.monet_conv_wgrad, (v, C.byref(d), P(("in", j)), dy,
                                                     self.gview[(op.id, "weight")].data_ptr(), 0, ws,
                                                     s.workspace, None), d))
+            if "bias" in op.params:
+                out.append(("k", lib.monet_bias_grad, (dy, self.gview[(op.id, "bias")].data_ptr(),
+                                                       op.numel // op.shape[-1], op.shape[-1], 0, self.scratch_ptr,
+                                                       None)))
+        elif op.kind == "dropout":
+            j = op.deps[0]
+            out.append(("k", lib.monet_dropout_bwd, (dy, P(("g", j)), op.numel, C.c_float(op.attrs["p"]),
+                                                     self.seed_ptr, op.id, acc(j), None)))
         elif op.kind == "bn":
             c = op.shape[-1]
             rows = op.numel // c
@@ -400,7 +422,7 @@ class Runtime:
             out.append(("k", lib.monet_avgpool_bwd, (dy, P(("g", j)), n, h * w, c, acc(j), None)))
         elif op.kind == "fc":
             j = op.deps[0]
-            n, fi = net.op(j).shape
+            n, fi = net.fc_dims(op)
             fo = op.shape[1]
             v = 1 if s.impl == "gemm-splitk" else 0
             out.append(("k", lib.monet_linear_bwd,
@@ -423,6 +445,8 @@ class Runtime:
                       (self.params.data_ptr(), self.grads.data_ptr(), self.mom.data_ptr(), self.params.numel(),
                        C.c_float(self.lr), C.c_float(self.momentum), C.c_float(self.weight_decay),
                        C.c_float(self.grad_scale), 0, None)))
+        if any(op.kind == "dropout" for op in self.net.ops):
+            calls.append(("k", self.lib.dll.monet_seed_advance, (self.seed_ptr, None)))
         return calls
 
     # ------------------------------------------------------------ running

@@ -162,7 +162,7 @@ def _families(g: Graph, kind_of) -> dict:
             kinds = kinds | {"relu-join"}
         return {x for x in ids if kind_of(x) in kinds}
 
-    base = {"input", "maxpool", "avgpool", "fc", "xent"}
+    base = {"input", "maxpool", "avgpool", "fc", "xent", "dropout"}
     fam["all"] = set(ids)
     fam["conv+relu+mask"] = pick(base | {"conv", "relu", "mask", "idx"})
     fam["conv+mask"] = pick(base | {"conv", "mask", "idx"})

@@ -73,8 +73,17 @@ def _conv_calls(bx: _Bench, net, op, variant: str):
     ws_b = lib.monet_conv_ws_bytes(v, 3, C.byref(d))
     ws = bx.buf(max(ws_f, ws_b))
     need_dx = xin.kind != "input"
+    bias = "bias" in op.params
+    if bias:
+        b, db = bx.buf(4 * op.shape[3]), bx.buf(4 * op.shape[3])
+        rows = op.numel // op.shape[3]
+        scratch = bx.buf(lib.monet_bn_scratch_bytes(rows, op.shape[3]))
 
     def fwd():
+        if bias:
+            bx.check(lib.monet_conv_fwd_bias(v, C.byref(d), x.data_ptr(), w.data_ptr(), b.data_ptr(), y.data_ptr(),
+                                             ws.data_ptr(), ws_f, sp))
+            return
         bx.check(lib.monet_conv_fwd(v, C.byref(d), x.data_ptr(), w.data_ptr(), y.data_ptr(), ws.data_ptr(), ws_f, sp))
 
     def bwd():
@@ -83,6 +92,8 @@ def _conv_calls(bx: _Bench, net, op, variant: str):
                                           ws.data_ptr(), ws_b, sp))
         bx.check(lib.monet_conv_wgrad(v, C.byref(d), x.data_ptr(), dy.data_ptr(), dw.data_ptr(), 0, ws.data_ptr(),
                                       ws_b, sp))
+        if bias:
+            bx.check(lib.monet_bias_grad(dy.data_ptr(), db.data_ptr(), rows, op.shape[3], 0, scratch.data_ptr(), sp))
     return fwd, bwd
 
 
@@ -168,8 +179,15 @@ def _local_calls(bx: _Bench, net, op):
         out[("fwd", "avgpool")] = lambda: bx.check(lib.monet_avgpool_fwd(x.data_ptr(), y.data_ptr(), nb, h * w, c, sp))
         out[("bwd", "bwd")] = lambda: bx.check(lib.monet_avgpool_bwd(dy.data_ptr(), dx.data_ptr(), nb, h * w, c, 0,
                                                                        sp))
+    elif kind == "dropout":
+        seed = torch.zeros(1, dtype=torch.int64, device=bx.dev)
+        pf = C.c_float(op.attrs["p"])
+        out[("fwd", "dropout")] = lambda: bx.check(lib.monet_dropout_fwd(x.data_ptr(), y.data_ptr(), n, pf,
+                                                                          seed.data_ptr(), op.id, sp))
+        out[("bwd", "bwd-rng")] = lambda: bx.check(lib.monet_dropout_bwd(dy.data_ptr(), dx.data_ptr(), n, pf,
+                                                                          seed.data_ptr(), op.id, 0, sp))
     elif kind == "fc":
-        nb, fi = xin.shape
+        nb, fi = net.fc_dims(op)
         fo = op.shape[1]
         wgt, bias, dw, dbias = bx.buf(4 * fi * fo), bx.buf(4 * fo), bx.buf(4 * fi * fo), bx.buf(4 * fo)
         for name, v in (("gemm", 0), ("gemm-splitk", 1)):

@@ -121,8 +121,8 @@ class Network:
         lib = _native.lib()
         s = 0
         for op in self.ops:
-            if op.kind in ("bn", "bnrelu"):
-                rows = op.numel // op.shape[-1]
+            if op.kind in ("bn", "bnrelu") or (op.kind == "conv" and "bias" in op.params):
+                rows = op.numel // op.shape[-1]  # conv bias gradient: per-channel sum of dy
                 s = max(s, lib.bn_scratch_bytes(rows, op.shape[-1]))
         s = max(s, lib.xent_scratch_bytes(self.batch))
         return (s + 255) // 256 * 256
@@ -164,6 +164,11 @@ class Network:
         return {"format": 1, "params_bytes": self.params_bytes(), "nodes": nodes,
                 "backward": backward, "intermediates": inters}
 
+    def fc_dims(self, op: Op):
+        """(rows, in_features) of an fc op; a 4-D input is read flattened (NHWC order)."""
+        x = self.op(op.deps[0])
+        return x.shape[0], x.numel // x.shape[0]
+
     def variants(self, op: Op):
         """(forward variants, backward variants) as (name, workspace_bytes, deps) tuples."""
         lib = _native.lib()
@@ -182,7 +187,7 @@ class Network:
             if self.pair_variants:
                 bwd.append(("pair", lib.conv_ws_bytes(4, 3, d), x))
         elif op.kind == "fc":
-            n, fi = self.op(op.deps[0]).shape
+            n, fi = self.fc_dims(op)
             fo = op.shape[1]
             fwd.append(("gemm", 0))
             ws = lib.linear_ws_bytes(1, 0, n, fi, fo)
@@ -212,6 +217,9 @@ class Network:
         elif op.kind in ("add", "avgpool"):
             fwd.append((op.kind, 0))
             bwd.append(("bwd", 0, []))
+        elif op.kind == "dropout":  # backward reads dy only (mask regenerated)
+            fwd.append(("dropout", 0))
+            bwd.append(("bwd-rng", 0, []))
         elif op.kind == "xent":
             fwd.append(("xent", 0))
             bwd.append(("bwd", 0, x))
@@ -274,6 +282,7 @@ BWD_IMPLS = {
     "addrelu": [("bwd-out", "output"), ("bwd-in", "input")],
     "relu": [("bwd-in", "input"), ("bwd-out", "output"), ("bwd-mask", "intermediate")],
     "maxpool": [("bwd-in", "input"), ("bwd-idx", "intermediate")],
+    "dropout": [("bwd-rng", "input")],  # catalog deps []: the keep-mask is regenerated from the step seed
     "add": [("bwd", "input")],
     "avgpool": [("bwd", "input")],
     "xent": [("bwd", "input")],
@@ -347,8 +356,8 @@ def trace_graph(model: torch.nn.Module, example_input: torch.Tensor, num_classes
             x = ops[src - 1]
             nid = len(ops) + 1
             if isinstance(mod, torch.nn.Conv2d):
-                if mod.groups != 1 or mod.bias is not None or _pair(mod.dilation) != 1:
-                    raise NotImplementedError(f"{node.target}: only dense bias-free convs")
+                if mod.groups != 1 or _pair(mod.dilation) != 1:
+                    raise NotImplementedError(f"{node.target}: only dense, undilated convs")
                 r, s = mod.kernel_size
                 st, pd = _pair(mod.stride), _pair(mod.padding)
                 _, hh, ww, cin = x.shape
@@ -357,8 +366,11 @@ def trace_graph(model: torch.nn.Module, example_input: torch.Tensor, num_classes
                 wt = mod.weight.detach().float().permute(0, 2, 3, 1).contiguous()  # KRSC
                 if wt.shape[3] != cin:
                     wt = torch.nn.functional.pad(wt, (0, cin - wt.shape[3]))
+                prm = {"weight": wt}
+                if mod.bias is not None:  # VGG-style conv bias: added in the GEMM epilogue
+                    prm["bias"] = mod.bias.detach().float().clone()
                 ops.append(Op(nid, "conv", (src,), (n, p, q, mod.out_channels),
-                              {"r": r, "s": s, "stride": st, "pad": pd}, {"weight": wt}, node.target))
+                              {"r": r, "s": s, "stride": st, "pad": pd}, prm, node.target))
             elif isinstance(mod, torch.nn.BatchNorm2d):
                 ops.append(Op(nid, "bn", (src,), x.shape, {"eps": mod.eps, "momentum": mod.momentum},
                               {"weight": mod.weight.detach().float().clone(),
@@ -377,11 +389,28 @@ def trace_graph(model: torch.nn.Module, example_input: torch.Tensor, num_classes
                 ops.append(Op(nid, "maxpool", (src,), (n, p, q, cc),
                               {"r": r, "s": r, "stride": st, "pad": pd}, name=node.target))
             elif isinstance(mod, torch.nn.AdaptiveAvgPool2d):
+                osz = mod.output_size if isinstance(mod.output_size, tuple) else (mod.output_size,) * 2
+                if len(x.shape) == 4 and tuple(osz) == tuple(x.shape[1:3]):
+                    where[node.name] = src  # VGG's (7, 7) pool on a 7 x 7 map is the identity
+                    continue
+                if tuple(osz) != (1, 1):
+                    raise NotImplementedError(f"{node.target}: adaptive pool to {osz}")
                 ops.append(Op(nid, "avgpool", (src,), (n, x.shape[3]), name=node.target))
+            elif isinstance(mod, torch.nn.Flatten):
+                where[node.name] = src  # fc reads a 4-D input flattened in the engine's NHWC order
+                continue
+            elif isinstance(mod, torch.nn.Dropout):
+                if mod.p <= 0.0:
+                    where[node.name] = src
+                    continue
+                ops.append(Op(nid, "dropout", (src,), x.shape, {"p": float(mod.p)}, name=node.target))
             elif isinstance(mod, torch.nn.Linear):
+                wt = mod.weight.detach().float().clone()
+                if len(x.shape) == 4:  # torch flattens (c, h, w); the engine's activations are (h, w, c)
+                    _, hh, ww, cc = x.shape
+                    wt = wt.view(-1, cc, hh, ww).permute(0, 2, 3, 1).reshape(wt.shape[0], -1).contiguous()
                 ops.append(Op(nid, "fc", (src,), (n, mod.out_features), {},
-                              {"weight": mod.weight.detach().float().clone(),
-                               "bias": mod.bias.detach().float().clone()}, node.target))
+                              {"weight": wt, "bias": mod.bias.detach().float().clone()}, node.target))
             else:
                 raise NotImplementedError(f"module {type(mod).__name__} at {node.target}")
             where[node.name] = nid

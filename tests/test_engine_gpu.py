@@ -139,3 +139,42 @@ def test_invalid_schedule_raises(cuda, r18):
     rt = Runtime(net)
     with pytest.raises(M.SimulationError):
         rt.plan(M.schedule_from_doc(doc), g, cat)
+
+
+def test_vgg_style_engine(cuda):
+    """VGG-family ops (biased convs, identity adaptive pool, flatten -> fc, dropout)
+    under a recompute schedule: ledger = simulate(), every recompute bit-identical
+    (dropout regenerates its mask), loss / weights / gradients = CPU oracle."""
+    from nets import SmallVGG
+
+    torch.manual_seed(0)
+    net = M.trace_graph(SmallVGG(), torch.empty(4, 3, 32, 32, device="meta"), 10)
+    assert any(op.kind == "dropout" for op in net.ops)
+    g = M.load_graph(net.graph_doc())
+    cat = M.load_catalog(net.catalog_doc(), g)
+    se = M.store_everything_schedule(g, cat)
+    act = M.simulate(se, g, cat).peak_memory - g.params_bytes
+    from paper_2010_14501_b200.planner import plan_schedule
+    sched, _ = plan_schedule(g, cat, g.params_bytes + int(0.6 * act), kinds=net.storable_kinds())
+    assert sched is not None and any(s.recompute for s in sched.stages)
+    gen = torch.Generator().manual_seed(0)
+    x = torch.randn(4, 3, 32, 32, generator=gen)
+    y = torch.randint(0, 10, (4,), generator=gen)
+    rt = Runtime(net)
+    rt.set_batch(x.to(cuda), y.to(cuda))
+    plan = rt.plan(sched, g, cat)
+    assert M.trace_report(plan.trace) == M.trace_report(M.simulate(sched, g, cat))
+    acts, mismatched = capture(rt, plan)  # one step at dropout seed 0
+    assert not mismatched
+    doc = M.schedule_to_doc(sched)
+    loss = run_step(CpuState(net), doc, x, y)
+    assert abs(rt.loss_value() - loss) <= REL * abs(loss)
+    st = CpuState(net)
+    run_step(st, doc, x, y, forced=acts)
+    for (nid, pname), v in params_nhwc(st).items():
+        assert rel(rt.pview[(nid, pname)].view(v.shape), v) <= REL, (net.op(nid).name, pname)
+        gg = st.grads[(nid, pname)]
+        if net.op(nid).kind == "conv" and pname == "weight":
+            gg = gg.permute(0, 2, 3, 1)
+        assert rel(rt.gview[(nid, pname)].view(gg.shape), gg) <= REL, (net.op(nid).name, pname, "grad")
+    assert int(rt.seed.item()) == 1  # advanced once by the optimizer group

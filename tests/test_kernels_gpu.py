@@ -6,6 +6,7 @@ bf16x3 / 3xTF32 tensor-core paths (products carry ~2^-17 relative error, so
 the sums land near 1e-5; the engine-level parity bar is 1e-4) and 1e-5 for
 fp32 CUDA-core ops.  Bit-level outputs (ReLU sign masks, maxpool indices) are exact.
 """
+import ctypes
 import math
 
 import numpy as np
@@ -341,3 +342,55 @@ def test_xent_and_sgd(cuda):
         lib.sgd_step(wd.data_ptr(), gd.data_ptr(), buf.data_ptr(), 1000, 0.1, 0.9, 1e-4, 1.0, int(step == 0),
                      stream())
     assert rel_err(wd, ref) < REL_EW
+
+
+@pytest.mark.parametrize("variant", ["implicit", "splitk", "tf32x3"])
+def test_conv_bias_and_bias_grad(cuda, variant):
+    n, h, w, c, k, r, s, stride, pad = (2, 12, 12, 32, 48, 3, 3, 1, 1)
+    g = torch.Generator().manual_seed(5)
+    x = torch.randn(n, h, w, c, generator=g)
+    wt = torch.randn(k, r, s, c, generator=g) / math.sqrt(r * s * c)
+    b = torch.randn(k, generator=g)
+    d = N.conv_desc(n, h, w, c, k, r, s, stride, pad)
+    lib = N.lib()
+    v = N.CONV_VARIANTS[variant]
+    xd, wd, bd = x.to(cuda), wt.to(cuda), b.to(cuda)
+    y = torch.empty(n, d.p, d.q, k, device=cuda)
+    wsb = lib.conv_ws_bytes(v, 0, d)
+    ws = torch.empty(max(wsb, 4) // 4 + 1, device=cuda)
+    lib.conv_fwd_bias(v, d, xd.data_ptr(), wd.data_ptr(), bd.data_ptr(), y.data_ptr(), ws.data_ptr(), wsb, stream())
+    ref = conv_ref(x, wt, stride, pad) + b
+    assert rel_err(y, ref) < REL_TC
+    dy = torch.randn(n * d.p * d.q, k, generator=g).to(cuda)
+    db = torch.full((k,), 3.0, device=cuda)
+    scratch = torch.empty(lib.bn_scratch_bytes(dy.shape[0], k) // 4 + 1, device=cuda)
+    lib.bias_grad(dy.data_ptr(), db.data_ptr(), dy.shape[0], k, 0, scratch.data_ptr(), stream())
+    assert rel_err(db, dy.double().sum(0)) < 1e-6
+    lib.bias_grad(dy.data_ptr(), db.data_ptr(), dy.shape[0], k, 1, scratch.data_ptr(), stream())
+    assert rel_err(db, 2 * dy.double().sum(0)) < 1e-6
+
+
+def test_dropout_mask_matches_oracle(cuda):
+    """The keep-mask is bit-identical to the oracle's restatement; backward
+    regenerates it; the seed is read from device memory at run time."""
+    from oracle.dropout import keep_mask
+
+    n, p, salt = 1 << 20, 0.4, 13
+    lib = N.lib()
+    x = torch.randn(n, device=cuda).abs_().add_(0.1)  # nonzero: y == 0 <=> dropped
+    y = torch.empty_like(x)
+    seed = torch.tensor([7], dtype=torch.int64, device=cuda)
+    lib.dropout_fwd(x.data_ptr(), y.data_ptr(), n, ctypes.c_float(p), seed.data_ptr(), salt, stream())
+    keep = torch.from_numpy(keep_mask(n, p, 7, salt)).to(cuda)
+    assert torch.equal(y != 0, keep)
+    scale = float(np.float32(1.0 / (1.0 - float(np.float32(p)))))
+    assert torch.equal(y[keep], x[keep] * scale)
+    assert abs(keep.float().mean().item() - (1 - p)) < 3e-3
+    dy = torch.randn(n, device=cuda)
+    dx = torch.ones(n, device=cuda)
+    lib.dropout_bwd(dy.data_ptr(), dx.data_ptr(), n, ctypes.c_float(p), seed.data_ptr(), salt, 1, stream())
+    assert torch.equal(dx, 1 + torch.where(keep, dy * scale, torch.zeros_like(dy)))
+    lib.seed_advance(seed.data_ptr(), stream())
+    lib.dropout_fwd(x.data_ptr(), y.data_ptr(), n, ctypes.c_float(p), seed.data_ptr(), salt, stream())
+    assert int(seed.item()) == 8
+    assert torch.equal(y != 0, torch.from_numpy(keep_mask(n, p, 8, salt)).to(cuda))

@@ -39,6 +39,7 @@ def _autograd_step(model, x, y):
     model.double().train()
     x = x.double()
     opt = torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9)
+    _OPT[id(model)] = opt
     loss = torch.nn.functional.cross_entropy(model(x), y)
     opt.zero_grad()
     loss.backward()
@@ -124,3 +125,75 @@ def test_bitmask_roundtrip():
         # bit b of word k <-> element 32k+b
         for e in range(n):
             assert ((w[e // 32] >> (e % 32)) & 1) == (x[e] > 0)
+
+
+def _torch_layout(net, op, pname, have, want):
+    """Engine-layout parameter -> torch layout (conv KRSC, fc over an NHWC-flattened input)."""
+    if op.kind == "conv" and pname == "weight":
+        return have[..., : want.shape[1]].permute(0, 3, 1, 2)
+    if op.kind == "fc" and pname == "weight" and len(net.op(op.deps[0]).shape) == 4:
+        _, h, w, c = net.op(op.deps[0]).shape
+        return have.view(-1, h, w, c).permute(0, 3, 1, 2).reshape(have.shape[0], -1)
+    return have
+
+
+def test_oracle_vgg_style_equals_autograd():
+    """Conv bias, identity adaptive pool, flatten-to-fc and dropout (hash keep-mask):
+    two consecutive oracle steps under recompute schedules equal autograd + SGD."""
+    from nets import SmallVGG, use_hash_dropout
+
+    torch.manual_seed(0)
+    model = SmallVGG()
+    net = trace_graph(model, torch.empty(2, 3, 32, 32, device="meta"), 10)
+    kinds = {op.kind for op in net.ops}
+    assert {"conv", "dropout", "fc", "maxpool"} <= kinds and "avgpool" not in kinds
+    assert all("bias" in op.params for op in net.ops if op.kind == "conv")
+    g = M.load_graph(net.graph_doc())
+    cat = M.load_catalog(net.catalog_doc(), g)
+    gen = torch.Generator().manual_seed(1)
+    x = torch.randn(2, 3, 32, 32, generator=gen)
+    y = torch.randint(0, 10, (2,), generator=gen)
+    scheds = _schedules(g, cat) + _planned(net, g, cat)
+    assert any(n != "store_everything" for n, _ in scheds), "no recompute schedule to test"
+    for name, sched in scheds:
+        ref_model = SmallVGG()
+        ref_model.load_state_dict(model.state_dict())
+        st = CpuState(net, dtype=torch.float64)
+        for step in range(2):  # the second step draws a new mask (seed advanced)
+            use_hash_dropout(ref_model, net, seed=step)
+            ref_loss = _autograd_step(ref_model, x, y) if step == 0 else _autograd_step_keep(ref_model, x, y)
+            loss = run_step(st, M.schedule_to_doc(sched), x.double(), y)
+            assert abs(loss - ref_loss) <= TOL * abs(ref_loss), (name, step)
+        ref = {n: p.detach() for n, p in ref_model.named_parameters()}
+        got = params_nhwc(st)
+        for op in net.ops:
+            for pname in op.params:
+                want = ref[f"{op.name}.{pname}"]
+                have = _torch_layout(net, op, pname, got[(op.id, pname)], want)
+                assert _rel(have, want) < TOL, (name, op.name, pname)
+
+
+_OPT = {}
+
+
+def _planned(net, g, cat, fracs=(0.7, 0.6)):
+    """Host-planner recompute schedules at fractions of the store-everything activations."""
+    from paper_2010_14501_b200.planner import plan_schedule
+
+    act = M.simulate(M.store_everything_schedule(g, cat), g, cat).peak_memory - g.params_bytes
+    out = []
+    for f in fracs:
+        s, _ = plan_schedule(g, cat, g.params_bytes + int(f * act), kinds=net.storable_kinds())
+        if s is not None and any(st.recompute for st in s.stages):
+            out.append((f"planned-{f}", s))
+    return out
+
+
+def _autograd_step_keep(model, x, y):
+    """Second SGD step with the optimizer (momentum buffers) of the first."""
+    opt = _OPT[id(model)]
+    loss = torch.nn.functional.cross_entropy(model(x.double()), y)
+    opt.zero_grad()
+    loss.backward()
+    opt.step()
+    return loss.item()
