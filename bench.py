@@ -74,7 +74,7 @@ def measured_catalog(net, args):
     """The frozen on-device profile (tools/profile_catalog.py) when it matches this graph."""
     import hashlib
 
-    path = ROOT / "profiles" / f"catalog_{args.arch}{'_fused' if args.fuse else ''}_b{args.batch}_{args.image}.json"
+    path = ROOT / "profiles" / f"catalog_{args.arch}{'_fused' if net.fused else ''}_b{args.batch}_{args.image}.json"
     if not path.exists():
         return None
     doc = json.loads(path.read_text())

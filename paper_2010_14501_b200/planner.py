@@ -179,14 +179,48 @@ FAMILIES = ("all", "conv+relu+mask", "conv+mask", "bn+relu+mask", "bn+mask", "re
             "conv+add+mask", "add+mask", "join")
 
 
-def plan_schedule(g: Graph, cat: Catalog, budget: int, kinds: dict | None = None):
+EXACT_MAX_NODES = 64  # graphs up to this size also go through the exact ILP (VGG-16: 40 nodes)
+
+
+def plan_schedule(g: Graph, cat: Catalog, budget: int, kinds: dict | None = None,
+                  exact_time_s: float | None = None):
     """Cheapest feasible schedule among the demand-construction candidates.
 
     ``kinds`` maps storable id -> family label; by default inferred from the
     graph structure is not possible, so the tracer's op kinds are expected via
     ``Network.storable_kinds()``; without it every storable counts as "all".
+    ``exact_time_s``: on graphs of at most EXACT_MAX_NODES nodes, also run the
+    reference-exact 0-1 ILP (ilp.build_model + solver.solve) for that long,
+    seeded with the best candidate as its incumbent; its schedule wins when it
+    is cheaper or the only feasible one.
     Returns (schedule or None, info dict).
     """
+    sch, info = _plan_heuristic(g, cat, budget, kinds)
+    if exact_time_s and g.n <= EXACT_MAX_NODES:
+        from .ilp import assignment_from_schedule, build_model
+        from .schedule import decode
+        from .solver import solve
+
+        model = build_model(g, compute_dependency_sets(g), cat, budget)
+        opts = {"time_limit_s": exact_time_s}
+        if sch is not None:
+            opts["incumbent"] = assignment_from_schedule(model, sch)
+        res = solve(model, opts)
+        if res.assignment is not None:
+            ilp = decode(res, g, cat)
+            if sch is None or ilp.objective < sch.objective:
+                ok, peak, _ = FastBound(g, compute_dependency_sets(g, "upper"), cat).check(ilp, budget)
+                simulate(ilp, g, cat)
+                se = info.get("se_cost")
+                info = {"family": f"exact-ilp/{res.status}", "candidates": info["candidates"], "modeled_peak": peak,
+                        "objective": str(ilp.objective), "ilp_gap": None if res.gap is None else float(res.gap),
+                        "overhead_vs_store_everything": None if se is None else float(Fraction(ilp.objective) / se - 1)}
+                sch = ilp
+    info.pop("se_cost", None)
+    return sch, info
+
+
+def _plan_heuristic(g: Graph, cat: Catalog, budget: int, kinds: dict | None = None):
     sets = compute_dependency_sets(g, "upper")
     fb = FastBound(g, sets, cat)
     kind_of = (lambda x: kinds.get(x, "other")) if kinds else (lambda x: "other")
@@ -232,16 +266,16 @@ def plan_schedule(g: Graph, cat: Catalog, budget: int, kinds: dict | None = None
         except SimulationError:
             continue
         best = (name, sch, peak)
-    if best is None:
-        return None, {"candidates": tried}
     se_cost = None
     try:
         se_cost = store_everything_schedule(g, cat).objective
     except ValueError:
         pass
+    if best is None:
+        return None, {"candidates": tried, "se_cost": se_cost}
     name, sch, peak = best
     info = {"family": name, "candidates": tried, "modeled_peak": peak,
-            "objective": str(sch.objective),
+            "objective": str(sch.objective), "se_cost": se_cost,
             "overhead_vs_store_everything": None if se_cost is None
             else float(Fraction(sch.objective) / se_cost - 1)}
     return sch, info

@@ -26,11 +26,11 @@ def digest(doc):
     return hashlib.sha256(json.dumps(doc, sort_keys=True).encode()).hexdigest()[:16]
 
 
-def main(jobs):
+def main(jobs, exact_time_s=None):
     OUT.mkdir(exist_ok=True)
     for arch, batch, img, gib, fuse in jobs:
         net = build_network(arch, batch, img, fuse=fuse)
-        arch = arch + ("_fused" if fuse else "")
+        arch = arch + ("_fused" if net.fused else "")
         gdoc, cdoc = net.graph_doc(), net.catalog_doc()
         measured = ROOT / "profiles" / f"catalog_{arch}_b{batch}_{img}.json"
         if measured.exists():  # plan with the on-device profile when it matches this graph
@@ -42,7 +42,7 @@ def main(jobs):
         cat = M.load_catalog(cdoc, g)
         budget = int(gib * (1 << 30))
         t = time.time()
-        sched, info = plan_schedule(g, cat, budget, kinds=net.storable_kinds())
+        sched, info = plan_schedule(g, cat, budget, kinds=net.storable_kinds(), exact_time_s=exact_time_s)
         dt = time.time() - t
         if sched is None:
             print(arch, batch, img, gib, "no feasible schedule", info)
@@ -56,5 +56,15 @@ def main(jobs):
 
 
 if __name__ == "__main__":
-    fuse = "--fused" in sys.argv
-    main([("resnet50", 184, 224, gib, fuse) for gib in (10, 8, 6)])
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--fused", action="store_true")
+    ap.add_argument("--arch", default="resnet50")
+    ap.add_argument("--batch", type=int, default=184)
+    ap.add_argument("--image", type=int, default=224)
+    ap.add_argument("--budgets", default="10,8,6", help="GiB, comma separated")
+    ap.add_argument("--exact", type=float, default=None,
+                    help="seconds of exact ILP search on graphs of <= planner.EXACT_MAX_NODES nodes")
+    a = ap.parse_args()
+    main([(a.arch, a.batch, a.image, float(b), a.fused) for b in a.budgets.split(",")], a.exact)

@@ -25,7 +25,7 @@ def digest(doc):
 
 def main(arch="resnet50", batch=184, image=224, fuse=False):
     net = build_network(arch, batch, image, fuse=fuse)
-    arch = arch + ("_fused" if fuse else "")
+    arch = arch + ("_fused" if net.fused else "")
     t = time.time()
     costs = profile_network(net, log=print)
     doc = {"arch": arch, "batch": batch, "image": image, "graph_digest": digest(net.graph_doc()),
