@@ -64,6 +64,8 @@ int64_t place(const std::vector<int64_t>& order, const int64_t* sizes, const int
 //     bottom -- then size
 //   2 blocks live at the peak instant first (by allocation time), then size
 //   3 allocation order (what a first-fit runtime allocator would see)
+//   4 lifetime length descending, 5 lifetime x size descending
+// then, if none is gap-free at the peak instant, a seeded local search.
 extern "C" int monet_arena_plan(int64_t count, const int64_t* sizes, const int64_t* t_alloc, const int64_t* t_free,
                                 int64_t align, int64_t capacity_bytes, int64_t* offsets, int64_t* peak_bytes) {
   if (count < 0 || align <= 0) return -22;
@@ -94,7 +96,7 @@ extern "C" int monet_arena_plan(int64_t count, const int64_t* sizes, const int64
     if (sizes[a] != sizes[b]) return sizes[a] > sizes[b];
     return t_alloc[a] < t_alloc[b];
   };
-  std::vector<std::vector<int64_t>> orders(4, base);
+  std::vector<std::vector<int64_t>> orders(6, base);
   std::stable_sort(orders[0].begin(), orders[0].end(), by_size);
   std::stable_sort(orders[1].begin(), orders[1].end(), [&](int64_t a, int64_t b) {
     if (heat[a] != heat[b]) return heat[a] > heat[b];
@@ -110,15 +112,50 @@ extern "C" int monet_arena_plan(int64_t count, const int64_t* sizes, const int64
     if (t_alloc[a] != t_alloc[b]) return t_alloc[a] < t_alloc[b];
     return a < b;
   });
-  std::vector<int64_t> offs(count), best_offs;
+  std::stable_sort(orders[4].begin(), orders[4].end(), [&](int64_t a, int64_t b) {
+    const int64_t la = t_free[a] - t_alloc[a], lb = t_free[b] - t_alloc[b];
+    if (la != lb) return la > lb;
+    return by_size(a, b);
+  });
+  std::stable_sort(orders[5].begin(), orders[5].end(), [&](int64_t a, int64_t b) {
+    const double aa = (double)(t_free[a] - t_alloc[a]) * sizes[a], ab = (double)(t_free[b] - t_alloc[b]) * sizes[b];
+    if (aa != ab) return aa > ab;
+    return by_size(a, b);
+  });
+  std::vector<int64_t> offs(count), best_offs, best_order;
   int64_t best = INT64_MAX;
   for (const auto& order : orders) {
     const int64_t peak = place(order, sizes, t_alloc, t_free, align, offs);
     if (peak < best) {
       best = peak;
       best_offs = offs;
+      best_order = order;
     }
     if (best == best_live) break;  // gap-free at the peak: optimal
+  }
+  // Still fragmented (few, huge, long-lived blocks -- VGG's 2 GiB activations):
+  // deterministic local search over the placement order, 1-3 random swaps per
+  // trial (fixed-seed LCG), accepting non-worsening orders, until gap-free.
+  if (count > 1 && best > best_live) {
+    uint64_t rng = 0x9E3779B97F4A7C15ull;
+    auto next = [&](int64_t m) {
+      rng = rng * 6364136223846793005ull + 1442695040888963407ull;
+      return (int64_t)((rng >> 33) % (uint64_t)m);
+    };
+    std::vector<int64_t> trial;
+    const int64_t budget_ops = 400000000;  // ~ trials * count^2 placement work
+    const int64_t trials = std::max<int64_t>(64, std::min<int64_t>(8000, budget_ops / (count * count)));
+    for (int64_t it = 0; it < trials && best > best_live; ++it) {
+      trial = best_order;
+      const int64_t swaps = 1 + next(3);
+      for (int64_t k = 0; k < swaps; ++k) std::swap(trial[next(count)], trial[next(count)]);
+      const int64_t peak = place(trial, sizes, t_alloc, t_free, align, offs);
+      if (peak <= best) {
+        best = peak;
+        best_offs = offs;
+        best_order = trial;
+      }
+    }
   }
   if (count == 0) best = 0;
   std::copy(best_offs.begin(), best_offs.end(), offsets);

@@ -1,4 +1,4 @@
-"""The planned arena of every committed ResNet-50 schedule fits its ILP bound.
+"""The planned arena of every committed schedule (ResNet-50, VGG-16) fits its ILP bound.
 
 Physical peak = params_bytes + arena high-water mark (csrc/arena.cpp) must not
 exceed check_schedule's modeled peak (oracle.py:287), which must not exceed
@@ -17,25 +17,30 @@ from paper_2010_14501_b200.schedule import ledger
 from paper_2010_14501_b200.tracer import build_network
 
 ROOT = Path(__file__).resolve().parent.parent
-SCHEDULES = sorted((ROOT / "schedules").glob("resnet50*_b184_224_*gib.json"))
+SCHEDULES = sorted((ROOT / "schedules").glob("*_b*_224_*gib.json"))
 
 
 _NETS = {}
 
 
-def _r50(fused: bool):
-    if fused not in _NETS:
-        net = build_network("resnet50", 184, 224, fuse=fused)
+def _net(path):
+    """(network, graph, catalog) a schedule file was planned for (name: arch[_fused]_b<batch>_224_...)."""
+    stem = path.name.split("_b")[0]
+    arch, fused = stem.removesuffix("_fused"), stem.endswith("_fused")
+    batch = int(path.name.split("_b")[1].split("_")[0])
+    key = (arch, fused, batch)
+    if key not in _NETS:
+        net = build_network(arch, batch, 224, fuse=fused)
         g = M.load_graph(net.graph_doc())
-        path = ROOT / "profiles" / f"catalog_resnet50{'_fused' if fused else ''}_b184_224.json"
-        cdoc = json.loads(path.read_text())["catalog"] if path.exists() else net.catalog_doc()
-        _NETS[fused] = (net, g, M.load_catalog(cdoc, g))
-    return _NETS[fused]
+        cpath = ROOT / "profiles" / f"catalog_{stem}_b{batch}_224.json"
+        cdoc = json.loads(cpath.read_text())["catalog"] if cpath.exists() else net.catalog_doc()
+        _NETS[key] = (net, g, M.load_catalog(cdoc, g))
+    return _NETS[key]
 
 
 @pytest.mark.parametrize("path", SCHEDULES, ids=[p.stem for p in SCHEDULES])
 def test_physical_peak_within_ilp_bound(path):
-    net, g, cat = _r50("_fused" in path.name)
+    net, g, cat = _net(path)
     doc = json.loads(path.read_text())
     digest = hashlib.sha256(json.dumps(net.graph_doc(), sort_keys=True).encode()).hexdigest()[:16]
     assert doc["graph_digest"] == digest, "schedule was planned for another graph"
