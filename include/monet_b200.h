@@ -88,6 +88,16 @@ int monet_dropout_bwd(const float* dy, float* dx, int64_t n, float p, const unsi
                       int accumulate, void* stream);
 int monet_seed_advance(unsigned long long* seed, void* stream);
 
+/* --- depthwise conv (groups = C; MobileNet-V2) ------------------------------------
+ * NHWC, d->k == d->c, R*S <= 9, weights [R][S][C].  HBM-bound direct kernels.
+ * wgrad reduces in two fixed-order levels through ws (monet_dwconv_ws_bytes). */
+size_t monet_dwconv_ws_bytes(const monet_conv_desc* d);
+int monet_dwconv_fwd(const monet_conv_desc* d, const float* x, const float* w, float* y, void* stream);
+int monet_dwconv_dgrad(const monet_conv_desc* d, const float* dy, const float* w, float* dx, int accumulate,
+                       void* stream);
+int monet_dwconv_wgrad(const monet_conv_desc* d, const float* x, const float* dy, float* dw, void* ws,
+                       size_t ws_bytes, void* stream);
+
 /* --- dense layer (fc) -------------------------------------------------------- */
 size_t monet_linear_ws_bytes(int variant, int pass, int n, int in_f, int out_f);
 int monet_linear_fwd(int variant, const float* x, const float* w, const float* b, float* y, int n, int in_f,
@@ -101,6 +111,12 @@ int monet_relu_fwd(const float* x, float* y, uint32_t* mask, int64_t n, void* st
 int monet_relu_bwd_mask(const uint32_t* mask, const float* dy, float* dx, int64_t n, int accumulate, void* stream);
 int monet_relu_bwd_out(const float* y, const float* dy, float* dx, int64_t n, int accumulate, void* stream);
 int monet_relu_bwd_in(const float* x, const float* dy, float* dx, int64_t n, int accumulate, void* stream);
+
+/* ReLU6 = hardtanh(0, 6) (MobileNet-V2): y = min(max(x, 0), 6); mask bit = the gradient
+ * gate 0 < x < 6, so the backward from the mask is monet_relu_bwd_mask. */
+int monet_relu6_fwd(const float* x, float* y, uint32_t* mask, int64_t n, void* stream);
+int monet_relu6_bwd_out(const float* y, const float* dy, float* dx, int64_t n, int accumulate, void* stream);
+int monet_relu6_bwd_in(const float* x, const float* dy, float* dx, int64_t n, int accumulate, void* stream);
 
 /* --- BatchNorm, training mode, [rows = n*h*w, c] (K6-K8) ----------------------
  * scratch: monet_bn_scratch_bytes(rows, c) bytes of caller memory. */

@@ -40,6 +40,8 @@ class CpuState:
                 v = t.to(dtype).clone()
                 if op.kind == "conv" and name == "weight":
                     v = v.permute(0, 3, 1, 2).contiguous()  # KRSC -> KCRS (OIHW)
+                elif op.kind == "dwconv" and name == "weight":
+                    v = v.permute(2, 0, 1).unsqueeze(1).contiguous()  # [R][S][C] -> [C][1][R][S]
                 self.params[(op.id, name)] = v
         self.mom = {k: torch.zeros_like(v) for k, v in self.params.items()}
         self.running = {op.id: [op.attrs["running_mean"].to(dtype).clone(),
@@ -113,6 +115,16 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
             y = F.conv2d(xs[0], P[(op.id, "weight")], P.get((op.id, "bias")), stride=a["stride"], padding=a["pad"])
         elif op.kind == "dropout":
             y = xs[0] * _dropout_scale(op, xs[0], state.seed)
+        elif op.kind == "dwconv":
+            a = op.attrs
+            y = F.conv2d(xs[0], P[(op.id, "weight")], stride=a["stride"], padding=a["pad"], groups=xs[0].shape[1])
+        elif op.kind == "relu6":
+            x = xs[0]
+            y = torch.clamp(x, 0.0, 6.0)
+            if want_int:
+                gate = (x > 0) & (x < 6)
+                extra = pack_sign_mask(torch.where(gate, 1.0, -1.0).permute(0, 2, 3, 1).numpy()
+                                       if x.dim() == 4 else torch.where(gate, 1.0, -1.0).numpy())
         elif op.kind in ("bn", "bnrelu"):
             g, b = P[(op.id, "weight")], P[(op.id, "bias")]
             if mode == "forward":
@@ -177,6 +189,28 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
                 state.grads[(op.id, "bias")] = dy.sum(dim=(0, 2, 3))
         elif op.kind == "dropout":
             put_grad(op.deps[0], dy * _dropout_scale(op, dy, state.seed), created)
+        elif op.kind == "dwconv":
+            a = op.attrs
+            j = op.deps[0]
+            x = x_of(j)
+            w = P[(op.id, "weight")]
+            grp = x.shape[1]
+            if net.grad_bytes(net.op(j)) > 0:
+                put_grad(j, torch.nn.grad.conv2d_input(x.shape, w, dy, a["stride"], a["pad"], groups=grp), created)
+            state.grads[(op.id, "weight")] = torch.nn.grad.conv2d_weight(x, w.shape, dy, a["stride"], a["pad"],
+                                                                         groups=grp)
+        elif op.kind == "relu6":
+            j = op.deps[0]
+            if impl == "bwd-mask":
+                bits = torch.from_numpy(unpack_sign_mask(x_of(net.intermediate_of[op.id]), dy.numel()))
+                if dy.dim() == 4:
+                    keep = bits.view(dy.shape[0], dy.shape[2], dy.shape[3], dy.shape[1]).permute(0, 3, 1, 2)
+                else:
+                    keep = bits.view(dy.shape)
+            else:
+                s_ = x_of(op.id) if impl == "bwd-out" else x_of(j)
+                keep = (s_ > 0) & (s_ < 6)
+            put_grad(j, torch.where(keep, dy, torch.zeros_like(dy)), created)
         elif op.kind in ("bn", "bnrelu"):
             j = op.deps[0]
             g, b = P[(op.id, "weight")], P[(op.id, "bias")]
@@ -379,5 +413,7 @@ def params_nhwc(state: CpuState):
     for (nid, name), v in state.params.items():
         if state.net.op(nid).kind == "conv" and name == "weight":
             v = v.permute(0, 2, 3, 1).contiguous()
+        elif state.net.op(nid).kind == "dwconv" and name == "weight":
+            v = v.squeeze(1).permute(1, 2, 0).contiguous()
         out[(nid, name)] = v
     return out

@@ -38,6 +38,13 @@ SIGNATURES = {
     "monet_dropout_fwd": (_i32, [_vp, _vp, _i64, _f32, _vp, C.c_uint64, _vp]),
     "monet_dropout_bwd": (_i32, [_vp, _vp, _i64, _f32, _vp, C.c_uint64, _i32, _vp]),
     "monet_seed_advance": (_i32, [_vp, _vp]),
+    "monet_dwconv_ws_bytes": (_sz, [_PCONV]),
+    "monet_dwconv_fwd": (_i32, [_PCONV, _vp, _vp, _vp, _vp]),
+    "monet_dwconv_dgrad": (_i32, [_PCONV, _vp, _vp, _vp, _i32, _vp]),
+    "monet_dwconv_wgrad": (_i32, [_PCONV, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "monet_relu6_fwd": (_i32, [_vp, _vp, _vp, _i64, _vp]),
+    "monet_relu6_bwd_out": (_i32, [_vp, _vp, _vp, _i64, _i32, _vp]),
+    "monet_relu6_bwd_in": (_i32, [_vp, _vp, _vp, _i64, _i32, _vp]),
     "monet_linear_ws_bytes": (_sz, [_i32, _i32, _i32, _i32, _i32]),
     "monet_linear_fwd": (_i32, [_i32, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _sz, _vp]),
     "monet_linear_bwd": (_i32, [_i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _i32, _i32, _i32, _vp, _sz, _vp]),

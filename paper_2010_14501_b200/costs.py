@@ -34,7 +34,11 @@ def analytic_cost(net, op, pass_, name) -> int:
         fi = net.fc_dims(op)[1]
         flops = 2.0 * n * fi
         return _ns(flops if pass_ == "fwd" else 2 * flops, launches=2 if pass_ == "fwd" else 4)
-    if op.kind == "relu":
+    if op.kind == "dwconv":  # direct, HBM-bound: fwd r x w y; bwd r dy (x2) r x w dx
+        x = net.op(op.deps[0])
+        return _ns(nbytes=4.0 * (x.numel + n) if pass_ == "fwd" else 4.0 * (2 * n + 2 * x.numel),
+                   launches=1 if pass_ == "fwd" else 3)
+    if op.kind in ("relu", "relu6"):
         if pass_ == "fwd":
             return _ns(nbytes=8.125 * n)
         return _ns(nbytes=(8.125 if name == "bwd-mask" else 12.0) * n)

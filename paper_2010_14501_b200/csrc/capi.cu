@@ -10,6 +10,7 @@
 #include "gemm_bf16x3.cuh"
 #include "gemm_tc.cuh"
 #include "local_ops.cuh"
+#include "dwconv.cuh"
 
 using namespace monet;
 
@@ -676,7 +677,7 @@ int monet_gemm(int variant, const float* a, int a_mn, int64_t lda, const float* 
 
 // ------------------------------------------------------------------- ReLU
 int monet_relu_fwd(const float* x, float* y, uint32_t* mask, int64_t n, void* stream) {
-  relu_fwd_kernel<<<ew_blocks((n + 7) / 8), kEwThreads, 0, S(stream)>>>(x, y, mask, n);
+  relu_fwd_kernel<false><<<ew_blocks((n + 7) / 8), kEwThreads, 0, S(stream)>>>(x, y, mask, n);
   return last_error();
 }
 int monet_relu_bwd_mask(const uint32_t* mask, const float* dy, float* dx, int64_t n, int accumulate, void* stream) {
@@ -684,11 +685,63 @@ int monet_relu_bwd_mask(const uint32_t* mask, const float* dy, float* dx, int64_
   return last_error();
 }
 int monet_relu_bwd_out(const float* y, const float* dy, float* dx, int64_t n, int accumulate, void* stream) {
-  relu_bwd_sign_kernel<<<ew_blocks(n / 4 + 1), kEwThreads, 0, S(stream)>>>(y, dy, dx, n, accumulate);
+  relu_bwd_sign_kernel<false><<<ew_blocks(n / 4 + 1), kEwThreads, 0, S(stream)>>>(y, dy, dx, n, accumulate);
   return last_error();
 }
 int monet_relu_bwd_in(const float* x, const float* dy, float* dx, int64_t n, int accumulate, void* stream) {
   return monet_relu_bwd_out(x, dy, dx, n, accumulate, stream);
+}
+
+// ReLU6 (hardtanh(0, 6)): the mask bit is the gradient gate 0 < x < 6, so the
+// backward from the mask is monet_relu_bwd_mask; from the output or the input
+// the gate is the same test.
+int monet_relu6_fwd(const float* x, float* y, uint32_t* mask, int64_t n, void* stream) {
+  relu_fwd_kernel<true><<<ew_blocks((n + 7) / 8), kEwThreads, 0, S(stream)>>>(x, y, mask, n);
+  return last_error();
+}
+int monet_relu6_bwd_out(const float* y, const float* dy, float* dx, int64_t n, int accumulate, void* stream) {
+  relu_bwd_sign_kernel<true><<<ew_blocks(n / 4 + 1), kEwThreads, 0, S(stream)>>>(y, dy, dx, n, accumulate);
+  return last_error();
+}
+int monet_relu6_bwd_in(const float* x, const float* dy, float* dx, int64_t n, int accumulate, void* stream) {
+  return monet_relu6_bwd_out(x, dy, dx, n, accumulate, stream);
+}
+
+// ------------------------------------------------------------ depthwise conv
+static int dw_check(const monet_conv_desc* d) {
+  if (!d || d->c % 4 || d->k != d->c || d->r * d->s > kDwMaxTaps || d->n <= 0) return -(int)cudaErrorInvalidValue;
+  return 0;
+}
+static int dw_blocks(const monet_conv_desc* d) {
+  const long long rows = (long long)d->n * d->p * d->q;
+  return (int)std::max(1LL, std::min((rows + 63) / 64, (long long)kNumSMs * 4));
+}
+size_t monet_dwconv_ws_bytes(const monet_conv_desc* d) {
+  if (dw_check(d)) return 0;
+  return (size_t)dw_blocks(d) * d->r * d->s * d->c * sizeof(float);
+}
+int monet_dwconv_fwd(const monet_conv_desc* d, const float* x, const float* w, float* y, void* stream) {
+  if (int e = dw_check(d)) return e;
+  const long long total = (long long)d->n * d->p * d->q * (d->c / 4);
+  dwconv_fwd_kernel<<<ew_blocks(total), kEwThreads, 0, S(stream)>>>(x, w, y, geom(d));
+  return last_error();
+}
+int monet_dwconv_dgrad(const monet_conv_desc* d, const float* dy, const float* w, float* dx, int accumulate,
+                       void* stream) {
+  if (int e = dw_check(d)) return e;
+  const long long total = (long long)d->n * d->h * d->w * (d->c / 4);
+  dwconv_dgrad_kernel<<<ew_blocks(total), kEwThreads, 0, S(stream)>>>(dy, w, dx, geom(d), accumulate);
+  return last_error();
+}
+int monet_dwconv_wgrad(const monet_conv_desc* d, const float* x, const float* dy, float* dw, void* ws,
+                       size_t ws_bytes, void* stream) {
+  if (int e = dw_check(d)) return e;
+  if (ws == nullptr || ws_bytes < monet_dwconv_ws_bytes(d)) return -(int)cudaErrorInvalidValue;
+  const int nb = dw_blocks(d), taps = d->r * d->s;
+  float* part = static_cast<float*>(ws);
+  dwconv_wgrad_partial_kernel<<<nb, kEwThreads, 0, S(stream)>>>(x, dy, part, geom(d));
+  dwconv_wgrad_final_kernel<<<(taps * d->c + 255) / 256, 256, 0, S(stream)>>>(part, nb, taps, d->c, dw);
+  return last_error();
 }
 
 // ------------------------------------------------------------------- BatchNorm

@@ -15,8 +15,19 @@ constexpr int kEwThreads = 256;
 
 // ------------------------------------------------------------------ ReLU
 // y = max(x, 0) (NaN -> 0, matching mask bit x > 0); optional packed mask.
+// kSix (ReLU6 = hardtanh(0, 6), MobileNet-V2): y = min(max(x, 0), 6) and the
+// mask bit is the gradient gate 0 < x < 6.
 // Each thread handles 8 consecutive elements (two float4) -> one byte of mask;
 // 4 consecutive lanes assemble one 32-bit word with shuffles.
+template <bool kSix>
+MONET_DEV bool relu_gate(float v) {
+  return kSix ? (v > 0.f && v < 6.f) : v > 0.f;
+}
+template <bool kSix>
+MONET_DEV float relu_val(float v) {
+  return kSix ? (v > 0.f ? fminf(v, 6.f) : 0.f) : (v > 0.f ? v : 0.f);
+}
+template <bool kSix = false>
 __global__ void relu_fwd_kernel(const float* __restrict__ x, float* y, uint32_t* __restrict__ mask,
                                 long long n) {
   const long long n8 = (n + 7) / 8;
@@ -30,24 +41,24 @@ __global__ void relu_fwd_kernel(const float* __restrict__ x, float* y, uint32_t*
       if (e0 + 8 <= n) {
         float4 a = *reinterpret_cast<const float4*>(x + e0);
         float4 b = *reinterpret_cast<const float4*>(x + e0 + 4);
-        byte = (a.x > 0.f) | ((a.y > 0.f) << 1) | ((a.z > 0.f) << 2) | ((a.w > 0.f) << 3) | ((b.x > 0.f) << 4) |
-               ((b.y > 0.f) << 5) | ((b.z > 0.f) << 6) | ((b.w > 0.f) << 7);
-        a.x = a.x > 0.f ? a.x : 0.f;
-        a.y = a.y > 0.f ? a.y : 0.f;
-        a.z = a.z > 0.f ? a.z : 0.f;
-        a.w = a.w > 0.f ? a.w : 0.f;
-        b.x = b.x > 0.f ? b.x : 0.f;
-        b.y = b.y > 0.f ? b.y : 0.f;
-        b.z = b.z > 0.f ? b.z : 0.f;
-        b.w = b.w > 0.f ? b.w : 0.f;
+        byte = relu_gate<kSix>(a.x) | (relu_gate<kSix>(a.y) << 1) | (relu_gate<kSix>(a.z) << 2) |
+               (relu_gate<kSix>(a.w) << 3) | (relu_gate<kSix>(b.x) << 4) | (relu_gate<kSix>(b.y) << 5) |
+               (relu_gate<kSix>(b.z) << 6) | (relu_gate<kSix>(b.w) << 7);
+        a.x = relu_val<kSix>(a.x);
+        a.y = relu_val<kSix>(a.y);
+        a.z = relu_val<kSix>(a.z);
+        a.w = relu_val<kSix>(a.w);
+        b.x = relu_val<kSix>(b.x);
+        b.y = relu_val<kSix>(b.y);
+        b.z = relu_val<kSix>(b.z);
+        b.w = relu_val<kSix>(b.w);
         *reinterpret_cast<float4*>(y + e0) = a;
         *reinterpret_cast<float4*>(y + e0 + 4) = b;
       } else {
         for (long long e = e0; e < n; ++e) {
           float v = x[e];
-          bool pos = v > 0.f;
-          byte |= (uint32_t)pos << (e - e0);
-          y[e] = pos ? v : 0.f;
+          byte |= (uint32_t)relu_gate<kSix>(v) << (e - e0);
+          y[e] = relu_val<kSix>(v);
         }
       }
     }
@@ -96,7 +107,9 @@ __global__ void relu_bwd_mask_kernel(const uint32_t* __restrict__ mask, const fl
   }
 }
 
-// dx (=|+=) dy * [s > 0] where s is the ReLU input or output (same sign test).
+// dx (=|+=) dy * [s > 0] where s is the ReLU input or output (same sign test);
+// kSix: [0 < s < 6] (ReLU6 input or output: the same gate).
+template <bool kSix = false>
 __global__ void relu_bwd_sign_kernel(const float* __restrict__ s, const float* __restrict__ dy, float* dx,
                                      long long n, int accumulate) {
   const long long n4 = n / 4;
@@ -104,10 +117,10 @@ __global__ void relu_bwd_sign_kernel(const float* __restrict__ s, const float* _
        i += (long long)gridDim.x * blockDim.x) {
     float4 v = *reinterpret_cast<const float4*>(s + 4 * i);
     float4 g = *reinterpret_cast<const float4*>(dy + 4 * i);
-    g.x = v.x > 0.f ? g.x : 0.f;
-    g.y = v.y > 0.f ? g.y : 0.f;
-    g.z = v.z > 0.f ? g.z : 0.f;
-    g.w = v.w > 0.f ? g.w : 0.f;
+    g.x = relu_gate<kSix>(v.x) ? g.x : 0.f;
+    g.y = relu_gate<kSix>(v.y) ? g.y : 0.f;
+    g.z = relu_gate<kSix>(v.z) ? g.z : 0.f;
+    g.w = relu_gate<kSix>(v.w) ? g.w : 0.f;
     if (accumulate) {
       float4 c = *reinterpret_cast<const float4*>(dx + 4 * i);
       g.x += c.x; g.y += c.y; g.z += c.z; g.w += c.w;
@@ -116,7 +129,7 @@ __global__ void relu_bwd_sign_kernel(const float* __restrict__ s, const float* _
   }
   if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
     long long e = n4 * 4 + threadIdx.x;
-    float v = s[e] > 0.f ? dy[e] : 0.f;
+    float v = relu_gate<kSix>(s[e]) ? dy[e] : 0.f;
     dx[e] = accumulate ? dx[e] + v : v;
   }
 }

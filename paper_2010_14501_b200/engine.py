@@ -269,6 +269,14 @@ class Runtime:
                                                                s.workspace, None), d))
                 else:
                     out.append(("k", lib.monet_conv_fwd, (v, C.byref(d), xs[0], wt, y, ws, s.workspace, None), d))
+            elif op.kind == "dwconv":
+                d = net.conv_desc(op)
+                out.append(("k", lib.monet_dwconv_fwd, (C.byref(d), xs[0], self.pview[(op.id, "weight")].data_ptr(),
+                                                        y, None), d))
+            elif op.kind == "relu6":
+                mid = net.intermediate_of[op.id]
+                mask = P(("a", mid)) if mid in s.planned_ints else None
+                out.append(("k", lib.monet_relu6_fwd, (xs[0], y, mask, op.numel, None)))
             elif op.kind == "dropout":
                 out.append(("k", lib.monet_dropout_fwd, (xs[0], y, op.numel, C.c_float(op.attrs["p"]),
                                                          self.seed_ptr, op.id, None)))
@@ -360,6 +368,24 @@ class Runtime:
                 out.append(("k", lib.monet_bias_grad, (dy, self.gview[(op.id, "bias")].data_ptr(),
                                                        op.numel // op.shape[-1], op.shape[-1], 0, self.scratch_ptr,
                                                        None)))
+        elif op.kind == "dwconv":
+            d = net.conv_desc(op)
+            j = op.deps[0]
+            wt = self.pview[(op.id, "weight")].data_ptr()
+            if net.grad_bytes(net.op(j)) > 0:
+                out.append(("k", lib.monet_dwconv_dgrad, (C.byref(d), dy, wt, P(("g", j)), acc(j), None), d))
+            out.append(("k", lib.monet_dwconv_wgrad, (C.byref(d), P(("in", j)), dy,
+                                                      self.gview[(op.id, "weight")].data_ptr(), ws, s.workspace,
+                                                      None), d))
+        elif op.kind == "relu6":
+            j = op.deps[0]
+            if s.impl == "bwd-mask":
+                src, fn = P(("in", net.intermediate_of[op.id])), lib.monet_relu_bwd_mask
+            elif s.impl == "bwd-out":
+                src, fn = P(("in", op.id)), lib.monet_relu6_bwd_out
+            else:
+                src, fn = P(("in", j)), lib.monet_relu6_bwd_in
+            out.append(("k", fn, (src, dy, P(("g", j)), op.numel, acc(j), None)))
         elif op.kind == "dropout":
             j = op.deps[0]
             out.append(("k", lib.monet_dropout_bwd, (dy, P(("g", j)), op.numel, C.c_float(op.attrs["p"]),

@@ -179,6 +179,32 @@ def _local_calls(bx: _Bench, net, op):
         out[("fwd", "avgpool")] = lambda: bx.check(lib.monet_avgpool_fwd(x.data_ptr(), y.data_ptr(), nb, h * w, c, sp))
         out[("bwd", "bwd")] = lambda: bx.check(lib.monet_avgpool_bwd(dy.data_ptr(), dx.data_ptr(), nb, h * w, c, 0,
                                                                        sp))
+    elif kind == "relu6":
+        mask = bx.buf((n + 31) // 32 * 4)
+        out[("fwd", "relu6")] = lambda: bx.check(lib.monet_relu6_fwd(x.data_ptr(), y.data_ptr(), mask.data_ptr(), n,
+                                                                      sp))
+        out[("bwd", "bwd-in")] = lambda: bx.check(lib.monet_relu6_bwd_in(x.data_ptr(), dy.data_ptr(), dx.data_ptr(),
+                                                                          n, 0, sp))
+        out[("bwd", "bwd-out")] = lambda: bx.check(lib.monet_relu6_bwd_out(y.data_ptr(), dy.data_ptr(),
+                                                                            dx.data_ptr(), n, 0, sp))
+        out[("bwd", "bwd-mask")] = lambda: bx.check(lib.monet_relu_bwd_mask(mask.data_ptr(), dy.data_ptr(),
+                                                                             dx.data_ptr(), n, 0, sp))
+    elif kind == "dwconv":
+        d = net.conv_desc(op)
+        wgt, dw = bx.buf(4 * op.attrs["r"] * op.attrs["s"] * op.shape[3]), bx.buf(4 * op.attrs["r"] * op.attrs["s"] *
+                                                                                   op.shape[3])
+        wsb = lib.monet_dwconv_ws_bytes(C.byref(d))
+        ws = bx.buf(wsb)
+        need_dx = xin.kind != "input"
+        out[("fwd", "direct")] = lambda: bx.check(lib.monet_dwconv_fwd(C.byref(d), x.data_ptr(), wgt.data_ptr(),
+                                                                        y.data_ptr(), sp))
+
+        def dw_bwd():
+            if need_dx:
+                bx.check(lib.monet_dwconv_dgrad(C.byref(d), dy.data_ptr(), wgt.data_ptr(), dx.data_ptr(), 0, sp))
+            bx.check(lib.monet_dwconv_wgrad(C.byref(d), x.data_ptr(), dy.data_ptr(), dw.data_ptr(), ws.data_ptr(),
+                                            wsb, sp))
+        out[("bwd", "direct")] = dw_bwd
     elif kind == "dropout":
         seed = torch.zeros(1, dtype=torch.int64, device=bx.dev)
         pf = C.c_float(op.attrs["p"])

@@ -77,7 +77,7 @@ class Network:
         self.intermediate_bytes: dict[int, int] = {}
         nid = self.n + 1
         for op in ops:
-            if op.kind == "relu":
+            if op.kind in ("relu", "relu6"):
                 self.intermediate_of[op.id] = nid
                 self.intermediate_bytes[nid] = mask_bytes(op.numel)
                 nid += 1
@@ -100,9 +100,13 @@ class Network:
                 kind = "relu"
             elif kind == "addrelu":  # ... at a residual join
                 kind = "relu-join"
+            elif kind == "relu6":
+                kind = "relu"
+            elif kind == "dwconv":
+                kind = "conv"
             out[op.id] = kind
             if op.id in self.intermediate_of:
-                out[self.intermediate_of[op.id]] = "mask" if op.kind == "relu" else "idx"
+                out[self.intermediate_of[op.id]] = "mask" if op.kind in ("relu", "relu6") else "idx"
         return out
 
     # -------------------------------------------------------------- fixed region
@@ -195,10 +199,13 @@ class Network:
                 fwd.append(("gemm-splitk", ws))
             bwd.append(("gemm-splitk", lib.linear_ws_bytes(1, 3, n, fi, fo), x))
             bwd.append(("gemm", lib.linear_ws_bytes(0, 3, n, fi, fo), x))
-        elif op.kind == "relu":
-            fwd.append(("relu", 0))
+        elif op.kind in ("relu", "relu6"):
+            fwd.append((op.kind, 0))
             bwd += [("bwd-in", 0, x), ("bwd-out", 0, [op.id]),
                     ("bwd-mask", 0, [self.intermediate_of[op.id]])]
+        elif op.kind == "dwconv":  # depthwise: one direct kernel per pass, wgrad partials in ws
+            fwd.append(("direct", 0))
+            bwd.append(("direct", lib.dwconv_ws_bytes(self.conv_desc(op)), x))
         elif op.kind == "bn":
             fwd.append(("bn", 0))
             bwd += [("bwd-in", 0, x), ("bwd-out", 0, [op.id])]
@@ -282,7 +289,9 @@ BWD_IMPLS = {
     "addrelu": [("bwd-out", "output"), ("bwd-in", "input")],
     "relu": [("bwd-in", "input"), ("bwd-out", "output"), ("bwd-mask", "intermediate")],
     "maxpool": [("bwd-in", "input"), ("bwd-idx", "intermediate")],
-    "dropout": [("bwd-rng", "input")],  # catalog deps []: the keep-mask is regenerated from the step seed
+    "dropout": [("bwd-rng", "input")],
+    "relu6": [("bwd-in", "input"), ("bwd-out", "output"), ("bwd-mask", "intermediate")],
+    "dwconv": [("direct", "input")],  # catalog deps []: the keep-mask is regenerated from the step seed
     "add": [("bwd", "input")],
     "avgpool": [("bwd", "input")],
     "xent": [("bwd", "input")],
@@ -355,9 +364,20 @@ def trace_graph(model: torch.nn.Module, example_input: torch.Tensor, num_classes
             src = where[node.args[0].name]
             x = ops[src - 1]
             nid = len(ops) + 1
-            if isinstance(mod, torch.nn.Conv2d):
-                if mod.groups != 1 or _pair(mod.dilation) != 1:
-                    raise NotImplementedError(f"{node.target}: only dense, undilated convs")
+            if isinstance(mod, torch.nn.Conv2d) and mod.groups > 1:
+                _, hh, ww, cin = x.shape
+                if mod.groups != cin or mod.out_channels != cin or mod.bias is not None or _pair(mod.dilation) != 1:
+                    raise NotImplementedError(f"{node.target}: grouped convs only as bias-free depthwise")
+                r, s = mod.kernel_size
+                st, pd = _pair(mod.stride), _pair(mod.padding)
+                p = (hh + 2 * pd - r) // st + 1
+                q = (ww + 2 * pd - s) // st + 1
+                wt = mod.weight.detach().float().view(cin, r, s).permute(1, 2, 0).contiguous()  # [R][S][C]
+                ops.append(Op(nid, "dwconv", (src,), (n, p, q, cin), {"r": r, "s": s, "stride": st, "pad": pd},
+                              {"weight": wt}, node.target))
+            elif isinstance(mod, torch.nn.Conv2d):
+                if _pair(mod.dilation) != 1:
+                    raise NotImplementedError(f"{node.target}: only undilated convs")
                 r, s = mod.kernel_size
                 st, pd = _pair(mod.stride), _pair(mod.padding)
                 _, hh, ww, cin = x.shape
@@ -380,6 +400,8 @@ def trace_graph(model: torch.nn.Module, example_input: torch.Tensor, num_classes
                 ops[-1].attrs["running_var"] = mod.running_var.detach().float().clone()
             elif isinstance(mod, torch.nn.ReLU):
                 ops.append(Op(nid, "relu", (src,), x.shape, name=node.target))
+            elif isinstance(mod, torch.nn.ReLU6):
+                ops.append(Op(nid, "relu6", (src,), x.shape, name=node.target))
             elif isinstance(mod, torch.nn.MaxPool2d):
                 r = _pair(mod.kernel_size)
                 st, pd = _pair(mod.stride), _pair(mod.padding)
@@ -422,6 +444,14 @@ def trace_graph(model: torch.nn.Module, example_input: torch.Tensor, num_classes
                 where[node.name] = nid
             elif node.target is torch.flatten:
                 where[node.name] = where[node.args[0].name]  # avgpool already emits (N, C)
+            elif node.target is torch.nn.functional.adaptive_avg_pool2d:
+                osz = node.args[1] if len(node.args) > 1 else node.kwargs["output_size"]
+                if osz not in (1, (1, 1), [1, 1]):
+                    raise NotImplementedError(f"adaptive_avg_pool2d to {osz}")
+                src = where[node.args[0].name]
+                nid = len(ops) + 1
+                ops.append(Op(nid, "avgpool", (src,), (n, ops[src - 1].shape[3]), name=node.name))
+                where[node.name] = nid
             else:
                 raise NotImplementedError(f"function {node.target}")
         elif node.op == "call_method" and node.target in ("flatten", "view", "reshape"):

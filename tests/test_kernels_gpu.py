@@ -394,3 +394,59 @@ def test_dropout_mask_matches_oracle(cuda):
     lib.dropout_fwd(x.data_ptr(), y.data_ptr(), n, ctypes.c_float(p), seed.data_ptr(), salt, stream())
     assert int(seed.item()) == 8
     assert torch.equal(y != 0, torch.from_numpy(keep_mask(n, p, 8, salt)).to(cuda))
+
+
+@pytest.mark.parametrize("case", [(2, 14, 14, 32, 3, 1, 1), (3, 15, 13, 96, 3, 2, 1), (2, 8, 8, 8, 3, 2, 1),
+                                  (1, 33, 30, 144, 3, 1, 1)])
+def test_dwconv_passes(cuda, case):
+    n, h, w, c, r, stride, pad = case
+    g = torch.Generator().manual_seed(7)
+    x = torch.randn(n, h, w, c, generator=g)
+    wt = torch.randn(c, 1, r, r, generator=g) / r
+    d = N.conv_desc(n, h, w, c, c, r, r, stride, pad)
+    lib = N.lib()
+    xd = x.to(cuda)
+    wd = wt.view(c, r, r).permute(1, 2, 0).contiguous().to(cuda)  # [R][S][C]
+    y = torch.empty(n, d.p, d.q, c, device=cuda)
+    lib.dwconv_fwd(d, xd.data_ptr(), wd.data_ptr(), y.data_ptr(), stream())
+    xr = x.double().permute(0, 3, 1, 2).requires_grad_()
+    wr = wt.double().requires_grad_()
+    yr = F.conv2d(xr, wr, stride=stride, padding=pad, groups=c)
+    assert rel_err(y, yr.detach().permute(0, 2, 3, 1)) < 1e-6
+    dy = torch.randn(n, d.p, d.q, c, generator=g)
+    yr.backward(dy.double().permute(0, 3, 1, 2))
+    dyd = dy.to(cuda)
+    dx = torch.full((n, h, w, c), 2.0, device=cuda)
+    lib.dwconv_dgrad(d, dyd.data_ptr(), wd.data_ptr(), dx.data_ptr(), 1, stream())
+    assert rel_err(dx, 2.0 + xr.grad.permute(0, 2, 3, 1)) < 1e-6
+    wsb = lib.dwconv_ws_bytes(d)
+    ws = torch.empty(wsb // 4 + 1, device=cuda)
+    dw = torch.empty(r, r, c, device=cuda)
+    lib.dwconv_wgrad(d, xd.data_ptr(), dyd.data_ptr(), dw.data_ptr(), ws.data_ptr(), wsb, stream())
+    assert rel_err(dw, wr.grad.view(c, r, r).permute(1, 2, 0)) < 1e-5
+    dw2 = torch.empty_like(dw)
+    lib.dwconv_wgrad(d, xd.data_ptr(), dyd.data_ptr(), dw2.data_ptr(), ws.data_ptr(), wsb, stream())
+    assert torch.equal(dw, dw2)  # fixed-order two-level reduction: deterministic
+
+
+def test_relu6_mask_and_backward(cuda):
+    from oracle.bitmask import pack_sign_mask
+
+    n = 100003
+    g = torch.Generator().manual_seed(8)
+    x = (torch.randn(n, generator=g) * 5).to(cuda)
+    x[:64] = torch.tensor([0.0, 6.0, -0.0, 5.999, 6.001, 1e-30] * 10 + [3.0] * 4, device=cuda)
+    lib = N.lib()
+    y = torch.empty_like(x)
+    mask = torch.zeros((n + 31) // 32, dtype=torch.int32, device=cuda)
+    lib.relu6_fwd(x.data_ptr(), y.data_ptr(), mask.data_ptr(), n, stream())
+    assert torch.equal(y, torch.clamp(x, 0, 6))
+    gate = ((x > 0) & (x < 6)).cpu()
+    want = pack_sign_mask(torch.where(gate, 1.0, -1.0).numpy())
+    assert np.array_equal(mask.cpu().numpy().view(np.uint32), want)
+    dy = torch.randn(n, device=cuda)
+    ref = torch.where(gate.to(cuda), dy, torch.zeros_like(dy))
+    for fn, src in ((lib.relu_bwd_mask, mask), (lib.relu6_bwd_out, y), (lib.relu6_bwd_in, x)):
+        dx = torch.empty_like(x)
+        fn(src.data_ptr(), dy.data_ptr(), dx.data_ptr(), n, 0, stream())
+        assert torch.equal(dx, ref)

@@ -197,3 +197,50 @@ def _autograd_step_keep(model, x, y):
     loss.backward()
     opt.step()
     return loss.item()
+
+
+def test_oracle_mobilenet_v2_equals_autograd():
+    """Depthwise convs, ReLU6 (mask / output / input backward), residual adds without
+    ReLU, functional adaptive pool and dropout: torchvision MobileNet-V2 (width 0.25) at 64 x 64 (the last BNs then see 8 values per channel, not 2)."""
+    from nets import use_hash_dropout
+
+    torch.manual_seed(0)
+    model = torchvision.models.mobilenet_v2(num_classes=10, width_mult=0.25)
+    net = trace_graph(model, torch.empty(2, 3, 64, 64, device="meta"), 10)
+    kinds = {op.kind for op in net.ops}
+    assert {"dwconv", "relu6", "add", "avgpool", "dropout"} <= kinds
+    g = M.load_graph(net.graph_doc())
+    cat = M.load_catalog(net.catalog_doc(), g)
+    gen = torch.Generator().manual_seed(1)
+    x = torch.randn(2, 3, 64, 64, generator=gen)
+    y = torch.randint(0, 10, (2,), generator=gen)
+    scheds = [("store_everything", M.store_everything_schedule(g, cat))] + _planned(net, g, cat)
+    assert len(scheds) > 1, "no recompute schedule to test"
+    for name, sched in scheds:
+        ref_model = torchvision.models.mobilenet_v2(num_classes=10, width_mult=0.25)
+        ref_model.load_state_dict(model.state_dict())
+        use_hash_dropout(ref_model, net, seed=0)
+        ref_loss = _autograd_step(ref_model, x, y)
+        st = CpuState(net, dtype=torch.float64)
+        loss = run_step(st, M.schedule_to_doc(sched), x.double(), y)
+        assert abs(loss - ref_loss) <= TOL * abs(ref_loss), name
+        ref = {n: p.detach() for n, p in ref_model.named_parameters()}
+        ref_bn = {n: b for n, b in ref_model.named_buffers() if "running" in n}
+        got = params_nhwc(st)
+        for op in net.ops:
+            for pname in op.params:
+                want = ref[f"{op.name}.{pname}"]
+                have = got[(op.id, pname)]
+                if op.kind == "dwconv":
+                    have = have.permute(2, 0, 1).unsqueeze(1)
+                else:
+                    have = _torch_layout(net, op, pname, have, want)
+                # floor: BN biases feeding another BN (through a 1x1 conv) have a zero gradient;
+                # both sides then hold ~1e-16 rounding noise
+                err = (have.double() - want.double()).abs().max().item()
+                assert err <= TOL * max(want.double().abs().max().item(), 1e-3), (name, op.name, pname)
+            if op.kind == "bn":
+                rm, rv = st.running[op.id]
+                for have, want in ((rm, ref_bn[f"{op.name}.running_mean"]), (rv, ref_bn[f"{op.name}.running_var"])):
+                    err = (have.double() - want.double()).abs().max().item()
+                    assert err <= TOL * max(want.double().abs().max().item(), 1e-3), (name, op.name)
