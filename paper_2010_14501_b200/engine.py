@@ -35,7 +35,9 @@ from .schedule import Schedule, SimulationError, Trace, ledger, validate
 
 __all__ = ["Runtime", "Plan", "ExecResult", "BudgetExceeded", "execute", "lifetimes", "place_blocks"]
 
-ALIGN = 256
+ALIGN = 256        # fixed region (params, grads, momentum, ...): cudaMalloc-like alignment
+ARENA_ALIGN = 16   # arena blocks: TMA / float4 alignment; every graph size is a multiple of it
+                   # (tracer.py), so a gap-free packing is exactly the ledger peak
 
 
 class BudgetExceeded(RuntimeError):
@@ -572,7 +574,7 @@ def place_blocks(blocks, capacity: int = 0):
     peak = C.c_int64(0)
     cap = capacity
     rc = _native.lib().dll.monet_arena_plan(n, C.cast(sizes, C.c_void_p), C.cast(ta, C.c_void_p),
-                                       C.cast(tf, C.c_void_p), ALIGN, cap, C.cast(offs, C.c_void_p),
+                                       C.cast(tf, C.c_void_p), ARENA_ALIGN, cap, C.cast(offs, C.c_void_p),
                                        C.byref(peak))
     if rc == -12:
         raise BudgetExceeded(f"arena plan needs {peak.value} B, only {cap} B left under the budget")

@@ -51,15 +51,22 @@ class Op:
 
     @property
     def nbytes(self) -> int:
-        return self.numel * F32
+        return r16(self.numel * F32)
+
+
+def r16(b: int) -> int:
+    """Allocation size: the arena places blocks at 16-byte granularity (engine.ARENA_ALIGN),
+    so every size the graph and catalog report is already a multiple of 16 and the
+    reference's byte ledger equals the physical footprint of a gap-free packing."""
+    return (b + 15) // 16 * 16
 
 
 def mask_bytes(numel: int) -> int:
-    return (numel + 31) // 32 * 4
+    return r16((numel + 31) // 32 * 4)
 
 
 def idx_bytes(numel: int) -> int:
-    return (numel + 3) // 4 * 4
+    return r16(numel)
 
 
 class Network:
@@ -232,7 +239,7 @@ class Network:
             bwd.append(("bwd", 0, x))
         else:
             raise ValueError(op.kind)
-        return fwd, bwd
+        return [(nm, r16(ws)) for nm, ws in fwd], [(nm, r16(ws), deps) for nm, ws, deps in bwd]
 
     def catalog_doc(self, costs=None) -> dict:
         """Catalog with measured costs (``costs[(node, pass, name)]`` -> int ns) or the

@@ -107,7 +107,9 @@ def main():
     cat = R.load_catalog(cdoc, g)
     se = store_everything_case(gdoc, cdoc)
     act = se["peak"] - gdoc["params_bytes"]
-    budgets = [gdoc["params_bytes"] + int(f * act) for f in (0.5, 0.4)]
+    # several fractions: the reference heuristic's schedule is rejected by its own
+    # simulator at some budgets; the GPU test needs >= 1 that runs
+    budgets = [gdoc["params_bytes"] + int(f * act) for f in (0.5, 0.4, 0.55, 0.6)]
     cases = [solve_case(gdoc, cdoc, b, heuristic_only=True) for b in budgets]
     cases += [solve_case(gdoc, cdoc, b, node_limit=256) for b in budgets]
     r18 = {"graph": gdoc, "catalog": cdoc, "store_everything": se, "cases": cases}

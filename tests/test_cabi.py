@@ -68,7 +68,8 @@ def test_arena_plan_overlap_and_cap(lib):
         for j, (sj, aj, fj) in enumerate(blocks):
             if i < j and ai < fj and aj < fi:     # live together -> disjoint
                 assert offs[i] + si <= offs[j] or offs[j] + sj <= offs[i]
-    assert peak >= 1024 + 512 + 768
+    assert peak >= 1008 + 512 + 704  # blocks 0-2 live together, each rounded to 16 B (ARENA_ALIGN)
+    assert all(o % 16 == 0 for o in offs)
     from paper_2010_14501_b200.engine import BudgetExceeded
     with pytest.raises(BudgetExceeded):
         place_blocks(blocks, capacity=1000)
