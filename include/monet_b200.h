@@ -147,6 +147,17 @@ int monet_bnrelu_bwd(const float* x, const float* dz, float* dx, int accumulate,
                      const float* beta, const float* saved_mean, const float* saved_invstd, float* dgamma,
                      float* dbeta, int64_t rows, int c, void* scratch, void* stream);
 
+/* fused BN+ReLU6 (MobileNet-V2's expand / depthwise blocks): z = min(max(BN(x), 0), 6); the
+ * backward recomputes the gate 0 < BN(x) < 6 from x and the saved statistics. */
+int monet_bnrelu6_fwd_train(const float* x, float* z, const float* gamma, const float* beta, float* saved_mean,
+                            float* saved_invstd, float* running_mean, float* running_var, int64_t rows, int c,
+                            float eps, float momentum, int update_running, void* scratch, void* stream);
+int monet_bnrelu6_fwd_replay(const float* x, float* z, const float* gamma, const float* beta,
+                             const float* saved_mean, const float* saved_invstd, int64_t rows, int c, void* stream);
+int monet_bnrelu6_bwd(const float* x, const float* dz, float* dx, int accumulate, const float* gamma,
+                      const float* beta, const float* saved_mean, const float* saved_invstd, float* dgamma,
+                      float* dbeta, int64_t rows, int c, void* scratch, void* stream);
+
 /* --- residual add / gradient pass-through (K12) --------------------------- */
 int monet_add_fwd(const float* a, const float* b, float* y, int64_t n, void* stream);
 int monet_grad_pass(const float* dy, float* dx, int64_t n, float scale, int accumulate, void* stream);

@@ -46,7 +46,7 @@ class CpuState:
         self.mom = {k: torch.zeros_like(v) for k, v in self.params.items()}
         self.running = {op.id: [op.attrs["running_mean"].to(dtype).clone(),
                                 op.attrs["running_var"].to(dtype).clone()]
-                        for op in net.ops if op.kind in ("bn", "bnrelu")}
+                        for op in net.ops if op.kind in ("bn", "bnrelu", "bnrelu6")}
         self.saved = {}
         self.grads = {}
         self.seed = 0  # dropout step seed: the engine's device counter, advanced once per step
@@ -125,7 +125,7 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
                 gate = (x > 0) & (x < 6)
                 extra = pack_sign_mask(torch.where(gate, 1.0, -1.0).permute(0, 2, 3, 1).numpy()
                                        if x.dim() == 4 else torch.where(gate, 1.0, -1.0).numpy())
-        elif op.kind in ("bn", "bnrelu"):
+        elif op.kind in ("bn", "bnrelu", "bnrelu6"):
             g, b = P[(op.id, "weight")], P[(op.id, "bias")]
             if mode == "forward":
                 mean, invstd, var = _bn_stats(xs[0], op.attrs["eps"])
@@ -139,6 +139,8 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
             y = _bn_apply(xs[0], mean, invstd, g, b)
             if op.kind == "bnrelu":  # fused: relu(BN(x)); the BN output is never kept
                 y = torch.where(y > 0, y, torch.zeros_like(y))
+            elif op.kind == "bnrelu6":  # fused: relu6(BN(x))
+                y = torch.clamp(y, 0.0, 6.0)
         elif op.kind == "relu":
             x = xs[0]
             y = torch.where(x > 0, x, torch.zeros_like(x))
@@ -211,13 +213,16 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
                 s_ = x_of(op.id) if impl == "bwd-out" else x_of(j)
                 keep = (s_ > 0) & (s_ < 6)
             put_grad(j, torch.where(keep, dy, torch.zeros_like(dy)), created)
-        elif op.kind in ("bn", "bnrelu"):
+        elif op.kind in ("bn", "bnrelu", "bnrelu6"):
             j = op.deps[0]
             g, b = P[(op.id, "weight")], P[(op.id, "bias")]
             mean, invstd = state.saved[op.id]
             v = lambda t: t.view(1, -1, 1, 1)
             if op.kind == "bnrelu":  # gate by the recomputed BN output's sign (PAPER App. D, K10)
                 dy = torch.where(_bn_apply(x_of(j), mean, invstd, g, b) > 0, dy, torch.zeros_like(dy))
+            elif op.kind == "bnrelu6":
+                z = _bn_apply(x_of(j), mean, invstd, g, b)
+                dy = torch.where((z > 0) & (z < 6), dy, torch.zeros_like(dy))
             if impl == "bwd-in":
                 xhat = (x_of(j) - v(mean)) * v(invstd)
             else:

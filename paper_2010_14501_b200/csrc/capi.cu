@@ -812,9 +812,13 @@ int monet_bn_bwd_out(const float* y, const float* dy, float* dx, int accumulate,
 }
 
 // ------------------------------------------------------------------- fused BN+ReLU (K9 / K10)
-int monet_bnrelu_fwd_train(const float* x, float* z, const float* gamma, const float* beta, float* saved_mean,
-                           float* saved_invstd, float* running_mean, float* running_var, int64_t rows, int c,
-                           float eps, float momentum, int update_running, void* scratch, void* stream) {
+}  // extern "C"
+
+namespace {
+template <bool kSix>
+int bnrelu_fwd_train(const float* x, float* z, const float* gamma, const float* beta, float* saved_mean,
+                            float* saved_invstd, float* running_mean, float* running_var, int64_t rows, int c,
+                            float eps, float momentum, int update_running, void* scratch, void* stream) {
   if (c % 4) return -(int)cudaErrorInvalidValue;
   cudaStream_t st = S(stream);
   float* ws = static_cast<float*>(scratch);
@@ -822,34 +826,75 @@ int monet_bnrelu_fwd_train(const float* x, float* z, const float* gamma, const f
   bn_reduce_kernel<<<nb, kEwThreads, 0, st>>>(0, x, nullptr, nullptr, nullptr, rows, c, ws);
   bn_finalize_fwd_kernel<<<(c + 7) / 8, 256, 0, st>>>(ws, nb, rows, c, eps, momentum, update_running, saved_mean,
                                                       saved_invstd, running_mean, running_var);
-  bnrelu_apply_kernel<<<ew_blocks(rows * c / 4), kEwThreads, 0, st>>>(x, z, saved_mean, saved_invstd, gamma, beta,
-                                                                      rows, c);
+  bnrelu_apply_kernel<kSix><<<ew_blocks(rows * c / 4), kEwThreads, 0, st>>>(x, z, saved_mean, saved_invstd, gamma,
+                                                                            beta, rows, c);
   return last_error();
 }
 
-int monet_bnrelu_fwd_replay(const float* x, float* z, const float* gamma, const float* beta, const float* saved_mean,
-                            const float* saved_invstd, int64_t rows, int c, void* stream) {
+template <bool kSix>
+int bnrelu_fwd_replay(const float* x, float* z, const float* gamma, const float* beta,
+                             const float* saved_mean, const float* saved_invstd, int64_t rows, int c, void* stream) {
   if (c % 4) return -(int)cudaErrorInvalidValue;
-  bnrelu_apply_kernel<<<ew_blocks(rows * c / 4), kEwThreads, 0, S(stream)>>>(x, z, saved_mean, saved_invstd, gamma,
-                                                                             beta, rows, c);
+  bnrelu_apply_kernel<kSix><<<ew_blocks(rows * c / 4), kEwThreads, 0, S(stream)>>>(x, z, saved_mean, saved_invstd,
+                                                                                   gamma, beta, rows, c);
   return last_error();
 }
 
-int monet_bnrelu_bwd(const float* x, const float* dz, float* dx, int accumulate, const float* gamma,
-                     const float* beta, const float* saved_mean, const float* saved_invstd, float* dgamma,
-                     float* dbeta, int64_t rows, int c, void* scratch, void* stream) {
+template <bool kSix>
+int bnrelu_bwd(const float* x, const float* dz, float* dx, int accumulate, const float* gamma,
+                      const float* beta, const float* saved_mean, const float* saved_invstd, float* dgamma,
+                      float* dbeta, int64_t rows, int c, void* scratch, void* stream) {
   if (c % 4) return -(int)cudaErrorInvalidValue;
   cudaStream_t st = S(stream);
   float* ws = static_cast<float*>(scratch);
   int nb = bn_blocks(rows);
   float* coef_b = ws + (size_t)nb * 2 * c;
   float* coef_c = coef_b + c;
-  bn_reduce_kernel<<<nb, kEwThreads, 0, st>>>(3, x, dz, saved_mean, saved_invstd, rows, c, ws, gamma, beta);
+  bn_reduce_kernel<<<nb, kEwThreads, 0, st>>>(kSix ? 4 : 3, x, dz, saved_mean, saved_invstd, rows, c, ws, gamma,
+                                              beta);
   bn_finalize_bwd_kernel<<<(c + 7) / 8, 256, 0, st>>>(ws, nb, c, rows, saved_mean, saved_invstd, gamma,
                                                       saved_invstd, coef_b, coef_c, dgamma, dbeta);
-  bnrelu_bwd_apply_kernel<<<ew_blocks(rows * c / 4), kEwThreads, 0, st>>>(
+  bnrelu_bwd_apply_kernel<kSix><<<ew_blocks(rows * c / 4), kEwThreads, 0, st>>>(
       x, dz, dx, saved_mean, beta, gamma, saved_invstd, coef_b, coef_c, rows, c, accumulate);
   return last_error();
+}
+}  // namespace
+
+extern "C" {
+
+int monet_bnrelu_fwd_train(const float* x, float* z, const float* gamma, const float* beta, float* saved_mean,
+                           float* saved_invstd, float* running_mean, float* running_var, int64_t rows, int c,
+                           float eps, float momentum, int update_running, void* scratch, void* stream) {
+  return bnrelu_fwd_train<false>(x, z, gamma, beta, saved_mean, saved_invstd, running_mean, running_var, rows, c, eps,
+                                 momentum, update_running, scratch, stream);
+}
+int monet_bnrelu_fwd_replay(const float* x, float* z, const float* gamma, const float* beta, const float* saved_mean,
+                            const float* saved_invstd, int64_t rows, int c, void* stream) {
+  return bnrelu_fwd_replay<false>(x, z, gamma, beta, saved_mean, saved_invstd, rows, c, stream);
+}
+int monet_bnrelu_bwd(const float* x, const float* dz, float* dx, int accumulate, const float* gamma,
+                     const float* beta, const float* saved_mean, const float* saved_invstd, float* dgamma,
+                     float* dbeta, int64_t rows, int c, void* scratch, void* stream) {
+  return bnrelu_bwd<false>(x, dz, dx, accumulate, gamma, beta, saved_mean, saved_invstd, dgamma, dbeta, rows, c,
+                           scratch, stream);
+}
+
+// fused BN+ReLU6 (MobileNet-V2): z = min(max(BN(x), 0), 6), backward gated by 0 < BN(x) < 6
+int monet_bnrelu6_fwd_train(const float* x, float* z, const float* gamma, const float* beta, float* saved_mean,
+                            float* saved_invstd, float* running_mean, float* running_var, int64_t rows, int c,
+                            float eps, float momentum, int update_running, void* scratch, void* stream) {
+  return bnrelu_fwd_train<true>(x, z, gamma, beta, saved_mean, saved_invstd, running_mean, running_var, rows, c, eps,
+                                momentum, update_running, scratch, stream);
+}
+int monet_bnrelu6_fwd_replay(const float* x, float* z, const float* gamma, const float* beta,
+                             const float* saved_mean, const float* saved_invstd, int64_t rows, int c, void* stream) {
+  return bnrelu_fwd_replay<true>(x, z, gamma, beta, saved_mean, saved_invstd, rows, c, stream);
+}
+int monet_bnrelu6_bwd(const float* x, const float* dz, float* dx, int accumulate, const float* gamma,
+                      const float* beta, const float* saved_mean, const float* saved_invstd, float* dgamma,
+                      float* dbeta, int64_t rows, int c, void* scratch, void* stream) {
+  return bnrelu_bwd<true>(x, dz, dx, accumulate, gamma, beta, saved_mean, saved_invstd, dgamma, dbeta, rows, c,
+                          scratch, stream);
 }
 
 // ------------------------------------------------------------------- add / pass

@@ -251,6 +251,7 @@ __host__ __device__ inline BnLayout bn_layout(int C) {
 // mode 2: sum dy, sum dy*xhat      (backward, xhat = (y-beta)/gamma)
 // mode 3: as mode 1 with dy = dz * [gamma*xhat + beta > 0]  (fused BN+ReLU
 //         backward from x; p2 / p3 = gamma / beta)
+// mode 4: as mode 3 with the ReLU6 gate [0 < gamma*xhat + beta < 6]  (fused BN+ReLU6)
 __global__ void bn_reduce_kernel(int mode, const float* __restrict__ x, const float* __restrict__ dy,
                                  const float* __restrict__ p0, const float* __restrict__ p1, long long rows, int C,
                                  float* __restrict__ ws, const float* __restrict__ p2 = nullptr,
@@ -272,16 +273,18 @@ __global__ void bn_reduce_kernel(int mode, const float* __restrict__ x, const fl
         a = *reinterpret_cast<const float4*>(p0 + 4 * q);  // mean | beta
         b = *reinterpret_cast<const float4*>(p1 + 4 * q);  // invstd | 1/gamma
       }
-      if (mode == 3) {
+      if (mode >= 3) {
         ga = *reinterpret_cast<const float4*>(p2 + 4 * q);
         be = *reinterpret_cast<const float4*>(p3 + 4 * q);
       }
       auto acc = [&](const float4& v, float4 g) {
-        if (mode == 3) {  // the ReLU's gradient gate, recomputed with the forward's formula
-          g.x = ((v.x - a.x) * b.x * ga.x + be.x > 0.f) ? g.x : 0.f;
-          g.y = ((v.y - a.y) * b.y * ga.y + be.y > 0.f) ? g.y : 0.f;
-          g.z = ((v.z - a.z) * b.z * ga.z + be.z > 0.f) ? g.z : 0.f;
-          g.w = ((v.w - a.w) * b.w * ga.w + be.w > 0.f) ? g.w : 0.f;
+        if (mode >= 3) {  // the ReLU's gradient gate, recomputed with the forward's formula
+          const bool six = mode == 4;
+          auto gate = [six](float u) { return six ? (u > 0.f && u < 6.f) : u > 0.f; };
+          g.x = gate((v.x - a.x) * b.x * ga.x + be.x) ? g.x : 0.f;
+          g.y = gate((v.y - a.y) * b.y * ga.y + be.y) ? g.y : 0.f;
+          g.z = gate((v.z - a.z) * b.z * ga.z + be.z) ? g.z : 0.f;
+          g.w = gate((v.w - a.w) * b.w * ga.w + be.w) ? g.w : 0.f;
         }
         if (mode == 0) {
           s1[0] += v.x; s1[1] += v.y; s1[2] += v.z; s1[3] += v.w;
@@ -453,6 +456,7 @@ __global__ void bn_bwd_apply_kernel(const float* __restrict__ s, const float* __
 // Fused BN+ReLU forward apply: z = max((x - mean) * invstd * gamma + beta, 0)
 // (same expression as bn_apply, so a recompute is bit-identical and the
 // backward's recomputed gate matches the forward's sign exactly).
+template <bool kSix = false>
 __global__ void bnrelu_apply_kernel(const float* __restrict__ x, float* z, const float* __restrict__ mean,
                                     const float* __restrict__ invstd, const float* __restrict__ gamma,
                                     const float* __restrict__ beta, long long rows, int C) {
@@ -466,15 +470,16 @@ __global__ void bnrelu_apply_kernel(const float* __restrict__ x, float* z, const
     const float4 s = *reinterpret_cast<const float4*>(invstd + 4 * q);
     const float4 g = *reinterpret_cast<const float4*>(gamma + 4 * q);
     const float4 b = *reinterpret_cast<const float4*>(beta + 4 * q);
-    v.x = fmaxf((v.x - m.x) * s.x * g.x + b.x, 0.f);
-    v.y = fmaxf((v.y - m.y) * s.y * g.y + b.y, 0.f);
-    v.z = fmaxf((v.z - m.z) * s.z * g.z + b.z, 0.f);
-    v.w = fmaxf((v.w - m.w) * s.w * g.w + b.w, 0.f);
+    v.x = relu_val<kSix>((v.x - m.x) * s.x * g.x + b.x);
+    v.y = relu_val<kSix>((v.y - m.y) * s.y * g.y + b.y);
+    v.z = relu_val<kSix>((v.z - m.z) * s.z * g.z + b.z);
+    v.w = relu_val<kSix>((v.w - m.w) * s.w * g.w + b.w);
     *reinterpret_cast<float4*>(z + 4 * i) = v;
   }
 }
 
 // Fused BN+ReLU backward apply from x: dy = dz * [bn(x) > 0]; dx = k*dy + cb*x + cc
+template <bool kSix = false>
 __global__ void bnrelu_bwd_apply_kernel(const float* __restrict__ x, const float* __restrict__ dz, float* dx,
                                         const float* __restrict__ mean, const float* __restrict__ beta,
                                         const float* __restrict__ gamma, const float* __restrict__ invstd,
@@ -493,10 +498,10 @@ __global__ void bnrelu_bwd_apply_kernel(const float* __restrict__ x, const float
     const float4 is = *reinterpret_cast<const float4*>(invstd + 4 * q);
     const float4 cb = *reinterpret_cast<const float4*>(coef_b + 4 * q);
     const float4 cc = *reinterpret_cast<const float4*>(coef_c + 4 * q);
-    g.x = ((v.x - m.x) * is.x * ga.x + be.x > 0.f) ? g.x : 0.f;
-    g.y = ((v.y - m.y) * is.y * ga.y + be.y > 0.f) ? g.y : 0.f;
-    g.z = ((v.z - m.z) * is.z * ga.z + be.z > 0.f) ? g.z : 0.f;
-    g.w = ((v.w - m.w) * is.w * ga.w + be.w > 0.f) ? g.w : 0.f;
+    g.x = relu_gate<kSix>((v.x - m.x) * is.x * ga.x + be.x) ? g.x : 0.f;
+    g.y = relu_gate<kSix>((v.y - m.y) * is.y * ga.y + be.y) ? g.y : 0.f;
+    g.z = relu_gate<kSix>((v.z - m.z) * is.z * ga.z + be.z) ? g.z : 0.f;
+    g.w = relu_gate<kSix>((v.w - m.w) * is.w * ga.w + be.w) ? g.w : 0.f;
     float4 o;
     o.x = fmaf(ga.x * is.x, g.x, fmaf(cb.x, v.x, cc.x));
     o.y = fmaf(ga.y * is.y, g.y, fmaf(cb.y, v.y, cc.y));

@@ -137,7 +137,7 @@ class Runtime:
         self.bn = {}
         pos = 0
         for op in self.net.ops:
-            if op.kind not in ("bn", "bnrelu"):
+            if op.kind not in ("bn", "bnrelu", "bnrelu6"):
                 continue
             c = op.shape[-1]
             views = [stats[pos + j * c: pos + (j + 1) * c] for j in range(4)]
@@ -294,18 +294,20 @@ class Runtime:
                                  C.c_float(op.attrs["momentum"]), 1, self.scratch_ptr, None)))
                 else:  # recompute: reuse saved statistics, running stats untouched
                     out.append(("k", lib.monet_bn_fwd_replay, (xs[0], y, gma, bta, sm, si, rows, c, None)))
-            elif op.kind == "bnrelu":
+            elif op.kind in ("bnrelu", "bnrelu6"):
                 c = op.shape[-1]
                 rows = op.numel // c
                 sm, si, rm, rv = (t.data_ptr() for t in self.bn[op.id])
                 gma = self.pview[(op.id, "weight")].data_ptr()
                 bta = self.pview[(op.id, "bias")].data_ptr()
+                six = op.kind == "bnrelu6"
                 if s.kind == "forward":
-                    out.append(("k", lib.monet_bnrelu_fwd_train,
+                    out.append(("k", lib.monet_bnrelu6_fwd_train if six else lib.monet_bnrelu_fwd_train,
                                 (xs[0], y, gma, bta, sm, si, rm, rv, rows, c, C.c_float(op.attrs["eps"]),
                                  C.c_float(op.attrs["momentum"]), 1, self.scratch_ptr, None)))
                 else:
-                    out.append(("k", lib.monet_bnrelu_fwd_replay, (xs[0], y, gma, bta, sm, si, rows, c, None)))
+                    out.append(("k", lib.monet_bnrelu6_fwd_replay if six else lib.monet_bnrelu_fwd_replay,
+                                (xs[0], y, gma, bta, sm, si, rows, c, None)))
             elif op.kind == "relu":
                 mid = net.intermediate_of[op.id]
                 mask = P(("a", mid)) if mid in s.planned_ints else None
@@ -407,12 +409,12 @@ class Runtime:
             else:
                 out.append(("k", lib.monet_bn_bwd_out, (P(("in", op.id)), dy, P(("g", j)), acc(j), gma, bta, si,
                                                        dg, db, rows, c, self.scratch_ptr, None)))
-        elif op.kind == "bnrelu":
+        elif op.kind in ("bnrelu", "bnrelu6"):
             c = op.shape[-1]
             rows = op.numel // c
             j = op.deps[0]
             sm, si, _, _ = (t.data_ptr() for t in self.bn[op.id])
-            out.append(("k", lib.monet_bnrelu_bwd,
+            out.append(("k", lib.monet_bnrelu6_bwd if op.kind == "bnrelu6" else lib.monet_bnrelu_bwd,
                         (P(("in", j)), dy, P(("g", j)), acc(j), self.pview[(op.id, "weight")].data_ptr(),
                          self.pview[(op.id, "bias")].data_ptr(), sm, si, self.gview[(op.id, "weight")].data_ptr(),
                          self.gview[(op.id, "bias")].data_ptr(), rows, c, self.scratch_ptr, None)))

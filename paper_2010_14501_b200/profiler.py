@@ -133,7 +133,7 @@ def _local_calls(bx: _Bench, net, op):
             x.data_ptr(), dy.data_ptr(), dx.data_ptr(), 0, g_, m_, s_, dg, db, rows, c, scratch.data_ptr(), sp))
         out[("bwd", "bwd-out")] = lambda: bx.check(lib.monet_bn_bwd_out(
             y.data_ptr(), dy.data_ptr(), dx.data_ptr(), 0, g_, b_, s_, dg, db, rows, c, scratch.data_ptr(), sp))
-    elif kind == "bnrelu":
+    elif kind in ("bnrelu", "bnrelu6"):
         c = op.shape[-1]
         rows = n // c
         ch = [bx.buf(4 * c) for _ in range(8)]
@@ -141,10 +141,13 @@ def _local_calls(bx: _Bench, net, op):
             t.abs_().add_(0.5)
         scratch = bx.buf(lib.monet_bn_scratch_bytes(rows, c))
         g_, b_, m_, s_, rm, rv, dg, db = (t.data_ptr() for t in ch)
-        out[("fwd", "bnrelu")] = lambda: bx.check(lib.monet_bnrelu_fwd_train(
+        six = kind == "bnrelu6"
+        fwd_fn = lib.monet_bnrelu6_fwd_train if six else lib.monet_bnrelu_fwd_train
+        bwd_fn = lib.monet_bnrelu6_bwd if six else lib.monet_bnrelu_bwd
+        out[("fwd", kind)] = lambda: bx.check(fwd_fn(
             x.data_ptr(), y.data_ptr(), g_, b_, m_, s_, rm, rv, rows, c, C.c_float(1e-5), C.c_float(0.1), 1,
             scratch.data_ptr(), sp))
-        out[("bwd", "bwd-in")] = lambda: bx.check(lib.monet_bnrelu_bwd(
+        out[("bwd", "bwd-in")] = lambda: bx.check(bwd_fn(
             x.data_ptr(), dy.data_ptr(), dx.data_ptr(), 0, g_, b_, m_, s_, dg, db, rows, c, scratch.data_ptr(), sp))
     elif kind == "add":
         x2 = bx.buf(op.nbytes)

@@ -74,7 +74,7 @@ class Network:
 
     def __init__(self, ops: list[Op], batch: int, num_classes: int):
         self.ops = ops
-        self.fused = any(op.kind == "bnrelu" for op in ops)
+        self.fused = any(op.kind in ("bnrelu", "bnrelu6") for op in ops)
         self.pair_variants = False  # offer the cta_group::2 conv variant in the catalog
         self.batch = batch
         self.num_classes = num_classes
@@ -103,7 +103,7 @@ class Network:
             kind = op.kind
             if kind == "relu" and self.op(op.deps[0]).kind == "add":
                 kind = "relu-join"
-            elif kind == "bnrelu":   # a fused op's output is a ReLU output
+            elif kind in ("bnrelu", "bnrelu6"):   # a fused op's output is a ReLU output
                 kind = "relu"
             elif kind == "addrelu":  # ... at a residual join
                 kind = "relu-join"
@@ -126,13 +126,13 @@ class Network:
         return sum(t.numel() for _, _, t in self.param_items())
 
     def bn_channels(self) -> int:
-        return sum(op.shape[-1] for op in self.ops if op.kind in ("bn", "bnrelu"))
+        return sum(op.shape[-1] for op in self.ops if op.kind in ("bn", "bnrelu", "bnrelu6"))
 
     def scratch_bytes(self) -> int:
         lib = _native.lib()
         s = 0
         for op in self.ops:
-            if op.kind in ("bn", "bnrelu") or (op.kind == "conv" and "bias" in op.params):
+            if op.kind in ("bn", "bnrelu", "bnrelu6") or (op.kind == "conv" and "bias" in op.params):
                 rows = op.numel // op.shape[-1]  # conv bias gradient: per-channel sum of dy
                 s = max(s, lib.bn_scratch_bytes(rows, op.shape[-1]))
         s = max(s, lib.xent_scratch_bytes(self.batch))
@@ -216,8 +216,8 @@ class Network:
         elif op.kind == "bn":
             fwd.append(("bn", 0))
             bwd += [("bwd-in", 0, x), ("bwd-out", 0, [op.id])]
-        elif op.kind == "bnrelu":  # fused BN+ReLU: backward from the BN input only (K10)
-            fwd.append(("bnrelu", 0))
+        elif op.kind in ("bnrelu", "bnrelu6"):  # fused BN+ReLU(6): backward from the BN input only (K10)
+            fwd.append((op.kind, 0))
             bwd.append(("bwd-in", 0, x))
         elif op.kind == "addrelu":  # fused residual join + ReLU: gate from the output or the inputs
             fwd.append(("addrelu", 0))
@@ -293,6 +293,7 @@ BWD_IMPLS = {
     "fc": [("gemm-splitk", "input"), ("gemm", "input")],
     "bn": [("bwd-in", "input"), ("bwd-out", "output")],
     "bnrelu": [("bwd-in", "input")],
+    "bnrelu6": [("bwd-in", "input")],
     "addrelu": [("bwd-out", "output"), ("bwd-in", "input")],
     "relu": [("bwd-in", "input"), ("bwd-out", "output"), ("bwd-mask", "intermediate")],
     "maxpool": [("bwd-in", "input"), ("bwd-idx", "intermediate")],
@@ -322,11 +323,15 @@ def fuse_bn_relu(ops: list[Op]) -> list[Op]:
         for j in op.deps:
             readers.setdefault(j, []).append(op.id)
     fused_into: dict[int, int] = {}  # relu id -> bn id
+    six: set[int] = set()            # bn ids fused with a ReLU6 (MobileNet-V2)
     for op in ops:
         if op.kind in ("bn", "add") and len(readers.get(op.id, [])) == 1 and len(set(op.deps)) == len(op.deps):
             r = ops[readers[op.id][0] - 1]
             if r.kind == "relu" and r.deps == (op.id,):
                 fused_into[r.id] = op.id
+            elif r.kind == "relu6" and op.kind == "bn" and r.deps == (op.id,):
+                fused_into[r.id] = op.id
+                six.add(op.id)
     new_id: dict[int, int] = {}
     out: list[Op] = []
     for op in ops:
@@ -336,8 +341,8 @@ def fuse_bn_relu(ops: list[Op]) -> list[Op]:
         nid = len(out) + 1
         new_id[op.id] = nid
         fused = op.id in fused_into.values()
-        kind = {"bn": "bnrelu", "add": "addrelu"}[op.kind] if fused else op.kind
-        name = op.name + "+relu" if fused else op.name
+        kind = ("bnrelu6" if op.id in six else {"bn": "bnrelu", "add": "addrelu"}[op.kind]) if fused else op.kind
+        name = op.name + ("+relu6" if op.id in six else "+relu") if fused else op.name
         out.append(Op(nid, kind, tuple(new_id[j] for j in op.deps), op.shape, dict(op.attrs), op.params, name))
     return out
 

@@ -180,7 +180,8 @@ def test_vgg_style_engine(cuda):
     assert int(rt.seed.item()) == 1  # advanced once by the optimizer group
 
 
-def test_mobilenet_v2_engine(cuda):
+@pytest.mark.parametrize("fuse", [False, True])
+def test_mobilenet_v2_engine(cuda, fuse):
     """torchvision MobileNet-V2 (width 0.25, 64 x 64): depthwise convs, ReLU6 masks,
     residual adds, dropout under a recompute schedule -- ledger = simulate(), recomputes
     bit-identical, loss / weights / gradients = CPU oracle (fed the GPU activations)."""
@@ -188,7 +189,8 @@ def test_mobilenet_v2_engine(cuda):
 
     torch.manual_seed(0)
     model = torchvision.models.mobilenet_v2(num_classes=10, width_mult=0.25)
-    net = M.trace_graph(model, torch.empty(4, 3, 64, 64, device="meta"), 10)
+    net = M.trace_graph(model, torch.empty(4, 3, 64, 64, device="meta"), 10, fuse=fuse)
+    assert any(op.kind == "bnrelu6" for op in net.ops) == fuse
     g = M.load_graph(net.graph_doc())
     cat = M.load_catalog(net.catalog_doc(), g)
     se = M.store_everything_schedule(g, cat)

@@ -199,16 +199,18 @@ def _autograd_step_keep(model, x, y):
     return loss.item()
 
 
-def test_oracle_mobilenet_v2_equals_autograd():
+@pytest.mark.parametrize("fuse", [False, True])
+def test_oracle_mobilenet_v2_equals_autograd(fuse):
     """Depthwise convs, ReLU6 (mask / output / input backward), residual adds without
     ReLU, functional adaptive pool and dropout: torchvision MobileNet-V2 (width 0.25) at 64 x 64 (the last BNs then see 8 values per channel, not 2)."""
     from nets import use_hash_dropout
 
     torch.manual_seed(0)
     model = torchvision.models.mobilenet_v2(num_classes=10, width_mult=0.25)
-    net = trace_graph(model, torch.empty(2, 3, 64, 64, device="meta"), 10)
+    net = trace_graph(model, torch.empty(2, 3, 64, 64, device="meta"), 10, fuse=fuse)
     kinds = {op.kind for op in net.ops}
-    assert {"dwconv", "relu6", "add", "avgpool", "dropout"} <= kinds
+    assert {"dwconv", "add", "avgpool", "dropout"} <= kinds
+    assert ("bnrelu6" in kinds) == fuse and ("relu6" in kinds) != fuse
     g = M.load_graph(net.graph_doc())
     cat = M.load_catalog(net.catalog_doc(), g)
     gen = torch.Generator().manual_seed(1)
@@ -229,7 +231,7 @@ def test_oracle_mobilenet_v2_equals_autograd():
         got = params_nhwc(st)
         for op in net.ops:
             for pname in op.params:
-                want = ref[f"{op.name}.{pname}"]
+                want = ref[f"{op.name.removesuffix('+relu6')}.{pname}"]
                 have = got[(op.id, pname)]
                 if op.kind == "dwconv":
                     have = have.permute(2, 0, 1).unsqueeze(1)
@@ -239,8 +241,9 @@ def test_oracle_mobilenet_v2_equals_autograd():
                 # both sides then hold ~1e-16 rounding noise
                 err = (have.double() - want.double()).abs().max().item()
                 assert err <= TOL * max(want.double().abs().max().item(), 1e-3), (name, op.name, pname)
-            if op.kind == "bn":
+            if op.kind in ("bn", "bnrelu6"):
                 rm, rv = st.running[op.id]
-                for have, want in ((rm, ref_bn[f"{op.name}.running_mean"]), (rv, ref_bn[f"{op.name}.running_var"])):
+                base = op.name.removesuffix("+relu6")
+                for have, want in ((rm, ref_bn[f"{base}.running_mean"]), (rv, ref_bn[f"{base}.running_var"])):
                     err = (have.double() - want.double()).abs().max().item()
                     assert err <= TOL * max(want.double().abs().max().item(), 1e-3), (name, op.name)
