@@ -88,6 +88,13 @@ int monet_dropout_bwd(const float* dy, float* dx, int64_t n, float p, const unsi
                       int accumulate, void* stream);
 int monet_seed_advance(unsigned long long* seed, void* stream);
 
+/* --- channel concat (GoogLeNet inception outputs) ---------------------------------
+ * NHWC channel-slice copy: dst[pix][dst_off + j] (+)= src[pix][src_off + j], j < count
+ * (all channel counts and offsets multiples of 4).  Concat forward = one call per input
+ * into its channel range; backward = one call per input taking its slice of dy. */
+int monet_channel_copy(const float* src, int src_c, int src_off, float* dst, int dst_c, int dst_off, int count,
+                       int64_t pixels, int accumulate, void* stream);
+
 /* --- depthwise conv (groups = C; MobileNet-V2) ------------------------------------
  * NHWC, d->k == d->c, R*S <= 9, weights [R][S][C].  HBM-bound direct kernels.
  * wgrad reduces in two fixed-order levels through ws (monet_dwconv_ws_bytes). */

@@ -115,6 +115,8 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
             y = F.conv2d(xs[0], P[(op.id, "weight")], P.get((op.id, "bias")), stride=a["stride"], padding=a["pad"])
         elif op.kind == "dropout":
             y = xs[0] * _dropout_scale(op, xs[0], state.seed)
+        elif op.kind == "concat":
+            y = torch.cat([x_of(j) for j in op.attrs["inputs"]], dim=1)
         elif op.kind == "dwconv":
             a = op.attrs
             y = F.conv2d(xs[0], P[(op.id, "weight")], stride=a["stride"], padding=a["pad"], groups=xs[0].shape[1])
@@ -153,7 +155,8 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
             y = torch.where(y > 0, y, torch.zeros_like(y))
         elif op.kind == "maxpool":
             a = op.attrs
-            y, flat = F.max_pool2d(xs[0], a["r"], a["stride"], a["pad"], return_indices=True)
+            y, flat = F.max_pool2d(xs[0], a["r"], a["stride"], a["pad"], ceil_mode=a.get("ceil", False),
+                                   return_indices=True)
             if want_int:
                 extra = _window_index(flat, xs[0].shape, y.shape, a)
         elif op.kind == "avgpool":
@@ -191,6 +194,12 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
                 state.grads[(op.id, "bias")] = dy.sum(dim=(0, 2, 3))
         elif op.kind == "dropout":
             put_grad(op.deps[0], dy * _dropout_scale(op, dy, state.seed), created)
+        elif op.kind == "concat":
+            off = 0
+            for j in op.attrs["inputs"]:
+                cj = net.op(j).shape[3]
+                put_grad(j, dy[:, off:off + cj].contiguous(), created)
+                off += cj
         elif op.kind == "dwconv":
             a = op.attrs
             j = op.deps[0]
@@ -264,7 +273,8 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
                 widx = x_of(net.intermediate_of[op.id])
                 flat = _flat_index(widx, shp, dy.shape, a)
             else:
-                _, flat = F.max_pool2d(x_of(j), a["r"], a["stride"], a["pad"], return_indices=True)
+                _, flat = F.max_pool2d(x_of(j), a["r"], a["stride"], a["pad"], ceil_mode=a.get("ceil", False),
+                                       return_indices=True)
             dx = torch.zeros(shp, dtype=dt).view(shp[0], shp[1], -1)
             dx.scatter_add_(2, flat.view(shp[0], shp[1], -1), dy.reshape(shp[0], shp[1], -1))
             put_grad(j, dx.view(shp), created)

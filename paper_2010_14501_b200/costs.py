@@ -28,6 +28,8 @@ def analytic_cost(net, op, pass_, name) -> int:
         passes = 1 if net.op(op.deps[0]).kind == "input" else 2
         bias = 4.0 * n if "bias" in op.params else 0.0  # bias gradient: one more read of dy
         return _ns(passes * flops, 8.0 * (x.numel + n) + bias, launches=3)
+    if op.kind == "concat":  # each input read once, output written once (bwd: slices of dy)
+        return _ns(nbytes=8.0 * n, launches=len(op.attrs["inputs"]))
     if op.kind == "dropout":  # r4 w4, mask regenerated (never stored)
         return _ns(nbytes=8.0 * n)
     if op.kind == "fc":

@@ -707,6 +707,19 @@ int monet_relu6_bwd_in(const float* x, const float* dy, float* dx, int64_t n, in
   return monet_relu6_bwd_out(x, dy, dx, n, accumulate, stream);
 }
 
+// ------------------------------------------------------------ concat slices
+int monet_channel_copy(const float* src, int src_c, int src_off, float* dst, int dst_c, int dst_off, int count,
+                       int64_t pixels, int accumulate, void* stream) {
+  if (count % 4 || src_c % 4 || dst_c % 4 || src_off % 4 || dst_off % 4 || src_off + count > src_c ||
+      dst_off + count > dst_c)
+    return -(int)cudaErrorInvalidValue;
+  if (pixels == 0 || count == 0) return 0;
+  channel_copy_kernel<<<ew_blocks(pixels * (count / 4)), kEwThreads, 0, S(stream)>>>(src, src_c, src_off, dst, dst_c,
+                                                                                      dst_off, count, pixels,
+                                                                                      accumulate);
+  return last_error();
+}
+
 // ------------------------------------------------------------ depthwise conv
 static int dw_check(const monet_conv_desc* d) {
   if (!d || d->c % 4 || d->k != d->c || d->r * d->s > kDwMaxTaps || d->n <= 0) return -(int)cudaErrorInvalidValue;

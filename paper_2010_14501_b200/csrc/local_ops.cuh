@@ -773,6 +773,31 @@ __global__ void dropout_kernel(const float* __restrict__ x, float* y, long long 
 
 __global__ void seed_advance_kernel(unsigned long long* seed) { *seed += 1; }
 
+// ---------------------------------------------------------------- concat
+// Channel-slice copy between NHWC tensors (the concat of GoogLeNet's inception
+// branches): dst[pix, dst_off + j] (+)= src[pix, src_off + j], j < count.
+// Forward puts each input into its channel range; backward takes the slices out.
+__global__ void channel_copy_kernel(const float* __restrict__ src, int src_c, int src_off, float* dst, int dst_c,
+                                    int dst_off, int count, long long pixels, int accumulate) {
+  const int q4 = count / 4;
+  const long long total = pixels * q4;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long pix = i / q4;
+    const int j = (int)(i - pix * q4) * 4;
+    float4 v = *reinterpret_cast<const float4*>(src + pix * src_c + src_off + j);
+    float4* o = reinterpret_cast<float4*>(dst + pix * dst_c + dst_off + j);
+    if (accumulate) {
+      const float4 a = *o;
+      v.x += a.x;
+      v.y += a.y;
+      v.z += a.z;
+      v.w += a.w;
+    }
+    *o = v;
+  }
+}
+
 // db[k] = sum_n dy[n, k]  (fixed order)
 __global__ void col_sum_kernel(const float* __restrict__ dy, float* db, int N, int K) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;

@@ -271,6 +271,12 @@ class Runtime:
                                                                s.workspace, None), d))
                 else:
                     out.append(("k", lib.monet_conv_fwd, (v, C.byref(d), xs[0], wt, y, ws, s.workspace, None), d))
+            elif op.kind == "concat":
+                pix, ct, off = op.numel // op.shape[3], op.shape[3], 0
+                for j in op.attrs["inputs"]:
+                    cj = net.op(j).shape[3]
+                    out.append(("k", lib.monet_channel_copy, (P(("in", j)), cj, 0, y, ct, off, cj, pix, 0, None)))
+                    off += cj
             elif op.kind == "dwconv":
                 d = net.conv_desc(op)
                 out.append(("k", lib.monet_dwconv_fwd, (C.byref(d), xs[0], self.pview[(op.id, "weight")].data_ptr(),
@@ -372,6 +378,13 @@ class Runtime:
                 out.append(("k", lib.monet_bias_grad, (dy, self.gview[(op.id, "bias")].data_ptr(),
                                                        op.numel // op.shape[-1], op.shape[-1], 0, self.scratch_ptr,
                                                        None)))
+        elif op.kind == "concat":
+            pix, ct, off = op.numel // op.shape[3], op.shape[3], 0
+            for j in op.attrs["inputs"]:
+                cj = net.op(j).shape[3]
+                if net.grad_bytes(net.op(j)) > 0:
+                    out.append(("k", lib.monet_channel_copy, (dy, ct, off, P(("g", j)), cj, 0, cj, pix, acc(j), None)))
+                off += cj
         elif op.kind == "dwconv":
             d = net.conv_desc(op)
             j = op.deps[0]

@@ -182,6 +182,20 @@ def _local_calls(bx: _Bench, net, op):
         out[("fwd", "avgpool")] = lambda: bx.check(lib.monet_avgpool_fwd(x.data_ptr(), y.data_ptr(), nb, h * w, c, sp))
         out[("bwd", "bwd")] = lambda: bx.check(lib.monet_avgpool_bwd(dy.data_ptr(), dx.data_ptr(), nb, h * w, c, 0,
                                                                        sp))
+    elif kind == "concat":
+        ins = [(bx.buf(net.op(j).nbytes), net.op(j).shape[3]) for j in op.attrs["inputs"]]
+        pix, ct = n // op.shape[3], op.shape[3]
+
+        def cat(backward):
+            off = 0
+            for t, cj in ins:
+                if backward:
+                    bx.check(lib.monet_channel_copy(dy.data_ptr(), ct, off, t.data_ptr(), cj, 0, cj, pix, 0, sp))
+                else:
+                    bx.check(lib.monet_channel_copy(t.data_ptr(), cj, 0, y.data_ptr(), ct, off, cj, pix, 0, sp))
+                off += cj
+        out[("fwd", "concat")] = lambda: cat(False)
+        out[("bwd", "bwd")] = lambda: cat(True)
     elif kind == "relu6":
         mask = bx.buf((n + 31) // 32 * 4)
         out[("fwd", "relu6")] = lambda: bx.check(lib.monet_relu6_fwd(x.data_ptr(), y.data_ptr(), mask.data_ptr(), n,

@@ -228,7 +228,7 @@ class Network:
         elif op.kind == "input":
             fwd.append(("load", 0))
             bwd.append(("none", 0, []))
-        elif op.kind in ("add", "avgpool"):
+        elif op.kind in ("add", "avgpool", "concat"):
             fwd.append((op.kind, 0))
             bwd.append(("bwd", 0, []))
         elif op.kind == "dropout":  # backward reads dy only (mask regenerated)
@@ -298,6 +298,7 @@ BWD_IMPLS = {
     "relu": [("bwd-in", "input"), ("bwd-out", "output"), ("bwd-mask", "intermediate")],
     "maxpool": [("bwd-in", "input"), ("bwd-idx", "intermediate")],
     "dropout": [("bwd-rng", "input")],
+    "concat": [("bwd", "input")],  # catalog deps []: the backward slices dy
     "relu6": [("bwd-in", "input"), ("bwd-out", "output"), ("bwd-mask", "intermediate")],
     "dwconv": [("direct", "input")],  # catalog deps []: the keep-mask is regenerated from the step seed
     "add": [("bwd", "input")],
@@ -343,7 +344,10 @@ def fuse_bn_relu(ops: list[Op]) -> list[Op]:
         fused = op.id in fused_into.values()
         kind = ("bnrelu6" if op.id in six else {"bn": "bnrelu", "add": "addrelu"}[op.kind]) if fused else op.kind
         name = op.name + ("+relu6" if op.id in six else "+relu") if fused else op.name
-        out.append(Op(nid, kind, tuple(new_id[j] for j in op.deps), op.shape, dict(op.attrs), op.params, name))
+        attrs = dict(op.attrs)
+        if "inputs" in attrs:  # concat order
+            attrs["inputs"] = [new_id[j] for j in attrs["inputs"]]
+        out.append(Op(nid, kind, tuple(new_id[j] for j in op.deps), op.shape, attrs, op.params, name))
     return out
 
 
@@ -418,10 +422,17 @@ def trace_graph(model: torch.nn.Module, example_input: torch.Tensor, num_classes
                 r = _pair(mod.kernel_size)
                 st, pd = _pair(mod.stride), _pair(mod.padding)
                 _, hh, ww, cc = x.shape
-                p = (hh + 2 * pd - r) // st + 1
-                q = (ww + 2 * pd - r) // st + 1
-                ops.append(Op(nid, "maxpool", (src,), (n, p, q, cc),
-                              {"r": r, "s": r, "stride": st, "pad": pd}, name=node.target))
+
+                def osz(size):  # torch pooling output size (ceil_mode: last window starts inside)
+                    if not mod.ceil_mode:
+                        return (size + 2 * pd - r) // st + 1
+                    o = -(-(size + 2 * pd - r) // st) + 1
+                    return o - 1 if (o - 1) * st >= size + pd else o
+                p, q = osz(hh), osz(ww)
+                attrs = {"r": r, "s": r, "stride": st, "pad": pd}
+                if mod.ceil_mode:
+                    attrs["ceil"] = True
+                ops.append(Op(nid, "maxpool", (src,), (n, p, q, cc), attrs, name=node.target))
             elif isinstance(mod, torch.nn.AdaptiveAvgPool2d):
                 osz = mod.output_size if isinstance(mod.output_size, tuple) else (mod.output_size,) * 2
                 if len(x.shape) == 4 and tuple(osz) == tuple(x.shape[1:3]):
@@ -454,6 +465,22 @@ def trace_graph(model: torch.nn.Module, example_input: torch.Tensor, num_classes
                 nid = len(ops) + 1
                 ops.append(Op(nid, "add", tuple(sorted((a, b))), ops[a - 1].shape, name=node.name))
                 where[node.name] = nid
+            elif node.target in (torch.nn.functional.relu, torch.relu, torch.nn.functional.relu6):
+                src = where[node.args[0].name]
+                nid = len(ops) + 1
+                kind = "relu6" if node.target is torch.nn.functional.relu6 else "relu"
+                ops.append(Op(nid, kind, (src,), ops[src - 1].shape, name=node.name))
+                where[node.name] = nid
+            elif node.target is torch.cat:
+                srcs = [where[a.name] for a in node.args[0]]
+                dim = node.args[1] if len(node.args) > 1 else node.kwargs.get("dim", 0)
+                if dim != 1 or len(set(srcs)) != len(srcs):
+                    raise NotImplementedError("torch.cat: channel concat of distinct tensors only")
+                shp = [ops[j - 1].shape for j in srcs]
+                nid = len(ops) + 1
+                ops.append(Op(nid, "concat", tuple(sorted(srcs)), (*shp[0][:3], sum(s[3] for s in shp)),
+                              {"inputs": srcs}, name=node.name))
+                where[node.name] = nid
             elif node.target is torch.flatten:
                 where[node.name] = where[node.args[0].name]  # avgpool already emits (N, C)
             elif node.target is torch.nn.functional.adaptive_avg_pool2d:
@@ -483,6 +510,7 @@ def build_network(arch: str, batch: int, image: int | tuple = 224, num_classes: 
     import torchvision
 
     torch.manual_seed(seed)
-    model = getattr(torchvision.models, arch)(num_classes=num_classes)
+    kw = {"aux_logits": False, "init_weights": True} if arch in ("googlenet", "inception_v3") else {}
+    model = getattr(torchvision.models, arch)(num_classes=num_classes, **kw)
     hw = (image, image) if isinstance(image, int) else image
     return trace_graph(model, torch.empty(batch, 3, *hw, device="meta"), num_classes, fuse)

@@ -219,3 +219,40 @@ def test_mobilenet_v2_engine(cuda, fuse):
         got = rt.pview[(nid, pname)].view(v.shape)
         assert (got.cpu().double() - v.double()).abs().max().item() <= REL * max(v.abs().max().item(), 0.05), \
             (net.op(nid).name, pname)
+
+
+@pytest.mark.parametrize("fuse", [False, True])
+def test_googlenet_engine(cuda, fuse):
+    """torchvision GoogLeNet (64 x 64): concat forward / slice backward, ceil-mode pools with
+    8-bit indices, under a recompute schedule -- ledger = simulate(), recomputes
+    bit-identical, loss and updated weights = CPU oracle (fed the GPU activations)."""
+    import torchvision
+
+    torch.manual_seed(0)
+    model = torchvision.models.googlenet(num_classes=10, aux_logits=False, init_weights=True)
+    net = M.trace_graph(model, torch.empty(4, 3, 64, 64, device="meta"), 10, fuse=fuse)
+    g = M.load_graph(net.graph_doc())
+    cat = M.load_catalog(net.catalog_doc(), g)
+    se = M.store_everything_schedule(g, cat)
+    act = M.simulate(se, g, cat).peak_memory - g.params_bytes
+    from paper_2010_14501_b200.planner import plan_schedule
+    sched, _ = plan_schedule(g, cat, g.params_bytes + int(0.6 * act), kinds=net.storable_kinds())
+    assert sched is not None and any(s.recompute for s in sched.stages)
+    gen = torch.Generator().manual_seed(0)
+    x = torch.randn(4, 3, 64, 64, generator=gen)
+    y = torch.randint(0, 10, (4,), generator=gen)
+    rt = Runtime(net)
+    rt.set_batch(x.to(cuda), y.to(cuda))
+    plan = rt.plan(sched, g, cat)
+    assert M.trace_report(plan.trace) == M.trace_report(M.simulate(sched, g, cat))
+    acts, mismatched = capture(rt, plan)
+    assert not mismatched
+    doc = M.schedule_to_doc(sched)
+    loss = run_step(CpuState(net), doc, x, y)
+    assert abs(rt.loss_value() - loss) <= REL * abs(loss)
+    st = CpuState(net)
+    run_step(st, doc, x, y, forced=acts)
+    for (nid, pname), v in params_nhwc(st).items():
+        got = rt.pview[(nid, pname)].view(v.shape)
+        assert (got.cpu().double() - v.double()).abs().max().item() <= REL * max(v.abs().max().item(), 0.05), \
+            (net.op(nid).name, pname)

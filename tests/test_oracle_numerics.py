@@ -247,3 +247,41 @@ def test_oracle_mobilenet_v2_equals_autograd(fuse):
                 for have, want in ((rm, ref_bn[f"{base}.running_mean"]), (rv, ref_bn[f"{base}.running_var"])):
                     err = (have.double() - want.double()).abs().max().item()
                     assert err <= TOL * max(want.double().abs().max().item(), 1e-3), (name, op.name)
+
+
+@pytest.mark.parametrize("fuse", [False, True])
+def test_oracle_googlenet_equals_autograd(fuse):
+    """Inception concats (backward = channel slices), ceil-mode max pools (stride 1 and 2),
+    functional ReLU, BN eps 1e-3 and dropout: torchvision GoogLeNet at 64 x 64."""
+    from nets import use_hash_dropout
+
+    torch.manual_seed(0)
+    mk = lambda: torchvision.models.googlenet(num_classes=10, aux_logits=False, init_weights=True)  # noqa: E731
+    model = mk()
+    net = trace_graph(model, torch.empty(2, 3, 64, 64, device="meta"), 10, fuse=fuse)
+    kinds = {op.kind for op in net.ops}
+    assert {"concat", "maxpool", "dropout"} <= kinds
+    assert any(op.attrs.get("ceil") for op in net.ops if op.kind == "maxpool")
+    g = M.load_graph(net.graph_doc())
+    cat = M.load_catalog(net.catalog_doc(), g)
+    gen = torch.Generator().manual_seed(1)
+    x = torch.randn(2, 3, 64, 64, generator=gen)
+    y = torch.randint(0, 10, (2,), generator=gen)
+    scheds = [("store_everything", M.store_everything_schedule(g, cat))] + _planned(net, g, cat)
+    assert len(scheds) > 1, "no recompute schedule to test"
+    for name, sched in scheds:
+        ref_model = mk()
+        ref_model.load_state_dict(model.state_dict())
+        use_hash_dropout(ref_model, net, seed=0)
+        ref_loss = _autograd_step(ref_model, x, y)
+        st = CpuState(net, dtype=torch.float64)
+        loss = run_step(st, M.schedule_to_doc(sched), x.double(), y)
+        assert abs(loss - ref_loss) <= TOL * abs(ref_loss), name
+        ref = {n: p.detach() for n, p in ref_model.named_parameters()}
+        got = params_nhwc(st)
+        for op in net.ops:
+            for pname in op.params:
+                want = ref[f"{op.name.removesuffix('+relu')}.{pname}"]
+                have = _torch_layout(net, op, pname, got[(op.id, pname)], want)
+                err = (have.double() - want.double()).abs().max().item()
+                assert err <= TOL * max(want.double().abs().max().item(), 1e-3), (name, op.name, pname)
