@@ -30,7 +30,8 @@ from .bound import FastBound
 from .costmodel import Catalog
 from .graph import Graph, compute_dependency_sets
 from .memmodel import schedule_cost
-from .schedule import Schedule, SimulationError, StagePlan, simulate, store_everything_schedule
+from .schedule import (Schedule, SimulationError, StagePlan, fastest_store_everything_schedule, simulate,
+                       store_everything_schedule)
 
 __all__ = ["plan_schedule", "demand_schedule", "FAMILIES"]
 
@@ -152,6 +153,13 @@ def demand_schedule(g: Graph, cat: Catalog, store0: set, window: int | None = No
     return Schedule(sched.forward_impls, sched.forward_store, sched.stages, schedule_cost(g, cat, sched))
 
 
+def _fwd_cost(cat: Catalog, g: Graph, x: int):
+    """Cheapest forward cost of a storable's creator (what keeping it saves per rebuild)."""
+    u = g.storable_by_id[x]
+    node = u.creator if u.is_intermediate else x
+    return min(v.cost for v in cat.fwd(node))
+
+
 def _families(g: Graph, kind_of) -> dict:
     """Named checkpoint sets by tensor family."""
     ids = [u.id for u in g.storables]
@@ -231,6 +239,7 @@ def _plan_heuristic(g: Graph, cat: Catalog, budget: int, kinds: dict | None = No
     cands = []
     try:
         cands.append(("store_everything", store_everything_schedule(g, cat)))
+        cands.append(("store_everything/fastest", fastest_store_everything_schedule(g, cat)))
     except ValueError:
         pass
     for name in FAMILIES:
@@ -251,24 +260,56 @@ def _plan_heuristic(g: Graph, cat: Catalog, budget: int, kinds: dict | None = No
                 for prefer in ("cost", "lean"):
                     sch = demand_schedule(g, cat, s0v, window=window, prefer=prefer)
                     if sch is not None:
-                        cands.append((f"{vname}/w{window}/{prefer}", sch))
+                        cands.append((f"{vname}/w{window}/{prefer}", sch, (s0v, window, prefer)))
     best = None
     tried = 0
-    for name, sch in cands:
+    feasible = []
+    for name, sch, *rest in cands:
         tried += 1
         ok, peak, _ = fb.check(sch, budget)
         if not ok:
-            continue
-        if best is not None and sch.objective >= best[1].objective:
             continue
         try:
             simulate(sch, g, cat)
         except SimulationError:
             continue
-        best = (name, sch, peak)
+        feasible.append((sch.objective, name, sch, peak, rest[0] if rest else None))
+        if best is None or sch.objective < best[1].objective:
+            best = (name, sch, peak)
+    # greedy augmentation of the best few demand constructions: also keep one more
+    # tensor from the forward pass (most expensive forward first) whenever the
+    # schedule still fits and gets cheaper; repeat until no single addition helps
+    feasible.sort(key=lambda e: e[0])
+    order = sorted((u.id for u in g.storables), key=lambda x: -_fwd_cost(cat, g, x))
+    for _, name, sch, peak, spec in feasible[:3]:
+        if spec is None:
+            continue
+        s0v, window, prefer = spec
+        cur_s0, cur, cur_peak, grown = set(s0v), sch, peak, 0
+        improved = True
+        while improved:
+            improved = False
+            for x in order:
+                if x in cur_s0:
+                    continue
+                trial = demand_schedule(g, cat, cur_s0 | {x}, window=window, prefer=prefer)
+                tried += 1
+                if trial is None or trial.objective >= cur.objective:
+                    continue
+                ok, pk, _ = fb.check(trial, budget)
+                if not ok:
+                    continue
+                try:
+                    simulate(trial, g, cat)
+                except SimulationError:
+                    continue
+                cur_s0, cur, cur_peak, grown = cur_s0 | {x}, trial, pk, grown + 1
+                improved = True
+        if grown and cur.objective < best[1].objective:
+            best = (f"{name}/+{grown}", cur, cur_peak)
     se_cost = None
     try:
-        se_cost = store_everything_schedule(g, cat).objective
+        se_cost = fastest_store_everything_schedule(g, cat).objective
     except ValueError:
         pass
     if best is None:
