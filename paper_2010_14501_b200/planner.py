@@ -191,19 +191,21 @@ EXACT_MAX_NODES = 64  # graphs up to this size also go through the exact ILP (VG
 
 
 def plan_schedule(g: Graph, cat: Catalog, budget: int, kinds: dict | None = None,
-                  exact_time_s: float | None = None):
+                  exact_time_s: float | None = None, exchange: bool = False):
     """Cheapest feasible schedule among the demand-construction candidates.
 
     ``kinds`` maps storable id -> family label; by default inferred from the
     graph structure is not possible, so the tracer's op kinds are expected via
     ``Network.storable_kinds()``; without it every storable counts as "all".
+    ``exchange``: after the greedy additions, also try exchange moves (keep one more
+    tensor, drop a cheaper one) -- offline planning (tools/make_schedules.py), seconds more.
     ``exact_time_s``: on graphs of at most EXACT_MAX_NODES nodes, also run the
     reference-exact 0-1 ILP (ilp.build_model + solver.solve) for that long,
     seeded with the best candidate as its incumbent; its schedule wins when it
     is cheaper or the only feasible one.
     Returns (schedule or None, info dict).
     """
-    sch, info = _plan_heuristic(g, cat, budget, kinds)
+    sch, info = _plan_heuristic(g, cat, budget, kinds, exchange)
     if exact_time_s and g.n <= EXACT_MAX_NODES:
         from .ilp import assignment_from_schedule, build_model
         from .schedule import decode
@@ -228,7 +230,7 @@ def plan_schedule(g: Graph, cat: Catalog, budget: int, kinds: dict | None = None
     return sch, info
 
 
-def _plan_heuristic(g: Graph, cat: Catalog, budget: int, kinds: dict | None = None):
+def _plan_heuristic(g: Graph, cat: Catalog, budget: int, kinds: dict | None = None, exchange: bool = False):
     sets = compute_dependency_sets(g, "upper")
     fb = FastBound(g, sets, cat)
     kind_of = (lambda x: kinds.get(x, "other")) if kinds else (lambda x: "other")
@@ -305,8 +307,33 @@ def _plan_heuristic(g: Graph, cat: Catalog, budget: int, kinds: dict | None = No
                     continue
                 cur_s0, cur, cur_peak, grown = cur_s0 | {x}, trial, pk, grown + 1
                 improved = True
-        if grown and cur.objective < best[1].objective:
-            best = (f"{name}/+{grown}", cur, cur_peak)
+        # exchange moves: keep an expensive-to-rebuild tensor in place of a cheap one
+        swaps = 0
+        improved = exchange
+        while improved:
+            improved = False
+            adds = [x for x in order if x not in cur_s0][:24]
+            drops = [y for y in reversed(order) if y in cur_s0 and y not in s0v][:32]
+            for x in adds:
+                for y in drops:
+                    trial = demand_schedule(g, cat, (cur_s0 - {y}) | {x}, window=window, prefer=prefer)
+                    tried += 1
+                    if trial is None or trial.objective >= cur.objective:
+                        continue
+                    ok, pk, _ = fb.check(trial, budget)
+                    if not ok:
+                        continue
+                    try:
+                        simulate(trial, g, cat)
+                    except SimulationError:
+                        continue
+                    cur_s0, cur, cur_peak, swaps = (cur_s0 - {y}) | {x}, trial, pk, swaps + 1
+                    improved = True
+                    break
+                if improved:
+                    break
+        if (grown or swaps) and cur.objective < best[1].objective:
+            best = (f"{name}/+{grown}~{swaps}", cur, cur_peak)
     se_cost = None
     try:
         se_cost = fastest_store_everything_schedule(g, cat).objective

@@ -6,3 +6,4 @@ for b in 8 6 10; do
 done
 bash tools/gpu_bench_vgg.sh
 bash tools/gpu_bench_c4.sh
+ARCH=googlenet B=320 bash tools/gpu_bench_c4.sh
