@@ -729,12 +729,66 @@ static int dw_blocks(const monet_conv_desc* d) {
   const long long rows = (long long)d->n * d->p * d->q;
   return (int)std::max(1LL, std::min((rows + 63) / 64, (long long)kNumSMs * 4));
 }
+// shared-memory tiled kernels (csrc/dwconv.cuh): channel slabs of 16, staged window <= 200 KB
+constexpr size_t kDwSmemMax = 200 * 1024;
+static size_t dw_fwd_smem(const monet_conv_desc* d) {
+  const int nr = (kDwRows - 1) * d->stride_h + d->r, nc = (d->q - 1) * d->stride_w + d->s;
+  return (size_t)nr * nc * kDwSlab * sizeof(float);
+}
+static size_t dw_dgrad_smem(const monet_conv_desc* d) {
+  const int nr = (kDwRows + d->r - 1) / d->stride_h + 2, nc = (d->w + d->s - 1) / d->stride_w + 2;
+  return (size_t)nr * nc * kDwSlab * sizeof(float);
+}
+static size_t dw_wgrad_smem(const monet_conv_desc* d) {  // staged window, or the 256-float4 final reduction
+  return std::max(dw_fwd_smem(d) + (size_t)kDwRows * d->q * kDwSlab * sizeof(float), (size_t)256 * sizeof(float4));
+}
+static bool dw_tiled(const monet_conv_desc* d) {
+  return d->c % kDwSlab == 0 && dw_fwd_smem(d) <= kDwSmemMax && dw_dgrad_smem(d) <= kDwSmemMax &&
+         dw_wgrad_smem(d) <= kDwSmemMax;
+}
+// 1 / 2: the 3x3 stride-1 / stride-2 specialisations; 0: runtime geometry
+static int dw_kind(const monet_conv_desc* d) {
+  if (d->r != 3 || d->s != 3 || d->stride_h != d->stride_w) return 0;
+  return (d->stride_h == 1 || d->stride_h == 2) ? d->stride_h : 0;
+}
+}  // extern "C"
+namespace {
+template <bool kTrans>
+void dw_launch(const monet_conv_desc* d, dim3 grid, size_t smem, const float* src, const float* w, float* out,
+               int accumulate, cudaStream_t st) {
+  static bool attr = false;  // the three specialisations share a signature: set all of them once
+  if (!attr) {
+    for (auto kern : {dwconv_tile_kernel<kTrans, 0>, dwconv_tile_kernel<kTrans, 1>, dwconv_tile_kernel<kTrans, 2>})
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDwSmemMax);
+    attr = true;
+  }
+  auto run = [&](auto kern) { kern<<<grid, 256, smem, st>>>(src, w, out, geom(d), accumulate); };
+  const int k = dw_kind(d);
+  if (k == 1)
+    run(dwconv_tile_kernel<kTrans, 1>);
+  else if (k == 2)
+    run(dwconv_tile_kernel<kTrans, 2>);
+  else
+    run(dwconv_tile_kernel<kTrans, 0>);
+}
+}  // namespace
+extern "C" {
+static int dw_tile_nb(const monet_conv_desc* d) {  // band walkers per channel slab (wgrad)
+  const int bands = d->n * ((d->p + kDwRows - 1) / kDwRows);
+  return std::max(1, std::min(bands, kNumSMs * 4 / std::max(1, d->c / kDwSlab)));
+}
 size_t monet_dwconv_ws_bytes(const monet_conv_desc* d) {
   if (dw_check(d)) return 0;
-  return (size_t)dw_blocks(d) * d->r * d->s * d->c * sizeof(float);
+  const int nb = dw_tiled(d) ? dw_tile_nb(d) : dw_blocks(d);
+  return (size_t)nb * d->r * d->s * d->c * sizeof(float);
 }
 int monet_dwconv_fwd(const monet_conv_desc* d, const float* x, const float* w, float* y, void* stream) {
   if (int e = dw_check(d)) return e;
+  if (dw_tiled(d)) {
+    dim3 grid((d->p + kDwRows - 1) / kDwRows, d->n, d->c / kDwSlab);
+    dw_launch<false>(d, grid, dw_fwd_smem(d), x, w, y, 0, S(stream));
+    return last_error();
+  }
   const long long total = (long long)d->n * d->p * d->q * (d->c / 4);
   dwconv_fwd_kernel<<<ew_blocks(total), kEwThreads, 0, S(stream)>>>(x, w, y, geom(d));
   return last_error();
@@ -742,6 +796,11 @@ int monet_dwconv_fwd(const monet_conv_desc* d, const float* x, const float* w, f
 int monet_dwconv_dgrad(const monet_conv_desc* d, const float* dy, const float* w, float* dx, int accumulate,
                        void* stream) {
   if (int e = dw_check(d)) return e;
+  if (dw_tiled(d)) {
+    dim3 grid((d->h + kDwRows - 1) / kDwRows, d->n, d->c / kDwSlab);
+    dw_launch<true>(d, grid, dw_dgrad_smem(d), dy, w, dx, accumulate, S(stream));
+    return last_error();
+  }
   const long long total = (long long)d->n * d->h * d->w * (d->c / 4);
   dwconv_dgrad_kernel<<<ew_blocks(total), kEwThreads, 0, S(stream)>>>(dy, w, dx, geom(d), accumulate);
   return last_error();
@@ -750,9 +809,30 @@ int monet_dwconv_wgrad(const monet_conv_desc* d, const float* x, const float* dy
                        size_t ws_bytes, void* stream) {
   if (int e = dw_check(d)) return e;
   if (ws == nullptr || ws_bytes < monet_dwconv_ws_bytes(d)) return -(int)cudaErrorInvalidValue;
-  const int nb = dw_blocks(d), taps = d->r * d->s;
+  const int taps = d->r * d->s;
   float* part = static_cast<float*>(ws);
-  dwconv_wgrad_partial_kernel<<<nb, kEwThreads, 0, S(stream)>>>(x, dy, part, geom(d));
+  int nb;
+  if (dw_tiled(d)) {
+    nb = dw_tile_nb(d);
+    const dim3 grid(nb, d->c / kDwSlab);
+    const int k = dw_kind(d);
+    static bool attr = false;  // all three specialisations at once (shared signature)
+    if (!attr) {
+      for (auto kern : {dwconv_wgrad_tile_kernel<0>, dwconv_wgrad_tile_kernel<1>, dwconv_wgrad_tile_kernel<2>})
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDwSmemMax);
+      attr = true;
+    }
+    auto run = [&](auto kern) { kern<<<grid, 256, dw_wgrad_smem(d), S(stream)>>>(x, dy, part, geom(d), nb); };
+    if (k == 1)
+      run(dwconv_wgrad_tile_kernel<1>);
+    else if (k == 2)
+      run(dwconv_wgrad_tile_kernel<2>);
+    else
+      run(dwconv_wgrad_tile_kernel<0>);
+  } else {
+    nb = dw_blocks(d);
+    dwconv_wgrad_partial_kernel<<<nb, kEwThreads, 0, S(stream)>>>(x, dy, part, geom(d));
+  }
   dwconv_wgrad_final_kernel<<<(taps * d->c + 255) / 256, 256, 0, S(stream)>>>(part, nb, taps, d->c, dw);
   return last_error();
 }

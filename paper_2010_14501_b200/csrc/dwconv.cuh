@@ -162,3 +162,203 @@ __global__ void dwconv_wgrad_final_kernel(const float* __restrict__ part, int nb
 }
 
 }  // namespace monet
+
+namespace monet {
+
+// ---------------------------------------------------------------------------
+// Shared-memory tiled depthwise kernels.  A CTA owns kDwRows output rows of one
+// image and one kDwSlab-channel slab; the source rows it needs (input rows for
+// fwd / wgrad, dy rows for dgrad) are staged once into shared memory with zero
+// padding, so each source pixel crosses L2 -> SM about once instead of once per
+// tap.  Channel slab = 16 floats (4 quads): 64 B per pixel, two full sectors.
+constexpr int kDwSlab = 16, kDwRows = 4;
+
+// dst[i] = load(i) for i < count, blockDim-strided, 8 loads in flight per thread
+template <class F>
+MONET_DEV void dw_stage(float4* dst, int count, F load) {
+  constexpr int kU = 8;
+  for (int base = threadIdx.x; base < count; base += blockDim.x * kU) {
+    float4 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = base + u * (int)blockDim.x;
+      v[u] = i < count ? load(i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = base + u * (int)blockDim.x;
+      if (i < count) dst[i] = v[u];
+    }
+  }
+}
+
+// fwd: out = y (P x Q), src = x (H x W); dgrad (kTrans): out = dx (H x W), src = dy (P x Q)
+// kStride > 0: 3x3 taps and that stride at compile time (MobileNet-V2's layers); 0: runtime geometry
+template <bool kTrans, int kStride = 0>
+__global__ void __launch_bounds__(256) dwconv_tile_kernel(const float* __restrict__ src, const float* __restrict__ w,
+                                                          float* out, ConvGeom g, int accumulate) {
+  extern __shared__ float4 dw_smem[];
+  if (kStride > 0) {
+    g.sh = g.sw = kStride;
+    g.R = g.S = 3;
+  }
+  const int OH = kTrans ? g.H : g.P, OW = kTrans ? g.W : g.Q;  // output extent
+  const int SH = kTrans ? g.P : g.H, SW = kTrans ? g.Q : g.W;  // source extent
+  const int o0 = blockIdx.x * kDwRows;
+  const int n = blockIdx.y;
+  const int c0 = blockIdx.z * kDwSlab;
+  const int orows = min(kDwRows, OH - o0);
+  // staged source window
+  int s_r0, s_nr, s_c0, s_nc;
+  if (!kTrans) {  // output row o reads input rows o*sh - ph + r
+    s_r0 = o0 * g.sh - g.ph;
+    s_nr = (orows - 1) * g.sh + g.R;
+    s_c0 = -g.pw;
+    s_nc = (OW - 1) * g.sw + g.S;
+  } else {  // dx row h reads dy rows (h + ph - r) / sh for r with matching parity
+    const int lo = o0 + g.ph - (g.R - 1), hi = o0 + orows - 1 + g.ph;
+    s_r0 = lo >= 0 ? lo / g.sh : -((-lo + g.sh - 1) / g.sh);
+    s_nr = hi / g.sh - s_r0 + 1;
+    const int wl = g.pw - (g.S - 1), wh = OW - 1 + g.pw;
+    s_c0 = wl >= 0 ? wl / g.sw : -((-wl + g.sw - 1) / g.sw);
+    s_nc = wh / g.sw - s_c0 + 1;
+  }
+  // stage: s_nr x s_nc pixels x 4 quads of this slab (zero outside the source); 8 independent
+  // loads in flight per thread before the shared-memory stores
+  const int tot = s_nr * s_nc * 4;
+  dw_stage(dw_smem, tot, [&](int i) {
+    const int j = i & 3, pc = i >> 2;
+    const int cc = pc % s_nc, rr = pc / s_nc;
+    const int sr = s_r0 + rr, sc = s_c0 + cc;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if ((unsigned)sr < (unsigned)SH && (unsigned)sc < (unsigned)SW)
+      v = __ldg(reinterpret_cast<const float4*>(src + (((long long)n * SH + sr) * SW + sc) * g.C + c0) + j);
+    return v;
+  });
+  __syncthreads();
+  // compute: outputs orows x OW x 4 quads; a thread's quad j is fixed (blockDim % 4 == 0),
+  // so its taps' weights stay in registers
+  const int outs = orows * OW * 4;
+  const int jq = threadIdx.x & 3;
+  float4 wreg[kDwMaxTaps];
+#pragma unroll
+  for (int k = 0; k < kDwMaxTaps; ++k)
+    wreg[k] = k < g.R * g.S ? __ldg(reinterpret_cast<const float4*>(w + k * g.C + c0) + jq)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i = threadIdx.x; i < outs; i += blockDim.x) {
+    const int j = jq, po = i >> 2;
+    const int ow = po % OW, orr = po / OW;
+    const int oh = o0 + orr;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < (kStride > 0 ? 3 : kDwMaxTaps); ++r) {
+      if (r >= g.R) break;
+      int sr;
+      if (!kTrans) {
+        sr = oh * g.sh - g.ph + r - s_r0;
+      } else {
+        const int t = oh + g.ph - r;
+        if (t < 0 || t % g.sh) continue;
+        sr = t / g.sh - s_r0;
+        if (sr >= s_nr || t / g.sh >= SH) continue;
+      }
+#pragma unroll
+      for (int s = 0; s < (kStride > 0 ? 3 : kDwMaxTaps); ++s) {
+        if (s >= g.S) break;
+        int sc;
+        if (!kTrans) {
+          sc = ow * g.sw - g.pw + s - s_c0;
+        } else {
+          const int t = ow + g.pw - s;
+          if (t < 0 || t % g.sw) continue;
+          sc = t / g.sw - s_c0;
+          if (sc >= s_nc || t / g.sw >= SW) continue;
+        }
+        const float4 v = dw_smem[(sr * s_nc + sc) * 4 + j];
+        fma4(acc, v, wreg[r * g.S + s]);
+      }
+    }
+    float4* o = reinterpret_cast<float4*>(out + (((long long)n * OH + oh) * OW + ow) * g.C + c0) + j;
+    if (accumulate) {
+      const float4 a = *o;
+      acc.x += a.x;
+      acc.y += a.y;
+      acc.z += a.z;
+      acc.w += a.w;
+    }
+    *o = acc;
+  }
+}
+
+// wgrad, persistent: grid (nb, C / kDwSlab); CTA b of slab z walks bands
+// (n, row band) b, b + nb, ... staging the band's input rows and dy rows, and
+// accumulates dw[tap][slab] for its (tap, quad) pairs over the band's pixels in
+// registers (threads = 8 pixel groups x 32 (tap, quad) lanes); the groups are
+// combined in shared memory once at the end -> part[b][tap][c] (fixed order).
+template <int kStride = 0>
+__global__ void __launch_bounds__(256) dwconv_wgrad_tile_kernel(const float* __restrict__ x,
+                                                                const float* __restrict__ dy, float* __restrict__ part,
+                                                                ConvGeom g, int nb) {
+  extern __shared__ float4 dw_smem[];
+  if (kStride > 0) {
+    g.sh = g.sw = kStride;
+    g.R = g.S = 3;
+  }
+  const int c0 = blockIdx.y * kDwSlab;
+  const int bands_per_img = (g.P + kDwRows - 1) / kDwRows;
+  const int total_bands = g.N * bands_per_img;
+  const int taps = g.R * g.S;
+  const int lane = threadIdx.x & 63, grp = threadIdx.x >> 6;  // 64 (tap, quad) slots x 4 pixel groups
+  const int tap = lane >> 2, j = lane & 3;
+  const bool active = tap < taps;
+  const int r = active ? tap / g.S : 0, s = active ? tap - r * g.S : 0;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int x_nc = (g.Q - 1) * g.sw + g.S;
+  for (int band = blockIdx.x; band < total_bands; band += nb) {
+    const int n = band / bands_per_img;
+    const int p0 = (band - n * bands_per_img) * kDwRows;
+    const int prow = min(kDwRows, g.P - p0);
+    const int x_r0 = p0 * g.sh - g.ph, x_nr = (prow - 1) * g.sh + g.R;
+    float4* xs = dw_smem;
+    float4* ds = dw_smem + x_nr * x_nc * 4;
+    __syncthreads();  // previous band's readers are done
+    dw_stage(xs, x_nr * x_nc * 4, [&](int i) {
+      const int jj = i & 3, pc = i >> 2;
+      const int cc = pc % x_nc, rr = pc / x_nc;
+      const int hr = x_r0 + rr, wc = cc - g.pw;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if ((unsigned)hr < (unsigned)g.H && (unsigned)wc < (unsigned)g.W)
+        v = __ldg(reinterpret_cast<const float4*>(x + (((long long)n * g.H + hr) * g.W + wc) * g.C + c0) + jj);
+      return v;
+    });
+    dw_stage(ds, prow * g.Q * 4, [&](int i) {
+      const int jj = i & 3, pq = i >> 2;
+      const int q = pq % g.Q, pr = pq / g.Q;
+      return __ldg(reinterpret_cast<const float4*>(dy + (((long long)n * g.P + p0 + pr) * g.Q + q) * g.C + c0) + jj);
+    });
+    __syncthreads();
+    if (active) {
+      for (int pr = 0; pr < prow; ++pr) {
+        const float4* drow = ds + pr * g.Q * 4 + j;
+        const float4* xrow = xs + ((pr * g.sh + r) * x_nc + s) * 4 + j;
+        for (int q = grp; q < g.Q; q += 4) fma4(acc, xrow[q * g.sw * 4], drow[q * 4]);
+      }
+    }
+  }
+  __syncthreads();
+  dw_smem[threadIdx.x] = acc;
+  __syncthreads();
+  if (grp == 0 && active) {
+    float4 t = dw_smem[lane];
+    for (int k = 1; k < 4; ++k) {
+      const float4 v = dw_smem[k * 64 + lane];
+      t.x += v.x;
+      t.y += v.y;
+      t.z += v.z;
+      t.w += v.w;
+    }
+    reinterpret_cast<float4*>(part + ((long long)blockIdx.x * taps + tap) * g.C + c0)[j] = t;
+  }
+}
+
+}  // namespace monet
