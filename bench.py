@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--arch", default="resnet50")
     ap.add_argument("--batch", type=int, default=184)
-    ap.add_argument("--image", type=int, default=224)
+    ap.add_argument("--image", default="224", help="224, or HxW (UNet: 416x608)")
     ap.add_argument("--budget-gib", type=float, default=8.0)
     ap.add_argument("--no-fuse", dest="fuse", action="store_false",
                     help="separate BN and ReLU operators (default: fused BN+ReLU ops, tracer fuse=True)")
@@ -127,7 +127,19 @@ class ClockSampler:
 
 def conv_flops(net, op):
     x = net.op(op.deps[0])
+    if op.kind == "convT":  # the adjoint conv's GEMM: input pixels x in-channels x out-channels x taps
+        return 2.0 * x.numel * op.shape[3] * op.attrs["r"] * op.attrs["s"]
     return 2.0 * op.numel * x.shape[3] * op.attrs["r"] * op.attrs["s"]
+
+
+def image_arg(v: str):
+    from paper_2010_14501_b200.tracer import parse_image
+    return parse_image(v)
+
+
+def n_classes(arch: str) -> int:
+    from paper_2010_14501_b200.tracer import default_classes
+    return default_classes(arch)
 
 
 LOCAL_BYTES = {  # minimal fp32 HBM bytes per element
@@ -167,7 +179,7 @@ def kernel_roofline(rt, plan, net, peaks):
         ms = a.elapsed_time(b)
         total_t += ms
         op = net.op(s.node)
-        if op.kind == "conv":
+        if op.kind in ("conv", "convT"):
             f = conv_flops(net, op)
             if s.kind == "backward":
                 f *= 1 if net.op(op.deps[0]).kind == "input" else 2
@@ -216,7 +228,7 @@ def cpu_baseline_run(args, budget_frac, steps=2):
 
     torch.set_num_threads(os.cpu_count() or 1)
     n = args.cpu_sample
-    net = build_network(args.arch, n, args.image)
+    net = build_network(args.arch, n, image_arg(args.image), num_classes=n_classes(args.arch))
     g = M.load_graph(net.graph_doc())
     cat = M.load_catalog(net.catalog_doc(), g)
     se_peak = M.simulate(M.store_everything_schedule(g, cat), g, cat).peak_memory
@@ -226,8 +238,10 @@ def cpu_baseline_run(args, budget_frac, steps=2):
         sched = M.store_everything_schedule(g, cat)
     doc = M.schedule_to_doc(sched)
     gen = torch.Generator().manual_seed(0)
-    x = torch.randn(n, 3, args.image, args.image, generator=gen)
-    y = torch.randint(0, 1000, (n,), generator=gen)
+    hw = image_arg(args.image)
+    hw = hw if isinstance(hw, tuple) else (hw, hw)
+    x = torch.randn(n, 3, *hw, generator=gen)
+    y = torch.randint(0, n_classes(args.arch), (net.label_count(),), generator=gen)
     st = CpuState(net)
     run_step(st, doc, x, y)  # warm-up
     t = time.perf_counter()
@@ -235,7 +249,7 @@ def cpu_baseline_run(args, budget_frac, steps=2):
         run_step(st, doc, x, y)
     dt = (time.perf_counter() - t) / steps
     return {"value": round(n / dt, 3), "unit": "img/s", "cores": torch.get_num_threads(), "kind": "port",
-            "sample": f"{args.arch} batch {n} at {args.image}x{args.image}, one scheduled training step "
+            "sample": f"{args.arch} batch {n} at {hw[0]}x{hw[1]}, one scheduled training step "
                       f"(budget fraction {budget_frac:.3f} of its store-everything activations), "
                       f"torch CPU fp32 oracle replay, mean of {steps} steps after 1 warm-up"}
 
@@ -285,7 +299,7 @@ def ours_arm(args):
 
     gib = args.budget_gib
     budget = int(gib * (1 << 30))
-    net = build_network(args.arch, args.batch, args.image, fuse=args.fuse)
+    net = build_network(args.arch, args.batch, image_arg(args.image), num_classes=n_classes(args.arch), fuse=args.fuse)
     gdoc = net.graph_doc()
     g = M.load_graph(gdoc)
     cat = M.load_catalog(measured_catalog(net, args) or net.catalog_doc(), g)
@@ -300,8 +314,10 @@ def ours_arm(args):
     plan = rt.plan(sched, g, cat)
 
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
-    x = torch.randn(args.batch, 3, args.image, args.image, device=dev, generator=gen)
-    y = torch.randint(0, 1000, (args.batch,), device=dev, generator=gen)
+    hw = image_arg(args.image)
+    hw = hw if isinstance(hw, tuple) else (hw, hw)
+    x = torch.randn(args.batch, 3, *hw, device=dev, generator=gen)
+    y = torch.randint(0, n_classes(args.arch), (net.label_count(),), device=dev, generator=gen)
     rt.set_batch(x, y)
     x_keep = x if not args.no_overhead_run else None
     del x
@@ -347,9 +363,9 @@ def ours_arm(args):
 
     # ---- end to end: pinned host batch in, loss out, through Runtime.train_step
     c_pad = net.ops[0].shape[3]
-    host = torch.zeros(args.batch, args.image, args.image, c_pad, pin_memory=True)
+    host = torch.zeros(args.batch, hw[0], hw[1], c_pad, pin_memory=True)
     host[..., :3].normal_()
-    host_y = torch.randint(0, 1000, (args.batch,), dtype=torch.int32).pin_memory()
+    host_y = torch.randint(0, n_classes(args.arch), (net.label_count(),), dtype=torch.int32).pin_memory()
     loss_host = torch.empty(1, pin_memory=True)
     for _ in range(2):
         rt.train_step(plan, host, host_y)
@@ -413,7 +429,7 @@ def ours_arm(args):
             "warmup": max(3, args.warmup), "ms_per_step": round(ms, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32 (convs: bf16x3-split tensor-core MMAs, fp32 accumulate)",
             "data": "synthetic N(0,1) images, uniform labels; random-init torchvision weights (seed 0)",
-            "config": {"workload": f"{args.arch} {args.image}x{args.image} batch {args.batch}/GPU, "
+            "config": {"workload": f"{args.arch} {hw[0]}x{hw[1]} batch {args.batch}/GPU, "
                                    f"{gib:g} GiB per-GPU budget, MONeT schedule ({source})"
                                    + (", fused BN+ReLU operators" if args.fuse else ""),
                        "model": args.arch, "global_batch": world * args.batch, "per_gpu_batch": args.batch,

@@ -88,6 +88,17 @@ int monet_dropout_bwd(const float* dy, float* dx, int64_t n, float p, const unsi
                       int accumulate, void* stream);
 int monet_seed_advance(unsigned long long* seed, void* stream);
 
+/* --- transposed conv (UNet up-sampling) --------------------------------------------
+ * The adjoint of the conv described by d: d's input is the transposed conv's OUTPUT y
+ * [n][h][w][c], d's output its INPUT x [n][p][q][k]; weights KRSC (torch [in][out][R][S]
+ * with in = k, out = c).  Forward = the conv dgrad kernel (+ bias), input gradient = the conv
+ * forward kernel (optionally accumulating), weight gradient = the conv wgrad kernel. */
+size_t monet_convT_ws_bytes(int variant, int pass, const monet_conv_desc* d);
+int monet_convT_fwd(int variant, const monet_conv_desc* d, const float* x, const float* w, const float* bias, float* y,
+                    void* ws, size_t ws_bytes, void* stream);
+int monet_convT_bwd(int variant, const monet_conv_desc* d, const float* x, const float* w, const float* dy, float* dx,
+                    int dx_accumulate, float* dw, void* ws, size_t ws_bytes, void* stream);
+
 /* --- channel concat (GoogLeNet inception outputs) ---------------------------------
  * NHWC channel-slice copy: dst[pix][dst_off + j] (+)= src[pix][src_off + j], j < count
  * (all channel counts and offsets multiples of 4).  Concat forward = one call per input

@@ -38,8 +38,8 @@ class CpuState:
         for op in net.ops:
             for name, t in op.params.items():
                 v = t.to(dtype).clone()
-                if op.kind == "conv" and name == "weight":
-                    v = v.permute(0, 3, 1, 2).contiguous()  # KRSC -> KCRS (OIHW)
+                if op.kind in ("conv", "convT") and name == "weight":
+                    v = v.permute(0, 3, 1, 2).contiguous()  # KRSC -> KCRS (OIHW; convT: [in][out][R][S])
                 elif op.kind == "dwconv" and name == "weight":
                     v = v.permute(2, 0, 1).unsqueeze(1).contiguous()  # [R][S][C] -> [C][1][R][S]
                 self.params[(op.id, name)] = v
@@ -117,6 +117,10 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
             y = xs[0] * _dropout_scale(op, xs[0], state.seed)
         elif op.kind == "concat":
             y = torch.cat([x_of(j) for j in op.attrs["inputs"]], dim=1)
+        elif op.kind == "convT":
+            a = op.attrs
+            y = F.conv_transpose2d(xs[0], P[(op.id, "weight")], P.get((op.id, "bias")), stride=a["stride"],
+                                   padding=a["pad"])
         elif op.kind == "dwconv":
             a = op.attrs
             y = F.conv2d(xs[0], P[(op.id, "weight")], stride=a["stride"], padding=a["pad"], groups=xs[0].shape[1])
@@ -163,7 +167,7 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
             y = xs[0].mean(dim=(2, 3))
         elif op.kind == "fc":
             y = F.linear(_flat_nhwc(xs[0]), P[(op.id, "weight")], P[(op.id, "bias")])
-        elif op.kind == "xent":
+        elif op.kind == "xent":  # (N, K) logits, or per-pixel (N, K, H, W) with (N, H, W) labels
             y = F.cross_entropy(xs[0], labels.long())
             loss_val = float(y)
         else:
@@ -194,6 +198,16 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
                 state.grads[(op.id, "bias")] = dy.sum(dim=(0, 2, 3))
         elif op.kind == "dropout":
             put_grad(op.deps[0], dy * _dropout_scale(op, dy, state.seed), created)
+        elif op.kind == "convT":
+            a = op.attrs
+            j = op.deps[0]
+            x = x_of(j)
+            w = P[(op.id, "weight")]
+            if net.grad_bytes(net.op(j)) > 0:
+                put_grad(j, F.conv2d(dy, w, stride=a["stride"], padding=a["pad"]), created)
+            state.grads[(op.id, "weight")] = torch.nn.grad.conv2d_weight(dy, w.shape, x, a["stride"], a["pad"])
+            if (op.id, "bias") in P:
+                state.grads[(op.id, "bias")] = dy.sum(dim=(0, 2, 3))
         elif op.kind == "concat":
             off = 0
             for j in op.attrs["inputs"]:
@@ -296,8 +310,12 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
             j = op.deps[0]
             z = x_of(j)
             p = torch.softmax(z, dim=1)
-            p[torch.arange(z.shape[0]), labels.long()] -= 1.0
-            put_grad(j, p * (dy / z.shape[0]), created)
+            if z.dim() == 4:  # per-pixel loss: mean over N*H*W
+                p = p - F.one_hot(labels.long(), z.shape[1]).permute(0, 3, 1, 2).to(p.dtype)
+                put_grad(j, p * (dy / (z.numel() // z.shape[1])), created)
+            else:
+                p[torch.arange(z.shape[0]), labels.long()] -= 1.0
+                put_grad(j, p * (dy / z.shape[0]), created)
         else:
             raise ValueError(op.kind)
 
@@ -426,7 +444,7 @@ def params_nhwc(state: CpuState):
     """Parameters in the engine layout (conv weights KRSC) for comparison with the GPU."""
     out = {}
     for (nid, name), v in state.params.items():
-        if state.net.op(nid).kind == "conv" and name == "weight":
+        if state.net.op(nid).kind in ("conv", "convT") and name == "weight":
             v = v.permute(0, 2, 3, 1).contiguous()
         elif state.net.op(nid).kind == "dwconv" and name == "weight":
             v = v.squeeze(1).permute(1, 2, 0).contiguous()

@@ -38,6 +38,9 @@ SIGNATURES = {
     "monet_dropout_fwd": (_i32, [_vp, _vp, _i64, _f32, _vp, C.c_uint64, _vp]),
     "monet_dropout_bwd": (_i32, [_vp, _vp, _i64, _f32, _vp, C.c_uint64, _i32, _vp]),
     "monet_seed_advance": (_i32, [_vp, _vp]),
+    "monet_convT_ws_bytes": (_sz, [_i32, _i32, _PCONV]),
+    "monet_convT_fwd": (_i32, [_i32, _PCONV, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "monet_convT_bwd": (_i32, [_i32, _PCONV, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _sz, _vp]),
     "monet_channel_copy": (_i32, [_vp, _i32, _i32, _vp, _i32, _i32, _i32, _i64, _i32, _vp]),
     "monet_dwconv_ws_bytes": (_sz, [_PCONV]),
     "monet_dwconv_fwd": (_i32, [_PCONV, _vp, _vp, _vp, _vp]),

@@ -20,6 +20,11 @@ def _ns(flops=0.0, nbytes=0.0, launches=1) -> int:
 
 def analytic_cost(net, op, pass_, name) -> int:
     n = op.numel
+    if op.kind == "convT":  # same GEMM work as the conv it is the adjoint of
+        x = net.op(op.deps[0])
+        flops = 2.0 * x.numel * op.shape[3] * op.attrs["r"] * op.attrs["s"]
+        return _ns(flops if pass_ == "fwd" else 2 * flops, 4.0 * (x.numel + n) * (1 if pass_ == "fwd" else 2),
+                   launches=1 if pass_ == "fwd" else 3)
     if op.kind == "conv":
         x = net.op(op.deps[0])
         flops = 2.0 * n * x.shape[3] * op.attrs["r"] * op.attrs["s"]

@@ -1052,12 +1052,24 @@ int monet_avgpool_bwd(const float* dy, float* dx, int n, int hw, int c, int accu
 }
 
 // ------------------------------------------------------------------- loss / SGD
-size_t monet_xent_scratch_bytes(int n) { return (size_t)n * sizeof(float); }
+// rows (n) x classes logits; per-pixel segmentation losses are rows = N*H*W of an NHWC tensor
+constexpr int kXentSmallK = 32, kXentPartials = 1024;
+size_t monet_xent_scratch_bytes(int n) {
+  return ((size_t)n * sizeof(float) + 15) / 16 * 16 + (size_t)kXentPartials * sizeof(double);
+}
 
 int monet_xent_fwd(const float* logits, const int32_t* labels, float* loss, int n, int classes, void* scratch,
                    void* stream) {
   cudaStream_t st = S(stream);
   float* rows = static_cast<float*>(scratch);
+  if (classes <= kXentSmallK) {
+    double* part = reinterpret_cast<double*>(static_cast<char*>(scratch) + ((size_t)n * sizeof(float) + 15) / 16 * 16);
+    xent_small_fwd_kernel<<<ew_blocks(n), kEwThreads, 0, st>>>(logits, labels, rows, n, classes);
+    const int nb = (int)std::min<long long>(kXentPartials, std::max(1, (n + 4095) / 4096));
+    block_sum_kernel<<<nb, 256, 0, st>>>(rows, n, part);
+    mean_of_partials_kernel<<<1, 32, 0, st>>>(part, nb, n, loss);
+    return last_error();
+  }
   xent_fwd_kernel<<<n, 256, 0, st>>>(logits, labels, rows, n, classes);
   mean_kernel<<<1, 32, 0, st>>>(rows, n, loss);
   return last_error();
@@ -1065,8 +1077,41 @@ int monet_xent_fwd(const float* logits, const int32_t* labels, float* loss, int 
 
 int monet_xent_bwd(const float* logits, const int32_t* labels, const float* dloss, float* dlogits, int n,
                    int classes, int accumulate, void* stream) {
+  if (classes <= kXentSmallK) {
+    xent_small_bwd_kernel<<<ew_blocks(n), kEwThreads, 0, S(stream)>>>(logits, labels, dloss, dlogits, n, classes,
+                                                                       accumulate);
+    return last_error();
+  }
   xent_bwd_kernel<<<n, 256, 0, S(stream)>>>(logits, labels, dloss, dlogits, n, classes, accumulate);
   return last_error();
+}
+
+// ---------------------------------------------------------------- transposed conv
+// ConvTranspose2d (UNet's up-sampling) as the adjoint of the conv described by d:
+// d's input is the transposed conv's OUTPUT y [n][h][w][c], d's output is its INPUT
+// x [n][p][q][k], weights KRSC = torch [in][out][R][S] permuted (in = k, out = c).
+//   forward: y = dgrad(dy := x) (+ bias);  dx = fwd conv of dy_T;  dw = wgrad(x := dy_T, dy := x)
+size_t monet_convT_ws_bytes(int variant, int pass, const monet_conv_desc* d) {
+  if (pass == MONET_PASS_FWD) return monet_conv_ws_bytes(variant, MONET_PASS_DGRAD, d);
+  return std::max(monet_conv_ws_bytes(variant, MONET_PASS_FWD, d), monet_conv_ws_bytes(variant, MONET_PASS_WGRAD, d));
+}
+int monet_convT_fwd(int variant, const monet_conv_desc* d, const float* x, const float* w, const float* bias, float* y,
+                    void* ws, size_t ws_bytes, void* stream) {
+  if (int e = check_desc(d)) return e;
+  if (bias) {
+    const long long tot = (long long)d->n * d->h * d->w * d->c;
+    bias_fill_kernel<<<(int)((tot + 255) / 256), 256, 0, S(stream)>>>(y, bias, (int)(tot / d->c), d->c);
+  }
+  return monet_conv_dgrad(variant, d, x, w, y, bias ? 1 : 0, ws, ws_bytes, stream);
+}
+int monet_convT_bwd(int variant, const monet_conv_desc* d, const float* x, const float* w, const float* dy, float* dx,
+                    int dx_accumulate, float* dw, void* ws, size_t ws_bytes, void* stream) {
+  if (int e = check_desc(d)) return e;
+  if (dx) {
+    GemmParams p = conv_params(MONET_PASS_FWD, d, dy, w, dx);
+    if (int e = launch_gemm(p, variant, dx_accumulate, ws, ws_bytes, S(stream))) return e;
+  }
+  return monet_conv_wgrad(variant, d, dy, x, dw, 0, ws, ws_bytes, stream);
 }
 
 int monet_sgd_step(float* w, const float* g, float* momentum_buf, int64_t n, float lr, float momentum,

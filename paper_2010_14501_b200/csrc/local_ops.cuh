@@ -690,6 +690,58 @@ __global__ void mean_kernel(const float* __restrict__ v, int n, float* out) {
   }
 }
 
+// Small class counts (per-pixel segmentation losses, K <= 32): one thread per row.
+__global__ void xent_small_fwd_kernel(const float* __restrict__ z, const int* __restrict__ labels, float* row_loss,
+                                     long long N, int K) {
+  for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < N; n += (long long)gridDim.x * blockDim.x) {
+    const float* row = z + n * K;
+    float m = -INFINITY;
+    for (int k = 0; k < K; ++k) m = fmaxf(m, row[k]);
+    float s = 0.f;
+    for (int k = 0; k < K; ++k) s += expf(row[k] - m);
+    row_loss[n] = logf(s) + m - row[labels[n]];
+  }
+}
+__global__ void xent_small_bwd_kernel(const float* __restrict__ z, const int* __restrict__ labels,
+                                     const float* __restrict__ dloss, float* dz, long long N, int K, int accumulate) {
+  const float g = *dloss / (float)N;
+  for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < N; n += (long long)gridDim.x * blockDim.x) {
+    const float* row = z + n * K;
+    float m = -INFINITY;
+    for (int k = 0; k < K; ++k) m = fmaxf(m, row[k]);
+    float s = 0.f;
+    for (int k = 0; k < K; ++k) s += expf(row[k] - m);
+    const float inv = 1.f / s;
+    const int lab = labels[n];
+    for (int k = 0; k < K; ++k) {
+      const float v = (expf(row[k] - m) * inv - (k == lab ? 1.f : 0.f)) * g;
+      dz[n * K + k] = accumulate ? dz[n * K + k] + v : v;
+    }
+  }
+}
+// mean of n row losses in two fixed-order levels: 256-wide block sums (fp64), then one thread
+__global__ void block_sum_kernel(const float* __restrict__ v, long long n, double* partial) {
+  __shared__ double sh[256];
+  const long long per = (n + gridDim.x - 1) / gridDim.x;
+  const long long a = blockIdx.x * per, b = min(n, a + per);
+  double s = 0.0;
+  for (long long i = a + threadIdx.x; i < b; i += blockDim.x) s += v[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < (int)blockDim.x; ++k) t += sh[k];
+    partial[blockIdx.x] = t;
+  }
+}
+__global__ void mean_of_partials_kernel(const double* __restrict__ partial, int nb, long long n, float* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < nb; ++i) s += partial[i];
+    *out = (float)(s / (double)n);
+  }
+}
+
 // dz (=|+=) dloss * (softmax(z) - onehot) / N
 __global__ void xent_bwd_kernel(const float* __restrict__ z, const int* __restrict__ labels,
                                 const float* __restrict__ dloss, float* dz, int N, int K, int accumulate) {

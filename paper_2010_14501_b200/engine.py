@@ -153,12 +153,12 @@ class Runtime:
         if x.shape[3] != c:
             x[..., c:].zero_()
         x[..., :c].copy_(images.permute(0, 2, 3, 1), non_blocking=True)
-        self.labels.copy_(labels.to(torch.int32), non_blocking=True)
+        self.labels.copy_(labels.to(torch.int32).reshape(-1), non_blocking=True)  # (N,) or per-pixel (N,H,W)
 
     def set_batch_nhwc(self, images_nhwc: torch.Tensor, labels: torch.Tensor):
         """Stage a batch already in the engine layout (N,H,W,Cpad) — one copy each."""
         self.staging.copy_(images_nhwc.reshape(-1), non_blocking=True)
-        self.labels.copy_(labels, non_blocking=True)
+        self.labels.copy_(labels.reshape(-1), non_blocking=True)
 
     def loss_value(self) -> float:
         return float(self.consts[1].item())
@@ -271,6 +271,12 @@ class Runtime:
                                                                s.workspace, None), d))
                 else:
                     out.append(("k", lib.monet_conv_fwd, (v, C.byref(d), xs[0], wt, y, ws, s.workspace, None), d))
+            elif op.kind == "convT":
+                d = net.conv_desc(op)
+                v = _native.CONV_VARIANTS[s.impl]
+                b = self.pview[(op.id, "bias")].data_ptr() if "bias" in op.params else None
+                out.append(("k", lib.monet_convT_fwd, (v, C.byref(d), xs[0], self.pview[(op.id, "weight")].data_ptr(),
+                                                       b, y, ws, s.workspace, None), d))
             elif op.kind == "concat":
                 pix, ct, off = op.numel // op.shape[3], op.shape[3], 0
                 for j in op.attrs["inputs"]:
@@ -338,7 +344,7 @@ class Runtime:
                             (v, xs[0], self.pview[(op.id, "weight")].data_ptr(),
                              self.pview[(op.id, "bias")].data_ptr(), y, n, fi, fo, ws, s.workspace, None)))
             elif op.kind == "xent":
-                out.append(("k", lib.monet_xent_fwd, (xs[0], self.labels.data_ptr(), y, net.batch,
+                out.append(("k", lib.monet_xent_fwd, (xs[0], self.labels.data_ptr(), y, net.label_count(),
                                                       net.num_classes, self.scratch_ptr, None)))
                 out.append(("copy", self.consts.data_ptr() + 4, y, 4))
             else:
@@ -374,6 +380,18 @@ class Runtime:
             out.append(("k", lib.monet_conv_wgrad, (v, C.byref(d), P(("in", j)), dy,
                                                     self.gview[(op.id, "weight")].data_ptr(), 0, ws,
                                                     s.workspace, None), d))
+            if "bias" in op.params:
+                out.append(("k", lib.monet_bias_grad, (dy, self.gview[(op.id, "bias")].data_ptr(),
+                                                       op.numel // op.shape[-1], op.shape[-1], 0, self.scratch_ptr,
+                                                       None)))
+        elif op.kind == "convT":
+            d = net.conv_desc(op)
+            v = _native.CONV_VARIANTS[s.impl]
+            j = op.deps[0]
+            dxp = P(("g", j)) if net.grad_bytes(net.op(j)) > 0 else None
+            out.append(("k", lib.monet_convT_bwd, (v, C.byref(d), P(("in", j)), self.pview[(op.id, "weight")].data_ptr(),
+                                                   dy, dxp, acc(j) if dxp else 0,
+                                                   self.gview[(op.id, "weight")].data_ptr(), ws, s.workspace, None), d))
             if "bias" in op.params:
                 out.append(("k", lib.monet_bias_grad, (dy, self.gview[(op.id, "bias")].data_ptr(),
                                                        op.numel // op.shape[-1], op.shape[-1], 0, self.scratch_ptr,
@@ -475,7 +493,7 @@ class Runtime:
         elif op.kind == "xent":
             j = op.deps[0]
             out.append(("k", lib.monet_xent_bwd, (P(("in", j)), self.labels.data_ptr(), dy, P(("g", j)),
-                                                  net.batch, net.num_classes, acc(j), None)))
+                                                  net.label_count(), net.num_classes, acc(j), None)))
         else:
             raise ValueError(op.kind)
         return out

@@ -97,6 +97,37 @@ def _conv_calls(bx: _Bench, net, op, variant: str):
     return fwd, bwd
 
 
+def _convT_calls(bx: _Bench, net, op, variant: str):
+    """(fwd closure, bwd closure) of a transposed-conv variant (the conv kernels, roles swapped)."""
+    lib, sp = bx.lib, bx.sp
+    d = net.conv_desc(op)
+    v = _native.CONV_VARIANTS[variant]
+    xin = net.op(op.deps[0])
+    x, y, dy, dx = bx.buf(xin.nbytes), bx.buf(op.nbytes), bx.buf(op.nbytes), bx.buf(xin.nbytes)
+    w = bx.buf(4 * op.attrs["r"] * op.attrs["s"] * xin.shape[3] * op.shape[3])
+    dw = bx.buf(w.numel() * 4)
+    b = bx.buf(4 * op.shape[3]) if "bias" in op.params else None
+    ws_f = lib.monet_convT_ws_bytes(v, 0, C.byref(d))
+    ws_b = lib.monet_convT_ws_bytes(v, 3, C.byref(d))
+    ws = bx.buf(max(ws_f, ws_b))
+    if b is not None:
+        db = bx.buf(4 * op.shape[3])
+        rows = op.numel // op.shape[3]
+        scratch = bx.buf(lib.monet_bn_scratch_bytes(rows, op.shape[3]))
+
+    def fwd():
+        bx.check(lib.monet_convT_fwd(v, C.byref(d), x.data_ptr(), w.data_ptr(), None if b is None else b.data_ptr(),
+                                     y.data_ptr(), ws.data_ptr(), ws_f, sp))
+
+    def bwd():
+        bx.check(lib.monet_convT_bwd(v, C.byref(d), x.data_ptr(), w.data_ptr(), dy.data_ptr(),
+                                     dx.data_ptr() if xin.kind != "input" else None, 0, dw.data_ptr(),
+                                     ws.data_ptr(), ws_b, sp))
+        if b is not None:
+            bx.check(lib.monet_bias_grad(dy.data_ptr(), db.data_ptr(), rows, op.shape[3], 0, scratch.data_ptr(), sp))
+    return fwd, bwd
+
+
 def _local_calls(bx: _Bench, net, op):
     """{(pass, variant): closure} for the non-conv operators (engine.Runtime._bind)."""
     lib, sp = bx.lib, bx.sp
@@ -242,8 +273,9 @@ def _local_calls(bx: _Bench, net, op):
             out[("bwd", name)] = (lambda v=v, wb=wb, ws=ws: bx.check(lib.monet_linear_bwd(
                 v, x.data_ptr(), wgt.data_ptr(), dy.data_ptr(), dx.data_ptr(), 0, dw.data_ptr(), dbias.data_ptr(),
                 nb, fi, fo, ws.data_ptr(), wb, sp)))
-    elif kind == "xent":
-        nb, classes = xin.shape
+    elif kind == "xent":  # (N, K) or per-pixel NHWC logits
+        classes = xin.shape[-1]
+        nb = xin.numel // classes
         labels = torch.randint(0, classes, (nb,), dtype=torch.int32, device=bx.dev)
         loss = bx.buf(4)
         scratch = bx.buf(lib.monet_xent_scratch_bytes(nb))
@@ -273,12 +305,12 @@ def profile_network(net, device="cuda:0", warmup=2, iters=5, reps=3, log=None) -
         sig = _signature(net, op)
         if sig not in cache:
             res = {}
-            if op.kind == "conv":
+            if op.kind in ("conv", "convT"):
                 for name, _ in fv:
-                    f, _b = _conv_calls(bx, net, op, name)
+                    f, _b = (_convT_calls if op.kind == "convT" else _conv_calls)(bx, net, op, name)
                     res[("fwd", name)] = bx.time_ns(f)
                 for name, _, _ in bv:
-                    _f, b = _conv_calls(bx, net, op, name)
+                    _f, b = (_convT_calls if op.kind == "convT" else _conv_calls)(bx, net, op, name)
                     res[("bwd", name)] = bx.time_ns(b)
             else:
                 calls = _local_calls(bx, net, op)

@@ -132,10 +132,10 @@ class Network:
         lib = _native.lib()
         s = 0
         for op in self.ops:
-            if op.kind in ("bn", "bnrelu", "bnrelu6") or (op.kind == "conv" and "bias" in op.params):
+            if op.kind in ("bn", "bnrelu", "bnrelu6") or (op.kind in ("conv", "convT") and "bias" in op.params):
                 rows = op.numel // op.shape[-1]  # conv bias gradient: per-channel sum of dy
                 s = max(s, lib.bn_scratch_bytes(rows, op.shape[-1]))
-        s = max(s, lib.xent_scratch_bytes(self.batch))
+        s = max(s, lib.xent_scratch_bytes(self.label_count()))
         return (s + 255) // 256 * 256
 
     def input_bytes(self) -> int:
@@ -149,7 +149,7 @@ class Network:
             "bn_stats": 4 * self.bn_channels() * F32,   # saved mean/invstd, running mean/var
             "scratch": self.scratch_bytes(),
             "staging_input": self.input_bytes(),
-            "labels": self.batch * 4,
+            "labels": self.label_count() * 4,
             "consts": 256,
         }
 
@@ -174,6 +174,11 @@ class Network:
                 inters.append({"id": u, "bytes": self.intermediate_bytes[u], "creator": op.id})
         return {"format": 1, "params_bytes": self.params_bytes(), "nodes": nodes,
                 "backward": backward, "intermediates": inters}
+
+    def label_count(self) -> int:
+        """Rows of the loss: images, or pixels for a per-pixel (segmentation) loss."""
+        logits = self.op(self.ops[-1].deps[0])
+        return logits.numel // logits.shape[-1]
 
     def fc_dims(self, op: Op):
         """(rows, in_features) of an fc op; a 4-D input is read flattened (NHWC order)."""
@@ -210,6 +215,14 @@ class Network:
             fwd.append((op.kind, 0))
             bwd += [("bwd-in", 0, x), ("bwd-out", 0, [op.id]),
                     ("bwd-mask", 0, [self.intermediate_of[op.id]])]
+        elif op.kind == "convT":  # transposed conv: the conv kernels with the roles swapped
+            d = self.conv_desc(op)
+            fwd.append(("implicit", lib.convT_ws_bytes(0, 0, d)))
+            ws = lib.convT_ws_bytes(1, 0, d)
+            if ws:
+                fwd.append(("splitk", ws))
+            bwd.append(("splitk", lib.convT_ws_bytes(1, 3, d), x))
+            bwd.append(("implicit", lib.convT_ws_bytes(0, 3, d), x))
         elif op.kind == "dwconv":  # depthwise: one direct kernel per pass, wgrad partials in ws
             fwd.append(("direct", 0))
             bwd.append(("direct", lib.dwconv_ws_bytes(self.conv_desc(op)), x))
@@ -259,6 +272,11 @@ class Network:
         return {"format": 1, "forward": fwd_doc, "backward": bwd_doc}
 
     def conv_desc(self, op: Op):
+        if op.kind == "convT":  # the conv whose input is this op's output and whose output is its input
+            n, p, q, k = self.op(op.deps[0]).shape
+            _, h, w, c = op.shape
+            a = op.attrs
+            return _native.ConvDesc(n, h, w, c, k, a["r"], a["s"], p, q, a["stride"], a["stride"], a["pad"], a["pad"])
         n, h, w, c = self.op(op.deps[0]).shape
         a = op.attrs
         return _native.ConvDesc(n, h, w, c, op.shape[3], a["r"], a["s"], op.shape[1], op.shape[2],
@@ -300,7 +318,8 @@ BWD_IMPLS = {
     "dropout": [("bwd-rng", "input")],
     "concat": [("bwd", "input")],  # catalog deps []: the backward slices dy
     "relu6": [("bwd-in", "input"), ("bwd-out", "output"), ("bwd-mask", "intermediate")],
-    "dwconv": [("direct", "input")],  # catalog deps []: the keep-mask is regenerated from the step seed
+    "dwconv": [("direct", "input")],
+    "convT": [("splitk", "input"), ("implicit", "input")],  # catalog deps []: the keep-mask is regenerated from the step seed
     "add": [("bwd", "input")],
     "avgpool": [("bwd", "input")],
     "xent": [("bwd", "input")],
@@ -418,6 +437,20 @@ def trace_graph(model: torch.nn.Module, example_input: torch.Tensor, num_classes
                 ops.append(Op(nid, "relu", (src,), x.shape, name=node.target))
             elif isinstance(mod, torch.nn.ReLU6):
                 ops.append(Op(nid, "relu6", (src,), x.shape, name=node.target))
+            elif isinstance(mod, torch.nn.ConvTranspose2d):
+                if mod.groups != 1 or _pair(mod.dilation) != 1 or _pair(mod.output_padding) != 0:
+                    raise NotImplementedError(f"{node.target}: plain transposed convs only")
+                r, s = mod.kernel_size
+                st, pd = _pair(mod.stride), _pair(mod.padding)
+                _, hh, ww, cin = x.shape
+                p = (hh - 1) * st - 2 * pd + r
+                q = (ww - 1) * st - 2 * pd + s
+                wt = mod.weight.detach().float().permute(0, 2, 3, 1).contiguous()  # [in][R][S][out] = KRSC
+                prm = {"weight": wt}
+                if mod.bias is not None:
+                    prm["bias"] = mod.bias.detach().float().clone()
+                ops.append(Op(nid, "convT", (src,), (n, p, q, mod.out_channels),
+                              {"r": r, "s": s, "stride": st, "pad": pd}, prm, node.target))
             elif isinstance(mod, torch.nn.MaxPool2d):
                 r = _pair(mod.kernel_size)
                 st, pd = _pair(mod.stride), _pair(mod.padding)
@@ -503,6 +536,21 @@ def trace_graph(model: torch.nn.Module, example_input: torch.Tensor, num_classes
     return Network(fuse_bn_relu(ops) if fuse else ops, n, k)
 
 
+def parse_image(v):
+    """Image size argument: 224, "224", or "HxW" (UNet: "416x608") -> int or (h, w)."""
+    if isinstance(v, (tuple, list)):
+        return tuple(v)
+    if "x" in str(v):
+        h, w = str(v).split("x")
+        return int(h), int(w)
+    return int(v)
+
+
+def default_classes(arch: str) -> int:
+    """Classes of the benchmark configs: ImageNet's 1000, UNet's 4 (segmentation)."""
+    return 4 if arch == "unet" else 1000
+
+
 def build_network(arch: str, batch: int, image: int | tuple = 224, num_classes: int = 1000,
                   seed: int = 0, fuse: bool = False) -> Network:
     """torchvision ``arch`` with default init under ``torch.manual_seed(seed)``, traced
@@ -510,7 +558,54 @@ def build_network(arch: str, batch: int, image: int | tuple = 224, num_classes: 
     import torchvision
 
     torch.manual_seed(seed)
-    kw = {"aux_logits": False, "init_weights": True} if arch in ("googlenet", "inception_v3") else {}
-    model = getattr(torchvision.models, arch)(num_classes=num_classes, **kw)
+    if arch == "unet":
+        model = UNet(num_classes)
+    else:
+        kw = {"aux_logits": False, "init_weights": True} if arch in ("googlenet", "inception_v3") else {}
+        model = getattr(torchvision.models, arch)(num_classes=num_classes, **kw)
     hw = (image, image) if isinstance(image, int) else image
     return trace_graph(model, torch.empty(batch, 3, *hw, device="meta"), num_classes, fuse)
+
+
+# ------------------------------------------------------------------ UNet (config C3)
+class _DoubleConv(torch.nn.Sequential):
+    def __init__(self, cin, cout):
+        super().__init__(torch.nn.Conv2d(cin, cout, 3, padding=1, bias=False), torch.nn.BatchNorm2d(cout),
+                         torch.nn.ReLU(inplace=True), torch.nn.Conv2d(cout, cout, 3, padding=1, bias=False),
+                         torch.nn.BatchNorm2d(cout), torch.nn.ReLU(inplace=True))
+
+
+class _Up(torch.nn.Module):
+    def __init__(self, cin, cout):
+        super().__init__()
+        self.up = torch.nn.ConvTranspose2d(cin, cin // 2, 2, stride=2)
+        self.conv = _DoubleConv(cin, cout)
+
+    def forward(self, x, skip):
+        return self.conv(torch.cat([skip, self.up(x)], dim=1))
+
+
+class UNet(torch.nn.Module):
+    """The UNet of config C3 (MONeT's segmentation benchmark, 608 x 416): the common
+    DoubleConv / Down (maxpool + DoubleConv) / Up (2x2 stride-2 transposed conv, skip concat,
+    DoubleConv) / 1x1 OutConv layout, widths 64..1024.  Input sizes divisible by 16 (no
+    crop / pad in the skips).  Classes must be a multiple of 4 (the conv kernels' channel
+    granularity); the loss is the per-pixel softmax cross-entropy."""
+
+    def __init__(self, num_classes=4, in_channels=3, width=64):
+        super().__init__()
+        w = width
+        self.inc = _DoubleConv(in_channels, w)
+        self.down = torch.nn.ModuleList(
+            torch.nn.Sequential(torch.nn.MaxPool2d(2), _DoubleConv(w * 2 ** i, w * 2 ** (i + 1))) for i in range(4))
+        self.up = torch.nn.ModuleList(_Up(w * 2 ** (4 - i), w * 2 ** (3 - i)) for i in range(4))
+        self.outc = torch.nn.Conv2d(w, num_classes, 1)
+
+    def forward(self, x):
+        skips = [self.inc(x)]
+        for d in self.down:
+            skips.append(d(skips[-1]))
+        y = skips.pop()
+        for u in self.up:
+            y = u(y, skips.pop())
+        return self.outc(y)

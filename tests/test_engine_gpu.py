@@ -256,3 +256,37 @@ def test_googlenet_engine(cuda, fuse):
         got = rt.pview[(nid, pname)].view(v.shape)
         assert (got.cpu().double() - v.double()).abs().max().item() <= REL * max(v.abs().max().item(), 0.05), \
             (net.op(nid).name, pname)
+
+
+def test_unet_engine(cuda):
+    """UNet (width 8, 32 x 48): transposed convs with bias, decoder concats, per-pixel loss, under a
+    recompute schedule -- ledger = simulate(), recomputes bit-identical, loss / weights = oracle."""
+    from paper_2010_14501_b200.tracer import UNet
+
+    torch.manual_seed(0)
+    net = M.trace_graph(UNet(num_classes=4, width=8), torch.empty(2, 3, 32, 48, device="meta"), 4, fuse=True)
+    g = M.load_graph(net.graph_doc())
+    cat = M.load_catalog(net.catalog_doc(), g)
+    se = M.store_everything_schedule(g, cat)
+    act = M.simulate(se, g, cat).peak_memory - g.params_bytes
+    from paper_2010_14501_b200.planner import plan_schedule
+    sched, _ = plan_schedule(g, cat, g.params_bytes + int(0.6 * act), kinds=net.storable_kinds())
+    assert sched is not None and any(s.recompute for s in sched.stages)
+    gen = torch.Generator().manual_seed(0)
+    x = torch.randn(2, 3, 32, 48, generator=gen)
+    y = torch.randint(0, 4, (2, 32, 48), generator=gen)
+    rt = Runtime(net)
+    rt.set_batch(x.to(cuda), y.to(cuda))
+    plan = rt.plan(sched, g, cat)
+    assert M.trace_report(plan.trace) == M.trace_report(M.simulate(sched, g, cat))
+    acts, mismatched = capture(rt, plan)
+    assert not mismatched
+    doc = M.schedule_to_doc(sched)
+    loss = run_step(CpuState(net), doc, x, y)
+    assert abs(rt.loss_value() - loss) <= REL * abs(loss)
+    st = CpuState(net)
+    run_step(st, doc, x, y, forced=acts)
+    for (nid, pname), v in params_nhwc(st).items():
+        got = rt.pview[(nid, pname)].view(v.shape)
+        assert (got.cpu().double() - v.double()).abs().max().item() <= REL * max(v.abs().max().item(), 0.05), \
+            (net.op(nid).name, pname)

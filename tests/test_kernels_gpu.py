@@ -451,3 +451,56 @@ def test_relu6_mask_and_backward(cuda):
         dx = torch.empty_like(x)
         fn(src.data_ptr(), dy.data_ptr(), dx.data_ptr(), n, 0, stream())
         assert torch.equal(dx, ref)
+
+
+@pytest.mark.parametrize("variant", ["implicit", "splitk"])
+def test_conv_transpose(cuda, variant):
+    """ConvTranspose2d(2x2, stride 2) through the conv kernels: forward = dgrad (+ bias),
+    input gradient = forward conv (accumulating), weight gradient = wgrad."""
+    n, h, w, cin, cout = 2, 9, 13, 64, 32
+    g = torch.Generator().manual_seed(9)
+    x = torch.randn(n, h, w, cin, generator=g)
+    wt = torch.randn(cin, cout, 2, 2, generator=g) / 8
+    b = torch.randn(cout, generator=g)
+    d = N.conv_desc(n, 2 * h, 2 * w, cout, cin, 2, 2, 2, 0)  # the adjoint conv: y -> x
+    assert (d.p, d.q) == (h, w)
+    lib = N.lib()
+    v = N.CONV_VARIANTS[variant]
+    xd, wd, bd = x.to(cuda), wt.permute(0, 2, 3, 1).contiguous().to(cuda), b.to(cuda)
+    y = torch.empty(n, 2 * h, 2 * w, cout, device=cuda)
+    wsb = max(lib.convT_ws_bytes(v, 0, d), lib.convT_ws_bytes(v, 3, d))
+    ws = torch.empty(wsb // 4 + 1, device=cuda)
+    lib.convT_fwd(v, d, xd.data_ptr(), wd.data_ptr(), bd.data_ptr(), y.data_ptr(), ws.data_ptr(), wsb, stream())
+    xr = x.double().permute(0, 3, 1, 2).requires_grad_()
+    wr = wt.double().requires_grad_()
+    yr = F.conv_transpose2d(xr, wr, b.double(), stride=2)
+    assert rel_err(y, yr.detach().permute(0, 2, 3, 1)) < REL_TC
+    dy = torch.randn(n, 2 * h, 2 * w, cout, generator=g)
+    yr.backward(dy.double().permute(0, 3, 1, 2))
+    dx = torch.ones(n, h, w, cin, device=cuda)
+    dw = torch.empty(cin, 2, 2, cout, device=cuda)
+    lib.convT_bwd(v, d, xd.data_ptr(), wd.data_ptr(), dy.to(cuda).data_ptr(), dx.data_ptr(), 1, dw.data_ptr(),
+                  ws.data_ptr(), wsb, stream())
+    assert rel_err(dx, 1 + xr.grad.permute(0, 2, 3, 1)) < REL_TC
+    assert rel_err(dw, wr.grad.permute(0, 2, 3, 1)) < REL_TC
+
+
+def test_pixel_xent(cuda):
+    """Per-pixel softmax cross-entropy (K <= 32 path): loss = mean over N*H*W rows."""
+    rows, k = 3 * 40 * 56, 4
+    g = torch.Generator().manual_seed(10)
+    z = torch.randn(rows, k, generator=g)
+    lab = torch.randint(0, k, (rows,), generator=g, dtype=torch.int32)
+    lib = N.lib()
+    zd, ld = z.to(cuda), lab.to(cuda)
+    loss = torch.zeros(1, device=cuda)
+    scratch = torch.empty(lib.xent_scratch_bytes(rows) // 4 + 1, device=cuda)
+    lib.xent_fwd(zd.data_ptr(), ld.data_ptr(), loss.data_ptr(), rows, k, scratch.data_ptr(), stream())
+    zr = z.double().requires_grad_()
+    ref = F.cross_entropy(zr, lab.long())
+    ref.backward()
+    assert abs(loss.item() - ref.item()) < 1e-5 * abs(ref.item())
+    one = torch.ones(1, device=cuda)
+    dz = torch.empty(rows, k, device=cuda)
+    lib.xent_bwd(zd.data_ptr(), ld.data_ptr(), one.data_ptr(), dz.data_ptr(), rows, k, 0, stream())
+    assert rel_err(dz, zr.grad) < 1e-5

@@ -285,3 +285,40 @@ def test_oracle_googlenet_equals_autograd(fuse):
                 have = _torch_layout(net, op, pname, got[(op.id, pname)], want)
                 err = (have.double() - want.double()).abs().max().item()
                 assert err <= TOL * max(want.double().abs().max().item(), 1e-3), (name, op.name, pname)
+
+
+def test_oracle_unet_equals_autograd():
+    """UNet: transposed convs (with bias), decoder concats and the per-pixel cross-entropy."""
+    from paper_2010_14501_b200.tracer import UNet
+
+    torch.manual_seed(0)
+    model = UNet(num_classes=4, width=8)
+    net = trace_graph(model, torch.empty(2, 3, 32, 48, device="meta"), 4)
+    assert {"convT", "concat", "xent"} <= {op.kind for op in net.ops}
+    assert net.label_count() == 2 * 32 * 48
+    g = M.load_graph(net.graph_doc())
+    cat = M.load_catalog(net.catalog_doc(), g)
+    gen = torch.Generator().manual_seed(1)
+    x = torch.randn(2, 3, 32, 48, generator=gen)
+    y = torch.randint(0, 4, (2, 32, 48), generator=gen)
+    scheds = [("store_everything", M.store_everything_schedule(g, cat))] + _planned(net, g, cat)
+    assert len(scheds) > 1, "no recompute schedule to test"
+    for name, sched in scheds:
+        ref_model = UNet(num_classes=4, width=8)
+        ref_model.load_state_dict(model.state_dict())
+        ref_loss = _autograd_step(ref_model, x, y)
+        st = CpuState(net, dtype=torch.float64)
+        loss = run_step(st, M.schedule_to_doc(sched), x.double(), y)
+        assert abs(loss - ref_loss) <= TOL * abs(ref_loss), name
+        ref = {n: p.detach() for n, p in ref_model.named_parameters()}
+        got = params_nhwc(st)
+        for op in net.ops:
+            for pname in op.params:
+                want = ref[f"{op.name}.{pname}"]
+                have = got[(op.id, pname)]
+                if op.kind == "conv" and pname == "weight":
+                    have = have[..., : want.shape[1]].permute(0, 3, 1, 2)
+                elif op.kind == "convT" and pname == "weight":
+                    have = have.permute(0, 3, 1, 2)
+                err = (have.double() - want.double()).abs().max().item()
+                assert err <= TOL * max(want.double().abs().max().item(), 1e-3), (name, op.name, pname)

@@ -17,7 +17,7 @@ sys.path.insert(0, str(ROOT))
 
 import paper_2010_14501_b200 as M  # noqa: E402
 from paper_2010_14501_b200.planner import plan_schedule  # noqa: E402
-from paper_2010_14501_b200.tracer import build_network  # noqa: E402
+from paper_2010_14501_b200.tracer import build_network, default_classes, parse_image  # noqa: E402
 
 OUT = ROOT / "schedules"
 
@@ -29,7 +29,7 @@ def digest(doc):
 def main(jobs, exact_time_s=None):
     OUT.mkdir(exist_ok=True)
     for arch, batch, img, gib, fuse in jobs:
-        net = build_network(arch, batch, img, fuse=fuse)
+        net = build_network(arch, batch, parse_image(img), num_classes=default_classes(arch), fuse=fuse)
         arch = arch + ("_fused" if net.fused else "")
         gdoc, cdoc = net.graph_doc(), net.catalog_doc()
         measured = ROOT / "profiles" / f"catalog_{arch}_b{batch}_{img}.json"
@@ -62,7 +62,7 @@ if __name__ == "__main__":
     ap.add_argument("--fused", action="store_true")
     ap.add_argument("--arch", default="resnet50")
     ap.add_argument("--batch", type=int, default=184)
-    ap.add_argument("--image", type=int, default=224)
+    ap.add_argument("--image", default="224", help="224 or HxW (UNet: 416x608)")
     ap.add_argument("--budgets", default="10,8,6", help="GiB, comma separated")
     ap.add_argument("--exact", type=float, default=None,
                     help="seconds of exact ILP search on graphs of <= planner.EXACT_MAX_NODES nodes")

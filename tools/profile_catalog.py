@@ -16,7 +16,7 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
 from paper_2010_14501_b200.profiler import profile_network  # noqa: E402
-from paper_2010_14501_b200.tracer import build_network  # noqa: E402
+from paper_2010_14501_b200.tracer import build_network, default_classes, parse_image  # noqa: E402
 
 
 def digest(doc):
@@ -24,7 +24,7 @@ def digest(doc):
 
 
 def main(arch="resnet50", batch=184, image=224, fuse=False):
-    net = build_network(arch, batch, image, fuse=fuse)
+    net = build_network(arch, batch, parse_image(image), num_classes=default_classes(arch), fuse=fuse)
     arch = arch + ("_fused" if net.fused else "")
     t = time.time()
     costs = profile_network(net, log=print)
@@ -38,4 +38,4 @@ def main(arch="resnet50", batch=184, image=224, fuse=False):
 if __name__ == "__main__":
     fuse = "--fused" in sys.argv
     a = [x for x in sys.argv[1:] if x != "--fused"]
-    main(a[0], int(a[1]), int(a[2]), fuse) if a else main(fuse=fuse)
+    main(a[0], int(a[1]), a[2], fuse) if a else main(fuse=fuse)

@@ -13,7 +13,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
-from paper_2010_14501_b200.tracer import build_network, r16  # noqa: E402
+from paper_2010_14501_b200.tracer import build_network, default_classes, parse_image, r16  # noqa: E402
 
 
 def digest(doc):
@@ -23,7 +23,8 @@ def digest(doc):
 for path in sorted((ROOT / "profiles").glob("catalog_*.json")):
     doc = json.loads(path.read_text())
     arch = doc["arch"].removesuffix("_fused")
-    net = build_network(arch, doc["batch"], doc["image"], fuse=doc["arch"].endswith("_fused"))
+    net = build_network(arch, doc["batch"], parse_image(doc["image"]), num_classes=default_classes(arch),
+                        fuse=doc["arch"].endswith("_fused"))
     fresh = net.catalog_doc()
     ws = {}
     for sec in ("forward", "backward"):
