@@ -7,3 +7,4 @@ done
 bash tools/gpu_bench_vgg.sh
 bash tools/gpu_bench_c4.sh
 ARCH=googlenet B=320 bash tools/gpu_bench_c4.sh
+ARCH=unet B=11 IMG=416x608 bash tools/gpu_bench_c4.sh
