@@ -148,6 +148,7 @@ LOCAL_BYTES = {  # minimal fp32 HBM bytes per element
     ("bn", "bwd"): 20.0, ("add", "forward"): 12.0, ("add", "bwd"): 16.0,
     ("bnrelu", "train"): 12.0, ("bnrelu", "replay"): 8.0, ("bnrelu", "bwd"): 20.0,
     ("bnrelu6", "train"): 12.0, ("bnrelu6", "replay"): 8.0, ("bnrelu6", "bwd"): 20.0,
+    ("bnaddrelu", "train"): 16.0, ("bnaddrelu", "replay"): 12.0, ("bnaddrelu", "bwd"): 32.0,
     ("addrelu", "forward"): 12.0, ("addrelu", "bwd-out"): 16.0, ("addrelu", "bwd-in"): 20.0,
 }
 
@@ -186,10 +187,10 @@ def kernel_roofline(rt, plan, net, peaks):
             conv_t += ms
             conv_f += f
             n_conv += 1
-        elif op.kind in ("relu", "bn", "bnrelu", "bnrelu6", "add", "addrelu"):
+        elif op.kind in ("relu", "bn", "bnrelu", "bnrelu6", "bnaddrelu", "add", "addrelu"):
             if s.kind == "backward":
                 key = (op.kind, s.impl) if op.kind in ("relu", "addrelu") else (op.kind, "bwd")
-            elif op.kind in ("bn", "bnrelu", "bnrelu6"):
+            elif op.kind in ("bn", "bnrelu", "bnrelu6", "bnaddrelu"):
                 key = (op.kind, "train" if s.kind == "forward" else "replay")
             elif op.kind == "relu":
                 key = ("relu", "forward", net.intermediate_of[op.id] in s.planned_ints)

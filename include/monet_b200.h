@@ -176,6 +176,20 @@ int monet_bnrelu6_bwd(const float* x, const float* dz, float* dx, int accumulate
                       const float* beta, const float* saved_mean, const float* saved_invstd, float* dgamma,
                       float* dbeta, int64_t rows, int c, void* scratch, void* stream);
 
+/* fused BN + residual add + ReLU (a bottleneck's last BN feeding its join): z = max(BN(x) + skip, 0),
+ * the BN output never exists.  Backward gate from z (gate_from_out = 1, gate_src = z) or recomputed
+ * from x and skip (0, gate_src = skip); writes / accumulates dx and dskip in one pass. */
+int monet_bnaddrelu_fwd_train(const float* x, const float* skip, float* z, const float* gamma, const float* beta,
+                              float* saved_mean, float* saved_invstd, float* running_mean, float* running_var,
+                              int64_t rows, int c, float eps, float momentum, int update_running, void* scratch,
+                              void* stream);
+int monet_bnaddrelu_fwd_replay(const float* x, const float* skip, float* z, const float* gamma, const float* beta,
+                               const float* saved_mean, const float* saved_invstd, int64_t rows, int c, void* stream);
+int monet_bnaddrelu_bwd(const float* x, const float* gate_src, int gate_from_out, const float* dz, float* dx,
+                        int acc_x, float* dskip, int acc_skip, const float* gamma, const float* beta,
+                        const float* saved_mean, const float* saved_invstd, float* dgamma, float* dbeta, int64_t rows,
+                        int c, void* scratch, void* stream);
+
 /* --- residual add / gradient pass-through (K12) --------------------------- */
 int monet_add_fwd(const float* a, const float* b, float* y, int64_t n, void* stream);
 int monet_grad_pass(const float* dy, float* dx, int64_t n, float scale, int accumulate, void* stream);

@@ -46,7 +46,7 @@ class CpuState:
         self.mom = {k: torch.zeros_like(v) for k, v in self.params.items()}
         self.running = {op.id: [op.attrs["running_mean"].to(dtype).clone(),
                                 op.attrs["running_var"].to(dtype).clone()]
-                        for op in net.ops if op.kind in ("bn", "bnrelu", "bnrelu6")}
+                        for op in net.ops if op.kind in ("bn", "bnrelu", "bnrelu6", "bnaddrelu")}
         self.saved = {}
         self.grads = {}
         self.seed = 0  # dropout step seed: the engine's device counter, advanced once per step
@@ -131,19 +131,23 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
                 gate = (x > 0) & (x < 6)
                 extra = pack_sign_mask(torch.where(gate, 1.0, -1.0).permute(0, 2, 3, 1).numpy()
                                        if x.dim() == 4 else torch.where(gate, 1.0, -1.0).numpy())
-        elif op.kind in ("bn", "bnrelu", "bnrelu6"):
+        elif op.kind in ("bn", "bnrelu", "bnrelu6", "bnaddrelu"):
             g, b = P[(op.id, "weight")], P[(op.id, "bias")]
+            xin = x_of(op.attrs["x"]) if op.kind == "bnaddrelu" else xs[0]
             if mode == "forward":
-                mean, invstd, var = _bn_stats(xs[0], op.attrs["eps"])
+                mean, invstd, var = _bn_stats(xin, op.attrs["eps"])
                 state.saved[op.id] = (mean, invstd)
                 m = op.attrs["momentum"]
-                rows = xs[0].numel() // xs[0].shape[1]
+                rows = xin.numel() // xin.shape[1]
                 rm, rv = state.running[op.id]
                 rm.mul_(1 - m).add_(m * mean)
                 rv.mul_(1 - m).add_(m * var * rows / max(rows - 1, 1))
             mean, invstd = state.saved[op.id]
-            y = _bn_apply(xs[0], mean, invstd, g, b)
-            if op.kind == "bnrelu":  # fused: relu(BN(x)); the BN output is never kept
+            y = _bn_apply(xin, mean, invstd, g, b)
+            if op.kind == "bnaddrelu":  # fused: relu(BN(x) + skip); the BN output is never kept
+                y = y + x_of(op.attrs["skip"])
+                y = torch.where(y > 0, y, torch.zeros_like(y))
+            elif op.kind == "bnrelu":  # fused: relu(BN(x)); the BN output is never kept
                 y = torch.where(y > 0, y, torch.zeros_like(y))
             elif op.kind == "bnrelu6":  # fused: relu6(BN(x))
                 y = torch.clamp(y, 0.0, 6.0)
@@ -236,8 +240,8 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
                 s_ = x_of(op.id) if impl == "bwd-out" else x_of(j)
                 keep = (s_ > 0) & (s_ < 6)
             put_grad(j, torch.where(keep, dy, torch.zeros_like(dy)), created)
-        elif op.kind in ("bn", "bnrelu", "bnrelu6"):
-            j = op.deps[0]
+        elif op.kind in ("bn", "bnrelu", "bnrelu6", "bnaddrelu"):
+            j = op.attrs["x"] if op.kind == "bnaddrelu" else op.deps[0]
             g, b = P[(op.id, "weight")], P[(op.id, "bias")]
             mean, invstd = state.saved[op.id]
             v = lambda t: t.view(1, -1, 1, 1)
@@ -246,7 +250,14 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
             elif op.kind == "bnrelu6":
                 z = _bn_apply(x_of(j), mean, invstd, g, b)
                 dy = torch.where((z > 0) & (z < 6), dy, torch.zeros_like(dy))
-            if impl == "bwd-in":
+            elif op.kind == "bnaddrelu":  # gate from z (bwd-out) or recomputed from x and skip (bwd-in)
+                if impl == "bwd-out":
+                    gate = x_of(op.id) > 0
+                else:
+                    gate = (_bn_apply(x_of(j), mean, invstd, g, b) + x_of(op.attrs["skip"])) > 0
+                dy = torch.where(gate, dy, torch.zeros_like(dy))
+                put_grad(op.attrs["skip"], dy.clone(), created)
+            if impl == "bwd-in" or op.kind == "bnaddrelu":  # bnaddrelu's bwd-out names the gate source only
                 xhat = (x_of(j) - v(mean)) * v(invstd)
             else:
                 gc = torch.where(g.abs() < 1e-12, torch.full_like(g, 1e-12) * torch.where(g < 0, -1.0, 1.0), g)

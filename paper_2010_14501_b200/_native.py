@@ -70,6 +70,11 @@ SIGNATURES = {
                                        _vp]),
     "monet_bnrelu6_fwd_replay": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp]),
     "monet_bnrelu6_bwd": (_i32, [_vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp]),
+    "monet_bnaddrelu_fwd_train": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _f32, _f32, _i32,
+                                         _vp, _vp]),
+    "monet_bnaddrelu_fwd_replay": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp]),
+    "monet_bnaddrelu_bwd": (_i32, [_vp, _vp, _i32, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i64,
+                                   _i32, _vp, _vp]),
     "monet_add_fwd": (_i32, [_vp, _vp, _vp, _i64, _vp]),
     "monet_grad_pass": (_i32, [_vp, _vp, _i64, _f32, _i32, _vp]),
     "monet_addrelu_fwd": (_i32, [_vp, _vp, _vp, _i64, _vp]),

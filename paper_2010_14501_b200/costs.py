@@ -51,6 +51,8 @@ def analytic_cost(net, op, pass_, name) -> int:
         return _ns(nbytes=(8.125 if name == "bwd-mask" else 12.0) * n)
     if op.kind == "bn":
         return _ns(nbytes=(12.0 if pass_ == "fwd" else 20.0) * n, launches=3)
+    if op.kind == "bnaddrelu":  # stats r4 + apply r4 r4 w4; bwd reduce r4 r4 r4 + apply r4 r4 r4 w4 w4
+        return _ns(nbytes=(16.0 if pass_ == "fwd" else 32.0) * n, launches=3)
     if op.kind in ("bnrelu", "bnrelu6"):  # stats r4 + apply r4 w4; bwd reduce r4 r4 + apply r4 r4 w4
         return _ns(nbytes=(12.0 if pass_ == "fwd" else 20.0) * n, launches=3)
     if op.kind == "addrelu":  # fwd r4 r4 w4; bwd r4 (gate) r4 (dz) w4 w4

@@ -990,6 +990,50 @@ int monet_bnrelu6_bwd(const float* x, const float* dz, float* dx, int accumulate
                           scratch, stream);
 }
 
+// fused BN + residual add + ReLU: z = max(BN(x) + skip, 0)
+int monet_bnaddrelu_fwd_train(const float* x, const float* skip, float* z, const float* gamma, const float* beta,
+                              float* saved_mean, float* saved_invstd, float* running_mean, float* running_var,
+                              int64_t rows, int c, float eps, float momentum, int update_running, void* scratch,
+                              void* stream) {
+  if (c % 4) return -(int)cudaErrorInvalidValue;
+  cudaStream_t st = S(stream);
+  float* ws = static_cast<float*>(scratch);
+  int nb = bn_blocks(rows);
+  bn_reduce_kernel<<<nb, kEwThreads, 0, st>>>(0, x, nullptr, nullptr, nullptr, rows, c, ws);
+  bn_finalize_fwd_kernel<<<(c + 7) / 8, 256, 0, st>>>(ws, nb, rows, c, eps, momentum, update_running, saved_mean,
+                                                      saved_invstd, running_mean, running_var);
+  bnaddrelu_apply_kernel<<<ew_blocks(rows * c / 4), kEwThreads, 0, st>>>(x, skip, z, saved_mean, saved_invstd, gamma,
+                                                                         beta, rows, c);
+  return last_error();
+}
+int monet_bnaddrelu_fwd_replay(const float* x, const float* skip, float* z, const float* gamma, const float* beta,
+                               const float* saved_mean, const float* saved_invstd, int64_t rows, int c, void* stream) {
+  if (c % 4) return -(int)cudaErrorInvalidValue;
+  bnaddrelu_apply_kernel<<<ew_blocks(rows * c / 4), kEwThreads, 0, S(stream)>>>(x, skip, z, saved_mean, saved_invstd,
+                                                                                gamma, beta, rows, c);
+  return last_error();
+}
+// gate_src = z (gate_from_out = 1, output-activated) or skip (0, input-activated)
+int monet_bnaddrelu_bwd(const float* x, const float* gate_src, int gate_from_out, const float* dz, float* dx,
+                        int acc_x, float* dskip, int acc_skip, const float* gamma, const float* beta,
+                        const float* saved_mean, const float* saved_invstd, float* dgamma, float* dbeta, int64_t rows,
+                        int c, void* scratch, void* stream) {
+  if (c % 4) return -(int)cudaErrorInvalidValue;
+  cudaStream_t st = S(stream);
+  float* ws = static_cast<float*>(scratch);
+  int nb = bn_blocks(rows);
+  float* coef_b = ws + (size_t)nb * 2 * c;
+  float* coef_c = coef_b + c;
+  bn_reduce_kernel<<<nb, kEwThreads, 0, st>>>(gate_from_out ? 5 : 6, x, dz, saved_mean, saved_invstd, rows, c, ws,
+                                              gamma, beta, gate_src);
+  bn_finalize_bwd_kernel<<<(c + 7) / 8, 256, 0, st>>>(ws, nb, c, rows, saved_mean, saved_invstd, gamma,
+                                                      saved_invstd, coef_b, coef_c, dgamma, dbeta);
+  bnaddrelu_bwd_apply_kernel<<<ew_blocks(rows * c / 4), kEwThreads, 0, st>>>(
+      x, gate_src, gate_from_out, dz, dx, acc_x, dskip, acc_skip, saved_mean, beta, gamma, saved_invstd, coef_b,
+      coef_c, rows, c);
+  return last_error();
+}
+
 // ------------------------------------------------------------------- add / pass
 int monet_add_fwd(const float* a, const float* b, float* y, int64_t n, void* stream) {
   add_kernel<<<ew_blocks(n / 4 + 1), kEwThreads, 0, S(stream)>>>(a, b, y, n);

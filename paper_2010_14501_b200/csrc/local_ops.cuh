@@ -252,10 +252,12 @@ __host__ __device__ inline BnLayout bn_layout(int C) {
 // mode 3: as mode 1 with dy = dz * [gamma*xhat + beta > 0]  (fused BN+ReLU
 //         backward from x; p2 / p3 = gamma / beta)
 // mode 4: as mode 3 with the ReLU6 gate [0 < gamma*xhat + beta < 6]  (fused BN+ReLU6)
+// mode 5: as mode 1 with dy = dz * [z > 0], z = p4  (fused BN+add+ReLU, gate from its output)
+// mode 6: as mode 1 with dy = dz * [gamma*xhat + beta + skip > 0], skip = p4 (gate from its inputs)
 __global__ void bn_reduce_kernel(int mode, const float* __restrict__ x, const float* __restrict__ dy,
                                  const float* __restrict__ p0, const float* __restrict__ p1, long long rows, int C,
                                  float* __restrict__ ws, const float* __restrict__ p2 = nullptr,
-                                 const float* __restrict__ p3 = nullptr) {
+                                 const float* __restrict__ p3 = nullptr, const float* __restrict__ p4 = nullptr) {
   const BnLayout L = bn_layout(C);
   const int t = threadIdx.x;
   const int rsub = t / L.tpr;
@@ -273,12 +275,22 @@ __global__ void bn_reduce_kernel(int mode, const float* __restrict__ x, const fl
         a = *reinterpret_cast<const float4*>(p0 + 4 * q);  // mean | beta
         b = *reinterpret_cast<const float4*>(p1 + 4 * q);  // invstd | 1/gamma
       }
-      if (mode >= 3) {
+      if (mode == 3 || mode == 4 || mode == 6) {
         ga = *reinterpret_cast<const float4*>(p2 + 4 * q);
         be = *reinterpret_cast<const float4*>(p3 + 4 * q);
       }
-      auto acc = [&](const float4& v, float4 g) {
-        if (mode >= 3) {  // the ReLU's gradient gate, recomputed with the forward's formula
+      auto acc = [&](const float4& v, float4 g, const float4& e) {
+        if (mode == 5) {  // gate from the fused op's output z = e
+          g.x = e.x > 0.f ? g.x : 0.f;
+          g.y = e.y > 0.f ? g.y : 0.f;
+          g.z = e.z > 0.f ? g.z : 0.f;
+          g.w = e.w > 0.f ? g.w : 0.f;
+        } else if (mode == 6) {  // gate recomputed from x and the skip input e (forward's formula)
+          g.x = ((v.x - a.x) * b.x * ga.x + be.x + e.x > 0.f) ? g.x : 0.f;
+          g.y = ((v.y - a.y) * b.y * ga.y + be.y + e.y > 0.f) ? g.y : 0.f;
+          g.z = ((v.z - a.z) * b.z * ga.z + be.z + e.z > 0.f) ? g.z : 0.f;
+          g.w = ((v.w - a.w) * b.w * ga.w + be.w + e.w > 0.f) ? g.w : 0.f;
+        } else if (mode >= 3) {  // the ReLU's gradient gate, recomputed with the forward's formula
           const bool six = mode == 4;
           auto gate = [six](float u) { return six ? (u > 0.f && u < 6.f) : u > 0.f; };
           g.x = gate((v.x - a.x) * b.x * ga.x + be.x) ? g.x : 0.f;
@@ -299,19 +311,21 @@ __global__ void bn_reduce_kernel(int mode, const float* __restrict__ x, const fl
       long long r = r_begin + rsub;
       // four rows in flight per thread (same accumulation order as one at a time)
       for (; r + 3 * L.rpi < r_end; r += 4 * L.rpi) {
-        float4 v[4], g[4];
+        float4 v[4], g[4], e[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const long long off = (r + u * L.rpi) * C + 4 * q;
           v[u] = *reinterpret_cast<const float4*>(x + off);
           g[u] = mode == 0 ? z4 : *reinterpret_cast<const float4*>(dy + off);
+          e[u] = mode >= 5 ? *reinterpret_cast<const float4*>(p4 + off) : z4;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) acc(v[u], g[u]);
+        for (int u = 0; u < 4; ++u) acc(v[u], g[u], e[u]);
       }
       for (; r < r_end; r += L.rpi) {
         const long long off = r * C + 4 * q;
-        acc(*reinterpret_cast<const float4*>(x + off), mode == 0 ? z4 : *reinterpret_cast<const float4*>(dy + off));
+        acc(*reinterpret_cast<const float4*>(x + off), mode == 0 ? z4 : *reinterpret_cast<const float4*>(dy + off),
+            mode >= 5 ? *reinterpret_cast<const float4*>(p4 + off) : z4);
       }
     }
     // combine the rpi row-subgroups of each channel quad in shared memory
@@ -475,6 +489,82 @@ __global__ void bnrelu_apply_kernel(const float* __restrict__ x, float* z, const
     v.z = relu_val<kSix>((v.z - m.z) * s.z * g.z + b.z);
     v.w = relu_val<kSix>((v.w - m.w) * s.w * g.w + b.w);
     *reinterpret_cast<float4*>(z + 4 * i) = v;
+  }
+}
+
+// Fused BN + residual add + ReLU (the last BN of a bottleneck block feeding the join):
+// z = max(BN(x) + skip, 0); the BN output never exists.
+__global__ void bnaddrelu_apply_kernel(const float* __restrict__ x, const float* __restrict__ skip, float* z,
+                                       const float* __restrict__ mean, const float* __restrict__ invstd,
+                                       const float* __restrict__ gamma, const float* __restrict__ beta, long long rows,
+                                       int C) {
+  const int cq = C / 4;
+  const long long n4 = rows * cq;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int q = (int)(i % cq);
+    float4 v = *reinterpret_cast<const float4*>(x + 4 * i);
+    const float4 k = *reinterpret_cast<const float4*>(skip + 4 * i);
+    const float4 m = *reinterpret_cast<const float4*>(mean + 4 * q);
+    const float4 s = *reinterpret_cast<const float4*>(invstd + 4 * q);
+    const float4 g = *reinterpret_cast<const float4*>(gamma + 4 * q);
+    const float4 b = *reinterpret_cast<const float4*>(beta + 4 * q);
+    v.x = fmaxf((v.x - m.x) * s.x * g.x + b.x + k.x, 0.f);
+    v.y = fmaxf((v.y - m.y) * s.y * g.y + b.y + k.y, 0.f);
+    v.z = fmaxf((v.z - m.z) * s.z * g.z + b.z + k.z, 0.f);
+    v.w = fmaxf((v.w - m.w) * s.w * g.w + b.w + k.w, 0.f);
+    *reinterpret_cast<float4*>(z + 4 * i) = v;
+  }
+}
+
+// its backward apply: g = dz * gate (gate_from_out: [e > 0] with e = z; else [BN(x) + e > 0] with
+// e = skip); dx = k*g + cb*x + cc and dskip = g, each written or accumulated
+__global__ void bnaddrelu_bwd_apply_kernel(const float* __restrict__ x, const float* __restrict__ e,
+                                           int gate_from_out, const float* __restrict__ dz, float* dx, int acc_x,
+                                           float* dskip, int acc_skip, const float* __restrict__ mean,
+                                           const float* __restrict__ beta, const float* __restrict__ gamma,
+                                           const float* __restrict__ invstd, const float* __restrict__ coef_b,
+                                           const float* __restrict__ coef_c, long long rows, int C) {
+  const int cq = C / 4;
+  const long long n4 = rows * cq;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int q = (int)(i % cq);
+    const float4 v = *reinterpret_cast<const float4*>(x + 4 * i);
+    const float4 ev = *reinterpret_cast<const float4*>(e + 4 * i);
+    float4 g = *reinterpret_cast<const float4*>(dz + 4 * i);
+    const float4 m = *reinterpret_cast<const float4*>(mean + 4 * q);
+    const float4 be = *reinterpret_cast<const float4*>(beta + 4 * q);
+    const float4 ga = *reinterpret_cast<const float4*>(gamma + 4 * q);
+    const float4 is = *reinterpret_cast<const float4*>(invstd + 4 * q);
+    const float4 cb = *reinterpret_cast<const float4*>(coef_b + 4 * q);
+    const float4 cc = *reinterpret_cast<const float4*>(coef_c + 4 * q);
+    if (gate_from_out) {
+      g.x = ev.x > 0.f ? g.x : 0.f;
+      g.y = ev.y > 0.f ? g.y : 0.f;
+      g.z = ev.z > 0.f ? g.z : 0.f;
+      g.w = ev.w > 0.f ? g.w : 0.f;
+    } else {
+      g.x = ((v.x - m.x) * is.x * ga.x + be.x + ev.x > 0.f) ? g.x : 0.f;
+      g.y = ((v.y - m.y) * is.y * ga.y + be.y + ev.y > 0.f) ? g.y : 0.f;
+      g.z = ((v.z - m.z) * is.z * ga.z + be.z + ev.z > 0.f) ? g.z : 0.f;
+      g.w = ((v.w - m.w) * is.w * ga.w + be.w + ev.w > 0.f) ? g.w : 0.f;
+    }
+    float4 o;
+    o.x = fmaf(ga.x * is.x, g.x, fmaf(cb.x, v.x, cc.x));
+    o.y = fmaf(ga.y * is.y, g.y, fmaf(cb.y, v.y, cc.y));
+    o.z = fmaf(ga.z * is.z, g.z, fmaf(cb.z, v.z, cc.z));
+    o.w = fmaf(ga.w * is.w, g.w, fmaf(cb.w, v.w, cc.w));
+    if (acc_x) {
+      const float4 d = *reinterpret_cast<const float4*>(dx + 4 * i);
+      o.x += d.x; o.y += d.y; o.z += d.z; o.w += d.w;
+    }
+    *reinterpret_cast<float4*>(dx + 4 * i) = o;
+    if (acc_skip) {
+      const float4 d = *reinterpret_cast<const float4*>(dskip + 4 * i);
+      g.x += d.x; g.y += d.y; g.z += d.z; g.w += d.w;
+    }
+    *reinterpret_cast<float4*>(dskip + 4 * i) = g;
   }
 }
 

@@ -137,7 +137,7 @@ class Runtime:
         self.bn = {}
         pos = 0
         for op in self.net.ops:
-            if op.kind not in ("bn", "bnrelu", "bnrelu6"):
+            if op.kind not in ("bn", "bnrelu", "bnrelu6", "bnaddrelu"):
                 continue
             c = op.shape[-1]
             views = [stats[pos + j * c: pos + (j + 1) * c] for j in range(4)]
@@ -328,6 +328,19 @@ class Runtime:
                 out.append(("k", lib.monet_add_fwd, (xs[0], xs[1], y, op.numel, None)))
             elif op.kind == "addrelu":
                 out.append(("k", lib.monet_addrelu_fwd, (xs[0], xs[1], y, op.numel, None)))
+            elif op.kind == "bnaddrelu":
+                c = op.shape[-1]
+                rows = op.numel // c
+                sm, si, rm, rv = (t.data_ptr() for t in self.bn[op.id])
+                gma = self.pview[(op.id, "weight")].data_ptr()
+                bta = self.pview[(op.id, "bias")].data_ptr()
+                xp, kp = P(("in", op.attrs["x"])), P(("in", op.attrs["skip"]))
+                if s.kind == "forward":
+                    out.append(("k", lib.monet_bnaddrelu_fwd_train,
+                                (xp, kp, y, gma, bta, sm, si, rm, rv, rows, c, C.c_float(op.attrs["eps"]),
+                                 C.c_float(op.attrs["momentum"]), 1, self.scratch_ptr, None)))
+                else:
+                    out.append(("k", lib.monet_bnaddrelu_fwd_replay, (xp, kp, y, gma, bta, sm, si, rows, c, None)))
             elif op.kind == "maxpool":
                 d = net.pool_desc(op)
                 mid = net.intermediate_of[op.id]
@@ -461,6 +474,18 @@ class Runtime:
         elif op.kind == "add":
             for j in op.deps:
                 out.append(("k", lib.monet_grad_pass, (dy, P(("g", j)), op.numel, C.c_float(1.0), acc(j), None)))
+        elif op.kind == "bnaddrelu":
+            c = op.shape[-1]
+            rows = op.numel // c
+            jx, jk = op.attrs["x"], op.attrs["skip"]
+            sm, si, _, _ = (t.data_ptr() for t in self.bn[op.id])
+            from_out = s.impl == "bwd-out"
+            gate = P(("in", op.id)) if from_out else P(("in", jk))
+            out.append(("k", lib.monet_bnaddrelu_bwd,
+                        (P(("in", jx)), gate, 1 if from_out else 0, dy, P(("g", jx)), acc(jx), P(("g", jk)), acc(jk),
+                         self.pview[(op.id, "weight")].data_ptr(), self.pview[(op.id, "bias")].data_ptr(), sm, si,
+                         self.gview[(op.id, "weight")].data_ptr(), self.gview[(op.id, "bias")].data_ptr(), rows, c,
+                         self.scratch_ptr, None)))
         elif op.kind == "addrelu":
             j0, j1 = op.deps
             if s.impl == "bwd-out":

@@ -180,6 +180,22 @@ def _local_calls(bx: _Bench, net, op):
             scratch.data_ptr(), sp))
         out[("bwd", "bwd-in")] = lambda: bx.check(bwd_fn(
             x.data_ptr(), dy.data_ptr(), dx.data_ptr(), 0, g_, b_, m_, s_, dg, db, rows, c, scratch.data_ptr(), sp))
+    elif kind == "bnaddrelu":
+        c = op.shape[-1]
+        rows = n // c
+        ch = [bx.buf(4 * c) for _ in range(8)]
+        for t in ch[:4]:
+            t.abs_().add_(0.5)
+        scratch = bx.buf(lib.monet_bn_scratch_bytes(rows, c))
+        g_, b_, m_, s_, rm, rv, dg, db = (t.data_ptr() for t in ch)
+        xx, kk, dk = bx.buf(op.nbytes), bx.buf(op.nbytes), bx.buf(op.nbytes)
+        out[("fwd", "bnaddrelu")] = lambda: bx.check(lib.monet_bnaddrelu_fwd_train(
+            xx.data_ptr(), kk.data_ptr(), y.data_ptr(), g_, b_, m_, s_, rm, rv, rows, c, C.c_float(1e-5),
+            C.c_float(0.1), 1, scratch.data_ptr(), sp))
+        for name, src, from_out in (("bwd-out", y, 1), ("bwd-in", kk, 0)):
+            out[("bwd", name)] = (lambda src=src, from_out=from_out: bx.check(lib.monet_bnaddrelu_bwd(
+                xx.data_ptr(), src.data_ptr(), from_out, dy.data_ptr(), dx.data_ptr(), 0, dk.data_ptr(), 0, g_, b_,
+                m_, s_, dg, db, rows, c, scratch.data_ptr(), sp)))
     elif kind == "add":
         x2 = bx.buf(op.nbytes)
         out[("fwd", "add")] = lambda: bx.check(lib.monet_add_fwd(x.data_ptr(), x2.data_ptr(), y.data_ptr(), n, sp))

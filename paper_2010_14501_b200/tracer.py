@@ -74,7 +74,7 @@ class Network:
 
     def __init__(self, ops: list[Op], batch: int, num_classes: int):
         self.ops = ops
-        self.fused = any(op.kind in ("bnrelu", "bnrelu6") for op in ops)
+        self.fused = any(op.kind in ("bnrelu", "bnrelu6", "bnaddrelu") for op in ops)
         self.pair_variants = False  # offer the cta_group::2 conv variant in the catalog
         self.batch = batch
         self.num_classes = num_classes
@@ -105,7 +105,7 @@ class Network:
                 kind = "relu-join"
             elif kind in ("bnrelu", "bnrelu6"):   # a fused op's output is a ReLU output
                 kind = "relu"
-            elif kind == "addrelu":  # ... at a residual join
+            elif kind in ("addrelu", "bnaddrelu"):  # ... at a residual join
                 kind = "relu-join"
             elif kind == "relu6":
                 kind = "relu"
@@ -126,13 +126,14 @@ class Network:
         return sum(t.numel() for _, _, t in self.param_items())
 
     def bn_channels(self) -> int:
-        return sum(op.shape[-1] for op in self.ops if op.kind in ("bn", "bnrelu", "bnrelu6"))
+        return sum(op.shape[-1] for op in self.ops if op.kind in ("bn", "bnrelu", "bnrelu6", "bnaddrelu"))
 
     def scratch_bytes(self) -> int:
         lib = _native.lib()
         s = 0
         for op in self.ops:
-            if op.kind in ("bn", "bnrelu", "bnrelu6") or (op.kind in ("conv", "convT") and "bias" in op.params):
+            if op.kind in ("bn", "bnrelu", "bnrelu6", "bnaddrelu") or (op.kind in ("conv", "convT") and
+                                                                       "bias" in op.params):
                 rows = op.numel // op.shape[-1]  # conv bias gradient: per-channel sum of dy
                 s = max(s, lib.bn_scratch_bytes(rows, op.shape[-1]))
         s = max(s, lib.xent_scratch_bytes(self.label_count()))
@@ -166,8 +167,9 @@ class Network:
         nodes, backward, inters = [], [], []
         for op in self.ops:
             nodes.append({"id": op.id, "output_bytes": op.nbytes, "deps": list(op.deps)})
-            impls = [{"name": n, "deps_kind": k, "extra_deps": []} for n, k in BWD_IMPLS[op.kind]
-                     if n != "pair" or self.pair_variants]
+            impls = [{"name": n, "deps_kind": k,
+                      "extra_deps": [op.attrs["x"]] if op.kind == "bnaddrelu" and n == "bwd-out" else []}
+                     for n, k in BWD_IMPLS[op.kind] if n != "pair" or self.pair_variants]
             backward.append({"node": op.id, "grad_bytes": self.grad_bytes(op), "impls": impls})
             if op.id in self.intermediate_of:
                 u = self.intermediate_of[op.id]
@@ -232,6 +234,9 @@ class Network:
         elif op.kind in ("bnrelu", "bnrelu6"):  # fused BN+ReLU(6): backward from the BN input only (K10)
             fwd.append((op.kind, 0))
             bwd.append(("bwd-in", 0, x))
+        elif op.kind == "bnaddrelu":  # fused BN + join + ReLU: BN backward from x, gate from z or (x, skip)
+            fwd.append(("bnaddrelu", 0))
+            bwd += [("bwd-out", 0, sorted([op.attrs["x"], op.id])), ("bwd-in", 0, x)]
         elif op.kind == "addrelu":  # fused residual join + ReLU: gate from the output or the inputs
             fwd.append(("addrelu", 0))
             bwd += [("bwd-out", 0, [op.id]), ("bwd-in", 0, x)]
@@ -312,6 +317,7 @@ BWD_IMPLS = {
     "bn": [("bwd-in", "input"), ("bwd-out", "output")],
     "bnrelu": [("bwd-in", "input")],
     "bnrelu6": [("bwd-in", "input")],
+    "bnaddrelu": [("bwd-out", "output"), ("bwd-in", "input")],  # bwd-out also reads x (extra_deps)
     "addrelu": [("bwd-out", "output"), ("bwd-in", "input")],
     "relu": [("bwd-in", "input"), ("bwd-out", "output"), ("bwd-mask", "intermediate")],
     "maxpool": [("bwd-in", "input"), ("bwd-idx", "intermediate")],
@@ -367,6 +373,48 @@ def fuse_bn_relu(ops: list[Op]) -> list[Op]:
         if "inputs" in attrs:  # concat order
             attrs["inputs"] = [new_id[j] for j in attrs["inputs"]]
         out.append(Op(nid, kind, tuple(new_id[j] for j in op.deps), op.shape, attrs, op.params, name))
+    return out
+
+
+def fuse_bn_addrelu(ops: list[Op]) -> list[Op]:
+    """Merge a BN whose only reader is a fused add+ReLU into it: z = relu(BN(x) + skip)
+    ("bnaddrelu"; the residual block's last BN).  The BN output is never materialized;
+    the op reads x and skip.  Where both join inputs are such BNs (a downsample block),
+    the main-path one (lower id) is fused."""
+    readers: dict[int, list[int]] = {}
+    for op in ops:
+        for j in op.deps:
+            readers.setdefault(j, []).append(op.id)
+    absorbed: dict[int, int] = {}  # addrelu id -> bn id
+    for op in ops:
+        if op.kind != "addrelu":
+            continue
+        for j in sorted(op.deps):
+            b = ops[j - 1]
+            if b.kind == "bn" and readers.get(j) == [op.id] and j not in absorbed.values():
+                absorbed[op.id] = j
+                break
+    gone = set(absorbed.values())
+    new_id: dict[int, int] = {}
+    out: list[Op] = []
+    for op in ops:
+        if op.id in gone:
+            continue
+        nid = len(out) + 1
+        new_id[op.id] = nid
+        attrs = dict(op.attrs)
+        if "inputs" in attrs:
+            attrs["inputs"] = [new_id[j] for j in attrs["inputs"]]
+        if op.id in absorbed:
+            b = ops[absorbed[op.id] - 1]
+            x = b.deps[0]
+            skip = next(j for j in op.deps if j != b.id)
+            attrs = dict(b.attrs)
+            attrs["x"], attrs["skip"] = new_id[x], new_id[skip]
+            out.append(Op(nid, "bnaddrelu", tuple(sorted((new_id[x], new_id[skip]))), op.shape, attrs, b.params,
+                          b.name + "+add+relu"))
+        else:
+            out.append(Op(nid, op.kind, tuple(new_id[j] for j in op.deps), op.shape, attrs, op.params, op.name))
     return out
 
 
@@ -533,7 +581,7 @@ def trace_graph(model: torch.nn.Module, example_input: torch.Tensor, num_classes
     logits = ops[src - 1]
     k = num_classes or logits.shape[1]
     ops.append(Op(len(ops) + 1, "xent", (src,), (), name="loss"))
-    return Network(fuse_bn_relu(ops) if fuse else ops, n, k)
+    return Network(fuse_bn_addrelu(fuse_bn_relu(ops)) if fuse else ops, n, k)
 
 
 def parse_image(v):

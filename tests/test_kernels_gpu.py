@@ -504,3 +504,38 @@ def test_pixel_xent(cuda):
     dz = torch.empty(rows, k, device=cuda)
     lib.xent_bwd(zd.data_ptr(), ld.data_ptr(), one.data_ptr(), dz.data_ptr(), rows, k, 0, stream())
     assert rel_err(dz, zr.grad) < 1e-5
+
+
+@pytest.mark.parametrize("from_out", [1, 0])
+def test_fused_bn_add_relu(cuda, from_out):
+    """z = relu(BN(x) + skip) forward (train) and backward (gate from z or from x, skip):
+    dx, dskip (accumulated), dgamma, dbeta against float64 autograd."""
+    rows, c = 4 * 9 * 11, 64
+    g = torch.Generator().manual_seed(11)
+    x = torch.randn(rows, c, generator=g)
+    k = torch.randn(rows, c, generator=g)
+    gam, bet = torch.rand(c, generator=g) + 0.5, torch.randn(c, generator=g) * 0.1
+    lib = N.lib()
+    xd, kd, gd, bd = x.to(cuda), k.to(cuda), gam.to(cuda), bet.to(cuda)
+    z = torch.empty(rows, c, device=cuda)
+    sm, si, rm, rv, dg, db = (torch.zeros(c, device=cuda) for _ in range(6))
+    rv += 1
+    scratch = torch.empty(lib.bn_scratch_bytes(rows, c) // 4 + 1, device=cuda)
+    lib.bnaddrelu_fwd_train(xd.data_ptr(), kd.data_ptr(), z.data_ptr(), gd.data_ptr(), bd.data_ptr(), sm.data_ptr(),
+                            si.data_ptr(), rm.data_ptr(), rv.data_ptr(), rows, c, 1e-5, 0.1, 1, scratch.data_ptr(),
+                            stream())
+    xr, kr = x.double().requires_grad_(), k.double().requires_grad_()
+    gr, br = gam.double().requires_grad_(), bet.double().requires_grad_()
+    zr = torch.relu(F.batch_norm(xr, None, None, gr, br, training=True, eps=1e-5) + kr)
+    assert rel_err(z, zr.detach()) < 1e-5
+    dz = torch.randn(rows, c, generator=g)
+    zr.backward(dz.double())
+    dx = torch.ones(rows, c, device=cuda)
+    dk = torch.full((rows, c), 2.0, device=cuda)
+    gate = z if from_out else kd
+    lib.bnaddrelu_bwd(xd.data_ptr(), gate.data_ptr(), from_out, dz.to(cuda).data_ptr(), dx.data_ptr(), 1, dk.data_ptr(),
+                      1, gd.data_ptr(), bd.data_ptr(), sm.data_ptr(), si.data_ptr(), dg.data_ptr(), db.data_ptr(), rows,
+                      c, scratch.data_ptr(), stream())
+    assert rel_err(dx, 1 + xr.grad) < 1e-4
+    assert rel_err(dk, 2 + kr.grad) < 1e-5
+    assert rel_err(dg, gr.grad) < 1e-4 and rel_err(db, br.grad) < 1e-5

@@ -81,14 +81,14 @@ def test_oracle_replay_equals_autograd(arch, fuse):
         got = params_nhwc(st)
         for op in net.ops:
             for pname in op.params:
-                want = ref[f"{op.name.removesuffix('+relu')}.{pname}"]
+                want = ref[f"{op.name.split('+')[0]}.{pname}"]
                 have = got[(op.id, pname)]
                 if op.kind == "conv":
                     have = have[..., : want.shape[1]].permute(0, 3, 1, 2)
                 assert _rel(have, want) < TOL, (name, op.name, pname)
-            if op.kind in ("bn", "bnrelu"):
+            if op.kind in ("bn", "bnrelu", "bnaddrelu"):
                 rm, rv = st.running[op.id]
-                base = op.name.removesuffix("+relu")
+                base = op.name.split('+')[0]
                 assert _rel(rm, ref_bn[f"{base}.running_mean"]) < TOL
                 assert _rel(rv, ref_bn[f"{base}.running_var"]) < TOL
 
@@ -102,15 +102,22 @@ def test_fusion_pass():
         return op.kind in ("bn", "add") and len(readers) == 1 and readers[0].kind == "relu"
     n_bn = sum(1 for op in plain.ops if op.kind == "bn" and fusable(op))
     n_add = sum(1 for op in plain.ops if op.kind == "add" and fusable(op))
+    # every add+ReLU join then absorbs one BN input whose only reader it is (the block's last BN)
+    n_join_bn = sum(op.kind == "bnaddrelu" for op in net.ops)
     assert sum(op.kind == "bnrelu" for op in net.ops) == n_bn > 0
-    assert sum(op.kind == "addrelu" for op in net.ops) == n_add > 0
-    assert net.n == plain.n - n_bn - n_add
+    assert sum(op.kind in ("addrelu", "bnaddrelu") for op in net.ops) == n_add > 0
+    assert n_join_bn == n_add  # ResNet: every join has such a BN
+    assert net.n == plain.n - n_bn - n_add - n_join_bn
     for op in net.ops:
         if op.kind == "bnrelu":  # backward reads the BN input only
             (v,) = cat.bwd(op.id)
             assert v.name == "bwd-in" and set(v.deps) == set(op.deps)
         elif op.kind == "addrelu":  # gate from the output or from both inputs
             assert {v.name: set(v.deps) for v in cat.bwd(op.id)} == {"bwd-out": {op.id}, "bwd-in": set(op.deps)}
+        elif op.kind == "bnaddrelu":  # BN backward from x; gate from z, or from x and the skip
+            assert {v.name: set(v.deps) for v in cat.bwd(op.id)} == {"bwd-out": {op.attrs["x"], op.id},
+                                                                      "bwd-in": set(op.deps)}
+            assert net.op(op.attrs["skip"]).kind in ("bnrelu", "addrelu", "bnaddrelu", "bn", "maxpool")
     assert g.params_bytes == plain.params_bytes()
 
 
@@ -281,7 +288,7 @@ def test_oracle_googlenet_equals_autograd(fuse):
         got = params_nhwc(st)
         for op in net.ops:
             for pname in op.params:
-                want = ref[f"{op.name.removesuffix('+relu')}.{pname}"]
+                want = ref[f"{op.name.split('+')[0]}.{pname}"]
                 have = _torch_layout(net, op, pname, got[(op.id, pname)], want)
                 err = (have.double() - want.double()).abs().max().item()
                 assert err <= TOL * max(want.double().abs().max().item(), 1e-3), (name, op.name, pname)
