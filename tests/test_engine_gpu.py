@@ -290,3 +290,31 @@ def test_unet_engine(cuda):
         got = rt.pview[(nid, pname)].view(v.shape)
         assert (got.cpu().double() - v.double()).abs().max().item() <= REL * max(v.abs().max().item(), 0.05), \
             (net.op(nid).name, pname)
+
+
+def test_cli_train_execute_exit_codes(cuda, tmp_path):
+    """`train` / `execute` on the GPU with the reference's exit codes: 0 ok, 5 invalid schedule,
+    6 planned footprint over the budget."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    common = ["--arch", "resnet18", "--batch", "4", "--image", "32", "--classes", "10", "--fuse"]
+
+    def run(*args):
+        return subprocess.run([sys.executable, "-m", "paper_2010_14501_b200", *args], cwd=root, capture_output=True,
+                              text=True, timeout=900)
+
+    r = run("train", *common, "--budget-gib", "1", "--steps", "2", "-o", str(tmp_path / "t.json"))
+    assert r.returncode == 0, r.stderr
+    out = json.loads((tmp_path / "t.json").read_text())
+    assert len(out["losses"]) == 2 and out["physical_peak_bytes"] <= out["ilp_bound_bytes"] <= 1 << 30
+    assert run("plan", *common, "--budget-gib", "1", "-o", str(tmp_path / "s.json")).returncode == 0
+    assert run("execute", *common, "--schedule", str(tmp_path / "s.json"), "--budget-gib", "1").returncode == 0
+    doc = json.loads((tmp_path / "s.json").read_text())
+    doc["schedule"]["stages"][2]["store"] = []  # drop what the remaining backward stages read
+    (tmp_path / "bad.json").write_text(json.dumps(doc))
+    assert run("execute", *common, "--schedule", str(tmp_path / "bad.json")).returncode == 5
+    assert run("execute", *common, "--schedule", str(tmp_path / "s.json"), "--budget-gib", "0.01").returncode == 6
