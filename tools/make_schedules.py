@@ -26,7 +26,7 @@ def digest(doc):
     return hashlib.sha256(json.dumps(doc, sort_keys=True).encode()).hexdigest()[:16]
 
 
-def main(jobs, exact_time_s=None):
+def main(jobs, exact_time_s=None, exchange=False):
     OUT.mkdir(exist_ok=True)
     for arch, batch, img, gib, fuse in jobs:
         net = build_network(arch, batch, parse_image(img), num_classes=default_classes(arch), fuse=fuse)
@@ -42,7 +42,8 @@ def main(jobs, exact_time_s=None):
         cat = M.load_catalog(cdoc, g)
         budget = int(gib * (1 << 30))
         t = time.time()
-        sched, info = plan_schedule(g, cat, budget, kinds=net.storable_kinds(), exact_time_s=exact_time_s)
+        sched, info = plan_schedule(g, cat, budget, kinds=net.storable_kinds(), exact_time_s=exact_time_s,
+                                    exchange=exchange)
         dt = time.time() - t
         if sched is None:
             print(arch, batch, img, gib, "no feasible schedule", info)
@@ -66,5 +67,6 @@ if __name__ == "__main__":
     ap.add_argument("--budgets", default="10,8,6", help="GiB, comma separated")
     ap.add_argument("--exact", type=float, default=None,
                     help="seconds of exact ILP search on graphs of <= planner.EXACT_MAX_NODES nodes")
+    ap.add_argument("--exchange", action="store_true", help="also try exchange moves (slower)")
     a = ap.parse_args()
-    main([(a.arch, a.batch, a.image, float(b), a.fused) for b in a.budgets.split(",")], a.exact)
+    main([(a.arch, a.batch, a.image, float(b), a.fused) for b in a.budgets.split(",")], a.exact, a.exchange)
