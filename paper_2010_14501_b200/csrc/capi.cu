@@ -1071,6 +1071,18 @@ int monet_maxpool_bwd(const monet_conv_desc* d, const uint8_t* idx8, const float
                       int accumulate, void* stream) {
   if (d->c % 4) return -(int)cudaErrorInvalidValue;
   long long total = (long long)d->n * d->h * d->w * (d->c / 4);
+  const bool sq = idx8 && d->r == d->s && d->stride_h == d->stride_w && d->pad_h == d->pad_w &&
+                  total < (1LL << 31) && ((long long)d->n * d->p * d->q * d->c) < (1LL << 40);
+  if (sq && d->r == 2 && d->stride_h == 2) {
+    maxpool_bwd_idx_kernel<2, 2><<<ew_blocks(total), kEwThreads, 0, S(stream)>>>(
+        idx8, dy, dx, d->h, d->w, d->c, d->p, d->q, d->pad_h, (unsigned)total, accumulate);
+    return last_error();
+  }
+  if (sq && d->r == 3 && d->stride_h == 2) {
+    maxpool_bwd_idx_kernel<3, 2><<<ew_blocks(total), kEwThreads, 0, S(stream)>>>(
+        idx8, dy, dx, d->h, d->w, d->c, d->p, d->q, d->pad_h, (unsigned)total, accumulate);
+    return last_error();
+  }
   maxpool_bwd_kernel<<<ew_blocks(total), kEwThreads, 0, S(stream)>>>(idx8, x, dy, dx, d->n, d->h, d->w, d->c, d->p,
                                                                      d->q, d->r, d->s, d->stride_h, d->stride_w,
                                                                      d->pad_h, d->pad_w, accumulate);

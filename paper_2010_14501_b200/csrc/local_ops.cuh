@@ -729,6 +729,55 @@ __global__ void maxpool_bwd_kernel(const uint8_t* __restrict__ idx, const float*
   }
 }
 
+// Index-path backward specialised for square K x K windows at stride ST (VGG's 2x2/2,
+// ResNet's 3x3/2): at most ceil(K/ST)^2 candidate windows per input pixel, fully unrolled,
+// 32-bit index math (total < 2^31 checked on the host).
+template <int K, int ST>
+__global__ void maxpool_bwd_idx_kernel(const uint8_t* __restrict__ idx, const float* __restrict__ dy, float* dx,
+                                       int H, int W, int C, int P, int Q, int pad, unsigned total, int accumulate) {
+  constexpr int kWin = (K + ST - 1) / ST;
+  const unsigned cq = C / 4;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const unsigned c4 = i % cq, pix = i / cq;
+    const int w = (int)(pix % W);
+    const unsigned t = pix / W;
+    const int h = (int)(t % H), n = (int)(t / H);
+    // windows p with p*ST - pad <= h <= p*ST - pad + K - 1
+    const int hp = h + pad, wp = w + pad;
+    const int p_hi = hp / ST, q_hi = wp / ST;
+    float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int di = 0; di < kWin; ++di) {
+      const int p = p_hi - di;
+      const int r = hp - p * ST;
+      if (p < 0 || p >= P || r >= K) continue;
+#pragma unroll
+      for (int dj = 0; dj < kWin; ++dj) {
+        const int q = q_hi - dj;
+        const int s = wp - q * ST;
+        if (q < 0 || q >= Q || s >= K) continue;
+        const size_t o = (((size_t)n * P + p) * Q + q) * C + 4 * c4;
+        const uint32_t packed = __ldg(reinterpret_cast<const uint32_t*>(idx + o));
+        const float4 d = __ldg(reinterpret_cast<const float4*>(dy + o));
+        const uint32_t me = (uint32_t)(r * K + s);
+        if ((packed & 0xFF) == me) g.x += d.x;
+        if (((packed >> 8) & 0xFF) == me) g.y += d.y;
+        if (((packed >> 16) & 0xFF) == me) g.z += d.z;
+        if ((packed >> 24) == me) g.w += d.w;
+      }
+    }
+    float4* out = reinterpret_cast<float4*>(dx + (size_t)pix * C + 4 * c4);
+    if (accumulate) {
+      const float4 o4 = *out;
+      g.x += o4.x;
+      g.y += o4.y;
+      g.z += o4.z;
+      g.w += o4.w;
+    }
+    *out = g;
+  }
+}
+
 // global average pool: y[n, c] = mean_{hw} x[n, hw, c]
 __global__ void avgpool_fwd_kernel(const float* __restrict__ x, float* __restrict__ y, int N, int HW, int C) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;

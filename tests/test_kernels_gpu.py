@@ -539,3 +539,25 @@ def test_fused_bn_add_relu(cuda, from_out):
     assert rel_err(dx, 1 + xr.grad) < 1e-4
     assert rel_err(dk, 2 + kr.grad) < 1e-5
     assert rel_err(dg, gr.grad) < 1e-4 and rel_err(db, br.grad) < 1e-5
+
+
+@pytest.mark.parametrize("k,st,pad", [(2, 2, 0), (3, 2, 1), (3, 2, 0), (3, 1, 1), (2, 1, 0)])
+def test_maxpool_bwd_index_paths(cuda, k, st, pad):
+    """Backward from the 8-bit index: the specialised 2x2/2 and 3x3/2 kernels and the generic one
+    (stride 1), with accumulation, against float64 autograd."""
+    n, h, w, c = 2, 11, 14, 32
+    g = torch.Generator().manual_seed(12)
+    x = torch.randn(n, h, w, c, generator=g)
+    d = N.conv_desc(n, h, w, c, c, k, k, st, pad)
+    lib = N.lib()
+    xd = x.to(cuda)
+    y = torch.empty(n, d.p, d.q, c, device=cuda)
+    idx = torch.empty(n, d.p, d.q, c, dtype=torch.uint8, device=cuda)
+    lib.maxpool_fwd(d, xd.data_ptr(), y.data_ptr(), idx.data_ptr(), stream())
+    xr = x.double().permute(0, 3, 1, 2).requires_grad_()
+    yr = F.max_pool2d(xr, k, st, pad)
+    dy = torch.randn(n, d.p, d.q, c, generator=g)
+    yr.backward(dy.double().permute(0, 3, 1, 2))
+    dx = torch.ones(n, h, w, c, device=cuda)
+    lib.maxpool_bwd(d, idx.data_ptr(), None, dy.to(cuda).data_ptr(), dx.data_ptr(), 1, stream())
+    assert rel_err(dx, 1 + xr.grad.permute(0, 2, 3, 1)) < REL_EW
