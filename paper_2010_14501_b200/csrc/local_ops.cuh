@@ -309,6 +309,15 @@ __global__ void bn_reduce_kernel(int mode, const float* __restrict__ x, const fl
       };
       const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
       long long r = r_begin + rsub;
+      if (mode == 0) {  // statistics read one tensor: eight rows in flight to cover the latency
+        for (; r + 7 * L.rpi < r_end; r += 8 * L.rpi) {
+          float4 v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = *reinterpret_cast<const float4*>(x + (r + u * L.rpi) * C + 4 * q);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc(v[u], z4, z4);
+        }
+      }
       // four rows in flight per thread (same accumulation order as one at a time)
       for (; r + 3 * L.rpi < r_end; r += 4 * L.rpi) {
         float4 v[4], g[4], e[4];
