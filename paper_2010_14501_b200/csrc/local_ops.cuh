@@ -317,6 +317,18 @@ __global__ void bn_reduce_kernel(int mode, const float* __restrict__ x, const fl
 #pragma unroll
           for (int u = 0; u < 8; ++u) acc(v[u], z4, z4);
         }
+      } else if (mode < 5) {  // two tensors (x, dy): eight rows in flight as well
+        for (; r + 7 * L.rpi < r_end; r += 8 * L.rpi) {
+          float4 v[8], g[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const long long off = (r + u * L.rpi) * C + 4 * q;
+            v[u] = *reinterpret_cast<const float4*>(x + off);
+            g[u] = *reinterpret_cast<const float4*>(dy + off);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc(v[u], g[u], z4);
+        }
       }
       // four rows in flight per thread (same accumulation order as one at a time)
       for (; r + 3 * L.rpi < r_end; r += 4 * L.rpi) {
