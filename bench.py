@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -218,63 +219,132 @@ def kernel_roofline(rt, plan, net, peaks):
     return roof, local, total_t
 
 
-def cpu_baseline_run(args, budget_frac, steps=2):
-    """The CPU oracle replaying a schedule of the same kind on a bounded sample."""
+def _spec_and_schedule(args):
+    """The frozen network (oracle/specs) and the committed schedule of this workload:
+    plain JSON, so the CPU arms never import the product package or map its .so."""
+    from oracle import netspec
+
+    fused = args.fuse
+    spec = netspec.spec_path(args.arch, fused, args.batch, args.image)
+    sched = ROOT / "schedules" / f"{args.arch}{'_fused' if fused else ''}_b{args.batch}_{args.image}_{args.budget_gib:g}gib.json"
+    cat = ROOT / "profiles" / f"catalog_{args.arch}{'_fused' if fused else ''}_b{args.batch}_{args.image}.json"
+    missing = [str(p.relative_to(ROOT)) for p in (spec, sched, cat) if not p.exists()]
+    if missing:
+        raise FileNotFoundError(f"frozen inputs missing: {missing} (tools/freeze_netspec.py, tools/make_schedules.py)")
+    sdoc = json.loads(sched.read_text())
+    spec_doc = json.loads(spec.read_text())
+    if sdoc["graph_digest"] != spec_doc["graph_digest"]:
+        raise ValueError(f"{sched.name} was planned for another graph than {spec.name}")
+    return spec, sdoc, json.loads(cat.read_text())["catalog"], sched
+
+
+def cpu_baseline_run(args, steps=2, warmup=1):
+    """The CPU oracle port (oracle/cpu_executor.py) replaying the committed schedule on the
+    same workload (network, batch, budget) with all host threads; no product code."""
     import torch
 
-    import paper_2010_14501_b200 as M
+    from oracle import netspec
     from oracle.cpu_executor import CpuState, run_step
-    from paper_2010_14501_b200.planner import plan_schedule
-    from paper_2010_14501_b200.tracer import build_network
 
     torch.set_num_threads(os.cpu_count() or 1)
-    n = args.cpu_sample
-    net = build_network(args.arch, n, image_arg(args.image), num_classes=n_classes(args.arch))
-    g = M.load_graph(net.graph_doc())
-    cat = M.load_catalog(net.catalog_doc(), g)
-    se_peak = M.simulate(M.store_everything_schedule(g, cat), g, cat).peak_memory
-    budget = g.params_bytes + int(budget_frac * (se_peak - g.params_bytes))
-    sched, info = plan_schedule(g, cat, budget, kinds=net.storable_kinds())
-    if sched is None:
-        sched = M.store_everything_schedule(g, cat)
-    doc = M.schedule_to_doc(sched)
+    spec, sdoc, _, sched_path = _spec_and_schedule(args)
+    net = netspec.load(spec)
+    n = net.batch
     gen = torch.Generator().manual_seed(0)
-    hw = image_arg(args.image)
-    hw = hw if isinstance(hw, tuple) else (hw, hw)
+    hw = _hw(args.image)
     x = torch.randn(n, 3, *hw, generator=gen)
-    y = torch.randint(0, n_classes(args.arch), (net.label_count(),), generator=gen)
+    y = torch.randint(0, net.num_classes, (net.label_count(),), generator=gen)
     st = CpuState(net)
-    run_step(st, doc, x, y)  # warm-up
+    for _ in range(warmup):
+        run_step(st, sdoc["schedule"], x, y)
     t = time.perf_counter()
     for _ in range(steps):
-        run_step(st, doc, x, y)
+        loss = run_step(st, sdoc["schedule"], x, y)
     dt = (time.perf_counter() - t) / steps
     return {"value": round(n / dt, 3), "unit": "img/s", "cores": torch.get_num_threads(), "kind": "port",
-            "sample": f"{args.arch} batch {n} at {hw[0]}x{hw[1]}, one scheduled training step "
-                      f"(budget fraction {budget_frac:.3f} of its store-everything activations), "
-                      f"torch CPU fp32 oracle replay, mean of {steps} steps after 1 warm-up"}
+            "sample": f"{args.arch} batch {n} at {hw[0]}x{hw[1]}: one training step replaying the committed "
+                      f"{args.budget_gib:g} GiB schedule ({sched_path.relative_to(ROOT)}) with the torch-CPU fp32 "
+                      f"oracle port, mean of {steps} step(s) after {warmup} warm-up; synthetic seeded weights "
+                      f"(oracle/netspec.py)", "loss": round(float(loss), 4)}
+
+
+def reference_planner_run(args, node_limit=1):
+    """The reference's own CPU path for this workload, unmodified (remsched 0.1.0 from
+    baseline/_ref): load the graph/catalog/schedule documents, build the 0-1 ILP at the
+    budget (ilp.py:121), run its branch-and-bound with the committed schedule as the
+    incumbent and a node limit (solver.py:441, cli.py:129), decode, validate, simulate
+    (schedule.py:320) and compute the ILP bound (oracle.py:287).  Wall time per phase."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "remsched").exists():
+        return {"unavailable": "baseline/_ref/remsched not installed"}
+    sys.path.insert(0, str(ref))
+    import remsched as R
+
+    spec, sdoc, cat_doc, _ = _spec_and_schedule(args)
+    graph_doc = json.loads(spec.read_text())["graph"]
+    out = {"impl": f"remsched {getattr(R, '__version__', '0.1.0')} (baseline/_ref, unmodified)", "cores": 1}
+    t0 = time.perf_counter()
+    g = R.load_graph(graph_doc)
+    cat = R.load_catalog(cat_doc, g)
+    sched = R.schedule_from_doc(sdoc["schedule"])
+    sets = R.compute_dependency_sets(g)
+    t1 = time.perf_counter()
+    model = R.build_model(g, sets, cat, sdoc["budget_bytes"], {"inplace": True})
+    t2 = time.perf_counter()
+    res = R.solve(model, {"node_limit": node_limit, "incumbent": R.assignment_from_schedule(model, sched)})
+    t3 = time.perf_counter()
+    dec = R.decode(res, g, cat) if res.assignment is not None else sched
+    tags = R.validate(dec, g, sets, cat)
+    tr = R.simulate(dec, g, cat)
+    t4 = time.perf_counter()
+    ok, bound, _ = R.check_schedule(g, sets, cat, dec, sdoc["budget_bytes"])
+    t5 = time.perf_counter()
+    out.update({"load_s": round(t1 - t0, 3), "build_model_s": round(t2 - t1, 3), "solve_s": round(t3 - t2, 3),
+                "validate_simulate_s": round(t4 - t3, 3), "check_schedule_s": round(t5 - t4, 3),
+                "total_s": round(t5 - t0, 3), "node_limit": node_limit, "status": res.status,
+                "nodes": res.nodes, "objective": None if res.objective is None else str(res.objective),
+                "lower_bound": None if res.lower_bound is None else str(res.lower_bound),
+                "validate_tags": len(tags), "simulated_peak_bytes": tr.peak_memory, "ilp_bound_bytes": bound,
+                "within_budget": bool(ok)})
+    return out
+
+
+def _hw(image):
+    if "x" in str(image):
+        h, w = str(image).split("x")
+        return int(h), int(w)
+    return int(image), int(image)
 
 
 # --------------------------------------------------------------------------- arms
 
 def reference_arm(args):
+    """The reference-side CPU path on the same workload as ours_arm (no product code: the
+    network, catalog and schedule are the committed JSON files).  ``value``: the oracle
+    port replaying the committed schedule at the full batch on all host threads;
+    ``reference_planner``: the reference's own remsched path for the same instance."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import torch
-
-    base = 26.55 * (1 << 30)  # ResNet-50 b184 store-everything ledger peak (for the budget fraction)
-    frac = max(0.05, min(1.0, (args.budget_gib * (1 << 30)) / base))
-    steps = max(1, args.steps)
-    res = cpu_baseline_run(args, frac, steps=min(steps, 3))
+    steps = max(1, min(args.steps, 2))
+    res = cpu_baseline_run(args, steps=steps, warmup=1)
+    planner = reference_planner_run(args)
+    hw = _hw(args.image)
     out = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": "img/s", "n_gpus": args.gpus,
-           "steps": min(steps, 3), "warmup": 1, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-           "dtype": "f32", "data": "synthetic",
-           "config": {"workload": f"{args.arch} {args.image}x{args.image} scheduled training step under a "
-                                  f"{args.budget_gib:g} GiB-equivalent budget fraction, CPU sample batch "
-                                  f"{args.cpu_sample}", "parallelism": "host cores"},
-           "cpu_baseline": res, "e2e": {"value": res["value"], "unit": "img/s", "h2d_bytes_per_step": 0,
-                                        "d2h_bytes_per_step": 0}}
+           "steps": steps, "warmup": 1, "ms_per_step": round(1e3 * args.batch / res["value"], 1),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic N(0,1) images, uniform labels; seeded synthetic weights",
+           "config": {"workload": f"{args.arch} {hw[0]}x{hw[1]} batch {args.batch}/GPU, {args.budget_gib:g} GiB "
+                                  f"per-GPU budget, MONeT schedule (schedules/{args.arch}"
+                                  f"{'_fused' if args.fuse else ''}_b{args.batch}_{args.image}_{args.budget_gib:g}gib"
+                                  f".json)" + (", fused BN+ReLU operators" if args.fuse else ""),
+                      "model": args.arch, "global_batch": args.batch, "per_gpu_batch": args.batch,
+                      "image": args.image, "budget_bytes": int(args.budget_gib * (1 << 30)),
+                      "parallelism": "host cores"},
+           "cpu_baseline": res, "reference_planner": planner,
+           # this arm runs only oracle/ + the reference package: the product must not be loaded
+           "product_loaded": "paper_2010_14501_b200" in sys.modules,
+           "e2e": {"value": res["value"], "unit": "img/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
 
@@ -308,21 +378,30 @@ def ours_arm(args):
     from paper_2010_14501_b200.schedule import fastest_store_everything_schedule
     se = fastest_store_everything_schedule(g, cat)  # min-cost no-recompute
 
-    rt = Runtime(net, device=dev, budget_bytes=budget)
+    # SGD lr 0.1 (momentum 0.9) as in the paper's ResNet runs; VGG-16 has no BN and
+    # diverges at 0.1 from torchvision's init (loss NaN within a few steps), so it
+    # trains at torchvision's reference lr 0.01
+    lr = 0.01 if args.arch.startswith("vgg") else 0.1
+    rt = Runtime(net, device=dev, budget_bytes=budget, lr=lr)
     if world > 1:
         from paper_2010_14501_b200.dp import DataParallel
         DataParallel(rt)
     plan = rt.plan(sched, g, cat)
 
-    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     hw = image_arg(args.image)
     hw = hw if isinstance(hw, tuple) else (hw, hw)
-    x = torch.randn(args.batch, 3, *hw, device=dev, generator=gen)
-    y = torch.randint(0, n_classes(args.arch), (net.label_count(),), device=dev, generator=gen)
+
+    def batch():  # the synthetic batch (regenerated for the store-everything run, never kept)
+        gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+        x = torch.randn(args.batch, 3, *hw, device=dev, generator=gen)
+        y = torch.randint(0, n_classes(args.arch), (net.label_count(),), device=dev, generator=gen)
+        return x, y
+
+    x, y = batch()
     rt.set_batch(x, y)
-    x_keep = x if not args.no_overhead_run else None
-    del x
     torch.cuda.synchronize()
+    del x, y  # staged in the fixed region: nothing outside the runtime stays allocated
+    torch.cuda.empty_cache()
 
     graph = None
     use_graph = not args.no_graph and world == 1
@@ -339,6 +418,7 @@ def ours_arm(args):
         step()
     torch.cuda.synchronize()
     torch.cuda.reset_peak_memory_stats(dev)
+    free0, total0 = torch.cuda.mem_get_info(dev)
 
     sampler = ClockSampler(local)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -360,7 +440,17 @@ def ours_arm(args):
     ms = float(t.item())
     value = world * args.batch / (ms * 1e-3)
     loss = rt.loss_value()
-    torch_peak = torch.cuda.max_memory_allocated(dev)
+    mstats = torch.cuda.memory_stats(dev)
+    free1, _ = torch.cuda.mem_get_info(dev)
+    device_mem = {
+        # what the process asked the allocator for at its peak during the timed steps
+        "torch_peak_requested_bytes": mstats.get("requested_bytes.all.peak"),
+        "torch_peak_allocated_bytes": mstats.get("allocated_bytes.all.peak"),  # + 512-B allocator rounding
+        "torch_reserved_bytes": mstats.get("reserved_bytes.all.current"),
+        # CUDA context, NCCL buffers, cuBLAS/library workspaces: device memory in use that
+        # torch's allocator does not hold
+        "non_allocator_bytes": (total0 - min(free0, free1)) - mstats.get("reserved_bytes.all.current", 0),
+    }
 
     # ---- end to end: pinned host batch in, loss out, through Runtime.train_step
     c_pad = net.ops[0].shape[3]
@@ -400,7 +490,9 @@ def ours_arm(args):
         del graph
         rt_se = Runtime(net, device=dev)
         plan_se = rt_se.plan(se, g, cat)
-        rt_se.set_batch(x_keep, y)
+        xs, ys = batch()
+        rt_se.set_batch(xs, ys)
+        del xs, ys
         g_se = rt_se.capture(plan_se) if use_graph else None
         run_se = (lambda: g_se.replay()) if g_se is not None else (lambda: rt_se.run(plan_se))
         for _ in range(max(3, args.warmup)):
@@ -419,9 +511,8 @@ def ours_arm(args):
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline:
-            frac = (budget - g.params_bytes) / (M.simulate(se, g, cat).peak_memory - g.params_bytes)
             try:
-                cpu = cpu_baseline_run(args, frac)
+                cpu = cpu_baseline_run(args, steps=1, warmup=0)
             except Exception as exc:  # keep the GPU line even if the host run fails
                 cpu = {"value": None, "error": str(exc)[:200]}
         n_rec = sum(sum(1 for u, impl in s.recompute if impl is not None) for s in sched.stages)
@@ -440,8 +531,10 @@ def ours_arm(args):
             "memory": {"ledger_peak_bytes": plan.ledger_peak, "ilp_bound_bytes": plan.bound_peak,
                        "physical_peak_bytes": g.params_bytes + plan.arena_bytes,
                        "params_bytes": g.params_bytes, "arena_bytes": plan.arena_bytes,
-                       "torch_max_allocated_bytes": torch_peak,
+                       **device_mem,
                        "within_bound": g.params_bytes + plan.arena_bytes <= (plan.bound_peak or 0),
+                       "device_within_bound": (device_mem["torch_peak_requested_bytes"] or 1 << 62)
+                                              <= (plan.bound_peak or 0),
                        "store_everything_ledger_peak_bytes": M.simulate(se, g, cat).peak_memory},
             "overhead": {"modeled_pct": round(100 * overhead_model, 2), "recomputes": n_rec,
                          "measured_pct": None if se_ms is None else round(100 * (ms / se_ms - 1), 2),
@@ -457,7 +550,9 @@ def ours_arm(args):
             "gpu_launches": plan.launches * args.steps,
             "roofline": roof, "roofline_local_ops": local_roof,
             "cpu_baseline": cpu,
-            "clocks": sampler.summary(), "loss": loss,
+            "clocks": sampler.summary(), "loss": loss, "lr": lr,
+            # a diverged run is not a valid measurement of a training step
+            "loss_finite": math.isfinite(loss),
         }
         tr = ROOT / "profiles" / "traffic.json"
         if tr.exists():
@@ -465,8 +560,12 @@ def ours_arm(args):
         else:
             roof["traffic"] = None
         print(json.dumps(out), flush=True)
+        if not math.isfinite(loss):
+            print(f"bench: loss is {loss} after {args.warmup + args.steps + 2} steps -- invalid run", file=sys.stderr)
     if world > 1:
         dist.destroy_process_group()
+    if not math.isfinite(loss):
+        sys.exit(3)
 
 
 def main():

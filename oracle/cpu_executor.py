@@ -63,8 +63,19 @@ def _bn_apply(x, mean, invstd, g, b):
     return (x - v(mean)) * v(invstd) * v(g) + v(b)
 
 
+def _bn_pre(x, mean, invstd, g, b):
+    """The engine's BN affine value with its exact rounding (csrc/local_ops.cuh:bn_aff):
+    t = fp32(fp32(x - mean) * invstd), then one fused multiply-add t * gamma + beta rounded
+    once to fp32.  t * gamma is exact in fp64 (24 x 24 bits), so fp64 t*gamma + beta has the
+    exact sum's sign; rounding it to fp32 matches the FMA except in the rare double-rounding
+    case.  Recomputed ReLU gates use this so they agree with the GPU's bit for bit."""
+    v = lambda t: t.view(1, -1, 1, 1)
+    t = ((x.float() - v(mean.float())) * v(invstd.float())).double()
+    return (t * v(g.double()) + v(b.double())).float()
+
+
 def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torch.Tensor, record=None,
-             forced=None, fwd_record=None):
+             forced=None, fwd_record=None, forced_stats=None):
     """One training step following ``schedule`` (a schedule document). Returns the loss.
 
     ``forced`` (node id -> NCHW tensor) substitutes the given forward outputs
@@ -73,7 +84,10 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
     derivatives, which are discontinuous, are evaluated on the same inputs on
     both sides (SURVEY.md §8c); ``record`` collects input gradients per stage;
     ``fwd_record`` collects the oracle's own forward outputs (computed from the
-    possibly forced inputs) before any substitution.
+    possibly forced inputs) before any substitution; ``forced_stats`` (BN node id ->
+    (mean, invstd)) substitutes the GPU's saved batch statistics for the oracle's own, so
+    that recomputed ReLU gates (fused BN+ReLU backward from x) see the same values -- at
+    batch 184 a 1e-7 difference in invstd flips hundreds of gates per step.
     """
     net = state.net
     dt = state.dtype
@@ -137,6 +151,8 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
             if mode == "forward":
                 mean, invstd, var = _bn_stats(xin, op.attrs["eps"])
                 state.saved[op.id] = (mean, invstd)
+                if forced_stats is not None and op.id in forced_stats:
+                    state.saved[op.id] = tuple(t.to(dt) for t in forced_stats[op.id])
                 m = op.attrs["momentum"]
                 rows = xin.numel() // xin.shape[1]
                 rm, rv = state.running[op.id]
@@ -246,15 +262,15 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
             mean, invstd = state.saved[op.id]
             v = lambda t: t.view(1, -1, 1, 1)
             if op.kind == "bnrelu":  # gate by the recomputed BN output's sign (PAPER App. D, K10)
-                dy = torch.where(_bn_apply(x_of(j), mean, invstd, g, b) > 0, dy, torch.zeros_like(dy))
+                dy = torch.where(_bn_pre(x_of(j), mean, invstd, g, b) > 0, dy, torch.zeros_like(dy))
             elif op.kind == "bnrelu6":
-                z = _bn_apply(x_of(j), mean, invstd, g, b)
+                z = _bn_pre(x_of(j), mean, invstd, g, b)
                 dy = torch.where((z > 0) & (z < 6), dy, torch.zeros_like(dy))
             elif op.kind == "bnaddrelu":  # gate from z (bwd-out) or recomputed from x and skip (bwd-in)
                 if impl == "bwd-out":
                     gate = x_of(op.id) > 0
                 else:
-                    gate = (_bn_apply(x_of(j), mean, invstd, g, b) + x_of(op.attrs["skip"])) > 0
+                    gate = (_bn_pre(x_of(j), mean, invstd, g, b) + x_of(op.attrs["skip"]).float()) > 0
                 dy = torch.where(gate, dy, torch.zeros_like(dy))
                 put_grad(op.attrs["skip"], dy.clone(), created)
             if impl == "bwd-in" or op.kind == "bnaddrelu":  # bnaddrelu's bwd-out names the gate source only
@@ -419,6 +435,8 @@ def _dropout_scale(op, like, seed):
 
 
 def _bwd_deps(net, k, impl):
+    if hasattr(net, "bwd_deps"):  # frozen network (oracle/netspec.py)
+        return net.bwd_deps(k, impl)
     op = net.op(k)
     fv, bv = net.variants(op)
     for name, _, deps in bv:

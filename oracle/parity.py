@@ -38,6 +38,72 @@ def capture(rt, plan):
     return nchw, mismatched
 
 
+def gpu_stats(rt):
+    """BN node id -> (saved mean, saved invstd) of the GPU's last forward (CPU fp32 copies),
+    for run_step(..., forced_stats=...)."""
+    return {i: (v[0].detach().cpu().clone(), v[1].detach().cpu().clone()) for i, v in rt.bn.items()}
+
+
 def rel(a, b):
     a, b = a.detach().double().cpu(), b.detach().double().cpu()
     return (a - b).abs().max().item() / max(b.abs().max().item(), 1e-30)
+
+
+def grads_nhwc(state):
+    """Parameter gradients of the oracle in the engine layout (conv weights KRSC)."""
+    out = {}
+    for (nid, name), g in state.grads.items():
+        kind = state.net.op(nid).kind
+        if kind in ("conv", "convT") and name == "weight":
+            g = g.permute(0, 2, 3, 1).contiguous()
+        elif kind == "dwconv" and name == "weight":
+            g = g.squeeze(1).permute(1, 2, 0).contiguous()
+        out[(nid, name)] = g
+    return out
+
+
+def step_parity(rt, st, free=None, floor=1e-3):
+    """Per-tensor errors of one GPU training step against the oracle.
+
+    ``st``: the oracle state after ``run_step(..., forced=acts)`` (the GPU's
+    activations fed in); ``free``: an oracle state stepped on its own (for the
+    BN running statistics, which depend only on forward values).  Each error is
+    max|gpu - cpu| / max(max|cpu|, floor * G), G = the largest magnitude of that
+    kind of tensor over the whole model: tensors whose exact value is ~0 (e.g.
+    the bias gradient of a BN feeding straight into another BN) are judged
+    against the model's scale instead of their own rounding noise.
+
+    Returns {"grad": [(err, name)], "param": [...], "running": [...]}.
+    """
+    from .cpu_executor import params_nhwc
+
+    net = rt.net
+    out = {"grad": [], "param": [], "running": []}
+
+    def errs(pairs, kind):
+        pairs = list(pairs)
+        scale = max((ref.abs().max().item() for _, _, ref in pairs), default=0.0)
+        for name, got, ref in pairs:
+            ref64 = ref.detach().double().cpu()
+            got64 = got.detach().double().cpu().view(ref64.shape)
+            den = max(ref64.abs().max().item(), floor * scale, 1e-30)
+            out[kind].append(((got64 - ref64).abs().max().item() / den, name))
+
+    g = grads_nhwc(st)
+    errs(((f"{net.op(n).name}.{p}", rt.gview[(n, p)], g[(n, p)]) for (n, p) in g), "grad")
+    pv = params_nhwc(st)
+    errs(((f"{net.op(n).name}.{p}", rt.pview[(n, p)], v) for (n, p), v in pv.items()), "param")
+    if free is not None:
+        pairs = []
+        for op in net.ops:
+            if op.id in rt.bn:
+                rm, rv = free.running[op.id]
+                pairs += [(f"{op.name}.running_mean", rt.bn[op.id][2], rm),
+                          (f"{op.name}.running_var", rt.bn[op.id][3], rv)]
+        errs(pairs, "running")
+    return out
+
+
+def worst(report):
+    """(kind, err, name) of the largest error in a step_parity report."""
+    return max(((k, e, n) for k, v in report.items() for e, n in v), key=lambda t: t[1], default=("", 0.0, ""))

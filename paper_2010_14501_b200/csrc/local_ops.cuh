@@ -227,6 +227,15 @@ __global__ void scale_acc_kernel(const float* __restrict__ dy, float* dx, long l
 }
 
 // ------------------------------------------------------------------ BatchNorm
+
+// The BN affine map of one element, y = ((x - mean) * invstd) * gamma + beta, with its
+// rounding pinned: subtract, multiply, then one fused multiply-add.  Every forward apply,
+// replay and recomputed ReLU gate evaluates exactly this, so the gate a backward
+// recomputes is the forward's sign bit for bit -- and the CPU oracle reproduces it
+// (oracle/cpu_executor.py:_bn_pre).
+MONET_DEV float bn_aff(float x, float m, float s, float g, float b) {
+  return __fmaf_rn(__fmul_rn(__fsub_rn(x, m), s), g, b);
+}
 // Per-channel reduction over rows of an NHWC [rows, C] matrix.  Each block
 // owns a contiguous range of rows; a thread owns channel quad q and rows
 // r0 + rpi*j.  Partial sums go to ws[block][2][C] and are combined in fp64
@@ -254,6 +263,9 @@ __host__ __device__ inline BnLayout bn_layout(int C) {
 // mode 4: as mode 3 with the ReLU6 gate [0 < gamma*xhat + beta < 6]  (fused BN+ReLU6)
 // mode 5: as mode 1 with dy = dz * [z > 0], z = p4  (fused BN+add+ReLU, gate from its output)
 // mode 6: as mode 1 with dy = dz * [gamma*xhat + beta + skip > 0], skip = p4 (gate from its inputs)
+// mode 7: sum (x - x0), sum (x - x0)^2 with the pivot x0 = the channel's value in row 0: the
+//         shifted statistics bn_finalize_fwd turns into mean and variance without the
+//         E[x^2] - mean^2 cancellation when |mean| >> std
 __global__ void bn_reduce_kernel(int mode, const float* __restrict__ x, const float* __restrict__ dy,
                                  const float* __restrict__ p0, const float* __restrict__ p1, long long rows, int C,
                                  float* __restrict__ ws, const float* __restrict__ p2 = nullptr,
@@ -271,7 +283,9 @@ __global__ void bn_reduce_kernel(int mode, const float* __restrict__ x, const fl
     float s1[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
     if (rsub < L.rpi && q < C / 4) {
       float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a, ga = a, be = a;
-      if (mode != 0) {
+      const bool sums = mode == 0 || mode == 7;  // one input tensor, plain (shifted) sums
+      if (mode == 7) a = *reinterpret_cast<const float4*>(x + 4 * q);  // pivot: row 0
+      if (!sums) {
         a = *reinterpret_cast<const float4*>(p0 + 4 * q);  // mean | beta
         b = *reinterpret_cast<const float4*>(p1 + 4 * q);  // invstd | 1/gamma
       }
@@ -286,21 +300,22 @@ __global__ void bn_reduce_kernel(int mode, const float* __restrict__ x, const fl
           g.z = e.z > 0.f ? g.z : 0.f;
           g.w = e.w > 0.f ? g.w : 0.f;
         } else if (mode == 6) {  // gate recomputed from x and the skip input e (forward's formula)
-          g.x = ((v.x - a.x) * b.x * ga.x + be.x + e.x > 0.f) ? g.x : 0.f;
-          g.y = ((v.y - a.y) * b.y * ga.y + be.y + e.y > 0.f) ? g.y : 0.f;
-          g.z = ((v.z - a.z) * b.z * ga.z + be.z + e.z > 0.f) ? g.z : 0.f;
-          g.w = ((v.w - a.w) * b.w * ga.w + be.w + e.w > 0.f) ? g.w : 0.f;
-        } else if (mode >= 3) {  // the ReLU's gradient gate, recomputed with the forward's formula
+          g.x = (__fadd_rn(bn_aff(v.x, a.x, b.x, ga.x, be.x), e.x) > 0.f) ? g.x : 0.f;
+          g.y = (__fadd_rn(bn_aff(v.y, a.y, b.y, ga.y, be.y), e.y) > 0.f) ? g.y : 0.f;
+          g.z = (__fadd_rn(bn_aff(v.z, a.z, b.z, ga.z, be.z), e.z) > 0.f) ? g.z : 0.f;
+          g.w = (__fadd_rn(bn_aff(v.w, a.w, b.w, ga.w, be.w), e.w) > 0.f) ? g.w : 0.f;
+        } else if (mode >= 3 && mode <= 4) {  // the ReLU's gradient gate, recomputed with the forward's formula
           const bool six = mode == 4;
           auto gate = [six](float u) { return six ? (u > 0.f && u < 6.f) : u > 0.f; };
-          g.x = gate((v.x - a.x) * b.x * ga.x + be.x) ? g.x : 0.f;
-          g.y = gate((v.y - a.y) * b.y * ga.y + be.y) ? g.y : 0.f;
-          g.z = gate((v.z - a.z) * b.z * ga.z + be.z) ? g.z : 0.f;
-          g.w = gate((v.w - a.w) * b.w * ga.w + be.w) ? g.w : 0.f;
+          g.x = gate(bn_aff(v.x, a.x, b.x, ga.x, be.x)) ? g.x : 0.f;
+          g.y = gate(bn_aff(v.y, a.y, b.y, ga.y, be.y)) ? g.y : 0.f;
+          g.z = gate(bn_aff(v.z, a.z, b.z, ga.z, be.z)) ? g.z : 0.f;
+          g.w = gate(bn_aff(v.w, a.w, b.w, ga.w, be.w)) ? g.w : 0.f;
         }
-        if (mode == 0) {
-          s1[0] += v.x; s1[1] += v.y; s1[2] += v.z; s1[3] += v.w;
-          s2[0] += v.x * v.x; s2[1] += v.y * v.y; s2[2] += v.z * v.z; s2[3] += v.w * v.w;
+        if (sums) {
+          const float d0 = v.x - a.x, d1 = v.y - a.y, d2 = v.z - a.z, d3 = v.w - a.w;
+          s1[0] += d0; s1[1] += d1; s1[2] += d2; s1[3] += d3;
+          s2[0] += d0 * d0; s2[1] += d1 * d1; s2[2] += d2 * d2; s2[3] += d3 * d3;
         } else {
           float h0 = (v.x - a.x) * b.x, h1 = (v.y - a.y) * b.y, h2 = (v.z - a.z) * b.z, h3 = (v.w - a.w) * b.w;
           s1[0] += g.x; s1[1] += g.y; s1[2] += g.z; s1[3] += g.w;
@@ -309,7 +324,7 @@ __global__ void bn_reduce_kernel(int mode, const float* __restrict__ x, const fl
       };
       const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
       long long r = r_begin + rsub;
-      if (mode == 0) {  // statistics read one tensor: eight rows in flight to cover the latency
+      if (sums) {  // statistics read one tensor: eight rows in flight to cover the latency
         for (; r + 7 * L.rpi < r_end; r += 8 * L.rpi) {
           float4 v[8];
 #pragma unroll
@@ -337,16 +352,16 @@ __global__ void bn_reduce_kernel(int mode, const float* __restrict__ x, const fl
         for (int u = 0; u < 4; ++u) {
           const long long off = (r + u * L.rpi) * C + 4 * q;
           v[u] = *reinterpret_cast<const float4*>(x + off);
-          g[u] = mode == 0 ? z4 : *reinterpret_cast<const float4*>(dy + off);
-          e[u] = mode >= 5 ? *reinterpret_cast<const float4*>(p4 + off) : z4;
+          g[u] = sums ? z4 : *reinterpret_cast<const float4*>(dy + off);
+          e[u] = (mode == 5 || mode == 6) ? *reinterpret_cast<const float4*>(p4 + off) : z4;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) acc(v[u], g[u], e[u]);
       }
       for (; r < r_end; r += L.rpi) {
         const long long off = r * C + 4 * q;
-        acc(*reinterpret_cast<const float4*>(x + off), mode == 0 ? z4 : *reinterpret_cast<const float4*>(dy + off),
-            mode >= 5 ? *reinterpret_cast<const float4*>(p4 + off) : z4);
+        acc(*reinterpret_cast<const float4*>(x + off), sums ? z4 : *reinterpret_cast<const float4*>(dy + off),
+            (mode == 5 || mode == 6) ? *reinterpret_cast<const float4*>(p4 + off) : z4);
       }
     }
     // combine the rpi row-subgroups of each channel quad in shared memory
@@ -390,18 +405,19 @@ __device__ __forceinline__ void bn_warp_sum(const float* __restrict__ ws, int nb
   }
 }
 
-// forward: mean/invstd from sums; running-stat update (momentum, unbiased var).
-// One warp per channel (launch C warps).
+// forward: mean/invstd from the shifted sums of bn_reduce mode 7 (pivot x0 = row 0 of x);
+// running-stat update (momentum, unbiased var).  One warp per channel (launch C warps).
 __global__ void bn_finalize_fwd_kernel(const float* __restrict__ ws, int nblocks, long long rows, int C, float eps,
                                        float momentum, int update_running, float* mean_out, float* invstd_out,
-                                       float* running_mean, float* running_var) {
+                                       float* running_mean, float* running_var, const float* __restrict__ x) {
   const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (c >= C) return;
   double s1, s2;
   bn_warp_sum(ws, nblocks, C, c, s1, s2);
   if ((threadIdx.x & 31) != 0) return;
-  double mean = s1 / (double)rows;
-  double var = s2 / (double)rows - mean * mean;
+  const double shift = s1 / (double)rows;  // mean - x0
+  double mean = (double)x[c] + shift;
+  double var = s2 / (double)rows - shift * shift;
   if (var < 0.0) var = 0.0;
   mean_out[c] = (float)mean;
   invstd_out[c] = (float)(1.0 / sqrt(var + (double)eps));
@@ -450,10 +466,10 @@ __global__ void bn_apply_kernel(const float* __restrict__ x, float* y, const flo
     float4 s = *reinterpret_cast<const float4*>(invstd + 4 * q);
     float4 g = *reinterpret_cast<const float4*>(gamma + 4 * q);
     float4 b = *reinterpret_cast<const float4*>(beta + 4 * q);
-    v.x = (v.x - m.x) * s.x * g.x + b.x;
-    v.y = (v.y - m.y) * s.y * g.y + b.y;
-    v.z = (v.z - m.z) * s.z * g.z + b.z;
-    v.w = (v.w - m.w) * s.w * g.w + b.w;
+    v.x = bn_aff(v.x, m.x, s.x, g.x, b.x);
+    v.y = bn_aff(v.y, m.y, s.y, g.y, b.y);
+    v.z = bn_aff(v.z, m.z, s.z, g.z, b.z);
+    v.w = bn_aff(v.w, m.w, s.w, g.w, b.w);
     *reinterpret_cast<float4*>(y + 4 * i) = v;
   }
 }
@@ -505,10 +521,10 @@ __global__ void bnrelu_apply_kernel(const float* __restrict__ x, float* z, const
     const float4 s = *reinterpret_cast<const float4*>(invstd + 4 * q);
     const float4 g = *reinterpret_cast<const float4*>(gamma + 4 * q);
     const float4 b = *reinterpret_cast<const float4*>(beta + 4 * q);
-    v.x = relu_val<kSix>((v.x - m.x) * s.x * g.x + b.x);
-    v.y = relu_val<kSix>((v.y - m.y) * s.y * g.y + b.y);
-    v.z = relu_val<kSix>((v.z - m.z) * s.z * g.z + b.z);
-    v.w = relu_val<kSix>((v.w - m.w) * s.w * g.w + b.w);
+    v.x = relu_val<kSix>(bn_aff(v.x, m.x, s.x, g.x, b.x));
+    v.y = relu_val<kSix>(bn_aff(v.y, m.y, s.y, g.y, b.y));
+    v.z = relu_val<kSix>(bn_aff(v.z, m.z, s.z, g.z, b.z));
+    v.w = relu_val<kSix>(bn_aff(v.w, m.w, s.w, g.w, b.w));
     *reinterpret_cast<float4*>(z + 4 * i) = v;
   }
 }
@@ -530,10 +546,10 @@ __global__ void bnaddrelu_apply_kernel(const float* __restrict__ x, const float*
     const float4 s = *reinterpret_cast<const float4*>(invstd + 4 * q);
     const float4 g = *reinterpret_cast<const float4*>(gamma + 4 * q);
     const float4 b = *reinterpret_cast<const float4*>(beta + 4 * q);
-    v.x = fmaxf((v.x - m.x) * s.x * g.x + b.x + k.x, 0.f);
-    v.y = fmaxf((v.y - m.y) * s.y * g.y + b.y + k.y, 0.f);
-    v.z = fmaxf((v.z - m.z) * s.z * g.z + b.z + k.z, 0.f);
-    v.w = fmaxf((v.w - m.w) * s.w * g.w + b.w + k.w, 0.f);
+    v.x = fmaxf(__fadd_rn(bn_aff(v.x, m.x, s.x, g.x, b.x), k.x), 0.f);
+    v.y = fmaxf(__fadd_rn(bn_aff(v.y, m.y, s.y, g.y, b.y), k.y), 0.f);
+    v.z = fmaxf(__fadd_rn(bn_aff(v.z, m.z, s.z, g.z, b.z), k.z), 0.f);
+    v.w = fmaxf(__fadd_rn(bn_aff(v.w, m.w, s.w, g.w, b.w), k.w), 0.f);
     *reinterpret_cast<float4*>(z + 4 * i) = v;
   }
 }
@@ -566,10 +582,10 @@ __global__ void bnaddrelu_bwd_apply_kernel(const float* __restrict__ x, const fl
       g.z = ev.z > 0.f ? g.z : 0.f;
       g.w = ev.w > 0.f ? g.w : 0.f;
     } else {
-      g.x = ((v.x - m.x) * is.x * ga.x + be.x + ev.x > 0.f) ? g.x : 0.f;
-      g.y = ((v.y - m.y) * is.y * ga.y + be.y + ev.y > 0.f) ? g.y : 0.f;
-      g.z = ((v.z - m.z) * is.z * ga.z + be.z + ev.z > 0.f) ? g.z : 0.f;
-      g.w = ((v.w - m.w) * is.w * ga.w + be.w + ev.w > 0.f) ? g.w : 0.f;
+      g.x = (__fadd_rn(bn_aff(v.x, m.x, is.x, ga.x, be.x), ev.x) > 0.f) ? g.x : 0.f;
+      g.y = (__fadd_rn(bn_aff(v.y, m.y, is.y, ga.y, be.y), ev.y) > 0.f) ? g.y : 0.f;
+      g.z = (__fadd_rn(bn_aff(v.z, m.z, is.z, ga.z, be.z), ev.z) > 0.f) ? g.z : 0.f;
+      g.w = (__fadd_rn(bn_aff(v.w, m.w, is.w, ga.w, be.w), ev.w) > 0.f) ? g.w : 0.f;
     }
     float4 o;
     o.x = fmaf(ga.x * is.x, g.x, fmaf(cb.x, v.x, cc.x));
@@ -609,10 +625,10 @@ __global__ void bnrelu_bwd_apply_kernel(const float* __restrict__ x, const float
     const float4 is = *reinterpret_cast<const float4*>(invstd + 4 * q);
     const float4 cb = *reinterpret_cast<const float4*>(coef_b + 4 * q);
     const float4 cc = *reinterpret_cast<const float4*>(coef_c + 4 * q);
-    g.x = relu_gate<kSix>((v.x - m.x) * is.x * ga.x + be.x) ? g.x : 0.f;
-    g.y = relu_gate<kSix>((v.y - m.y) * is.y * ga.y + be.y) ? g.y : 0.f;
-    g.z = relu_gate<kSix>((v.z - m.z) * is.z * ga.z + be.z) ? g.z : 0.f;
-    g.w = relu_gate<kSix>((v.w - m.w) * is.w * ga.w + be.w) ? g.w : 0.f;
+    g.x = relu_gate<kSix>(bn_aff(v.x, m.x, is.x, ga.x, be.x)) ? g.x : 0.f;
+    g.y = relu_gate<kSix>(bn_aff(v.y, m.y, is.y, ga.y, be.y)) ? g.y : 0.f;
+    g.z = relu_gate<kSix>(bn_aff(v.z, m.z, is.z, ga.z, be.z)) ? g.z : 0.f;
+    g.w = relu_gate<kSix>(bn_aff(v.w, m.w, is.w, ga.w, be.w)) ? g.w : 0.f;
     float4 o;
     o.x = fmaf(ga.x * is.x, g.x, fmaf(cb.x, v.x, cc.x));
     o.y = fmaf(ga.y * is.y, g.y, fmaf(cb.y, v.y, cc.y));

@@ -59,6 +59,16 @@ class Plan:
     n_blocks: int
     launches: int
     step_kinds: dict = field(default_factory=dict)
+    g: Graph | None = None
+    catalog: Catalog | None = None
+    graph: object = None  # captured torch.cuda.CUDAGraph (Runtime.capture)
+
+    @property
+    def within_bound(self) -> bool | None:
+        """params_bytes + arena high-water mark <= check_schedule's ILP bound."""
+        if self.bound_peak is None or self.g is None:
+            return None
+        return self.g.params_bytes + self.arena_bytes <= self.bound_peak
 
 
 @dataclass
@@ -176,6 +186,9 @@ class Runtime:
                 self.set_batch(images, labels)
             else:
                 self.set_batch_nhwc(images, labels)
+        if plan.calls is None:
+            raise RuntimeError("this plan was invalidated when the runtime's arena was reallocated; "
+                               "call Runtime.plan() again")
         if getattr(plan, "graph", None) is not None:
             plan.graph.replay()
         else:
@@ -202,9 +215,10 @@ class Runtime:
 
     # ------------------------------------------------------------ planning
     def plan(self, schedule: Schedule, g: Graph, catalog: Catalog, check_bound: bool = True) -> Plan:
-        key = id(schedule)
-        if key in self._plans and self._plans[key].schedule is schedule:
-            return self._plans[key]
+        key = (id(schedule), id(g), id(catalog))
+        hit = self._plans.get(key)
+        if hit is not None and hit.schedule is schedule and hit.g is g and hit.catalog is catalog:
+            return hit
         self._check_graph(g)
         tags = validate(schedule, g, compute_dependency_sets(g), catalog)
         if tags:
@@ -218,6 +232,12 @@ class Runtime:
             raise BudgetExceeded(f"planned footprint {fixed_peak} B exceeds budget {self.budget_bytes} B "
                                  f"(ledger peak {trace.peak_memory} B)")
         if self.arena is None or self.arena.numel() < arena_bytes:
+            # every cached plan (and its captured graph) holds absolute pointers into the
+            # old arena: drop them before the buffer goes away
+            for old in self._plans.values():
+                old.graph = None
+                old.calls = None
+            self._plans.clear()
             self.arena = None
             torch.cuda.empty_cache()
             self.arena = torch.empty(max(arena_bytes, ALIGN), dtype=torch.uint8, device=self.device)
@@ -235,6 +255,7 @@ class Runtime:
         plan = Plan(schedule, trace, calls, arena_bytes, trace.peak_memory, bound, len(blocks),
                     sum(1 for group in calls for c in group if c[0] == "k"))
         plan.steps, plan.step_ptrs = steps, step_ptrs
+        plan.g, plan.catalog = g, catalog
         self._plans[key] = plan
         return plan
 
@@ -377,7 +398,27 @@ class Runtime:
         out = []
         dy = P(("g", op.id))
         ws = ptrs.get(("ws",))
-        acc = lambda j: 0 if j in s.new_grads else 1
+        written = set()
+
+        def acc(j):
+            # first write of a gradient this step overwrites, every later one (another
+            # consumer, or the same input read twice as in add(x, x)) accumulates
+            a = 0 if (j in s.new_grads and j not in written) else 1
+            written.add(j)
+            return a
+
+        def needs(j):
+            # inputs without a gradient buffer (the network input) get no dx kernel
+            return net.grad_bytes(net.op(j)) > 0
+
+        def must(j):
+            if not needs(j):
+                raise ValueError(f"{op.kind} node {op.id} reads node {j} directly, which has no gradient "
+                                 "buffer; this operator's backward kernel always writes its input gradient")
+
+        if op.kind in ("bn", "bnrelu", "bnrelu6", "bnaddrelu", "addrelu", "maxpool", "avgpool", "fc", "xent"):
+            for j in op.deps:
+                must(j)
         if op.id == net.n:
             out.append(("copy", dy, self.consts.data_ptr(), 4))  # seed dL/dL = 1
         if op.kind == "input":
@@ -433,10 +474,12 @@ class Runtime:
                 src, fn = P(("in", op.id)), lib.monet_relu6_bwd_out
             else:
                 src, fn = P(("in", j)), lib.monet_relu6_bwd_in
-            out.append(("k", fn, (src, dy, P(("g", j)), op.numel, acc(j), None)))
+            if needs(j):
+                out.append(("k", fn, (src, dy, P(("g", j)), op.numel, acc(j), None)))
         elif op.kind == "dropout":
             j = op.deps[0]
-            out.append(("k", lib.monet_dropout_bwd, (dy, P(("g", j)), op.numel, C.c_float(op.attrs["p"]),
+            if needs(j):
+                out.append(("k", lib.monet_dropout_bwd, (dy, P(("g", j)), op.numel, C.c_float(op.attrs["p"]),
                                                      self.seed_ptr, op.id, acc(j), None)))
         elif op.kind == "bn":
             c = op.shape[-1]
@@ -470,9 +513,12 @@ class Runtime:
                 src, fn = P(("in", op.id)), lib.monet_relu_bwd_out
             else:
                 src, fn = P(("in", j)), lib.monet_relu_bwd_in
-            out.append(("k", fn, (src, dy, P(("g", j)), op.numel, acc(j), None)))
+            if needs(j):
+                out.append(("k", fn, (src, dy, P(("g", j)), op.numel, acc(j), None)))
         elif op.kind == "add":
             for j in op.deps:
+                if not needs(j):
+                    continue
                 out.append(("k", lib.monet_grad_pass, (dy, P(("g", j)), op.numel, C.c_float(1.0), acc(j), None)))
         elif op.kind == "bnaddrelu":
             c = op.shape[-1]
@@ -541,6 +587,9 @@ class Runtime:
 
         ``after_step(i)`` (debugging) is called after ledger step i is enqueued.
         """
+        if plan.calls is None:
+            raise RuntimeError("this plan was invalidated when the runtime's arena was reallocated; "
+                               "call Runtime.plan() again")
         stream = torch.cuda.current_stream(self.device)
         sp = C.c_void_p(stream.cuda_stream)
         cudart = _cudart()

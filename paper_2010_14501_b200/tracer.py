@@ -75,7 +75,6 @@ class Network:
     def __init__(self, ops: list[Op], batch: int, num_classes: int):
         self.ops = ops
         self.fused = any(op.kind in ("bnrelu", "bnrelu6", "bnaddrelu") for op in ops)
-        self.pair_variants = False  # offer the cta_group::2 conv variant in the catalog
         self.batch = batch
         self.num_classes = num_classes
         self.n = len(ops)
@@ -169,7 +168,7 @@ class Network:
             nodes.append({"id": op.id, "output_bytes": op.nbytes, "deps": list(op.deps)})
             impls = [{"name": n, "deps_kind": k,
                       "extra_deps": [op.attrs["x"]] if op.kind == "bnaddrelu" and n == "bwd-out" else []}
-                     for n, k in BWD_IMPLS[op.kind] if n != "pair" or self.pair_variants]
+                     for n, k in BWD_IMPLS[op.kind]]
             backward.append({"node": op.id, "grad_bytes": self.grad_bytes(op), "impls": impls})
             if op.id in self.intermediate_of:
                 u = self.intermediate_of[op.id]
@@ -198,12 +197,8 @@ class Network:
             ws = lib.conv_ws_bytes(1, 0, d)
             if ws:
                 fwd.append(("splitk", ws))
-            if self.pair_variants:  # 2-CTA (cta_group::2) tiles: same bytes, another speed point
-                fwd.append(("pair", 0))
             bwd.append(("splitk", lib.conv_ws_bytes(1, 3, d), x))
             bwd.append(("implicit", lib.conv_ws_bytes(0, 3, d), x))
-            if self.pair_variants:
-                bwd.append(("pair", lib.conv_ws_bytes(4, 3, d), x))
         elif op.kind == "fc":
             n, fi = self.fc_dims(op)
             fo = op.shape[1]
@@ -312,7 +307,7 @@ def _cost(costs, key, fallback):
 
 BWD_IMPLS = {
     "input": [("none", "input")],
-    "conv": [("splitk", "input"), ("implicit", "input"), ("pair", "input")],
+    "conv": [("splitk", "input"), ("implicit", "input")],
     "fc": [("gemm-splitk", "input"), ("gemm", "input")],
     "bn": [("bwd-in", "input"), ("bwd-out", "output")],
     "bnrelu": [("bwd-in", "input")],

@@ -1,4 +1,4 @@
-"""The planned arena of every committed schedule (ResNet-50, VGG-16) fits its ILP bound.
+"""The planned arena of every committed schedule (schedules/*.json) fits its ILP bound.
 
 Physical peak = params_bytes + arena high-water mark (csrc/arena.cpp) must not
 exceed check_schedule's modeled peak (oracle.py:287), which must not exceed
@@ -17,22 +17,25 @@ from paper_2010_14501_b200.schedule import ledger
 from paper_2010_14501_b200.tracer import build_network
 
 ROOT = Path(__file__).resolve().parent.parent
-SCHEDULES = sorted((ROOT / "schedules").glob("*_b*_224_*gib.json"))
+SCHEDULES = sorted((ROOT / "schedules").glob("*_b*_*gib.json"))
 
 
 _NETS = {}
 
 
 def _net(path):
-    """(network, graph, catalog) a schedule file was planned for (name: arch[_fused]_b<batch>_224_...)."""
+    """(network, graph, catalog) a schedule file was planned for
+    (name: arch[_fused]_b<batch>_<image>_<budget>gib, image 224 or HxW)."""
     stem = path.name.split("_b")[0]
     arch, fused = stem.removesuffix("_fused"), stem.endswith("_fused")
-    batch = int(path.name.split("_b")[1].split("_")[0])
-    key = (arch, fused, batch)
+    batch, image = path.name.split("_b")[1].split("_")[:2]
+    batch = int(batch)
+    key = (arch, fused, batch, image)
     if key not in _NETS:
-        net = build_network(arch, batch, 224, fuse=fused)
+        from paper_2010_14501_b200.tracer import default_classes, parse_image
+        net = build_network(arch, batch, parse_image(image), num_classes=default_classes(arch), fuse=fused)
         g = M.load_graph(net.graph_doc())
-        cpath = ROOT / "profiles" / f"catalog_{stem}_b{batch}_224.json"
+        cpath = ROOT / "profiles" / f"catalog_{stem}_b{batch}_{image}.json"
         cdoc = json.loads(cpath.read_text())["catalog"] if cpath.exists() else net.catalog_doc()
         _NETS[key] = (net, g, M.load_catalog(cdoc, g))
     return _NETS[key]

@@ -1,0 +1,143 @@
+"""Kernel numerics at the headline config's shapes (ResNet-50, batch 184, 224x224).
+
+The small-shape tests in test_kernels_gpu.py reduce over at most ~35k pixels;
+the C2 step reduces 16-65x longer.  These cases run the exact C2 layer shapes
+and compare with float64 torch on the same device (an independent fp64
+implementation: cuDNN / ATen double kernels):
+
+  * the 7x7/2 stem wgrad over 184*112*112 = 2.31 M output pixels (tap-view path);
+  * a layer1 3x3 64->64 wgrad over 184*56*56 = 577 k pixels (TMEM chains of
+    1024 k flushed with red.global.add);
+  * BatchNorm statistics and backward over 2.31 M rows with |mean| / std = 10
+    and 1000 (shifted single-pass statistics, bn_reduce mode 7).
+
+Tolerance: max|gpu - ref| / max|ref| per tensor, 5e-5 for the bf16x3
+tensor-core passes, 1e-5 (2e-5 output-activated) for the CUDA-core BN.
+"""
+import math
+
+import pytest
+import torch
+import torch.nn.functional as F
+
+from paper_2010_14501_b200 import _native as N
+
+pytestmark = pytest.mark.gpu
+
+REL_TC = 5e-5
+REL_EW = 1e-5
+
+
+def rel(a, b):
+    a, b = a.double(), b.double()
+    return ((a - b).abs().max() / b.abs().max().clamp_min(1e-300)).item()
+
+
+def stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _wgrad_case(cuda, n, h, w, c, k, r, s, stride, pad, variant):
+    g = torch.Generator(device=cuda).manual_seed(11)
+    x = torch.randn(n, h, w, c, device=cuda, generator=g)
+    d = N.conv_desc(n, h, w, c, k, r, s, stride, pad)
+    dy = torch.randn(n, d.p, d.q, k, device=cuda, generator=g)
+    lib = N.lib()
+    v = N.CONV_VARIANTS[variant]
+    ws_b = lib.conv_ws_bytes(v, N.PASS["wgrad"], d)
+    ws = torch.empty(max(ws_b, 16), dtype=torch.uint8, device=cuda)
+    dw = torch.empty(k, r, s, c, device=cuda)
+    lib.conv_wgrad(v, d, x.data_ptr(), dy.data_ptr(), dw.data_ptr(), 0, ws.data_ptr(), ws_b, stream())
+    ref = torch.nn.grad.conv2d_weight(x.double().permute(0, 3, 1, 2), (k, c, r, s),
+                                      dy.double().permute(0, 3, 1, 2), stride=stride, padding=pad)
+    err = rel(dw, ref.permute(0, 2, 3, 1))
+    assert err < REL_TC, (variant, err)
+    return x, dy, d, err
+
+
+@pytest.mark.parametrize("variant", ["implicit", "splitk"])
+def test_stem_wgrad_c2(cuda, variant):
+    """7x7/2 stem, input padded to 4 channels, 2.31 M output pixels."""
+    _wgrad_case(cuda, 184, 224, 224, 4, 64, 7, 7, 2, 3, variant)
+
+
+@pytest.mark.parametrize("variant", ["implicit", "splitk"])
+def test_layer1_3x3_wgrad_c2(cuda, variant):
+    """layer1 3x3 64->64 over 577 k pixels."""
+    _wgrad_case(cuda, 184, 56, 56, 64, 64, 3, 3, 1, 1, variant)
+
+
+def test_layer1_3x3_fwd_dgrad_c2(cuda):
+    n, h, w, c, k = 184, 56, 56, 64, 64
+    g = torch.Generator(device=cuda).manual_seed(12)
+    x = torch.randn(n, h, w, c, device=cuda, generator=g)
+    wt = torch.randn(k, 3, 3, c, device=cuda, generator=g) / math.sqrt(9 * c)
+    d = N.conv_desc(n, h, w, c, k, 3, 3, 1, 1)
+    lib = N.lib()
+    v = N.CONV_VARIANTS["splitk"]
+    ws_b = lib.conv_ws_bytes(v, N.PASS["bwd"], d)
+    ws = torch.empty(max(ws_b, 16), dtype=torch.uint8, device=cuda)
+    y = torch.empty(n, h, w, k, device=cuda)
+    lib.conv_fwd(v, d, x.data_ptr(), wt.data_ptr(), y.data_ptr(), ws.data_ptr(), ws_b, stream())
+    ref = F.conv2d(x.double().permute(0, 3, 1, 2), wt.double().permute(0, 3, 1, 2), padding=1)
+    assert rel(y, ref.permute(0, 2, 3, 1)) < REL_TC
+    dy = torch.randn(n, h, w, k, device=cuda, generator=g)
+    dx = torch.empty_like(x)
+    lib.conv_dgrad(v, d, dy.data_ptr(), wt.data_ptr(), dx.data_ptr(), 0, ws.data_ptr(), ws_b, stream())
+    ref = torch.nn.grad.conv2d_input(x.permute(0, 3, 1, 2).shape, wt.double().permute(0, 3, 1, 2),
+                                     dy.double().permute(0, 3, 1, 2), padding=1)
+    assert rel(dx, ref.permute(0, 2, 3, 1)) < REL_TC
+
+
+@pytest.mark.parametrize("ratio", [10.0, 1000.0])
+def test_batchnorm_c2_rows_large_mean(cuda, ratio):
+    """BN over the stem output's 2.31 M rows x 64 channels, channel means = ratio x std."""
+    n, h, w, c = 184, 112, 112, 64
+    rows = n * h * w
+    g = torch.Generator(device=cuda).manual_seed(13)
+    std = torch.rand(c, device=cuda, generator=g) + 0.5
+    mu = ratio * std * torch.sign(torch.randn(c, device=cuda, generator=g))
+    x = torch.randn(n, h, w, c, device=cuda, generator=g) * std + mu
+    gamma = torch.rand(c, device=cuda, generator=g) + 0.5
+    beta = torch.randn(c, device=cuda, generator=g)
+    dy = torch.randn(n, h, w, c, device=cuda, generator=g)
+    lib = N.lib()
+    y = torch.empty_like(x)
+    mean, invstd = torch.empty(c, device=cuda), torch.empty(c, device=cuda)
+    rm, rv = torch.zeros(c, device=cuda), torch.ones(c, device=cuda)
+    scratch = torch.empty(lib.bn_scratch_bytes(rows, c) // 4 + 1, device=cuda)
+    lib.bn_fwd_train(x.data_ptr(), y.data_ptr(), gamma.data_ptr(), beta.data_ptr(), mean.data_ptr(),
+                     invstd.data_ptr(), rm.data_ptr(), rv.data_ptr(), rows, c, 1e-5, 0.1, 1, scratch.data_ptr(),
+                     stream())
+    xd = x.double().reshape(rows, c)
+    m64 = xd.mean(0)
+    v64 = ((xd - m64) ** 2).mean(0)
+    is64 = 1.0 / torch.sqrt(v64 + 1e-5)
+    assert rel(mean, m64) < REL_EW
+    assert rel(invstd, is64) < REL_EW, rel(invstd, is64)
+    assert rel(rv, 0.9 + 0.1 * v64 * rows / (rows - 1)) < REL_EW
+    # the statistics hold 1e-5 at any ratio; the elementwise outputs evaluate
+    # x - mean in fp32, where x itself carries |mean| * 2^-24 of rounding: at
+    # ratio 1000 that is ~6e-5 of a standard deviation, so their bar scales with it
+    ew = REL_EW * max(1.0, ratio / 100)
+    xhat = (xd - m64) * is64
+    y64 = xhat * gamma.double() + beta.double()
+    assert rel(y.reshape(rows, c), y64) < ew
+    # backward from the input (bwd-in) and from the output (bwd-out)
+    g64 = dy.double().reshape(rows, c)
+    s1, s2 = g64.sum(0), (g64 * xhat).sum(0)
+    dx64 = gamma.double() * is64 * (g64 - s1 / rows - xhat * s2 / rows)
+    for fn in ("bn_bwd_in", "bn_bwd_out"):
+        dx = torch.empty_like(x)
+        dg, db = torch.empty(c, device=cuda), torch.empty(c, device=cuda)
+        if fn == "bn_bwd_in":
+            lib.bn_bwd_in(x.data_ptr(), dy.data_ptr(), dx.data_ptr(), 0, gamma.data_ptr(), mean.data_ptr(),
+                          invstd.data_ptr(), dg.data_ptr(), db.data_ptr(), rows, c, scratch.data_ptr(), stream())
+            tol = ew
+        else:
+            lib.bn_bwd_out(y.data_ptr(), dy.data_ptr(), dx.data_ptr(), 0, gamma.data_ptr(), beta.data_ptr(),
+                           invstd.data_ptr(), dg.data_ptr(), db.data_ptr(), rows, c, scratch.data_ptr(), stream())
+            tol = 2 * ew
+        assert rel(dx.reshape(rows, c), dx64) < tol, (fn, rel(dx.reshape(rows, c), dx64))
+        assert rel(dg, s2) < tol, (fn, rel(dg, s2))
+        assert rel(db, s1) < REL_EW, (fn, rel(db, s1))
