@@ -383,9 +383,10 @@ def ours_arm(args):
     # trains at torchvision's reference lr 0.01
     lr = 0.01 if args.arch.startswith("vgg") else 0.1
     rt = Runtime(net, device=dev, budget_bytes=budget, lr=lr)
+    dp = None
     if world > 1:
         from paper_2010_14501_b200.dp import DataParallel
-        DataParallel(rt)
+        dp = DataParallel(rt)
     plan = rt.plan(sched, g, cat)
 
     hw = image_arg(args.image)
@@ -404,7 +405,9 @@ def ours_arm(args):
     torch.cuda.empty_cache()
 
     graph = None
-    use_graph = not args.no_graph and world == 1
+    # N > 1: the native communicator's bucket all-reduces are stream operations, so the
+    # data-parallel step is captured whole as well
+    use_graph = not args.no_graph and (world == 1 or getattr(rt.comm, "capturable", False))
     if use_graph:
         graph = rt.capture(plan)
 
@@ -563,6 +566,8 @@ def ours_arm(args):
         if not math.isfinite(loss):
             print(f"bench: loss is {loss} after {args.warmup + args.steps + 2} steps -- invalid run", file=sys.stderr)
     if world > 1:
+        del graph
+        dp.close()
         dist.destroy_process_group()
     if not math.isfinite(loss):
         sys.exit(3)

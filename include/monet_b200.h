@@ -42,8 +42,8 @@ typedef struct {
  *                                    fp32 partials in workspace (honest ws/speed trade)
  *   MONET_CONV_TF32      "tf32"      single-pass TF32 (faster, ~1e-3 relative error; tests only)
  *   MONET_CONV_TF32X3    "tf32x3"    3xTF32 all-shared-memory kernel (round-1 baseline)
- *   MONET_CONV_PAIR      "pair"      as implicit, on CTA pairs (cta_group::2, 256 x 128 tiles, each
- *                                    CTA holds half of B) -- the 1-CTA vs 2-CTA tile point */
+ *   MONET_CONV_PAIR      "pair"      retired (returns -cudaErrorNotSupported): CTA pairs measured
+ *                                    15-25 % slower than one CTA per tile */
 enum { MONET_CONV_IMPLICIT = 0, MONET_CONV_SPLITK = 1, MONET_CONV_TF32 = 2, MONET_CONV_TF32X3 = 3,
        MONET_CONV_PAIR = 4 };
 enum { MONET_PASS_FWD = 0, MONET_PASS_DGRAD = 1, MONET_PASS_WGRAD = 2, MONET_PASS_BWD = 3 };
@@ -54,12 +54,51 @@ int monet_device_check(void); /* 0 if the current device is sm_100 */
 /* device-to-device byte copy on `stream` (staging the input batch into the arena,
  * the loss seed); the executor needs no other CUDA runtime entry point */
 int monet_copy_async(void* dst, const void* src, size_t bytes, void* stream);
-/* debug only: make the bf16x3 GEMM dump the raw A / B operands it consumes
- * ([rows][K rounded up to 64] fp32 device buffers; NULL disables) */
-void monet_debug_dump(float* a_dump, float* b_dump);
-/* debug only: accumulate per-role barrier wait cycles of the bf16x3 GEMM into
- * 16 uint64 device counters (see gemm_bf16x3.cuh TWAIT; NULL disables) */
-void monet_debug_timers(unsigned long long* counters);
+/* (The operand-dump and wait-counter hooks of the GEMM exist only in the debug build,
+ * libmonet_b200_dbg.so, `python -m paper_2010_14501_b200.build --debug`; not part of this ABI.) */
+
+/* --- data-parallel gradient exchange (SURVEY.md §8b "Comm", §8e) ----------------------
+ * One communicator per GPU process (NCCL, resolved at run time from the process's own
+ * libnccl.so.2).  Rank 0 creates the unique id (monet_comm_unique_id_bytes() bytes), the
+ * caller broadcasts it (torch.distributed), every rank calls monet_comm_init.
+ * monet_allreduce_bucket forks the in-place fp32 sum of one gradient bucket off `stream`
+ * onto the communicator's own stream, ordered after everything already enqueued on
+ * `stream` (the backward kernels that finalize the bucket), so it overlaps the remaining
+ * backward stages; monet_comm_join makes `stream` wait for every bucket forked since the
+ * last join (before the optimizer).  All of it is stream-ordered and CUDA-graph
+ * capturable.  NCCL failures return -(1000 + ncclResult_t). */
+typedef struct monet_comm monet_comm;
+size_t monet_comm_unique_id_bytes(void);
+int monet_comm_unique_id(void* id_out);
+int monet_comm_init(const void* unique_id, int rank, int nranks, monet_comm** out);
+int monet_comm_destroy(monet_comm* comm);
+int monet_allreduce_bucket(monet_comm* comm, float* buf, size_t count, void* stream);
+int monet_comm_join(monet_comm* comm, void* stream);
+
+/* --- profiler (R3: fills the catalog's variant costs and workspace, costmodel.py:85-181) ---
+ * monet_profile_variant times one operator variant on synthetic operands it allocates
+ * and frees itself: two warm-up launches, then the median of three CUDA-event-timed
+ * groups of `iters` launches on `stream`.  *ns = nanoseconds per launch (an integer,
+ * units.py:61-62 forbids fractional costs in a catalog), *ws_bytes = the workspace the
+ * variant takes from the arena (conv: monet_conv_ws_bytes of that variant and pass; 0 for
+ * the local operators, whose scratch lives in the fixed region).
+ *   op  MONET_OP_CONV   pass FWD (forward) or BWD (dgrad, if conv_needs_dx, + wgrad); variant
+ *                       = MONET_CONV_*; desc in `conv`
+ *       MONET_OP_RELU   pass FWD (with the 1-bit mask) or BWD with variant MONET_BWD_IN /
+ *                       _OUT / _MASK; rows * c elements
+ *       MONET_OP_BN     pass FWD (train: statistics + apply) or BWD (MONET_BWD_IN / _OUT)
+ *       MONET_OP_BNRELU fused BN+ReLU: FWD, or BWD (MONET_BWD_IN, from x) */
+enum { MONET_OP_CONV = 0, MONET_OP_RELU = 1, MONET_OP_BN = 2, MONET_OP_BNRELU = 3 };
+enum { MONET_BWD_IN = 0, MONET_BWD_OUT = 1, MONET_BWD_MASK = 2 };
+typedef struct {
+  int op, pass;
+  monet_conv_desc conv;
+  int conv_needs_dx; /* 0 when the conv reads the network input (no dgrad) */
+  int64_t rows;      /* local ops: [rows, c] NHWC */
+  int c;
+} monet_prof_desc;
+int monet_profile_variant(const monet_prof_desc* d, int variant, int iters, int64_t* ns, size_t* ws_bytes,
+                          void* stream);
 
 /* --- convolution (K1-K3; replaces conv entries of Catalog, costmodel.py:30-44) */
 size_t monet_conv_ws_bytes(int variant, int pass, const monet_conv_desc* d);

@@ -22,13 +22,28 @@ class ConvDesc(C.Structure):
 
 _PCONV = C.POINTER(ConvDesc)
 
+
+class ProfDesc(C.Structure):
+    """monet_prof_desc (include/monet_b200.h)."""
+    _fields_ = [("op", C.c_int), ("pass_", C.c_int), ("conv", ConvDesc), ("conv_needs_dx", C.c_int),
+                ("rows", C.c_int64), ("c", C.c_int)]
+
+
+PROF_OP = {"conv": 0, "relu": 1, "bn": 2, "bnrelu": 3}
+PROF_BWD = {"bwd-in": 0, "bwd-out": 1, "bwd-mask": 2}
+
 # name -> (restype, argtypes)
 SIGNATURES = {
     "monet_version": (C.c_char_p, []),
     "monet_device_check": (_i32, []),
     "monet_copy_async": (_i32, [_vp, _vp, _sz, _vp]),
-    "monet_debug_dump": (None, [_vp, _vp]),
-    "monet_debug_timers": (None, [_vp]),
+    "monet_comm_unique_id_bytes": (_sz, []),
+    "monet_comm_unique_id": (_i32, [_vp]),
+    "monet_comm_init": (_i32, [_vp, _i32, _i32, C.POINTER(_vp)]),
+    "monet_comm_destroy": (_i32, [_vp]),
+    "monet_allreduce_bucket": (_i32, [_vp, _vp, _sz, _vp]),
+    "monet_comm_join": (_i32, [_vp, _vp]),
+    "monet_profile_variant": (_i32, [C.c_void_p, _i32, _i32, C.POINTER(_i64), C.POINTER(_sz), _vp]),
     "monet_conv_ws_bytes": (_sz, [_i32, _i32, _PCONV]),
     "monet_conv_fwd": (_i32, [_i32, _PCONV, _vp, _vp, _vp, _vp, _sz, _vp]),
     "monet_conv_dgrad": (_i32, [_i32, _PCONV, _vp, _vp, _vp, _i32, _vp, _sz, _vp]),
@@ -144,6 +159,23 @@ def lib() -> _Lib:
     if _LIB is None:
         _LIB = _Lib(LIB_PATH)
     return _LIB
+
+
+_DBG: _Lib | None = None
+
+
+def debug_lib() -> _Lib:
+    """libmonet_b200_dbg.so (build.py --debug): the ABI plus the GEMM's operand-dump and
+    wait-counter hooks, for tools/ only -- the product never loads it."""
+    global _DBG
+    if _DBG is None:
+        from . import build
+        _DBG = _Lib(build.build(debug=True))
+        _DBG.dll.monet_debug_dump.restype = None
+        _DBG.dll.monet_debug_dump.argtypes = [_vp, _vp]
+        _DBG.dll.monet_debug_timers.restype = None
+        _DBG.dll.monet_debug_timers.argtypes = [_vp]
+    return _DBG
 
 
 def conv_desc(n, h, w, c, k, r, s, stride=1, pad=0) -> ConvDesc:

@@ -29,14 +29,34 @@ inline int ew_blocks(long long work_items) {
 }
 
 // ----------------------------------------------------------------- GEMM setup
+// Split-K factor of the "splitk" variant.  The persistent kernel walks tiles x splits
+// units in rounds of kNumSMs; a round's time is set by its longest unit (kb_per_split
+// k-blocks, rounded up to whole bf16x3 stages).  Up to the old target of ~2 units per SM,
+// pick the split count with the least modeled time rounds * kb_per_split (ties: fewer
+// splits, i.e. less partial-sum traffic): e.g. 36 tiles -> 8 splits (288 units, 2 full
+// rounds) instead of 9 (324 units, a third round for 28 of them).  Never more splits than
+// the old rule, so the workspace never grows.
 int choose_splits(int variant, int M, int N, int Kd, int n_pitch = BN) {
   const int tiles = ((M + BM - 1) / BM) * ((N + n_pitch - 1) / n_pitch);
   const int kblocks = (Kd + BK - 1) / BK;
   if (variant != MONET_CONV_SPLITK) return 1;
   if (tiles >= kNumSMs) return 1;
-  int want = (2 * kNumSMs + tiles - 1) / tiles;
-  int cap = std::max(1, kblocks / 4);
-  return std::max(1, std::min(want, cap));
+  const int want = (2 * kNumSMs + tiles - 1) / tiles;
+  const int hi = std::max(1, std::min(want, std::max(1, kblocks / 4)));
+  int best = 1;
+  long long best_cost = -1;
+  for (int s = 1; s <= hi; ++s) {
+    int kbps = (kblocks + s - 1) / s;
+    kbps = (kbps + 1) & ~1;
+    const int splits = (kblocks + kbps - 1) / kbps;
+    const long long rounds = (tiles * (long long)splits + kNumSMs - 1) / kNumSMs;
+    const long long cost = rounds * kbps;
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = s;
+    }
+  }
+  return best;
 }
 
 size_t gemm_ws(int variant, int M, int N, int Kd, int n_pitch = BN) {
@@ -94,6 +114,9 @@ int dispatch_modes(const GemmParams& p, int grid, cudaStream_t st) {
   if (a == OP_MNMAJOR && b == OP_IM2COL_WGRAD) return launch_inst<kBx3, kPair, OP_MNMAJOR, OP_IM2COL_WGRAD, NB>(p, grid, st);
   if (a == OP_MNMAJOR && b == OP_MNMAJOR) return launch_inst<kBx3, kPair, OP_MNMAJOR, OP_MNMAJOR, NB>(p, grid, st);
   if (a == OP_MNMAJOR && b == OP_KMAJOR) return launch_inst<kBx3, kPair, OP_MNMAJOR, OP_KMAJOR, NB>(p, grid, st);
+  if constexpr (kBx3)  // swapped wgrad of narrow convs: A = im2col(x)^T, B = dy^T
+    if (a == OP_IM2COL_WGRAD && b == OP_MNMAJOR)
+      return launch_inst<kBx3, kPair, OP_IM2COL_WGRAD, OP_MNMAJOR, NB>(p, grid, st);
   return -(int)cudaErrorInvalidValue;
 }
 
@@ -148,7 +171,7 @@ int im2col_map(CUtensorMap* m, const float* ptr, int n, int h, int w, int c, int
 // TMA descriptor for one bf16x3 operand; returns Operand::tma (0 = use the
 // 16B cp.async fallback).  Raw layouts: K-major boxes are 32 fp32 x 128 rows
 // with SWIZZLE_128B, MN-major boxes 128 (or p.mn_seg) rows x 32 k, unswizzled.
-int make_tma(GemmParams& p, const Operand& op, CUtensorMap* m) {
+int make_tma(GemmParams& p, Operand& op, CUtensorMap* m) {
   if (!tma_available() || (reinterpret_cast<uintptr_t>(op.ptr) & 15) != 0) return 0;
   const ConvGeom& g = p.g;
   if (p.wv_q) {  // wgrad tap view (k = (n, p, q < wv_q)); out-of-range q / r load as zeros
@@ -222,7 +245,7 @@ int make_tma(GemmParams& p, const Operand& op, CUtensorMap* m) {
       const int seg = std::min(g.C, rb);
       const int r = im2col_map(m, op.ptr, g.N, g.H, g.W, g.C, -g.pw, -g.ph, g.pw - (g.S - 1), g.ph - (g.R - 1),
                                g.sw, g.sh, seg, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
-      if (r) p.mn_seg = seg;
+      if (r) op.seg = seg;
       return r;
     }
   }
@@ -252,7 +275,8 @@ int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_b
   if (bx) {
     // MONET_TMA_MASK (debug): bit 0 enables TMA for A, bit 1 for B (default 3)
     static const int mask = getenv("MONET_TMA_MASK") ? atoi(getenv("MONET_TMA_MASK")) : 3;
-    p.mn_seg = p.wv_q ? p.g.S * p.g.C : p.b.rows_box;
+    p.a.seg = p.a.rows_box;
+    p.b.seg = p.wv_q ? p.g.S * p.g.C : p.b.rows_box;
     // MONET_CHUNK (debug): MMA stages (64 k each) per TMEM accumulation chain
     static const int chunk = getenv("MONET_CHUNK") ? atoi(getenv("MONET_CHUNK")) : 16;
     p.chunk_stages = chunk > 0 ? chunk : 16;
@@ -285,7 +309,7 @@ int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_b
   if (p.splits > 1) {
     long long total = (long long)p.M * p.N;
     splitk_reduce_kernel<<<ew_blocks(total), kEwThreads, 0, st>>>(p.ws, p.c, p.M, p.N, p.ldc, p.splits, accumulate,
-                                                                  p.bias);
+                                                                  p.bias, p.c_trans);
   }
   return last_error();
 }
@@ -410,6 +434,30 @@ WView wgrad_view(int variant, const monet_conv_desc* d) {
 
 size_t align256(size_t b) { return (b + 255) / 256 * 256; }
 
+// Wgrad of a narrow conv (K_out < 128 output channels, e.g. ResNet-50's 64-channel layer1):
+// the natural mapping M = K_out fills only half of every 128-row MMA.  Swapped, the GEMM
+// rows are the filter taps x input channels (M = R*S*C) and the columns the output
+// channels on a 64-wide N tile; the epilogue stores the result transposed into the KRSC
+// weight gradient.  Same tile count and split-K workspace as the natural mapping.
+bool wgrad_swapped(int variant, const monet_conv_desc* d) {
+  return uses_bx3(variant) && d->k < BM && (long long)d->r * d->s * d->c > d->k;
+}
+
+GemmParams wgrad_swapped_params(const monet_conv_desc* d, const float* x, const float* dy, float* dw) {
+  GemmParams p{};
+  p.g = geom(d);
+  const int rsc = d->r * d->s * d->c;
+  p.M = rsc;
+  p.N = d->k;
+  p.Kd = d->n * d->p * d->q;
+  p.a = is_pointwise(d) ? op_mnmajor(x, d->c, d->c) : op_gather(OP_IM2COL_WGRAD, x, rsc);  // A[(tap, c), pix]
+  p.b = op_mnmajor(dy, d->k, d->k);                                                          // B[kout, pix]
+  p.c = dw;
+  p.ldc = rsc;
+  p.c_trans = 1;
+  return p;
+}
+
 // xp[n][hp][wp][c] = x[n][hp - pad_h][wp - pad_w][c], zero outside
 __global__ void wgrad_pad_kernel(const float* __restrict__ x, float* __restrict__ xp, int n, int h, int w, int c,
                                  int hp, int wp, int pad_h, int pad_w) {
@@ -481,14 +529,16 @@ int monet_device_check(void) {
   return (major == 10 && minor == 0) ? 0 : -2;
 }
 
-// debug hook (not part of the product path): the bf16x3 splitters dump the raw
-// operands they consume to these device buffers ([rows][K padded to 64])
+#ifdef MONET_DEBUG
+// debug build only (libmonet_b200_dbg.so; not in include/monet_b200.h): the bf16x3 splitters
+// dump the raw operands they consume ([rows][K padded to 64]); per-role wait counters
 void monet_debug_dump(float* a_dump, float* b_dump) {
   g_dbg_a = a_dump;
   g_dbg_b = b_dump;
 }
 
 void monet_debug_timers(unsigned long long* counters) { g_dbg_t = counters; }
+#endif
 
 int monet_copy_async(void* dst, const void* src, size_t bytes, void* stream) {
   if (bytes == 0) return 0;
@@ -592,8 +642,10 @@ int monet_conv_dgrad(int variant, const monet_conv_desc* d, const float* dy, con
 int monet_conv_wgrad(int variant, const monet_conv_desc* d, const float* x, const float* dy, float* dw,
                      int accumulate, void* ws, size_t ws_bytes, void* stream) {
   if (int e = check_desc(d)) return e;
-  GemmParams p = conv_params(MONET_PASS_WGRAD, d, x, dy, dw);
   const WView v = wgrad_view(variant, d);
+  if (!v.on && wgrad_swapped(variant, d))
+    return launch_gemm(wgrad_swapped_params(d, x, dy, dw), variant, accumulate, ws, ws_bytes, S(stream));
+  GemmParams p = conv_params(MONET_PASS_WGRAD, d, x, dy, dw);
   if (v.on) {
     const size_t part = align256(gemm_ws(variant, p.M, p.N, (int)v.kd, v.n_pitch));
     // a workspace without room for the padded input (callers sizing it by hand) takes the gather path

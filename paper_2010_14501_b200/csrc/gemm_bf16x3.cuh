@@ -358,8 +358,8 @@ struct Loader {
       mbar_arrive_tx(bar, op.rows_box * BKR * 4);
       const int np = k / p.wv_q, pp = np % g.P;
       tma_5d(dst, m, 0, k - np * p.wv_q, tap_r, pp, np / g.P, bar);
-    } else {  // IM2COL_WGRAD: rows (tap, c) in segments of p.mn_seg channels, k = 32 output pixels
-      const int seg = p.mn_seg;
+    } else {  // IM2COL_WGRAD: rows (tap, c) in segments of op.seg channels, k = 32 output pixels
+      const int seg = op.seg;
       mbar_arrive_tx(bar, op.rows_box * BKR * 4);
       const int q = k % g.Q, t = k / g.Q, pp = t % g.P, n = t / g.P;
       const int w0 = q * g.sw - g.pw, h0 = pp * g.sh - g.ph;
@@ -388,7 +388,7 @@ struct Loader {
         if (r >= op.rows_box) continue;  // the B half of a CTA pair covers 64 rows
         row = row0 + r;
         k = kk0 + kr;
-        off = mn_off(r, kr, MODE == OP_IM2COL_WGRAD ? p.mn_seg : op.rows_box);
+        off = mn_off(r, kr, op.seg);
       } else {
         const int r = (sub >> 3) + 8 * i;
         if (r >= op.rows_box) continue;
@@ -561,9 +561,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
           TWAIT(8, mbar_wait(&raw_full[slot], (item / kRawSlots) & 1));
           const uint8_t* rt = raw + slot * kRawBytes;
           float v[32];
-          if constexpr (a_mn) {
+          if constexpr (a_mn) {  // segment-major (mn_off): p.a.seg rows per segment
+            const int seg = p.a.seg, sg = row / seg;
+            const uint8_t* base = rt + sg * (BKR * seg * 4) + (row - sg * seg) * 4;
 #pragma unroll
-            for (int k = 0; k < 32; ++k) v[k] = *reinterpret_cast<const float*>(rt + k * (BM * 4) + row * 4);
+            for (int k = 0; k < 32; ++k) v[k] = *reinterpret_cast<const float*>(base + k * seg * 4);
           } else if (p.a.tma == 3) {  // chunk-major: tap box j holds C channels per row
             const int cb = p.g.C * 4;
 #pragma unroll
@@ -636,7 +638,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
           for (int i = 0; i < kBChunks; ++i) {
             uint32_t off;
             if constexpr (b_mn) {
-              off = mn_off(4 * g, kr0 + kStep * i, p.mn_seg);
+              off = mn_off(4 * g, kr0 + kStep * i, p.b.seg);
             } else {
               off = sw128_offset(rbase + 32 * i, t & 7);
             }
@@ -721,6 +723,20 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
               ld = p.ldc;
             }
             const int ncols = min(min(32, p.N - n0), p.n_pitch - cc * 32);
+            if (p.c_trans && p.epi != EPI_PARTIAL) {
+              // transposed result: column n0 + j is a row of c; the 32 lanes hold consecutive m,
+              // so every j is one coalesced 128-B store (or reduction)
+              float* col = p.c + (long long)n0 * p.ldc + m;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                if (j < ncols) {
+                  if (add_old)
+                    atomicAdd(col + (long long)j * p.ldc, v[j]);
+                  else
+                    col[(long long)j * p.ldc] = v[j];
+                }
+              }
+            } else {
             if (add_bias) {
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] += j < ncols ? __ldg(p.bias + n0 + j) : 0.f;
@@ -748,6 +764,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
                 }
               }
             }
+            }  // not transposed
           }
           __syncwarp();
         }

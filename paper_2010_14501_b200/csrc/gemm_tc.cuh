@@ -51,8 +51,10 @@ struct Operand {
                 //   3 = TMA im2col with C < 32: one box per filter tap, chunk-major raw layout,
                 //   4 = wgrad tap view (C < 32): tiled maps over k = (n, p, q padded to wv_q) --
                 //       A = dy as {kout, q, n*p}, B = the zero-padded input as {s*c, q, r, p, n}
-  int rows_box; // bf16x3 kernel: rows of this operand one CTA loads per tile (128, or 64 for the
-                //   B half of a CTA pair)
+  int rows_box; // bf16x3 kernel: rows of this operand one CTA loads per tile (128, or 64 for a
+                //   64-wide N tile)
+  int seg;      // bf16x3 kernel, MN-major operands: rows per segment of the raw smem layout
+                //   (rows_box, or C when a wgrad im2col tile spans several filter taps)
 };
 
 enum EpiMode : int { EPI_STORE = 0, EPI_ACCUM = 1, EPI_PARTIAL = 2 };
@@ -80,7 +82,8 @@ struct GemmParams {
   int kb_per_split;
   int m_tiles, n_tiles;
   int split_tf32;   // 1: 3xTF32 (hi/lo), 0: plain tf32
-  int mn_seg;       // bf16x3: rows per segment of the MN-major raw B layout (128, or C for wgrad)
+  int c_trans;      // bf16x3: element (m, n) of the result is stored at c[n * ldc + m] (the swapped
+                    //   wgrad of narrow convs: rows = (tap, c), columns = output channels, dw is KRSC)
   PhaseInfo ph;     // bf16x3: strided dgrad phase (ph.on == 0 otherwise)
   int chunk_stages; // bf16x3: MMA stages accumulated in TMEM before a flush to fp32 memory
   int n_pitch;      // output columns per n-tile (BN, or R-segments x S*C for the wgrad tap view)
@@ -565,15 +568,24 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32_kernel(const GemmParams
 
 // Deterministic split-K reduction: out[m, n] (=|+=) sum_{s=0..S-1} ws[s, m, n].
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, float* __restrict__ out, int M, int N,
-                                     long long ldc, int splits, int accumulate, const float* __restrict__ bias) {
+                                     long long ldc, int splits, int accumulate, const float* __restrict__ bias,
+                                     int trans) {
   const long long total = (long long)M * N;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
+    long long m, n;
+    if (trans) {  // out[n][m]: walk m fastest so the stores coalesce
+      n = i / M;
+      m = i - n * M;
+    } else {
+      m = i / N;
+      n = i - m * N;
+    }
+    const long long e = m * N + n;
     float s = 0.f;
-    for (int k = 0; k < splits; ++k) s += ws[(long long)k * total + i];
-    const long long m = i / N, n = i - m * N;
+    for (int k = 0; k < splits; ++k) s += ws[(long long)k * total + e];
     if (bias) s += bias[n];
-    float* o = out + m * ldc + n;
+    float* o = trans ? out + n * ldc + m : out + m * ldc + n;
     *o = accumulate ? (*o + s) : s;
   }
 }

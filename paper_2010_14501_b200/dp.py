@@ -18,13 +18,27 @@ per-GPU budget.  The only exchange is the gradient all-reduce:
 * `finish()` (enqueued before SGD) waits for the outstanding reductions; the
   1/world average is folded into the SGD kernel's ``grad_scale``.
 
+Two backends issue the bucket all-reduces:
+
+* ``native`` (default on CUDA with an NCCL process group): the library's own
+  communicator (include/monet_b200.h, csrc/comm.cu).  `monet_allreduce_bucket`
+  forks the bucket's NCCL all-reduce onto a comm stream after the producing
+  kernels and `monet_comm_join` joins it back before SGD -- plain stream
+  operations in the plan's call list, so the whole data-parallel step is
+  captured into one CUDA graph (no Python on the step's path);
+* ``torch``: `torch.distributed.all_reduce(async_op=True)` from a Python call
+  in the plan (any backend: gloo for the CPU and one-GPU multi-process tests);
+  not graph-capturable.
+
 NCCL's internal buffers live outside the budgeted arena and are reported
-separately by the bench.  The same code runs on gloo (CPU tensors) for the
-world-size-2 tests.
+separately by the bench.
 """
 
 from __future__ import annotations
 
+import ctypes as C
+
+import torch
 import torch.distributed as dist
 
 __all__ = ["DataParallel", "plan_buckets", "bucket_ranges"]
@@ -65,10 +79,17 @@ def plan_buckets(net, bucket_bytes: int = 25 << 20):
 
 
 class DataParallel:
-    def __init__(self, runtime, group=None, bucket_bytes: int = 25 << 20):
+    def __init__(self, runtime, group=None, bucket_bytes: int = 25 << 20, backend: str = "auto"):
         self.rt = runtime
         self.group = group
         self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if backend == "auto":
+            on_cuda = isinstance(getattr(runtime, "grads", None), torch.Tensor) and runtime.grads.is_cuda
+            backend = "native" if on_cuda and dist.get_backend(group) == "nccl" else "torch"
+        if backend not in ("native", "torch"):
+            raise ValueError(f"unknown DataParallel backend {backend!r}")
+        self.backend = backend
         runtime.grad_scale = 1.0 / self.world
         runtime.comm = self
         self.buckets = plan_buckets(runtime.net, bucket_bytes)
@@ -76,6 +97,54 @@ class DataParallel:
         for a, b, node in self.buckets:
             self.by_node.setdefault(node, []).append((a, b))
         self.works = []
+        self.handle = None
+        if backend == "native":
+            self._init_native()
+
+    # ------------------------------------------------------------ native communicator
+    def _init_native(self):
+        from . import _native
+
+        lib = _native.lib().dll
+        uid = (C.c_char * lib.monet_comm_unique_id_bytes())()
+        if self.rank == 0:
+            rc = lib.monet_comm_unique_id(uid)
+            if rc:
+                raise _native.NativeError(f"monet_comm_unique_id failed ({rc})")
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=dist.get_global_rank(self.group, 0) if self.group else 0,
+                                   group=self.group)
+        uid = (C.c_char * len(box[0])).from_buffer_copy(box[0])
+        h = C.c_void_p()
+        rc = lib.monet_comm_init(uid, self.rank, self.world, C.byref(h))
+        if rc:
+            raise _native.NativeError(f"monet_comm_init failed ({rc})")
+        self.handle = h
+        self._lib = lib
+
+    def close(self):
+        if self.handle is not None:
+            self._lib.monet_comm_destroy(self.handle)
+            self.handle = None
+
+    @property
+    def capturable(self) -> bool:
+        """The step's calls are all stream operations (CUDA-graph capturable)."""
+        return self.backend == "native"
+
+    def bucket_calls(self, node: int) -> list:
+        """Plan entries that start the all-reduce of every bucket `node`'s backward completes."""
+        if self.backend == "native":
+            g = self.rt.grads
+            return [("k", self._lib.monet_allreduce_bucket,
+                     (self.handle, g.data_ptr() + 4 * a, b - a, None)) for a, b in self.by_node.get(node, ())]
+        return [("py", lambda node=node: self.bucket_ready(node))]
+
+    def finish_calls(self) -> list:
+        """Plan entries that order the optimizer after every outstanding reduction."""
+        if self.backend == "native":
+            return [("k", self._lib.monet_comm_join, (self.handle, None))]
+        return [("py", self.finish)]
 
     def ready_nodes(self):
         return set(self.by_node)

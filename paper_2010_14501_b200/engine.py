@@ -198,8 +198,9 @@ class Runtime:
     def capture(self, plan: "Plan"):
         """Capture the whole training step into a CUDA graph (plan.graph); the
         kernels' device pointers are static because the arena is planned."""
-        if self.comm is not None:
-            raise RuntimeError("CUDA-graph capture with a Python-side collective is not supported")
+        if self.comm is not None and not getattr(self.comm, "capturable", False):
+            raise RuntimeError("CUDA-graph capture needs the native (stream-ordered) DataParallel backend; "
+                               "the torch.distributed backend issues its all-reduces from Python")
         self.run(plan)  # first launches set kernel attributes outside capture
         torch.cuda.synchronize(self.device)
         graph = torch.cuda.CUDAGraph()
@@ -390,7 +391,7 @@ class Runtime:
         if self.comm is not None and op.id in self.comm.ready_nodes():
             # this stage finalizes a gradient bucket: start its all-reduce now (async,
             # ordered after the kernels above) so it overlaps the remaining stages
-            out.append(("py", lambda node=op.id: self.comm.bucket_ready(node)))
+            out += self.comm.bucket_calls(op.id)
         return out
 
     def _bind_backward(self, s, op, P, ptrs):
@@ -572,7 +573,7 @@ class Runtime:
     def _bind_optimizer(self):
         calls = []
         if self.comm is not None:
-            calls.append(("py", self.comm.finish))  # SGD waits for the bucket reductions
+            calls += self.comm.finish_calls()  # SGD waits for the bucket reductions
         calls.append(("k", self.lib.dll.monet_sgd_step,
                       (self.params.data_ptr(), self.grads.data_ptr(), self.mom.data_ptr(), self.params.numel(),
                        C.c_float(self.lr), C.c_float(self.momentum), C.c_float(self.weight_decay),

@@ -22,7 +22,7 @@ import torch
 
 from . import _native
 
-__all__ = ["profile", "profile_network"]
+__all__ = ["profile", "profile_network", "profile_variant"]
 
 
 class _Bench:
@@ -55,46 +55,6 @@ class _Bench:
     def check(self, rc):
         if rc != 0:
             raise _native.NativeError(f"profiled kernel failed with code {rc}")
-
-
-def _conv_calls(bx: _Bench, net, op, variant: str):
-    """(fwd closure, bwd closure, fwd ws, bwd ws) of a conv variant."""
-    lib, sp = bx.lib, bx.sp
-    d = net.conv_desc(op)
-    v = _native.CONV_VARIANTS[variant]
-    xin = net.op(op.deps[0])
-    x = bx.buf(xin.nbytes)
-    w = bx.buf(4 * op.attrs["r"] * op.attrs["s"] * xin.shape[3] * op.shape[3])
-    y = bx.buf(op.nbytes)
-    dy = bx.buf(op.nbytes)
-    dx = bx.buf(xin.nbytes)
-    dw = bx.buf(w.numel() * 4)
-    ws_f = lib.monet_conv_ws_bytes(v, 0, C.byref(d))
-    ws_b = lib.monet_conv_ws_bytes(v, 3, C.byref(d))
-    ws = bx.buf(max(ws_f, ws_b))
-    need_dx = xin.kind != "input"
-    bias = "bias" in op.params
-    if bias:
-        b, db = bx.buf(4 * op.shape[3]), bx.buf(4 * op.shape[3])
-        rows = op.numel // op.shape[3]
-        scratch = bx.buf(lib.monet_bn_scratch_bytes(rows, op.shape[3]))
-
-    def fwd():
-        if bias:
-            bx.check(lib.monet_conv_fwd_bias(v, C.byref(d), x.data_ptr(), w.data_ptr(), b.data_ptr(), y.data_ptr(),
-                                             ws.data_ptr(), ws_f, sp))
-            return
-        bx.check(lib.monet_conv_fwd(v, C.byref(d), x.data_ptr(), w.data_ptr(), y.data_ptr(), ws.data_ptr(), ws_f, sp))
-
-    def bwd():
-        if need_dx:
-            bx.check(lib.monet_conv_dgrad(v, C.byref(d), dy.data_ptr(), w.data_ptr(), dx.data_ptr(), 0,
-                                          ws.data_ptr(), ws_b, sp))
-        bx.check(lib.monet_conv_wgrad(v, C.byref(d), x.data_ptr(), dy.data_ptr(), dw.data_ptr(), 0, ws.data_ptr(),
-                                      ws_b, sp))
-        if bias:
-            bx.check(lib.monet_bias_grad(dy.data_ptr(), db.data_ptr(), rows, op.shape[3], 0, scratch.data_ptr(), sp))
-    return fwd, bwd
 
 
 def _convT_calls(bx: _Bench, net, op, variant: str):
@@ -140,30 +100,8 @@ def _local_calls(bx: _Bench, net, op):
         return out
     xin = net.op(op.deps[0])
     x, y, dy, dx = bx.buf(xin.nbytes), bx.buf(op.nbytes), bx.buf(op.nbytes), bx.buf(xin.nbytes)
-    if kind == "relu":
-        mask = bx.buf((n + 31) // 32 * 4)
-        out[("fwd", "relu")] = lambda: bx.check(lib.monet_relu_fwd(x.data_ptr(), y.data_ptr(), mask.data_ptr(), n, sp))
-        out[("bwd", "bwd-in")] = lambda: bx.check(lib.monet_relu_bwd_in(x.data_ptr(), dy.data_ptr(), dx.data_ptr(), n,
-                                                                         0, sp))
-        out[("bwd", "bwd-out")] = lambda: bx.check(lib.monet_relu_bwd_out(y.data_ptr(), dy.data_ptr(), dx.data_ptr(),
-                                                                           n, 0, sp))
-        out[("bwd", "bwd-mask")] = lambda: bx.check(lib.monet_relu_bwd_mask(mask.data_ptr(), dy.data_ptr(),
-                                                                             dx.data_ptr(), n, 0, sp))
-    elif kind == "bn":
-        c = op.shape[-1]
-        rows = n // c
-        ch = [bx.buf(4 * c) for _ in range(8)]  # gamma beta mean invstd rmean rvar dgamma dbeta
-        for t in ch[:4]:
-            t.abs_().add_(0.5)
-        scratch = bx.buf(lib.monet_bn_scratch_bytes(rows, c))
-        g_, b_, m_, s_, rm, rv, dg, db = (t.data_ptr() for t in ch)
-        out[("fwd", "bn")] = lambda: bx.check(lib.monet_bn_fwd_train(
-            x.data_ptr(), y.data_ptr(), g_, b_, m_, s_, rm, rv, rows, c, C.c_float(1e-5), C.c_float(0.1), 1,
-            scratch.data_ptr(), sp))
-        out[("bwd", "bwd-in")] = lambda: bx.check(lib.monet_bn_bwd_in(
-            x.data_ptr(), dy.data_ptr(), dx.data_ptr(), 0, g_, m_, s_, dg, db, rows, c, scratch.data_ptr(), sp))
-        out[("bwd", "bwd-out")] = lambda: bx.check(lib.monet_bn_bwd_out(
-            y.data_ptr(), dy.data_ptr(), dx.data_ptr(), 0, g_, b_, s_, dg, db, rows, c, scratch.data_ptr(), sp))
+    if kind in ("relu", "bn", "conv"):
+        raise ValueError(f"{kind} is profiled through monet_profile_variant")
     elif kind in ("bnrelu", "bnrelu6"):
         c = op.shape[-1]
         rows = n // c
@@ -305,6 +243,32 @@ def _local_calls(bx: _Bench, net, op):
     return out
 
 
+def profile_variant(net, op, pss: str, variant: str, iters: int = 5, stream=None) -> tuple[int, int]:
+    """(ns per launch, workspace bytes) of one variant through the C-ABI profiler entry
+    point monet_profile_variant (csrc/profile.cu): conv fwd / bwd, ReLU, BN, fused BN+ReLU."""
+    d = _native.ProfDesc()
+    d.op = _native.PROF_OP[op.kind]
+    d.pass_ = _native.PASS["fwd"] if pss == "fwd" else _native.PASS["bwd"]
+    if op.kind == "conv":
+        d.conv = net.conv_desc(op)
+        d.conv_needs_dx = int(net.op(op.deps[0]).kind != "input")
+        v = _native.CONV_VARIANTS[variant]
+    else:
+        d.c = op.shape[-1]
+        d.rows = op.numel // d.c
+        v = 0 if pss == "fwd" else _native.PROF_BWD[variant]
+    ns, ws = C.c_int64(0), C.c_size_t(0)
+    if stream is None:
+        stream = torch.cuda.current_stream().cuda_stream
+    rc = _native.lib().dll.monet_profile_variant(C.byref(d), v, iters, C.byref(ns), C.byref(ws), C.c_void_p(stream))
+    if rc != 0:
+        raise _native.NativeError(f"monet_profile_variant({op.kind} {pss} {variant}) failed with code {rc}")
+    return int(ns.value), int(ws.value)
+
+
+_NATIVE_PROFILED = ("conv", "relu", "bn", "bnrelu")
+
+
 def _signature(net, op):
     ins = tuple((net.op(j).kind == "input", net.op(j).shape) for j in op.deps)
     attrs = tuple(sorted((k, v) for k, v in op.attrs.items() if isinstance(v, (int, float, str))))
@@ -321,12 +285,21 @@ def profile_network(net, device="cuda:0", warmup=2, iters=5, reps=3, log=None) -
         sig = _signature(net, op)
         if sig not in cache:
             res = {}
-            if op.kind in ("conv", "convT"):
+            if op.kind in _NATIVE_PROFILED:  # through the C-ABI profiler entry point
+                for name, ws in fv:
+                    ns, ws_k = profile_variant(net, op, "fwd", name, iters, bx.stream.cuda_stream)
+                    assert ws_k == ws, (op.name, name, ws_k, ws)
+                    res[("fwd", name)] = ns
+                for name, ws, _ in bv:
+                    ns, ws_k = profile_variant(net, op, "bwd", name, iters, bx.stream.cuda_stream)
+                    assert op.kind != "conv" or ws_k == ws, (op.name, name, ws_k, ws)
+                    res[("bwd", name)] = ns
+            elif op.kind == "convT":
                 for name, _ in fv:
-                    f, _b = (_convT_calls if op.kind == "convT" else _conv_calls)(bx, net, op, name)
+                    f, _b = _convT_calls(bx, net, op, name)
                     res[("fwd", name)] = bx.time_ns(f)
                 for name, _, _ in bv:
-                    _f, b = (_convT_calls if op.kind == "convT" else _conv_calls)(bx, net, op, name)
+                    _f, b = _convT_calls(bx, net, op, name)
                     res[("bwd", name)] = bx.time_ns(b)
             else:
                 calls = _local_calls(bx, net, op)

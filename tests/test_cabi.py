@@ -73,3 +73,18 @@ def test_arena_plan_overlap_and_cap(lib):
     from paper_2010_14501_b200.engine import BudgetExceeded
     with pytest.raises(BudgetExceeded):
         place_blocks(blocks, capacity=1000)
+
+
+def test_public_abi_has_no_debug_hooks(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_native.LIB_PATH)], capture_output=True, text=True,
+                         check=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines() if line.strip()}
+    assert not [s for s in exported if s.startswith("monet_debug")]
+    assert "monet_profile_variant" in exported
+
+
+def test_prof_desc_layout_matches_header():
+    # monet_prof_desc: op, pass, conv (13 ints), conv_needs_dx, then int64 rows (8-aligned), c
+    assert C.sizeof(_native.ConvDesc) == 13 * 4
+    assert _native.ProfDesc.rows.offset == 8 + 13 * 4 + 4
+    assert C.sizeof(_native.ProfDesc) == 80

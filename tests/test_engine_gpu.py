@@ -31,13 +31,13 @@ GOLD = Path(__file__).resolve().parent / "golden"
 REL = 1e-4
 
 
-def _assert_step_parity(rt, st, free=None):
-    """Every parameter gradient and SGD-updated weight (and BN running statistic, given
-    the free-running oracle) within REL, per tensor (oracle/parity.py:step_parity:
+def _assert_step_parity(rt, st):
+    """Every parameter gradient, SGD-updated weight and BN running statistic within REL,
+    per tensor (oracle/parity.py:step_parity:
     tensors whose exact value is ~0 -- e.g. the bias gradient of a BN feeding a 1x1
     conv and another BN in MobileNet-V2's linear bottlenecks -- are judged against
-    1e-3 of the largest tensor of their kind instead of their own rounding noise)."""
-    rep = step_parity(rt, st, free)
+    1 % of the largest tensor of their kind instead of their own rounding noise)."""
+    rep = step_parity(rt, st)
     assert rep["grad"] and rep["param"]
     for kind, v in rep.items():
         bad = sorted(((e, n) for e, n in v if not e <= REL), reverse=True)
@@ -228,7 +228,7 @@ def test_mobilenet_v2_engine(cuda, fuse):
     assert abs(rt.loss_value() - loss) <= REL * abs(loss)
     st = CpuState(net)
     run_step(st, doc, x, y, forced=acts, forced_stats=gpu_stats(rt))
-    _assert_step_parity(rt, st, free)
+    _assert_step_parity(rt, st)
 
 
 @pytest.mark.parametrize("fuse", [False, True])
@@ -263,7 +263,7 @@ def test_googlenet_engine(cuda, fuse):
     assert abs(rt.loss_value() - loss) <= REL * abs(loss)
     st = CpuState(net)
     run_step(st, doc, x, y, forced=acts, forced_stats=gpu_stats(rt))
-    _assert_step_parity(rt, st, free)
+    _assert_step_parity(rt, st)
 
 
 def test_unet_engine(cuda):
@@ -295,7 +295,7 @@ def test_unet_engine(cuda):
     assert abs(rt.loss_value() - loss) <= REL * abs(loss)
     st = CpuState(net)
     run_step(st, doc, x, y, forced=acts, forced_stats=gpu_stats(rt))
-    _assert_step_parity(rt, st, free)
+    _assert_step_parity(rt, st)
 
 
 def test_cli_train_execute_exit_codes(cuda, tmp_path):

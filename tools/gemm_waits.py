@@ -16,7 +16,7 @@ d = N.conv_desc(n, h, w, c, k, r, s, stride, pad)
 x = torch.randn(n, h, w, c, device=dev)
 wt = torch.randn(k, r, s, c, device=dev)
 y = torch.randn(n, d.p, d.q, k, device=dev)
-lib = N.lib()
+lib = N.debug_lib()  # the debug build carries the GEMM hooks
 v = N.CONV_VARIANTS["splitk"]
 pid = N.PASS[pss]
 wsb = lib.conv_ws_bytes(v, pid, d)

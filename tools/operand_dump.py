@@ -18,7 +18,7 @@ M, Kd = n * d.p * d.q, r * s * c
 kpad = (Kd + 63) // 64 * 64
 da = torch.full((M, kpad), 777.0, device=dev)
 db = torch.full((k, kpad), 777.0, device=dev)
-lib = N.lib()
+lib = N.debug_lib()  # the debug build carries the GEMM hooks
 lib.dll.monet_debug_dump(da.data_ptr(), db.data_ptr())
 xd, wd = x.to(dev), wt.to(dev)
 y = torch.empty(n, d.p, d.q, k, device=dev)
