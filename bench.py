@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--budget-gib", type=float, default=8.0)
     ap.add_argument("--no-fuse", dest="fuse", action="store_false",
                     help="separate BN and ReLU operators (default: fused BN+ReLU ops, tracer fuse=True)")
+    ap.add_argument("--split", action="store_true",
+                    help="conv backward split into dgrad / wgrad graph nodes (tracer.split_conv_backward)")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels from Python instead of a CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-overhead-run", action="store_true", help="skip timing the store-everything schedule")
@@ -59,7 +61,7 @@ def load_or_plan(net, g, cat, budget, arch, batch, image, gib):
     import paper_2010_14501_b200 as M
     from paper_2010_14501_b200.planner import plan_schedule
 
-    path = ROOT / "schedules" / f"{arch}{'_fused' if net.fused else ''}_b{batch}_{image}_{gib:g}gib.json"
+    path = ROOT / "schedules" / f"{stem(arch, net)}_b{batch}_{image}_{gib:g}gib.json"
     digest = lambda d: hashlib.sha256(json.dumps(d, sort_keys=True).encode()).hexdigest()[:16]  # noqa: E731
     if path.exists():
         doc = json.loads(path.read_text())
@@ -71,11 +73,18 @@ def load_or_plan(net, g, cat, budget, arch, batch, image, gib):
     return sched, info, "planned at startup"
 
 
+def stem(arch, net=None, fused=None, split=None):
+    """File-name stem of a workload: arch[_fused][_split] (schedules/, profiles/, oracle/specs/)."""
+    fused = net.fused if net is not None else fused
+    split = net.split if net is not None else split
+    return f"{arch}{'_fused' if fused else ''}{'_split' if split else ''}"
+
+
 def measured_catalog(net, args):
     """The frozen on-device profile (tools/profile_catalog.py) when it matches this graph."""
     import hashlib
 
-    path = ROOT / "profiles" / f"catalog_{args.arch}{'_fused' if net.fused else ''}_b{args.batch}_{args.image}.json"
+    path = ROOT / "profiles" / f"catalog_{stem(args.arch, net)}_b{args.batch}_{args.image}.json"
     if not path.exists():
         return None
     doc = json.loads(path.read_text())
@@ -181,10 +190,15 @@ def kernel_roofline(rt, plan, net, peaks):
         ms = a.elapsed_time(b)
         total_t += ms
         op = net.op(s.node)
-        if op.kind in ("conv", "convT"):
-            f = conv_flops(net, op)
-            if s.kind == "backward":
-                f *= 1 if net.op(op.deps[0]).kind == "input" else 2
+        if op.kind in ("conv", "convT", "wgrad"):
+            if op.kind == "wgrad":  # a split conv's weight gradient (no forward work)
+                f = conv_flops(net, net.op(op.attrs["conv"])) if s.kind == "backward" else 0.0
+            else:
+                f = conv_flops(net, op)
+            if s.kind == "backward" and op.kind != "wgrad":
+                # dgrad (unless the input has no gradient) + wgrad, or dgrad alone when split
+                dg = 0 if net.op(op.deps[0]).kind == "input" else 1
+                f *= dg + (0 if op.attrs.get("split") else 1)
             conv_t += ms
             conv_f += f
             n_conv += 1
@@ -224,10 +238,12 @@ def _spec_and_schedule(args):
     plain JSON, so the CPU arms never import the product package or map its .so."""
     from oracle import netspec
 
-    fused = args.fuse
-    spec = netspec.spec_path(args.arch, fused, args.batch, args.image)
-    sched = ROOT / "schedules" / f"{args.arch}{'_fused' if fused else ''}_b{args.batch}_{args.image}_{args.budget_gib:g}gib.json"
-    cat = ROOT / "profiles" / f"catalog_{args.arch}{'_fused' if fused else ''}_b{args.batch}_{args.image}.json"
+    # architectures without BN+ReLU pairs (VGG-16) trace to the same graph with or without fusion
+    fused = args.fuse and netspec.spec_path(args.arch, True, args.batch, args.image, args.split).exists()
+    spec = netspec.spec_path(args.arch, fused, args.batch, args.image, args.split)
+    name = stem(args.arch, fused=fused, split=args.split)
+    sched = ROOT / "schedules" / f"{name}_b{args.batch}_{args.image}_{args.budget_gib:g}gib.json"
+    cat = ROOT / "profiles" / f"catalog_{name}_b{args.batch}_{args.image}.json"
     missing = [str(p.relative_to(ROOT)) for p in (spec, sched, cat) if not p.exists()]
     if missing:
         raise FileNotFoundError(f"frozen inputs missing: {missing} (tools/freeze_netspec.py, tools/make_schedules.py)")
@@ -262,6 +278,7 @@ def cpu_baseline_run(args, steps=2, warmup=1):
         loss = run_step(st, sdoc["schedule"], x, y)
     dt = (time.perf_counter() - t) / steps
     return {"value": round(n / dt, 3), "unit": "img/s", "cores": torch.get_num_threads(), "kind": "port",
+            "schedule": str(sched_path.relative_to(ROOT)),
             "sample": f"{args.arch} batch {n} at {hw[0]}x{hw[1]}: one training step replaying the committed "
                       f"{args.budget_gib:g} GiB schedule ({sched_path.relative_to(ROOT)}) with the torch-CPU fp32 "
                       f"oracle port, mean of {steps} step(s) after {warmup} warm-up; synthetic seeded weights "
@@ -335,9 +352,9 @@ def reference_arm(args):
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
            "data": "synthetic N(0,1) images, uniform labels; seeded synthetic weights",
            "config": {"workload": f"{args.arch} {hw[0]}x{hw[1]} batch {args.batch}/GPU, {args.budget_gib:g} GiB "
-                                  f"per-GPU budget, MONeT schedule (schedules/{args.arch}"
-                                  f"{'_fused' if args.fuse else ''}_b{args.batch}_{args.image}_{args.budget_gib:g}gib"
-                                  f".json)" + (", fused BN+ReLU operators" if args.fuse else ""),
+                                  f"per-GPU budget, MONeT schedule ({res['schedule']})"
+                                  + (", fused BN+ReLU operators" if "_fused" in res["schedule"] else "")
+                                  + (", conv backward split" if args.split else ""),
                       "model": args.arch, "global_batch": args.batch, "per_gpu_batch": args.batch,
                       "image": args.image, "budget_bytes": int(args.budget_gib * (1 << 30)),
                       "parallelism": "host cores"},
@@ -370,7 +387,8 @@ def ours_arm(args):
 
     gib = args.budget_gib
     budget = int(gib * (1 << 30))
-    net = build_network(args.arch, args.batch, image_arg(args.image), num_classes=n_classes(args.arch), fuse=args.fuse)
+    net = build_network(args.arch, args.batch, image_arg(args.image), num_classes=n_classes(args.arch), fuse=args.fuse,
+                        split=args.split)
     gdoc = net.graph_doc()
     g = M.load_graph(gdoc)
     cat = M.load_catalog(measured_catalog(net, args) or net.catalog_doc(), g)
@@ -437,13 +455,13 @@ def ours_arm(args):
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1) / args.steps
+    mstats = torch.cuda.memory_stats(dev)  # before anything else is allocated
     t = torch.tensor([ms], device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     value = world * args.batch / (ms * 1e-3)
     loss = rt.loss_value()
-    mstats = torch.cuda.memory_stats(dev)
     free1, _ = torch.cuda.mem_get_info(dev)
     device_mem = {
         # what the process asked the allocator for at its peak during the timed steps
@@ -526,7 +544,8 @@ def ours_arm(args):
             "data": "synthetic N(0,1) images, uniform labels; random-init torchvision weights (seed 0)",
             "config": {"workload": f"{args.arch} {hw[0]}x{hw[1]} batch {args.batch}/GPU, "
                                    f"{gib:g} GiB per-GPU budget, MONeT schedule ({source})"
-                                   + (", fused BN+ReLU operators" if args.fuse else ""),
+                                   + (", fused BN+ReLU operators" if net.fused else "")
+                                   + (", conv backward split" if net.split else ""),
                        "model": args.arch, "global_batch": world * args.batch, "per_gpu_batch": args.batch,
                        "image": args.image, "budget_bytes": budget, "parallelism": f"dp{world}",
                        "cuda_graph": use_graph,

@@ -82,8 +82,9 @@ int monet_comm_join(monet_comm* comm, void* stream);
  * units.py:61-62 forbids fractional costs in a catalog), *ws_bytes = the workspace the
  * variant takes from the arena (conv: monet_conv_ws_bytes of that variant and pass; 0 for
  * the local operators, whose scratch lives in the fixed region).
- *   op  MONET_OP_CONV   pass FWD (forward) or BWD (dgrad, if conv_needs_dx, + wgrad); variant
- *                       = MONET_CONV_*; desc in `conv`
+ *   op  MONET_OP_CONV   pass FWD (forward), BWD (dgrad, if conv_needs_dx, + wgrad), or DGRAD /
+ *                       WGRAD alone (a split conv's two backward nodes); variant = MONET_CONV_*;
+ *                       desc in `conv`
  *       MONET_OP_RELU   pass FWD (with the 1-bit mask) or BWD with variant MONET_BWD_IN /
  *                       _OUT / _MASK; rows * c elements
  *       MONET_OP_BN     pass FWD (train: statistics + apply) or BWD (MONET_BWD_IN / _OUT)

@@ -120,7 +120,9 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
         nonlocal loss_val
         xs = [x_of(j) for j in op.deps]
         extra = None
-        if op.kind == "input":
+        if op.kind == "wgrad":  # split conv's weight-gradient anchor: no forward tensor
+            y = torch.zeros(0, dtype=dt)
+        elif op.kind == "input":
             c_pad = op.shape[3]
             y = torch.zeros(images.shape[0], c_pad, images.shape[2], images.shape[3], dtype=dt)
             y[:, :images.shape[1]] = images.to(dt)
@@ -205,12 +207,27 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
     def bwd(op, impl, created):
         if op.kind == "input":
             return
+        if op.kind == "wgrad":  # split conv: dW from the conv input and the conv's output gradient
+            conv = net.op(op.attrs["conv"])
+            a = conv.attrs
+            w = P[(conv.id, "weight")]
+            state.grads[(conv.id, "weight")] = torch.nn.grad.conv2d_weight(x_of(conv.deps[0]), w.shape, grad[conv.id],
+                                                                          a["stride"], a["pad"])
+            return
         dy = grad[op.id]
         if op.kind == "conv":
             a = op.attrs
             j = op.deps[0]
-            x = x_of(j)
             w = P[(op.id, "weight")]
+            if a.get("split"):  # dgrad only: reads dy and w, never x
+                in_shape = net.op(j).shape
+                shp = (in_shape[0], in_shape[3], in_shape[1], in_shape[2])
+                if net.grad_bytes(net.op(j)) > 0:
+                    put_grad(j, torch.nn.grad.conv2d_input(shp, w, dy, a["stride"], a["pad"]), created)
+                if (op.id, "bias") in P:
+                    state.grads[(op.id, "bias")] = dy.sum(dim=(0, 2, 3))
+                return
+            x = x_of(j)
             if net.grad_bytes(net.op(j)) > 0:
                 put_grad(j, torch.nn.grad.conv2d_input(x.shape, w, dy, a["stride"], a["pad"]), created)
             state.grads[(op.id, "weight")] = torch.nn.grad.conv2d_weight(x, w.shape, dy, a["stride"], a["pad"])

@@ -40,6 +40,10 @@ class SpecOp:
     def numel(self) -> int:
         return int(math.prod(self.shape)) if self.shape else 1
 
+    @property
+    def nbytes(self) -> int:
+        return 0 if self.kind == "wgrad" else (self.numel * 4 + 15) // 16 * 16
+
 
 class SpecNet:
     def __init__(self, doc: dict, seed: int = 0):
@@ -69,12 +73,13 @@ class SpecNet:
         self.n = len(self.ops)
         self._bwd = {int(k): v for k, v in doc["bwd_deps"].items()}
         self.fused = any(op.kind in ("bnrelu", "bnrelu6", "bnaddrelu") for op in self.ops)
+        self.split = any(op.kind == "wgrad" for op in self.ops)
 
     def op(self, i: int) -> SpecOp:
         return self.ops[i - 1]
 
     def grad_bytes(self, op: SpecOp) -> int:
-        return 0 if op.kind == "input" else (op.numel * 4 + 15) // 16 * 16
+        return 0 if op.kind in ("input", "wgrad") else op.nbytes
 
     def bwd_deps(self, k: int, impl: str) -> list:
         return list(self._bwd[k][impl])
@@ -84,8 +89,8 @@ class SpecNet:
         return logits.numel // logits.shape[-1]
 
 
-def spec_path(arch: str, fused: bool, batch: int, image: str) -> Path:
-    return SPECS / f"{arch}{'_fused' if fused else ''}_b{batch}_{image}.json"
+def spec_path(arch: str, fused: bool, batch: int, image: str, split: bool = False) -> Path:
+    return SPECS / f"{arch}{'_fused' if fused else ''}{'_split' if split else ''}_b{batch}_{image}.json"
 
 
 def load(path, seed: int = 0) -> SpecNet:

@@ -24,7 +24,7 @@ def capture(rt, plan):
         if s.kind == "backward":
             return
         op = net.op(s.node)
-        if op.kind == "xent":
+        if op.kind in ("xent", "wgrad"):  # the loss scalar; split-conv anchors hold no tensor
             return
         v = _view(rt, plan.step_ptrs[i][("a", s.node)], op.shape).clone()
         if s.kind == "forward":

@@ -25,11 +25,20 @@ def analytic_cost(net, op, pass_, name) -> int:
         flops = 2.0 * x.numel * op.shape[3] * op.attrs["r"] * op.attrs["s"]
         return _ns(flops if pass_ == "fwd" else 2 * flops, 4.0 * (x.numel + n) * (1 if pass_ == "fwd" else 2),
                    launches=1 if pass_ == "fwd" else 3)
+    if op.kind == "wgrad":  # split conv: the weight gradient (r x, r dy)
+        if pass_ == "fwd":
+            return 1
+        conv = net.op(op.attrs["conv"])
+        x = net.op(conv.deps[0])
+        return _ns(2.0 * conv.numel * x.shape[3] * conv.attrs["r"] * conv.attrs["s"], 4.0 * (x.numel + conv.numel))
     if op.kind == "conv":
         x = net.op(op.deps[0])
         flops = 2.0 * n * x.shape[3] * op.attrs["r"] * op.attrs["s"]
         if pass_ == "fwd":
             return _ns(flops, 4.0 * (x.numel + n))
+        if op.attrs.get("split"):  # dgrad only (+ bias gradient)
+            bias = 4.0 * n if "bias" in op.params else 0.0
+            return _ns(flops, 4.0 * (x.numel + n) + bias, launches=2)
         passes = 1 if net.op(op.deps[0]).kind == "input" else 2
         bias = 4.0 * n if "bias" in op.params else 0.0  # bias gradient: one more read of dy
         return _ns(passes * flops, 8.0 * (x.numel + n) + bias, launches=3)

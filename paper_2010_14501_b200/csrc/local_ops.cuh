@@ -451,6 +451,23 @@ __global__ void bn_finalize_bwd_kernel(const float* __restrict__ ws, int nblocks
   coef_c[c] = (float)(-k * s1 * inv_m + k * a1 * a0 * s2 * inv_m);
 }
 
+// The apply passes below stream float4 groups of an NHWC [rows, C] tensor with a grid-stride
+// loop that keeps kEwUnroll independent 16-B loads per input in flight per thread (issued
+// before any of them is used): one load at a time leaves ~32 KB per SM in flight, below what
+// HBM3e needs to reach its bandwidth (profiles/ncu_r2.md: bnrelu_apply 4.4 TB/s -> ...).
+constexpr int kEwUnroll = 4;
+
+#define MONET_EW_LOOP_BEGIN(n4)                                                             \
+  const long long ew_stride_ = (long long)gridDim.x * blockDim.x;                            \
+  for (long long ew_i0_ = blockIdx.x * (long long)blockDim.x + threadIdx.x; ew_i0_ < (n4); \
+       ew_i0_ += kEwUnroll * ew_stride_) {
+#define MONET_EW_IDX(u) (ew_i0_ + (long long)(u) * ew_stride_)
+#define MONET_EW_LOOP_END }
+
+MONET_DEV float4 ld4(const float* p, long long i) { return __ldcs(reinterpret_cast<const float4*>(p) + i); }
+MONET_DEV float4 ldc4(const float* p, int q) { return __ldg(reinterpret_cast<const float4*>(p) + q); }
+MONET_DEV void st4(float* p, long long i, float4 v) { reinterpret_cast<float4*>(p)[i] = v; }
+
 // y = (x - mean) * invstd * gamma + beta   (train and replay share this kernel,
 // so a recompute with saved statistics is bit-identical to the first forward)
 __global__ void bn_apply_kernel(const float* __restrict__ x, float* y, const float* __restrict__ mean,
@@ -458,20 +475,25 @@ __global__ void bn_apply_kernel(const float* __restrict__ x, float* y, const flo
                                 const float* __restrict__ beta, long long rows, int C) {
   const int cq = C / 4;
   const long long n4 = rows * cq;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
-       i += (long long)gridDim.x * blockDim.x) {
+  MONET_EW_LOOP_BEGIN(n4)
+  float4 v[kEwUnroll];
+#pragma unroll
+  for (int u = 0; u < kEwUnroll; ++u)
+    if (MONET_EW_IDX(u) < n4) v[u] = ld4(x, MONET_EW_IDX(u));
+#pragma unroll
+  for (int u = 0; u < kEwUnroll; ++u) {
+    const long long i = MONET_EW_IDX(u);
+    if (i >= n4) break;
     const int q = (int)(i % cq);
-    float4 v = *reinterpret_cast<const float4*>(x + 4 * i);
-    float4 m = *reinterpret_cast<const float4*>(mean + 4 * q);
-    float4 s = *reinterpret_cast<const float4*>(invstd + 4 * q);
-    float4 g = *reinterpret_cast<const float4*>(gamma + 4 * q);
-    float4 b = *reinterpret_cast<const float4*>(beta + 4 * q);
-    v.x = bn_aff(v.x, m.x, s.x, g.x, b.x);
-    v.y = bn_aff(v.y, m.y, s.y, g.y, b.y);
-    v.z = bn_aff(v.z, m.z, s.z, g.z, b.z);
-    v.w = bn_aff(v.w, m.w, s.w, g.w, b.w);
-    *reinterpret_cast<float4*>(y + 4 * i) = v;
+    const float4 m = ldc4(mean, q), sd = ldc4(invstd, q), g = ldc4(gamma, q), b = ldc4(beta, q);
+    float4 o;
+    o.x = bn_aff(v[u].x, m.x, sd.x, g.x, b.x);
+    o.y = bn_aff(v[u].y, m.y, sd.y, g.y, b.y);
+    o.z = bn_aff(v[u].z, m.z, sd.z, g.z, b.z);
+    o.w = bn_aff(v[u].w, m.w, sd.w, g.w, b.w);
+    st4(y, i, o);
   }
+  MONET_EW_LOOP_END
 }
 
 // dx (=|+=) gamma*invstd*(dy - sum_dy/M - xhat*sum_dyxhat/M) = k*dy + cb*v + cc
@@ -482,26 +504,32 @@ __global__ void bn_bwd_apply_kernel(const float* __restrict__ s, const float* __
                                     long long rows, int C, int accumulate) {
   const int cq = C / 4;
   const long long n4 = rows * cq;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
-       i += (long long)gridDim.x * blockDim.x) {
+  MONET_EW_LOOP_BEGIN(n4)
+  float4 v[kEwUnroll], g[kEwUnroll];
+#pragma unroll
+  for (int u = 0; u < kEwUnroll; ++u)
+    if (MONET_EW_IDX(u) < n4) {
+      v[u] = ld4(s, MONET_EW_IDX(u));
+      g[u] = ld4(dy, MONET_EW_IDX(u));
+    }
+#pragma unroll
+  for (int u = 0; u < kEwUnroll; ++u) {
+    const long long i = MONET_EW_IDX(u);
+    if (i >= n4) break;
     const int q = (int)(i % cq);
-    const float4 v = *reinterpret_cast<const float4*>(s + 4 * i);
-    const float4 g = *reinterpret_cast<const float4*>(dy + 4 * i);
-    const float4 ga = *reinterpret_cast<const float4*>(gamma + 4 * q);
-    const float4 is = *reinterpret_cast<const float4*>(invstd + 4 * q);
-    const float4 cb = *reinterpret_cast<const float4*>(coef_b + 4 * q);
-    const float4 cc = *reinterpret_cast<const float4*>(coef_c + 4 * q);
+    const float4 ga = ldc4(gamma, q), is = ldc4(invstd, q), cb = ldc4(coef_b, q), cc = ldc4(coef_c, q);
     float4 o;
-    o.x = fmaf(ga.x * is.x, g.x, fmaf(cb.x, v.x, cc.x));
-    o.y = fmaf(ga.y * is.y, g.y, fmaf(cb.y, v.y, cc.y));
-    o.z = fmaf(ga.z * is.z, g.z, fmaf(cb.z, v.z, cc.z));
-    o.w = fmaf(ga.w * is.w, g.w, fmaf(cb.w, v.w, cc.w));
+    o.x = fmaf(ga.x * is.x, g[u].x, fmaf(cb.x, v[u].x, cc.x));
+    o.y = fmaf(ga.y * is.y, g[u].y, fmaf(cb.y, v[u].y, cc.y));
+    o.z = fmaf(ga.z * is.z, g[u].z, fmaf(cb.z, v[u].z, cc.z));
+    o.w = fmaf(ga.w * is.w, g[u].w, fmaf(cb.w, v[u].w, cc.w));
     if (accumulate) {
-      const float4 d = *reinterpret_cast<const float4*>(dx + 4 * i);
+      const float4 d = reinterpret_cast<const float4*>(dx)[i];
       o.x += d.x; o.y += d.y; o.z += d.z; o.w += d.w;
     }
-    *reinterpret_cast<float4*>(dx + 4 * i) = o;
+    st4(dx, i, o);
   }
+  MONET_EW_LOOP_END
 }
 
 // Fused BN+ReLU forward apply: z = max((x - mean) * invstd * gamma + beta, 0)
@@ -513,20 +541,25 @@ __global__ void bnrelu_apply_kernel(const float* __restrict__ x, float* z, const
                                     const float* __restrict__ beta, long long rows, int C) {
   const int cq = C / 4;
   const long long n4 = rows * cq;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
-       i += (long long)gridDim.x * blockDim.x) {
+  MONET_EW_LOOP_BEGIN(n4)
+  float4 v[kEwUnroll];
+#pragma unroll
+  for (int u = 0; u < kEwUnroll; ++u)
+    if (MONET_EW_IDX(u) < n4) v[u] = ld4(x, MONET_EW_IDX(u));
+#pragma unroll
+  for (int u = 0; u < kEwUnroll; ++u) {
+    const long long i = MONET_EW_IDX(u);
+    if (i >= n4) break;
     const int q = (int)(i % cq);
-    float4 v = *reinterpret_cast<const float4*>(x + 4 * i);
-    const float4 m = *reinterpret_cast<const float4*>(mean + 4 * q);
-    const float4 s = *reinterpret_cast<const float4*>(invstd + 4 * q);
-    const float4 g = *reinterpret_cast<const float4*>(gamma + 4 * q);
-    const float4 b = *reinterpret_cast<const float4*>(beta + 4 * q);
-    v.x = relu_val<kSix>(bn_aff(v.x, m.x, s.x, g.x, b.x));
-    v.y = relu_val<kSix>(bn_aff(v.y, m.y, s.y, g.y, b.y));
-    v.z = relu_val<kSix>(bn_aff(v.z, m.z, s.z, g.z, b.z));
-    v.w = relu_val<kSix>(bn_aff(v.w, m.w, s.w, g.w, b.w));
-    *reinterpret_cast<float4*>(z + 4 * i) = v;
+    const float4 m = ldc4(mean, q), sd = ldc4(invstd, q), g = ldc4(gamma, q), b = ldc4(beta, q);
+    float4 o;
+    o.x = relu_val<kSix>(bn_aff(v[u].x, m.x, sd.x, g.x, b.x));
+    o.y = relu_val<kSix>(bn_aff(v[u].y, m.y, sd.y, g.y, b.y));
+    o.z = relu_val<kSix>(bn_aff(v[u].z, m.z, sd.z, g.z, b.z));
+    o.w = relu_val<kSix>(bn_aff(v[u].w, m.w, sd.w, g.w, b.w));
+    st4(z, i, o);
   }
+  MONET_EW_LOOP_END
 }
 
 // Fused BN + residual add + ReLU (the last BN of a bottleneck block feeding the join):
@@ -537,21 +570,28 @@ __global__ void bnaddrelu_apply_kernel(const float* __restrict__ x, const float*
                                        int C) {
   const int cq = C / 4;
   const long long n4 = rows * cq;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
-       i += (long long)gridDim.x * blockDim.x) {
+  MONET_EW_LOOP_BEGIN(n4)
+  float4 v[kEwUnroll], k[kEwUnroll];
+#pragma unroll
+  for (int u = 0; u < kEwUnroll; ++u)
+    if (MONET_EW_IDX(u) < n4) {
+      v[u] = ld4(x, MONET_EW_IDX(u));
+      k[u] = ld4(skip, MONET_EW_IDX(u));
+    }
+#pragma unroll
+  for (int u = 0; u < kEwUnroll; ++u) {
+    const long long i = MONET_EW_IDX(u);
+    if (i >= n4) break;
     const int q = (int)(i % cq);
-    float4 v = *reinterpret_cast<const float4*>(x + 4 * i);
-    const float4 k = *reinterpret_cast<const float4*>(skip + 4 * i);
-    const float4 m = *reinterpret_cast<const float4*>(mean + 4 * q);
-    const float4 s = *reinterpret_cast<const float4*>(invstd + 4 * q);
-    const float4 g = *reinterpret_cast<const float4*>(gamma + 4 * q);
-    const float4 b = *reinterpret_cast<const float4*>(beta + 4 * q);
-    v.x = fmaxf(__fadd_rn(bn_aff(v.x, m.x, s.x, g.x, b.x), k.x), 0.f);
-    v.y = fmaxf(__fadd_rn(bn_aff(v.y, m.y, s.y, g.y, b.y), k.y), 0.f);
-    v.z = fmaxf(__fadd_rn(bn_aff(v.z, m.z, s.z, g.z, b.z), k.z), 0.f);
-    v.w = fmaxf(__fadd_rn(bn_aff(v.w, m.w, s.w, g.w, b.w), k.w), 0.f);
-    *reinterpret_cast<float4*>(z + 4 * i) = v;
+    const float4 m = ldc4(mean, q), sd = ldc4(invstd, q), g = ldc4(gamma, q), b = ldc4(beta, q);
+    float4 o;
+    o.x = fmaxf(__fadd_rn(bn_aff(v[u].x, m.x, sd.x, g.x, b.x), k[u].x), 0.f);
+    o.y = fmaxf(__fadd_rn(bn_aff(v[u].y, m.y, sd.y, g.y, b.y), k[u].y), 0.f);
+    o.z = fmaxf(__fadd_rn(bn_aff(v[u].z, m.z, sd.z, g.z, b.z), k[u].z), 0.f);
+    o.w = fmaxf(__fadd_rn(bn_aff(v[u].w, m.w, sd.w, g.w, b.w), k[u].w), 0.f);
+    st4(z, i, o);
   }
+  MONET_EW_LOOP_END
 }
 
 // its backward apply: g = dz * gate (gate_from_out: [e > 0] with e = z; else [BN(x) + e > 0] with
@@ -564,45 +604,51 @@ __global__ void bnaddrelu_bwd_apply_kernel(const float* __restrict__ x, const fl
                                            const float* __restrict__ coef_c, long long rows, int C) {
   const int cq = C / 4;
   const long long n4 = rows * cq;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
-       i += (long long)gridDim.x * blockDim.x) {
+  MONET_EW_LOOP_BEGIN(n4)
+  float4 v[kEwUnroll], ev[kEwUnroll], gz[kEwUnroll];
+#pragma unroll
+  for (int u = 0; u < kEwUnroll; ++u)
+    if (MONET_EW_IDX(u) < n4) {
+      v[u] = ld4(x, MONET_EW_IDX(u));
+      ev[u] = ld4(e, MONET_EW_IDX(u));
+      gz[u] = ld4(dz, MONET_EW_IDX(u));
+    }
+#pragma unroll
+  for (int u = 0; u < kEwUnroll; ++u) {
+    const long long i = MONET_EW_IDX(u);
+    if (i >= n4) break;
     const int q = (int)(i % cq);
-    const float4 v = *reinterpret_cast<const float4*>(x + 4 * i);
-    const float4 ev = *reinterpret_cast<const float4*>(e + 4 * i);
-    float4 g = *reinterpret_cast<const float4*>(dz + 4 * i);
-    const float4 m = *reinterpret_cast<const float4*>(mean + 4 * q);
-    const float4 be = *reinterpret_cast<const float4*>(beta + 4 * q);
-    const float4 ga = *reinterpret_cast<const float4*>(gamma + 4 * q);
-    const float4 is = *reinterpret_cast<const float4*>(invstd + 4 * q);
-    const float4 cb = *reinterpret_cast<const float4*>(coef_b + 4 * q);
-    const float4 cc = *reinterpret_cast<const float4*>(coef_c + 4 * q);
+    const float4 m = ldc4(mean, q), be = ldc4(beta, q), ga = ldc4(gamma, q), is = ldc4(invstd, q);
+    const float4 cb = ldc4(coef_b, q), cc = ldc4(coef_c, q);
+    float4 g = gz[u];
     if (gate_from_out) {
-      g.x = ev.x > 0.f ? g.x : 0.f;
-      g.y = ev.y > 0.f ? g.y : 0.f;
-      g.z = ev.z > 0.f ? g.z : 0.f;
-      g.w = ev.w > 0.f ? g.w : 0.f;
+      g.x = ev[u].x > 0.f ? g.x : 0.f;
+      g.y = ev[u].y > 0.f ? g.y : 0.f;
+      g.z = ev[u].z > 0.f ? g.z : 0.f;
+      g.w = ev[u].w > 0.f ? g.w : 0.f;
     } else {
-      g.x = (__fadd_rn(bn_aff(v.x, m.x, is.x, ga.x, be.x), ev.x) > 0.f) ? g.x : 0.f;
-      g.y = (__fadd_rn(bn_aff(v.y, m.y, is.y, ga.y, be.y), ev.y) > 0.f) ? g.y : 0.f;
-      g.z = (__fadd_rn(bn_aff(v.z, m.z, is.z, ga.z, be.z), ev.z) > 0.f) ? g.z : 0.f;
-      g.w = (__fadd_rn(bn_aff(v.w, m.w, is.w, ga.w, be.w), ev.w) > 0.f) ? g.w : 0.f;
+      g.x = (__fadd_rn(bn_aff(v[u].x, m.x, is.x, ga.x, be.x), ev[u].x) > 0.f) ? g.x : 0.f;
+      g.y = (__fadd_rn(bn_aff(v[u].y, m.y, is.y, ga.y, be.y), ev[u].y) > 0.f) ? g.y : 0.f;
+      g.z = (__fadd_rn(bn_aff(v[u].z, m.z, is.z, ga.z, be.z), ev[u].z) > 0.f) ? g.z : 0.f;
+      g.w = (__fadd_rn(bn_aff(v[u].w, m.w, is.w, ga.w, be.w), ev[u].w) > 0.f) ? g.w : 0.f;
     }
     float4 o;
-    o.x = fmaf(ga.x * is.x, g.x, fmaf(cb.x, v.x, cc.x));
-    o.y = fmaf(ga.y * is.y, g.y, fmaf(cb.y, v.y, cc.y));
-    o.z = fmaf(ga.z * is.z, g.z, fmaf(cb.z, v.z, cc.z));
-    o.w = fmaf(ga.w * is.w, g.w, fmaf(cb.w, v.w, cc.w));
+    o.x = fmaf(ga.x * is.x, g.x, fmaf(cb.x, v[u].x, cc.x));
+    o.y = fmaf(ga.y * is.y, g.y, fmaf(cb.y, v[u].y, cc.y));
+    o.z = fmaf(ga.z * is.z, g.z, fmaf(cb.z, v[u].z, cc.z));
+    o.w = fmaf(ga.w * is.w, g.w, fmaf(cb.w, v[u].w, cc.w));
     if (acc_x) {
-      const float4 d = *reinterpret_cast<const float4*>(dx + 4 * i);
+      const float4 d = reinterpret_cast<const float4*>(dx)[i];
       o.x += d.x; o.y += d.y; o.z += d.z; o.w += d.w;
     }
-    *reinterpret_cast<float4*>(dx + 4 * i) = o;
+    st4(dx, i, o);
     if (acc_skip) {
-      const float4 d = *reinterpret_cast<const float4*>(dskip + 4 * i);
+      const float4 d = reinterpret_cast<const float4*>(dskip)[i];
       g.x += d.x; g.y += d.y; g.z += d.z; g.w += d.w;
     }
-    *reinterpret_cast<float4*>(dskip + 4 * i) = g;
+    st4(dskip, i, g);
   }
+  MONET_EW_LOOP_END
 }
 
 // Fused BN+ReLU backward apply from x: dy = dz * [bn(x) > 0]; dx = k*dy + cb*x + cc
@@ -614,32 +660,38 @@ __global__ void bnrelu_bwd_apply_kernel(const float* __restrict__ x, const float
                                         long long rows, int C, int accumulate) {
   const int cq = C / 4;
   const long long n4 = rows * cq;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
-       i += (long long)gridDim.x * blockDim.x) {
+  MONET_EW_LOOP_BEGIN(n4)
+  float4 v[kEwUnroll], gz[kEwUnroll];
+#pragma unroll
+  for (int u = 0; u < kEwUnroll; ++u)
+    if (MONET_EW_IDX(u) < n4) {
+      v[u] = ld4(x, MONET_EW_IDX(u));
+      gz[u] = ld4(dz, MONET_EW_IDX(u));
+    }
+#pragma unroll
+  for (int u = 0; u < kEwUnroll; ++u) {
+    const long long i = MONET_EW_IDX(u);
+    if (i >= n4) break;
     const int q = (int)(i % cq);
-    const float4 v = *reinterpret_cast<const float4*>(x + 4 * i);
-    float4 g = *reinterpret_cast<const float4*>(dz + 4 * i);
-    const float4 m = *reinterpret_cast<const float4*>(mean + 4 * q);
-    const float4 be = *reinterpret_cast<const float4*>(beta + 4 * q);
-    const float4 ga = *reinterpret_cast<const float4*>(gamma + 4 * q);
-    const float4 is = *reinterpret_cast<const float4*>(invstd + 4 * q);
-    const float4 cb = *reinterpret_cast<const float4*>(coef_b + 4 * q);
-    const float4 cc = *reinterpret_cast<const float4*>(coef_c + 4 * q);
-    g.x = relu_gate<kSix>(bn_aff(v.x, m.x, is.x, ga.x, be.x)) ? g.x : 0.f;
-    g.y = relu_gate<kSix>(bn_aff(v.y, m.y, is.y, ga.y, be.y)) ? g.y : 0.f;
-    g.z = relu_gate<kSix>(bn_aff(v.z, m.z, is.z, ga.z, be.z)) ? g.z : 0.f;
-    g.w = relu_gate<kSix>(bn_aff(v.w, m.w, is.w, ga.w, be.w)) ? g.w : 0.f;
+    const float4 m = ldc4(mean, q), be = ldc4(beta, q), ga = ldc4(gamma, q), is = ldc4(invstd, q);
+    const float4 cb = ldc4(coef_b, q), cc = ldc4(coef_c, q);
+    float4 g = gz[u];
+    g.x = relu_gate<kSix>(bn_aff(v[u].x, m.x, is.x, ga.x, be.x)) ? g.x : 0.f;
+    g.y = relu_gate<kSix>(bn_aff(v[u].y, m.y, is.y, ga.y, be.y)) ? g.y : 0.f;
+    g.z = relu_gate<kSix>(bn_aff(v[u].z, m.z, is.z, ga.z, be.z)) ? g.z : 0.f;
+    g.w = relu_gate<kSix>(bn_aff(v[u].w, m.w, is.w, ga.w, be.w)) ? g.w : 0.f;
     float4 o;
-    o.x = fmaf(ga.x * is.x, g.x, fmaf(cb.x, v.x, cc.x));
-    o.y = fmaf(ga.y * is.y, g.y, fmaf(cb.y, v.y, cc.y));
-    o.z = fmaf(ga.z * is.z, g.z, fmaf(cb.z, v.z, cc.z));
-    o.w = fmaf(ga.w * is.w, g.w, fmaf(cb.w, v.w, cc.w));
+    o.x = fmaf(ga.x * is.x, g.x, fmaf(cb.x, v[u].x, cc.x));
+    o.y = fmaf(ga.y * is.y, g.y, fmaf(cb.y, v[u].y, cc.y));
+    o.z = fmaf(ga.z * is.z, g.z, fmaf(cb.z, v[u].z, cc.z));
+    o.w = fmaf(ga.w * is.w, g.w, fmaf(cb.w, v[u].w, cc.w));
     if (accumulate) {
-      const float4 d = *reinterpret_cast<const float4*>(dx + 4 * i);
+      const float4 d = reinterpret_cast<const float4*>(dx)[i];
       o.x += d.x; o.y += d.y; o.z += d.z; o.w += d.w;
     }
-    *reinterpret_cast<float4*>(dx + 4 * i) = o;
+    st4(dx, i, o);
   }
+  MONET_EW_LOOP_END
 }
 
 // 1/gamma with |gamma| clamped away from 0 (output-activated BN needs gamma != 0)

@@ -62,7 +62,8 @@ extern "C" int monet_profile_variant(const monet_prof_desc* d, int variant, int 
   B.st = st;
   size_t ws = 0;
   const int pass = d->pass;
-  if (pass != MONET_PASS_FWD && pass != MONET_PASS_BWD) return -(int)cudaErrorInvalidValue;
+  if (pass < MONET_PASS_FWD || pass > MONET_PASS_BWD) return -(int)cudaErrorInvalidValue;
+  if (d->op != MONET_OP_CONV && pass != MONET_PASS_FWD && pass != MONET_PASS_BWD) return -(int)cudaErrorInvalidValue;
   // one launch of the variant; returns 0 or a negative error
   std::function<int()> run;
   if (d->op == MONET_OP_CONV) {
@@ -70,15 +71,16 @@ extern "C" int monet_profile_variant(const monet_prof_desc* d, int variant, int 
     if (c->c % 4 || c->k % 4) return -(int)cudaErrorInvalidValue;
     const size_t xb = (size_t)c->n * c->h * c->w * c->c * 4, yb = (size_t)c->n * c->p * c->q * c->k * 4;
     const size_t wb = (size_t)c->k * c->r * c->s * c->c * 4;
-    ws = monet_conv_ws_bytes(variant, pass == MONET_PASS_FWD ? MONET_PASS_FWD : MONET_PASS_BWD, c);
+    ws = monet_conv_ws_bytes(variant, pass, c);
     float *x = B.get(xb, 1), *w = B.get(wb, 2), *y = B.get(yb, 3), *wsp = B.get(ws, 4);
-    float *dx = pass == MONET_PASS_BWD ? B.get(xb, 5) : nullptr, *dw = pass == MONET_PASS_BWD ? B.get(wb, 6) : nullptr;
+    float *dx = pass != MONET_PASS_FWD ? B.get(xb, 5) : nullptr, *dw = pass != MONET_PASS_FWD ? B.get(wb, 6) : nullptr;
     if (B.err) return B.err;
     const bool need_dx = d->conv_needs_dx != 0;
-    run = [=]() -> int {
+    run = [=]() -> int {  // BWD: dgrad (if the input has a gradient) + wgrad; DGRAD / WGRAD: one pass
       if (pass == MONET_PASS_FWD) return monet_conv_fwd(variant, c, x, w, y, wsp, ws, st);
-      if (need_dx)
+      if ((pass == MONET_PASS_BWD && need_dx) || pass == MONET_PASS_DGRAD)
         if (int e = monet_conv_dgrad(variant, c, y, w, dx, 0, wsp, ws, st)) return e;
+      if (pass == MONET_PASS_DGRAD) return 0;
       return monet_conv_wgrad(variant, c, x, y, dw, 0, wsp, ws, st);
     };
   } else if (d->op == MONET_OP_RELU) {

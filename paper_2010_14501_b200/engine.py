@@ -283,6 +283,8 @@ class Runtime:
             if op.kind == "input":
                 nb = op.nbytes
                 out.append(("copy", y, self.staging.data_ptr(), nb))
+            elif op.kind == "wgrad":
+                pass  # a split conv's weight-gradient anchor: no forward work, no tensor
             elif op.kind == "conv":
                 d = net.conv_desc(op)
                 v = _native.CONV_VARIANTS[s.impl]
@@ -417,9 +419,11 @@ class Runtime:
                 raise ValueError(f"{op.kind} node {op.id} reads node {j} directly, which has no gradient "
                                  "buffer; this operator's backward kernel always writes its input gradient")
 
-        if op.kind in ("bn", "bnrelu", "bnrelu6", "bnaddrelu", "addrelu", "maxpool", "avgpool", "fc", "xent"):
+        if op.kind in ("bn", "bnrelu", "bnrelu6", "bnaddrelu", "addrelu", "maxpool", "avgpool", "fc"):
             for j in op.deps:
                 must(j)
+        elif op.kind == "xent":
+            must(op.deps[0])  # further deps: the zero-byte wgrad anchors of a split graph
         if op.id == net.n:
             out.append(("copy", dy, self.consts.data_ptr(), 4))  # seed dL/dL = 1
         if op.kind == "input":
@@ -432,13 +436,21 @@ class Runtime:
             if net.grad_bytes(net.op(j)) > 0:
                 out.append(("k", lib.monet_conv_dgrad, (v, C.byref(d), dy, wt, P(("g", j)), acc(j), ws,
                                                         s.workspace, None), d))
-            out.append(("k", lib.monet_conv_wgrad, (v, C.byref(d), P(("in", j)), dy,
-                                                    self.gview[(op.id, "weight")].data_ptr(), 0, ws,
-                                                    s.workspace, None), d))
+            if not op.attrs.get("split"):  # split convs: the weight gradient is the wgrad node's stage
+                out.append(("k", lib.monet_conv_wgrad, (v, C.byref(d), P(("in", j)), dy,
+                                                        self.gview[(op.id, "weight")].data_ptr(), 0, ws,
+                                                        s.workspace, None), d))
             if "bias" in op.params:
                 out.append(("k", lib.monet_bias_grad, (dy, self.gview[(op.id, "bias")].data_ptr(),
                                                        op.numel // op.shape[-1], op.shape[-1], 0, self.scratch_ptr,
                                                        None)))
+        elif op.kind == "wgrad":  # weight gradient of a split conv: reads x and the conv's dy
+            conv = net.op(op.attrs["conv"])
+            d = net.conv_desc(conv)
+            v = _native.CONV_VARIANTS[s.impl]
+            out.append(("k", lib.monet_conv_wgrad, (v, C.byref(d), P(("in", conv.deps[0])), P(("g", conv.id)),
+                                                    self.gview[(conv.id, "weight")].data_ptr(), 0, ws,
+                                                    s.workspace, None), d))
         elif op.kind == "convT":
             d = net.conv_desc(op)
             v = _native.CONV_VARIANTS[s.impl]

@@ -146,7 +146,22 @@ def demand_schedule(g: Graph, cat: Catalog, store0: set, window: int | None = No
                     rec.discard(x)
         order = sorted(rec, key=lambda x: (by_id[x].pos, by_id[x].is_intermediate, x))
         entries = tuple((x, None if by_id[x].is_intermediate else fwd_impl[x - 1]) for x in order)
-        plans.append(StagePlan(k, entries, tuple(u.id for u in g.storables if u.id in cur), v.name, ()))
+        # recompute in place (schedule.py:403-411) where the input dies with it: it is not kept,
+        # not read by this backward, not read by a later recompute of the stage and was not
+        # carried in as this node's output
+        inplace = []
+        nodes = [x for x in order if not by_id[x].is_intermediate]
+        for pos, i in enumerate(nodes):
+            deps = g.deps(i)
+            if len(deps) != 1 or i in prev:
+                continue
+            fv = cat.fwd(i)[cat.fwd_index(i, fwd_impl[i - 1])]
+            j = deps[0]
+            if (fv.inplace_capable and g.output_bytes(i) == g.output_bytes(j) and j not in cur
+                    and j not in v.deps and not any(j in g.deps(u) for u in nodes[pos + 1:])):
+                inplace.append(i)
+        plans.append(StagePlan(k, entries, tuple(u.id for u in g.storables if u.id in cur), v.name,
+                               tuple(inplace)))
         chosen_bwd.append(l)
         prev = cur
     sched = Schedule(tuple(fwd_impl), tuple(u.id for u in g.storables if u.id in store0), tuple(plans), None)
@@ -170,7 +185,7 @@ def _families(g: Graph, kind_of) -> dict:
             kinds = kinds | {"relu-join"}
         return {x for x in ids if kind_of(x) in kinds}
 
-    base = {"input", "maxpool", "avgpool", "fc", "xent", "dropout"}
+    base = {"input", "maxpool", "avgpool", "fc", "xent", "dropout", "wgrad"}  # wgrad anchors: 0 bytes
     fam["all"] = set(ids)
     fam["conv+relu+mask"] = pick(base | {"conv", "relu", "mask", "idx"})
     fam["conv+mask"] = pick(base | {"conv", "mask", "idx"})
@@ -188,10 +203,75 @@ FAMILIES = ("all", "conv+relu+mask", "conv+mask", "bn+relu+mask", "bn+mask", "re
 
 
 EXACT_MAX_NODES = 64  # graphs up to this size also go through the exact ILP (VGG-16: 40 nodes)
+LP_THRESHOLDS = (0.05, 0.1, 0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9, 0.95)
+
+
+def ilp_relaxation(g: Graph, cat: Catalog, budget: int, mip_time_s: float | None = None) -> dict | None:
+    """The reference's 0-1 ILP (ilp.build_model: same variables, rows and objective as
+    pkg/src/remsched/ilp.py:121) handed to HiGHS through scipy.optimize.milp.
+
+    * LP relaxation (seconds at ResNet-50 scale, 58k variables / 113k rows): its optimum
+      is a lower bound on the cost of every schedule at this budget, and its row-0 store
+      values S[0, u] in [0, 1] say which tensors the forward pass should keep;
+    * optionally the MIP itself for ``mip_time_s``: HiGHS's dual bound (tighter than the
+      LP's) and its incumbent, decoded like the reference decodes its own (schedule.py:132).
+
+    Returns {"lp_bound", "s0", "model"[, "mip_bound", "mip_schedule", "mip_status"]}, or
+    None when scipy / HiGHS is unavailable.  Host-side planning only (no GPU)."""
+    try:
+        import numpy as np
+        import scipy.sparse as sp
+        from scipy.optimize import Bounds, LinearConstraint, milp
+    except ImportError:
+        return None
+    from .ilp import build_model
+
+    m = build_model(g, compute_dependency_sets(g), cat, budget)
+    n = m.n_vars
+    c = np.zeros(n)
+    for j, cost in m.objective:
+        c[j] += float(cost)
+    ri, ci, va, lo, hi = [], [], [], [], []
+    for r, row in enumerate(m.rows):
+        for j, a in row.terms:
+            ri.append(r)
+            ci.append(j)
+            va.append(float(a))
+        lo.append(-np.inf if row.sense == "<=" else float(row.rhs))
+        hi.append(float(row.rhs))
+    A = sp.csr_matrix((va, (ri, ci)), shape=(len(m.rows), n))
+    lb, ub = np.zeros(n), np.ones(n)
+    for j, v in m.fixed.items():
+        lb[j] = ub[j] = v
+    cons, bnds = LinearConstraint(A, lo, hi), Bounds(lb, ub)
+    lp = milp(c, constraints=cons, integrality=np.zeros(n), bounds=bnds)
+    if lp.status != 0:
+        return {"lp_bound": None, "s0": {}, "model": m, "lp_status": lp.message}
+    s0 = {v.node: float(lp.x[j]) for j, v in enumerate(m.var_ids) if v.kind == "S" and v.row == 0}
+    out = {"lp_bound": Fraction(lp.fun).limit_denominator(1 << 20), "s0": s0, "model": m}
+    if mip_time_s:
+        res = milp(c, constraints=cons, integrality=np.ones(n), bounds=bnds, options={"time_limit": mip_time_s})
+        out["mip_status"] = res.message
+        bound = getattr(res, "mip_dual_bound", None)
+        out["mip_bound"] = None if bound is None else Fraction(bound).limit_denominator(1 << 20)
+        if res.x is not None:
+            from .ilp import evaluate_assignment
+            from .schedule import decode
+
+            x = [int(round(v)) for v in res.x]
+            if evaluate_assignment(m, x)["feasible"]:
+                class _R:  # the fields decode() reads from a solver result
+                    status, assignment, model = "feasible-gap", x, m
+                try:
+                    out["mip_schedule"] = decode(_R, g, cat)
+                except ValueError:
+                    pass
+    return out
 
 
 def plan_schedule(g: Graph, cat: Catalog, budget: int, kinds: dict | None = None,
-                  exact_time_s: float | None = None, exchange: bool = False):
+                  exact_time_s: float | None = None, exchange: bool = False, lp: bool = False,
+                  mip_time_s: float | None = None):
     """Cheapest feasible schedule among the demand-construction candidates.
 
     ``kinds`` maps storable id -> family label; by default inferred from the
@@ -203,9 +283,35 @@ def plan_schedule(g: Graph, cat: Catalog, budget: int, kinds: dict | None = None
     reference-exact 0-1 ILP (ilp.build_model + solver.solve) for that long,
     seeded with the best candidate as its incumbent; its schedule wins when it
     is cheaper or the only feasible one.
+    ``lp``: solve the ILP's LP relaxation (ilp_relaxation, HiGHS) and add forward-store
+    sets thresholded from its row-0 store values as demand-construction seeds; the LP
+    optimum (or, with ``mip_time_s``, HiGHS's MIP dual bound) is reported as the lower
+    bound and the chosen schedule's gap to it.
     Returns (schedule or None, info dict).
     """
-    sch, info = _plan_heuristic(g, cat, budget, kinds, exchange)
+    relax = ilp_relaxation(g, cat, budget, mip_time_s) if (lp or mip_time_s) else None
+    seeds = []
+    if relax and relax["s0"]:
+        for thr in LP_THRESHOLDS:
+            seeds.append((f"lp{thr:g}", {u for u, val in relax["s0"].items() if val >= thr}))
+    sch, info = _plan_heuristic(g, cat, budget, kinds, exchange, seeds)
+    if relax is not None:
+        mip = relax.get("mip_schedule")
+        if mip is not None and (sch is None or mip.objective < sch.objective):
+            ok, peak, _ = FastBound(g, compute_dependency_sets(g, "upper"), cat).check(mip, budget)
+            if ok:
+                simulate(mip, g, cat)
+                se = info.get("se_cost")
+                info = {"family": "ilp-highs/feasible", "candidates": info["candidates"], "modeled_peak": peak,
+                        "objective": str(mip.objective), "se_cost": se,
+                        "overhead_vs_store_everything": None if se is None else float(Fraction(mip.objective) / se - 1)}
+                sch = mip
+        bound = max(b for b in (relax.get("lp_bound"), relax.get("mip_bound")) if b is not None) \
+            if relax.get("lp_bound") is not None else None
+        info["ilp_lower_bound"] = None if bound is None else round(float(bound), 1)
+        info["ilp_lower_bound_source"] = "highs-mip-dual" if relax.get("mip_bound") is not None else "highs-lp"
+        if bound is not None and sch is not None:
+            info["ilp_gap"] = float(1 - bound / Fraction(sch.objective))
     if exact_time_s and g.n <= EXACT_MAX_NODES:
         from .ilp import assignment_from_schedule, build_model
         from .schedule import decode
@@ -230,7 +336,8 @@ def plan_schedule(g: Graph, cat: Catalog, budget: int, kinds: dict | None = None
     return sch, info
 
 
-def _plan_heuristic(g: Graph, cat: Catalog, budget: int, kinds: dict | None = None, exchange: bool = False):
+def _plan_heuristic(g: Graph, cat: Catalog, budget: int, kinds: dict | None = None, exchange: bool = False,
+                    seeds=()):
     sets = compute_dependency_sets(g, "upper")
     fb = FastBound(g, sets, cat)
     kind_of = (lambda x: kinds.get(x, "other")) if kinds else (lambda x: "other")
@@ -244,11 +351,18 @@ def _plan_heuristic(g: Graph, cat: Catalog, budget: int, kinds: dict | None = No
         cands.append(("store_everything/fastest", fastest_store_everything_schedule(g, cat)))
     except ValueError:
         pass
-    for name in FAMILIES:
-        s0 = fams.get(name)
+    for name in FAMILIES + tuple(n for n, _ in seeds):
+        s0 = fams.get(name) if name in fams else dict(seeds).get(name)
         if not s0:
             continue
         variants = [(name, s0)]
+        if name not in fams:  # LP-guided seeds are used as given (no residual thinning)
+            for window in (None, 8, 2, 0):
+                for prefer in ("cost", "lean"):
+                    sch = demand_schedule(g, cat, s0, window=window, prefer=prefer)
+                    if sch is not None:
+                        cands.append((f"{name}/w{window}/{prefer}", sch, (s0, window, prefer)))
+            continue
         for stride in (2, 3):
             for phase in range(stride):
                 keep_segs = set()
@@ -258,7 +372,7 @@ def _plan_heuristic(g: Graph, cat: Catalog, budget: int, kinds: dict | None = No
                 thin = {x for x in s0 if g.storable_by_id[x].pos not in keep_segs or x in fams["join"]}
                 variants.append((f"{name}/thin{stride}.{phase}", thin))
         for vname, s0v in variants:
-            for window in (None, 8, 2):
+            for window in (None, 8, 2, 0):
                 for prefer in ("cost", "lean"):
                     sch = demand_schedule(g, cat, s0v, window=window, prefer=prefer)
                     if sch is not None:

@@ -247,11 +247,16 @@ def profile_variant(net, op, pss: str, variant: str, iters: int = 5, stream=None
     """(ns per launch, workspace bytes) of one variant through the C-ABI profiler entry
     point monet_profile_variant (csrc/profile.cu): conv fwd / bwd, ReLU, BN, fused BN+ReLU."""
     d = _native.ProfDesc()
-    d.op = _native.PROF_OP[op.kind]
+    d.op = _native.PROF_OP["conv" if op.kind == "wgrad" else op.kind]
     d.pass_ = _native.PASS["fwd"] if pss == "fwd" else _native.PASS["bwd"]
-    if op.kind == "conv":
-        d.conv = net.conv_desc(op)
-        d.conv_needs_dx = int(net.op(op.deps[0]).kind != "input")
+    if op.kind in ("conv", "wgrad"):
+        conv = net.op(op.attrs["conv"]) if op.kind == "wgrad" else op
+        d.conv = net.conv_desc(conv)
+        d.conv_needs_dx = int(net.op(conv.deps[0]).kind != "input")
+        if pss == "bwd" and op.kind == "wgrad":  # a split conv's weight-gradient node
+            d.pass_ = _native.PASS["wgrad"]
+        elif pss == "bwd" and op.attrs.get("split"):  # ... and its input-gradient node
+            d.pass_ = _native.PASS["dgrad"]
         v = _native.CONV_VARIANTS[variant]
     else:
         d.c = op.shape[-1]
@@ -266,12 +271,15 @@ def profile_variant(net, op, pss: str, variant: str, iters: int = 5, stream=None
     return int(ns.value), int(ws.value)
 
 
-_NATIVE_PROFILED = ("conv", "relu", "bn", "bnrelu")
+_NATIVE_PROFILED = ("conv", "wgrad", "relu", "bn", "bnrelu")
 
 
 def _signature(net, op):
+    if op.kind == "wgrad":  # identical to its conv's shape
+        return ("wgrad",) + _signature(net, net.op(op.attrs["conv"]))
     ins = tuple((net.op(j).kind == "input", net.op(j).shape) for j in op.deps)
-    attrs = tuple(sorted((k, v) for k, v in op.attrs.items() if isinstance(v, (int, float, str))))
+    attrs = tuple(sorted((k, v) for k, v in op.attrs.items()
+                         if isinstance(v, (int, float, str)) and k not in ("conv", "wgrad_node")))
     return op.kind, ins, op.shape, attrs
 
 
@@ -285,7 +293,13 @@ def profile_network(net, device="cuda:0", warmup=2, iters=5, reps=3, log=None) -
         sig = _signature(net, op)
         if sig not in cache:
             res = {}
-            if op.kind in _NATIVE_PROFILED:  # through the C-ABI profiler entry point
+            if op.kind == "wgrad":  # no forward work
+                res[("fwd", "none")] = 1
+                for name, ws, _ in bv:
+                    ns, ws_k = profile_variant(net, op, "bwd", name, iters, bx.stream.cuda_stream)
+                    assert ws_k == ws, (op.name, name, ws_k, ws)
+                    res[("bwd", name)] = ns
+            elif op.kind in _NATIVE_PROFILED:  # through the C-ABI profiler entry point
                 for name, ws in fv:
                     ns, ws_k = profile_variant(net, op, "fwd", name, iters, bx.stream.cuda_stream)
                     assert ws_k == ws, (op.name, name, ws_k, ws)

@@ -51,6 +51,8 @@ class Op:
 
     @property
     def nbytes(self) -> int:
+        if self.kind == "wgrad":  # the weight-gradient anchor of a split conv produces no tensor
+            return 0
         return r16(self.numel * F32)
 
 
@@ -75,6 +77,7 @@ class Network:
     def __init__(self, ops: list[Op], batch: int, num_classes: int):
         self.ops = ops
         self.fused = any(op.kind in ("bnrelu", "bnrelu6", "bnaddrelu") for op in ops)
+        self.split = any(op.kind == "wgrad" for op in ops)
         self.batch = batch
         self.num_classes = num_classes
         self.n = len(ops)
@@ -158,7 +161,7 @@ class Network:
 
     # -------------------------------------------------------------- documents
     def grad_bytes(self, op: Op) -> int:
-        if op.kind == "input":
+        if op.kind in ("input", "wgrad"):
             return 0
         return op.nbytes
 
@@ -197,8 +200,18 @@ class Network:
             ws = lib.conv_ws_bytes(1, 0, d)
             if ws:
                 fwd.append(("splitk", ws))
-            bwd.append(("splitk", lib.conv_ws_bytes(1, 3, d), x))
-            bwd.append(("implicit", lib.conv_ws_bytes(0, 3, d), x))
+            if op.attrs.get("split"):  # backward = dgrad only: reads dy and the weights, not x
+                bwd.append(("splitk", lib.conv_ws_bytes(1, 1, d), []))
+                bwd.append(("implicit", lib.conv_ws_bytes(0, 1, d), []))
+            else:
+                bwd.append(("splitk", lib.conv_ws_bytes(1, 3, d), x))
+                bwd.append(("implicit", lib.conv_ws_bytes(0, 3, d), x))
+        elif op.kind == "wgrad":  # split conv's weight gradient: reads the conv input x and dy
+            conv = self.op(op.attrs["conv"])
+            d = self.conv_desc(conv)
+            fwd.append(("none", 0))
+            bwd.append(("splitk", lib.conv_ws_bytes(1, 2, d), [conv.deps[0]]))
+            bwd.append(("implicit", lib.conv_ws_bytes(0, 2, d), [conv.deps[0]]))
         elif op.kind == "fc":
             n, fi = self.fc_dims(op)
             fo = op.shape[1]
@@ -254,6 +267,15 @@ class Network:
             raise ValueError(op.kind)
         return [(nm, r16(ws)) for nm, ws in fwd], [(nm, r16(ws), deps) for nm, ws, deps in bwd]
 
+    INPLACE_KINDS = ("relu", "relu6", "bn", "bnrelu", "bnrelu6", "dropout")
+
+    def inplace_capable(self, op: Op) -> bool:
+        """Elementwise one-input operators whose kernels accept y aliasing x: a recompute may
+        overwrite its input (costmodel.py:121-129; the schedule's stage ``inplace`` list, the
+        executor places both in one arena block).  The first forward never runs in place."""
+        return (op.kind in self.INPLACE_KINDS and len(op.deps) == 1
+                and self.op(op.deps[0]).nbytes == op.nbytes)
+
     def catalog_doc(self, costs=None) -> dict:
         """Catalog with measured costs (``costs[(node, pass, name)]`` -> int ns) or the
         analytic roofline estimate when a cost is not supplied."""
@@ -261,9 +283,11 @@ class Network:
         fwd_doc, bwd_doc = [], []
         for op in self.ops:
             fv, bv = self.variants(op)
+            inplace = self.inplace_capable(op)
             fwd_doc.append({"node": op.id, "variants": [
                 {"name": n, "workspace_bytes": ws,
-                 "cost": _cost(costs, (op.id, "fwd", n), lambda: analytic_cost(self, op, "fwd", n))}
+                 "cost": _cost(costs, (op.id, "fwd", n), lambda: analytic_cost(self, op, "fwd", n)),
+                 **({"inplace_capable": True} if inplace else {})}
                 for n, ws in fv]})
             bwd_doc.append({"node": op.id, "variants": [
                 {"name": n, "workspace_bytes": ws, "deps": sorted(deps),
@@ -308,6 +332,7 @@ def _cost(costs, key, fallback):
 BWD_IMPLS = {
     "input": [("none", "input")],
     "conv": [("splitk", "input"), ("implicit", "input")],
+    "wgrad": [("splitk", "input"), ("implicit", "input")],  # catalog deps: the conv's input (see split)
     "fc": [("gemm-splitk", "input"), ("gemm", "input")],
     "bn": [("bwd-in", "input"), ("bwd-out", "output")],
     "bnrelu": [("bwd-in", "input")],
@@ -413,8 +438,48 @@ def fuse_bn_addrelu(ops: list[Op]) -> list[Op]:
     return out
 
 
+def split_conv_backward(ops: list[Op]) -> list[Op]:
+    """Split every conv's backward into two graph nodes:
+
+    * the conv node keeps the forward and its backward becomes the input gradient
+      (dgrad), which reads only dy and the weights -- not the forward input x;
+    * a new zero-byte node right after it ("wgrad", deps: the conv) carries the weight
+      gradient, whose backward reads x and the conv's output gradient.  Its stage runs
+      before the conv's (stages descend), so x can be freed as soon as the weight
+      gradient is done and the dgrad allocates dx without x still live.
+
+    The anchors are extra dependencies of the loss node (the unique sink), whose
+    backward "produces" their zero-byte gradients -- the reference graph format needs
+    every backward node's gradient to come from a later stage (graph.py:349-358).
+    Convs reading the network input (no dgrad) are not split.  Ids are renumbered."""
+    new_id: dict[int, int] = {}
+    out: list[Op] = []
+    anchors: list[int] = []
+    for op in ops:
+        nid = len(out) + 1
+        new_id[op.id] = nid
+        attrs = dict(op.attrs)
+        if "inputs" in attrs:
+            attrs["inputs"] = [new_id[j] for j in attrs["inputs"]]
+        for key in ("x", "skip"):
+            if key in attrs:
+                attrs[key] = new_id[attrs[key]]
+        deps = tuple(new_id[j] for j in op.deps)
+        split = op.kind == "conv" and ops[op.deps[0] - 1].kind != "input"
+        if split:
+            attrs["split"] = True
+            attrs["wgrad_node"] = nid + 1
+        if op.kind == "xent":
+            deps = deps + tuple(anchors)
+        out.append(Op(nid, op.kind, deps, op.shape, attrs, op.params, op.name))
+        if split:
+            out.append(Op(nid + 1, "wgrad", (nid,), (), {"conv": nid}, name=op.name + ".wgrad"))
+            anchors.append(nid + 1)
+    return out
+
+
 def trace_graph(model: torch.nn.Module, example_input: torch.Tensor, num_classes: int | None = None,
-                fuse: bool = False) -> Network:
+                fuse: bool = False, split: bool = False) -> Network:
     """Trace a torchvision-style CNN into a Network (engine layout parameters).
 
     Supported modules: Conv2d (no bias, groups=1), BatchNorm2d, ReLU,
@@ -576,7 +641,11 @@ def trace_graph(model: torch.nn.Module, example_input: torch.Tensor, num_classes
     logits = ops[src - 1]
     k = num_classes or logits.shape[1]
     ops.append(Op(len(ops) + 1, "xent", (src,), (), name="loss"))
-    return Network(fuse_bn_addrelu(fuse_bn_relu(ops)) if fuse else ops, n, k)
+    if fuse:
+        ops = fuse_bn_addrelu(fuse_bn_relu(ops))
+    if split:
+        ops = split_conv_backward(ops)
+    return Network(ops, n, k)
 
 
 def parse_image(v):
@@ -595,9 +664,10 @@ def default_classes(arch: str) -> int:
 
 
 def build_network(arch: str, batch: int, image: int | tuple = 224, num_classes: int = 1000,
-                  seed: int = 0, fuse: bool = False) -> Network:
+                  seed: int = 0, fuse: bool = False, split: bool = False) -> Network:
     """torchvision ``arch`` with default init under ``torch.manual_seed(seed)``, traced
-    (``fuse``: BN+ReLU pairs become single fused ops)."""
+    (``fuse``: BN+ReLU pairs become single fused ops; ``split``: conv backward split
+    into dgrad / wgrad graph nodes, split_conv_backward)."""
     import torchvision
 
     torch.manual_seed(seed)
@@ -607,7 +677,7 @@ def build_network(arch: str, batch: int, image: int | tuple = 224, num_classes: 
         kw = {"aux_logits": False, "init_weights": True} if arch in ("googlenet", "inception_v3") else {}
         model = getattr(torchvision.models, arch)(num_classes=num_classes, **kw)
     hw = (image, image) if isinstance(image, int) else image
-    return trace_graph(model, torch.empty(batch, 3, *hw, device="meta"), num_classes, fuse)
+    return trace_graph(model, torch.empty(batch, 3, *hw, device="meta"), num_classes, fuse, split)
 
 
 # ------------------------------------------------------------------ UNet (config C3)

@@ -94,10 +94,14 @@ def test_engine_matches_reference_ledger_and_oracle(cuda, r18, which):
             assert rel(rt.bn[op.id][2], rm) <= REL and rel(rt.bn[op.id][3], rv) <= REL
 
 
-def test_fused_bn_relu_engine(cuda):
+@pytest.mark.parametrize("split", [False, True])
+def test_fused_bn_relu_engine(cuda, split):
     """ResNet-18 with fused BN+ReLU ops under a recompute schedule: ledger = simulate(),
-    loss / weights / gradients = CPU oracle (fed the GPU activations)."""
-    net = build_network("resnet18", 4, 32, num_classes=10, fuse=True)
+    loss / weights / gradients = CPU oracle (fed the GPU activations).  ``split``: conv
+    backward split into dgrad / wgrad nodes (tracer.split_conv_backward), with in-place
+    recomputes where the planner finds them."""
+    net = build_network("resnet18", 4, 32, num_classes=10, fuse=True, split=split)
+    assert net.split == split
     assert any(op.kind == "bnrelu" for op in net.ops)
     g = M.load_graph(net.graph_doc())
     cat = M.load_catalog(net.catalog_doc(), g)
@@ -121,8 +125,7 @@ def test_fused_bn_relu_engine(cuda):
     assert abs(rt.loss_value() - loss) <= REL * abs(loss)
     st = CpuState(net)
     run_step(st, doc, x, y, forced=acts, forced_stats=gpu_stats(rt))
-    for (nid, pname), v in params_nhwc(st).items():
-        assert rel(rt.pview[(nid, pname)].view(v.shape), v) <= REL, (net.op(nid).name, pname)
+    _assert_step_parity(rt, st)
 
 
 def test_forward_ops_match_oracle(cuda, r18):

@@ -27,10 +27,13 @@ def test_spec_matches_tracer(path):
     doc = json.loads(path.read_text())
     stem = path.stem
     arch = stem.split("_b")[0]
+    split = arch.endswith("_split")
+    arch = arch.removesuffix("_split")
     fused = arch.endswith("_fused")
     arch = arch.removesuffix("_fused")
     batch, image = stem.split("_b")[1].split("_")
-    net = build_network(arch, int(batch), parse_image(image), num_classes=default_classes(arch), fuse=fused)
+    net = build_network(arch, int(batch), parse_image(image), num_classes=default_classes(arch), fuse=fused,
+                        split=split)
     gdoc = net.graph_doc()
     assert doc["graph"] == gdoc
     assert doc["graph_digest"] == hashlib.sha256(json.dumps(gdoc, sort_keys=True).encode()).hexdigest()[:16]
@@ -41,7 +44,7 @@ def test_spec_matches_tracer(path):
 def test_reference_planner_without_product():
     code = (
         "import sys, json, argparse; sys.path.insert(0, %r); import bench; "
-        "a = argparse.Namespace(arch='resnet50', batch=184, image='224', budget_gib=8.0, fuse=True); "
+        "a = argparse.Namespace(arch='resnet50', batch=184, image='224', budget_gib=8.0, fuse=True, split=False); "
         "r = bench.reference_planner_run(a); "
         "r['product_loaded'] = any(m.startswith('paper_2010_14501_b200') for m in sys.modules); "
         "print(json.dumps(r))" % str(ROOT))

@@ -21,12 +21,14 @@ def main():
     ap.add_argument("--batch", type=int, default=184)
     ap.add_argument("--image", default="224")
     ap.add_argument("--no-fuse", dest="fuse", action="store_false")
+    ap.add_argument("--split", action="store_true")
     a = ap.parse_args()
-    net = build_network(a.arch, a.batch, parse_image(a.image), num_classes=default_classes(a.arch), fuse=a.fuse)
+    net = build_network(a.arch, a.batch, parse_image(a.image), num_classes=default_classes(a.arch), fuse=a.fuse,
+                        split=a.split)
     gdoc = net.graph_doc()
     doc = netspec.freeze(net, gdoc)
     doc["graph_digest"] = hashlib.sha256(json.dumps(gdoc, sort_keys=True).encode()).hexdigest()[:16]
-    out = netspec.spec_path(a.arch, a.fuse, a.batch, a.image)
+    out = netspec.spec_path(a.arch, net.fused, a.batch, a.image, net.split)
     out.parent.mkdir(exist_ok=True)
     out.write_text(json.dumps(doc, sort_keys=True, separators=(",", ":")))
     print(f"wrote {out.relative_to(ROOT)} ({out.stat().st_size} B, {len(doc['ops'])} ops, digest {doc['graph_digest']})")

@@ -26,11 +26,11 @@ def digest(doc):
     return hashlib.sha256(json.dumps(doc, sort_keys=True).encode()).hexdigest()[:16]
 
 
-def main(jobs, exact_time_s=None, exchange=False):
+def main(jobs, exact_time_s=None, exchange=False, lp=False, mip_time_s=None):
     OUT.mkdir(exist_ok=True)
-    for arch, batch, img, gib, fuse in jobs:
-        net = build_network(arch, batch, parse_image(img), num_classes=default_classes(arch), fuse=fuse)
-        arch = arch + ("_fused" if net.fused else "")
+    for arch, batch, img, gib, fuse, split in jobs:
+        net = build_network(arch, batch, parse_image(img), num_classes=default_classes(arch), fuse=fuse, split=split)
+        arch = arch + ("_fused" if net.fused else "") + ("_split" if net.split else "")
         gdoc, cdoc = net.graph_doc(), net.catalog_doc()
         measured = ROOT / "profiles" / f"catalog_{arch}_b{batch}_{img}.json"
         if measured.exists():  # plan with the on-device profile when it matches this graph
@@ -43,7 +43,7 @@ def main(jobs, exact_time_s=None, exchange=False):
         budget = int(gib * (1 << 30))
         t = time.time()
         sched, info = plan_schedule(g, cat, budget, kinds=net.storable_kinds(), exact_time_s=exact_time_s,
-                                    exchange=exchange)
+                                    exchange=exchange, lp=lp, mip_time_s=mip_time_s)
         dt = time.time() - t
         if sched is None:
             print(arch, batch, img, gib, "no feasible schedule", info)
@@ -68,5 +68,9 @@ if __name__ == "__main__":
     ap.add_argument("--exact", type=float, default=None,
                     help="seconds of exact ILP search on graphs of <= planner.EXACT_MAX_NODES nodes")
     ap.add_argument("--exchange", action="store_true", help="also try exchange moves (slower)")
+    ap.add_argument("--split", action="store_true", help="conv backward split into dgrad / wgrad nodes")
+    ap.add_argument("--lp", action="store_true", help="seed the planner with the ILP's LP relaxation (HiGHS)")
+    ap.add_argument("--mip", type=float, default=None, help="seconds of HiGHS MIP search for a dual bound")
     a = ap.parse_args()
-    main([(a.arch, a.batch, a.image, float(b), a.fused) for b in a.budgets.split(",")], a.exact, a.exchange)
+    main([(a.arch, a.batch, a.image, float(b), a.fused, a.split) for b in a.budgets.split(",")], a.exact,
+         a.exchange, a.lp, a.mip)

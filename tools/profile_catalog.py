@@ -1,6 +1,6 @@
 """Measure the catalog of a network on the B200 and freeze it (R3 profiler).
 
-    python tools/profile_catalog.py [arch batch image]
+    python tools/profile_catalog.py [arch batch image] [--fused] [--split]
 
 Writes profiles/catalog_<arch>_b<batch>_<image>.json: the catalog document
 (measured ns costs, library workspace bytes) plus the graph digest it was
@@ -23,9 +23,9 @@ def digest(doc):
     return hashlib.sha256(json.dumps(doc, sort_keys=True).encode()).hexdigest()[:16]
 
 
-def main(arch="resnet50", batch=184, image=224, fuse=False):
-    net = build_network(arch, batch, parse_image(image), num_classes=default_classes(arch), fuse=fuse)
-    arch = arch + ("_fused" if net.fused else "")
+def main(arch="resnet50", batch=184, image=224, fuse=False, split=False):
+    net = build_network(arch, batch, parse_image(image), num_classes=default_classes(arch), fuse=fuse, split=split)
+    arch = arch + ("_fused" if net.fused else "") + ("_split" if net.split else "")
     t = time.time()
     costs = profile_network(net, log=print)
     doc = {"arch": arch, "batch": batch, "image": image, "graph_digest": digest(net.graph_doc()),
@@ -36,6 +36,6 @@ def main(arch="resnet50", batch=184, image=224, fuse=False):
 
 
 if __name__ == "__main__":
-    fuse = "--fused" in sys.argv
-    a = [x for x in sys.argv[1:] if x != "--fused"]
-    main(a[0], int(a[1]), a[2], fuse) if a else main(fuse=fuse)
+    fuse, split = "--fused" in sys.argv, "--split" in sys.argv
+    a = [x for x in sys.argv[1:] if x not in ("--fused", "--split")]
+    main(a[0], int(a[1]), a[2], fuse, split) if a else main(fuse=fuse, split=split)
