@@ -196,6 +196,22 @@ int make_tma(GemmParams& p, Operand& op, CUtensorMap* m) {
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? 4 : 0;
   }
+  if (p.fv_q && op.mode == OP_IM2COL_FPROP) {
+    // fprop tap view over the zero-padded input xp[n][Hp][Wp][c]: element (j, q, r, p, n) =
+    // xp[n][p*sh + r][q*sw][j] for j < 32 -- the filter row's S*C taps x channels (S*C <= 32;
+    // j >= S*C reads the next pixels, multiplied by the zero-padded weights) -- with the q
+    // stride sw*C below the 32-float row: overlapping rows, as in the wgrad tap view
+    const long long Wp = (long long)(g.Q - 1) * g.sw + g.S, Hp = (long long)(g.P - 1) * g.sh + g.R;
+    cuuint64_t dims[5] = {32, (cuuint64_t)p.fv_q, (cuuint64_t)g.R, (cuuint64_t)g.P, (cuuint64_t)g.N};
+    cuuint64_t strides[4] = {(cuuint64_t)g.sw * g.C * 4, (cuuint64_t)Wp * g.C * 4, (cuuint64_t)g.sh * Wp * g.C * 4,
+                             (cuuint64_t)Hp * Wp * g.C * 4};
+    cuuint32_t box[5] = {32, (cuuint32_t)p.fv_q, 1, 1, 1};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    CUresult r = g_enc_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(op.ptr), dims, strides, box,
+                             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 5 : 0;
+  }
   switch (op.mode) {
     case OP_KMAJOR: {
       if (op.ld % 4) return 0;
@@ -282,8 +298,9 @@ int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_b
     p.chunk_stages = chunk > 0 ? chunk : 16;
     p.a.tma = (mask & 1) ? make_tma(p, p.a, &p.tma_a) : 0;
     p.b.tma = (mask & 2) ? make_tma(p, p.b, &p.tma_b) : 0;
-    // the tap view's k order (n, p, padded q) exists only as tensor maps: no cp.async fallback
+    // the tap views' layouts exist only as tensor maps: no cp.async fallback
     if (p.wv_q && (p.a.tma != 4 || p.b.tma != 4)) return -(int)cudaErrorNotSupported;
+    if (p.fv_q && p.a.tma != 5) return -(int)cudaErrorNotSupported;
   }
   p.split_tf32 = variant == MONET_CONV_TF32 ? 0 : 1;
   p.m_tiles = (p.M + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM);
@@ -434,6 +451,39 @@ WView wgrad_view(int variant, const monet_conv_desc* d) {
 
 size_t align256(size_t b) { return (b + 255) / 256 * 256; }
 
+// Fprop "tap view" for narrow-channel inputs (the 7x7/2 stem, C = 4): the 4-channel im2col
+// boxes (16 B per pixel row, one TMA per filter tap) cap the stem forward at ~55 TF/s.
+// Instead the GEMM rows are (n, p, q padded to 128) -- one output row per M tile -- and the
+// reduction runs over k = (r, s*C + c padded to 32): every k-block is ONE tiled TMA box of
+// 128 x 32 floats over a zero-padded copy of the input (overlapping q rows), and the
+// weights are repacked to [K][R][32] with zeros for the padding.  Workspace = the padded
+// copy + the repacked weights, so it is the "splitk" (workspace) forward variant.
+struct FView {
+  bool on;
+  size_t pad_bytes, w_bytes;
+};
+
+FView fprop_view(int variant, const monet_conv_desc* d) {
+  FView v{};
+  if (variant != MONET_CONV_SPLITK || is_pointwise(d) || d->s * d->c > 32 || d->q > BM || d->c % 4) return v;
+  if ((long long)d->n * d->p * d->q < (1 << 15)) return v;  // small problems: the gather is fine
+  v.on = true;
+  const long long hp = (long long)(d->p - 1) * d->stride_h + d->r, wp = (long long)(d->q - 1) * d->stride_w + d->s;
+  // + slack: the last row's padded q (and j >= S*C) read up to one output row past the copy
+  v.pad_bytes = align256((size_t)d->n * hp * wp * d->c * sizeof(float) + (size_t)BM * d->stride_w * d->c * 4 + 4096);
+  v.w_bytes = align256((size_t)d->k * d->r * 32 * sizeof(float));
+  return v;
+}
+
+// w'[k][r][j] = w[k][r][s][c] for j = s*C + c < S*C, else 0
+__global__ void fview_weight_kernel(const float* __restrict__ w, float* __restrict__ wp, int K, int R, int S, int C) {
+  const int total = K * R * 32;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int j = i % 32, t = i / 32, r = t % R, k = t / R;
+    wp[i] = j < S * C ? w[((k * R + r) * S) * C + j] : 0.f;
+  }
+}
+
 // Wgrad of a narrow conv (K_out < 128 output channels, e.g. ResNet-50's 64-channel layer1):
 // the natural mapping M = K_out fills only half of every 128-row MMA.  Swapped, the GEMM
 // rows are the filter taps x input channels (M = R*S*C) and the columns the output
@@ -549,6 +599,10 @@ int monet_copy_async(void* dst, const void* src, size_t bytes, void* stream) {
 // ------------------------------------------------------------------- conv
 size_t monet_conv_ws_bytes(int variant, int pass, const monet_conv_desc* d) {
   if (check_desc(d)) return 0;
+  if (pass == MONET_PASS_FWD) {
+    const FView f = fprop_view(variant, d);
+    if (f.on) return f.pad_bytes + f.w_bytes;
+  }
   if (pass == MONET_PASS_BWD)
     return std::max(monet_conv_ws_bytes(variant, MONET_PASS_DGRAD, d), monet_conv_ws_bytes(variant, MONET_PASS_WGRAD, d));
   if (pass == MONET_PASS_DGRAD && use_phases(variant, d)) return 0;  // phase GEMMs never split K
@@ -563,6 +617,26 @@ size_t monet_conv_ws_bytes(int variant, int pass, const monet_conv_desc* d) {
 int monet_conv_fwd(int variant, const monet_conv_desc* d, const float* x, const float* w, float* y, void* ws,
                    size_t ws_bytes, void* stream) {
   if (int e = check_desc(d)) return e;
+  const FView f = fprop_view(variant, d);
+  if (f.on && ws != nullptr && ws_bytes >= f.pad_bytes + f.w_bytes && tma_available()) {
+    float* xp = static_cast<float*>(ws);
+    float* wp = reinterpret_cast<float*>(static_cast<char*>(ws) + f.pad_bytes);
+    const int hp = (d->p - 1) * d->stride_h + d->r, wpx = (d->q - 1) * d->stride_w + d->s;
+    wgrad_pad_kernel<<<ew_blocks((long long)d->n * hp * wpx * (d->c / 4)), kEwThreads, 0, S(stream)>>>(
+        x, xp, d->n, d->h, d->w, d->c, hp, wpx, d->pad_h, d->pad_w);
+    fview_weight_kernel<<<(d->k * d->r * 32 + 255) / 256, 256, 0, S(stream)>>>(w, wp, d->k, d->r, d->s, d->c);
+    GemmParams p{};
+    p.g = geom(d);
+    p.fv_q = BM;
+    p.M = d->n * d->p * BM;
+    p.N = d->k;
+    p.Kd = d->r * 32;
+    p.a = op_gather(OP_IM2COL_FPROP, xp, p.M);
+    p.b = op_kmajor(wp, d->k, p.Kd, p.Kd);
+    p.c = y;
+    p.ldc = d->k;
+    return launch_gemm(p, MONET_CONV_IMPLICIT, 0, nullptr, 0, S(stream));
+  }
   return launch_gemm(conv_params(MONET_PASS_FWD, d, x, w, y), variant, 0, ws, ws_bytes, S(stream));
 }
 

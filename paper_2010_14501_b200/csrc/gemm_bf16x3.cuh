@@ -309,6 +309,12 @@ struct Loader {
         tma_3d(dst, m, row0, p.ph.on ? p.ph.tap[kh] : kh, k - kh * op.kdiv, bar);
       }
     } else if constexpr (MODE == OP_IM2COL_FPROP) {
+      if (op.tma == 5) {  // fprop tap view: one box {32 (s, c), 128 q, filter row kb, p, n} per k-block
+        mbar_arrive_tx(bar, BM * BKR * 4);
+        const int t = row0 / p.fv_q;
+        tma_5d(dst, m, 0, 0, kb, t % g.P, t / g.P, bar);
+        return;
+      }
       if (op.tma == 3) {  // C < 32: the k-block spans 32 / C filter taps, one C-channel box each
         mbar_arrive_tx(bar, BM * BKR * 4);
         const int ntb = BKR / g.C;
@@ -696,9 +702,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
       const int nchunks = (nst + p.chunk_stages - 1) / p.chunk_stages;
       const int m = mt * kTileM + (int)rank * BM + quarter * 32 + lane;
       long long out_row = m;  // phase dgrad: scatter row (n, i, j) to dx[n][i*sh + a][j*sw + b]
+      bool row_ok = m < p.M;
       if (p.ph.on && m < p.M) {
         const int j = m % p.ph.Wp, t = m / p.ph.Wp, i = t % p.ph.Hp, n = t / p.ph.Hp;
         out_row = ((long long)n * p.g.H + i * p.g.sh + p.ph.a) * p.g.W + j * p.g.sw + p.ph.b;
+      }
+      if (p.fv_q) {  // fprop tap view: row (n, p, q < fv_q); q >= Q are padding rows
+        const int q = m % p.fv_q;
+        row_ok = row_ok && q < p.g.Q;
+        out_row = (long long)(m / p.fv_q) * p.g.Q + q;
       }
       for (int chunk = 0; chunk < nchunks; ++chunk) {
         // later chunks (and accumulate mode) add with fire-and-forget vector
@@ -712,7 +724,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
           float v[32];
           tmem_ld32(tmem_base + acc * NB + cc * 32 + ((uint32_t)(quarter * 32) << 16), v);
           const int n0 = nt * p.n_pitch + cc * 32;
-          if (m < p.M && n0 < p.N && cc * 32 < p.n_pitch) {
+          if (row_ok && n0 < p.N && cc * 32 < p.n_pitch) {
             float* dst;
             long long ld;
             if (p.epi == EPI_PARTIAL) {

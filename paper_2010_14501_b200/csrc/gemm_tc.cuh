@@ -88,6 +88,7 @@ struct GemmParams {
   int chunk_stages; // bf16x3: MMA stages accumulated in TMEM before a flush to fp32 memory
   int n_pitch;      // output columns per n-tile (BN, or R-segments x S*C for the wgrad tap view)
   int wv_q;         // wgrad tap view: output-row length padded to a multiple of 32 (0 = off)
+  int fv_q;         // fprop tap view: GEMM rows per output row (= BM; rows q >= Q are padding, 0 = off)
   const float* bias;  // bf16x3 EPI_STORE / split-K reduce: per-column bias added to the output (nullptr = none)
   unsigned long long* dbg_t;  // debug: per-CTA wait-time counters of the bf16x3 pipeline roles (nullptr = off)
   float* dbg_a;     // debug: bf16x3 A-split dumps the raw A operand [M][Kpad] here (nullptr = off)

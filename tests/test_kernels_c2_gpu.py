@@ -62,6 +62,25 @@ def test_stem_wgrad_c2(cuda, variant):
 
 
 @pytest.mark.parametrize("variant", ["implicit", "splitk"])
+def test_stem_fwd_c2(cuda, variant):
+    """7x7/2 stem forward over 2.31 M output pixels (splitk: the fprop tap view)."""
+    n, h, w, c, k = 184, 224, 224, 4, 64
+    g = torch.Generator(device=cuda).manual_seed(14)
+    x = torch.randn(n, h, w, c, device=cuda, generator=g)
+    wt = torch.randn(k, 7, 7, c, device=cuda, generator=g) / math.sqrt(196)
+    d = N.conv_desc(n, h, w, c, k, 7, 7, 2, 3)
+    lib = N.lib()
+    v = N.CONV_VARIANTS[variant]
+    ws_b = lib.conv_ws_bytes(v, N.PASS["fwd"], d)
+    assert (ws_b > 0) == (variant == "splitk")
+    ws = torch.empty(max(ws_b, 16), dtype=torch.uint8, device=cuda)
+    y = torch.full((n, d.p, d.q, k), float("nan"), device=cuda)
+    lib.conv_fwd(v, d, x.data_ptr(), wt.data_ptr(), y.data_ptr(), ws.data_ptr(), ws_b, stream())
+    ref = F.conv2d(x.double().permute(0, 3, 1, 2), wt.double().permute(0, 3, 1, 2), stride=2, padding=3)
+    assert rel(y, ref.permute(0, 2, 3, 1)) < REL_TC
+
+
+@pytest.mark.parametrize("variant", ["implicit", "splitk"])
 def test_layer1_3x3_wgrad_c2(cuda, variant):
     """layer1 3x3 64->64 over 577 k pixels."""
     _wgrad_case(cuda, 184, 56, 56, 64, 64, 3, 3, 1, 1, variant)

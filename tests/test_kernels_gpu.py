@@ -54,6 +54,7 @@ CONV_CASES = [
     (2, 12, 12, 64, 32, 3, 3, 2, 1),     # stride-2 dgrad gather, K = 32
     (21, 40, 40, 4, 160, 3, 3, 1, 1),    # wgrad tap view (>= 32K pixels): two m-tiles, q padded 40 -> 64
     (2, 350, 202, 8, 64, 5, 5, 2, 2),    # wgrad tap view: 3 filter rows (120 columns) per n-tile, Q = 101
+    (8, 129, 127, 4, 64, 7, 7, 2, 3),    # splitk fprop tap view (C*S <= 32, Q <= 128, >= 32K pixels)
 ]
 
 
