@@ -29,11 +29,15 @@ int64_t place(const std::vector<int64_t>& order, const int64_t* sizes, const int
   std::vector<std::pair<int64_t, int64_t>> busy;
   int64_t peak = 0;
   for (int64_t idx : order) {
-    const int64_t need = rnd(std::max<int64_t>(sizes[idx], 1));
+    const int64_t need = rnd(sizes[idx]);
+    if (need == 0) {  // zero-byte blocks (e.g. a split conv's wgrad anchor) take no space
+      offs[idx] = 0;
+      continue;
+    }
     busy.clear();
     for (int64_t j : placed)
       if (t_alloc[j] < t_free[idx] && t_alloc[idx] < t_free[j])
-        busy.emplace_back(offs[j], offs[j] + rnd(std::max<int64_t>(sizes[j], 1)));
+        busy.emplace_back(offs[j], offs[j] + rnd(sizes[j]));
     std::sort(busy.begin(), busy.end());
     int64_t best = -1, best_gap = INT64_MAX, cursor = 0;
     for (auto& b : busy) {
@@ -74,8 +78,8 @@ extern "C" int monet_arena_plan(int64_t count, const int64_t* sizes, const int64
   auto rnd = [&](int64_t v) { return (v + align - 1) / align * align; };
   std::vector<int64_t> live(horizon + 1, 0);  // live rounded bytes per event time
   for (int64_t i = 0; i < count; ++i) {
-    live[t_alloc[i]] += rnd(std::max<int64_t>(sizes[i], 1));
-    live[t_free[i]] -= rnd(std::max<int64_t>(sizes[i], 1));
+    live[t_alloc[i]] += rnd(sizes[i]);
+    live[t_free[i]] -= rnd(sizes[i]);
   }
   int64_t t_peak = 0, run = 0, best_live = -1;
   for (int64_t t = 0; t < horizon; ++t) {

@@ -259,9 +259,11 @@ def ilp_relaxation(g: Graph, cat: Catalog, budget: int, mip_time_s: float | None
             from .schedule import decode
 
             x = [int(round(v)) for v in res.x]
-            if evaluate_assignment(m, x)["feasible"]:
+            out["mip_s0"] = {v.node for j, v in enumerate(m.var_ids) if v.kind == "S" and v.row == 0 and x[j]}
+            ev = evaluate_assignment(m, x)
+            if ev["feasible"]:
                 class _R:  # the fields decode() reads from a solver result
-                    status, assignment, model = "feasible-gap", x, m
+                    status, assignment, model, objective = "feasible-gap", x, m, ev["objective"]
                 try:
                     out["mip_schedule"] = decode(_R, g, cat)
                 except ValueError:
@@ -294,13 +296,18 @@ def plan_schedule(g: Graph, cat: Catalog, budget: int, kinds: dict | None = None
     if relax and relax["s0"]:
         for thr in LP_THRESHOLDS:
             seeds.append((f"lp{thr:g}", {u for u, val in relax["s0"].items() if val >= thr}))
+    if relax and relax.get("mip_s0"):  # the MIP incumbent's forward store set, rebuilt by demand
+        seeds.append(("mip", relax["mip_s0"]))
     sch, info = _plan_heuristic(g, cat, budget, kinds, exchange, seeds)
     if relax is not None:
         mip = relax.get("mip_schedule")
         if mip is not None and (sch is None or mip.objective < sch.objective):
             ok, peak, _ = FastBound(g, compute_dependency_sets(g, "upper"), cat).check(mip, budget)
-            if ok:
+            try:  # an ILP-feasible decode the simulator rejects is not executable
                 simulate(mip, g, cat)
+            except SimulationError:
+                ok = False
+            if ok:
                 se = info.get("se_cost")
                 info = {"family": "ilp-highs/feasible", "candidates": info["candidates"], "modeled_peak": peak,
                         "objective": str(mip.objective), "se_cost": se,

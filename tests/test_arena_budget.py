@@ -25,15 +25,18 @@ _NETS = {}
 
 def _net(path):
     """(network, graph, catalog) a schedule file was planned for
-    (name: arch[_fused]_b<batch>_<image>_<budget>gib, image 224 or HxW)."""
+    (name: arch[_fused][_split]_b<batch>_<image>_<budget>gib, image 224 or HxW)."""
     stem = path.name.split("_b")[0]
-    arch, fused = stem.removesuffix("_fused"), stem.endswith("_fused")
+    split = stem.endswith("_split")
+    base = stem.removesuffix("_split")
+    arch, fused = base.removesuffix("_fused"), base.endswith("_fused")
     batch, image = path.name.split("_b")[1].split("_")[:2]
     batch = int(batch)
-    key = (arch, fused, batch, image)
+    key = (arch, fused, split, batch, image)
     if key not in _NETS:
         from paper_2010_14501_b200.tracer import default_classes, parse_image
-        net = build_network(arch, batch, parse_image(image), num_classes=default_classes(arch), fuse=fused)
+        net = build_network(arch, batch, parse_image(image), num_classes=default_classes(arch), fuse=fused,
+                            split=split)
         g = M.load_graph(net.graph_doc())
         cpath = ROOT / "profiles" / f"catalog_{stem}_b{batch}_{image}.json"
         cdoc = json.loads(cpath.read_text())["catalog"] if cpath.exists() else net.catalog_doc()
