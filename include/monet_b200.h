@@ -117,6 +117,23 @@ int monet_conv_fwd_bias(int variant, const monet_conv_desc* d, const float* x, c
                         float* y, void* ws, size_t ws_bytes, void* stream);
 int monet_bias_grad(const float* dy, float* db, int64_t rows, int c, int accumulate, void* scratch, void* stream);
 
+/* Pre-split weights: the bf16x3 GEMM splits every fp32 operand element into
+ * hi = bf16(x), lo = bf16(x - hi) (round to nearest even).  The weights change only at
+ * the optimizer step, so an executor keeps their split in two bf16 planes (w_hi, w_lo:
+ * the same element offsets as w) refreshed once per step, and the conv forward / input
+ * gradient load them by TMA straight into the MMA tiles (no per-tile B split).  Results
+ * are bit-identical to monet_conv_fwd[_bias] / monet_conv_dgrad, which these fall back to
+ * when the shape or alignment does not allow it (w_hi == NULL: always).  bias may be NULL.
+ * split_bf16_segments: table (device memory) holds nseg x {src_off, dst_off, count}
+ * (elements), max_count >= every count. */
+int monet_conv_fwd_w16(int variant, const monet_conv_desc* d, const float* x, const float* w, const uint16_t* w_hi,
+                       const uint16_t* w_lo, const float* bias, float* y, void* ws, size_t ws_bytes, void* stream);
+int monet_conv_dgrad_w16(int variant, const monet_conv_desc* d, const float* dy, const float* w, const uint16_t* w_hi,
+                         const uint16_t* w_lo, float* dx, int accumulate, void* ws, size_t ws_bytes, void* stream);
+int monet_split_bf16(const float* src, uint16_t* hi, uint16_t* lo, int64_t n, void* stream);
+int monet_split_bf16_segments(const float* src, uint16_t* hi, uint16_t* lo, const int64_t* table, int nseg,
+                              int64_t max_count, void* stream);
+
 /* --- dropout (VGG / MobileNet-V2 / GoogleNet classifiers) ------------------------
  * keep(i) <=> splitmix64(seed*0x9E3779B97F4A7C15 + salt*0xD1B54A32D192ED03 + i) >> 40 >= floor(p*2^24),
  * i = element index in NHWC order; y = keep ? x / (1-p) : 0.  The mask is never stored:

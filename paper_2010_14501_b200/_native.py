@@ -50,6 +50,10 @@ SIGNATURES = {
     "monet_conv_wgrad": (_i32, [_i32, _PCONV, _vp, _vp, _vp, _i32, _vp, _sz, _vp]),
     "monet_conv_fwd_bias": (_i32, [_i32, _PCONV, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "monet_bias_grad": (_i32, [_vp, _vp, _i64, _i32, _i32, _vp, _vp]),
+    "monet_conv_fwd_w16": (_i32, [_i32, _PCONV, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "monet_conv_dgrad_w16": (_i32, [_i32, _PCONV, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _sz, _vp]),
+    "monet_split_bf16": (_i32, [_vp, _vp, _vp, _i64, _vp]),
+    "monet_split_bf16_segments": (_i32, [_vp, _vp, _vp, _vp, _i32, _i64, _vp]),
     "monet_dropout_fwd": (_i32, [_vp, _vp, _i64, _f32, _vp, C.c_uint64, _vp]),
     "monet_dropout_bwd": (_i32, [_vp, _vp, _i64, _f32, _vp, C.c_uint64, _i32, _vp]),
     "monet_seed_advance": (_i32, [_vp, _vp]),

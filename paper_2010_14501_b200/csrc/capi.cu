@@ -73,14 +73,14 @@ int launch_inst(const GemmParams& p, int grid, cudaStream_t st) {
   if constexpr (kBx3) {
     auto kern = bx3::gemm_bf16x3_kernel<AM, BMODE, kPair, NB>;
     if (!attr) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bx3::kSmemBytes);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bx3::Cfg<BMODE, NB>::kSmemBytes);
       attr = true;
     }
     if constexpr (kPair) {  // CTA pairs: clusters of 2 (the two SMs of a TPC)
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3(grid);
       cfg.blockDim = dim3(bx3::kThreads);
-      cfg.dynamicSmemBytes = bx3::kSmemBytes;
+      cfg.dynamicSmemBytes = bx3::Cfg<BMODE, NB>::kSmemBytes;
       cfg.stream = st;
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeClusterDimension;
@@ -92,7 +92,7 @@ int launch_inst(const GemmParams& p, int grid, cudaStream_t st) {
       cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
       return e == cudaSuccess ? 0 : -(int)e;
     } else {
-      kern<<<grid, bx3::kThreads, bx3::kSmemBytes, st>>>(p);
+      kern<<<grid, bx3::kThreads, bx3::Cfg<BMODE, NB>::kSmemBytes, st>>>(p);
     }
   } else {
     if (!attr) {
@@ -114,9 +114,18 @@ int dispatch_modes(const GemmParams& p, int grid, cudaStream_t st) {
   if (a == OP_MNMAJOR && b == OP_IM2COL_WGRAD) return launch_inst<kBx3, kPair, OP_MNMAJOR, OP_IM2COL_WGRAD, NB>(p, grid, st);
   if (a == OP_MNMAJOR && b == OP_MNMAJOR) return launch_inst<kBx3, kPair, OP_MNMAJOR, OP_MNMAJOR, NB>(p, grid, st);
   if (a == OP_MNMAJOR && b == OP_KMAJOR) return launch_inst<kBx3, kPair, OP_MNMAJOR, OP_KMAJOR, NB>(p, grid, st);
-  if constexpr (kBx3)  // swapped wgrad of narrow convs: A = im2col(x)^T, B = dy^T
+  if constexpr (kBx3) {  // swapped wgrad of narrow convs: A = im2col(x)^T, B = dy^T
     if (a == OP_IM2COL_WGRAD && b == OP_MNMAJOR)
       return launch_inst<kBx3, kPair, OP_IM2COL_WGRAD, OP_MNMAJOR, NB>(p, grid, st);
+    if constexpr (!kPair) {  // pre-split bf16 weights (fprop B = w, dgrad B = w^T)
+      if (a == OP_IM2COL_FPROP && b == OP_W16_KMAJOR)
+        return launch_inst<kBx3, kPair, OP_IM2COL_FPROP, OP_W16_KMAJOR, NB>(p, grid, st);
+      if (a == OP_KMAJOR && b == OP_W16_KMAJOR) return launch_inst<kBx3, kPair, OP_KMAJOR, OP_W16_KMAJOR, NB>(p, grid, st);
+      if (a == OP_IM2COL_DGRAD && b == OP_W16_MNMAJOR)
+        return launch_inst<kBx3, kPair, OP_IM2COL_DGRAD, OP_W16_MNMAJOR, NB>(p, grid, st);
+      if (a == OP_KMAJOR && b == OP_W16_MNMAJOR) return launch_inst<kBx3, kPair, OP_KMAJOR, OP_W16_MNMAJOR, NB>(p, grid, st);
+    }
+  }
   return -(int)cudaErrorInvalidValue;
 }
 
@@ -148,6 +157,17 @@ int tiled_map(CUtensorMap* m, const float* ptr, int rank, const cuuint64_t* dims
   CUresult r = g_enc_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<float*>(ptr), dims, strides, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 1 : 0;
+}
+
+// bf16 planes (pre-split weights): SWIZZLE_128B boxes of 64 bf16 = 128 B rows, the
+// MMA's stage-tile layout as loaded
+int tiled_map_bf16(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+                   const cuuint32_t* box) {
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = g_enc_tiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 1 : 0;
 }
 
@@ -213,6 +233,22 @@ int make_tma(GemmParams& p, Operand& op, CUtensorMap* m) {
     return r == CUDA_SUCCESS ? 5 : 0;
   }
   switch (op.mode) {
+    case OP_W16_KMAJOR: {  // hi / lo planes [rows][ld]: {k, row, plane}, one 64 x rows_box box per plane
+      if (op.ld % 8 || op.plane <= 0 || op.plane % 16) return 0;
+      cuuint64_t dims[3] = {(cuuint64_t)p.Kd, (cuuint64_t)op.rows, 2};
+      cuuint64_t strides[2] = {(cuuint64_t)op.ld * 2, (cuuint64_t)op.plane};
+      cuuint32_t box[3] = {64, (cuuint32_t)op.rows_box, 1};
+      return tiled_map_bf16(m, op.ptr, 3, dims, strides, box);
+    }
+    case OP_W16_MNMAJOR: {  // w^T: {row (= c), tap, kout, plane}, boxes of 64 channels x 32 kout
+      if (op.kdiv % 32 || op.ld % 8 || op.ks1 % 8 || op.plane <= 0 || op.plane % 16) return 0;
+      if (!p.ph.on && p.Kd % op.kdiv) return 0;
+      const int ntaps = p.ph.on ? g.R * g.S : p.Kd / op.kdiv;
+      cuuint64_t dims[4] = {(cuuint64_t)op.rows, (cuuint64_t)ntaps, (cuuint64_t)op.kdiv, 2};
+      cuuint64_t strides[3] = {(cuuint64_t)op.ks1 * 2, (cuuint64_t)op.ld * 2, (cuuint64_t)op.plane};
+      cuuint32_t box[4] = {64, 1, 32, 1};
+      return tiled_map_bf16(m, op.ptr, 4, dims, strides, box);
+    }
     case OP_KMAJOR: {
       if (op.ld % 4) return 0;
       cuuint64_t dims[2] = {(cuuint64_t)p.Kd, (cuuint64_t)op.rows};
@@ -277,6 +313,10 @@ int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_b
   p.dbg_a = g_dbg_a;
   p.dbg_b = g_dbg_b;
   p.dbg_t = g_dbg_t;
+#ifdef MONET_DEBUG
+  static const int dbg_mode = getenv("MONET_DBG_MODE") ? atoi(getenv("MONET_DBG_MODE")) : 0;
+  p.dbg_mode = dbg_mode;
+#endif
   const bool bx = uses_bx3(variant);
   // variant "pair" (cta_group::2, 256-row tiles) is retired: 15-25 % slower than one CTA per
   // tile on every ResNet-50 shape, and one wrong-tile result seen in round-2 GPU testing that
@@ -301,6 +341,8 @@ int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_b
     // the tap views' layouts exist only as tensor maps: no cp.async fallback
     if (p.wv_q && (p.a.tma != 4 || p.b.tma != 4)) return -(int)cudaErrorNotSupported;
     if (p.fv_q && p.a.tma != 5) return -(int)cudaErrorNotSupported;
+    // pre-split weights load only by TMA; the caller then takes the fp32 path
+    if (mode_is_w16(p.b.mode) && !p.b.tma) return -(int)cudaErrorNotSupported;
   }
   p.split_tf32 = variant == MONET_CONV_TF32 ? 0 : 1;
   p.m_tiles = (p.M + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM);
@@ -332,6 +374,45 @@ int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_b
 }
 
 bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// Launch with the weight operand B taken from its pre-split bf16 planes (hi, lo: the
+// same element offsets as the fp32 weights at p.b.ptr) when the shape allows it, else
+// (or without planes) from the fp32 weights: the two give bit-identical results, the
+// split being the one the B-split warps would do (split_pair).
+int launch_gemm_w16(const GemmParams& p, const uint16_t* hi, const uint16_t* lo, int variant, int accumulate,
+                    void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (hi != nullptr && lo != nullptr && lo > hi && uses_bx3(variant) && al16(hi) &&
+      (p.b.mode == OP_KMAJOR || p.b.mode == OP_MNMAJOR)) {
+    GemmParams q = p;
+    q.b.mode = p.b.mode == OP_KMAJOR ? OP_W16_KMAJOR : OP_W16_MNMAJOR;
+    q.b.ptr = reinterpret_cast<const float*>(hi);
+    q.b.plane = reinterpret_cast<const char*>(lo) - reinterpret_cast<const char*>(hi);
+    const int e = launch_gemm(q, variant, accumulate, ws, ws_bytes, st);
+    if (e != -(int)cudaErrorNotSupported) return e;
+  }
+  return launch_gemm(p, variant, accumulate, ws, ws_bytes, st);
+}
+
+// hi = bf16(x), lo = bf16(x - hi), round to nearest even: the B split's own rounding
+__device__ __forceinline__ void split_one(float x, uint16_t& h, uint16_t& l) {
+  uint32_t h2, l2;
+  bx3::split_pair(x, 0.f, h2, l2);  // element x in the low halves
+  h = (uint16_t)(h2 & 0xFFFFu);
+  l = (uint16_t)(l2 & 0xFFFFu);
+}
+
+__global__ void split_bf16_kernel(const float* __restrict__ src, uint16_t* hi, uint16_t* lo, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    split_one(src[i], hi[i], lo[i]);
+}
+
+// segments {src_off, dst_off, count} (elements), one grid row per segment
+__global__ void split_bf16_segments_kernel(const float* __restrict__ src, uint16_t* hi, uint16_t* lo,
+                                           const long long* __restrict__ table) {
+  const long long s0 = table[3 * blockIdx.y], d0 = table[3 * blockIdx.y + 1], n = table[3 * blockIdx.y + 2];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    split_one(src[s0 + i], hi[d0 + i], lo[d0 + i]);
+}
 
 Operand op_kmajor(const float* ptr, int rows, long long ld, int kd) {
   return Operand{OP_KMAJOR, rows, ptr, ld, 1 << 30, 0, (al16(ptr) && ld % 4 == 0 && kd % 4 == 0) ? 1 : 0};
@@ -614,8 +695,8 @@ size_t monet_conv_ws_bytes(int variant, int pass, const monet_conv_desc* d) {
   return gemm_ws(variant, p.M, p.N, p.Kd);
 }
 
-int monet_conv_fwd(int variant, const monet_conv_desc* d, const float* x, const float* w, float* y, void* ws,
-                   size_t ws_bytes, void* stream) {
+static int conv_fwd_impl(int variant, const monet_conv_desc* d, const float* x, const float* w, const uint16_t* w_hi,
+                         const uint16_t* w_lo, float* y, void* ws, size_t ws_bytes, void* stream) {
   if (int e = check_desc(d)) return e;
   const FView f = fprop_view(variant, d);
   if (f.on && ws != nullptr && ws_bytes >= f.pad_bytes + f.w_bytes && tma_available()) {
@@ -637,22 +718,56 @@ int monet_conv_fwd(int variant, const monet_conv_desc* d, const float* x, const 
     p.ldc = d->k;
     return launch_gemm(p, MONET_CONV_IMPLICIT, 0, nullptr, 0, S(stream));
   }
-  return launch_gemm(conv_params(MONET_PASS_FWD, d, x, w, y), variant, 0, ws, ws_bytes, S(stream));
+  return launch_gemm_w16(conv_params(MONET_PASS_FWD, d, x, w, y), w_hi, w_lo, variant, 0, ws, ws_bytes, S(stream));
+}
+
+int monet_conv_fwd(int variant, const monet_conv_desc* d, const float* x, const float* w, float* y, void* ws,
+                   size_t ws_bytes, void* stream) {
+  return conv_fwd_impl(variant, d, x, w, nullptr, nullptr, y, ws, ws_bytes, stream);
 }
 
 static int bn_blocks(int64_t rows);
 
-int monet_conv_fwd_bias(int variant, const monet_conv_desc* d, const float* x, const float* w, const float* bias,
-                        float* y, void* ws, size_t ws_bytes, void* stream) {
+static int conv_fwd_bias_impl(int variant, const monet_conv_desc* d, const float* x, const float* w,
+                              const uint16_t* w_hi, const uint16_t* w_lo, const float* bias, float* y, void* ws,
+                              size_t ws_bytes, void* stream) {
   if (int e = check_desc(d)) return e;
   GemmParams p = conv_params(MONET_PASS_FWD, d, x, w, y);
   if (uses_bx3(variant)) {  // bias added in the epilogue (or the split-K reduce)
     p.bias = bias;
-    return launch_gemm(p, variant, 0, ws, ws_bytes, S(stream));
+    return launch_gemm_w16(p, w_hi, w_lo, variant, 0, ws, ws_bytes, S(stream));
   }
   const long long tot = (long long)p.M * p.N;
   bias_fill_kernel<<<(int)((tot + 255) / 256), 256, 0, S(stream)>>>(y, bias, p.M, p.N);
   return launch_gemm(p, variant, 1, ws, ws_bytes, S(stream));
+}
+
+int monet_conv_fwd_bias(int variant, const monet_conv_desc* d, const float* x, const float* w, const float* bias,
+                        float* y, void* ws, size_t ws_bytes, void* stream) {
+  return conv_fwd_bias_impl(variant, d, x, w, nullptr, nullptr, bias, y, ws, ws_bytes, stream);
+}
+
+int monet_conv_fwd_w16(int variant, const monet_conv_desc* d, const float* x, const float* w, const uint16_t* w_hi,
+                       const uint16_t* w_lo, const float* bias, float* y, void* ws, size_t ws_bytes, void* stream) {
+  if (bias != nullptr) return conv_fwd_bias_impl(variant, d, x, w, w_hi, w_lo, bias, y, ws, ws_bytes, stream);
+  return conv_fwd_impl(variant, d, x, w, w_hi, w_lo, y, ws, ws_bytes, stream);
+}
+
+int monet_split_bf16(const float* src, uint16_t* hi, uint16_t* lo, int64_t n, void* stream) {
+  if (n < 0) return -(int)cudaErrorInvalidValue;
+  if (n == 0) return 0;
+  split_bf16_kernel<<<ew_blocks(n), kEwThreads, 0, S(stream)>>>(src, hi, lo, n);
+  return last_error();
+}
+
+int monet_split_bf16_segments(const float* src, uint16_t* hi, uint16_t* lo, const int64_t* table, int nseg,
+                              int64_t max_count, void* stream) {
+  if (nseg < 0 || nseg > 65535 || max_count < 0) return -(int)cudaErrorInvalidValue;
+  if (nseg == 0 || max_count == 0) return 0;
+  const int bx = (int)std::min<int64_t>((max_count + kEwThreads - 1) / kEwThreads, 8 * kNumSMs / std::max(1, nseg / 8 + 1));
+  split_bf16_segments_kernel<<<dim3(std::max(bx, 1), nseg), kEwThreads, 0, S(stream)>>>(
+      src, hi, lo, reinterpret_cast<const long long*>(table));
+  return last_error();
 }
 
 int monet_bias_grad(const float* dy, float* db, int64_t rows, int c, int accumulate, void* scratch, void* stream) {
@@ -691,8 +806,9 @@ int monet_seed_advance(unsigned long long* seed, void* stream) {
   return last_error();
 }
 
-int monet_conv_dgrad(int variant, const monet_conv_desc* d, const float* dy, const float* w, float* dx,
-                     int accumulate, void* ws, size_t ws_bytes, void* stream) {
+static int conv_dgrad_impl(int variant, const monet_conv_desc* d, const float* dy, const float* w,
+                           const uint16_t* w_hi, const uint16_t* w_lo, float* dx, int accumulate, void* ws,
+                           size_t ws_bytes, void* stream) {
   if (int e = check_desc(d)) return e;
   if (use_phases(variant, d)) {  // stride > 1: one stride-1 GEMM per output parity class
     for (int a = 0; a < d->stride_h; ++a)
@@ -705,12 +821,24 @@ int monet_conv_dgrad(int variant, const monet_conv_desc* d, const float* dy, con
                                       S(stream)>>>(dx, d->n, d->h, d->w, d->c, a, b, d->stride_h, d->stride_w);
           continue;
         }
-        if (int e = launch_gemm(phase_params(d, ph, dy, w, dx), variant, accumulate, ws, ws_bytes, S(stream)))
+        if (int e = launch_gemm_w16(phase_params(d, ph, dy, w, dx), w_hi, w_lo, variant, accumulate, ws, ws_bytes,
+                                    S(stream)))
           return e;
       }
     return last_error();
   }
-  return launch_gemm(conv_params(MONET_PASS_DGRAD, d, dy, w, dx), variant, accumulate, ws, ws_bytes, S(stream));
+  return launch_gemm_w16(conv_params(MONET_PASS_DGRAD, d, dy, w, dx), w_hi, w_lo, variant, accumulate, ws, ws_bytes,
+                         S(stream));
+}
+
+int monet_conv_dgrad(int variant, const monet_conv_desc* d, const float* dy, const float* w, float* dx,
+                     int accumulate, void* ws, size_t ws_bytes, void* stream) {
+  return conv_dgrad_impl(variant, d, dy, w, nullptr, nullptr, dx, accumulate, ws, ws_bytes, stream);
+}
+
+int monet_conv_dgrad_w16(int variant, const monet_conv_desc* d, const float* dy, const float* w, const uint16_t* w_hi,
+                         const uint16_t* w_lo, float* dx, int accumulate, void* ws, size_t ws_bytes, void* stream) {
+  return conv_dgrad_impl(variant, d, dy, w, w_hi, w_lo, dx, accumulate, ws, ws_bytes, stream);
 }
 
 int monet_conv_wgrad(int variant, const monet_conv_desc* d, const float* x, const float* dy, float* dw,

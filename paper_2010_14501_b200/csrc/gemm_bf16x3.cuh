@@ -42,12 +42,8 @@ namespace bx3 {
 constexpr int BM = 128, BN = 128;
 constexpr int BKR = 32;              // raw k-block (fp32, 128B rows)
 constexpr int BKS = 64;              // MMA stage (bf16, 128B rows) = 2 raw k-blocks
-constexpr int kRawSlots = 4;
 constexpr int kRawTile = BM * BKR * 4;          // 16 KB (A or B raw, fp32)
-constexpr int kRawBytes = 2 * kRawTile;          // A + B
-constexpr int kStages = 3;                       // MMA stages (TMEM A + smem B)
-constexpr int kBTile = BN * BKS * 2;             // 16 KB (bf16 hi or lo)
-constexpr int kStageBytes = 2 * kBTile;          // B hi + B lo
+constexpr int kAStages = 3;                      // MMA stages of A (TMEM)
 constexpr int kLoaderWarps = 4, kASplitWarps = 8, kBSplitWarps = 8, kEpiWarps = 4;
 constexpr int kLoaderThreads = kLoaderWarps * 32;
 constexpr int kWarpASplit = kLoaderWarps;                       // 4
@@ -59,14 +55,30 @@ constexpr int kAccStages = 2;
 constexpr int kTmemCols = 512;
 constexpr int kTmemA = kAccStages * BN;          // A stages start at column 256
 constexpr int kAStageCols = 64;                  // 32 cols hi + 32 cols lo (bf16x2 per column)
-constexpr int kNumBars = 2 * kRawSlots + 3 * kStages + 2 * kAccStages;
-constexpr int kSmemBytes = kRawSlots * kRawBytes + kStages * kStageBytes + 1024 + 8 * kNumBars + 16;
 static_assert(kLoaderThreads == 128, "loader threads: 64 per operand");
 constexpr int kOpLoaders = kLoaderThreads / 2;
 constexpr int kBSplitThreads = kBSplitWarps * 32;
 static_assert(kBSplitThreads == 256, "B split: 256 threads x 4 row groups");
-static_assert(kSmemBytes <= 232448, "shared memory budget");
-static_assert(kTmemA + kStages * kAStageCols <= kTmemCols, "TMEM budget");
+static_assert(kTmemA + kAStages * kAStageCols <= kTmemCols, "TMEM budget");
+
+// Shared-memory plan per B mode and N-tile width.  TMA delivery is latency bound (~2 us
+// per box under load, tools/tma_bw_probe.cu), so the plan maximises bytes in flight:
+//   fp32 B : raw slots hold an A and a B k-block, the B split fills bf16 stages;
+//   pre-split B (OP_W16_*): raw slots hold A only, and the B stages -- filled by TMA
+//            straight from the bf16 planes -- are deeper.
+// A 64-wide N tile (NB = 64) halves every B buffer, which buys more slots.
+template <int BMODE, int NB = BN>
+struct Cfg {
+  static constexpr bool kW16 = mode_is_w16(BMODE);
+  static constexpr int kBTile = NB * BKS * 2;                   // bf16 hi (or lo) stage tile
+  static constexpr int kStageBytes = 2 * kBTile;                // B hi + B lo
+  static constexpr int kRawSlots = kW16 ? (NB == BN ? 6 : 8) : (NB == BN ? 4 : 6);
+  static constexpr int kRawBytes = kW16 ? kRawTile : kRawTile + NB * BKR * 4;
+  static constexpr int kBStages = kW16 ? (NB == BN ? 4 : 6) : (NB == BN ? 3 : 4);
+  static constexpr int kNumBars = 2 * kRawSlots + 2 * kAStages + 2 * kBStages + 2 * kAccStages;
+  static constexpr int kSmemBytes = kRawSlots * kRawBytes + kBStages * kStageBytes + 1024 + 8 * kNumBars + 16;
+  static_assert(kSmemBytes <= 232448, "shared memory budget");
+};
 
 MONET_DEV void cp_async_mbar_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -170,6 +182,13 @@ MONET_DEV void tma_3d(uint32_t dst, const CUtensorMap* m, int x, int y, int z, u
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
       "[%5];" ::"r"(dst),
       "l"(m), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+MONET_DEV void tma_4d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2, int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+      "%5}], [%6];" ::"r"(dst),
+      "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
       : "memory");
 }
 MONET_DEV void tma_5d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2, int c3, int c4, uint64_t* bar) {
@@ -289,38 +308,39 @@ struct Loader {
     }
   }
 
+  // go == false: only advance the incremental im2col coordinates (another issuer owns kb)
   MONET_DEV void issue_tma(const GemmParams& p, const Operand& op, const CUtensorMap* m, int kb, uint8_t* tile,
-                           uint64_t* bar) {
+                           uint64_t* bar, bool go = true) {
     const ConvGeom& g = p.g;
     const uint32_t dst = smem_u32(tile);
     const int k = kb * BKR;
     if constexpr (MODE == OP_KMAJOR) {
-      mbar_arrive_tx(bar, op.rows_box * BKR * 4);
-      tma_2d(dst, m, k, row0, bar);
+      if (go) mbar_arrive_tx(bar, op.rows_box * BKR * 4);
+      if (go) tma_2d(dst, m, k, row0, bar);
     } else if constexpr (MODE == OP_MNMAJOR) {
-      mbar_arrive_tx(bar, op.rows_box * BKR * 4);
+      if (go) mbar_arrive_tx(bar, op.rows_box * BKR * 4);
       if (op.tma == 4) {  // wgrad tap view: dy as {kout, q, n*p}
         const int np = k / p.wv_q;
-        tma_3d(dst, m, row0, k - np * p.wv_q, np, bar);
+        if (go) tma_3d(dst, m, row0, k - np * p.wv_q, np, bar);
       } else if (op.kdiv >= p.Kd && !p.ph.on) {
-        tma_2d(dst, m, row0, k, bar);
+        if (go) tma_2d(dst, m, row0, k, bar);
       } else {  // k = tap * kdiv + kout, kdiv % 32 == 0: tensor {rows, taps, kdiv}
         const int kh = k / op.kdiv;
-        tma_3d(dst, m, row0, p.ph.on ? p.ph.tap[kh] : kh, k - kh * op.kdiv, bar);
+        if (go) tma_3d(dst, m, row0, p.ph.on ? p.ph.tap[kh] : kh, k - kh * op.kdiv, bar);
       }
     } else if constexpr (MODE == OP_IM2COL_FPROP) {
       if (op.tma == 5) {  // fprop tap view: one box {32 (s, c), 128 q, filter row kb, p, n} per k-block
-        mbar_arrive_tx(bar, BM * BKR * 4);
+        if (go) mbar_arrive_tx(bar, BM * BKR * 4);
         const int t = row0 / p.fv_q;
-        tma_5d(dst, m, 0, 0, kb, t % g.P, t / g.P, bar);
+        if (go) tma_5d(dst, m, 0, 0, kb, t % g.P, t / g.P, bar);
         return;
       }
       if (op.tma == 3) {  // C < 32: the k-block spans 32 / C filter taps, one C-channel box each
-        mbar_arrive_tx(bar, BM * BKR * 4);
+        if (go) mbar_arrive_tx(bar, BM * BKR * 4);
         const int ntb = BKR / g.C;
         for (int j = 0; j < ntb; ++j) {
           const bool valid = tap_r < g.R;
-          tma_im2col(dst + j * (BM * g.C * 4), m, valid ? 0 : g.C, cw, chh, cn, valid ? tap_s : 0,
+          if (go) tma_im2col(dst + j * (BM * g.C * 4), m, valid ? 0 : g.C, cw, chh, cn, valid ? tap_s : 0,
                      valid ? tap_r : 0, bar);
           if (++tap_s == g.S) {
             tap_s = 0;
@@ -333,7 +353,7 @@ struct Loader {
     if constexpr (MODE == OP_KMAJOR || MODE == OP_MNMAJOR) {
       // issued above
     } else if constexpr (MODE == OP_IM2COL_FPROP || MODE == OP_IM2COL_DGRAD) {
-      mbar_arrive_tx(bar, BM * BKR * 4);
+      if (go) mbar_arrive_tx(bar, BM * BKR * 4);
       const bool phs = MODE == OP_IM2COL_DGRAD && p.ph.on;
       if (k < p.Kd) {
         int ow, oh;
@@ -347,9 +367,9 @@ struct Loader {
           ow = g.S - 1 - tap_s;
           oh = g.R - 1 - tap_r;
         }
-        tma_im2col(dst, m, kin0, cw, chh, cn, ow, oh, bar);
+        if (go) tma_im2col(dst, m, kin0, cw, chh, cn, ow, oh, bar);
       } else {  // zero-padded tail k-block: out-of-range channel coordinate -> zero fill
-        tma_im2col(dst, m, MODE == OP_IM2COL_FPROP ? g.C : g.K, cw, chh, cn, 0, 0, bar);
+        if (go) tma_im2col(dst, m, MODE == OP_IM2COL_FPROP ? g.C : g.K, cw, chh, cn, 0, 0, bar);
       }
       const int cx = MODE == OP_IM2COL_FPROP ? g.C : g.K;
       kin0 += BKR;
@@ -361,12 +381,12 @@ struct Loader {
         }
       }
     } else if (op.tma == 4) {  // wgrad tap view: one box {S*C, 32 q, R-segments, 1, 1}
-      mbar_arrive_tx(bar, op.rows_box * BKR * 4);
+      if (go) mbar_arrive_tx(bar, op.rows_box * BKR * 4);
       const int np = k / p.wv_q, pp = np % g.P;
-      tma_5d(dst, m, 0, k - np * p.wv_q, tap_r, pp, np / g.P, bar);
+      if (go) tma_5d(dst, m, 0, k - np * p.wv_q, tap_r, pp, np / g.P, bar);
     } else {  // IM2COL_WGRAD: rows (tap, c) in segments of op.seg channels, k = 32 output pixels
       const int seg = op.seg;
-      mbar_arrive_tx(bar, op.rows_box * BKR * 4);
+      if (go) mbar_arrive_tx(bar, op.rows_box * BKR * 4);
       const int q = k % g.Q, t = k / g.Q, pp = t % g.P, n = t / g.P;
       const int w0 = q * g.sw - g.pw, h0 = pp * g.sh - g.ph;
       for (int sg = 0; sg < op.rows_box / seg; ++sg) {
@@ -376,7 +396,7 @@ struct Loader {
         // rows past R*S*C: the tap offset stays in range, the channel
         // coordinate is pushed out of bounds (zero fill)
         const bool valid = tap < g.R * g.S && k < p.Kd;
-        tma_im2col(dst + sg * (BKR * seg * 4), m, valid ? c : g.C, w0, h0, n, valid ? s : 0, valid ? r : 0, bar);
+        if (go) tma_im2col(dst + sg * (BKR * seg * 4), m, valid ? c : g.C, w0, h0, n, valid ? s : 0, valid ? r : 0, bar);
       }
     }
   }
@@ -439,6 +459,11 @@ template <int AM, int BMODE, bool PR, int NB>
 __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_constant__ GemmParams p) {
   static_assert(NB == BN || (NB == 64 && !PR), "tile widths: 128 (1 CTA or pair), 64 (1 CTA)");
   constexpr bool a_mn = mode_is_mn(AM), b_mn = mode_is_mn(BMODE);
+  using CF = Cfg<BMODE, NB>;
+  constexpr bool kW16 = CF::kW16;
+  constexpr int kRawSlots = CF::kRawSlots, kRawBytes = CF::kRawBytes, kBStages = CF::kBStages;
+  constexpr int kBTile = CF::kBTile, kStageBytes = CF::kStageBytes;
+  static_assert(!(kW16 && PR), "pre-split B: one CTA per tile");
   constexpr int kPairN = PR ? 2 : 1;          // CTAs per tile
   constexpr int kBRows = NB / kPairN;         // B rows this CTA splits
   constexpr int kBChunks = kBRows / 32;       // K-major 16B chunks per B-split thread per raw k-block
@@ -448,15 +473,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
   // round trip) so the compiler keeps the shared address space: LDS / STS
   // instead of generic LD / ST in the splitters
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* raw = smem;                                  // kRawSlots x (A, B) fp32
-  uint8_t* bst = smem + kRawSlots * kRawBytes;          // kStages x (B hi, B lo) bf16
-  uint64_t* bars = reinterpret_cast<uint64_t*>(bst + kStages * kStageBytes);
+  uint8_t* raw = smem;                                  // kRawSlots x (A[, B]) fp32
+  uint8_t* bst = smem + kRawSlots * kRawBytes;          // kBStages x (B hi, B lo) bf16
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bst + kBStages * kStageBytes);
   uint64_t* raw_full = bars;                            // loaders -> splitters
   uint64_t* raw_empty = raw_full + kRawSlots;           // splitters -> loaders
   uint64_t* a_full = raw_empty + kRawSlots;             // A-split -> MMA
-  uint64_t* b_full = a_full + kStages;                  // B-split -> MMA
-  uint64_t* st_empty = b_full + kStages;                // MMA commit -> splitters
-  uint64_t* tfull = st_empty + kStages;                 // MMA commit -> epilogue
+  uint64_t* b_full = a_full + kAStages;                 // B-split (or pre-split B TMA) -> MMA
+  uint64_t* a_empty = b_full + kBStages;                // MMA commit -> A-split
+  uint64_t* b_empty = a_empty + kAStages;               // MMA commit -> B-split / B loader
+  uint64_t* tfull = b_empty + kBStages;                 // MMA commit -> epilogue
   uint64_t* tempty = tfull + kAccStages;                // epilogue -> MMA
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAccStages);
 
@@ -476,6 +502,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
         mbar_arrive(bar);
     }
   };
+#ifdef MONET_DEBUG
+  const int dm = p.dbg_mode;
+#else
+  constexpr int dm = 0;
+#endif
   long long twait[16] = {0};
   float* const dbg_a = p.dbg_a;  // hoisted: loop-invariant kernel parameters
   float* const dbg_b = p.dbg_b;
@@ -483,13 +514,17 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRawSlots; ++s) {
-      mbar_init(&raw_full[s], (p.a.tma ? 1 : kOpLoaders) + (p.b.tma ? 1 : kOpLoaders));
-      mbar_init(&raw_empty[s], (kASplitWarps / 2 + kBSplitWarps) * 32);  // one A half + all of B per item
+      mbar_init(&raw_full[s], (p.a.tma ? 1 : kOpLoaders) + (kW16 ? 0 : (p.b.tma ? 1 : kOpLoaders)));
+      // one A half (+ all of B) per item
+      mbar_init(&raw_empty[s], (kASplitWarps / 2 + (kW16 ? 0 : kBSplitWarps)) * 32);
     }
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kAStages; ++s) {
       mbar_init(&a_full[s], kASplitWarps * kPairN);
-      mbar_init(&b_full[s], kBSplitWarps * kPairN);
-      mbar_init(&st_empty[s], 1);
+      mbar_init(&a_empty[s], 1);
+    }
+    for (int s = 0; s < kBStages; ++s) {
+      mbar_init(&b_full[s], kW16 ? 1 : kBSplitWarps * kPairN);
+      mbar_init(&b_empty[s], 1);
     }
     for (int a = 0; a < kAccStages; ++a) {
       mbar_init(&tfull[a], 1);
@@ -515,30 +550,80 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
     // ---------------------------------------------------------------- loaders
     const int sub = threadIdx.x % kOpLoaders;
     const bool is_b = threadIdx.x >= kOpLoaders;
+    if constexpr (kW16) {
+      // pre-split B: one thread streams each 64-deep stage's bf16 hi / lo boxes straight
+      // into the B stage tiles (K-major: one box per plane; MN-major: 64-channel chunks x
+      // two 32-deep k halves per plane)
+      if (is_b && (sub & 31) == 0) {  // two issuers (lane 0 of each B loader warp), alternating stages
+        const int iss = sub >> 5;
+        int sitem = 0;
+        for (int tile = unit0; tile < n_tiles_total; tile += n_units) {
+          int mt, nt, kb0, nst;
+          tile_range(p, tile, mt, nt, kb0, nst);
+          const int n0 = nt * p.n_pitch;
+          for (int s = 0; s < nst; ++s, ++sitem) {
+            if ((sitem & 1) != iss) continue;
+            const int sb = sitem % kBStages;
+            TWAIT(0, mbar_wait(&b_empty[sb], ((sitem / kBStages) & 1) ^ 1));
+            const uint32_t hi = smem_u32(bst + sb * kStageBytes), lo = hi + kBTile;
+            uint64_t* bar = &b_full[sb];
+            const int k0 = (kb0 + 2 * s) * BKR;
+            if constexpr (BMODE == OP_W16_KMAJOR) {
+              mbar_arrive_tx(bar, 2 * p.b.rows_box * 128);
+              tma_3d(hi, &p.tma_b, k0, n0, 0, bar);
+              tma_3d(lo, &p.tma_b, k0, n0, 1, bar);
+            } else {
+              const int nch = (p.b.rows_box + 63) / 64;
+              mbar_arrive_tx(bar, 2 * 2 * nch * (BKR * 128));
+              for (int h = 0; h < 2; ++h) {
+                const int k = k0 + h * BKR;
+                int tap = 0, ko = p.b.kdiv;  // past Kd (odd tail of the last split): zero fill
+                if (k < p.Kd) {
+                  const int kh = k / p.b.kdiv;
+                  ko = k - kh * p.b.kdiv;
+                  tap = p.ph.on ? p.ph.tap[kh] : kh;
+                }
+                for (int c = 0; c < nch; ++c) {
+                  const uint32_t off = c * (BKS * 128) + h * (BKR * 128);
+                  tma_4d(hi + off, &p.tma_b, n0 + 64 * c, tap, ko, 0, bar);
+                  tma_4d(lo + off, &p.tma_b, n0 + 64 * c, tap, ko, 1, bar);
+                }
+              }
+            }
+          }
+        }
+      }
+    }
     const Operand& op = is_b ? p.b : p.a;
-    const bool active = !op.tma || sub == 0;  // one thread issues a TMA operand
+    // TMA operands: lane 0 of each of the operand's two warps issues every other k-block --
+    // a thread issues about one box per ~500 clk (tools/tma_bw_probe.cu), so one issuer
+    // would cap delivery near 16 KB / 500 clk per SM; pre-split B is streamed above
+    const bool active = (kW16 && is_b) ? false : (!op.tma || (sub & 31) == 0);
+    const int issuer = op.tma ? sub >> 5 : 0;
     Loader<AM> la;
     Loader<BMODE> lb;
     int item = 0;
     for (int tile = active ? unit0 : n_tiles_total; tile < n_tiles_total; tile += n_units) {
       int mt, nt, kb0, nst;
       tile_range(p, tile, mt, nt, kb0, nst);
-      if (is_b)
-        lb.init(p, p.b, nt * p.n_pitch + (int)rank * kBRows, kb0 * BKR);
-      else
+      if (is_b) {
+        if constexpr (!kW16) lb.init(p, p.b, nt * p.n_pitch + (int)rank * kBRows, kb0 * BKR);
+      } else
         la.init(p, p.a, mt * kTileM + (int)rank * BM, kb0 * BKR);
       for (int kb = kb0; kb < kb0 + 2 * nst; ++kb, ++item) {
         const int slot = item % kRawSlots;
-        TWAIT(0, mbar_wait(&raw_empty[slot], ((item / kRawSlots) & 1) ^ 1));
+        if (!op.tma || (item & 1) == issuer) TWAIT(0, mbar_wait(&raw_empty[slot], ((item / kRawSlots) & 1) ^ 1));
         uint8_t* base = raw + slot * kRawBytes;
         if (is_b) {
-          if (op.tma)
-            lb.issue_tma(p, op, &p.tma_b, kb, base + kRawTile, &raw_full[slot]);
-          else
-            lb.issue_fallback(p, op, kb, sub, base + kRawTile, &raw_full[slot]);
+          if constexpr (!kW16) {
+            if (op.tma)
+              lb.issue_tma(p, op, &p.tma_b, kb, base + kRawTile, &raw_full[slot], (item & 1) == issuer);
+            else
+              lb.issue_fallback(p, op, kb, sub, base + kRawTile, &raw_full[slot]);
+          }
         } else {
           if (op.tma)
-            la.issue_tma(p, op, &p.tma_a, kb, base, &raw_full[slot]);
+            la.issue_tma(p, op, &p.tma_a, kb, base, &raw_full[slot], (item & 1) == issuer);
           else
             la.issue_fallback(p, op, kb, sub, base, &raw_full[slot]);
         }
@@ -557,14 +642,18 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
       tile_range(p, tile, mt, nt, kb0, nst);
       const int item_kb0 = kb0;
       for (int s = 0; s < nst; ++s, ++stage_item) {
-        const int stage = stage_item % kStages;
-        TWAIT(7, mbar_wait(&st_empty[stage], ((stage_item / kStages) & 1) ^ 1));
+        const int stage = stage_item % kAStages;
+        TWAIT(7, mbar_wait(&a_empty[stage], ((stage_item / kAStages) & 1) ^ 1));
         tc_fence_after();
         const uint32_t a_hi = tmem_base + lane_sel + kTmemA + stage * kAStageCols;
-        {
+        do {  // a block (the debug skip's continue leaves it)
           const int item = 2 * stage_item + half;
           const int slot = item % kRawSlots;
           TWAIT(8, mbar_wait(&raw_full[slot], (item / kRawSlots) & 1));
+          if (dm & 1) {
+            mbar_arrive(&raw_empty[slot]);
+            continue;
+          }
           const uint8_t* rt = raw + slot * kRawBytes;
           float v[32];
           if constexpr (a_mn) {  // segment-major (mn_off): p.a.seg rows per segment
@@ -609,7 +698,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
           mbar_arrive(&raw_empty[slot]);
           tmem_st<16>(a_hi + half * 16, hi);
           tmem_st<16>(a_hi + 32 + half * 16, lo);
-        }
+        } while (0);
         tmem_st_wait();
         tc_fence_before();
         arrive_leader(&a_full[stage]);
@@ -617,20 +706,25 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
     }
   } else if (warp < kWarpEpi) {
     // ---------------------------------------------------------------- B split -> smem bf16
+    if constexpr (!kW16) {  // (pre-split B needs no split: these warps idle)
     const int t = threadIdx.x - kWarpBSplit * 32;  // 0..255
     int item = 0, stage_item = 0;
     for (int tile = unit0; tile < n_tiles_total; tile += n_units) {
       int mt, nt, kb0, nst;
       tile_range(p, tile, mt, nt, kb0, nst);
       for (int s = 0; s < nst; ++s, ++stage_item) {
-        const int stage = stage_item % kStages;
-        TWAIT(9, mbar_wait(&st_empty[stage], ((stage_item / kStages) & 1) ^ 1));
+        const int stage = stage_item % kBStages;
+        TWAIT(9, mbar_wait(&b_empty[stage], ((stage_item / kBStages) & 1) ^ 1));
         uint8_t* bhi = bst + stage * kStageBytes;
         uint8_t* blo = bhi + kBTile;
 #pragma unroll 1
         for (int half = 0; half < 2; ++half, ++item) {
           const int slot = item % kRawSlots;
           TWAIT(10, mbar_wait(&raw_full[slot], (item / kRawSlots) & 1));
+          if (dm & 2) {
+            mbar_arrive(&raw_empty[slot]);
+            continue;
+          }
           const uint8_t* rt = raw + slot * kRawBytes + kRawTile;
           // K-major: a warp covers rows {0,4,1,5}+base so that the two rows of
           // one 16-lane STS.64 phase land in opposite swizzle halves.
@@ -689,6 +783,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
         arrive_leader(&b_full[stage]);
       }
     }
+    }  // !kW16
   } else if (warp < kWarpMma) {
     // ---------------------------------------------------------------- epilogue
     const int quarter = warp & 3;
@@ -724,7 +819,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
           float v[32];
           tmem_ld32(tmem_base + acc * NB + cc * 32 + ((uint32_t)(quarter * 32) << 16), v);
           const int n0 = nt * p.n_pitch + cc * 32;
-          if (row_ok && n0 < p.N && cc * 32 < p.n_pitch) {
+          if (row_ok && n0 < p.N && cc * 32 < p.n_pitch && !(dm & 8)) {
             float* dst;
             long long ld;
             if (p.epi == EPI_PARTIAL) {
@@ -809,29 +904,30 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * NB;
         for (int s = c0; s < c1; ++s, ++stage_item) {
-          const int stage = stage_item % kStages;
-          const uint32_t ph = (stage_item / kStages) & 1;
-          TWAIT(3, wait(&a_full[stage], ph));
-          TWAIT(4, wait(&b_full[stage], ph));
+          const int stage = stage_item % kAStages, bstage = stage_item % kBStages;
+          TWAIT(3, wait(&a_full[stage], (stage_item / kAStages) & 1));
+          TWAIT(4, wait(&b_full[bstage], (stage_item / kBStages) & 1));
           tc_fence_after();
           if (lane == 0) {
             const long long t_issue = p.dbg_t ? clock64() : 0;
             const uint32_t a_hi = tmem_base + kTmemA + stage * kAStageCols;
             const uint32_t a_lo = a_hi + 32;
-            const uint32_t bhi = smem_u32(bst + stage * kStageBytes);
+            const uint32_t bhi = smem_u32(bst + bstage * kStageBytes);
             const uint32_t blo = bhi + kBTile;
 #pragma unroll
-            for (int kk = 0; kk < BKS / 16; ++kk) {
+            for (int kk = 0; kk < ((dm & 4) ? 0 : BKS / 16); ++kk) {
               const uint32_t first = (s == c0 && kk == 0) ? 0u : 1u;
               mma_bf16_ts<PR>(d_tmem, a_lo + kk * 8, b_desc(bhi, b_mn, kk), idesc, first);
               mma_bf16_ts<PR>(d_tmem, a_hi + kk * 8, b_desc(blo, b_mn, kk), idesc, 1u);
               mma_bf16_ts<PR>(d_tmem, a_hi + kk * 8, b_desc(bhi, b_mn, kk), idesc, 1u);
             }
             if constexpr (PR) {
-              mma_commit_pair(&st_empty[stage]);
+              mma_commit_pair(&a_empty[stage]);
+              mma_commit_pair(&b_empty[bstage]);
               if (s == c1 - 1) mma_commit_pair(&tfull[acc]);
             } else {
-              mma_commit(&st_empty[stage]);
+              mma_commit(&a_empty[stage]);
+              mma_commit(&b_empty[bstage]);
               if (s == c1 - 1) mma_commit(&tfull[acc]);
             }
             if (p.dbg_t) twait[11] += clock64() - t_issue;

@@ -31,9 +31,17 @@ enum OperandMode : int {
   OP_IM2COL_FPROP = 2, // rows = output pixels (n,p,q), k = (r,s,c)             (K-major)
   OP_IM2COL_DGRAD = 3, // rows = input pixels (n,h,w), k = (r,s,kout) over dy   (K-major)
   OP_IM2COL_WGRAD = 4, // rows = (r,s,c), k = output pixel (n,p,q) over x       (MN-major)
+  // bf16x3 kernel only: the operand is already split into bf16 hi / lo planes in global
+  // memory (conv weights, split once per step); TMA loads them straight into the MMA's
+  // SWIZZLE_128B stage tiles -- no fp32 staging, no split warps
+  OP_W16_KMAJOR = 5,   // element(row,k) = plane[row*ld + k]                    (fprop B = w)
+  OP_W16_MNMAJOR = 6,  // element(row,k) = plane[(k/kdiv)*ks1 + (k%kdiv)*ld + row] (dgrad B = w^T)
 };
 
-__host__ __device__ constexpr bool mode_is_mn(int m) { return m == OP_MNMAJOR || m == OP_IM2COL_WGRAD; }
+__host__ __device__ constexpr bool mode_is_mn(int m) {
+  return m == OP_MNMAJOR || m == OP_IM2COL_WGRAD || m == OP_W16_MNMAJOR;
+}
+__host__ __device__ constexpr bool mode_is_w16(int m) { return m == OP_W16_KMAJOR || m == OP_W16_MNMAJOR; }
 
 struct ConvGeom {
   int N, H, W, C, K, R, S, P, Q, sh, sw, ph, pw;
@@ -55,6 +63,7 @@ struct Operand {
                 //   64-wide N tile)
   int seg;      // bf16x3 kernel, MN-major operands: rows per segment of the raw smem layout
                 //   (rows_box, or C when a wgrad im2col tile spans several filter taps)
+  long long plane;  // OP_W16_*: bytes from the hi plane (ptr) to the lo plane
 };
 
 enum EpiMode : int { EPI_STORE = 0, EPI_ACCUM = 1, EPI_PARTIAL = 2 };
@@ -90,6 +99,7 @@ struct GemmParams {
   int wv_q;         // wgrad tap view: output-row length padded to a multiple of 32 (0 = off)
   int fv_q;         // fprop tap view: GEMM rows per output row (= BM; rows q >= Q are padding, 0 = off)
   const float* bias;  // bf16x3 EPI_STORE / split-K reduce: per-column bias added to the output (nullptr = none)
+  int dbg_mode;     // debug build only: skip pipeline work to find the limiter (1 A split, 2 B split, 4 MMA, 8 stores)
   unsigned long long* dbg_t;  // debug: per-CTA wait-time counters of the bf16x3 pipeline roles (nullptr = off)
   float* dbg_a;     // debug: bf16x3 A-split dumps the raw A operand [M][Kpad] here (nullptr = off)
   float* dbg_b;     // debug: bf16x3 B-split dumps the raw B operand [N][Kpad]

@@ -74,12 +74,17 @@ extern "C" int monet_profile_variant(const monet_prof_desc* d, int variant, int 
     ws = monet_conv_ws_bytes(variant, pass, c);
     float *x = B.get(xb, 1), *w = B.get(wb, 2), *y = B.get(yb, 3), *wsp = B.get(ws, 4);
     float *dx = pass != MONET_PASS_FWD ? B.get(xb, 5) : nullptr, *dw = pass != MONET_PASS_FWD ? B.get(wb, 6) : nullptr;
+    // the weights' bf16 split as an executor keeps it (monet_conv_*_w16): split once, untimed
+    const int64_t wn = (int64_t)(wb / 4), wn8 = (wn + 7) / 8 * 8;
+    uint16_t* whi = reinterpret_cast<uint16_t*>(B.get((size_t)wn8 * 4, 7));
     if (B.err) return B.err;
+    uint16_t* wlo = whi + wn8;
+    if (int e = monet_split_bf16(w, whi, wlo, wn, st)) return e;
     const bool need_dx = d->conv_needs_dx != 0;
     run = [=]() -> int {  // BWD: dgrad (if the input has a gradient) + wgrad; DGRAD / WGRAD: one pass
-      if (pass == MONET_PASS_FWD) return monet_conv_fwd(variant, c, x, w, y, wsp, ws, st);
+      if (pass == MONET_PASS_FWD) return monet_conv_fwd_w16(variant, c, x, w, whi, wlo, nullptr, y, wsp, ws, st);
       if ((pass == MONET_PASS_BWD && need_dx) || pass == MONET_PASS_DGRAD)
-        if (int e = monet_conv_dgrad(variant, c, y, w, dx, 0, wsp, ws, st)) return e;
+        if (int e = monet_conv_dgrad_w16(variant, c, y, w, whi, wlo, dx, 0, wsp, ws, st)) return e;
       if (pass == MONET_PASS_DGRAD) return 0;
       return monet_conv_wgrad(variant, c, x, y, dw, 0, wsp, ws, st);
     };

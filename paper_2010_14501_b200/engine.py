@@ -143,6 +143,20 @@ class Runtime:
             self.pview[(nid, name)] = self.params[pos:pos + n]
             self.gview[(nid, name)] = self.grads[pos:pos + n]
             pos += n
+        # pre-split conv weights (bf16 hi / lo planes, tracer.Network.w16_segments)
+        segs = self.net.w16_segments()
+        self.w16, self.w16_count = {}, len(segs)
+        self.w16_max = max((n for _, _, _, n in segs), default=0)
+        if segs:
+            off, nb = self.region["w16_table"]
+            table = self.fixed[off:off + 24 * len(segs)].view(torch.int64)
+            table.copy_(torch.tensor([[src, dst, n] for _, src, dst, n in segs], dtype=torch.int64).reshape(-1))
+            self.w16_table = self.fixed.data_ptr() + off
+            off, nb = self.region["w16"]
+            self.w16_hi = self.fixed.data_ptr() + off
+            self.w16_lo = self.w16_hi + nb // 2
+            for nid, _, dst, _ in segs:
+                self.w16[nid] = (self.w16_hi + 2 * dst, self.w16_lo + 2 * dst)
         stats = f32("bn_stats")
         self.bn = {}
         pos = 0
@@ -252,6 +266,12 @@ class Runtime:
             ptrs = {k: base + offsets[b] for k, b in sb["blocks"].items()}
             calls.append(self._bind(s, sb, ptrs, catalog))
             step_ptrs.append(ptrs)
+        if calls and self.w16_count:
+            # refresh the weights' bf16 split before the step's first use (the conv forwards /
+            # input gradients load it, monet_conv_*_w16): one launch over all conv weights
+            calls[0].insert(0, ("k", self.lib.dll.monet_split_bf16_segments,
+                                (self.params.data_ptr(), self.w16_hi, self.w16_lo, self.w16_table,
+                                 self.w16_count, self.w16_max, None)))
         calls.append(self._bind_optimizer())
         plan = Plan(schedule, trace, calls, arena_bytes, trace.peak_memory, bound, len(blocks),
                     sum(1 for group in calls for c in group if c[0] == "k"))
@@ -289,12 +309,10 @@ class Runtime:
                 d = net.conv_desc(op)
                 v = _native.CONV_VARIANTS[s.impl]
                 wt = self.pview[(op.id, "weight")].data_ptr()
-                if "bias" in op.params:
-                    out.append(("k", lib.monet_conv_fwd_bias, (v, C.byref(d), xs[0], wt,
-                                                               self.pview[(op.id, "bias")].data_ptr(), y, ws,
-                                                               s.workspace, None), d))
-                else:
-                    out.append(("k", lib.monet_conv_fwd, (v, C.byref(d), xs[0], wt, y, ws, s.workspace, None), d))
+                hi, lo = self.w16.get(op.id, (None, None))
+                bias = self.pview[(op.id, "bias")].data_ptr() if "bias" in op.params else None
+                out.append(("k", lib.monet_conv_fwd_w16, (v, C.byref(d), xs[0], wt, hi, lo, bias, y, ws,
+                                                          s.workspace, None), d))
             elif op.kind == "convT":
                 d = net.conv_desc(op)
                 v = _native.CONV_VARIANTS[s.impl]
@@ -434,8 +452,9 @@ class Runtime:
             j = op.deps[0]
             wt = self.pview[(op.id, "weight")].data_ptr()
             if net.grad_bytes(net.op(j)) > 0:
-                out.append(("k", lib.monet_conv_dgrad, (v, C.byref(d), dy, wt, P(("g", j)), acc(j), ws,
-                                                        s.workspace, None), d))
+                hi, lo = self.w16.get(op.id, (None, None))
+                out.append(("k", lib.monet_conv_dgrad_w16, (v, C.byref(d), dy, wt, hi, lo, P(("g", j)), acc(j), ws,
+                                                            s.workspace, None), d))
             if not op.attrs.get("split"):  # split convs: the weight gradient is the wgrad node's stage
                 out.append(("k", lib.monet_conv_wgrad, (v, C.byref(d), P(("in", j)), dy,
                                                         self.gview[(op.id, "weight")].data_ptr(), 0, ws,

@@ -144,11 +144,29 @@ class Network:
     def input_bytes(self) -> int:
         return self.ops[0].nbytes
 
+    def w16_segments(self) -> list:
+        """Conv weights kept pre-split in bf16 hi / lo planes (monet_conv_*_w16):
+        (op id, offset in the flat parameter buffer, offset in each plane, count), plane
+        offsets 16-B aligned (TMA).  Transposed and depthwise convs are not GEMM B operands
+        of that form."""
+        out, pos, dst = [], 0, 0
+        for nid, name, t in self.param_items():
+            n = t.numel()
+            if name == "weight" and self.op(nid).kind == "conv":
+                out.append((nid, pos, dst, n))
+                dst += (n + 7) // 8 * 8
+            pos += n
+        return out
+
     def fixed_layout(self) -> dict:
         """Byte sizes of everything outside the arena (all folded into params_bytes)."""
         p = self.n_param_elems() * F32
+        segs = self.w16_segments()
+        plane = sum((n + 7) // 8 * 8 for *_, n in segs)
         return {
             "params": p, "grads": p, "momentum": p,
+            "w16": 2 * 2 * plane,           # pre-split conv weights: bf16 hi plane, then lo plane
+            "w16_table": 24 * len(segs),    # their segment table (monet_split_bf16_segments)
             "bn_stats": 4 * self.bn_channels() * F32,   # saved mean/invstd, running mean/var
             "scratch": self.scratch_bytes(),
             "staging_input": self.input_bytes(),

@@ -4,6 +4,7 @@
 Prints achieved algorithmic TFLOP/s per (layer, pass, variant).
 """
 import argparse
+import ctypes as C
 import sys
 from pathlib import Path
 
@@ -28,6 +29,7 @@ def main():
     ap.add_argument("--only", default=None)
     ap.add_argument("--passes", default="fwd,dgrad,wgrad")
     ap.add_argument("--variants", default="splitk")
+    ap.add_argument("--fp32-weights", action="store_true", help="fwd / dgrad split the fp32 weights per tile")
     ap.add_argument("--resnet50", action="store_true",
                     help="every unique conv shape of ResNet-50 b184 224^2, weighted by its count")
     a = ap.parse_args()
@@ -52,10 +54,16 @@ def main():
                 pid = N.PASS[pss]
                 wsb = lib.conv_ws_bytes(v, pid, d)
                 ws = torch.empty(max(wsb, 16) // 4, device=dev)
-                if pss == "fwd":
+                if pss == "fwd" and a.fp32_weights:
                     fn = lambda: lib.conv_fwd(v, d, x.data_ptr(), wt.data_ptr(), y.data_ptr(), ws.data_ptr(), wsb, st)
-                elif pss == "dgrad":
+                elif pss == "fwd":
+                    fn = lambda: lib.conv_fwd_w16(v, C.byref(d), x.data_ptr(), wt.data_ptr(), hi, lo, None,
+                                                  y.data_ptr(), ws.data_ptr(), wsb, st)
+                elif pss == "dgrad" and a.fp32_weights:
                     fn = lambda: lib.conv_dgrad(v, d, y.data_ptr(), wt.data_ptr(), dx.data_ptr(), 0, ws.data_ptr(), wsb, st)
+                elif pss == "dgrad":
+                    fn = lambda: lib.conv_dgrad_w16(v, C.byref(d), y.data_ptr(), wt.data_ptr(), hi, lo, dx.data_ptr(),
+                                                    0, ws.data_ptr(), wsb, st)
                 else:
                     fn = lambda: lib.conv_wgrad(v, d, x.data_ptr(), y.data_ptr(), dw.data_ptr(), 0, ws.data_ptr(), wsb, st)
                 fn()
@@ -92,6 +100,11 @@ def resnet50_table(a):
         wt = torch.randn(k, r, s, c, device=dev)
         y = torch.randn(n, d.p, d.q, k, device=dev)
         dw, dx = torch.empty_like(wt), torch.empty_like(x)
+        # the weights' bf16 split as the executor keeps it (monet_conv_*_w16)
+        n8 = (wt.numel() + 7) // 8 * 8
+        planes = torch.zeros(2 * n8, dtype=torch.int16, device=dev)
+        hi, lo = planes.data_ptr(), planes.data_ptr() + 2 * n8
+        lib.split_bf16(wt.data_ptr(), hi, lo, wt.numel(), None)
         flops = 2.0 * n * d.p * d.q * k * c * r * s
         line = f"{cnt:2d}x n{n} {h}x{w} c{c:4d} k{k:4d} {r}x{s}/{stride}"
         for vname in a.variants.split(","):
@@ -103,10 +116,16 @@ def resnet50_table(a):
                 pid = N.PASS[pss]
                 wsb = lib.conv_ws_bytes(v, pid, d)
                 ws = torch.empty(max(wsb, 16) // 4, device=dev)
-                if pss == "fwd":
+                if pss == "fwd" and a.fp32_weights:
                     fn = lambda: lib.conv_fwd(v, d, x.data_ptr(), wt.data_ptr(), y.data_ptr(), ws.data_ptr(), wsb, st)
-                elif pss == "dgrad":
+                elif pss == "fwd":
+                    fn = lambda: lib.conv_fwd_w16(v, C.byref(d), x.data_ptr(), wt.data_ptr(), hi, lo, None,
+                                                  y.data_ptr(), ws.data_ptr(), wsb, st)
+                elif pss == "dgrad" and a.fp32_weights:
                     fn = lambda: lib.conv_dgrad(v, d, y.data_ptr(), wt.data_ptr(), dx.data_ptr(), 0, ws.data_ptr(), wsb, st)
+                elif pss == "dgrad":
+                    fn = lambda: lib.conv_dgrad_w16(v, C.byref(d), y.data_ptr(), wt.data_ptr(), hi, lo, dx.data_ptr(),
+                                                    0, ws.data_ptr(), wsb, st)
                 else:
                     fn = lambda: lib.conv_wgrad(v, d, x.data_ptr(), y.data_ptr(), dw.data_ptr(), 0, ws.data_ptr(), wsb, st)
                 fn()
