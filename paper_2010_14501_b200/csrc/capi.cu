@@ -308,6 +308,8 @@ float* g_dbg_a = nullptr;
 float* g_dbg_b = nullptr;
 unsigned long long* g_dbg_t = nullptr;
 
+bool al16(const void* p);
+
 int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (p.M <= 0 || p.N <= 0) return 0;
   p.dbg_a = g_dbg_a;
@@ -345,6 +347,7 @@ int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_b
     if (mode_is_w16(p.b.mode) && !p.b.tma) return -(int)cudaErrorNotSupported;
   }
   p.split_tf32 = variant == MONET_CONV_TF32 ? 0 : 1;
+  p.c_tma = 0;
   p.m_tiles = (p.M + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM);
   p.n_tiles = (p.N + p.n_pitch - 1) / p.n_pitch;
   const int kblocks = std::max(1, (p.Kd + BK - 1) / BK);
@@ -359,6 +362,18 @@ int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_b
   p.splits = (kblocks + p.kb_per_split - 1) / p.kb_per_split;
   p.ws = static_cast<float*>(ws);
   p.epi = p.splits > 1 ? EPI_PARTIAL : (accumulate ? EPI_ACCUM : EPI_STORE);
+  // pre-split-B kernels: output blocks through smem + TMA store when the output rows are plain
+  // (no phase scatter, tap-view padding rows or transposed store) and 16-B aligned
+  if (bx && mode_is_w16(p.b.mode) && !p.ph.on && !p.fv_q && !p.c_trans && p.n_pitch % 32 == 0) {
+    float* out = p.epi == EPI_PARTIAL ? p.ws : p.c;
+    const long long ld = p.epi == EPI_PARTIAL ? p.N : p.ldc;
+    if (al16(out) && ld % 4 == 0) {
+      cuuint64_t dims[3] = {(cuuint64_t)p.N, (cuuint64_t)p.M, (cuuint64_t)(p.epi == EPI_PARTIAL ? p.splits : 1)};
+      cuuint64_t strides[2] = {(cuuint64_t)ld * 4, (cuuint64_t)p.M * ld * 4};
+      cuuint32_t box[3] = {32, 32, 1};
+      p.c_tma = tiled_map(&p.tma_c, out, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    }
+  }
   const int tiles = p.m_tiles * p.n_tiles * p.splits;
   const int grid = pair ? 2 * std::min(tiles, kNumSMs / 2) : std::min(tiles, kNumSMs);
   const int e = !bx     ? dispatch_modes<false, false>(p, grid, st)

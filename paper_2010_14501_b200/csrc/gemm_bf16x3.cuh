@@ -72,11 +72,14 @@ struct Cfg {
   static constexpr bool kW16 = mode_is_w16(BMODE);
   static constexpr int kBTile = NB * BKS * 2;                   // bf16 hi (or lo) stage tile
   static constexpr int kStageBytes = 2 * kBTile;                // B hi + B lo
-  static constexpr int kRawSlots = kW16 ? (NB == BN ? 6 : 8) : (NB == BN ? 4 : 6);
+  static constexpr int kRawSlots = kW16 ? (NB == BN ? 4 : 6) : (NB == BN ? 4 : 6);
   static constexpr int kRawBytes = kW16 ? kRawTile : kRawTile + NB * BKR * 4;
   static constexpr int kBStages = kW16 ? (NB == BN ? 4 : 6) : (NB == BN ? 3 : 4);
+  // pre-split-B kernels store the output through smem + TMA: two 32x32 fp32 blocks per epilogue warp
+  static constexpr int kEpiBytes = kW16 ? kEpiWarps * 2 * 32 * 32 * 4 : 0;
   static constexpr int kNumBars = 2 * kRawSlots + 2 * kAStages + 2 * kBStages + 2 * kAccStages;
-  static constexpr int kSmemBytes = kRawSlots * kRawBytes + kBStages * kStageBytes + 1024 + 8 * kNumBars + 16;
+  static constexpr int kSmemBytes =
+      kRawSlots * kRawBytes + kBStages * kStageBytes + kEpiBytes + 1024 + 8 * kNumBars + 16;
   static_assert(kSmemBytes <= 232448, "shared memory budget");
 };
 
@@ -184,6 +187,25 @@ MONET_DEV void tma_3d(uint32_t dst, const CUtensorMap* m, int x, int y, int z, u
       "l"(m), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
       : "memory");
 }
+// TMA store / reduce-add of a 32 x 32 fp32 smem block (SWIZZLE_128B) to the output map
+// {N, M, splits}: rows past M are clipped per split
+MONET_DEV void tma_store_3d(const CUtensorMap* m, uint32_t src, int x, int y, int z, bool add) {
+  if (add)
+    asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(m),
+                 "r"(src), "r"(x), "r"(y), "r"(z)
+                 : "memory");
+  else
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(m),
+                 "r"(src), "r"(x), "r"(y), "r"(z)
+                 : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+MONET_DEV void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+MONET_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 MONET_DEV void tma_4d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2, int c3, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
@@ -475,7 +497,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* raw = smem;                                  // kRawSlots x (A[, B]) fp32
   uint8_t* bst = smem + kRawSlots * kRawBytes;          // kBStages x (B hi, B lo) bf16
-  uint64_t* bars = reinterpret_cast<uint64_t*>(bst + kBStages * kStageBytes);
+  uint8_t* epi_st = bst + kBStages * kStageBytes;       // epilogue staging (pre-split-B kernels)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi_st + CF::kEpiBytes);
   uint64_t* raw_full = bars;                            // loaders -> splitters
   uint64_t* raw_empty = raw_full + kRawSlots;           // splitters -> loaders
   uint64_t* a_full = raw_empty + kRawSlots;             // A-split -> MMA
@@ -815,6 +838,43 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
         const bool add_bias = p.bias != nullptr && chunk == 0 && p.epi == EPI_STORE;
         TWAIT(6, mbar_wait(&tfull[acc], acc_phase));
         tc_fence_after();
+        if constexpr (kW16) {
+          if (p.c_tma) {
+            // 32x32 blocks staged in smem (SWIZZLE_128B: conflict-free row writes) and stored by one
+            // TMA per block -- full 128-B lines instead of 16-B pieces of 32 rows per instruction.
+            // A later chunk's reduce-add waits for the earlier flushes of the tile to land, so the
+            // adds to an element happen in chunk order (deterministic).
+            if (chunk > 0 && lane == 0) bulk_wait_all();
+            __syncwarp();
+            const int mrow = mt * kTileM + quarter * 32, zs = p.epi == EPI_PARTIAL ? sp : 0;
+            for (int cc = 0; cc < NB / 32; ++cc) {
+              float v[32];
+              tmem_ld32(tmem_base + acc * NB + cc * 32 + ((uint32_t)(quarter * 32) << 16), v);
+              const int n0 = nt * p.n_pitch + cc * 32;
+              if (add_bias) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] += (n0 + j < p.N) ? __ldg(p.bias + n0 + j) : 0.f;
+              }
+              uint8_t* blk = epi_st + (quarter * 2 + (cc & 1)) * 4096;
+              if (lane == 0) bulk_wait_read<1>();  // this buffer's previous store has read smem
+              __syncwarp();
+#pragma unroll
+              for (int c = 0; c < 8; ++c)
+                *reinterpret_cast<float4*>(blk + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+                    make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0 && n0 < p.N && !(dm & 8)) tma_store_3d(&p.tma_c, smem_u32(blk), n0, mrow, zs, add_old);
+            }
+            tc_fence_before();
+            arrive_leader(&tempty[acc]);
+            if (++acc == kAccStages) {
+              acc = 0;
+              acc_phase ^= 1;
+            }
+            continue;
+          }
+        }
         for (int cc = 0; cc < NB / 32; ++cc) {
           float v[32];
           tmem_ld32(tmem_base + acc * NB + cc * 32 + ((uint32_t)(quarter * 32) << 16), v);
@@ -942,6 +1002,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
     }
   }
 
+  if constexpr (kW16) {
+    if (warp >= kWarpEpi && warp < kWarpMma && lane == 0 && p.c_tma) bulk_wait_all();  // stores read smem / land
+  }
   if (p.dbg_t) {  // one representative thread per role reports its waits
     const bool rep = threadIdx.x == 0 || threadIdx.x == kWarpASplit * 32 || threadIdx.x == kWarpBSplit * 32 ||
                      threadIdx.x == kWarpEpi * 32 || threadIdx.x == kWarpMma * 32;

@@ -103,7 +103,10 @@ struct GemmParams {
   unsigned long long* dbg_t;  // debug: per-CTA wait-time counters of the bf16x3 pipeline roles (nullptr = off)
   float* dbg_a;     // debug: bf16x3 A-split dumps the raw A operand [M][Kpad] here (nullptr = off)
   float* dbg_b;     // debug: bf16x3 B-split dumps the raw B operand [N][Kpad]
+  int c_tma;        // bf16x3 pre-split-B kernels: the epilogue stages 32x32 blocks in smem and
+                    //   stores (or reduce-adds) them with TMA through tma_c (0 = per-thread stores)
   CUtensorMap tma_a, tma_b;  // bf16x3: TMA descriptors (valid when Operand::tma != 0)
+  CUtensorMap tma_c;         // output [rows][N] (EPI_PARTIAL: the split-K workspace [splits*M][N])
 };
 
 constexpr int BM = 128, BN = 128, BK = 32;

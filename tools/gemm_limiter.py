@@ -31,11 +31,17 @@ for name, pss in zip(args[::2], args[1::2]):
     v = N.CONV_VARIANTS["splitk"]
     wsb = lib.conv_ws_bytes(v, N.PASS[pss], d)
     ws = torch.empty(max(wsb, 16) // 4, device=dev)
+    n8 = (wt.numel() + 7) // 8 * 8  # the weights' bf16 split, as the executor keeps it
+    planes = torch.zeros(2 * n8, dtype=torch.int16, device=dev)
+    hi, lo = planes.data_ptr(), planes.data_ptr() + 2 * n8
+    lib.split_bf16(wt.data_ptr(), hi, lo, wt.numel(), None)
     if pss == "fwd":
-        fn = lambda: lib.conv_fwd(v, d, x.data_ptr(), wt.data_ptr(), y.data_ptr(), ws.data_ptr(), wsb, st)
+        fn = lambda: lib.conv_fwd_w16(v, d, x.data_ptr(), wt.data_ptr(), hi, lo, None, y.data_ptr(), ws.data_ptr(),
+                                      wsb, st)
     elif pss == "dgrad":
         dx = torch.empty_like(x)
-        fn = lambda: lib.conv_dgrad(v, d, y.data_ptr(), wt.data_ptr(), dx.data_ptr(), 0, ws.data_ptr(), wsb, st)
+        fn = lambda: lib.conv_dgrad_w16(v, d, y.data_ptr(), wt.data_ptr(), hi, lo, dx.data_ptr(), 0, ws.data_ptr(),
+                                        wsb, st)
     else:
         dw = torch.empty_like(wt)
         fn = lambda: lib.conv_wgrad(v, d, x.data_ptr(), y.data_ptr(), dw.data_ptr(), 0, ws.data_ptr(), wsb, st)
