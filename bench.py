@@ -190,7 +190,7 @@ def kernel_roofline(rt, plan, net, peaks):
         ms = a.elapsed_time(b)
         total_t += ms
         op = net.op(s.node)
-        if op.kind in ("conv", "convT", "wgrad"):
+        if op.kind in ("conv", "convrelu", "convT", "wgrad"):
             if op.kind == "wgrad":  # a split conv's weight gradient (no forward work)
                 f = conv_flops(net, net.op(op.attrs["conv"])) if s.kind == "backward" else 0.0
             else:
@@ -440,6 +440,8 @@ def ours_arm(args):
     torch.cuda.synchronize()
     torch.cuda.reset_peak_memory_stats(dev)
     free0, total0 = torch.cuda.mem_get_info(dev)
+    # device memory the allocator holds for anything but the runtime (fixed region + arena)
+    other0 = torch.cuda.memory_stats(dev).get("requested_bytes.all.current", 0) - rt.fixed.numel() - rt.arena.numel()
 
     sampler = ClockSampler(local)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -468,6 +470,10 @@ def ours_arm(args):
         "torch_peak_requested_bytes": mstats.get("requested_bytes.all.peak"),
         "torch_peak_allocated_bytes": mstats.get("allocated_bytes.all.peak"),  # + 512-B allocator rounding
         "torch_reserved_bytes": mstats.get("reserved_bytes.all.current"),
+        # allocations outside the runtime alive during the timed steps (bench bookkeeping)
+        "other_allocated_bytes": other0,
+        # the runtime's own peak: requested peak minus those
+        "runtime_peak_bytes": (mstats.get("requested_bytes.all.peak") or 0) - other0,
         # CUDA context, NCCL buffers, cuBLAS/library workspaces: device memory in use that
         # torch's allocator does not hold
         "non_allocator_bytes": (total0 - min(free0, free1)) - mstats.get("reserved_bytes.all.current", 0),
@@ -486,8 +492,14 @@ def ours_arm(args):
         dist.barrier()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    for _ in range(args.steps):
-        lt = rt.train_step(plan, host, host_y)
+    # every step's batch is copied from pinned host memory inside the timed region; the copy of
+    # batch i+1 is prefetched while step i runs (Runtime.prefetch: it starts once step i has
+    # read the staging buffer), and step i's loss is read back before step i+1 is launched
+    rt.prefetch(host, host_y)
+    for i in range(args.steps):
+        lt = rt.train_step(plan)
+        if i + 1 < args.steps:
+            rt.prefetch(host, host_y)
         loss_host.copy_(lt, non_blocking=True)
         torch.cuda.current_stream().synchronize()
     b.record()
@@ -555,8 +567,7 @@ def ours_arm(args):
                        "params_bytes": g.params_bytes, "arena_bytes": plan.arena_bytes,
                        **device_mem,
                        "within_bound": g.params_bytes + plan.arena_bytes <= (plan.bound_peak or 0),
-                       "device_within_bound": (device_mem["torch_peak_requested_bytes"] or 1 << 62)
-                                              <= (plan.bound_peak or 0),
+                       "device_within_bound": device_mem["runtime_peak_bytes"] <= (plan.bound_peak or 0),
                        "store_everything_ledger_peak_bytes": M.simulate(se, g, cat).peak_memory},
             "overhead": {"modeled_pct": round(100 * overhead_model, 2), "recomputes": n_rec,
                          "measured_pct": None if se_ms is None else round(100 * (ms / se_ms - 1), 2),
@@ -568,7 +579,7 @@ def ours_arm(args):
                          "planner": pinfo},
             "e2e": {"value": round(world * args.batch / (e2e_ms * 1e-3), 2), "unit": "img/s",
                     "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": host.numel() * 4 + args.batch * 4,
-                    "d2h_bytes_per_step": 4, "api": "Runtime.train_step(plan, pinned host batch) + loss D2H"},
+                    "d2h_bytes_per_step": 4, "api": "Runtime.prefetch(pinned host batch i+1) overlapping Runtime.train_step(plan) of batch i + loss D2H"},
             "gpu_launches": plan.launches * args.steps,
             "roofline": roof, "roofline_local_ops": local_roof,
             "cpu_baseline": cpu,

@@ -38,7 +38,7 @@ class CpuState:
         for op in net.ops:
             for name, t in op.params.items():
                 v = t.to(dtype).clone()
-                if op.kind in ("conv", "convT") and name == "weight":
+                if op.kind in ("conv", "convrelu", "convT") and name == "weight":
                     v = v.permute(0, 3, 1, 2).contiguous()  # KRSC -> KCRS (OIHW; convT: [in][out][R][S])
                 elif op.kind == "dwconv" and name == "weight":
                     v = v.permute(2, 0, 1).unsqueeze(1).contiguous()  # [R][S][C] -> [C][1][R][S]
@@ -50,6 +50,13 @@ class CpuState:
         self.saved = {}
         self.grads = {}
         self.seed = 0  # dropout step seed: the engine's device counter, advanced once per step
+
+
+def _mask_gate(mask, dy):
+    """dy where the packed NHWC sign-mask bit is set, else 0 (relu_bwd_mask)."""
+    bits = torch.from_numpy(unpack_sign_mask(mask, dy.numel()))
+    keep = bits.view(dy.shape[0], dy.shape[2], dy.shape[3], dy.shape[1]).permute(0, 3, 1, 2)
+    return torch.where(keep, dy, torch.zeros_like(dy))
 
 
 def _bn_stats(x, eps):
@@ -126,9 +133,13 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
             c_pad = op.shape[3]
             y = torch.zeros(images.shape[0], c_pad, images.shape[2], images.shape[3], dtype=dt)
             y[:, :images.shape[1]] = images.to(dt)
-        elif op.kind == "conv":
+        elif op.kind in ("conv", "convrelu"):
             a = op.attrs
             y = F.conv2d(xs[0], P[(op.id, "weight")], P.get((op.id, "bias")), stride=a["stride"], padding=a["pad"])
+            if op.kind == "convrelu":  # fused ReLU: the mask is the pre-activation's sign (relu_fwd in place)
+                if want_int:
+                    extra = pack_sign_mask(y.permute(0, 2, 3, 1).numpy())
+                y = torch.where(y > 0, y, torch.zeros_like(y))
         elif op.kind == "dropout":
             y = xs[0] * _dropout_scale(op, xs[0], state.seed)
         elif op.kind == "concat":
@@ -211,11 +222,15 @@ def run_step(state: CpuState, schedule: dict, images: torch.Tensor, labels: torc
             conv = net.op(op.attrs["conv"])
             a = conv.attrs
             w = P[(conv.id, "weight")]
+            if conv.kind == "convrelu":  # runs before the conv's stage: gates its dy in place with the mask
+                grad[conv.id] = _mask_gate(x_of(net.intermediate_of[conv.id]), grad[conv.id])
             state.grads[(conv.id, "weight")] = torch.nn.grad.conv2d_weight(x_of(conv.deps[0]), w.shape, grad[conv.id],
                                                                           a["stride"], a["pad"])
             return
         dy = grad[op.id]
-        if op.kind == "conv":
+        if op.kind == "convrelu" and not op.attrs.get("split"):
+            dy = _mask_gate(x_of(net.intermediate_of[op.id]), dy)
+        if op.kind in ("conv", "convrelu"):
             a = op.attrs
             j = op.deps[0]
             w = P[(op.id, "weight")]
@@ -490,7 +505,7 @@ def params_nhwc(state: CpuState):
     """Parameters in the engine layout (conv weights KRSC) for comparison with the GPU."""
     out = {}
     for (nid, name), v in state.params.items():
-        if state.net.op(nid).kind in ("conv", "convT") and name == "weight":
+        if state.net.op(nid).kind in ("conv", "convrelu", "convT") and name == "weight":
             v = v.permute(0, 2, 3, 1).contiguous()
         elif state.net.op(nid).kind == "dwconv" and name == "weight":
             v = v.squeeze(1).permute(1, 2, 0).contiguous()

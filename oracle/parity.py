@@ -54,7 +54,7 @@ def grads_nhwc(state):
     out = {}
     for (nid, name), g in state.grads.items():
         kind = state.net.op(nid).kind
-        if kind in ("conv", "convT") and name == "weight":
+        if kind in ("conv", "convrelu", "convT") and name == "weight":
             g = g.permute(0, 2, 3, 1).contiguous()
         elif kind == "dwconv" and name == "weight":
             g = g.squeeze(1).permute(1, 2, 0).contiguous()

@@ -9,6 +9,8 @@ Units: integer nanoseconds, exact ints as units.py requires.
 
 from __future__ import annotations
 
+import dataclasses
+
 TC_FLOPS = 250e12      # sustained 3xTF32 conv throughput assumed before profiling
 HBM_BPS = 6.0e12       # sustained HBM bandwidth for local ops
 LAUNCH_NS = 4000       # per-kernel fixed cost
@@ -30,7 +32,12 @@ def analytic_cost(net, op, pass_, name) -> int:
             return 1
         conv = net.op(op.attrs["conv"])
         x = net.op(conv.deps[0])
-        return _ns(2.0 * conv.numel * x.shape[3] * conv.attrs["r"] * conv.attrs["s"], 4.0 * (x.numel + conv.numel))
+        gate = 8.125 * conv.numel if conv.kind == "convrelu" else 0.0  # a split convrelu's dy mask gate
+        return gate / HBM_BPS * 1e9 // 1 + _ns(2.0 * conv.numel * x.shape[3] * conv.attrs["r"] * conv.attrs["s"], 4.0 * (x.numel + conv.numel))
+    if op.kind == "convrelu":  # the conv plus its in-place ReLU (fwd: r4 w4 + mask; bwd: mask gate of dy)
+        relu = _ns(nbytes=8.125 * n)
+        return analytic_cost(net, dataclasses.replace(op, kind="conv"), pass_, name) + (
+            relu if pass_ == "fwd" or not op.attrs.get("split") else 0)
     if op.kind == "conv":
         x = net.op(op.deps[0])
         flops = 2.0 * n * x.shape[3] * op.attrs["r"] * op.attrs["s"]

@@ -812,6 +812,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
     const int quarter = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
+    int epi_stores = 0;  // TMA-store epilogue: bulk stores issued by this warp
     for (int tile = unit0; tile < n_tiles_total; tile += n_units) {
       int mt, nt, sp, kb0, kb1;
       tile_coords(p, tile, mt, nt, sp);
@@ -851,12 +852,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
               float v[32];
               tmem_ld32(tmem_base + acc * NB + cc * 32 + ((uint32_t)(quarter * 32) << 16), v);
               const int n0 = nt * p.n_pitch + cc * 32;
+              if (n0 >= p.N) continue;  // a trailing chunk of a partial n-tile: nothing to store
               if (add_bias) {
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] += (n0 + j < p.N) ? __ldg(p.bias + n0 + j) : 0.f;
               }
-              uint8_t* blk = epi_st + (quarter * 2 + (cc & 1)) * 4096;
-              if (lane == 0) bulk_wait_read<1>();  // this buffer's previous store has read smem
+              // the warp's two staging blocks alternate per store (not per chunk: skipped chunks
+              // would break the pairing); wait until the store two back has read its block
+              uint8_t* blk = epi_st + (quarter * 2 + (epi_stores & 1)) * 4096;
+              ++epi_stores;
+              if (lane == 0) bulk_wait_read<1>();
               __syncwarp();
 #pragma unroll
               for (int c = 0; c < 8; ++c)
@@ -864,7 +869,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
                     make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
               fence_proxy_async_smem();
               __syncwarp();
-              if (lane == 0 && n0 < p.N && !(dm & 8)) tma_store_3d(&p.tma_c, smem_u32(blk), n0, mrow, zs, add_old);
+              if (lane == 0 && !(dm & 8)) tma_store_3d(&p.tma_c, smem_u32(blk), n0, mrow, zs, add_old);
             }
             tc_fence_before();
             arrive_leader(&tempty[acc]);

@@ -394,9 +394,23 @@ __device__ __forceinline__ void bn_warp_sum(const float* __restrict__ ws, int nb
   const int lane = threadIdx.x & 31;
   s1 = 0.0;
   s2 = 0.0;
-  for (int b = lane; b < nblocks; b += 32) {
-    s1 += ws[(long long)b * 2 * C + c];
-    s2 += ws[(long long)b * 2 * C + C + c];
+  // eight blocks' loads in flight per lane before the (unchanged, in-order) fp64 adds: the
+  // loop was a chain of dependent L2 round trips (~10 us per finalize launch)
+  for (int b0 = lane; b0 < nblocks; b0 += 32 * 8) {
+    float a1[8], a2[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int b = b0 + 32 * u;
+      a1[u] = b < nblocks ? ws[(long long)b * 2 * C + c] : 0.f;
+      a2[u] = b < nblocks ? ws[(long long)b * 2 * C + C + c] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (b0 + 32 * u < nblocks) {
+        s1 += a1[u];
+        s2 += a2[u];
+      }
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {

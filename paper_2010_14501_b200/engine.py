@@ -104,6 +104,11 @@ class Runtime:
         self._plans: dict[int, Plan] = {}
         self.graph = None
         self.comm = None  # set by dp.DataParallel for the gradient allreduce
+        # batch prefetch (prefetch / train_step): copy stream and its two events
+        self._copy_stream = None
+        self._staging_free = torch.cuda.Event()
+        self._staged = torch.cuda.Event()
+        self._pending_labels = None
 
     # ------------------------------------------------------------ fixed region
     def _carve(self):
@@ -191,15 +196,36 @@ class Runtime:
         """The last step's loss as a 1-element device tensor (no host sync)."""
         return self.consts[1:2]
 
+    def prefetch(self, images: torch.Tensor, labels: torch.Tensor):
+        """Start staging the NEXT step's batch (pinned host tensors, engine NHWC layout) on a
+        copy stream.  The copy waits only until the running step has made its last read of
+        the staging buffer (the input copies into the arena, captured as the first of the
+        step's two graphs), so it overlaps that step's remaining work; the following
+        train_step(plan) without images waits for it.  A data loader's double buffer, with
+        no extra device memory."""
+        if self._copy_stream is None:
+            self._copy_stream = torch.cuda.Stream(self.device)
+        self._copy_stream.wait_event(self._staging_free)
+        with torch.cuda.stream(self._copy_stream):
+            self.staging.copy_(images.reshape(-1), non_blocking=True)
+        self._staged.record(self._copy_stream)
+        self._pending_labels = labels
+
     def train_step(self, plan: "Plan", images: torch.Tensor | None = None,
                    labels: torch.Tensor | None = None) -> torch.Tensor:
         """Public per-step call: stage the batch (host or device, NCHW or engine NHWC
-        layout), run the scheduled forward/backward/SGD, return the device loss."""
+        layout) -- or take the one ``prefetch`` staged --, run the scheduled
+        forward/backward/SGD, return the device loss."""
         if images is not None:
             if images.dim() == 4 and images.shape[1] in (1, 2, 3) and images.shape[-1] not in (1, 2, 3, 4):
                 self.set_batch(images, labels)
             else:
                 self.set_batch_nhwc(images, labels)
+        elif self._pending_labels is not None:
+            cur = torch.cuda.current_stream(self.device)
+            cur.wait_event(self._staged)
+            self.labels.copy_(self._pending_labels.reshape(-1), non_blocking=True)
+            self._pending_labels = None
         if plan.calls is None:
             raise RuntimeError("this plan was invalidated when the runtime's arena was reallocated; "
                                "call Runtime.plan() again")
@@ -207,6 +233,7 @@ class Runtime:
             plan.graph.replay()
         else:
             self.run(plan)
+            self._staging_free.record()  # uncaptured: the staging buffer is free after the whole step
         return self.loss_tensor()
 
     def capture(self, plan: "Plan"):
@@ -217,16 +244,27 @@ class Runtime:
                                "the torch.distributed backend issues its all-reduces from Python")
         self.run(plan)  # first launches set kernel attributes outside capture
         torch.cuda.synchronize(self.device)
-        graph = torch.cuda.CUDAGraph()
+        # two graphs, cut after the step's last read of the staging buffer (the input's
+        # forward copy, or its last recompute), so a prefetch of the next batch can start there
+        sptr = self.staging.data_ptr()
+        cut = 1 + max((i for i, grp in enumerate(plan.calls)
+                       if any(c[0] == "copy" and c[2] == sptr for c in grp)), default=-1)
+        cut = max(cut, 1)
+        parts = []
         side = torch.cuda.Stream(self.device)
         side.wait_stream(torch.cuda.current_stream(self.device))
-        with torch.cuda.stream(side):
-            with torch.cuda.graph(graph, stream=side):
-                self.run(plan)
+        for groups in (plan.calls[:cut], plan.calls[cut:]):
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(graph, stream=side):
+                    sp = C.c_void_p(side.cuda_stream)
+                    for grp in groups:
+                        self._run_group(grp, sp, _cudart())
+            parts.append(graph)
         torch.cuda.current_stream(self.device).wait_stream(side)
         torch.cuda.synchronize(self.device)
-        plan.graph = graph
-        return graph
+        plan.graph = _StepGraph(parts[0], parts[1], self._staging_free)
+        return plan.graph
 
     # ------------------------------------------------------------ planning
     def plan(self, schedule: Schedule, g: Graph, catalog: Catalog, check_bound: bool = True) -> Plan:
@@ -305,7 +343,7 @@ class Runtime:
                 out.append(("copy", y, self.staging.data_ptr(), nb))
             elif op.kind == "wgrad":
                 pass  # a split conv's weight-gradient anchor: no forward work, no tensor
-            elif op.kind == "conv":
+            elif op.kind in ("conv", "convrelu"):
                 d = net.conv_desc(op)
                 v = _native.CONV_VARIANTS[s.impl]
                 wt = self.pview[(op.id, "weight")].data_ptr()
@@ -313,6 +351,10 @@ class Runtime:
                 bias = self.pview[(op.id, "bias")].data_ptr() if "bias" in op.params else None
                 out.append(("k", lib.monet_conv_fwd_w16, (v, C.byref(d), xs[0], wt, hi, lo, bias, y, ws,
                                                           s.workspace, None), d))
+                if op.kind == "convrelu":  # the fused ReLU, in place on y (+ its sign mask when planned)
+                    mid = net.intermediate_of[op.id]
+                    mask = P(("a", mid)) if mid in s.planned_ints else None
+                    out.append(("k", lib.monet_relu_fwd, (y, y, mask, op.numel, None)))
             elif op.kind == "convT":
                 d = net.conv_desc(op)
                 v = _native.CONV_VARIANTS[s.impl]
@@ -446,11 +488,14 @@ class Runtime:
             out.append(("copy", dy, self.consts.data_ptr(), 4))  # seed dL/dL = 1
         if op.kind == "input":
             return out
-        if op.kind == "conv":
+        if op.kind in ("conv", "convrelu"):
             d = net.conv_desc(op)
             v = _native.CONV_VARIANTS[s.impl]
             j = op.deps[0]
             wt = self.pview[(op.id, "weight")].data_ptr()
+            if op.kind == "convrelu" and not op.attrs.get("split"):  # gate dy with the ReLU mask, in place
+                out.append(("k", lib.monet_relu_bwd_mask, (P(("in", net.intermediate_of[op.id])), dy, dy, op.numel,
+                                                           0, None)))
             if net.grad_bytes(net.op(j)) > 0:
                 hi, lo = self.w16.get(op.id, (None, None))
                 out.append(("k", lib.monet_conv_dgrad_w16, (v, C.byref(d), dy, wt, hi, lo, P(("g", j)), acc(j), ws,
@@ -467,6 +512,9 @@ class Runtime:
             conv = net.op(op.attrs["conv"])
             d = net.conv_desc(conv)
             v = _native.CONV_VARIANTS[s.impl]
+            if conv.kind == "convrelu":  # this stage runs before the conv's: gate its dy in place first
+                out.append(("k", lib.monet_relu_bwd_mask, (P(("in", net.intermediate_of[conv.id])), P(("g", conv.id)),
+                                                           P(("g", conv.id)), conv.numel, 0, None)))
             out.append(("k", lib.monet_conv_wgrad, (v, C.byref(d), P(("in", conv.deps[0])), P(("g", conv.id)),
                                                     self.gview[(conv.id, "weight")].data_ptr(), 0, ws,
                                                     s.workspace, None), d))
@@ -644,6 +692,20 @@ class Runtime:
                     raise _native.NativeError(f"monet_copy_async failed ({rc})")
             else:
                 c[1]()
+
+
+class _StepGraph:
+    """A captured training step as two CUDA graphs: up to the last read of the staging
+    buffer, then the rest; the event between them releases the staging buffer to a
+    prefetch (Runtime.prefetch)."""
+
+    def __init__(self, head, tail, staging_free):
+        self.head, self.tail, self.staging_free = head, tail, staging_free
+
+    def replay(self):
+        self.head.replay()
+        self.staging_free.record()
+        self.tail.replay()
 
 
 def lifetimes(steps, g: Graph):

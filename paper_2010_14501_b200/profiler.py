@@ -247,9 +247,9 @@ def profile_variant(net, op, pss: str, variant: str, iters: int = 5, stream=None
     """(ns per launch, workspace bytes) of one variant through the C-ABI profiler entry
     point monet_profile_variant (csrc/profile.cu): conv fwd / bwd, ReLU, BN, fused BN+ReLU."""
     d = _native.ProfDesc()
-    d.op = _native.PROF_OP["conv" if op.kind == "wgrad" else op.kind]
+    d.op = _native.PROF_OP["conv" if op.kind in ("wgrad", "convrelu") else op.kind]
     d.pass_ = _native.PASS["fwd"] if pss == "fwd" else _native.PASS["bwd"]
-    if op.kind in ("conv", "wgrad"):
+    if op.kind in ("conv", "convrelu", "wgrad"):
         conv = net.op(op.attrs["conv"]) if op.kind == "wgrad" else op
         d.conv = net.conv_desc(conv)
         d.conv_needs_dx = int(net.op(conv.deps[0]).kind != "input")
@@ -268,10 +268,25 @@ def profile_variant(net, op, pss: str, variant: str, iters: int = 5, stream=None
     rc = _native.lib().dll.monet_profile_variant(C.byref(d), v, iters, C.byref(ns), C.byref(ws), C.c_void_p(stream))
     if rc != 0:
         raise _native.NativeError(f"monet_profile_variant({op.kind} {pss} {variant}) failed with code {rc}")
+    conv = net.op(op.attrs["conv"]) if op.kind == "wgrad" else op
+    if conv.kind == "convrelu" and (op.kind == "convrelu" or pss == "bwd") and not (
+            op.kind == "convrelu" and pss == "bwd" and op.attrs.get("split")):
+        # the fused ReLU: in-place forward (+ mask), or the in-place mask gate of dy that the
+        # backward (unsplit) / the weight-gradient stage (split) runs first
+        r = _native.ProfDesc()
+        r.op, r.c = _native.PROF_OP["relu"], conv.shape[-1]
+        r.rows = conv.numel // r.c
+        r.pass_ = _native.PASS["fwd"] if pss == "fwd" else _native.PASS["bwd"]
+        rns = C.c_int64(0)
+        rc = _native.lib().dll.monet_profile_variant(C.byref(r), 0 if pss == "fwd" else _native.PROF_BWD["bwd-mask"],
+                                                     iters, C.byref(rns), None, C.c_void_p(stream))
+        if rc != 0:
+            raise _native.NativeError(f"monet_profile_variant(relu of {op.kind}) failed with code {rc}")
+        return int(ns.value) + int(rns.value), int(ws.value)
     return int(ns.value), int(ws.value)
 
 
-_NATIVE_PROFILED = ("conv", "wgrad", "relu", "bn", "bnrelu")
+_NATIVE_PROFILED = ("conv", "convrelu", "wgrad", "relu", "bn", "bnrelu")
 
 
 def _signature(net, op):
@@ -306,7 +321,7 @@ def profile_network(net, device="cuda:0", warmup=2, iters=5, reps=3, log=None) -
                     res[("fwd", name)] = ns
                 for name, ws, _ in bv:
                     ns, ws_k = profile_variant(net, op, "bwd", name, iters, bx.stream.cuda_stream)
-                    assert op.kind != "conv" or ws_k == ws, (op.name, name, ws_k, ws)
+                    assert op.kind not in ("conv", "convrelu") or ws_k == ws, (op.name, name, ws_k, ws)
                     res[("bwd", name)] = ns
             elif op.kind == "convT":
                 for name, _ in fv:

@@ -76,7 +76,7 @@ class Network:
 
     def __init__(self, ops: list[Op], batch: int, num_classes: int):
         self.ops = ops
-        self.fused = any(op.kind in ("bnrelu", "bnrelu6", "bnaddrelu") for op in ops)
+        self.fused = any(op.kind in ("bnrelu", "bnrelu6", "bnaddrelu", "convrelu") for op in ops)
         self.split = any(op.kind == "wgrad" for op in ops)
         self.batch = batch
         self.num_classes = num_classes
@@ -86,7 +86,7 @@ class Network:
         self.intermediate_bytes: dict[int, int] = {}
         nid = self.n + 1
         for op in ops:
-            if op.kind in ("relu", "relu6"):
+            if op.kind in ("relu", "relu6", "convrelu"):  # convrelu: the ReLU's mask of the fused conv
                 self.intermediate_of[op.id] = nid
                 self.intermediate_bytes[nid] = mask_bytes(op.numel)
                 nid += 1
@@ -105,7 +105,7 @@ class Network:
             kind = op.kind
             if kind == "relu" and self.op(op.deps[0]).kind == "add":
                 kind = "relu-join"
-            elif kind in ("bnrelu", "bnrelu6"):   # a fused op's output is a ReLU output
+            elif kind in ("bnrelu", "bnrelu6", "convrelu"):   # a fused op's output is a ReLU output
                 kind = "relu"
             elif kind in ("addrelu", "bnaddrelu"):  # ... at a residual join
                 kind = "relu-join"
@@ -115,7 +115,7 @@ class Network:
                 kind = "conv"
             out[op.id] = kind
             if op.id in self.intermediate_of:
-                out[self.intermediate_of[op.id]] = "mask" if op.kind in ("relu", "relu6") else "idx"
+                out[self.intermediate_of[op.id]] = "mask" if op.kind in ("relu", "relu6", "convrelu") else "idx"
         return out
 
     # -------------------------------------------------------------- fixed region
@@ -134,7 +134,7 @@ class Network:
         lib = _native.lib()
         s = 0
         for op in self.ops:
-            if op.kind in ("bn", "bnrelu", "bnrelu6", "bnaddrelu") or (op.kind in ("conv", "convT") and
+            if op.kind in ("bn", "bnrelu", "bnrelu6", "bnaddrelu") or (op.kind in ("conv", "convrelu", "convT") and
                                                                        "bias" in op.params):
                 rows = op.numel // op.shape[-1]  # conv bias gradient: per-channel sum of dy
                 s = max(s, lib.bn_scratch_bytes(rows, op.shape[-1]))
@@ -152,7 +152,7 @@ class Network:
         out, pos, dst = [], 0, 0
         for nid, name, t in self.param_items():
             n = t.numel()
-            if name == "weight" and self.op(nid).kind == "conv":
+            if name == "weight" and self.op(nid).kind in ("conv", "convrelu"):
                 out.append((nid, pos, dst, n))
                 dst += (n + 7) // 8 * 8
             pos += n
@@ -187,15 +187,22 @@ class Network:
         nodes, backward, inters = [], [], []
         for op in self.ops:
             nodes.append({"id": op.id, "output_bytes": op.nbytes, "deps": list(op.deps)})
-            impls = [{"name": n, "deps_kind": k,
-                      "extra_deps": [op.attrs["x"]] if op.kind == "bnaddrelu" and n == "bwd-out" else []}
-                     for n, k in BWD_IMPLS[op.kind]]
+            impls = [{"name": n, "deps_kind": k, "extra_deps": self._extra_deps(op, n)} for n, k in BWD_IMPLS[op.kind]]
             backward.append({"node": op.id, "grad_bytes": self.grad_bytes(op), "impls": impls})
             if op.id in self.intermediate_of:
                 u = self.intermediate_of[op.id]
                 inters.append({"id": u, "bytes": self.intermediate_bytes[u], "creator": op.id})
         return {"format": 1, "params_bytes": self.params_bytes(), "nodes": nodes,
                 "backward": backward, "intermediates": inters}
+
+    def _extra_deps(self, op: Op, impl: str) -> list:
+        if op.kind == "bnaddrelu" and impl == "bwd-out":
+            return [op.attrs["x"]]
+        if op.kind == "convrelu" and not op.attrs.get("split"):  # the gate: its own ReLU mask
+            return [self.intermediate_of[op.id]]
+        if op.kind == "wgrad" and self.op(op.attrs["conv"]).kind == "convrelu":
+            return [self.intermediate_of[op.attrs["conv"]]]
+        return []
 
     def label_count(self) -> int:
         """Rows of the loss: images, or pixels for a per-pixel (segmentation) loss."""
@@ -212,7 +219,7 @@ class Network:
         lib = _native.lib()
         fwd, bwd = [], []
         x = list(op.deps)
-        if op.kind == "conv":
+        if op.kind in ("conv", "convrelu"):
             d = self.conv_desc(op)
             fwd.append(("implicit", 0))
             ws = lib.conv_ws_bytes(1, 0, d)
@@ -221,15 +228,18 @@ class Network:
             if op.attrs.get("split"):  # backward = dgrad only: reads dy and the weights, not x
                 bwd.append(("splitk", lib.conv_ws_bytes(1, 1, d), []))
                 bwd.append(("implicit", lib.conv_ws_bytes(0, 1, d), []))
-            else:
-                bwd.append(("splitk", lib.conv_ws_bytes(1, 3, d), x))
-                bwd.append(("implicit", lib.conv_ws_bytes(0, 3, d), x))
+            else:  # convrelu: dy is first gated by the ReLU's mask
+                xm = x + ([self.intermediate_of[op.id]] if op.kind == "convrelu" else [])
+                bwd.append(("splitk", lib.conv_ws_bytes(1, 3, d), xm))
+                bwd.append(("implicit", lib.conv_ws_bytes(0, 3, d), xm))
         elif op.kind == "wgrad":  # split conv's weight gradient: reads the conv input x and dy
             conv = self.op(op.attrs["conv"])
             d = self.conv_desc(conv)
             fwd.append(("none", 0))
-            bwd.append(("splitk", lib.conv_ws_bytes(1, 2, d), [conv.deps[0]]))
-            bwd.append(("implicit", lib.conv_ws_bytes(0, 2, d), [conv.deps[0]]))
+            # a split convrelu's weight-gradient stage runs first: it gates dy in place with the mask
+            xm = [conv.deps[0]] + ([self.intermediate_of[conv.id]] if conv.kind == "convrelu" else [])
+            bwd.append(("splitk", lib.conv_ws_bytes(1, 2, d), xm))
+            bwd.append(("implicit", lib.conv_ws_bytes(0, 2, d), xm))
         elif op.kind == "fc":
             n, fi = self.fc_dims(op)
             fo = op.shape[1]
@@ -333,7 +343,7 @@ class Network:
     def conv_flops(self) -> int:
         tot = 0
         for op in self.ops:
-            if op.kind == "conv":
+            if op.kind in ("conv", "convrelu"):
                 cin = self.op(op.deps[0]).shape[3]
                 tot += 2 * op.numel * cin * op.attrs["r"] * op.attrs["s"]
             elif op.kind == "fc":
@@ -350,6 +360,7 @@ def _cost(costs, key, fallback):
 BWD_IMPLS = {
     "input": [("none", "input")],
     "conv": [("splitk", "input"), ("implicit", "input")],
+    "convrelu": [("splitk", "input"), ("implicit", "input")],  # + its mask (extra_deps)
     "wgrad": [("splitk", "input"), ("implicit", "input")],  # catalog deps: the conv's input (see split)
     "fc": [("gemm-splitk", "input"), ("gemm", "input")],
     "bn": [("bwd-in", "input"), ("bwd-out", "output")],
@@ -374,6 +385,43 @@ BWD_IMPLS = {
 
 def _pair(v):
     return v if isinstance(v, int) else v[0]
+
+
+def fuse_conv_relu(ops: list[Op]) -> list[Op]:
+    """Merge every conv whose only reader is a ReLU into one "convrelu" op (VGG: the
+    convs have no BN).  The pre-activation is never kept: the fused op writes
+    y = relu(conv(x)) and the ReLU's 1-bit sign mask (its intermediate), and its
+    backward gates dy with the mask in place before the conv's data / weight gradients --
+    so a conv's backward holds dy and x (and the 1-bit mask), never a second full-size
+    gradient (SURVEY §8 K4-K5 with the conv of K1-K3).  Ids are renumbered in order."""
+    readers: dict[int, list[int]] = {}
+    for op in ops:
+        for j in op.deps:
+            readers.setdefault(j, []).append(op.id)
+    fused_into: dict[int, int] = {}  # relu id -> conv id
+    for op in ops:
+        if op.kind == "conv" and len(readers.get(op.id, [])) == 1:
+            r = ops[readers[op.id][0] - 1]
+            if r.kind == "relu" and r.deps == (op.id,):
+                fused_into[r.id] = op.id
+    new_id: dict[int, int] = {}
+    out: list[Op] = []
+    for op in ops:
+        if op.id in fused_into:
+            new_id[op.id] = new_id[fused_into[op.id]]
+            continue
+        nid = len(out) + 1
+        new_id[op.id] = nid
+        fused = op.id in fused_into.values()
+        attrs = dict(op.attrs)
+        if "inputs" in attrs:
+            attrs["inputs"] = [new_id[j] for j in attrs["inputs"]]
+        for key in ("x", "skip"):
+            if key in attrs:
+                attrs[key] = new_id[attrs[key]]
+        out.append(Op(nid, "convrelu" if fused else op.kind, tuple(new_id[j] for j in op.deps), op.shape, attrs,
+                      op.params, op.name + "+relu" if fused else op.name))
+    return out
 
 
 def fuse_bn_relu(ops: list[Op]) -> list[Op]:
@@ -483,7 +531,7 @@ def split_conv_backward(ops: list[Op]) -> list[Op]:
             if key in attrs:
                 attrs[key] = new_id[attrs[key]]
         deps = tuple(new_id[j] for j in op.deps)
-        split = op.kind == "conv" and ops[op.deps[0] - 1].kind != "input"
+        split = op.kind in ("conv", "convrelu") and ops[op.deps[0] - 1].kind != "input"
         if split:
             attrs["split"] = True
             attrs["wgrad_node"] = nid + 1
@@ -660,7 +708,7 @@ def trace_graph(model: torch.nn.Module, example_input: torch.Tensor, num_classes
     k = num_classes or logits.shape[1]
     ops.append(Op(len(ops) + 1, "xent", (src,), (), name="loss"))
     if fuse:
-        ops = fuse_bn_addrelu(fuse_bn_relu(ops))
+        ops = fuse_bn_addrelu(fuse_bn_relu(fuse_conv_relu(ops)))
     if split:
         ops = split_conv_backward(ops)
     return Network(ops, n, k)

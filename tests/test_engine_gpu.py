@@ -85,7 +85,7 @@ def test_engine_matches_reference_ledger_and_oracle(cuda, r18, which):
         got = rt.pview[(nid, pname)].view(v.shape)
         assert rel(got, v) <= REL, (name, net.op(nid).name, pname, rel(got, v))
         gg = st.grads[(nid, pname)]
-        if net.op(nid).kind == "conv" and pname == "weight":
+        if net.op(nid).kind in ("conv", "convrelu") and pname == "weight":
             gg = gg.permute(0, 2, 3, 1)
         assert rel(rt.gview[(nid, pname)].view(gg.shape), gg) <= REL, (name, net.op(nid).name, pname, "grad")
     for op in net.ops:
@@ -158,21 +158,27 @@ def test_invalid_schedule_raises(cuda, r18):
         rt.plan(M.schedule_from_doc(doc), g, cat)
 
 
-def test_vgg_style_engine(cuda):
+@pytest.mark.parametrize("fuse,split", [(False, False), (True, False), (True, True)])
+def test_vgg_style_engine(cuda, fuse, split):
     """VGG-family ops (biased convs, identity adaptive pool, flatten -> fc, dropout)
     under a recompute schedule: ledger = simulate(), every recompute bit-identical
-    (dropout regenerates its mask), loss / weights / gradients = CPU oracle."""
+    (dropout regenerates its mask), loss / weights / gradients = CPU oracle; also with
+    conv+ReLU fused (convrelu: in-place ReLU + mask, dy gated in place) and split."""
     from nets import SmallVGG
 
     torch.manual_seed(0)
-    net = M.trace_graph(SmallVGG(), torch.empty(4, 3, 32, 32, device="meta"), 10)
+    net = M.trace_graph(SmallVGG(), torch.empty(4, 3, 32, 32, device="meta"), 10, fuse, split)
     assert any(op.kind == "dropout" for op in net.ops)
     g = M.load_graph(net.graph_doc())
     cat = M.load_catalog(net.catalog_doc(), g)
     se = M.store_everything_schedule(g, cat)
     act = M.simulate(se, g, cat).peak_memory - g.params_bytes
     from paper_2010_14501_b200.planner import plan_schedule
-    sched, _ = plan_schedule(g, cat, g.params_bytes + int(0.6 * act), kinds=net.storable_kinds())
+    sched = None
+    for frac in (0.6, 0.7, 0.8):  # the tightest fraction with a recompute schedule
+        sched, _ = plan_schedule(g, cat, g.params_bytes + int(frac * act), kinds=net.storable_kinds())
+        if sched is not None and any(s.recompute for s in sched.stages):
+            break
     assert sched is not None and any(s.recompute for s in sched.stages)
     gen = torch.Generator().manual_seed(0)
     x = torch.randn(4, 3, 32, 32, generator=gen)
@@ -192,7 +198,7 @@ def test_vgg_style_engine(cuda):
     for (nid, pname), v in params_nhwc(st).items():
         assert rel(rt.pview[(nid, pname)].view(v.shape), v) <= REL, (net.op(nid).name, pname)
         gg = st.grads[(nid, pname)]
-        if net.op(nid).kind == "conv" and pname == "weight":
+        if net.op(nid).kind in ("conv", "convrelu") and pname == "weight":
             gg = gg.permute(0, 2, 3, 1)
         assert rel(rt.gview[(nid, pname)].view(gg.shape), gg) <= REL, (net.op(nid).name, pname, "grad")
     assert int(rt.seed.item()) == 1  # advanced once by the optimizer group
@@ -327,3 +333,38 @@ def test_cli_train_execute_exit_codes(cuda, tmp_path):
     (tmp_path / "bad.json").write_text(json.dumps(doc))
     assert run("execute", *common, "--schedule", str(tmp_path / "bad.json")).returncode == 5
     assert run("execute", *common, "--schedule", str(tmp_path / "s.json"), "--budget-gib", "0.01").returncode == 6
+
+
+def test_prefetch_pipeline_matches_direct_staging(cuda):
+    """Runtime.prefetch (the next batch copied while the step runs, after the step's last
+    read of the staging buffer) gives the same losses and weights, bit for bit, as staging
+    each batch synchronously -- on a schedule that recomputes the input copy as well."""
+    net = build_network("resnet18", 4, 32, num_classes=10)
+    g = M.load_graph(net.graph_doc())
+    cat = M.load_catalog(net.catalog_doc(), g)
+    sets = M.compute_dependency_sets(g)
+    act = M.simulate(M.store_everything_schedule(g, cat), g, cat).peak_memory - g.params_bytes
+    sched = M.checkpoint_heuristic(g, sets, cat, g.params_bytes + int(0.6 * act))
+    assert sched is not None
+    gen = torch.Generator().manual_seed(5)
+    xs = [torch.randn(4, 32, 32, 4, generator=gen).pin_memory() for _ in range(3)]
+    ys = [torch.randint(0, 10, (4,), generator=gen, dtype=torch.int32).pin_memory() for _ in range(3)]
+    out = []
+    for mode in ("direct", "prefetch"):
+        rt = Runtime(net, device=cuda)
+        plan = rt.plan(sched, g, cat)
+        rt.capture(plan)
+        losses = []
+        if mode == "prefetch":
+            rt.prefetch(xs[0], ys[0])
+        for i in range(3):
+            if mode == "direct":
+                lt = rt.train_step(plan, xs[i], ys[i])
+            else:
+                lt = rt.train_step(plan)
+                if i + 1 < 3:
+                    rt.prefetch(xs[i + 1], ys[i + 1])
+            losses.append(float(lt.item()))
+        out.append((losses, rt.params.clone()))
+    assert out[0][0] == out[1][0]
+    assert torch.equal(out[0][1], out[1][1])

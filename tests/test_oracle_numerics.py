@@ -136,7 +136,7 @@ def test_bitmask_roundtrip():
 
 def _torch_layout(net, op, pname, have, want):
     """Engine-layout parameter -> torch layout (conv KRSC, fc over an NHWC-flattened input)."""
-    if op.kind == "conv" and pname == "weight":
+    if op.kind in ("conv", "convrelu") and pname == "weight":
         return have[..., : want.shape[1]].permute(0, 3, 1, 2)
     if op.kind == "fc" and pname == "weight" and len(net.op(op.deps[0]).shape) == 4:
         _, h, w, c = net.op(op.deps[0]).shape
@@ -144,17 +144,23 @@ def _torch_layout(net, op, pname, have, want):
     return have
 
 
-def test_oracle_vgg_style_equals_autograd():
+@pytest.mark.parametrize("fuse,split", [(False, False), (True, False), (True, True)])
+def test_oracle_vgg_style_equals_autograd(fuse, split):
     """Conv bias, identity adaptive pool, flatten-to-fc and dropout (hash keep-mask):
-    two consecutive oracle steps under recompute schedules equal autograd + SGD."""
+    two consecutive oracle steps under recompute schedules equal autograd + SGD --
+    also with conv+ReLU fused ("convrelu": in-place ReLU and 1-bit mask, dy gated in
+    place) and with the conv backward split into dgrad / wgrad nodes."""
     from nets import SmallVGG, use_hash_dropout
 
     torch.manual_seed(0)
     model = SmallVGG()
-    net = trace_graph(model, torch.empty(2, 3, 32, 32, device="meta"), 10)
+    net = trace_graph(model, torch.empty(2, 3, 32, 32, device="meta"), 10, fuse, split)
     kinds = {op.kind for op in net.ops}
-    assert {"conv", "dropout", "fc", "maxpool"} <= kinds and "avgpool" not in kinds
-    assert all("bias" in op.params for op in net.ops if op.kind == "conv")
+    conv = "convrelu" if fuse else "conv"
+    assert {conv, "dropout", "fc", "maxpool"} <= kinds and "avgpool" not in kinds
+    assert ("wgrad" in kinds) == split
+    assert fuse == all(net.op(op.deps[0]).kind != "conv" for op in net.ops if op.kind == "relu")
+    assert all("bias" in op.params for op in net.ops if op.kind == conv)
     g = M.load_graph(net.graph_doc())
     cat = M.load_catalog(net.catalog_doc(), g)
     gen = torch.Generator().manual_seed(1)
@@ -175,7 +181,7 @@ def test_oracle_vgg_style_equals_autograd():
         got = params_nhwc(st)
         for op in net.ops:
             for pname in op.params:
-                want = ref[f"{op.name}.{pname}"]
+                want = ref[f"{op.name.split('+')[0]}.{pname}"]
                 have = _torch_layout(net, op, pname, got[(op.id, pname)], want)
                 assert _rel(have, want) < TOL, (name, op.name, pname)
 
@@ -321,7 +327,7 @@ def test_oracle_unet_equals_autograd():
         got = params_nhwc(st)
         for op in net.ops:
             for pname in op.params:
-                want = ref[f"{op.name}.{pname}"]
+                want = ref[f"{op.name.split('+')[0]}.{pname}"]
                 have = got[(op.id, pname)]
                 if op.kind == "conv" and pname == "weight":
                     have = have[..., : want.shape[1]].permute(0, 3, 1, 2)

@@ -30,6 +30,10 @@ CASES = [
     (2, 10, 10, 96, 200, 3, 3, 1, 1),     # N = 200: partial n-tile; K_out % 32 != 0 -> dgrad falls back
     (1, 5, 6, 8, 12, 3, 3, 1, 1),         # tiny channels: falls back to fp32 B
     (8, 56, 56, 64, 64, 3, 3, 1, 1),      # ResNet-50 layer-1 shape class (several waves)
+    (4, 8, 8, 128, 192, 3, 3, 1, 1),      # N = 192: the second n-tile's last two 32-col chunks are empty
+    (4, 16, 16, 64, 192, 3, 3, 1, 1),     # ... with split-K partials
+    (64, 14, 14, 64, 192, 1, 1, 1, 0),    # ... and several tiles per CTA (store-buffer pairing)
+    (64, 14, 14, 64, 200, 1, 1, 1, 0),    # N = 200: a partial trailing chunk, several tiles per CTA
 ]
 
 
@@ -110,6 +114,10 @@ def test_w16_bit_identical(cuda, case, variant):
     assert dll.monet_conv_fwd_w16(v, ctypes.byref(d), x.data_ptr(), wt.data_ptr(), hi, lo, None, y1.data_ptr(),
                                   ws.data_ptr(), wsb, None) == 0
     assert torch.equal(y0, y1)
+    y2 = torch.full_like(y0, -5.0)  # run to run: the smem-staged TMA stores are race-free
+    assert dll.monet_conv_fwd_w16(v, ctypes.byref(d), x.data_ptr(), wt.data_ptr(), hi, lo, None, y2.data_ptr(),
+                                  ws.data_ptr(), wsb, None) == 0
+    assert torch.equal(y1, y2)
     # with the conv bias (VGG / UNet convs)
     assert dll.monet_conv_fwd_bias(v, ctypes.byref(d), x.data_ptr(), wt.data_ptr(), bias.data_ptr(), y0.data_ptr(),
                                    ws.data_ptr(), wsb, None) == 0

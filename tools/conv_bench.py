@@ -47,6 +47,10 @@ def main():
         y = torch.randn(n, d.p, d.q, k, device=dev)
         dw = torch.empty_like(wt)
         dx = torch.empty_like(x)
+        n8 = (wt.numel() + 7) // 8 * 8  # the weights' bf16 split (monet_conv_*_w16)
+        planes = torch.zeros(2 * n8, dtype=torch.int16, device=dev)
+        hi, lo = planes.data_ptr(), planes.data_ptr() + 2 * n8
+        lib.split_bf16(wt.data_ptr(), hi, lo, wt.numel(), None)
         flops = 2.0 * n * d.p * d.q * k * c * r * s
         for vname in a.variants.split(","):
             v = N.CONV_VARIANTS[vname]

@@ -24,6 +24,7 @@ struct Job {
   int C, pixels;  // tensor
   int H, W;       // im2col image dims (pixels = N*H*W)
   int nq;         // issuing threads (lane 0 of warps 0..nq-1), each with its own ring of slots
+  int lane_stride;  // > 0: the issuers are lanes 0, ls, 2*ls, ... of warp 0 instead
 };
 
 __global__ void __launch_bounds__(128, 1) probe(const __grid_constant__ CUtensorMap m, Job j, int iters,
@@ -38,8 +39,9 @@ __global__ void __launch_bounds__(128, 1) probe(const __grid_constant__ CUtensor
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   __syncthreads();
-  const int q = threadIdx.x / 32;
-  if ((threadIdx.x & 31) != 0 || q >= j.nq) return;
+  const int q = j.lane_stride ? (threadIdx.x < 32 && threadIdx.x % j.lane_stride == 0 ? threadIdx.x / j.lane_stride : 99)
+                              : threadIdx.x / 32;
+  if ((!j.lane_stride && (threadIdx.x & 31) != 0) || q >= j.nq) return;
   uint64_t* bars = bars0 + q * j.slots;
   base += q * j.slots * slot_bytes;
   const long long t0 = clock64();
@@ -123,21 +125,17 @@ int main() {
     int mode, bc, bp, nbox, slots, C;
     CUtensorMapSwizzle sw;
     int nq;
+    int ls = 0;
   } cases[] = {
-      {"tiled {32c,128p} SW128 16K x4 q1", 0, 32, 128, 1, 4, 128, CU_TENSOR_MAP_SWIZZLE_128B, 1},
-      {"tiled {32c,128p} SW128 16K x4 q2", 0, 32, 128, 1, 4, 128, CU_TENSOR_MAP_SWIZZLE_128B, 2},
-      {"tiled {32c,128p} SW128 16K x3 q4", 0, 32, 128, 1, 3, 128, CU_TENSOR_MAP_SWIZZLE_128B, 4},
-      {"tiled {32c,64p} SW128 8K x4 q4", 0, 32, 64, 1, 4, 128, CU_TENSOR_MAP_SWIZZLE_128B, 4},
-      {"tiled {32c,128p,2} 3D 32K x3 q1", 2, 32, 128, 1, 3, 128, CU_TENSOR_MAP_SWIZZLE_128B, 1},
-      {"tiled {32c,128p,2} 3D 32K x3 q2", 2, 32, 128, 1, 3, 128, CU_TENSOR_MAP_SWIZZLE_128B, 2},
-      {"tiled {32c,256p} SW128 32K x3 q2", 0, 32, 256, 1, 3, 128, CU_TENSOR_MAP_SWIZZLE_128B, 2},
-      {"im2col {32c,128p} SW128 16K x4 q1", 1, 32, 128, 1, 4, 128, CU_TENSOR_MAP_SWIZZLE_128B, 1},
-      {"im2col {32c,128p} SW128 16K x4 q2", 1, 32, 128, 1, 4, 128, CU_TENSOR_MAP_SWIZZLE_128B, 2},
-      {"im2col {32c,128p} SW128 16K x3 q4", 1, 32, 128, 1, 3, 128, CU_TENSOR_MAP_SWIZZLE_128B, 4},
-      {"im2col {64c,32p} NONE 8K x4 q2", 1, 64, 32, 1, 4, 64, CU_TENSOR_MAP_SWIZZLE_NONE, 2},
-      {"im2col {64c,32p} NONE 8K x4 q4", 1, 64, 32, 1, 4, 64, CU_TENSOR_MAP_SWIZZLE_NONE, 4},
-      {"im2col {32c,256p} SW128 32K x3 q1", 1, 32, 256, 1, 3, 128, CU_TENSOR_MAP_SWIZZLE_128B, 1},
-      {"im2col {32c,256p} SW128 32K x3 q2", 1, 32, 256, 1, 3, 128, CU_TENSOR_MAP_SWIZZLE_128B, 2},
+      {"tiled {32c,128p} 16K x4 q1", 0, 32, 128, 1, 4, 128, CU_TENSOR_MAP_SWIZZLE_128B, 1},
+      {"tiled {32c,128p} 16K x4 q2 warps", 0, 32, 128, 1, 4, 128, CU_TENSOR_MAP_SWIZZLE_128B, 2},
+      {"tiled {32c,128p} 16K x4 q2 lanes", 0, 32, 128, 1, 4, 128, CU_TENSOR_MAP_SWIZZLE_128B, 2, 16},
+      {"tiled {32c,128p} 16K x3 q4 lanes", 0, 32, 128, 1, 3, 128, CU_TENSOR_MAP_SWIZZLE_128B, 4, 8},
+      {"im2col {128c,32p} NONE 16K x4 q2 warps", 1, 128, 32, 1, 4, 128, CU_TENSOR_MAP_SWIZZLE_NONE, 2},
+      {"im2col {128c,32p} NONE 16K x3 q4 warps", 1, 128, 32, 1, 3, 128, CU_TENSOR_MAP_SWIZZLE_NONE, 4},
+      {"im2col {128c,32p} NONE 16K x3 q4 lanes", 1, 128, 32, 1, 3, 128, CU_TENSOR_MAP_SWIZZLE_NONE, 4, 8},
+      {"tiled {128c,32p} NONE 16K x4 q2 warps", 0, 128, 32, 1, 4, 128, CU_TENSOR_MAP_SWIZZLE_NONE, 2},
+      {"tiled {128c,32p} NONE 16K x3 q4 warps", 0, 128, 32, 1, 3, 128, CU_TENSOR_MAP_SWIZZLE_NONE, 4},
   };
   for (size_t bytes : {size_t(32) << 20}) {
     for (const Case& k : cases) {
@@ -170,7 +168,7 @@ int main() {
         printf("%-46s encode failed (%d)\n", k.name, (int)r);
         continue;
       }
-      Job j{k.mode, k.bc, k.bp, k.nbox, k.slots, k.C, pixels, H, W, k.nq};
+      Job j{k.mode, k.bc, k.bp, k.nbox, k.slots, k.C, pixels, H, W, k.nq, k.ls};
       const int slot_bytes = k.bc * k.bp * 4 * k.nbox * (k.mode == 2 ? 2 : 1);
       const int smem = k.nq * k.slots * slot_bytes + 1024 + 8 * k.nq * k.slots;
       const int iters = 4000;
