@@ -97,6 +97,8 @@ typedef struct {
   int conv_needs_dx; /* 0 when the conv reads the network input (no dgrad) */
   int64_t rows;      /* local ops: [rows, c] NHWC */
   int c;
+  int fused_stats;   /* FWD: conv -> BN statistics handed over (monet_conv_fwd_w16_stats;
+                        BN / BNRELU: monet_bn_stats_finalize + the replay apply) */
 } monet_prof_desc;
 int monet_profile_variant(const monet_prof_desc* d, int variant, int iters, int64_t* ns, size_t* ws_bytes,
                           void* stream);
@@ -131,6 +133,19 @@ int monet_conv_fwd_w16(int variant, const monet_conv_desc* d, const float* x, co
 int monet_conv_dgrad_w16(int variant, const monet_conv_desc* d, const float* dy, const float* w, const uint16_t* w_hi,
                          const uint16_t* w_lo, float* dx, int accumulate, void* ws, size_t ws_bytes, void* stream);
 int monet_split_bf16(const float* src, uint16_t* hi, uint16_t* lo, int64_t n, void* stream);
+
+/* Conv -> BN forward without re-reading the conv output: monet_conv_fwd_w16_stats is
+ * monet_conv_fwd_w16 that also leaves per-128-row-tile BN statistics (mean, M2 per output
+ * channel) in `stats` (monet_conv_stats_bytes(d) bytes) -- from the GEMM epilogue when each
+ * tile is final in one accumulation chain, else from one extra pass over y.  The following
+ * BN's training forward is monet_bn_stats_finalize (batch mean / invstd and the running-stat
+ * update, merged in fp64 in a fixed order: deterministic) + the BN's *_fwd_replay apply. */
+size_t monet_conv_stats_bytes(const monet_conv_desc* d);
+int monet_conv_fwd_w16_stats(int variant, const monet_conv_desc* d, const float* x, const float* w,
+                             const uint16_t* w_hi, const uint16_t* w_lo, const float* bias, float* y, void* stats,
+                             void* ws, size_t ws_bytes, void* stream);
+int monet_bn_stats_finalize(const void* stats, int64_t rows, int c, float eps, float momentum, int update_running,
+                            float* mean, float* invstd, float* running_mean, float* running_var, void* stream);
 int monet_split_bf16_segments(const float* src, uint16_t* hi, uint16_t* lo, const int64_t* table, int nseg,
                               int64_t max_count, void* stream);
 

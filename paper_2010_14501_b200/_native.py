@@ -26,7 +26,7 @@ _PCONV = C.POINTER(ConvDesc)
 class ProfDesc(C.Structure):
     """monet_prof_desc (include/monet_b200.h)."""
     _fields_ = [("op", C.c_int), ("pass_", C.c_int), ("conv", ConvDesc), ("conv_needs_dx", C.c_int),
-                ("rows", C.c_int64), ("c", C.c_int)]
+                ("rows", C.c_int64), ("c", C.c_int), ("fused_stats", C.c_int)]
 
 
 PROF_OP = {"conv": 0, "relu": 1, "bn": 2, "bnrelu": 3}
@@ -53,6 +53,9 @@ SIGNATURES = {
     "monet_conv_fwd_w16": (_i32, [_i32, _PCONV, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "monet_conv_dgrad_w16": (_i32, [_i32, _PCONV, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _sz, _vp]),
     "monet_split_bf16": (_i32, [_vp, _vp, _vp, _i64, _vp]),
+    "monet_conv_stats_bytes": (_sz, [_PCONV]),
+    "monet_conv_fwd_w16_stats": (_i32, [_i32, _PCONV, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "monet_bn_stats_finalize": (_i32, [_vp, _i64, _i32, _f32, _f32, _i32, _vp, _vp, _vp, _vp, _vp]),
     "monet_split_bf16_segments": (_i32, [_vp, _vp, _vp, _vp, _i32, _i64, _vp]),
     "monet_dropout_fwd": (_i32, [_vp, _vp, _i64, _f32, _vp, C.c_uint64, _vp]),
     "monet_dropout_bwd": (_i32, [_vp, _vp, _i64, _f32, _vp, C.c_uint64, _i32, _vp]),

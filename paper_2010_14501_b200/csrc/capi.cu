@@ -374,6 +374,11 @@ int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_b
       p.c_tma = tiled_map(&p.tma_c, out, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
     }
   }
+  // BN statistics from the epilogue: only where every output element is final in one TMEM
+  // chain (no split-K, no chunk flushes) and the TMA-store epilogue runs
+  if (p.stats && !(p.c_tma && p.epi == EPI_STORE && p.splits == 1 && (p.kb_per_split + 1) / 2 <= p.chunk_stages))
+    p.stats = nullptr;
+  if (p.stats_done) *p.stats_done = p.stats != nullptr;
   const int tiles = p.m_tiles * p.n_tiles * p.splits;
   const int grid = pair ? 2 * std::min(tiles, kNumSMs / 2) : std::min(tiles, kNumSMs);
   const int e = !bx     ? dispatch_modes<false, false>(p, grid, st)
@@ -711,7 +716,9 @@ size_t monet_conv_ws_bytes(int variant, int pass, const monet_conv_desc* d) {
 }
 
 static int conv_fwd_impl(int variant, const monet_conv_desc* d, const float* x, const float* w, const uint16_t* w_hi,
-                         const uint16_t* w_lo, float* y, void* ws, size_t ws_bytes, void* stream) {
+                         const uint16_t* w_lo, float* y, void* ws, size_t ws_bytes, void* stream,
+                         float* stats = nullptr, int* stats_done = nullptr) {
+  if (stats_done) *stats_done = 0;
   if (int e = check_desc(d)) return e;
   const FView f = fprop_view(variant, d);
   if (f.on && ws != nullptr && ws_bytes >= f.pad_bytes + f.w_bytes && tma_available()) {
@@ -733,7 +740,10 @@ static int conv_fwd_impl(int variant, const monet_conv_desc* d, const float* x, 
     p.ldc = d->k;
     return launch_gemm(p, MONET_CONV_IMPLICIT, 0, nullptr, 0, S(stream));
   }
-  return launch_gemm_w16(conv_params(MONET_PASS_FWD, d, x, w, y), w_hi, w_lo, variant, 0, ws, ws_bytes, S(stream));
+  GemmParams p = conv_params(MONET_PASS_FWD, d, x, w, y);
+  p.stats = stats;
+  p.stats_done = stats_done;
+  return launch_gemm_w16(p, w_hi, w_lo, variant, 0, ws, ws_bytes, S(stream));
 }
 
 int monet_conv_fwd(int variant, const monet_conv_desc* d, const float* x, const float* w, float* y, void* ws,
@@ -745,11 +755,14 @@ static int bn_blocks(int64_t rows);
 
 static int conv_fwd_bias_impl(int variant, const monet_conv_desc* d, const float* x, const float* w,
                               const uint16_t* w_hi, const uint16_t* w_lo, const float* bias, float* y, void* ws,
-                              size_t ws_bytes, void* stream) {
+                              size_t ws_bytes, void* stream, float* stats = nullptr, int* stats_done = nullptr) {
+  if (stats_done) *stats_done = 0;
   if (int e = check_desc(d)) return e;
   GemmParams p = conv_params(MONET_PASS_FWD, d, x, w, y);
   if (uses_bx3(variant)) {  // bias added in the epilogue (or the split-K reduce)
     p.bias = bias;
+    p.stats = stats;
+    p.stats_done = stats_done;
     return launch_gemm_w16(p, w_hi, w_lo, variant, 0, ws, ws_bytes, S(stream));
   }
   const long long tot = (long long)p.M * p.N;
@@ -766,6 +779,137 @@ int monet_conv_fwd_w16(int variant, const monet_conv_desc* d, const float* x, co
                        const uint16_t* w_lo, const float* bias, float* y, void* ws, size_t ws_bytes, void* stream) {
   if (bias != nullptr) return conv_fwd_bias_impl(variant, d, x, w, w_hi, w_lo, bias, y, ws, ws_bytes, stream);
   return conv_fwd_impl(variant, d, x, w, w_hi, w_lo, y, ws, ws_bytes, stream);
+}
+
+// ------------------------------------------------------- conv -> BN statistics
+// Per-tile (128-row) BN statistics of a conv output [M][K]: (mean, M2) per channel
+// ([T][2][K], T = ceil(M / 128)), computed in the GEMM epilogue when the tile is final in
+// one chain, else by tile_stats_kernel over y (pivot = the tile's first row).  The BN
+// forward then merges the tiles (bn_tile_merge -> bn_finalize_tiles, Chan's formula in fp64,
+// fixed order) instead of re-reading the conv output.
+static long long conv_rows(const monet_conv_desc* d) { return (long long)d->n * d->p * d->q; }
+static long long stat_tiles(long long rows) { return (rows + 127) / 128; }
+
+__global__ void tile_stats_kernel(const float* __restrict__ y, long long M, int N, float* stats) {
+  const long long r0 = (long long)blockIdx.x * 128;
+  const int cnt = (int)min(128LL, M - r0);
+  for (int c = 4 * threadIdx.x; c < N; c += 4 * blockDim.x) {
+    const float4 piv = *reinterpret_cast<const float4*>(y + r0 * N + c);
+    float s1[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int r = 0; r < cnt; ++r) {
+      const float4 v = *reinterpret_cast<const float4*>(y + (r0 + r) * N + c);
+      const float d0 = v.x - piv.x, d1 = v.y - piv.y, d2 = v.z - piv.z, d3 = v.w - piv.w;
+      s1[0] += d0; s1[1] += d1; s1[2] += d2; s1[3] += d3;
+      s2[0] += d0 * d0; s2[1] += d1 * d1; s2[2] += d2 * d2; s2[3] += d3 * d3;
+    }
+    const float p[4] = {piv.x, piv.y, piv.z, piv.w};
+    for (int j = 0; j < 4; ++j) {
+      stats[(long long)(blockIdx.x * 2) * N + c + j] = p[j] + s1[j] / cnt;
+      stats[(long long)(blockIdx.x * 2 + 1) * N + c + j] = fmaxf(s2[j] - s1[j] * s1[j] / cnt, 0.f);
+    }
+  }
+}
+
+struct Welford {
+  double n, mean, m2;
+};
+__device__ __forceinline__ Welford chan_merge(Welford a, Welford b) {
+  if (b.n == 0.0) return a;
+  if (a.n == 0.0) return b;
+  const double n = a.n + b.n, delta = b.mean - a.mean;
+  return Welford{n, a.mean + delta * (b.n / n), a.m2 + b.m2 + delta * delta * (a.n * b.n / n)};
+}
+
+// groups of 32 tiles x 32 channels per block: warp w merges tiles 4w..4w+3 (lane = channel,
+// coalesced), warp 0 merges the 8 warps in order -> part[g] = (n, mean, M2) in fp64
+__global__ void bn_tile_merge_kernel(const float* __restrict__ stats, long long T, long long M, int C,
+                                     double* part) {
+  __shared__ double sm[8][3][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.y * 32 + lane;
+  Welford acc{0.0, 0.0, 0.0};
+  if (c < C) {
+    for (int i = 0; i < 4; ++i) {
+      const long long t = (long long)blockIdx.x * 32 + warp * 4 + i;
+      if (t >= T) break;
+      const double cnt = (double)min(128LL, M - t * 128);
+      acc = chan_merge(acc, Welford{cnt, (double)stats[(t * 2) * C + c], (double)stats[(t * 2 + 1) * C + c]});
+    }
+  }
+  sm[warp][0][lane] = acc.n;
+  sm[warp][1][lane] = acc.mean;
+  sm[warp][2][lane] = acc.m2;
+  __syncthreads();
+  if (warp == 0 && c < C) {
+    Welford a{0.0, 0.0, 0.0};
+    for (int w = 0; w < 8; ++w) a = chan_merge(a, Welford{sm[w][0][lane], sm[w][1][lane], sm[w][2][lane]});
+    part[((long long)blockIdx.x * 3) * C + c] = a.n;
+    part[((long long)blockIdx.x * 3 + 1) * C + c] = a.mean;
+    part[((long long)blockIdx.x * 3 + 2) * C + c] = a.m2;
+  }
+}
+
+// one warp per channel: lanes merge groups lane, lane+32, ... then a fixed xor tree (lower lane
+// first) -> mean, invstd, running statistics
+__global__ void bn_finalize_tiles_kernel(const double* __restrict__ part, long long G, long long rows, int C,
+                                         float eps, float momentum, int update_running, float* mean_out,
+                                         float* invstd_out, float* running_mean, float* running_var) {
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c >= C) return;
+  Welford a{0.0, 0.0, 0.0};
+  for (long long g = lane; g < G; g += 32)
+    a = chan_merge(a, Welford{part[(g * 3) * C + c], part[(g * 3 + 1) * C + c], part[(g * 3 + 2) * C + c]});
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const Welford b{__shfl_xor_sync(0xffffffffu, a.n, o), __shfl_xor_sync(0xffffffffu, a.mean, o),
+                    __shfl_xor_sync(0xffffffffu, a.m2, o)};
+    a = (lane & o) ? chan_merge(b, a) : chan_merge(a, b);
+  }
+  if (lane != 0) return;
+  double var = a.m2 / (double)rows;
+  if (var < 0.0) var = 0.0;
+  mean_out[c] = (float)a.mean;
+  invstd_out[c] = (float)(1.0 / sqrt(var + (double)eps));
+  if (update_running) {
+    const double unbiased = rows > 1 ? a.m2 / (double)(rows - 1) : var;
+    running_mean[c] = (float)((1.0 - momentum) * running_mean[c] + momentum * a.mean);
+    running_var[c] = (float)((1.0 - momentum) * running_var[c] + momentum * unbiased);
+  }
+}
+
+size_t monet_conv_stats_bytes(const monet_conv_desc* d) {
+  if (!d) return 0;
+  const long long T = stat_tiles(conv_rows(d)), G = (T + 31) / 32;
+  return align256((size_t)T * 2 * d->k * sizeof(float)) + align256((size_t)G * 3 * d->k * sizeof(double));
+}
+
+int monet_conv_fwd_w16_stats(int variant, const monet_conv_desc* d, const float* x, const float* w,
+                             const uint16_t* w_hi, const uint16_t* w_lo, const float* bias, float* y, void* stats,
+                             void* ws, size_t ws_bytes, void* stream) {
+  if (!stats) return -(int)cudaErrorInvalidValue;
+  float* st = static_cast<float*>(stats);
+  int fused = 0;
+  const int e = bias != nullptr
+                    ? conv_fwd_bias_impl(variant, d, x, w, w_hi, w_lo, bias, y, ws, ws_bytes, stream, st, &fused)
+                    : conv_fwd_impl(variant, d, x, w, w_hi, w_lo, y, ws, ws_bytes, stream, st, &fused);
+  if (e) return e;
+  if (!fused)  // split-K, chunked chains or the fp32-weight path: one pass over y
+    tile_stats_kernel<<<(int)stat_tiles(conv_rows(d)), 256, 0, S(stream)>>>(y, conv_rows(d), d->k, st);
+  return last_error();
+}
+
+int monet_bn_stats_finalize(const void* stats, int64_t rows, int c, float eps, float momentum, int update_running,
+                            float* mean, float* invstd, float* running_mean, float* running_var, void* stream) {
+  if (!stats || rows <= 0 || c <= 0) return -(int)cudaErrorInvalidValue;
+  const long long T = stat_tiles(rows), G = (T + 31) / 32;
+  const float* st = static_cast<const float*>(stats);
+  double* part = reinterpret_cast<double*>(static_cast<char*>(const_cast<void*>(stats)) +
+                                           align256((size_t)T * 2 * c * sizeof(float)));
+  bn_tile_merge_kernel<<<dim3((unsigned)G, (c + 31) / 32), 256, 0, S(stream)>>>(st, T, rows, c, part);
+  bn_finalize_tiles_kernel<<<(c + 7) / 8, 256, 0, S(stream)>>>(part, G, rows, c, eps, momentum, update_running, mean,
+                                                               invstd, running_mean, running_var);
+  return last_error();
 }
 
 int monet_split_bf16(const float* src, uint16_t* hi, uint16_t* lo, int64_t n, void* stream) {

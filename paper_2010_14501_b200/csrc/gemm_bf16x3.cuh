@@ -77,9 +77,10 @@ struct Cfg {
   static constexpr int kBStages = kW16 ? (NB == BN ? 4 : 6) : (NB == BN ? 3 : 4);
   // pre-split-B kernels store the output through smem + TMA: two 32x32 fp32 blocks per epilogue warp
   static constexpr int kEpiBytes = kW16 ? kEpiWarps * 2 * 32 * 32 * 4 : 0;
+  static constexpr int kStatBytes = kW16 ? kEpiWarps * 2 * 32 * 4 : 0;  // per-quarter (mean, M2) x 32 cols
   static constexpr int kNumBars = 2 * kRawSlots + 2 * kAStages + 2 * kBStages + 2 * kAccStages;
   static constexpr int kSmemBytes =
-      kRawSlots * kRawBytes + kBStages * kStageBytes + kEpiBytes + 1024 + 8 * kNumBars + 16;
+      kRawSlots * kRawBytes + kBStages * kStageBytes + kEpiBytes + kStatBytes + 1024 + 8 * kNumBars + 16;
   static_assert(kSmemBytes <= 232448, "shared memory budget");
 };
 
@@ -457,6 +458,63 @@ struct Loader {
     cp_async_mbar_arrive(bar);
   }
 };
+// BN statistics of a 128-row output tile from the epilogue (the conv -> BN forward):
+// each warp reduces its 32 rows per column around a pivot (its first row) -- a transposed
+// butterfly leaves column l's sums on lane l --, the four warps' (mean, M2) meet in smem and
+// warp 0 merges them in order (Chan) into stats[mt][0|1][n].  One named barrier pair per
+// 32-column chunk among the four epilogue warps.  Deterministic.
+MONET_DEV void tile_stats(const GemmParams& p, const float (&v)[32], float* sm, int row0, int quarter, int lane,
+                          int n0, int mt) {
+  const int rows_here = min(32, p.M - (row0 + quarter * 32));
+  const bool ok = lane < rows_here;
+  float d[32], q[32], pv[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float piv = __shfl_sync(0xffffffffu, v[j], 0);
+    const float t = ok ? v[j] - piv : 0.f;
+    pv[j] = piv;
+    d[j] = t;
+    q[j] = t * t;
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const float s1 = up ? d[i] : d[i + o], k1 = up ? d[i + o] : d[i];
+      const float s2 = up ? q[i] : q[i + o], k2 = up ? q[i + o] : q[i];
+      d[i] = k1 + __shfl_xor_sync(0xffffffffu, s1, o);
+      q[i] = k2 + __shfl_xor_sync(0xffffffffu, s2, o);
+      pv[i] = up ? pv[i + o] : pv[i];
+    }
+  }
+  float mean = 0.f, m2 = 0.f;
+  if (rows_here > 0) {
+    const float inv = 1.f / (float)rows_here;
+    mean = pv[0] + d[0] * inv;
+    m2 = fmaxf(q[0] - d[0] * d[0] * inv, 0.f);
+  }
+  sm[(quarter * 2) * 32 + lane] = mean;
+  sm[(quarter * 2 + 1) * 32 + lane] = m2;
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  if (quarter == 0 && n0 + lane < p.N) {
+    float n = 0.f, mu = 0.f, s = 0.f;
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+      const int c = min(32, p.M - (row0 + qq * 32));
+      if (c <= 0) break;
+      const float mb = sm[(qq * 2) * 32 + lane], sb = sm[(qq * 2 + 1) * 32 + lane];
+      const float nn = n + (float)c, delta = mb - mu;
+      mu += delta * ((float)c / nn);
+      s += sb + delta * delta * (n * (float)c / nn);
+      n = nn;
+    }
+    p.stats[(long long)(mt * 2) * p.N + n0 + lane] = mu;
+    p.stats[(long long)(mt * 2 + 1) * p.N + n0 + lane] = s;
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+
 // Debug wait-time accounting (p.dbg_t != nullptr): counters per CTA
 //   0 loader raw_empty, 3 MMA a_full, 4 MMA b_full, 5 MMA tempty, 6 epilogue tfull,
 //   7 A-split st_empty, 8 A-split raw_full, 9 B-split st_empty, 10 B-split raw_full,
@@ -498,7 +556,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
   uint8_t* raw = smem;                                  // kRawSlots x (A[, B]) fp32
   uint8_t* bst = smem + kRawSlots * kRawBytes;          // kBStages x (B hi, B lo) bf16
   uint8_t* epi_st = bst + kBStages * kStageBytes;       // epilogue staging (pre-split-B kernels)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(epi_st + CF::kEpiBytes);
+  float* stat_sm = reinterpret_cast<float*>(epi_st + CF::kEpiBytes);  // BN statistics exchange
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi_st + CF::kEpiBytes + CF::kStatBytes);
   uint64_t* raw_full = bars;                            // loaders -> splitters
   uint64_t* raw_empty = raw_full + kRawSlots;           // splitters -> loaders
   uint64_t* a_full = raw_empty + kRawSlots;             // A-split -> MMA
@@ -857,6 +916,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] += (n0 + j < p.N) ? __ldg(p.bias + n0 + j) : 0.f;
               }
+              if (p.stats) tile_stats(p, v, stat_sm, mt * kTileM, quarter, lane, n0, mt);
               // the warp's two staging blocks alternate per store (not per chunk: skipped chunks
               // would break the pairing); wait until the store two back has read its block
               uint8_t* blk = epi_st + (quarter * 2 + (epi_stores & 1)) * 4096;

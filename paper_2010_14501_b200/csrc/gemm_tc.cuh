@@ -103,6 +103,9 @@ struct GemmParams {
   unsigned long long* dbg_t;  // debug: per-CTA wait-time counters of the bf16x3 pipeline roles (nullptr = off)
   float* dbg_a;     // debug: bf16x3 A-split dumps the raw A operand [M][Kpad] here (nullptr = off)
   float* dbg_b;     // debug: bf16x3 B-split dumps the raw B operand [N][Kpad]
+  float* stats;     // bf16x3 pre-split-B kernels, single-chain EPI_STORE tiles: per-tile BN statistics of the
+                    //   output, [m_tiles][2][N] = (mean, M2) over the tile's rows (nullptr = off)
+  int* stats_done;  // host: set to 1 when the launch computes `stats` (else the caller reduces the output)
   int c_tma;        // bf16x3 pre-split-B kernels: the epilogue stages 32x32 blocks in smem and
                     //   stores (or reduce-adds) them with TMA through tma_c (0 = per-thread stores)
   CUtensorMap tma_a, tma_b;  // bf16x3: TMA descriptors (valid when Operand::tma != 0)

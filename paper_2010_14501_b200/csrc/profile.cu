@@ -81,7 +81,11 @@ extern "C" int monet_profile_variant(const monet_prof_desc* d, int variant, int 
     uint16_t* wlo = whi + wn8;
     if (int e = monet_split_bf16(w, whi, wlo, wn, st)) return e;
     const bool need_dx = d->conv_needs_dx != 0;
+    float* stats = (pass == MONET_PASS_FWD && d->fused_stats) ? B.get(monet_conv_stats_bytes(c), 8) : nullptr;
+    if (B.err) return B.err;
     run = [=]() -> int {  // BWD: dgrad (if the input has a gradient) + wgrad; DGRAD / WGRAD: one pass
+      if (pass == MONET_PASS_FWD && stats)
+        return monet_conv_fwd_w16_stats(variant, c, x, w, whi, wlo, nullptr, y, stats, wsp, ws, st);
       if (pass == MONET_PASS_FWD) return monet_conv_fwd_w16(variant, c, x, w, whi, wlo, nullptr, y, wsp, ws, st);
       if ((pass == MONET_PASS_BWD && need_dx) || pass == MONET_PASS_DGRAD)
         if (int e = monet_conv_dgrad_w16(variant, c, y, w, whi, wlo, dx, 0, wsp, ws, st)) return e;
@@ -107,9 +111,18 @@ extern "C" int monet_profile_variant(const monet_prof_desc* d, int variant, int 
     float *g = B.get(c * 4, 5, 1.f), *b = B.get(c * 4, 6), *mean = B.get(c * 4, 7), *inv = B.get(c * 4, 8, 1.f);
     float *rm = B.get(c * 4, 9), *rv = B.get(c * 4, 10, 1.f), *dg = B.get(c * 4, 11), *db = B.get(c * 4, 12);
     float* scratch = B.get(monet_bn_scratch_bytes(rows, c), 13);
+    // conv-provided statistics: tile stats [T][2][c] (+ merge partials), positive M2
+    const long long T = (rows + 127) / 128;
+    const size_t sb = ((size_t)T * 2 * c * 4 + 255) / 256 * 256 + ((size_t)((T + 31) / 32) * 3 * c * 8 + 255) / 256 * 256;
+    float* stats = d->fused_stats ? B.get(sb, 14, 2.f) : nullptr;
     if (B.err) return B.err;
     const bool fused = d->op == MONET_OP_BNRELU;
     run = [=]() -> int {
+      if (pass == MONET_PASS_FWD && stats) {
+        if (int e = monet_bn_stats_finalize(stats, rows, c, 1e-5f, 0.1f, 1, mean, inv, rm, rv, st)) return e;
+        return fused ? monet_bnrelu_fwd_replay(x, y, g, b, mean, inv, rows, c, st)
+                     : monet_bn_fwd_replay(x, y, g, b, mean, inv, rows, c, st);
+      }
       if (pass == MONET_PASS_FWD)
         return fused ? monet_bnrelu_fwd_train(x, y, g, b, mean, inv, rm, rv, rows, c, 1e-5f, 0.1f, 1, scratch, st)
                      : monet_bn_fwd_train(x, y, g, b, mean, inv, rm, rv, rows, c, 1e-5f, 0.1f, 1, scratch, st);

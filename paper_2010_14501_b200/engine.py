@@ -162,6 +162,9 @@ class Runtime:
             self.w16_lo = self.w16_hi + nb // 2
             for nid, _, dst, _ in segs:
                 self.w16[nid] = (self.w16_hi + 2 * dst, self.w16_lo + 2 * dst)
+        self.stats_convs = self.net.stats_convs()
+        self.stats_bns = {bn: conv for conv, bn in self.stats_convs.items()}
+        self.conv_stats_ptr = self.fixed.data_ptr() + self.region["conv_stats"][0]
         stats = f32("bn_stats")
         self.bn = {}
         pos = 0
@@ -349,8 +352,12 @@ class Runtime:
                 wt = self.pview[(op.id, "weight")].data_ptr()
                 hi, lo = self.w16.get(op.id, (None, None))
                 bias = self.pview[(op.id, "bias")].data_ptr() if "bias" in op.params else None
-                out.append(("k", lib.monet_conv_fwd_w16, (v, C.byref(d), xs[0], wt, hi, lo, bias, y, ws,
-                                                          s.workspace, None), d))
+                if s.kind == "forward" and op.id in self.stats_convs:  # + the next BN's batch statistics
+                    out.append(("k", lib.monet_conv_fwd_w16_stats, (v, C.byref(d), xs[0], wt, hi, lo, bias, y,
+                                                                    self.conv_stats_ptr, ws, s.workspace, None), d))
+                else:
+                    out.append(("k", lib.monet_conv_fwd_w16, (v, C.byref(d), xs[0], wt, hi, lo, bias, y, ws,
+                                                              s.workspace, None), d))
                 if op.kind == "convrelu":  # the fused ReLU, in place on y (+ its sign mask when planned)
                     mid = net.intermediate_of[op.id]
                     mask = P(("a", mid)) if mid in s.planned_ints else None
@@ -384,7 +391,10 @@ class Runtime:
                 sm, si, rm, rv = (t.data_ptr() for t in self.bn[op.id])
                 gma = self.pview[(op.id, "weight")].data_ptr()
                 bta = self.pview[(op.id, "bias")].data_ptr()
-                if s.kind == "forward":
+                if s.kind == "forward" and op.id in self.stats_bns:  # statistics left by the conv
+                    out.append(("k", lib.monet_bn_stats_finalize, (self.conv_stats_ptr, rows, c, C.c_float(op.attrs["eps"]), C.c_float(op.attrs["momentum"]), 1, sm, si, rm, rv, None)))
+                    out.append(("k", lib.monet_bn_fwd_replay, (xs[0], y, gma, bta, sm, si, rows, c, None)))
+                elif s.kind == "forward":
                     out.append(("k", lib.monet_bn_fwd_train,
                                 (xs[0], y, gma, bta, sm, si, rm, rv, rows, c, C.c_float(op.attrs["eps"]),
                                  C.c_float(op.attrs["momentum"]), 1, self.scratch_ptr, None)))
@@ -397,7 +407,11 @@ class Runtime:
                 gma = self.pview[(op.id, "weight")].data_ptr()
                 bta = self.pview[(op.id, "bias")].data_ptr()
                 six = op.kind == "bnrelu6"
-                if s.kind == "forward":
+                if s.kind == "forward" and op.id in self.stats_bns:  # statistics left by the conv
+                    out.append(("k", lib.monet_bn_stats_finalize, (self.conv_stats_ptr, rows, c, C.c_float(op.attrs["eps"]), C.c_float(op.attrs["momentum"]), 1, sm, si, rm, rv, None)))
+                    out.append(("k", lib.monet_bnrelu6_fwd_replay if six else lib.monet_bnrelu_fwd_replay,
+                                (xs[0], y, gma, bta, sm, si, rows, c, None)))
+                elif s.kind == "forward":
                     out.append(("k", lib.monet_bnrelu6_fwd_train if six else lib.monet_bnrelu_fwd_train,
                                 (xs[0], y, gma, bta, sm, si, rm, rv, rows, c, C.c_float(op.attrs["eps"]),
                                  C.c_float(op.attrs["momentum"]), 1, self.scratch_ptr, None)))
@@ -419,7 +433,10 @@ class Runtime:
                 gma = self.pview[(op.id, "weight")].data_ptr()
                 bta = self.pview[(op.id, "bias")].data_ptr()
                 xp, kp = P(("in", op.attrs["x"])), P(("in", op.attrs["skip"]))
-                if s.kind == "forward":
+                if s.kind == "forward" and op.id in self.stats_bns:  # statistics left by the conv
+                    out.append(("k", lib.monet_bn_stats_finalize, (self.conv_stats_ptr, rows, c, C.c_float(op.attrs["eps"]), C.c_float(op.attrs["momentum"]), 1, sm, si, rm, rv, None)))
+                    out.append(("k", lib.monet_bnaddrelu_fwd_replay, (xp, kp, y, gma, bta, sm, si, rows, c, None)))
+                elif s.kind == "forward":
                     out.append(("k", lib.monet_bnaddrelu_fwd_train,
                                 (xp, kp, y, gma, bta, sm, si, rm, rv, rows, c, C.c_float(op.attrs["eps"]),
                                  C.c_float(op.attrs["momentum"]), 1, self.scratch_ptr, None)))

@@ -113,9 +113,19 @@ def _local_calls(bx: _Bench, net, op):
         six = kind == "bnrelu6"
         fwd_fn = lib.monet_bnrelu6_fwd_train if six else lib.monet_bnrelu_fwd_train
         bwd_fn = lib.monet_bnrelu6_bwd if six else lib.monet_bnrelu_bwd
-        out[("fwd", kind)] = lambda: bx.check(fwd_fn(
-            x.data_ptr(), y.data_ptr(), g_, b_, m_, s_, rm, rv, rows, c, C.c_float(1e-5), C.c_float(0.1), 1,
-            scratch.data_ptr(), sp))
+        if op.id in net.stats_convs().values():  # statistics handed over by the conv
+            st = _stats_buf(bx, rows, c)
+            rep_fn = lib.monet_bnrelu6_fwd_replay if six else lib.monet_bnrelu_fwd_replay
+
+            def fwd_stats():
+                bx.check(lib.monet_bn_stats_finalize(st.data_ptr(), rows, c, C.c_float(1e-5), C.c_float(0.1), 1,
+                                                      m_, s_, rm, rv, sp))
+                bx.check(rep_fn(x.data_ptr(), y.data_ptr(), g_, b_, m_, s_, rows, c, sp))
+            out[("fwd", kind)] = fwd_stats
+        else:
+            out[("fwd", kind)] = lambda: bx.check(fwd_fn(
+                x.data_ptr(), y.data_ptr(), g_, b_, m_, s_, rm, rv, rows, c, C.c_float(1e-5), C.c_float(0.1), 1,
+                scratch.data_ptr(), sp))
         out[("bwd", "bwd-in")] = lambda: bx.check(bwd_fn(
             x.data_ptr(), dy.data_ptr(), dx.data_ptr(), 0, g_, b_, m_, s_, dg, db, rows, c, scratch.data_ptr(), sp))
     elif kind == "bnaddrelu":
@@ -127,9 +137,19 @@ def _local_calls(bx: _Bench, net, op):
         scratch = bx.buf(lib.monet_bn_scratch_bytes(rows, c))
         g_, b_, m_, s_, rm, rv, dg, db = (t.data_ptr() for t in ch)
         xx, kk, dk = bx.buf(op.nbytes), bx.buf(op.nbytes), bx.buf(op.nbytes)
-        out[("fwd", "bnaddrelu")] = lambda: bx.check(lib.monet_bnaddrelu_fwd_train(
-            xx.data_ptr(), kk.data_ptr(), y.data_ptr(), g_, b_, m_, s_, rm, rv, rows, c, C.c_float(1e-5),
-            C.c_float(0.1), 1, scratch.data_ptr(), sp))
+        if op.id in net.stats_convs().values():  # statistics handed over by the conv
+            st = _stats_buf(bx, rows, c)
+
+            def fwd_stats():
+                bx.check(lib.monet_bn_stats_finalize(st.data_ptr(), rows, c, C.c_float(1e-5), C.c_float(0.1), 1,
+                                                      m_, s_, rm, rv, sp))
+                bx.check(lib.monet_bnaddrelu_fwd_replay(xx.data_ptr(), kk.data_ptr(), y.data_ptr(), g_, b_, m_, s_,
+                                                         rows, c, sp))
+            out[("fwd", "bnaddrelu")] = fwd_stats
+        else:
+            out[("fwd", "bnaddrelu")] = lambda: bx.check(lib.monet_bnaddrelu_fwd_train(
+                xx.data_ptr(), kk.data_ptr(), y.data_ptr(), g_, b_, m_, s_, rm, rv, rows, c, C.c_float(1e-5),
+                C.c_float(0.1), 1, scratch.data_ptr(), sp))
         for name, src, from_out in (("bwd-out", y, 1), ("bwd-in", kk, 0)):
             out[("bwd", name)] = (lambda src=src, from_out=from_out: bx.check(lib.monet_bnaddrelu_bwd(
                 xx.data_ptr(), src.data_ptr(), from_out, dy.data_ptr(), dx.data_ptr(), 0, dk.data_ptr(), 0, g_, b_,
@@ -243,6 +263,16 @@ def _local_calls(bx: _Bench, net, op):
     return out
 
 
+def _stats_buf(bx, rows, c):
+    """A conv -> BN statistics buffer (tile means / M2, the merge scratch after them) with
+    positive values, as monet_conv_fwd_w16_stats would leave it."""
+    t = (rows + 127) // 128
+    nb = (t * 2 * c * 4 + 255) // 256 * 256 + ((t + 31) // 32 * 3 * c * 8 + 255) // 256 * 256
+    buf = bx.buf(nb)
+    buf.abs_().add_(0.5)
+    return buf
+
+
 def profile_variant(net, op, pss: str, variant: str, iters: int = 5, stream=None) -> tuple[int, int]:
     """(ns per launch, workspace bytes) of one variant through the C-ABI profiler entry
     point monet_profile_variant (csrc/profile.cu): conv fwd / bwd, ReLU, BN, fused BN+ReLU."""
@@ -262,6 +292,9 @@ def profile_variant(net, op, pss: str, variant: str, iters: int = 5, stream=None
         d.c = op.shape[-1]
         d.rows = op.numel // d.c
         v = 0 if pss == "fwd" else _native.PROF_BWD[variant]
+    # conv -> BN statistics handed over in the forward pass (Network.stats_convs)
+    sc = net.stats_convs()
+    d.fused_stats = int(pss == "fwd" and (op.id in sc or op.id in sc.values()))
     ns, ws = C.c_int64(0), C.c_size_t(0)
     if stream is None:
         stream = torch.cuda.current_stream().cuda_stream
@@ -295,7 +328,8 @@ def _signature(net, op):
     ins = tuple((net.op(j).kind == "input", net.op(j).shape) for j in op.deps)
     attrs = tuple(sorted((k, v) for k, v in op.attrs.items()
                          if isinstance(v, (int, float, str)) and k not in ("conv", "wgrad_node")))
-    return op.kind, ins, op.shape, attrs
+    sc = net.stats_convs()
+    return op.kind, ins, op.shape, attrs, op.id in sc or op.id in sc.values()
 
 
 def profile_network(net, device="cuda:0", warmup=2, iters=5, reps=3, log=None) -> dict:

@@ -158,6 +158,31 @@ class Network:
             pos += n
         return out
 
+    BN_KINDS = ("bn", "bnrelu", "bnrelu6", "bnaddrelu")
+
+    def bn_input(self, op: Op) -> int:
+        return op.attrs["x"] if op.kind == "bnaddrelu" else op.deps[0]
+
+    def stats_convs(self) -> dict:
+        """{conv id: BN id} for each conv whose output is the input of the BN that runs right
+        after it in the forward pass (split anchors have no forward work): the conv leaves the
+        BN's batch statistics in the stats scratch (monet_conv_fwd_w16_stats) and the BN's
+        training forward merges them instead of re-reading the conv output."""
+        out = {}
+        for op in self.ops:
+            if op.kind != "conv":
+                continue
+            j = op.id + 1
+            while j <= self.n and self.op(j).kind == "wgrad":
+                j += 1
+            if j <= self.n and self.op(j).kind in self.BN_KINDS and self.bn_input(self.op(j)) == op.id:
+                out[op.id] = j
+        return out
+
+    def conv_stats_bytes(self) -> int:
+        lib = _native.lib()
+        return max((lib.conv_stats_bytes(self.conv_desc(self.op(i))) for i in self.stats_convs()), default=0)
+
     def fixed_layout(self) -> dict:
         """Byte sizes of everything outside the arena (all folded into params_bytes)."""
         p = self.n_param_elems() * F32
@@ -167,6 +192,7 @@ class Network:
             "params": p, "grads": p, "momentum": p,
             "w16": 2 * 2 * plane,           # pre-split conv weights: bf16 hi plane, then lo plane
             "w16_table": 24 * len(segs),    # their segment table (monet_split_bf16_segments)
+            "conv_stats": self.conv_stats_bytes(),  # conv -> BN per-tile statistics (stats_convs)
             "bn_stats": 4 * self.bn_channels() * F32,   # saved mean/invstd, running mean/var
             "scratch": self.scratch_bytes(),
             "staging_input": self.input_bytes(),
