@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--budget-gib", type=float, default=8.0)
     ap.add_argument("--no-fuse", dest="fuse", action="store_false",
                     help="separate BN and ReLU operators (default: fused BN+ReLU ops, tracer fuse=True)")
+    ap.add_argument("--ablation", default=None, choices=["none", "conv", "out", "int", "all"],
+                    help="run the schedule planned with apply_ablation(catalog, mode) (schedules/*_abl-<mode>.json)")
     ap.add_argument("--split", action="store_true",
                     help="conv backward split into dgrad / wgrad graph nodes (tracer.split_conv_backward)")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels from Python instead of a CUDA graph")
@@ -55,13 +57,14 @@ def parse():
 
 # --------------------------------------------------------------------------- helpers
 
-def load_or_plan(net, g, cat, budget, arch, batch, image, gib):
+def load_or_plan(net, g, cat, budget, arch, batch, image, gib, ablation=None):
     import hashlib
 
     import paper_2010_14501_b200 as M
     from paper_2010_14501_b200.planner import plan_schedule
 
-    path = ROOT / "schedules" / f"{stem(arch, net)}_b{batch}_{image}_{gib:g}gib.json"
+    abl = f"_abl-{ablation}" if ablation else ""
+    path = ROOT / "schedules" / f"{stem(arch, net)}_b{batch}_{image}_{gib:g}gib{abl}.json"
     digest = lambda d: hashlib.sha256(json.dumps(d, sort_keys=True).encode()).hexdigest()[:16]  # noqa: E731
     if path.exists():
         doc = json.loads(path.read_text())
@@ -392,9 +395,12 @@ def ours_arm(args):
     gdoc = net.graph_doc()
     g = M.load_graph(gdoc)
     cat = M.load_catalog(measured_catalog(net, args) or net.catalog_doc(), g)
-    sched, pinfo, source = load_or_plan(net, g, cat, budget, args.arch, args.batch, args.image, gib)
     from paper_2010_14501_b200.schedule import fastest_store_everything_schedule
     se = fastest_store_everything_schedule(g, cat)  # min-cost no-recompute
+    cat_full = cat
+    if args.ablation:  # the schedule is planned with one ablation family; the baseline stays the same
+        cat = M.apply_ablation(cat, g, args.ablation)
+    sched, pinfo, source = load_or_plan(net, g, cat, budget, args.arch, args.batch, args.image, gib, args.ablation)
 
     # SGD lr 0.1 (momentum 0.9) as in the paper's ResNet runs; VGG-16 has no BN and
     # diverges at 0.1 from torchvision's init (loss NaN within a few steps), so it
@@ -514,7 +520,7 @@ def ours_arm(args):
     roof, local_roof, instr_ms = kernel_roofline(rt, plan, net, peaks)
 
     # ---- overhead vs the no-recompute schedule on the same kernels (analytic costs)
-    overhead_model = float(plan.trace.total_cost / M.simulate(se, g, cat).total_cost - 1)
+    overhead_model = float(plan.trace.total_cost / M.simulate(se, g, cat_full).total_cost - 1)
 
     # ---- measured overhead: the store-everything schedule (no budget, no
     # recompute, same kernels and variants' defaults) timed the same way
@@ -522,7 +528,7 @@ def ours_arm(args):
     if not args.no_overhead_run:
         del graph
         rt_se = Runtime(net, device=dev)
-        plan_se = rt_se.plan(se, g, cat)
+        plan_se = rt_se.plan(se, g, cat_full)
         xs, ys = batch()
         rt_se.set_batch(xs, ys)
         del xs, ys
@@ -560,7 +566,7 @@ def ours_arm(args):
                                    + (", conv backward split" if net.split else ""),
                        "model": args.arch, "global_batch": world * args.batch, "per_gpu_batch": args.batch,
                        "image": args.image, "budget_bytes": budget, "parallelism": f"dp{world}",
-                       "cuda_graph": use_graph,
+                       "cuda_graph": use_graph, "ablation": args.ablation or "all",
                        "l2": "inputs larger than L2 (activations ~26 GB per step); no explicit flush"},
             "memory": {"ledger_peak_bytes": plan.ledger_peak, "ilp_bound_bytes": plan.bound_peak,
                        "physical_peak_bytes": g.params_bytes + plan.arena_bytes,
@@ -568,7 +574,7 @@ def ours_arm(args):
                        **device_mem,
                        "within_bound": g.params_bytes + plan.arena_bytes <= (plan.bound_peak or 0),
                        "device_within_bound": device_mem["runtime_peak_bytes"] <= (plan.bound_peak or 0),
-                       "store_everything_ledger_peak_bytes": M.simulate(se, g, cat).peak_memory},
+                       "store_everything_ledger_peak_bytes": M.simulate(se, g, cat_full).peak_memory},
             "overhead": {"modeled_pct": round(100 * overhead_model, 2), "recomputes": n_rec,
                          "measured_pct": None if se_ms is None else round(100 * (ms / se_ms - 1), 2),
                          "unconstrained_ms_per_step": None if se_ms is None else round(se_ms, 3),

@@ -790,23 +790,54 @@ int monet_conv_fwd_w16(int variant, const monet_conv_desc* d, const float* x, co
 static long long conv_rows(const monet_conv_desc* d) { return (long long)d->n * d->p * d->q; }
 static long long stat_tiles(long long rows) { return (rows + 127) / 128; }
 
+// one 128-row tile per block: thread t takes channel quad t % (C/4) (BnLayout) and every rpi-th
+// row, four rows in flight; sums around the tile's first row (a common pivot), combined in smem
 __global__ void tile_stats_kernel(const float* __restrict__ y, long long M, int N, float* stats) {
+  const BnLayout L = bn_layout(N);
   const long long r0 = (long long)blockIdx.x * 128;
   const int cnt = (int)min(128LL, M - r0);
-  for (int c = 4 * threadIdx.x; c < N; c += 4 * blockDim.x) {
-    const float4 piv = *reinterpret_cast<const float4*>(y + r0 * N + c);
+  const int rsub = threadIdx.x / L.tpr, qb = threadIdx.x % L.tpr;
+  __shared__ float red[2][kEwThreads * 4];
+  for (int qi = 0; qi < L.qpt; ++qi) {
+    const int q = qb + qi * L.tpr;
     float s1[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int r = 0; r < cnt; ++r) {
-      const float4 v = *reinterpret_cast<const float4*>(y + (r0 + r) * N + c);
-      const float d0 = v.x - piv.x, d1 = v.y - piv.y, d2 = v.z - piv.z, d3 = v.w - piv.w;
-      s1[0] += d0; s1[1] += d1; s1[2] += d2; s1[3] += d3;
-      s2[0] += d0 * d0; s2[1] += d1 * d1; s2[2] += d2 * d2; s2[3] += d3 * d3;
+    if (rsub < L.rpi && q < N / 4) {
+      const float4 piv = *reinterpret_cast<const float4*>(y + r0 * N + 4 * q);
+      auto acc = [&](const float4& v) {
+        const float d0 = v.x - piv.x, d1 = v.y - piv.y, d2 = v.z - piv.z, d3 = v.w - piv.w;
+        s1[0] += d0; s1[1] += d1; s1[2] += d2; s1[3] += d3;
+        s2[0] += d0 * d0; s2[1] += d1 * d1; s2[2] += d2 * d2; s2[3] += d3 * d3;
+      };
+      int r = rsub;
+      for (; r + 3 * L.rpi < cnt; r += 4 * L.rpi) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = *reinterpret_cast<const float4*>(y + (r0 + r + u * L.rpi) * N + 4 * q);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc(v[u]);
+      }
+      for (; r < cnt; r += L.rpi) acc(*reinterpret_cast<const float4*>(y + (r0 + r) * N + 4 * q));
     }
-    const float p[4] = {piv.x, piv.y, piv.z, piv.w};
+#pragma unroll
     for (int j = 0; j < 4; ++j) {
-      stats[(long long)(blockIdx.x * 2) * N + c + j] = p[j] + s1[j] / cnt;
-      stats[(long long)(blockIdx.x * 2 + 1) * N + c + j] = fmaxf(s2[j] - s1[j] * s1[j] / cnt, 0.f);
+      red[0][threadIdx.x * 4 + j] = s1[j];
+      red[1][threadIdx.x * 4 + j] = s2[j];
     }
+    __syncthreads();
+    if (rsub == 0 && q < N / 4) {
+      const float4 piv = *reinterpret_cast<const float4*>(y + r0 * N + 4 * q);
+      const float pv[4] = {piv.x, piv.y, piv.z, piv.w};
+      for (int j = 0; j < 4; ++j) {
+        float a1 = 0.f, a2 = 0.f;
+        for (int k = 0; k < L.rpi; ++k) {
+          a1 += red[0][(k * L.tpr + qb) * 4 + j];
+          a2 += red[1][(k * L.tpr + qb) * 4 + j];
+        }
+        stats[(long long)(blockIdx.x * 2) * N + 4 * q + j] = pv[j] + a1 / cnt;
+        stats[(long long)(blockIdx.x * 2 + 1) * N + 4 * q + j] = fmaxf(a2 - a1 * a1 / cnt, 0.f);
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -895,7 +926,7 @@ int monet_conv_fwd_w16_stats(int variant, const monet_conv_desc* d, const float*
                     : conv_fwd_impl(variant, d, x, w, w_hi, w_lo, y, ws, ws_bytes, stream, st, &fused);
   if (e) return e;
   if (!fused)  // split-K, chunked chains or the fp32-weight path: one pass over y
-    tile_stats_kernel<<<(int)stat_tiles(conv_rows(d)), 256, 0, S(stream)>>>(y, conv_rows(d), d->k, st);
+    tile_stats_kernel<<<(int)stat_tiles(conv_rows(d)), kEwThreads, 0, S(stream)>>>(y, conv_rows(d), d->k, st);
   return last_error();
 }
 

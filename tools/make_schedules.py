@@ -26,7 +26,7 @@ def digest(doc):
     return hashlib.sha256(json.dumps(doc, sort_keys=True).encode()).hexdigest()[:16]
 
 
-def main(jobs, exact_time_s=None, exchange=False, lp=False, mip_time_s=None):
+def main(jobs, exact_time_s=None, exchange=False, lp=False, mip_time_s=None, ablation=None):
     OUT.mkdir(exist_ok=True)
     for arch, batch, img, gib, fuse, split in jobs:
         net = build_network(arch, batch, parse_image(img), num_classes=default_classes(arch), fuse=fuse, split=split)
@@ -40,6 +40,8 @@ def main(jobs, exact_time_s=None, exchange=False, lp=False, mip_time_s=None):
                 print("planning with measured catalog", measured.name)
         g = M.load_graph(gdoc)
         cat = M.load_catalog(cdoc, g)
+        if ablation:  # plan with one ablation family of the catalog (costmodel.py:220-252)
+            cat = M.apply_ablation(cat, g, ablation)
         budget = int(gib * (1 << 30))
         t = time.time()
         sched, info = plan_schedule(g, cat, budget, kinds=net.storable_kinds(), exact_time_s=exact_time_s,
@@ -48,10 +50,10 @@ def main(jobs, exact_time_s=None, exchange=False, lp=False, mip_time_s=None):
         if sched is None:
             print(arch, batch, img, gib, "no feasible schedule", info)
             continue
-        doc = {"arch": arch, "batch": batch, "image": img, "budget_bytes": budget,
+        doc = {"arch": arch, "batch": batch, "image": img, "budget_bytes": budget, "ablation": ablation or "all",
                "graph_digest": digest(gdoc), "catalog_digest": digest(cdoc), "planner": info,
                "plan_seconds": round(dt, 1), "schedule": M.schedule_to_doc(sched)}
-        path = OUT / f"{arch}_b{batch}_{img}_{gib:g}gib.json"
+        path = OUT / f"{arch}_b{batch}_{img}_{gib:g}gib{'_abl-' + ablation if ablation else ''}.json"
         path.write_text(json.dumps(doc, indent=1, sort_keys=True) + "\n")
         print(path.name, info, f"{dt:.1f}s")
 
@@ -71,6 +73,8 @@ if __name__ == "__main__":
     ap.add_argument("--split", action="store_true", help="conv backward split into dgrad / wgrad nodes")
     ap.add_argument("--lp", action="store_true", help="seed the planner with the ILP's LP relaxation (HiGHS)")
     ap.add_argument("--mip", type=float, default=None, help="seconds of HiGHS MIP search for a dual bound")
+    ap.add_argument("--ablation", default=None, choices=["none", "conv", "out", "int", "all"],
+                    help="plan with apply_ablation(catalog, mode); file suffix _abl-<mode>")
     a = ap.parse_args()
     main([(a.arch, a.batch, a.image, float(b), a.fused, a.split) for b in a.budgets.split(",")], a.exact,
-         a.exchange, a.lp, a.mip)
+         a.exchange, a.lp, a.mip, a.ablation)
