@@ -335,9 +335,12 @@ int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_b
     static const int mask = getenv("MONET_TMA_MASK") ? atoi(getenv("MONET_TMA_MASK")) : 3;
     p.a.seg = p.a.rows_box;
     p.b.seg = p.wv_q ? p.g.S * p.g.C : p.b.rows_box;
-    // MONET_CHUNK (debug): MMA stages (64 k each) per TMEM accumulation chain
-    static const int chunk = getenv("MONET_CHUNK") ? atoi(getenv("MONET_CHUNK")) : 16;
-    p.chunk_stages = chunk > 0 ? chunk : 16;
+    // MMA stages (64 k each) per TMEM accumulation chain before a flush to fp32 memory:
+    // 36 (K = 2304) keeps ResNet-50's 3x3 convs up to layer 3 in one chain (so their BN
+    // statistics come from the epilogue) at 6-9e-6 relative error (tools/chunk_accuracy.py;
+    // 16 stages: 5.7e-6, 72: 1.8e-5).  MONET_CHUNK (debug) overrides it.
+    static const int chunk = getenv("MONET_CHUNK") ? atoi(getenv("MONET_CHUNK")) : 36;
+    p.chunk_stages = chunk > 0 ? chunk : 36;
     p.a.tma = (mask & 1) ? make_tma(p, p.a, &p.tma_a) : 0;
     p.b.tma = (mask & 2) ? make_tma(p, p.b, &p.tma_b) : 0;
     // the tap views' layouts exist only as tensor maps: no cp.async fallback
