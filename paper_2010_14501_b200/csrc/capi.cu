@@ -378,8 +378,11 @@ int launch_gemm(GemmParams p, int variant, int accumulate, void* ws, size_t ws_b
     }
   }
   // BN statistics from the epilogue: only where every output element is final in one TMEM
-  // chain (no split-K, no chunk flushes) and the TMA-store epilogue runs
-  if (p.stats && !(p.c_tma && p.epi == EPI_STORE && p.splits == 1 && (p.kb_per_split + 1) / 2 <= p.chunk_stages))
+  // chain (no split-K, no chunk flushes), the TMA-store epilogue runs, and the reduction is long
+  // enough (K >= 512) to hide the column walk behind the MMAs -- output-heavy short-K convs
+  // (1x1 64 -> 256: +300 us in the epilogue vs ~90 us for one pass over y) take the pass instead
+  if (p.stats && !(p.c_tma && p.epi == EPI_STORE && p.splits == 1 && p.Kd >= 512 &&
+                   (p.kb_per_split + 1) / 2 <= p.chunk_stages))
     p.stats = nullptr;
   if (p.stats_done) *p.stats_done = p.stats != nullptr;
   const int tiles = p.m_tiles * p.n_tiles * p.splits;
@@ -795,52 +798,58 @@ static long long stat_tiles(long long rows) { return (rows + 127) / 128; }
 
 // one 128-row tile per block: thread t takes channel quad t % (C/4) (BnLayout) and every rpi-th
 // row, four rows in flight; sums around the tile's first row (a common pivot), combined in smem
+// 128-row tiles, a grid-stride loop of blocks over them: thread t takes channel quad t % (C/4)
+// (BnLayout) and every rpi-th row, four rows in flight; sums around the tile's first row (a
+// common pivot), combined in smem
 __global__ void tile_stats_kernel(const float* __restrict__ y, long long M, int N, float* stats) {
   const BnLayout L = bn_layout(N);
-  const long long r0 = (long long)blockIdx.x * 128;
-  const int cnt = (int)min(128LL, M - r0);
+  const long long T = (M + 127) / 128;
   const int rsub = threadIdx.x / L.tpr, qb = threadIdx.x % L.tpr;
   __shared__ float red[2][kEwThreads * 4];
-  for (int qi = 0; qi < L.qpt; ++qi) {
-    const int q = qb + qi * L.tpr;
-    float s1[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
-    if (rsub < L.rpi && q < N / 4) {
-      const float4 piv = *reinterpret_cast<const float4*>(y + r0 * N + 4 * q);
-      auto acc = [&](const float4& v) {
-        const float d0 = v.x - piv.x, d1 = v.y - piv.y, d2 = v.z - piv.z, d3 = v.w - piv.w;
-        s1[0] += d0; s1[1] += d1; s1[2] += d2; s1[3] += d3;
-        s2[0] += d0 * d0; s2[1] += d1 * d1; s2[2] += d2 * d2; s2[3] += d3 * d3;
-      };
-      int r = rsub;
-      for (; r + 3 * L.rpi < cnt; r += 4 * L.rpi) {
-        float4 v[4];
+  for (long long tile = blockIdx.x; tile < T; tile += gridDim.x) {
+    const long long r0 = tile * 128;
+    const int cnt = (int)min(128LL, M - r0);
+    for (int qi = 0; qi < L.qpt; ++qi) {
+      const int q = qb + qi * L.tpr;
+      float s1[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
+      float4 piv = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (q < N / 4) piv = *reinterpret_cast<const float4*>(y + r0 * N + 4 * q);
+      if (rsub < L.rpi && q < N / 4) {
+        auto acc = [&](const float4& v) {
+          const float d0 = v.x - piv.x, d1 = v.y - piv.y, d2 = v.z - piv.z, d3 = v.w - piv.w;
+          s1[0] += d0; s1[1] += d1; s1[2] += d2; s1[3] += d3;
+          s2[0] += d0 * d0; s2[1] += d1 * d1; s2[2] += d2 * d2; s2[3] += d3 * d3;
+        };
+        int r = rsub;
+        for (; r + 7 * L.rpi < cnt; r += 8 * L.rpi) {
+          float4 v[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = *reinterpret_cast<const float4*>(y + (r0 + r + u * L.rpi) * N + 4 * q);
+          for (int u = 0; u < 8; ++u) v[u] = *reinterpret_cast<const float4*>(y + (r0 + r + u * L.rpi) * N + 4 * q);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) acc(v[u]);
-      }
-      for (; r < cnt; r += L.rpi) acc(*reinterpret_cast<const float4*>(y + (r0 + r) * N + 4 * q));
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      red[0][threadIdx.x * 4 + j] = s1[j];
-      red[1][threadIdx.x * 4 + j] = s2[j];
-    }
-    __syncthreads();
-    if (rsub == 0 && q < N / 4) {
-      const float4 piv = *reinterpret_cast<const float4*>(y + r0 * N + 4 * q);
-      const float pv[4] = {piv.x, piv.y, piv.z, piv.w};
-      for (int j = 0; j < 4; ++j) {
-        float a1 = 0.f, a2 = 0.f;
-        for (int k = 0; k < L.rpi; ++k) {
-          a1 += red[0][(k * L.tpr + qb) * 4 + j];
-          a2 += red[1][(k * L.tpr + qb) * 4 + j];
+          for (int u = 0; u < 8; ++u) acc(v[u]);
         }
-        stats[(long long)(blockIdx.x * 2) * N + 4 * q + j] = pv[j] + a1 / cnt;
-        stats[(long long)(blockIdx.x * 2 + 1) * N + 4 * q + j] = fmaxf(a2 - a1 * a1 / cnt, 0.f);
+        for (; r < cnt; r += L.rpi) acc(*reinterpret_cast<const float4*>(y + (r0 + r) * N + 4 * q));
       }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        red[0][threadIdx.x * 4 + j] = s1[j];
+        red[1][threadIdx.x * 4 + j] = s2[j];
+      }
+      __syncthreads();
+      if (rsub == 0 && q < N / 4) {
+        const float pv[4] = {piv.x, piv.y, piv.z, piv.w};
+        for (int j = 0; j < 4; ++j) {
+          float a1 = 0.f, a2 = 0.f;
+          for (int k = 0; k < L.rpi; ++k) {
+            a1 += red[0][(k * L.tpr + qb) * 4 + j];
+            a2 += red[1][(k * L.tpr + qb) * 4 + j];
+          }
+          stats[(tile * 2) * N + 4 * q + j] = pv[j] + a1 / cnt;
+          stats[(tile * 2 + 1) * N + 4 * q + j] = fmaxf(a2 - a1 * a1 / cnt, 0.f);
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
 }
 
@@ -929,7 +938,8 @@ int monet_conv_fwd_w16_stats(int variant, const monet_conv_desc* d, const float*
                     : conv_fwd_impl(variant, d, x, w, w_hi, w_lo, y, ws, ws_bytes, stream, st, &fused);
   if (e) return e;
   if (!fused)  // split-K, chunked chains or the fp32-weight path: one pass over y
-    tile_stats_kernel<<<(int)stat_tiles(conv_rows(d)), kEwThreads, 0, S(stream)>>>(y, conv_rows(d), d->k, st);
+    tile_stats_kernel<<<(int)std::min<long long>(stat_tiles(conv_rows(d)), 8LL * kNumSMs), kEwThreads, 0, S(stream)>>>(
+        y, conv_rows(d), d->k, st);
   return last_error();
 }
 

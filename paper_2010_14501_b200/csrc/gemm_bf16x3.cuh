@@ -458,47 +458,37 @@ struct Loader {
     cp_async_mbar_arrive(bar);
   }
 };
-// BN statistics of a 128-row output tile from the epilogue (the conv -> BN forward):
-// each warp reduces its 32 rows per column around a pivot (its first row) -- a transposed
-// butterfly leaves column l's sums on lane l --, the four warps' (mean, M2) meet in smem and
-// warp 0 merges them in order (Chan) into stats[mt][0|1][n].  One named barrier pair per
-// 32-column chunk among the four epilogue warps.  Deterministic.
-MONET_DEV void tile_stats(const GemmParams& p, const float (&v)[32], float* sm, int row0, int quarter, int lane,
-                          int n0, int mt) {
+// BN statistics of a 128-row output tile from the epilogue (the conv -> BN forward): after the
+// warp has staged its 32x32 block in smem (SWIZZLE_128B, row r = lane r), lane l walks column l
+// down the 32 rows -- conflict-free, a handful of registers -- summing around the block's first
+// row (a pivot); the four warps' (mean, M2) meet in smem and warp 0 merges them in order (Chan)
+// into stats[mt][0|1][n].  One named-barrier pair per 32-column chunk among the four epilogue
+// warps.  Deterministic.
+MONET_DEV void tile_stats(const GemmParams& p, const uint8_t* blk, float* sm, int row0, int quarter, int lane, int n0,
+                          int mt) {
   const int rows_here = min(32, p.M - (row0 + quarter * 32));
-  const bool ok = lane < rows_here;
-  float d[32], q[32], pv[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const float piv = __shfl_sync(0xffffffffu, v[j], 0);
-    const float t = ok ? v[j] - piv : 0.f;
-    pv[j] = piv;
-    d[j] = t;
-    q[j] = t * t;
-  }
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    const bool up = (lane & o) != 0;
-#pragma unroll
-    for (int i = 0; i < o; ++i) {
-      const float s1 = up ? d[i] : d[i + o], k1 = up ? d[i + o] : d[i];
-      const float s2 = up ? q[i] : q[i + o], k2 = up ? q[i + o] : q[i];
-      d[i] = k1 + __shfl_xor_sync(0xffffffffu, s1, o);
-      q[i] = k2 + __shfl_xor_sync(0xffffffffu, s2, o);
-      pv[i] = up ? pv[i + o] : pv[i];
-    }
-  }
+  const int cc = lane >> 2, cw = (lane & 3) * 4;  // 16-B chunk and byte offset of column `lane`
   float mean = 0.f, m2 = 0.f;
   if (rows_here > 0) {
+    const float piv = *reinterpret_cast<const float*>(blk + ((cc ^ 0) << 4) + cw);
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll 8
+    for (int r = 1; r < 32; ++r) {
+      if (r < rows_here) {
+        const float d = *reinterpret_cast<const float*>(blk + r * 128 + ((cc ^ (r & 7)) << 4) + cw) - piv;
+        s1 += d;
+        s2 += d * d;
+      }
+    }
     const float inv = 1.f / (float)rows_here;
-    mean = pv[0] + d[0] * inv;
-    m2 = fmaxf(q[0] - d[0] * d[0] * inv, 0.f);
+    mean = piv + s1 * inv;
+    m2 = fmaxf(s2 - s1 * s1 * inv, 0.f);
   }
   sm[(quarter * 2) * 32 + lane] = mean;
   sm[(quarter * 2 + 1) * 32 + lane] = m2;
   asm volatile("bar.sync 1, 128;" ::: "memory");
   if (quarter == 0 && n0 + lane < p.N) {
-    float n = 0.f, mu = 0.f, s = 0.f;
+    float n = 0.f, mu = 0.f, sq = 0.f;
 #pragma unroll
     for (int qq = 0; qq < 4; ++qq) {
       const int c = min(32, p.M - (row0 + qq * 32));
@@ -506,11 +496,11 @@ MONET_DEV void tile_stats(const GemmParams& p, const float (&v)[32], float* sm, 
       const float mb = sm[(qq * 2) * 32 + lane], sb = sm[(qq * 2 + 1) * 32 + lane];
       const float nn = n + (float)c, delta = mb - mu;
       mu += delta * ((float)c / nn);
-      s += sb + delta * delta * (n * (float)c / nn);
+      sq += sb + delta * delta * (n * (float)c / nn);
       n = nn;
     }
     p.stats[(long long)(mt * 2) * p.N + n0 + lane] = mu;
-    p.stats[(long long)(mt * 2 + 1) * p.N + n0 + lane] = s;
+    p.stats[(long long)(mt * 2 + 1) * p.N + n0 + lane] = sq;
   }
   asm volatile("bar.sync 1, 128;" ::: "memory");
 }
@@ -916,7 +906,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] += (n0 + j < p.N) ? __ldg(p.bias + n0 + j) : 0.f;
               }
-              if (p.stats) tile_stats(p, v, stat_sm, mt * kTileM, quarter, lane, n0, mt);
               // the warp's two staging blocks alternate per store (not per chunk: skipped chunks
               // would break the pairing); wait until the store two back has read its block
               uint8_t* blk = epi_st + (quarter * 2 + (epi_stores & 1)) * 4096;
@@ -930,6 +919,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
               fence_proxy_async_smem();
               __syncwarp();
               if (lane == 0 && !(dm & 8)) tma_store_3d(&p.tma_c, smem_u32(blk), n0, mrow, zs, add_old);
+              if (p.stats) tile_stats(p, blk, stat_sm, mt * kTileM, quarter, lane, n0, mt);
             }
             tc_fence_before();
             arrive_leader(&tempty[acc]);
