@@ -525,7 +525,9 @@ MONET_DEV void tile_stats(const GemmParams& p, const uint8_t* blk, float* sm, in
 //
 // NB (N-tile width): 128, or 64 for problems with N <= 64 (64-channel convs):
 // half the B rows and half the MMA width per stage, same A work.
-template <int AM, int BMODE, bool PR, int NB>
+// ST: the epilogue also leaves BN statistics (p.stats) -- its own instantiation, so the plain
+// kernels carry none of that code (register allocation of the epilogue stays unchanged)
+template <int AM, int BMODE, bool PR, int NB, bool ST = false>
 __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_constant__ GemmParams p) {
   static_assert(NB == BN || (NB == 64 && !PR), "tile widths: 128 (1 CTA or pair), 64 (1 CTA)");
   constexpr bool a_mn = mode_is_mn(AM), b_mn = mode_is_mn(BMODE);
@@ -626,7 +628,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
       // pre-split B: one thread streams each 64-deep stage's bf16 hi / lo boxes straight
       // into the B stage tiles (K-major: one box per plane; MN-major: 64-channel chunks x
       // two 32-deep k halves per plane)
-      if (is_b && (sub & 31) == 0) {  // two issuers (lane 0 of each B loader warp), alternating stages
+      // two issuers (lane 0 of each B loader warp) taking alternate stages; one for the sub-pixel
+      // phase GEMMs of a strided dgrad (with two, those came out wrong and non-deterministic once
+      // CTAs ran several tiles -- tools/dgrad_phase_check.py; cause not isolated)
+      const int niss = ((dm & 16) || p.ph.on) ? 1 : 2;
+      if (is_b && (sub & 31) == 0 && (sub >> 5) < niss) {
         const int iss = sub >> 5;
         int sitem = 0;
         for (int tile = unit0; tile < n_tiles_total; tile += n_units) {
@@ -634,7 +640,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
           tile_range(p, tile, mt, nt, kb0, nst);
           const int n0 = nt * p.n_pitch;
           for (int s = 0; s < nst; ++s, ++sitem) {
-            if ((sitem & 1) != iss) continue;
+            if ((sitem % niss) != iss) continue;
             const int sb = sitem % kBStages;
             TWAIT(0, mbar_wait(&b_empty[sb], ((sitem / kBStages) & 1) ^ 1));
             const uint32_t hi = smem_u32(bst + sb * kStageBytes), lo = hi + kBTile;
@@ -919,7 +925,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_bf16x3_kernel(const __grid_c
               fence_proxy_async_smem();
               __syncwarp();
               if (lane == 0 && !(dm & 8)) tma_store_3d(&p.tma_c, smem_u32(blk), n0, mrow, zs, add_old);
-              if (p.stats) tile_stats(p, blk, stat_sm, mt * kTileM, quarter, lane, n0, mt);
+              if constexpr (ST) tile_stats(p, blk, stat_sm, mt * kTileM, quarter, lane, n0, mt);
             }
             tc_fence_before();
             arrive_leader(&tempty[acc]);

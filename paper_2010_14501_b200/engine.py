@@ -23,6 +23,7 @@ ledger step launches the sm_100a kernel of the chosen catalog variant.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import torch
@@ -162,7 +163,8 @@ class Runtime:
             self.w16_lo = self.w16_hi + nb // 2
             for nid, _, dst, _ in segs:
                 self.w16[nid] = (self.w16_hi + 2 * dst, self.w16_lo + 2 * dst)
-        self.stats_convs = self.net.stats_convs()
+        # MONET_NO_CONV_STATS=1 (measurement switch): BNs compute their own statistics
+        self.stats_convs = {} if os.environ.get("MONET_NO_CONV_STATS") else self.net.stats_convs()
         self.stats_bns = {bn: conv for conv, bn in self.stats_convs.items()}
         self.conv_stats_ptr = self.fixed.data_ptr() + self.region["conv_stats"][0]
         stats = f32("bn_stats")

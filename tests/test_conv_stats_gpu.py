@@ -24,6 +24,8 @@ CASES = [
     (3, 9, 11, 96, 200, 1, 1, 1, 0, 0.0),       # partial m- and n-tiles
     (4, 14, 14, 256, 128, 3, 3, 1, 1, 0.0),     # K = 2304: chunked chains -> pass over y
     (8, 28, 28, 64, 256, 1, 1, 1, 0, 1000.0),   # |mean| / std ~ 1000
+    (184, 56, 56, 64, 64, 3, 3, 1, 1, 0.0),     # ResNet-50 layer 1 at b184: 577k rows, 4508 tiles
+    (184, 56, 56, 64, 256, 1, 1, 1, 0, 0.0),
 ]
 
 
