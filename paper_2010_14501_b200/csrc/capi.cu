@@ -1195,20 +1195,39 @@ static int dw_blocks(const monet_conv_desc* d) {
 }
 // shared-memory tiled kernels (csrc/dwconv.cuh): channel slabs of 16, staged window <= 200 KB
 constexpr size_t kDwSmemMax = 200 * 1024;
-static size_t dw_fwd_smem(const monet_conv_desc* d) {
-  const int nr = (kDwRows - 1) * d->stride_h + d->r, nc = (d->q - 1) * d->stride_w + d->s;
+static size_t dw_fwd_smem(const monet_conv_desc* d, int rows = kDwRows) {
+  const int nr = (rows - 1) * d->stride_h + d->r, nc = (d->q - 1) * d->stride_w + d->s;
   return (size_t)nr * nc * kDwSlab * sizeof(float);
 }
-static size_t dw_dgrad_smem(const monet_conv_desc* d) {
-  const int nr = (kDwRows + d->r - 1) / d->stride_h + 2, nc = (d->w + d->s - 1) / d->stride_w + 2;
+static size_t dw_dgrad_smem(const monet_conv_desc* d, int rows = kDwRows) {
+  const int nr = (rows + d->r - 1) / d->stride_h + 2, nc = (d->w + d->s - 1) / d->stride_w + 2;
   return (size_t)nr * nc * kDwSlab * sizeof(float);
 }
-static size_t dw_wgrad_smem(const monet_conv_desc* d) {  // staged window, or the 256-float4 final reduction
-  return std::max(dw_fwd_smem(d) + (size_t)kDwRows * d->q * kDwSlab * sizeof(float), (size_t)256 * sizeof(float4));
+static size_t dw_wgrad_band_bytes(const monet_conv_desc* d) {  // one staged band (odd x pitch)
+  const int nr = (kDwRows - 1) * d->stride_h + d->r, nc = ((d->q - 1) * d->stride_w + d->s) | 1;
+  return (size_t)(nr * nc + kDwRows * d->q) * kDwSlab * sizeof(float);
+}
+// bands staged per barrier round by the 3x3 row walker (up to 32 KB of staging per round)
+static int dw_wgrad_kb(const monet_conv_desc* d) {
+  return (int)std::max<size_t>(1, std::min<size_t>(8, (32 << 10) / dw_wgrad_band_bytes(d)));
+}
+static size_t dw_wgrad_smem(const monet_conv_desc* d) {  // staged bands, or the final reduction
+  return std::max(dw_wgrad_band_bytes(d) * dw_wgrad_kb(d), (size_t)256 * 3 * sizeof(float4));
 }
 static bool dw_tiled(const monet_conv_desc* d) {
   return d->c % kDwSlab == 0 && dw_fwd_smem(d) <= kDwSmemMax && dw_dgrad_smem(d) <= kDwSmemMax &&
          dw_wgrad_smem(d) <= kDwSmemMax;
+}
+// output rows per fwd / dgrad CTA: about `pix` output pixels (whole images for the 7x7 and 14x14
+// layers, whose 4-row CTAs were launch- and halo-bound), at least kDwRows, with the staged window
+// under `cap` bytes so 5+ CTAs stay resident (measured per MobileNet-V2 shape: tools/dw_bench.py)
+static int dw_rows(const monet_conv_desc* d, bool trans) {
+  const int oh = trans ? d->h : d->p, ow = trans ? d->w : d->q;
+  const int pix = trans ? 1024 : 448;
+  const size_t cap = trans ? 40 << 10 : 32 << 10;
+  int rows = std::min(oh, std::max(kDwRows, (pix + ow - 1) / ow));
+  while (rows > kDwRows && (trans ? dw_dgrad_smem(d, rows) : dw_fwd_smem(d, rows)) > cap) --rows;
+  return std::max(1, std::min(oh, rows));
 }
 // 1 / 2: the 3x3 stride-1 / stride-2 specialisations; 0: runtime geometry
 static int dw_kind(const monet_conv_desc* d) {
@@ -1226,7 +1245,8 @@ void dw_launch(const monet_conv_desc* d, dim3 grid, size_t smem, const float* sr
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDwSmemMax);
     attr = true;
   }
-  auto run = [&](auto kern) { kern<<<grid, 256, smem, st>>>(src, w, out, geom(d), accumulate); };
+  const int rows = dw_rows(d, kTrans);
+  auto run = [&](auto kern) { kern<<<grid, 256, smem, st>>>(src, w, out, geom(d), accumulate, rows); };
   const int k = dw_kind(d);
   if (k == 1)
     run(dwconv_tile_kernel<kTrans, 1>);
@@ -1249,8 +1269,9 @@ size_t monet_dwconv_ws_bytes(const monet_conv_desc* d) {
 int monet_dwconv_fwd(const monet_conv_desc* d, const float* x, const float* w, float* y, void* stream) {
   if (int e = dw_check(d)) return e;
   if (dw_tiled(d)) {
-    dim3 grid((d->p + kDwRows - 1) / kDwRows, d->n, d->c / kDwSlab);
-    dw_launch<false>(d, grid, dw_fwd_smem(d), x, w, y, 0, S(stream));
+    const int rows = dw_rows(d, false);
+    dim3 grid((d->p + rows - 1) / rows, d->n, d->c / kDwSlab);
+    dw_launch<false>(d, grid, dw_fwd_smem(d, rows), x, w, y, 0, S(stream));
     return last_error();
   }
   const long long total = (long long)d->n * d->p * d->q * (d->c / 4);
@@ -1261,8 +1282,9 @@ int monet_dwconv_dgrad(const monet_conv_desc* d, const float* dy, const float* w
                        void* stream) {
   if (int e = dw_check(d)) return e;
   if (dw_tiled(d)) {
-    dim3 grid((d->h + kDwRows - 1) / kDwRows, d->n, d->c / kDwSlab);
-    dw_launch<true>(d, grid, dw_dgrad_smem(d), dy, w, dx, accumulate, S(stream));
+    const int rows = dw_rows(d, true);
+    dim3 grid((d->h + rows - 1) / rows, d->n, d->c / kDwSlab);
+    dw_launch<true>(d, grid, dw_dgrad_smem(d, rows), dy, w, dx, accumulate, S(stream));
     return last_error();
   }
   const long long total = (long long)d->n * d->h * d->w * (d->c / 4);
@@ -1284,15 +1306,23 @@ int monet_dwconv_wgrad(const monet_conv_desc* d, const float* x, const float* dy
     if (!attr) {
       for (auto kern : {dwconv_wgrad_tile_kernel<0>, dwconv_wgrad_tile_kernel<1>, dwconv_wgrad_tile_kernel<2>})
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDwSmemMax);
+      for (auto kern : {dwconv_wgrad_rows_kernel<1>, dwconv_wgrad_rows_kernel<2>})
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDwSmemMax);
       attr = true;
     }
-    auto run = [&](auto kern) { kern<<<grid, 256, dw_wgrad_smem(d), S(stream)>>>(x, dy, part, geom(d), nb); };
-    if (k == 1)
-      run(dwconv_wgrad_tile_kernel<1>);
+    const size_t smem = dw_wgrad_smem(d);
+    // row walker for rows >= 56 wide (it reads a third of the shared memory, which bounds those);
+    // the per-tap walker below that, where the band staging latency dominates (tools/dw_bench.py)
+    if (d->q < 56 && k == 1)
+      dwconv_wgrad_tile_kernel<1><<<grid, 256, smem, S(stream)>>>(x, dy, part, geom(d), nb);
+    else if (d->q < 56 && k == 2)
+      dwconv_wgrad_tile_kernel<2><<<grid, 256, smem, S(stream)>>>(x, dy, part, geom(d), nb);
+    else if (k == 1)
+      dwconv_wgrad_rows_kernel<1><<<grid, 256, smem, S(stream)>>>(x, dy, part, geom(d), nb, dw_wgrad_kb(d));
     else if (k == 2)
-      run(dwconv_wgrad_tile_kernel<2>);
+      dwconv_wgrad_rows_kernel<2><<<grid, 256, smem, S(stream)>>>(x, dy, part, geom(d), nb, dw_wgrad_kb(d));
     else
-      run(dwconv_wgrad_tile_kernel<0>);
+      dwconv_wgrad_tile_kernel<0><<<grid, 256, smem, S(stream)>>>(x, dy, part, geom(d), nb);
   } else {
     nb = dw_blocks(d);
     dwconv_wgrad_partial_kernel<<<nb, kEwThreads, 0, S(stream)>>>(x, dy, part, geom(d));

@@ -166,7 +166,7 @@ __global__ void dwconv_wgrad_final_kernel(const float* __restrict__ part, int nb
 namespace monet {
 
 // ---------------------------------------------------------------------------
-// Shared-memory tiled depthwise kernels.  A CTA owns kDwRows output rows of one
+// Shared-memory tiled depthwise kernels.  A CTA owns `rows` output rows of one
 // image and one kDwSlab-channel slab; the source rows it needs (input rows for
 // fwd / wgrad, dy rows for dgrad) are staged once into shared memory with zero
 // padding, so each source pixel crosses L2 -> SM about once instead of once per
@@ -196,7 +196,7 @@ MONET_DEV void dw_stage(float4* dst, int count, F load) {
 // kStride > 0: 3x3 taps and that stride at compile time (MobileNet-V2's layers); 0: runtime geometry
 template <bool kTrans, int kStride = 0>
 __global__ void __launch_bounds__(256) dwconv_tile_kernel(const float* __restrict__ src, const float* __restrict__ w,
-                                                          float* out, ConvGeom g, int accumulate) {
+                                                          float* out, ConvGeom g, int accumulate, int rows) {
   extern __shared__ float4 dw_smem[];
   if (kStride > 0) {
     g.sh = g.sw = kStride;
@@ -204,10 +204,10 @@ __global__ void __launch_bounds__(256) dwconv_tile_kernel(const float* __restric
   }
   const int OH = kTrans ? g.H : g.P, OW = kTrans ? g.W : g.Q;  // output extent
   const int SH = kTrans ? g.P : g.H, SW = kTrans ? g.Q : g.W;  // source extent
-  const int o0 = blockIdx.x * kDwRows;
+  const int o0 = blockIdx.x * rows;
   const int n = blockIdx.y;
   const int c0 = blockIdx.z * kDwSlab;
-  const int orows = min(kDwRows, OH - o0);
+  const int orows = min(rows, OH - o0);
   // staged source window
   int s_r0, s_nr, s_c0, s_nc;
   if (!kTrans) {  // output row o reads input rows o*sh - ph + r
@@ -358,6 +358,116 @@ __global__ void __launch_bounds__(256) dwconv_wgrad_tile_kernel(const float* __r
       t.w += v.w;
     }
     reinterpret_cast<float4*>(part + ((long long)blockIdx.x * taps + tap) * g.C + c0)[j] = t;
+  }
+}
+
+// wgrad for the 3x3 specialisations, persistent like dwconv_wgrad_tile_kernel (same grid, bands
+// and part[b][tap][c] layout): thread = (kernel row r, quad j) x pixel group; a group walks a run
+// of consecutive output columns of one band row and slides its three x taps along the staged row
+// (stride 1: one new x load per column; stride 2: two), so a staged pixel is read about twice per
+// kernel row instead of once per tap -- a third of the shared-memory reads of the per-tap walker,
+// which is what bounds it.  The staged x rows get an odd pixel pitch so the three kernel rows of
+// a quad fall on different banks.  Groups are combined in a fixed order at the end.
+template <int kStride>
+__global__ void __launch_bounds__(256) dwconv_wgrad_rows_kernel(const float* __restrict__ x,
+                                                                const float* __restrict__ dy, float* __restrict__ part,
+                                                                ConvGeom g, int nb, int kb) {
+  extern __shared__ float4 dw_smem[];
+  constexpr int kSlots = 12, kGroups = 256 / kSlots;  // 21 groups of (3 kernel rows x 4 quads)
+  const int c0 = blockIdx.y * kDwSlab;
+  const int bands_per_img = (g.P + kDwRows - 1) / kDwRows;
+  const int total_bands = g.N * bands_per_img;
+  const int slot = threadIdx.x % kSlots, grp = threadIdx.x / kSlots;
+  const int r = slot >> 2, j = slot & 3;
+  const int x_nc = (g.Q - 1) * kStride + 3, x_pitch = x_nc | 1;
+  const int x_band = ((kDwRows - 1) * kStride + 3) * x_pitch * 4, band_f4 = x_band + kDwRows * g.Q * 4;
+  // runs per band row: the split of Q that fills the groups with the shortest critical path
+  int nseg = 1, best = 1 << 30;
+  for (int ns = 1; ns <= g.Q; ++ns) {
+    const int len = (g.Q + ns - 1) / ns, nsr = (g.Q + len - 1) / len;
+    const int cost = ((kb * kDwRows * nsr + kGroups - 1) / kGroups) * (len + 2);
+    if (cost < best) {
+      best = cost;
+      nseg = nsr;
+    }
+  }
+  const int len = (g.Q + nseg - 1) / nseg;
+  float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, a2 = a0;
+  // rounds of kb bands (blockIdx.x + (round * kb + i) * nb): all kb stagings in flight per barrier
+  for (int band0 = blockIdx.x; band0 < total_bands; band0 += nb * kb) {
+    __syncthreads();  // previous round's readers are done
+    for (int i = 0; i < kb; ++i) {
+      const int band = band0 + i * nb;
+      if (band >= total_bands) break;
+      const int n = band / bands_per_img;
+      const int p0 = (band - n * bands_per_img) * kDwRows;
+      const int prow = min(kDwRows, g.P - p0);
+      const int x_r0 = p0 * kStride - g.ph, x_nr = (prow - 1) * kStride + 3;
+      float4* xs = dw_smem + i * band_f4;
+      dw_stage(xs, x_nr * x_pitch * 4, [&](int e) {
+        const int jj = e & 3, pc = e >> 2;
+        const int cc = pc % x_pitch, rr = pc / x_pitch;
+        const int hr = x_r0 + rr, wc = cc - g.pw;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if ((unsigned)hr < (unsigned)g.H && (unsigned)wc < (unsigned)g.W)
+          v = __ldg(reinterpret_cast<const float4*>(x + (((long long)n * g.H + hr) * g.W + wc) * g.C + c0) + jj);
+        return v;
+      });
+      dw_stage(xs + x_band, prow * g.Q * 4, [&](int e) {
+        const int jj = e & 3, pq = e >> 2;
+        const int q = pq % g.Q, pr = pq / g.Q;
+        return __ldg(reinterpret_cast<const float4*>(dy + (((long long)n * g.P + p0 + pr) * g.Q + q) * g.C + c0) +
+                     jj);
+      });
+    }
+    __syncthreads();
+    if (grp < kGroups) {
+      for (int it = grp; it < kb * kDwRows * nseg; it += kGroups) {
+        const int i = it / (kDwRows * nseg), rem = it - i * (kDwRows * nseg);
+        const int pr = rem / nseg, q0 = (rem - pr * nseg) * len, q1 = min(q0 + len, g.Q);
+        const int band = band0 + i * nb;
+        if (band >= total_bands || (band % bands_per_img) * kDwRows + pr >= g.P) continue;
+        const float4* xr = dw_smem + i * band_f4 + (pr * kStride + r) * x_pitch * 4 + j;
+        const float4* dr = dw_smem + i * band_f4 + x_band + pr * g.Q * 4 + j;
+        float4 u0 = xr[q0 * kStride * 4];
+        float4 u1 = kStride == 1 ? xr[(q0 + 1) * 4] : u0;
+        for (int q = q0; q < q1; ++q) {
+          const float4 d = dr[q * 4];
+          if (kStride != 1) u1 = xr[(q * kStride + 1) * 4];
+          const float4 u2 = xr[(q * kStride + 2) * 4];
+          fma4(a0, u0, d);
+          fma4(a1, u1, d);
+          fma4(a2, u2, d);
+          if (kStride == 1) {
+            u0 = u1;
+            u1 = u2;
+          } else {
+            u0 = u2;
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (grp < kGroups) {
+    float4* red = dw_smem + (grp * kSlots + slot) * 3;
+    red[0] = a0;
+    red[1] = a1;
+    red[2] = a2;
+  }
+  __syncthreads();
+  if (threadIdx.x < 36) {  // (tap, quad): fixed-order sum over the groups
+    const int tap = threadIdx.x >> 2, jj = threadIdx.x & 3;
+    const int sl = (tap / 3) * 4 + jj, s = tap % 3;
+    float4 t = dw_smem[sl * 3 + s];
+    for (int k = 1; k < kGroups; ++k) {
+      const float4 v = dw_smem[(k * kSlots + sl) * 3 + s];
+      t.x += v.x;
+      t.y += v.y;
+      t.z += v.z;
+      t.w += v.w;
+    }
+    reinterpret_cast<float4*>(part + ((long long)blockIdx.x * 9 + tap) * g.C + c0)[jj] = t;
   }
 }
 

@@ -399,7 +399,8 @@ def test_dropout_mask_matches_oracle(cuda):
 
 @pytest.mark.parametrize("case", [(2, 14, 14, 32, 3, 1, 1), (3, 15, 13, 96, 3, 2, 1), (2, 8, 8, 8, 3, 2, 1),
                                   (1, 33, 30, 144, 3, 1, 1), (4, 4, 4, 96, 3, 1, 1), (4, 2, 2, 160, 3, 1, 1),
-                                  (2, 7, 5, 48, 3, 2, 1)])
+                                  (2, 7, 5, 48, 3, 2, 1), (2, 56, 56, 32, 3, 1, 1), (2, 112, 112, 16, 3, 2, 1),
+                                  (3, 28, 28, 48, 3, 1, 1), (2, 61, 58, 32, 3, 1, 1), (1, 120, 114, 16, 3, 2, 1)])
 def test_dwconv_passes(cuda, case):
     n, h, w, c, r, stride, pad = case
     g = torch.Generator().manual_seed(7)
