@@ -1306,21 +1306,32 @@ int monet_dwconv_wgrad(const monet_conv_desc* d, const float* x, const float* dy
     if (!attr) {
       for (auto kern : {dwconv_wgrad_tile_kernel<0>, dwconv_wgrad_tile_kernel<1>, dwconv_wgrad_tile_kernel<2>})
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDwSmemMax);
-      for (auto kern : {dwconv_wgrad_rows_kernel<1>, dwconv_wgrad_rows_kernel<2>})
+      for (auto kern : {dwconv_wgrad_rows_kernel<1, false>, dwconv_wgrad_rows_kernel<2, false>,
+                        dwconv_wgrad_rows_kernel<1, true>, dwconv_wgrad_rows_kernel<2, true>})
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDwSmemMax);
       attr = true;
     }
     const size_t smem = dw_wgrad_smem(d);
     // row walker for rows >= 56 wide (it reads a third of the shared memory, which bounds those);
     // the per-tap walker below that, where the band staging latency dominates (tools/dw_bench.py)
-    if (d->q < 56 && k == 1)
+    // per row width (tools/dw_bench.py, MobileNet-V2 b272): input rows <= 14 wide -> row walker staging
+    // kb bands per barrier at 4 CTAs / SM (latency-bound: ~60 bands per walker); outputs up to 55 wide
+    // -> the per-tap walker; >= 56 -> row walker, one band per round (shared-memory-read bound)
+    const bool narrow = d->q * d->stride_w <= 14;  // 7x7 / 14x14 outputs of stride 1, 7x7 of stride 2
+    const int kb = narrow ? dw_wgrad_kb(d) : 1;
+    const auto args = [&](auto kern) { kern<<<grid, 256, smem, S(stream)>>>(x, dy, part, geom(d), nb, kb); };
+    if (k == 1 && narrow)
+      args(dwconv_wgrad_rows_kernel<1, true>);
+    else if (k == 2 && narrow)
+      args(dwconv_wgrad_rows_kernel<2, true>);
+    else if (k == 1 && d->q < 56)
       dwconv_wgrad_tile_kernel<1><<<grid, 256, smem, S(stream)>>>(x, dy, part, geom(d), nb);
-    else if (d->q < 56 && k == 2)
+    else if (k == 2 && d->q < 56)
       dwconv_wgrad_tile_kernel<2><<<grid, 256, smem, S(stream)>>>(x, dy, part, geom(d), nb);
     else if (k == 1)
-      dwconv_wgrad_rows_kernel<1><<<grid, 256, smem, S(stream)>>>(x, dy, part, geom(d), nb, dw_wgrad_kb(d));
+      args(dwconv_wgrad_rows_kernel<1, false>);
     else if (k == 2)
-      dwconv_wgrad_rows_kernel<2><<<grid, 256, smem, S(stream)>>>(x, dy, part, geom(d), nb, dw_wgrad_kb(d));
+      args(dwconv_wgrad_rows_kernel<2, false>);
     else
       dwconv_wgrad_tile_kernel<0><<<grid, 256, smem, S(stream)>>>(x, dy, part, geom(d), nb);
   } else {

@@ -368,12 +368,13 @@ __global__ void __launch_bounds__(256) dwconv_wgrad_tile_kernel(const float* __r
 // kernel row instead of once per tap -- a third of the shared-memory reads of the per-tap walker,
 // which is what bounds it.  The staged x rows get an odd pixel pitch so the three kernel rows of
 // a quad fall on different banks.  Groups are combined in a fixed order at the end.
-template <int kStride>
-__global__ void __launch_bounds__(256) dwconv_wgrad_rows_kernel(const float* __restrict__ x,
+template <int kStride, bool kBatch>
+__global__ void __launch_bounds__(256, kBatch ? 4 : 3) dwconv_wgrad_rows_kernel(const float* __restrict__ x,
                                                                 const float* __restrict__ dy, float* __restrict__ part,
                                                                 ConvGeom g, int nb, int kb) {
   extern __shared__ float4 dw_smem[];
   constexpr int kSlots = 12, kGroups = 256 / kSlots;  // 21 groups of (3 kernel rows x 4 quads)
+  if constexpr (!kBatch) kb = 1;                       // the one-band-per-round variant
   const int c0 = blockIdx.y * kDwSlab;
   const int bands_per_img = (g.P + kDwRows - 1) / kDwRows;
   const int total_bands = g.N * bands_per_img;
@@ -396,15 +397,36 @@ __global__ void __launch_bounds__(256) dwconv_wgrad_rows_kernel(const float* __r
   // rounds of kb bands (blockIdx.x + (round * kb + i) * nb): all kb stagings in flight per barrier
   for (int band0 = blockIdx.x; band0 < total_bands; band0 += nb * kb) {
     __syncthreads();  // previous round's readers are done
-    for (int i = 0; i < kb; ++i) {
-      const int band = band0 + i * nb;
-      if (band >= total_bands) break;
-      const int n = band / bands_per_img;
-      const int p0 = (band - n * bands_per_img) * kDwRows;
+    if constexpr (kBatch) {
+      // one staging pass over all kb bands (x window, then dy rows, per band): every load of the
+      // round is in flight before the barrier, not one band's at a time
+      dw_stage(dw_smem, kb * band_f4, [&](int e) {
+        const int i = e / band_f4, o = e - i * band_f4;
+        const int band = band0 + i * nb;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (band >= total_bands) return v;
+        const int n = band / bands_per_img;
+        const int p0 = (band - n * bands_per_img) * kDwRows;
+        const int jj = o & 3;
+        if (o < x_band) {
+          const int pc = o >> 2, cc = pc % x_pitch, rr = pc / x_pitch;
+          const int hr = p0 * kStride - g.ph + rr, wc = cc - g.pw;
+          if (rr < (min(kDwRows, g.P - p0) - 1) * kStride + 3 && (unsigned)hr < (unsigned)g.H &&
+              (unsigned)wc < (unsigned)g.W)
+            v = __ldg(reinterpret_cast<const float4*>(x + (((long long)n * g.H + hr) * g.W + wc) * g.C + c0) + jj);
+        } else {
+          const int pq = (o - x_band) >> 2, q = pq % g.Q, pr = pq / g.Q;
+          if (p0 + pr < g.P)
+            v = __ldg(reinterpret_cast<const float4*>(dy + (((long long)n * g.P + p0 + pr) * g.Q + q) * g.C + c0) + jj);
+        }
+        return v;
+      });
+    } else {  // one band per round (kb == 1): the two plain staging loops keep the registers down
+      const int n = band0 / bands_per_img;
+      const int p0 = (band0 - n * bands_per_img) * kDwRows;
       const int prow = min(kDwRows, g.P - p0);
       const int x_r0 = p0 * kStride - g.ph, x_nr = (prow - 1) * kStride + 3;
-      float4* xs = dw_smem + i * band_f4;
-      dw_stage(xs, x_nr * x_pitch * 4, [&](int e) {
+      dw_stage(dw_smem, x_nr * x_pitch * 4, [&](int e) {
         const int jj = e & 3, pc = e >> 2;
         const int cc = pc % x_pitch, rr = pc / x_pitch;
         const int hr = x_r0 + rr, wc = cc - g.pw;
@@ -413,7 +435,7 @@ __global__ void __launch_bounds__(256) dwconv_wgrad_rows_kernel(const float* __r
           v = __ldg(reinterpret_cast<const float4*>(x + (((long long)n * g.H + hr) * g.W + wc) * g.C + c0) + jj);
         return v;
       });
-      dw_stage(xs + x_band, prow * g.Q * 4, [&](int e) {
+      dw_stage(dw_smem + x_band, prow * g.Q * 4, [&](int e) {
         const int jj = e & 3, pq = e >> 2;
         const int q = pq % g.Q, pr = pq / g.Q;
         return __ldg(reinterpret_cast<const float4*>(dy + (((long long)n * g.P + p0 + pr) * g.Q + q) * g.C + c0) +
