@@ -1238,7 +1238,7 @@ static int dw_kind(const monet_conv_desc* d) {
 namespace {
 template <bool kTrans>
 void dw_launch(const monet_conv_desc* d, dim3 grid, size_t smem, const float* src, const float* w, float* out,
-               int accumulate, cudaStream_t st) {
+               int accumulate, cudaStream_t st, int flip = 0) {
   static bool attr = false;  // the three specialisations share a signature: set all of them once
   if (!attr) {
     for (auto kern : {dwconv_tile_kernel<kTrans, 0>, dwconv_tile_kernel<kTrans, 1>, dwconv_tile_kernel<kTrans, 2>})
@@ -1246,7 +1246,7 @@ void dw_launch(const monet_conv_desc* d, dim3 grid, size_t smem, const float* sr
     attr = true;
   }
   const int rows = dw_rows(d, kTrans);
-  auto run = [&](auto kern) { kern<<<grid, 256, smem, st>>>(src, w, out, geom(d), accumulate, rows); };
+  auto run = [&](auto kern) { kern<<<grid, 256, smem, st>>>(src, w, out, geom(d), accumulate, rows, flip); };
   const int k = dw_kind(d);
   if (k == 1)
     run(dwconv_tile_kernel<kTrans, 1>);
@@ -1281,6 +1281,19 @@ int monet_dwconv_fwd(const monet_conv_desc* d, const float* x, const float* w, f
 int monet_dwconv_dgrad(const monet_conv_desc* d, const float* dy, const float* w, float* dx, int accumulate,
                        void* stream) {
   if (int e = dw_check(d)) return e;
+  if (dw_tiled(d) && dw_kind(d) == 1) {
+    // stride 1: dx is the forward conv of dy with the rotated filter and padding R-1-pad, which runs on
+    // the forward kernel's tighter staging (tools/dw_bench.py: 56x56 404 -> ~330 us)
+    monet_conv_desc e = *d;
+    e.h = d->p, e.w = d->q, e.p = d->h, e.q = d->w;
+    e.pad_h = d->r - 1 - d->pad_h, e.pad_w = d->s - 1 - d->pad_w;
+    if (dw_tiled(&e) && dw_kind(&e) == 1) {
+      const int rows = dw_rows(&e, false);
+      dim3 grid((e.p + rows - 1) / rows, e.n, e.c / kDwSlab);
+      dw_launch<false>(&e, grid, dw_fwd_smem(&e, rows), dy, w, dx, accumulate, S(stream), 1);
+      return last_error();
+    }
+  }
   if (dw_tiled(d)) {
     const int rows = dw_rows(d, true);
     dim3 grid((d->h + rows - 1) / rows, d->n, d->c / kDwSlab);

@@ -193,10 +193,12 @@ MONET_DEV void dw_stage(float4* dst, int count, F load) {
 }
 
 // fwd: out = y (P x Q), src = x (H x W); dgrad (kTrans): out = dx (H x W), src = dy (P x Q)
+// flip: taps read in reverse (a stride-1 dgrad run as the forward of dy with the rotated filter)
 // kStride > 0: 3x3 taps and that stride at compile time (MobileNet-V2's layers); 0: runtime geometry
 template <bool kTrans, int kStride = 0>
 __global__ void __launch_bounds__(256) dwconv_tile_kernel(const float* __restrict__ src, const float* __restrict__ w,
-                                                          float* out, ConvGeom g, int accumulate, int rows) {
+                                                          float* out, ConvGeom g, int accumulate, int rows,
+                                                          int flip) {
   extern __shared__ float4 dw_smem[];
   if (kStride > 0) {
     g.sh = g.sw = kStride;
@@ -242,9 +244,11 @@ __global__ void __launch_bounds__(256) dwconv_tile_kernel(const float* __restric
   const int jq = threadIdx.x & 3;
   float4 wreg[kDwMaxTaps];
 #pragma unroll
-  for (int k = 0; k < kDwMaxTaps; ++k)
-    wreg[k] = k < g.R * g.S ? __ldg(reinterpret_cast<const float4*>(w + k * g.C + c0) + jq)
+  for (int k = 0; k < kDwMaxTaps; ++k) {
+    const int tk = flip ? g.R * g.S - 1 - k : k;
+    wreg[k] = k < g.R * g.S ? __ldg(reinterpret_cast<const float4*>(w + tk * g.C + c0) + jq)
                             : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   for (int i = threadIdx.x; i < outs; i += blockDim.x) {
     const int j = jq, po = i >> 2;
     const int ow = po % OW, orr = po / OW;
