@@ -1270,7 +1270,7 @@ int monet_dwconv_fwd(const monet_conv_desc* d, const float* x, const float* w, f
   if (int e = dw_check(d)) return e;
   if (dw_tiled(d)) {
     const int rows = dw_rows(d, false);
-    dim3 grid((d->p + rows - 1) / rows, d->n, d->c / kDwSlab);
+    dim3 grid(d->c / kDwSlab, (d->p + rows - 1) / rows, d->n);
     dw_launch<false>(d, grid, dw_fwd_smem(d, rows), x, w, y, 0, S(stream));
     return last_error();
   }
@@ -1289,14 +1289,14 @@ int monet_dwconv_dgrad(const monet_conv_desc* d, const float* dy, const float* w
     e.pad_h = d->r - 1 - d->pad_h, e.pad_w = d->s - 1 - d->pad_w;
     if (dw_tiled(&e) && dw_kind(&e) == 1) {
       const int rows = dw_rows(&e, false);
-      dim3 grid((e.p + rows - 1) / rows, e.n, e.c / kDwSlab);
+      dim3 grid(e.c / kDwSlab, (e.p + rows - 1) / rows, e.n);
       dw_launch<false>(&e, grid, dw_fwd_smem(&e, rows), dy, w, dx, accumulate, S(stream), 1);
       return last_error();
     }
   }
   if (dw_tiled(d)) {
     const int rows = dw_rows(d, true);
-    dim3 grid((d->h + rows - 1) / rows, d->n, d->c / kDwSlab);
+    dim3 grid(d->c / kDwSlab, (d->h + rows - 1) / rows, d->n);
     dw_launch<true>(d, grid, dw_dgrad_smem(d, rows), dy, w, dx, accumulate, S(stream));
     return last_error();
   }
@@ -1313,7 +1313,7 @@ int monet_dwconv_wgrad(const monet_conv_desc* d, const float* x, const float* dy
   int nb;
   if (dw_tiled(d)) {
     nb = dw_tile_nb(d);
-    const dim3 grid(nb, d->c / kDwSlab);
+    const dim3 grid(d->c / kDwSlab, nb);
     const int k = dw_kind(d);
     static bool attr = false;  // all three specialisations at once (shared signature)
     if (!attr) {

@@ -206,9 +206,9 @@ __global__ void __launch_bounds__(256) dwconv_tile_kernel(const float* __restric
   }
   const int OH = kTrans ? g.H : g.P, OW = kTrans ? g.W : g.Q;  // output extent
   const int SH = kTrans ? g.P : g.H, SW = kTrans ? g.Q : g.W;  // source extent
-  const int o0 = blockIdx.x * rows;
-  const int n = blockIdx.y;
-  const int c0 = blockIdx.z * kDwSlab;
+  const int c0 = blockIdx.x * kDwSlab;  // slabs fastest: a pixel's slabs share its DRAM lines in L2
+  const int o0 = blockIdx.y * rows;
+  const int n = blockIdx.z;
   const int orows = min(rows, OH - o0);
   // staged source window
   int s_r0, s_nr, s_c0, s_nc;
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(256) dwconv_wgrad_tile_kernel(const float* __r
     g.sh = g.sw = kStride;
     g.R = g.S = 3;
   }
-  const int c0 = blockIdx.y * kDwSlab;
+  const int c0 = blockIdx.x * kDwSlab, wk = blockIdx.y;  // slabs fastest (walker wk of every slab together)
   const int bands_per_img = (g.P + kDwRows - 1) / kDwRows;
   const int total_bands = g.N * bands_per_img;
   const int taps = g.R * g.S;
@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(256) dwconv_wgrad_tile_kernel(const float* __r
   const int r = active ? tap / g.S : 0, s = active ? tap - r * g.S : 0;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   const int x_nc = (g.Q - 1) * g.sw + g.S;
-  for (int band = blockIdx.x; band < total_bands; band += nb) {
+  for (int band = wk; band < total_bands; band += nb) {
     const int n = band / bands_per_img;
     const int p0 = (band - n * bands_per_img) * kDwRows;
     const int prow = min(kDwRows, g.P - p0);
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(256) dwconv_wgrad_tile_kernel(const float* __r
       t.z += v.z;
       t.w += v.w;
     }
-    reinterpret_cast<float4*>(part + ((long long)blockIdx.x * taps + tap) * g.C + c0)[j] = t;
+    reinterpret_cast<float4*>(part + ((long long)wk * taps + tap) * g.C + c0)[j] = t;
   }
 }
 
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(256, kBatch ? 4 : 3) dwconv_wgrad_rows_kernel(
   extern __shared__ float4 dw_smem[];
   constexpr int kSlots = 12, kGroups = 256 / kSlots;  // 21 groups of (3 kernel rows x 4 quads)
   if constexpr (!kBatch) kb = 1;                       // the one-band-per-round variant
-  const int c0 = blockIdx.y * kDwSlab;
+  const int c0 = blockIdx.x * kDwSlab, wk = blockIdx.y;  // slabs fastest (walker wk of every slab together)
   const int bands_per_img = (g.P + kDwRows - 1) / kDwRows;
   const int total_bands = g.N * bands_per_img;
   const int slot = threadIdx.x % kSlots, grp = threadIdx.x / kSlots;
@@ -398,8 +398,8 @@ __global__ void __launch_bounds__(256, kBatch ? 4 : 3) dwconv_wgrad_rows_kernel(
   }
   const int len = (g.Q + nseg - 1) / nseg;
   float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, a2 = a0;
-  // rounds of kb bands (blockIdx.x + (round * kb + i) * nb): all kb stagings in flight per barrier
-  for (int band0 = blockIdx.x; band0 < total_bands; band0 += nb * kb) {
+  // rounds of kb bands (wk + (round * kb + i) * nb): all kb stagings in flight per barrier
+  for (int band0 = wk; band0 < total_bands; band0 += nb * kb) {
     __syncthreads();  // previous round's readers are done
     if constexpr (kBatch) {
       // one staging pass over all kb bands (x window, then dy rows, per band): every load of the
@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(256, kBatch ? 4 : 3) dwconv_wgrad_rows_kernel(
       t.z += v.z;
       t.w += v.w;
     }
-    reinterpret_cast<float4*>(part + ((long long)blockIdx.x * 9 + tap) * g.C + c0)[jj] = t;
+    reinterpret_cast<float4*>(part + ((long long)wk * 9 + tap) * g.C + c0)[jj] = t;
   }
 }
 

@@ -1,6 +1,7 @@
 """Depthwise conv passes of MobileNet-V2 b272 224^2 (every distinct shape, weighted by count):
 time per pass and achieved HBM GB/s over the algorithmic bytes (x + y, dy + dx, x + dy).
-    python tools/dw_bench.py"""
+    python tools/dw_bench.py [H [stride]] [--iters N] [--warmup N]   (H / stride: only those shapes)"""
+import argparse
 import sys
 from collections import Counter
 from pathlib import Path
@@ -11,6 +12,12 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2010_14501_b200 import _native as N  # noqa: E402
 from paper_2010_14501_b200.tracer import build_network  # noqa: E402
 
+ap = argparse.ArgumentParser()
+ap.add_argument("h", type=int, nargs="?")
+ap.add_argument("stride", type=int, nargs="?")
+ap.add_argument("--iters", type=int, default=10)
+ap.add_argument("--warmup", type=int, default=3)
+a = ap.parse_args()
 net = build_network("mobilenet_v2", 272, 224, fuse=True)
 lib = N.lib()
 dev = torch.device("cuda:0")
@@ -18,7 +25,8 @@ shapes = Counter()
 for op in net.ops:
     if op.kind == "dwconv":
         d = net.conv_desc(op)
-        shapes[(d.n, d.h, d.w, d.c, d.r, d.s, d.stride_h, d.pad_h)] += 1
+        if (a.h is None or d.h == a.h) and (a.stride is None or d.stride_h == a.stride):
+            shapes[(d.n, d.h, d.w, d.c, d.r, d.s, d.stride_h, d.pad_h)] += 1
 tot = {"fwd": 0.0, "dgrad": 0.0, "wgrad": 0.0}
 for (n, h, w, c, r, s, st, pd), cnt in sorted(shapes.items()):
     d = N.conv_desc(n, h, w, c, c, r, s, st, pd)
@@ -35,15 +43,15 @@ for (n, h, w, c, r, s, st, pd), cnt in sorted(shapes.items()):
              x.numel() + y.numel()),
             ("wgrad", lambda: lib.dwconv_wgrad(d, x.data_ptr(), y.data_ptr(), dw.data_ptr(), ws.data_ptr(), wsb, None),
              x.numel() + y.numel())):
-        for _ in range(3):
+        for _ in range(a.warmup):
             fn()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(10):
+        for _ in range(a.iters):
             fn()
         e1.record()
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / 10
+        ms = e0.elapsed_time(e1) / a.iters
         tot[pss] += ms * cnt
         line += f" {pss} {ms * 1e3:7.1f} us ({4 * nbytes / ms / 1e6:5.0f} GB/s)"
     print(line, flush=True)
