@@ -156,8 +156,16 @@ __global__ void dwconv_wgrad_partial_kernel(const float* __restrict__ x, const f
 __global__ void dwconv_wgrad_final_kernel(const float* __restrict__ part, int nblocks, int taps, int C, float* dw) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= taps * C) return;
+  const long long stride = (long long)taps * C;
   double s = 0.0;
-  for (int b = 0; b < nblocks; ++b) s += part[(long long)b * taps * C + i];
+  for (int b0 = 0; b0 < nblocks; b0 += 8) {  // 8 loads in flight, added in the same order
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = b0 + u < nblocks ? part[(b0 + u) * stride + i] : 0.f;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (b0 + u < nblocks) s += v[u];
+  }
   dw[i] = (float)s;
 }
 
